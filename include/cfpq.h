@@ -1,0 +1,183 @@
+/*
+ * libcfpq — B200 (sm_100a) context-free path querying by matrix closure.
+ *
+ * Implements the hot path of Azimov & Grigorev, "Context-Free Path Querying by
+ * Matrix Multiplication" (arXiv 1707.01007); P:n cites PAPER.md line n.
+ *
+ *   seed     a_ij = {A_k | (i,x,j) ∈ E ∧ (A_k -> x) ∈ P}            (Alg. 1 lines 6-7)
+ *   closure  while T changes: T <- T ∪ (T × T)                        (Alg. 1 lines 8-9)
+ *            (T × T)_ij = ∪_k T_ik · T_kj,
+ *            N1 · N2 = {A | ∃B∈N1, ∃C∈N2, (A -> B C) ∈ P}
+ *   result   R_A = {(i,j) | A ∈ T^cf_ij}                              (Theorem 2)
+ *   lengths  single-path semantics: seed (A,1); a cell first added in iteration p
+ *            through A->BC gets l_A = l_B + l_C and is never overwritten.
+ *            Within one iteration the minimum candidate wins (reading c7).
+ *
+ * Conventions for every call:
+ *   - Return value: CFPQ_OK (0) or a negative cfpq_status.  On error the thread-local
+ *     message from cfpq_last_error() says why; outputs are left untouched unless the
+ *     call documents otherwise.
+ *   - Handles are opaque, created and destroyed by the library; the caller owns them
+ *     and must destroy them (destroy(NULL) is a no-op).  Handles are not thread-safe:
+ *     use one handle from one thread at a time.
+ *   - Input arrays are copied (host or device memory as flagged); the caller may free
+ *     them as soon as the call returns.  Output buffers are caller-allocated; query
+ *     sizes first (two-call pattern via cfpq_result_count).
+ *   - Node ids are dense 0..n_nodes-1 ("We enumerate the nodes ... from 0 to
+ *     (|V|-1)"); NT ids dense 0..n_nt-1; label ids dense 0..n_labels-1.
+ *   - Limits: n_nodes < 2^27, n_nt <= 1024.
+ *   - All device work runs on the stream given in cfpq_options.cuda_stream (NULL =
+ *     the legacy default stream) of the current CUDA device.  Calls that return host
+ *     data synchronise that stream.
+ */
+#ifndef CFPQ_H
+#define CFPQ_H
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define CFPQ_API __attribute__((visibility("default")))
+#else
+#define CFPQ_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    CFPQ_OK = 0,
+    CFPQ_E_INVAL = -1,          /* bad argument: out-of-range id, NULL pointer, size mismatch */
+    CFPQ_E_NOMEM = -2,          /* device or host allocation failed */
+    CFPQ_E_CUDA = -3,           /* a CUDA runtime error (message has cudaGetErrorString) */
+    CFPQ_E_NCCL = -4,           /* multi-GPU exchange failed */
+    CFPQ_E_NOT_CONVERGED = -5,  /* max_iterations reached before the fixpoint; the
+                                   result holds the (sound, monotone) partial T */
+    CFPQ_E_OVERFLOW = -6,       /* a single-path length exceeded 2^32-1 */
+    CFPQ_E_UNSUPPORTED = -7     /* option combination not implemented */
+} cfpq_status;
+
+typedef struct cfpq_grammar cfpq_grammar;
+typedef struct cfpq_graph cfpq_graph;
+typedef struct cfpq_result cfpq_result;
+
+/* ---------------------------------------------------------------------------------------
+ * Grammar: CNF without a start symbol: rules A -> B C and A -> x only.
+ *   bin  : host int32 [n_bin][3]  = (A, B, C) for A -> B C, ids in [0, n_nt)
+ *   term : host int32 [n_term][2] = (A, x)    for A -> x,   A in [0,n_nt), x in [0,n_labels)
+ * P is a set: duplicate rules collapse.  n_bin or n_term may be 0.
+ * Errors: CFPQ_E_INVAL on any out-of-range id or n_nt outside [1,1024].
+ * ------------------------------------------------------------------------------------- */
+CFPQ_API cfpq_status cfpq_grammar_create(int32_t n_nt, int32_t n_labels,
+                                const int32_t* bin, int64_t n_bin,
+                                const int32_t* term, int64_t n_term,
+                                cfpq_grammar** out);
+CFPQ_API void cfpq_grammar_destroy(cfpq_grammar* g);
+
+/* ---------------------------------------------------------------------------------------
+ * Graph D = (V, E), E ⊆ V × Σ × V.
+ *   edges: int32 [n_edges][3] = (src, label, dst); host memory if edges_on_device == 0,
+ *          else device memory of the current device.  0 <= src,dst < n_nodes.
+ *   Duplicate edges collapse (E is a set); parallel edges with different labels
+ *   accumulate; labels without a terminal rule seed nothing.
+ *   Edge validity (ranges) is checked on the host for host input; for device input
+ *   the seed kernel checks it and cfpq_closure returns CFPQ_E_INVAL.
+ * cfpq_graph_set_edges replaces the edge list of an existing graph (same n_nodes),
+ * reusing its device buffer when it is large enough (the host->device copy of a
+ * per-query upload).
+ * ------------------------------------------------------------------------------------- */
+CFPQ_API cfpq_status cfpq_graph_create(int64_t n_nodes, const int32_t* edges, int64_t n_edges,
+                              int32_t edges_on_device, void* cuda_stream, cfpq_graph** out);
+CFPQ_API cfpq_status cfpq_graph_set_edges(cfpq_graph* g, const int32_t* edges, int64_t n_edges,
+                                 int32_t edges_on_device, void* cuda_stream);
+CFPQ_API void cfpq_graph_destroy(cfpq_graph* g);
+
+/* ---------------------------------------------------------------------------------------
+ * Closure options.  Zero-initialise and set what you need (cfpq_options_default).
+ * ------------------------------------------------------------------------------------- */
+typedef struct {
+    int32_t semantics;       /* 0 relational; 1 single-path lengths. Lengths need
+                                8*n^2 bytes of device memory per non-preterminal NT.     */
+    int32_t schedule;        /* 0 jacobi: per-iteration states equal Alg. 1's T_k;
+                                1 seminaive: same states, same as 0 in this library       */
+    int32_t path_policy;     /* 0 auto, 1 sparse (index-list semi-naive), 2 tensor (tcgen05
+                                int8 dense), 3 rows (bit-row full-operand, paper-faithful) */
+    int32_t account_work;    /* 1: also record per-iteration Jacobi AND-true triple counts
+                                (the work of Alg. 1 line 9 on sparse operands); slower     */
+    int64_t max_iterations;  /* 0 = |V|^2 |N| + 1 (Theorem 3)                   */
+    void*   cuda_stream;     /* cudaStream_t to run on (NULL = default stream)             */
+    int32_t world_size;      /* 1 = single GPU                                             */
+    int32_t rank;
+    const void* nccl_unique_id;  /* reserved for world_size > 1                            */
+    int64_t log_capacity;    /* initial capacity (cells) of the derived-cell log; 0 = auto */
+    int32_t solo_threshold;  /* |Δ| at or below which one CTA runs iterations alone; -1 =
+                                auto, 0 = never                                            */
+    int32_t reserved[7];
+} cfpq_options;
+
+CFPQ_API void cfpq_options_default(cfpq_options* o);
+
+/* ---------------------------------------------------------------------------------------
+ * Run seed + closure to the fixpoint.
+ *   cfpq_closure        allocates a new result (device workspace sized for this grammar
+ *                       and graph) and runs.
+ *   cfpq_closure_reuse  re-runs into an existing result created with the same grammar
+ *                       shape, n_nodes and options (its workspace is cleared first, in
+ *                       O(previous result size)); for repeated queries / benchmarking.
+ * Both block until the closure finished (the stream is synchronised).
+ * Returns CFPQ_E_NOT_CONVERGED when max_iterations is reached first (the result is
+ * then valid and holds the partial T), CFPQ_E_OVERFLOW for a length > 2^32-1.
+ * ------------------------------------------------------------------------------------- */
+CFPQ_API cfpq_status cfpq_closure(const cfpq_grammar* g, const cfpq_graph* d, const cfpq_options* o,
+                         cfpq_result** out);
+CFPQ_API cfpq_status cfpq_closure_reuse(const cfpq_grammar* g, const cfpq_graph* d, const cfpq_options* o,
+                               cfpq_result* r);
+CFPQ_API void cfpq_result_destroy(cfpq_result* r);
+
+/* Loop bodies executed, including the final no-change pass ("k = 6 since T6 = T5"). */
+CFPQ_API cfpq_status cfpq_result_iterations(const cfpq_result* r, int64_t* out);
+
+/* |R_A| (Table 1/2 "#results" for the start NT). */
+CFPQ_API cfpq_status cfpq_result_count(cfpq_result* r, int32_t nt, int64_t* out);
+
+/* |{(i,j) : A ∈ T_k[i][j]}| and the pairs of T_k for iteration k (0 = seed T_0, up to
+ * iterations): the per-iteration states of Alg. 1, for golden tests. */
+CFPQ_API cfpq_status cfpq_result_count_at(cfpq_result* r, int32_t nt, int64_t k, int64_t* out);
+
+/* R_A as (i,j) int32 pairs in ascending (i,j) order into dst_pairs[2*capacity].
+ * *written = |R_A|; CFPQ_E_INVAL if capacity < |R_A|.  dst on host or device. */
+CFPQ_API cfpq_status cfpq_result_pairs(cfpq_result* r, int32_t nt, int32_t* dst_pairs, int64_t capacity,
+                              int32_t dst_is_device, int64_t* written);
+CFPQ_API cfpq_status cfpq_result_pairs_at(cfpq_result* r, int32_t nt, int64_t k, int32_t* dst_pairs,
+                                 int64_t capacity, int32_t dst_is_device, int64_t* written);
+
+/* The bit matrix of A: row i, bit j = word j>>5, bit j&31 (LSB first); dst rows are
+ * row_stride_words uint32 apart (>= ceil(n/32)); n rows.  dst on host or device. */
+CFPQ_API cfpq_status cfpq_result_matrix(cfpq_result* r, int32_t nt, uint32_t* dst, int64_t row_stride_words,
+                               int32_t dst_is_device);
+
+/* Single-path lengths of A in the order of cfpq_result_pairs: dst_len[capacity] uint32
+ * (only for semantics = 1).  *written = |R_A|. */
+CFPQ_API cfpq_status cfpq_result_lengths(cfpq_result* r, int32_t nt, uint32_t* dst_len, int64_t capacity,
+                                int32_t dst_is_device, int64_t* written);
+
+/* Diagnostics (all optional):
+ *   stats[0] iterations, [1] total derived cells incl. seeds, [2] log capacity used,
+ *   [3] overflow regrows, [4] kernel launches of the last closure, [5] iterations run
+ *   in single-CTA mode, [6] candidates expanded (semi-naive AND-true triples).
+ * Per-iteration arrays (length = iterations) via cfpq_result_iteration_stats:
+ *   new_cells[k-1] = |T_k \ T_{k-1}|, jacobi_triples[k-1] (only with account_work). */
+CFPQ_API cfpq_status cfpq_result_stats(const cfpq_result* r, int64_t* stats, int32_t n_stats);
+CFPQ_API cfpq_status cfpq_result_iteration_stats(cfpq_result* r, int64_t* new_cells, int64_t* jacobi_triples,
+                                        int64_t capacity);
+
+/* Thread-local message describing the last non-OK status. */
+CFPQ_API const char* cfpq_last_error(void);
+
+/* Library build/version string ("libcfpq <ver> sm_100a ..."). */
+CFPQ_API const char* cfpq_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CFPQ_H */

@@ -1,0 +1,786 @@
+// C-ABI of libcfpq (include/cfpq.h): handles, workspace planning, the closure driver
+// and result extraction.  All arithmetic of the method runs in the kernels of
+// engine.cu / extract.cu; this file only validates, allocates and launches.
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <set>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "cfpq_internal.cuh"
+
+namespace cfpq {
+static thread_local std::string g_last_error;
+void set_error(const std::string& msg) { g_last_error = msg; }
+}  // namespace cfpq
+
+using namespace cfpq;
+
+#define CFPQ_CHECK_ARG(cond, msg)          \
+    do {                                   \
+        if (!(cond)) {                     \
+            set_error(msg);                \
+            return CFPQ_E_INVAL;           \
+        }                                  \
+    } while (0)
+
+// ------------------------------------------------------------------------------------------
+// device buffer helper
+// ------------------------------------------------------------------------------------------
+template <typename T>
+static cfpq_status dalloc(T** p, size_t count, const char* what) {
+    *p = nullptr;
+    if (count == 0) count = 1;
+    cudaError_t e = cudaMalloc((void**)p, count * sizeof(T));
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        set_error(std::string("cudaMalloc(") + what + ", " + std::to_string(count * sizeof(T)) +
+                  " bytes): " + cudaGetErrorString(e));
+        *p = nullptr;
+        return CFPQ_E_NOMEM;
+    }
+    return CFPQ_OK;
+}
+template <typename T>
+static void dfree(T*& p) {
+    if (p) cudaFree((void*)p);
+    p = nullptr;
+}
+
+struct cfpq_result {
+    // shape
+    int64_t n = 0;
+    int32_t n_nt = 0, n_labels = 0;
+    int64_t Wp = 0;
+    cfpq_options opts{};
+    cudaStream_t stream = nullptr;
+    int32_t grid = 0;
+    std::vector<Rule3> rules;
+    std::vector<std::pair<int32_t, int32_t>> term;
+    // device buffers
+    uint32_t* d_T = nullptr;
+    uint32_t* d_snap = nullptr;       // S and ST slots
+    uint64_t* d_K = nullptr;
+    NTInfo* d_nt = nullptr;
+    Expansion* d_exps = nullptr;
+    int32_t* d_rules = nullptr;
+    int32_t* d_lab_ptr = nullptr;
+    int32_t* d_lab_nt = nullptr;
+    int32_t max_rules_per_label = 0;
+    int32_t* d_slot_row = nullptr;
+    int32_t* d_slot_col = nullptr;
+    int32_t n_adj_slots = 0;
+    int32_t* d_adj_cnt = nullptr;     // counts, then (scanned) pointers
+    int32_t* d_adj_ptr = nullptr;
+    int32_t* d_adj_cursor = nullptr;
+    int32_t* d_adj_idx = nullptr;
+    int64_t adj_idx_cap = 0;
+    uint64_t* d_log = nullptr;
+    unsigned long long log_cap = 0;
+    EngineState* d_st = nullptr;
+    unsigned long long* d_iter_off = nullptr;
+    long long iter_off_cap = 0;
+    unsigned long long* d_jac = nullptr;
+    uint32_t* d_rowc = nullptr;
+    uint32_t* d_colc = nullptr;
+    void* d_temp = nullptr;
+    size_t temp_bytes = 0;
+    // scratch for extraction
+    uint64_t* d_keys = nullptr;
+    unsigned long long keys_cap = 0;
+    unsigned long long* d_small = nullptr;   // [n_nt + 2] counters
+    // host-side copies
+    std::vector<NTInfo> h_nt;
+    int has_snapshots = 0;
+    EngineState h_st{};
+    int64_t iterations = 0;
+    unsigned long long n_cells = 0;
+    int64_t regrows = 0;
+    int64_t launches = 0;
+    std::vector<int64_t> counts;
+    bool counts_valid = false;
+    bool ran = false;
+
+    ~cfpq_result() {
+        dfree(d_T); dfree(d_snap); dfree(d_K); dfree(d_nt); dfree(d_exps); dfree(d_rules);
+        dfree(d_lab_ptr); dfree(d_lab_nt); dfree(d_slot_row); dfree(d_slot_col); dfree(d_adj_cnt);
+        dfree(d_adj_ptr); dfree(d_adj_cursor); dfree(d_adj_idx); dfree(d_log); dfree(d_st);
+        dfree(d_iter_off); dfree(d_jac); dfree(d_rowc); dfree(d_colc); dfree(d_temp); dfree(d_keys);
+        dfree(d_small);
+    }
+
+    EngineParams params() const {
+        EngineParams p{};
+        p.n = (int32_t)n;
+        p.n_nt = n_nt;
+        p.Wp = Wp;
+        p.nt = d_nt;
+        p.exps = d_exps;
+        p.adj_idx = d_adj_idx;
+        p.log = d_log;
+        p.log_cap = log_cap;
+        p.st = d_st;
+        p.iter_off = d_iter_off;
+        p.iter_off_cap = iter_off_cap;
+        p.jac = opts.account_work ? d_jac : nullptr;
+        p.rowc = opts.account_work ? d_rowc : nullptr;
+        p.colc = opts.account_work ? d_colc : nullptr;
+        p.rules = d_rules;
+        p.n_rules = (int32_t)rules.size();
+        p.lengths = opts.semantics == 1;
+        p.max_iter = opts.max_iterations;
+        p.solo_max = opts.solo_threshold;
+        p.has_snapshots = has_snapshots;
+        p.nblocks = grid;
+        return p;
+    }
+};
+
+// ------------------------------------------------------------------------------------------
+// grammar / graph
+// ------------------------------------------------------------------------------------------
+extern "C" cfpq_status cfpq_grammar_create(int32_t n_nt, int32_t n_labels, const int32_t* bin, int64_t n_bin,
+                                           const int32_t* term, int64_t n_term, cfpq_grammar** out) {
+    CFPQ_CHECK_ARG(out != nullptr, "cfpq_grammar_create: out is NULL");
+    CFPQ_CHECK_ARG(n_nt >= 1 && n_nt <= kMaxNT, "cfpq_grammar_create: n_nt must be in [1, 1024]");
+    CFPQ_CHECK_ARG(n_labels >= 0, "cfpq_grammar_create: n_labels < 0");
+    CFPQ_CHECK_ARG(n_bin >= 0 && n_term >= 0, "cfpq_grammar_create: negative rule count");
+    CFPQ_CHECK_ARG(n_bin == 0 || bin != nullptr, "cfpq_grammar_create: bin is NULL");
+    CFPQ_CHECK_ARG(n_term == 0 || term != nullptr, "cfpq_grammar_create: term is NULL");
+    std::set<std::tuple<int, int, int>> rs;
+    for (int64_t k = 0; k < n_bin; ++k) {
+        int A = bin[3 * k], B = bin[3 * k + 1], C = bin[3 * k + 2];
+        CFPQ_CHECK_ARG(A >= 0 && A < n_nt && B >= 0 && B < n_nt && C >= 0 && C < n_nt,
+                       "cfpq_grammar_create: binary rule id out of range");
+        rs.insert(std::make_tuple(A, B, C));
+    }
+    std::set<std::pair<int, int>> ts;
+    for (int64_t k = 0; k < n_term; ++k) {
+        int A = term[2 * k], x = term[2 * k + 1];
+        CFPQ_CHECK_ARG(A >= 0 && A < n_nt && x >= 0 && x < n_labels,
+                       "cfpq_grammar_create: terminal rule id out of range");
+        ts.insert(std::make_pair(A, x));
+    }
+    cfpq_grammar* g = new cfpq_grammar();
+    g->n_nt = n_nt;
+    g->n_labels = n_labels;
+    for (auto& t : rs) g->rules.push_back(Rule3{std::get<0>(t), std::get<1>(t), std::get<2>(t)});
+    for (auto& t : ts) g->term.push_back(t);
+    g->is_const.assign(n_nt, 1);
+    for (auto& r : g->rules) g->is_const[r.A] = 0;
+    *out = g;
+    return CFPQ_OK;
+}
+
+extern "C" void cfpq_grammar_destroy(cfpq_grammar* g) { delete g; }
+
+static cfpq_status upload_edges(cfpq_graph* g, const int32_t* edges, int64_t n_edges, int32_t on_device,
+                                cudaStream_t s) {
+    CFPQ_CHECK_ARG(n_edges >= 0, "edges: n_edges < 0");
+    CFPQ_CHECK_ARG(n_edges == 0 || edges != nullptr, "edges: NULL pointer");
+    if (!on_device) {
+        for (int64_t e = 0; e < n_edges; ++e) {
+            int64_t a = edges[3 * e], b = edges[3 * e + 2];
+            CFPQ_CHECK_ARG(a >= 0 && a < g->n_nodes && b >= 0 && b < g->n_nodes && edges[3 * e + 1] >= 0,
+                           "edges: node or label id out of range (edge " + std::to_string(e) + ")");
+        }
+    }
+    if (n_edges > g->cap_edges) {
+        dfree(g->d_edges);
+        int64_t cap = std::max<int64_t>(n_edges, 1);
+        cfpq_status st = dalloc(&g->d_edges, (size_t)cap * 3, "edges");
+        if (st != CFPQ_OK) return st;
+        g->cap_edges = cap;
+    }
+    if (n_edges > 0)
+        CFPQ_CUDA_TRY(cudaMemcpyAsync(g->d_edges, edges, (size_t)n_edges * 3 * sizeof(int32_t),
+                                      on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
+    g->n_edges = n_edges;
+    return CFPQ_OK;
+}
+
+extern "C" cfpq_status cfpq_graph_create(int64_t n_nodes, const int32_t* edges, int64_t n_edges,
+                                         int32_t edges_on_device, void* cuda_stream, cfpq_graph** out) {
+    CFPQ_CHECK_ARG(out != nullptr, "cfpq_graph_create: out is NULL");
+    CFPQ_CHECK_ARG(n_nodes >= 0 && n_nodes < (int64_t(1) << kNodeBits), "cfpq_graph_create: n_nodes out of range");
+    cfpq_graph* g = new cfpq_graph();
+    g->n_nodes = n_nodes;
+    cfpq_status st = upload_edges(g, edges, n_edges, edges_on_device, (cudaStream_t)cuda_stream);
+    if (st != CFPQ_OK) {
+        dfree(g->d_edges);
+        delete g;
+        return st;
+    }
+    *out = g;
+    return CFPQ_OK;
+}
+
+extern "C" cfpq_status cfpq_graph_set_edges(cfpq_graph* g, const int32_t* edges, int64_t n_edges,
+                                            int32_t edges_on_device, void* cuda_stream) {
+    CFPQ_CHECK_ARG(g != nullptr, "cfpq_graph_set_edges: graph is NULL");
+    return upload_edges(g, edges, n_edges, edges_on_device, (cudaStream_t)cuda_stream);
+}
+
+extern "C" void cfpq_graph_destroy(cfpq_graph* g) {
+    if (!g) return;
+    dfree(g->d_edges);
+    delete g;
+}
+
+extern "C" void cfpq_options_default(cfpq_options* o) {
+    if (!o) return;
+    memset(o, 0, sizeof(*o));
+    o->world_size = 1;
+    o->solo_threshold = -1;
+}
+
+// ------------------------------------------------------------------------------------------
+// planning: per-NT tables, expansions, buffers
+// ------------------------------------------------------------------------------------------
+static cfpq_status plan(cfpq_result* r, const cfpq_grammar* g, const cfpq_graph* d, const cfpq_options* o) {
+    r->n = d->n_nodes;
+    r->n_nt = g->n_nt;
+    r->n_labels = g->n_labels;
+    r->opts = *o;
+    if (r->opts.max_iterations <= 0) {
+        // Theorem 3: |V|^2 |N| changes at most -> |V|^2|N| + 1 loop bodies
+        double cap = (double)r->n * (double)r->n * (double)r->n_nt + 1.0;
+        r->opts.max_iterations = cap > 4e18 ? (long long)4e18 : (long long)cap;
+    }
+    if (r->opts.solo_threshold < 0) r->opts.solo_threshold = 1024;
+    r->stream = (cudaStream_t)o->cuda_stream;
+    r->rules = g->rules;
+    r->term = g->term;
+    const int64_t n = r->n;
+    const int64_t wn = (n + 31) / 32;
+    r->Wp = std::max<int64_t>(32, (wn + 31) / 32 * 32);
+
+    // expansions per NT (see engine.cu header)
+    std::vector<std::vector<Expansion>> ex(g->n_nt);
+    std::vector<int> need_csr(g->n_nt, 0), need_csc(g->n_nt, 0), need_S(g->n_nt, 0), need_ST(g->n_nt, 0);
+    for (auto& rl : g->rules) {
+        bool bc = g->is_const[rl.B], cc = g->is_const[rl.C];
+        if (!bc && !cc) {
+            ex[rl.B].push_back(Expansion{EXP_L_VAR, rl.A, rl.C, 0});
+            ex[rl.C].push_back(Expansion{EXP_R_VAR, rl.A, rl.B, 0});
+            need_S[rl.C] = 1;
+            need_ST[rl.B] = 1;
+        } else if (!bc && cc) {
+            ex[rl.B].push_back(Expansion{EXP_L_CONST, rl.A, rl.C, 0});
+            need_csr[rl.C] = 1;
+        } else if (bc && !cc) {
+            // Δ_B = T_B at iteration 1 only, where T_B × Δ_C already equals T_B × T_C
+            ex[rl.C].push_back(Expansion{EXP_R_CONST, rl.A, rl.B, 0});
+            need_csc[rl.B] = 1;
+        } else {
+            // both preterminal: only iteration 1 (Δ_0 of B) contributes
+            ex[rl.B].push_back(Expansion{EXP_L_CONST, rl.A, rl.C, 0});
+            need_csr[rl.C] = 1;
+        }
+    }
+    std::vector<Expansion> exps;
+    r->h_nt.assign(g->n_nt, NTInfo{});
+    for (int A = 0; A < g->n_nt; ++A) {
+        r->h_nt[A].exp_begin = (int32_t)exps.size();
+        for (auto& e : ex[A]) exps.push_back(e);
+        r->h_nt[A].exp_end = (int32_t)exps.size();
+        r->h_nt[A].is_const = g->is_const[A];
+    }
+    // terminal rules by label (CSR over labels)
+    std::vector<int32_t> lab_ptr(g->n_labels + 1, 0), lab_nt;
+    for (auto& t : g->term) lab_ptr[t.second + 1]++;
+    for (int x = 0; x < g->n_labels; ++x) lab_ptr[x + 1] += lab_ptr[x];
+    lab_nt.resize(g->term.size());
+    {
+        std::vector<int32_t> cur(lab_ptr.begin(), lab_ptr.end() - 1);
+        for (auto& t : g->term) lab_nt[cur[t.second]++] = t.first;
+    }
+    r->max_rules_per_label = 0;
+    for (int x = 0; x < g->n_labels; ++x)
+        r->max_rules_per_label = std::max(r->max_rules_per_label, lab_ptr[x + 1] - lab_ptr[x]);
+
+    cfpq_status st;
+    const size_t mat_words = (size_t)n * (size_t)r->Wp;
+    if ((st = dalloc(&r->d_T, mat_words * g->n_nt, "T bit matrices")) != CFPQ_OK) return st;
+    CFPQ_CUDA_TRY(cudaMemsetAsync(r->d_T, 0, mat_words * g->n_nt * 4, r->stream));
+    int n_snap = 0;
+    for (int A = 0; A < g->n_nt; ++A) n_snap += need_S[A] + need_ST[A];
+    r->has_snapshots = n_snap > 0;
+    if (n_snap) {
+        if ((st = dalloc(&r->d_snap, mat_words * n_snap, "snapshots")) != CFPQ_OK) return st;
+        CFPQ_CUDA_TRY(cudaMemsetAsync(r->d_snap, 0, mat_words * n_snap * 4, r->stream));
+    }
+    bool lengths = o->semantics == 1;
+    int n_key = 0;
+    if (lengths)
+        for (int A = 0; A < g->n_nt; ++A) n_key += g->is_const[A] ? 0 : 1;
+    if (n_key) {
+        if ((st = dalloc(&r->d_K, (size_t)n * n * n_key, "single-path keys")) != CFPQ_OK) return st;
+        CFPQ_CUDA_TRY(cudaMemsetAsync(r->d_K, 0xff, (size_t)n * n * n_key * 8, r->stream));
+    }
+    // adjacency slots
+    std::vector<int32_t> slot_row(g->n_nt, -1), slot_col(g->n_nt, -1);
+    int slots = 0;
+    for (int A = 0; A < g->n_nt; ++A) {
+        if (need_csr[A]) slot_row[A] = slots++;
+        if (need_csc[A]) slot_col[A] = slots++;
+    }
+    r->n_adj_slots = slots;
+    const size_t adj_len = (size_t)slots * (size_t)(n + 1);
+    if ((st = dalloc(&r->d_adj_cnt, adj_len, "adjacency counts")) != CFPQ_OK) return st;
+    if ((st = dalloc(&r->d_adj_ptr, adj_len + 1, "adjacency pointers")) != CFPQ_OK) return st;
+    if ((st = dalloc(&r->d_adj_cursor, adj_len, "adjacency cursor")) != CFPQ_OK) return st;
+    if ((st = dalloc(&r->d_slot_row, g->n_nt, "slots")) != CFPQ_OK) return st;
+    if ((st = dalloc(&r->d_slot_col, g->n_nt, "slots")) != CFPQ_OK) return st;
+    CFPQ_CUDA_TRY(cudaMemcpyAsync(r->d_slot_row, slot_row.data(), g->n_nt * 4, cudaMemcpyHostToDevice, r->stream));
+    CFPQ_CUDA_TRY(cudaMemcpyAsync(r->d_slot_col, slot_col.data(), g->n_nt * 4, cudaMemcpyHostToDevice, r->stream));
+
+    // per-NT pointers
+    int snap_i = 0, key_i = 0;
+    for (int A = 0; A < g->n_nt; ++A) {
+        NTInfo& t = r->h_nt[A];
+        t.T = r->d_T + (size_t)A * mat_words;
+        t.S = need_S[A] ? r->d_snap + (size_t)(snap_i++) * mat_words : nullptr;
+        t.ST = need_ST[A] ? r->d_snap + (size_t)(snap_i++) * mat_words : nullptr;
+        t.K = (lengths && !g->is_const[A]) ? r->d_K + (size_t)(key_i++) * n * n : nullptr;
+        t.csr_ptr = slot_row[A] >= 0 ? r->d_adj_ptr + (size_t)slot_row[A] * (n + 1) : nullptr;
+        t.csc_ptr = slot_col[A] >= 0 ? r->d_adj_ptr + (size_t)slot_col[A] * (n + 1) : nullptr;
+        t.needs_snapshot = (t.S || t.ST) ? 1 : 0;
+    }
+    if ((st = dalloc(&r->d_nt, g->n_nt, "NT table")) != CFPQ_OK) return st;
+    CFPQ_CUDA_TRY(cudaMemcpyAsync(r->d_nt, r->h_nt.data(), g->n_nt * sizeof(NTInfo), cudaMemcpyHostToDevice, r->stream));
+    if ((st = dalloc(&r->d_exps, exps.size(), "expansions")) != CFPQ_OK) return st;
+    if (!exps.empty())
+        CFPQ_CUDA_TRY(cudaMemcpyAsync(r->d_exps, exps.data(), exps.size() * sizeof(Expansion), cudaMemcpyHostToDevice,
+                                      r->stream));
+    if ((st = dalloc(&r->d_rules, g->rules.size() * 3, "rules")) != CFPQ_OK) return st;
+    if (!g->rules.empty())
+        CFPQ_CUDA_TRY(cudaMemcpyAsync(r->d_rules, g->rules.data(), g->rules.size() * sizeof(Rule3),
+                                      cudaMemcpyHostToDevice, r->stream));
+    if ((st = dalloc(&r->d_lab_ptr, lab_ptr.size(), "label table")) != CFPQ_OK) return st;
+    if ((st = dalloc(&r->d_lab_nt, lab_nt.size(), "label table")) != CFPQ_OK) return st;
+    CFPQ_CUDA_TRY(cudaMemcpyAsync(r->d_lab_ptr, lab_ptr.data(), lab_ptr.size() * 4, cudaMemcpyHostToDevice, r->stream));
+    if (!lab_nt.empty())
+        CFPQ_CUDA_TRY(cudaMemcpyAsync(r->d_lab_nt, lab_nt.data(), lab_nt.size() * 4, cudaMemcpyHostToDevice, r->stream));
+
+    if ((st = dalloc(&r->d_st, 1, "state")) != CFPQ_OK) return st;
+    r->iter_off_cap = std::min<long long>(r->opts.max_iterations + 2, 1ll << 22);
+    if ((st = dalloc(&r->d_iter_off, (size_t)r->iter_off_cap, "iteration offsets")) != CFPQ_OK) return st;
+    if (o->account_work) {
+        if ((st = dalloc(&r->d_jac, (size_t)r->iter_off_cap, "work counts")) != CFPQ_OK) return st;
+        if ((st = dalloc(&r->d_rowc, (size_t)g->n_nt * n, "row counts")) != CFPQ_OK) return st;
+        if ((st = dalloc(&r->d_colc, (size_t)g->n_nt * n, "col counts")) != CFPQ_OK) return st;
+        CFPQ_CUDA_TRY(cudaMemsetAsync(r->d_rowc, 0, (size_t)g->n_nt * n * 4, r->stream));
+        CFPQ_CUDA_TRY(cudaMemsetAsync(r->d_colc, 0, (size_t)g->n_nt * n * 4, r->stream));
+    }
+    if ((st = dalloc(&r->d_small, (size_t)g->n_nt + 2, "counters")) != CFPQ_OK) return st;
+    // temp storage for the adjacency scan (and later radix sorts)
+    size_t tb = 0;
+    CFPQ_CUDA_TRY(launch_scan(nullptr, nullptr, (int64_t)adj_len + 1, nullptr, &tb, r->stream));
+    r->temp_bytes = std::max<size_t>(tb, 1 << 16);
+    if ((st = dalloc((uint8_t**)&r->d_temp, r->temp_bytes, "temp")) != CFPQ_OK) return st;
+
+    int dev = 0, sms = 0;
+    CFPQ_CUDA_TRY(cudaGetDevice(&dev));
+    CFPQ_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    int bps = closure_kernel_blocks_per_sm();
+    if (bps <= 0) {
+        set_error("closure kernel cannot be resident (occupancy 0)");
+        return CFPQ_E_CUDA;
+    }
+    r->grid = sms * bps;
+    return CFPQ_OK;
+}
+
+// Make sure the log and adjacency arrays can hold this graph's seeds.
+static cfpq_status size_for_graph(cfpq_result* r, const cfpq_graph* d) {
+    const int64_t seeds_upper = d->n_edges * (int64_t)std::max(r->max_rules_per_label, 0);
+    unsigned long long want = r->opts.log_capacity > 0 ? (unsigned long long)r->opts.log_capacity
+                                                       : std::max<unsigned long long>(1ull << 22, 4ull * seeds_upper);
+    want = std::max<unsigned long long>(want, (unsigned long long)seeds_upper + 64ull);
+    if (want > r->log_cap) {
+        // keep the old content: a reused result clears its previous cells from the log
+        uint64_t* nl = nullptr;
+        cfpq_status st = dalloc(&nl, want, "cell log");
+        if (st != CFPQ_OK) return st;
+        if (r->d_log && r->n_cells)
+            CFPQ_CUDA_TRY(cudaMemcpyAsync(nl, r->d_log, r->n_cells * 8, cudaMemcpyDeviceToDevice, r->stream));
+        dfree(r->d_log);
+        r->d_log = nl;
+        r->log_cap = want;
+    }
+    int64_t adj_want = std::max<int64_t>(2 * seeds_upper, 1);
+    if (adj_want > r->adj_idx_cap) {
+        dfree(r->d_adj_idx);
+        cfpq_status st = dalloc(&r->d_adj_idx, (size_t)adj_want, "adjacency index");
+        if (st != CFPQ_OK) return st;
+        r->adj_idx_cap = adj_want;
+    }
+    return CFPQ_OK;
+}
+
+static cfpq_status grow_log(cfpq_result* r, unsigned long long reached) {
+    unsigned long long want = std::max<unsigned long long>(2 * r->log_cap, reached + reached / 4 + 1024);
+    uint64_t* nl = nullptr;
+    cfpq_status st = dalloc(&nl, want, "cell log (grow)");
+    if (st != CFPQ_OK) return st;
+    CFPQ_CUDA_TRY(cudaMemcpyAsync(nl, r->d_log, r->log_cap * 8, cudaMemcpyDeviceToDevice, r->stream));
+    CFPQ_CUDA_TRY(cudaStreamSynchronize(r->stream));
+    dfree(r->d_log);
+    r->d_log = nl;
+    r->log_cap = want;
+    r->regrows++;
+    return CFPQ_OK;
+}
+
+static cfpq_status run(cfpq_result* r, const cfpq_graph* d) {
+    cudaStream_t s = r->stream;
+    r->launches = 0;
+    r->counts_valid = false;
+    cfpq_status st = size_for_graph(r, d);
+    if (st != CFPQ_OK) return st;
+    EngineParams p = r->params();
+    // clear what a previous run derived (bitmaps, snapshots, keys, counters): O(|log|)
+    if (r->ran && r->n_cells) {
+        CFPQ_CUDA_TRY(launch_clear_log(p, r->n_cells, s));
+        r->launches++;
+    }
+    r->ran = true;
+    r->n_cells = 0;
+    if (r->n_adj_slots)
+        CFPQ_CUDA_TRY(cudaMemsetAsync(r->d_adj_cnt, 0, (size_t)r->n_adj_slots * (r->n + 1) * 4, s));
+    if (r->opts.account_work) CFPQ_CUDA_TRY(cudaMemsetAsync(r->d_jac, 0, r->iter_off_cap * 8, s));
+    CFPQ_CUDA_TRY(cudaMemsetAsync(r->d_st, 0, sizeof(EngineState), s));
+
+    // a1: seed T_0; Δ_0 = the distinct seed cells
+    const unsigned long long seeds_upper = (unsigned long long)d->n_edges * (unsigned long long)r->max_rules_per_label;
+    CFPQ_CUDA_TRY(launch_seed(d->d_edges, d->n_edges, (int32_t)r->n, r->d_lab_ptr, r->d_lab_nt, r->n_labels,
+                              r->max_rules_per_label, p, s));
+    CFPQ_CUDA_TRY(launch_begin(p, s));
+    r->launches += 2;
+    // preterminal adjacency (CSR rows / CSC columns), built once per closure
+    if (r->n_adj_slots) {
+        const size_t adj_len = (size_t)r->n_adj_slots * (r->n + 1);
+        CFPQ_CUDA_TRY(launch_adj_count(p, r->d_slot_row, r->d_slot_col, r->d_adj_cnt, seeds_upper, s));
+        CFPQ_CUDA_TRY(launch_scan(r->d_adj_cnt, r->d_adj_ptr, (int64_t)adj_len, r->d_temp, &r->temp_bytes, s));
+        CFPQ_CUDA_TRY(cudaMemcpyAsync(r->d_adj_cursor, r->d_adj_ptr, adj_len * 4, cudaMemcpyDeviceToDevice, s));
+        CFPQ_CUDA_TRY(launch_adj_fill(p, r->d_slot_row, r->d_slot_col, r->d_adj_cursor, r->d_adj_idx, seeds_upper, s));
+        r->launches += 3;
+    }
+    if (r->has_snapshots) {
+        CFPQ_CUDA_TRY(launch_seed_snapshots(p, seeds_upper, s));
+        r->launches++;
+    }
+    // a2-a5: the fixpoint loop, device-resident
+    for (;;) {
+        p = r->params();
+        CFPQ_CUDA_TRY(launch_closure(p, r->grid, s));
+        r->launches++;
+        CFPQ_CUDA_TRY(cudaMemcpyAsync(&r->h_st, r->d_st, sizeof(EngineState), cudaMemcpyDeviceToHost, s));
+        CFPQ_CUDA_TRY(cudaStreamSynchronize(s));
+        if (r->h_st.bad_edge) {
+            r->n_cells = std::min<unsigned long long>(r->h_st.log_size, r->log_cap);
+            set_error("graph has an edge with a node id >= n_nodes or a label id >= n_labels");
+            return CFPQ_E_INVAL;
+        }
+        if (r->h_st.status == ST_OVERFLOW) {
+            // Δ_k did not fit: grow the log keeping its valid prefix (every slot below
+            // the old capacity was written) and re-run iteration k.
+            unsigned long long old_cap = r->log_cap;
+            st = grow_log(r, r->h_st.log_size);
+            if (st != CFPQ_OK) return st;
+            EngineState fix = r->h_st;
+            fix.log_size = std::min<unsigned long long>(r->h_st.log_size, old_cap);
+            fix.status = ST_RUNNING;
+            fix.overflow = 0;
+            fix.bar_count = 0;
+            fix.bar_gen = 0;
+            if (r->opts.account_work && fix.iter + 1 < r->iter_off_cap)
+                CFPQ_CUDA_TRY(cudaMemsetAsync(r->d_jac + fix.iter + 1, 0, 8, s));
+            CFPQ_CUDA_TRY(cudaMemcpyAsync(r->d_st, &fix, sizeof(EngineState), cudaMemcpyHostToDevice, s));
+            continue;
+        }
+        break;
+    }
+    r->iterations = r->h_st.iter;
+    r->n_cells = std::min<unsigned long long>(r->h_st.log_size, r->log_cap);
+    if (r->h_st.status == ST_CAP) {
+        set_error("max_iterations reached before the fixpoint");
+        return CFPQ_E_NOT_CONVERGED;
+    }
+    if (r->h_st.status == ST_LEN_OVERFLOW) {
+        set_error("a single-path length exceeded 2^32-1");
+        return CFPQ_E_OVERFLOW;
+    }
+    if (r->h_st.status != ST_DONE) {
+        set_error("closure kernel stopped without reaching the fixpoint (status " +
+                  std::to_string(r->h_st.status) + ", barrier watchdog?)");
+        return CFPQ_E_CUDA;
+    }
+    return CFPQ_OK;
+}
+
+// ------------------------------------------------------------------------------------------
+// closure entry points
+// ------------------------------------------------------------------------------------------
+static cfpq_status check_inputs(const cfpq_grammar* g, const cfpq_graph* d, const cfpq_options* o) {
+    CFPQ_CHECK_ARG(g != nullptr && d != nullptr && o != nullptr, "cfpq_closure: NULL grammar/graph/options");
+    CFPQ_CHECK_ARG(o->semantics == 0 || o->semantics == 1, "cfpq_closure: semantics must be 0 or 1");
+    CFPQ_CHECK_ARG(o->schedule == 0 || o->schedule == 1, "cfpq_closure: schedule must be 0 (jacobi) or 1 (seminaive)");
+    CFPQ_CHECK_ARG(o->world_size <= 1, "cfpq_closure: world_size > 1 is not supported by this build");
+    if (o->path_policy == 2 || o->path_policy == 3) {
+        set_error("cfpq_closure: path_policy 2 (tensor) / 3 (rows) not available in this build");
+        return CFPQ_E_UNSUPPORTED;
+    }
+    CFPQ_CHECK_ARG(o->path_policy >= 0 && o->path_policy <= 3, "cfpq_closure: bad path_policy");
+    return CFPQ_OK;
+}
+
+extern "C" cfpq_status cfpq_closure(const cfpq_grammar* g, const cfpq_graph* d, const cfpq_options* o,
+                                    cfpq_result** out) {
+    CFPQ_CHECK_ARG(out != nullptr, "cfpq_closure: out is NULL");
+    cfpq_status st = check_inputs(g, d, o);
+    if (st != CFPQ_OK) return st;
+    cfpq_result* r = new cfpq_result();
+    st = plan(r, g, d, o);
+    if (st == CFPQ_OK) st = run(r, d);
+    if (st != CFPQ_OK && st != CFPQ_E_NOT_CONVERGED && st != CFPQ_E_OVERFLOW) {
+        std::string keep = g_last_error;
+        delete r;
+        set_error(keep);
+        return st;
+    }
+    *out = r;
+    return st;
+}
+
+extern "C" cfpq_status cfpq_closure_reuse(const cfpq_grammar* g, const cfpq_graph* d, const cfpq_options* o,
+                                          cfpq_result* r) {
+    CFPQ_CHECK_ARG(r != nullptr, "cfpq_closure_reuse: result is NULL");
+    cfpq_status st = check_inputs(g, d, o);
+    if (st != CFPQ_OK) return st;
+    CFPQ_CHECK_ARG(d->n_nodes == r->n && g->n_nt == r->n_nt && g->n_labels == r->n_labels &&
+                       g->rules.size() == r->rules.size() && o->semantics == r->opts.semantics &&
+                       o->account_work == r->opts.account_work,
+                   "cfpq_closure_reuse: grammar/graph/options differ from the result's plan");
+    for (size_t k = 0; k < g->rules.size(); ++k)
+        CFPQ_CHECK_ARG(g->rules[k].A == r->rules[k].A && g->rules[k].B == r->rules[k].B && g->rules[k].C == r->rules[k].C,
+                       "cfpq_closure_reuse: grammar differs from the result's plan");
+    CFPQ_CHECK_ARG(g->term == r->term, "cfpq_closure_reuse: terminal rules differ from the result's plan");
+    r->stream = (cudaStream_t)o->cuda_stream;
+    r->opts.cuda_stream = o->cuda_stream;
+    if (o->max_iterations > 0) r->opts.max_iterations = o->max_iterations;
+    if (o->solo_threshold >= 0) r->opts.solo_threshold = o->solo_threshold;
+    return run(r, d);
+}
+
+extern "C" void cfpq_result_destroy(cfpq_result* r) {
+    if (!r) return;
+    cudaStreamSynchronize(r->stream);
+    delete r;
+}
+
+extern "C" cfpq_status cfpq_result_iterations(const cfpq_result* r, int64_t* out) {
+    CFPQ_CHECK_ARG(r && out, "cfpq_result_iterations: NULL argument");
+    *out = r->iterations;
+    return CFPQ_OK;
+}
+
+// cells of T_k live in log[0, end_of(k)); k < 0 -> the final T
+static unsigned long long log_end(cfpq_result* r, int64_t k, cfpq_status* st) {
+    *st = CFPQ_OK;
+    if (k < 0 || k >= r->iterations) return r->n_cells;
+    if (k + 1 >= r->iter_off_cap) {
+        set_error("per-iteration offsets were not recorded for this iteration");
+        *st = CFPQ_E_UNSUPPORTED;
+        return 0;
+    }
+    unsigned long long v = 0;
+    cudaError_t e = cudaMemcpy(&v, r->d_iter_off + k + 1, 8, cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) {
+        set_error(cudaGetErrorString(e));
+        *st = CFPQ_E_CUDA;
+    }
+    return v;
+}
+
+static cfpq_status counts_upto(cfpq_result* r, unsigned long long end, std::vector<int64_t>& out) {
+    cudaStream_t s = r->stream;
+    CFPQ_CUDA_TRY(cudaMemsetAsync(r->d_small, 0, (r->n_nt + 2) * 8, s));
+    CFPQ_CUDA_TRY(launch_nt_histogram(r->d_log, end, r->d_small, s));
+    std::vector<unsigned long long> h(r->n_nt);
+    CFPQ_CUDA_TRY(cudaMemcpyAsync(h.data(), r->d_small, r->n_nt * 8, cudaMemcpyDeviceToHost, s));
+    CFPQ_CUDA_TRY(cudaStreamSynchronize(s));
+    out.assign(h.begin(), h.end());
+    return CFPQ_OK;
+}
+
+extern "C" cfpq_status cfpq_result_count(cfpq_result* r, int32_t nt, int64_t* out) {
+    CFPQ_CHECK_ARG(r && out, "cfpq_result_count: NULL argument");
+    CFPQ_CHECK_ARG(nt >= 0 && nt < r->n_nt, "cfpq_result_count: NT id out of range");
+    if (!r->counts_valid) {
+        cfpq_status st = counts_upto(r, r->n_cells, r->counts);
+        if (st != CFPQ_OK) return st;
+        r->counts_valid = true;
+    }
+    *out = r->counts[nt];
+    return CFPQ_OK;
+}
+
+extern "C" cfpq_status cfpq_result_count_at(cfpq_result* r, int32_t nt, int64_t k, int64_t* out) {
+    CFPQ_CHECK_ARG(r && out, "cfpq_result_count_at: NULL argument");
+    CFPQ_CHECK_ARG(nt >= 0 && nt < r->n_nt, "cfpq_result_count_at: NT id out of range");
+    CFPQ_CHECK_ARG(k >= 0, "cfpq_result_count_at: k < 0");
+    cfpq_status st;
+    unsigned long long end = log_end(r, k, &st);
+    if (st != CFPQ_OK) return st;
+    std::vector<int64_t> c;
+    st = counts_upto(r, end, c);
+    if (st != CFPQ_OK) return st;
+    *out = c[nt];
+    return CFPQ_OK;
+}
+
+// sorted (i<<27|j) keys of NT `nt` among log[0,end) into r->d_keys; returns the count
+static cfpq_status sorted_keys(cfpq_result* r, int32_t nt, unsigned long long end, unsigned long long* count) {
+    cudaStream_t s = r->stream;
+    std::vector<int64_t> c;
+    cfpq_status st = counts_upto(r, end, c);
+    if (st != CFPQ_OK) return st;
+    unsigned long long m = (unsigned long long)c[nt];
+    if (2 * m + 2 > r->keys_cap) {
+        dfree(r->d_keys);
+        st = dalloc(&r->d_keys, 2 * m + 2, "extraction keys");
+        if (st != CFPQ_OK) return st;
+        r->keys_cap = 2 * m + 2;
+    }
+    CFPQ_CUDA_TRY(cudaMemsetAsync(r->d_small + r->n_nt, 0, 8, s));
+    CFPQ_CUDA_TRY(launch_filter_nt(r->d_log, end, (uint32_t)nt, r->d_keys, r->d_small + r->n_nt, s));
+    if (m > 1) {
+        int bits = 1;
+        while ((1ll << bits) < r->n) ++bits;
+        int end_bit = kNodeBits + bits;
+        size_t need = 0;
+        CFPQ_CUDA_TRY(sort_keys(r->d_keys, r->d_keys + m + 1, m, end_bit, nullptr, &need, s));
+        if (need > r->temp_bytes) {
+            dfree(r->d_temp);
+            st = dalloc((uint8_t**)&r->d_temp, need, "sort temp");
+            if (st != CFPQ_OK) return st;
+            r->temp_bytes = need;
+        }
+        CFPQ_CUDA_TRY(sort_keys(r->d_keys, r->d_keys + m + 1, m, end_bit, r->d_temp, &r->temp_bytes, s));
+    }
+    *count = m;
+    return CFPQ_OK;
+}
+
+static cfpq_status pairs_impl(cfpq_result* r, int32_t nt, int64_t k, int32_t* dst, int64_t capacity, int32_t on_dev,
+                              int64_t* written) {
+    CFPQ_CHECK_ARG(r && written, "cfpq_result_pairs: NULL argument");
+    CFPQ_CHECK_ARG(nt >= 0 && nt < r->n_nt, "cfpq_result_pairs: NT id out of range");
+    cfpq_status st;
+    unsigned long long end = log_end(r, k, &st);
+    if (st != CFPQ_OK) return st;
+    unsigned long long m = 0;
+    st = sorted_keys(r, nt, end, &m);
+    if (st != CFPQ_OK) return st;
+    *written = (int64_t)m;
+    CFPQ_CHECK_ARG((int64_t)m <= capacity, "cfpq_result_pairs: capacity < |R_A|");
+    CFPQ_CHECK_ARG(m == 0 || dst != nullptr, "cfpq_result_pairs: dst is NULL");
+    if (m == 0) return CFPQ_OK;
+    cudaStream_t s = r->stream;
+    // unpack into the upper half of the key scratch (2m int32 = m uint64), then copy out
+    int32_t* tmp = on_dev ? dst : (int32_t*)(r->d_keys + m + 1);
+    CFPQ_CUDA_TRY(launch_unpack_pairs(r->d_keys, m, tmp, s));
+    if (!on_dev) {
+        CFPQ_CUDA_TRY(cudaMemcpyAsync(dst, tmp, m * 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    }
+    CFPQ_CUDA_TRY(cudaStreamSynchronize(s));
+    return CFPQ_OK;
+}
+
+extern "C" cfpq_status cfpq_result_pairs(cfpq_result* r, int32_t nt, int32_t* dst_pairs, int64_t capacity,
+                                         int32_t dst_is_device, int64_t* written) {
+    return pairs_impl(r, nt, -1, dst_pairs, capacity, dst_is_device, written);
+}
+
+extern "C" cfpq_status cfpq_result_pairs_at(cfpq_result* r, int32_t nt, int64_t k, int32_t* dst_pairs,
+                                            int64_t capacity, int32_t dst_is_device, int64_t* written) {
+    CFPQ_CHECK_ARG(k >= 0, "cfpq_result_pairs_at: k < 0");
+    return pairs_impl(r, nt, k, dst_pairs, capacity, dst_is_device, written);
+}
+
+extern "C" cfpq_status cfpq_result_matrix(cfpq_result* r, int32_t nt, uint32_t* dst, int64_t row_stride_words,
+                                          int32_t dst_is_device) {
+    CFPQ_CHECK_ARG(r && dst, "cfpq_result_matrix: NULL argument");
+    CFPQ_CHECK_ARG(nt >= 0 && nt < r->n_nt, "cfpq_result_matrix: NT id out of range");
+    const int64_t wn = (r->n + 31) / 32;
+    CFPQ_CHECK_ARG(row_stride_words >= wn, "cfpq_result_matrix: row_stride_words < ceil(n/32)");
+    if (r->n == 0) return CFPQ_OK;
+    const uint32_t* src = r->h_nt[nt].T;
+    CFPQ_CUDA_TRY(cudaMemcpy2DAsync(dst, row_stride_words * 4, src, r->Wp * 4, wn * 4, r->n,
+                                    dst_is_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, r->stream));
+    CFPQ_CUDA_TRY(cudaStreamSynchronize(r->stream));
+    return CFPQ_OK;
+}
+
+extern "C" cfpq_status cfpq_result_lengths(cfpq_result* r, int32_t nt, uint32_t* dst_len, int64_t capacity,
+                                           int32_t dst_is_device, int64_t* written) {
+    CFPQ_CHECK_ARG(r && written, "cfpq_result_lengths: NULL argument");
+    CFPQ_CHECK_ARG(nt >= 0 && nt < r->n_nt, "cfpq_result_lengths: NT id out of range");
+    if (r->opts.semantics != 1) {
+        set_error("cfpq_result_lengths: the closure ran with relational semantics");
+        return CFPQ_E_INVAL;
+    }
+    unsigned long long m = 0;
+    cfpq_status st = sorted_keys(r, nt, r->n_cells, &m);
+    if (st != CFPQ_OK) return st;
+    *written = (int64_t)m;
+    CFPQ_CHECK_ARG((int64_t)m <= capacity, "cfpq_result_lengths: capacity < |R_A|");
+    CFPQ_CHECK_ARG(m == 0 || dst_len != nullptr, "cfpq_result_lengths: dst is NULL");
+    if (m == 0) return CFPQ_OK;
+    cudaStream_t s = r->stream;
+    uint32_t* tmp = dst_is_device ? dst_len : (uint32_t*)(r->d_keys + m + 1);
+    CFPQ_CUDA_TRY(launch_gather_lengths(r->d_keys, m, r->h_nt[nt].K, r->n, tmp, s));
+    if (!dst_is_device) CFPQ_CUDA_TRY(cudaMemcpyAsync(dst_len, tmp, m * 4, cudaMemcpyDeviceToHost, s));
+    CFPQ_CUDA_TRY(cudaStreamSynchronize(s));
+    return CFPQ_OK;
+}
+
+extern "C" cfpq_status cfpq_result_stats(const cfpq_result* r, int64_t* stats, int32_t n_stats) {
+    CFPQ_CHECK_ARG(r && stats, "cfpq_result_stats: NULL argument");
+    int64_t v[7] = {r->iterations, (int64_t)r->n_cells, (int64_t)r->log_cap, r->regrows, r->launches,
+                    r->h_st.solo_iters, (int64_t)r->h_st.candidates};
+    for (int k = 0; k < n_stats && k < 7; ++k) stats[k] = v[k];
+    return CFPQ_OK;
+}
+
+extern "C" cfpq_status cfpq_result_iteration_stats(cfpq_result* r, int64_t* new_cells, int64_t* jacobi_triples,
+                                                   int64_t capacity) {
+    CFPQ_CHECK_ARG(r, "cfpq_result_iteration_stats: NULL result");
+    int64_t k = std::min<int64_t>(r->iterations, capacity);
+    k = std::min<int64_t>(k, r->iter_off_cap - 2);
+    if (k <= 0) return CFPQ_OK;
+    std::vector<unsigned long long> off(k + 2);
+    CFPQ_CUDA_TRY(cudaMemcpy(off.data(), r->d_iter_off, (k + 2) * 8, cudaMemcpyDeviceToHost));
+    if (new_cells)
+        for (int64_t t = 1; t <= k; ++t) new_cells[t - 1] = (int64_t)(off[t + 1] - off[t]);
+    if (jacobi_triples) {
+        if (!r->d_jac) {
+            set_error("cfpq_result_iteration_stats: run with account_work = 1 for work counts");
+            return CFPQ_E_INVAL;
+        }
+        std::vector<unsigned long long> j(k + 1);
+        CFPQ_CUDA_TRY(cudaMemcpy(j.data(), r->d_jac, (k + 1) * 8, cudaMemcpyDeviceToHost));
+        for (int64_t t = 1; t <= k; ++t) jacobi_triples[t - 1] = (int64_t)j[t];
+    }
+    return CFPQ_OK;
+}
+
+extern "C" const char* cfpq_last_error(void) { return g_last_error.c_str(); }
+
+extern "C" const char* cfpq_version(void) {
+    return "libcfpq 0.1 sm_100a (sparse semi-naive persistent engine)";
+}

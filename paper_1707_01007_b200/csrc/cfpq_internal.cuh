@@ -1,0 +1,174 @@
+// Internal declarations of libcfpq (not part of the C-ABI).
+//
+// Layout in HBM:
+//   T      : per NT A, an n x Wp bit matrix, uint32 words, row-major; bit j of row i
+//            is word j>>5, bit j&31.  Wp = words per row, padded to a multiple of 32
+//            (128-byte rows).  T_A = T + A*n*Wp.  The set-valued matrix of P:94/P:157 is
+//            exactly the bundle of these |N| bit matrices (Valiant's |N|^2 BMM view).
+//   log    : append-only list of derived cells, packed uint64 (A:10 | i:27 | j:27).
+//            Δ_0 = seeds, then Δ_1, Δ_2, ... (Δ_k = T_k \ T_{k-1}); iter_off[k] = start
+//            of Δ_k.  Iteration k expands exactly Δ_{k-1} (semi-naive, exact per
+//            iteration: T_k = T_{k-1} ∪ Δ_B×T_C ∪ T_B×Δ_C).
+//   adj    : CSR (rows) / CSC (columns) of preterminal NTs (LHS of no binary rule,
+//            constant after seeding), one concatenated index array.
+//   S, ST  : row / transposed snapshots of NTs that are operands of a rule whose two
+//            operands both change (needed to read T_{k-1} exactly while T_k is written).
+//   K      : single-path keys, uint64 per cell of non-preterminal NTs:
+//            (iteration << 32) | length; EMPTY = ~0.  atomicMin on the key gives
+//            first-write-wins across iterations (smaller stamp) and the minimum length
+//            within the discovery iteration (P:393 + reading c7), order-independently.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string>
+#include <vector>
+
+#include "../../include/cfpq.h"
+
+namespace cfpq {
+
+constexpr int kMaxNT = 1024;
+constexpr int kNodeBits = 27;
+constexpr uint64_t kNodeMask = (1ull << kNodeBits) - 1;
+constexpr uint64_t kEmptyKey = ~0ull;
+
+__host__ __device__ inline uint64_t pack_cell(uint32_t A, uint32_t i, uint32_t j) {
+    return ((uint64_t)A << (2 * kNodeBits)) | ((uint64_t)i << kNodeBits) | (uint64_t)j;
+}
+__host__ __device__ inline uint32_t cell_nt(uint64_t c) { return (uint32_t)(c >> (2 * kNodeBits)); }
+__host__ __device__ inline uint32_t cell_i(uint64_t c) { return (uint32_t)((c >> kNodeBits) & kNodeMask); }
+__host__ __device__ inline uint32_t cell_j(uint64_t c) { return (uint32_t)(c & kNodeMask); }
+
+// Expansion of one Δ entry of NT X through one rule A -> B C in which X occurs.
+enum ExpKind : int32_t {
+    EXP_L_CONST = 0,  // X = B, C preterminal : (i,r) -> (i, j) for j in CSR_C.row(r)
+    EXP_R_CONST = 1,  // X = C, B preterminal : (r,j) -> (i, j) for i in CSC_B.col(r)
+    EXP_L_VAR = 2,    // X = B, C changes     : (i,r) -> (i, j) for j in S_C row r
+    EXP_R_VAR = 3,    // X = C, B changes     : (r,j) -> (i, j) for i in ST_B row r
+};
+
+struct Expansion {
+    int32_t kind;
+    int32_t A;      // LHS
+    int32_t other;  // the other operand NT (C for L kinds, B for R kinds)
+    int32_t pad;
+};
+
+// Per-NT device table (read through the read-only path).
+struct NTInfo {
+    uint32_t* T;          // bit matrix
+    uint32_t* S;          // row snapshot (or null)
+    uint32_t* ST;         // transposed snapshot (or null)
+    uint64_t* K;          // single-path keys (or null: preterminal -> length 1)
+    const int32_t* csr_ptr;  // n+1 (or null)
+    const int32_t* csc_ptr;  // n+1 (or null)
+    int32_t exp_begin, exp_end;   // expansions of Δ entries of this NT
+    int32_t is_const;
+    int32_t needs_snapshot;       // S and/or ST present
+};
+
+// Global state of one closure run (device memory).
+struct EngineState {
+    unsigned long long log_size;   // append counter (may exceed cap on overflow)
+    unsigned long long lo, hi;     // Δ_{k-1} = log[lo, hi)
+    long long iter;                // iterations completed
+    int status;                    // ST_*
+    int overflow;                  // set by a failed append
+    unsigned bar_count;
+    unsigned bar_gen;
+    unsigned long long candidates; // expanded candidates (diagnostic)
+    long long solo_iters;          // iterations run by the single-CTA path
+    int bad_edge;                  // seed saw an out-of-range edge
+    int pad;
+};
+
+enum : int { ST_RUNNING = 0, ST_DONE = 1, ST_OVERFLOW = 2, ST_CAP = 3, ST_LEN_OVERFLOW = 4 };
+
+struct EngineParams {
+    int32_t n;
+    int32_t n_nt;
+    int64_t Wp;                    // words per bit-matrix row
+    const NTInfo* nt;              // [n_nt]
+    const Expansion* exps;
+    const int32_t* adj_idx;        // concatenated CSR/CSC index array
+    uint64_t* log;
+    unsigned long long log_cap;
+    EngineState* st;
+    unsigned long long* iter_off;  // [iter_off_cap]
+    long long iter_off_cap;
+    unsigned long long* jac;       // per-iteration Jacobi triple counts (account mode) or null
+    uint32_t* rowc;                // account mode: per NT row / column nnz of T (n_nt*n each)
+    uint32_t* colc;
+    const int32_t* rules;          // [n_rules][3] (account mode)
+    int32_t n_rules;
+    int32_t lengths;               // single-path semantics
+    long long max_iter;
+    int32_t solo_max;              // |Δ| <= solo_max -> single-CTA iterations
+    int32_t has_snapshots;
+    int32_t nblocks;
+};
+
+// ------------------------------------------------------------------------------------------
+// Host-side objects behind the opaque C handles
+// ------------------------------------------------------------------------------------------
+struct Rule3 { int32_t A, B, C; };
+
+}  // namespace cfpq
+
+struct cfpq_grammar {
+    int32_t n_nt = 0, n_labels = 0;
+    std::vector<cfpq::Rule3> rules;              // distinct binary rules
+    std::vector<std::pair<int32_t, int32_t>> term;  // distinct (A, x)
+    std::vector<int32_t> is_const;               // LHS of no binary rule
+};
+
+struct cfpq_graph {
+    int64_t n_nodes = 0;
+    int64_t n_edges = 0;
+    int64_t cap_edges = 0;
+    int32_t* d_edges = nullptr;    // device [cap][3]
+};
+
+struct cfpq_result;   // defined in api.cu
+
+namespace cfpq {
+
+// error plumbing
+void set_error(const std::string& msg);
+#define CFPQ_CUDA_TRY(expr)                                                               \
+    do {                                                                                  \
+        cudaError_t _e = (expr);                                                          \
+        if (_e != cudaSuccess) {                                                          \
+            ::cfpq::set_error(std::string(#expr) + ": " + cudaGetErrorString(_e));        \
+            return CFPQ_E_CUDA;                                                           \
+        }                                                                                 \
+    } while (0)
+
+// kernels/launchers implemented in the .cu files
+cudaError_t launch_seed(const int32_t* edges, int64_t n_edges, int32_t n_nodes, const int32_t* lab_ptr,
+                        const int32_t* lab_nt, int32_t n_labels, int32_t max_rules_per_label,
+                        const EngineParams& p, cudaStream_t s);
+cudaError_t launch_adj_count(const EngineParams& p, const int32_t* slot_row, const int32_t* slot_col,
+                             int32_t* counts, unsigned long long n_seed_upper, cudaStream_t s);
+cudaError_t launch_adj_fill(const EngineParams& p, const int32_t* slot_row, const int32_t* slot_col,
+                            int32_t* cursor, int32_t* idx, unsigned long long n_seed_upper, cudaStream_t s);
+cudaError_t launch_clear_log(const EngineParams& p, unsigned long long n_cells, cudaStream_t s);
+cudaError_t launch_begin(const EngineParams& p, cudaStream_t s);
+cudaError_t launch_seed_snapshots(const EngineParams& p, unsigned long long n_seed_upper, cudaStream_t s);
+int closure_kernel_blocks_per_sm();
+int closure_kernel_block_size();
+cudaError_t launch_closure(const EngineParams& p, int grid, cudaStream_t s);
+
+cudaError_t launch_nt_histogram(const uint64_t* log, unsigned long long n, unsigned long long* counts,
+                                cudaStream_t s);
+cudaError_t launch_filter_nt(const uint64_t* log, unsigned long long n, uint32_t A, uint64_t* keys,
+                             unsigned long long* count, cudaStream_t s);
+cudaError_t sort_keys(uint64_t* keys, uint64_t* keys_alt, unsigned long long n, int end_bit, void* temp,
+                      size_t* temp_bytes, cudaStream_t s);
+cudaError_t launch_unpack_pairs(const uint64_t* keys, unsigned long long n, int32_t* pairs, cudaStream_t s);
+cudaError_t launch_gather_lengths(const uint64_t* keys, unsigned long long n, const uint64_t* K, int64_t n_nodes,
+                                  uint32_t* out, cudaStream_t s);
+cudaError_t launch_scan(const int32_t* in, int32_t* out, int64_t n, void* temp, size_t* temp_bytes,
+                        cudaStream_t s);
+
+}  // namespace cfpq

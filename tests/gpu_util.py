@@ -1,0 +1,43 @@
+"""Shared helpers for the GPU parity tests: run a workload through the C-ABI binding and
+compare with the oracle element by element."""
+import numpy as np
+
+import oracle as O
+
+
+def cuda_ok() -> bool:
+    try:
+        import torch
+        return torch.cuda.is_available()
+    except Exception:
+        return False
+
+
+def gpu_closure(w, **opts):
+    from paper_1707_01007_b200 import cfpq as C
+    g = C.Grammar.from_workload(w)
+    d = C.Graph(w.n_nodes, w.edges)
+    r = C.closure(g, d, **opts)
+    return r, g, d
+
+
+def gpu_relations(r, n_nt):
+    return {A: set(map(tuple, r.pairs(A).tolist())) for A in range(n_nt)}
+
+
+def assert_parity(w, r, ores=None, lengths=False, check_iterations=True):
+    """Bit-exact comparison of every R_A (and lengths) with the oracle."""
+    ores = ores if ores is not None else O.run(w, lengths=lengths)
+    assert ores.status == 0
+    for A in range(w.n_nt):
+        exp = ores.pairs(A)
+        got = r.pairs(A)
+        assert got.shape == exp.shape, (w.name, w.nt_names[A], got.shape, exp.shape)
+        assert np.array_equal(got, exp), (w.name, w.nt_names[A])
+        if lengths:
+            el = ores.lengths(A)
+            gl = r.lengths(A)
+            assert np.array_equal(gl.astype(np.int64), el[:, 2]), (w.name, w.nt_names[A], "lengths")
+    if check_iterations:
+        assert r.iterations == ores.iterations, (w.name, r.iterations, ores.iterations)
+    return ores
