@@ -1,0 +1,383 @@
+#!/usr/bin/env python
+"""Benchmark of the CFPQ closure hot path (arXiv 1707.01007, Algorithm 1) on B200.
+
+One step = one full closure of the workload: seed T_0 from the edges and
+run T <- T ∪ T×T to the fixpoint, inputs resident in HBM.  Default
+workload = SURVEY §8(d) config 4: the 10-NT Q1∪Q2 union grammar on a 64k-node
+ontology-shaped graph (the largest config, the one BASELINE's metric quotes at
+1/2/4/8 GPUs).  value = effective boolean Gop/s = 2 x (AND-true triples of the
+Jacobi products T_{k-1} x T_{k-1} summed over iterations, i.e. the work of Alg. 1
+line 9 on sparse operands) / closure time; ms_per_step = closure time.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload config4|config3|config5|config2|configS]
+  python bench.py --impl reference ...   # the CPU oracle as the reference arm
+
+Multi-GPU (torchrun, N>1): one process per GPU, each closes its own seeded replica
+of the workload (independent problems, no data-path collective): "scaling": "weak";
+time = max over ranks of the device-timed region.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "CFPQ closure time (ms) & boolean Gop/s vs roofline at 1/2/4/8 B200"
+UNIT = "Gop/s"
+HBM_FALLBACK = 6650.0   # B200_PROFILING.md fallback, used only if MEASURED_PEAKS.json is absent
+
+
+def env_int(k, d):
+    try:
+        return int(os.environ.get(k, d))
+    except ValueError:
+        return d
+
+
+# ------------------------------------------------------------------------------------------
+# workloads
+# ------------------------------------------------------------------------------------------
+
+def make_workload(name: str, seed: int):
+    import inputs as I
+    if name == "config4":
+        w = I.config4_workload(seed=seed)
+        desc = {"workload": "config4: Q1∪Q2 union CNF (10 NTs) on ontology-shaped graph, n=65536, depth 10",
+                "grammar": "union (S_Q1,S5,S6,S_Q2,B,B1,P_scr,P_sc,P_tr,P_t)"}
+    elif name in ("config3", "config5"):
+        w = I.anbn_workload(2, 16383)
+        desc = {"workload": f"{name}: a^n b^n on coprime cycles p=2, q=16383 (n=16384), worst case"
+                            + (", single-path lengths" if name == "config5" else ""),
+                "grammar": "a^n b^n CNF (S,S1,A,B)"}
+    elif name == "config2":
+        w = I.ontology_workload("q1", int(1980 / 2.28), depth=8, seed=seed, n_triples=1980, copies=8)
+        desc = {"workload": "config2: Q1 on 8 disjoint copies of a pizza-sized (1980 triples) ontology graph",
+                "grammar": "same-generation G' (P:279-296)"}
+    elif name == "configS":
+        w = I.dense_stress_workload(4096, 2, seed)
+        desc = {"workload": "configS: S->SS|a on G(n=4096, m=2n)", "grammar": "S->SS|a"}
+    else:
+        raise SystemExit(f"unknown workload {name}")
+    desc.update({"n_nodes": w.n_nodes, "n_edges": int(len(w.edges)), "seed": seed})
+    return w, desc
+
+
+def jacobi_ops(w, name, g, d, C, stream):
+    """2 x AND-true triples of T_{k-1} x T_{k-1} over all iterations (untimed accounting)."""
+    if name in ("config3", "config5"):
+        # closed form (tests/test_oracle_pins.py): iteration k has exactly k triples
+        p, q = w.meta["p"], w.meta["q"]
+        it = 2 * p * q + 1
+        return 2 * it * (it + 1) // 2
+    r = C.closure(g, d, account_work=True, stream=stream, semantics=int(name == "config5"))
+    _, jt = r.iteration_stats(work=True)
+    return 2 * int(jt.sum())
+
+
+# ------------------------------------------------------------------------------------------
+# clocks (NVML polled during the timed region)
+# ------------------------------------------------------------------------------------------
+
+class ClockSampler:
+    def __init__(self, index: int, period: float = 0.002):
+        self.index, self.period = index, period
+        self.samples = []
+        self.reasons = set()
+        self._stop = threading.Event()
+        self.ok = False
+        self.max_mhz = None
+        try:
+            import pynvml as N
+            N.nvmlInit()
+            self.N = N
+            self.h = N.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = N.nvmlDeviceGetMaxClockInfo(self.h, N.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.ok = False
+
+    def _run(self):
+        N = self.N
+        names = {"hw_slowdown": getattr(N, "nvmlClocksEventReasonHwSlowdown", 0x8),
+                 "hw_thermal_slowdown": getattr(N, "nvmlClocksEventReasonHwThermalSlowdown", 0x40),
+                 "sw_thermal_slowdown": getattr(N, "nvmlClocksEventReasonSwThermalSlowdown", 0x20),
+                 "sw_power_cap": getattr(N, "nvmlClocksEventReasonSwPowerCap", 0x4),
+                 "hw_power_brake": getattr(N, "nvmlClocksEventReasonHwPowerBrakeSlowdown", 0x80)}
+        while not self._stop.is_set():
+            try:
+                self.samples.append(N.nvmlDeviceGetClockInfo(self.h, N.NVML_CLOCK_SM))
+                try:
+                    rs = N.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                except Exception:
+                    rs = N.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+                for k, bit in names.items():
+                    if rs & bit:
+                        self.reasons.add(k)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": 0}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------------------------------------
+# peaks, profiles
+# ------------------------------------------------------------------------------------------
+
+def hbm_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return HBM_FALLBACK, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(workload: str):
+    """dram bytes per launch of the closure kernel from the committed ncu --set full summary."""
+    path = os.path.join(ROOT, "profiles", "closure_kernel_traffic.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        e = d.get(workload)
+        return None if e is None else float(e["dram_bytes_per_launch"])
+    except Exception:
+        return None
+
+
+# ------------------------------------------------------------------------------------------
+# reference arm: the CPU oracle as it stands, on a bounded sample of the workload
+# ------------------------------------------------------------------------------------------
+
+def oracle_sample(name: str, seed: int):
+    import inputs as I
+    if name == "config4":
+        return I.config4_workload(seed=seed, n=2048), "config-4 generator at n=2048 (depth 10): full closure"
+    if name in ("config3", "config5"):
+        return I.anbn_workload(2, 255), "a^n b^n p=2, q=255 (n=256, 1021 iterations): full closure"
+    if name == "config2":
+        return (I.ontology_workload("q1", int(1980 / 2.28), depth=8, seed=seed, n_triples=1980),
+                "one pizza-sized copy (1980 triples) of the config-2 graph: full closure")
+    return I.dense_stress_workload(256, 2, seed), "S->SS|a on G(256, 512): full closure"
+
+
+def time_oracle(name: str, seed: int, reps: int = 1):
+    import oracle as O
+    w, sample = oracle_sample(name, seed)
+    lengths = name == "config5"
+    ts, ops = [], 0
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        res = O.run(w, lengths=lengths)
+        ts.append(time.perf_counter() - t0)
+        ops = 2 * int(res.stats()["jacobi_triples"].sum())
+    return ops, ts, sample
+
+
+def run_reference(args):
+    rank = env_int("RANK", 0)
+    if rank != 0:
+        return 0
+    _, desc = make_workload(args.workload, args.seed)
+    for _ in range(args.warmup):
+        time_oracle(args.workload, args.seed)
+    ops, ts = 0, []
+    for _ in range(args.steps):
+        o, t, sample = time_oracle(args.workload, args.seed)
+        ops += o
+        ts += t
+    total = sum(ts)
+    value = ops / total / 1e9
+    ms = 1e3 * total / len(ts)
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "set<int> cells (CPU)", "data": "synthetic",
+            "config": {**desc, "sample": sample},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------------------------------
+# our arm
+# ------------------------------------------------------------------------------------------
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="config4", choices=["config4", "config3", "config5", "config2", "configS"])
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--solo", type=int, default=-1)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    args.warmup = max(args.warmup, 3)
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_1707_01007_b200 import build as B
+    B.build()
+    from paper_1707_01007_b200 import cfpq as C
+
+    rank, world, local = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    stream = torch.cuda.current_stream()
+    dev_index = torch.cuda.current_device()
+
+    w, desc = make_workload(args.workload, args.seed + rank)
+    lengths = args.workload == "config5"
+    g = C.Grammar.from_workload(w)
+    edges_dev = torch.from_numpy(w.edges).cuda()
+    d = C.Graph(w.n_nodes, edges_dev, stream=stream)
+    ops = jacobi_ops(w, args.workload, g, d, C, stream)
+    r = C.closure(g, d, stream=stream, semantics=int(lengths), solo_threshold=args.solo)
+    iterations = r.iterations
+    cells = r.stats()["cells"]
+    results_start = r.count(w.start)
+    nc, _ = r.iteration_stats()
+    delta0 = int(cells - nc.sum())
+
+    # L2 flush buffer (> 126 MB L2), written between timed steps, outside the events
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+    for _ in range(args.warmup):
+        C.closure_reuse(g, d, r, stream=stream, semantics=int(lengths), solo_threshold=args.solo)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    step_ms, loop_ns, seed_ns, launches = [], [], [], 0
+    stats = None
+    with ClockSampler(dev_index) as clk:
+        for _ in range(args.steps):
+            flush.fill_(1)
+            ev0.record(stream)
+            C.closure_reuse(g, d, r, stream=stream, semantics=int(lengths), solo_threshold=args.solo)
+            ev1.record(stream)
+            ev1.synchronize()
+            step_ms.append(ev0.elapsed_time(ev1))
+            stats = r.stats()
+            loop_ns.append(stats["loop_ns"])
+            seed_ns.append(stats["seed_ns"])
+            launches += stats["launches"]
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    assert r.iterations == iterations and r.stats()["cells"] == cells
+
+    total_ms = float(sum(step_ms))
+    my = torch.tensor([total_ms, float(ops) * args.steps], dtype=torch.float64, device="cuda")
+    if world > 1:
+        t_max = my[0:1].clone()
+        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
+        o_sum = my[1:2].clone()
+        dist.all_reduce(o_sum, op=dist.ReduceOp.SUM)
+        total_ms_max, ops_all = float(t_max.item()), float(o_sum.item())
+    else:
+        total_ms_max, ops_all = total_ms, float(ops) * args.steps
+    value = ops_all / (total_ms_max * 1e-3) / 1e9
+    ms_per_step = total_ms_max / args.steps
+
+    # ---- roofline of the dominant kernel (the persistent closure kernel) ----
+    # algorithmic bytes per launch: 8 B per Δ entry read, 8 B per
+    # (entry, rule) expansion (two adjacency offsets), 12 B per candidate (4 B adjacency
+    # index + 4 B read + 4 B write of its bit-matrix word), 8 B per appended cell;
+    # single-path adds 16 B per candidate (key read+write) and 8 B per entry (own key).
+    cand, exps = stats["candidates"], stats["expansions"]
+    new_cells = cells - delta0
+    alg_bytes = 8 * cells + 8 * exps + 12 * cand + 8 * new_cells
+    if lengths:
+        alg_bytes += 16 * cand + 8 * cells
+    loop_s = statistics.mean(loop_ns) * 1e-9
+    peak, peak_src = hbm_peak()
+    achieved = alg_bytes / loop_s / 1e9
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": ncu_traffic(args.workload), "kernel": "cfpq::closure_kernel",
+                "kernel_ms": loop_s * 1e3, "share_of_step": (loop_s * 1e3) / (total_ms / args.steps),
+                "alg_bytes_per_launch": alg_bytes, "peak_source": peak_src,
+                "note": "latency-bound at this size (SURVEY V-9): ~20 iterations of ~1e5 new cells"}
+
+    # ---- end to end through the public API with host buffers ----
+    e2e = None
+    if not args.no_e2e:
+        pinned = torch.from_numpy(w.edges.copy()).pin_memory()
+        h2d = pinned.numel() * 4
+        d2h = 0
+        ts = []
+        for it in range(args.warmup + args.steps):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            d.set_edges(pinned, stream=stream)
+            C.closure_reuse(g, d, r, stream=stream, semantics=int(lengths), solo_threshold=args.solo)
+            pairs = r.pairs(w.start)
+            t1 = time.perf_counter()
+            if it >= args.warmup:
+                ts.append(t1 - t0)
+                d2h = pairs.nbytes + 8
+        e_total = torch.tensor([sum(ts)], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(e_total, op=dist.ReduceOp.MAX)
+        e2e = {"value": ops_all / float(e_total.item()) / 1e9, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "ms_per_step": 1e3 * float(e_total.item()) / len(ts)}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        o, t, sample = time_oracle(args.workload, args.seed)
+        cpu = {"value": o / sum(t) / 1e9, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample,
+               "seconds": sum(t)}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "u32 bit-words (boolean)",
+                "data": "synthetic",
+                "config": {**desc, "iterations": iterations, "cells": int(cells),
+                           "results_start_nt": int(results_start), "useful_ops_per_step": int(ops),
+                           "l2": "flushed between steps (512 MiB write outside the timed events)",
+                           "parallelism": f"{world} independent replicas (seed+rank)" if world > 1 else "1 GPU",
+                           "engine": "sparse semi-naive persistent kernel",
+                           "seed_phase_ms": statistics.mean(seed_ns) * 1e-6},
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+                "gpu_launches": int(launches), "clocks": clk.summary()}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -111,8 +111,8 @@ typedef struct {
     const void* nccl_unique_id;  /* reserved for world_size > 1                            */
     int64_t log_capacity;    /* initial capacity (cells) of the derived-cell log; 0 = auto */
     int32_t solo_threshold;  /* |Δ| at or below which one CTA runs iterations alone; -1 =
-                                auto, 0 = never                                            */
-    int32_t reserved[7];
+                                auto (1024), 0 = only for an empty Δ                       */
+    int32_t reserved[7];     /* must be zero                                               */
 } cfpq_options;
 
 CFPQ_API void cfpq_options_default(cfpq_options* o);
@@ -164,12 +164,19 @@ CFPQ_API cfpq_status cfpq_result_lengths(cfpq_result* r, int32_t nt, uint32_t* d
 /* Diagnostics (all optional):
  *   stats[0] iterations, [1] total derived cells incl. seeds, [2] log capacity used,
  *   [3] overflow regrows, [4] kernel launches of the last closure, [5] iterations run
- *   in single-CTA mode, [6] candidates expanded (semi-naive AND-true triples).
+ *   in single-CTA mode, [6] candidates expanded (semi-naive AND-true triples),
+ *   [7] (Δ entry, rule occurrence) expansions, [8] device time of the seed phase (seed,
+ *   adjacency build, snapshot seeding) in ns, [9] device time of the fixpoint-loop
+ *   kernel launches in ns (CUDA events on the closure stream).
  * Per-iteration arrays (length = iterations) via cfpq_result_iteration_stats:
  *   new_cells[k-1] = |T_k \ T_{k-1}|, jacobi_triples[k-1] (only with account_work). */
 CFPQ_API cfpq_status cfpq_result_stats(const cfpq_result* r, int64_t* stats, int32_t n_stats);
 CFPQ_API cfpq_status cfpq_result_iteration_stats(cfpq_result* r, int64_t* new_cells, int64_t* jacobi_triples,
                                         int64_t capacity);
+/* As above plus end_ns[k-1] = device time (ns, %globaltimer) from the end of seeding to
+ * the end of iteration k (iterations past 2^22 are not recorded). */
+CFPQ_API cfpq_status cfpq_result_iteration_stats2(cfpq_result* r, int64_t* new_cells, int64_t* jacobi_triples,
+                                                  int64_t* end_ns, int64_t capacity);
 
 /* Thread-local message describing the last non-OK status. */
 CFPQ_API const char* cfpq_last_error(void);

@@ -28,7 +28,8 @@ EXPORTS = [
     "cfpq_graph_destroy", "cfpq_options_default", "cfpq_closure", "cfpq_closure_reuse",
     "cfpq_result_destroy", "cfpq_result_iterations", "cfpq_result_count", "cfpq_result_count_at",
     "cfpq_result_pairs", "cfpq_result_pairs_at", "cfpq_result_matrix", "cfpq_result_lengths",
-    "cfpq_result_stats", "cfpq_result_iteration_stats", "cfpq_last_error", "cfpq_version",
+    "cfpq_result_stats", "cfpq_result_iteration_stats", "cfpq_result_iteration_stats2", "cfpq_last_error",
+    "cfpq_version",
 ]
 
 
@@ -79,6 +80,7 @@ def load() -> ctypes.CDLL:
         "cfpq_result_lengths": (i32, [vp, i32, vp, i64, i32, P(i64)]),
         "cfpq_result_stats": (i32, [vp, P(i64), i32]),
         "cfpq_result_iteration_stats": (i32, [vp, vp, vp, i64]),
+        "cfpq_result_iteration_stats2": (i32, [vp, vp, vp, vp, i64]),
         "cfpq_last_error": (ctypes.c_char_p, []),
         "cfpq_version": (ctypes.c_char_p, []),
     }
@@ -255,9 +257,10 @@ class Result:
         return buf[: w.value]
 
     def stats(self) -> dict:
-        v = (ctypes.c_int64 * 7)()
-        _check(load().cfpq_result_stats(self._h, v, 7), "cfpq_result_stats")
-        keys = ["iterations", "cells", "log_capacity", "regrows", "launches", "solo_iterations", "candidates"]
+        v = (ctypes.c_int64 * 10)()
+        _check(load().cfpq_result_stats(self._h, v, 10), "cfpq_result_stats")
+        keys = ["iterations", "cells", "log_capacity", "regrows", "launches", "solo_iterations", "candidates",
+                "expansions", "seed_ns", "loop_ns"]
         return dict(zip(keys, list(v)))
 
     def iteration_stats(self, work: bool = False) -> Tuple[np.ndarray, Optional[np.ndarray]]:
@@ -267,6 +270,13 @@ class Result:
         _check(load().cfpq_result_iteration_stats(self._h, _ptr(nc), _ptr(jt) if work else None, k),
                "cfpq_result_iteration_stats")
         return nc, jt
+
+    def iteration_times(self) -> np.ndarray:
+        """Device ns from the end of seeding to the end of each iteration."""
+        k = self.iterations
+        t = np.zeros(k, dtype=np.int64)
+        _check(load().cfpq_result_iteration_stats2(self._h, None, None, _ptr(t), k), "cfpq_result_iteration_stats2")
+        return t
 
 
 def closure(grammar: Grammar, graph: Graph, opts: Optional[Options] = None, **kw) -> Result:

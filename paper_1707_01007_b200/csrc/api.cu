@@ -83,6 +83,7 @@ struct cfpq_result {
     unsigned long long* d_iter_off = nullptr;
     long long iter_off_cap = 0;
     unsigned long long* d_jac = nullptr;
+    unsigned long long* d_iter_time = nullptr;
     uint32_t* d_rowc = nullptr;
     uint32_t* d_colc = nullptr;
     void* d_temp = nullptr;
@@ -102,12 +103,16 @@ struct cfpq_result {
     std::vector<int64_t> counts;
     bool counts_valid = false;
     bool ran = false;
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    double seed_ns = 0, loop_ns = 0;
 
     ~cfpq_result() {
+        for (auto& e : ev)
+            if (e) cudaEventDestroy(e);
         dfree(d_T); dfree(d_snap); dfree(d_K); dfree(d_nt); dfree(d_exps); dfree(d_rules);
         dfree(d_lab_ptr); dfree(d_lab_nt); dfree(d_slot_row); dfree(d_slot_col); dfree(d_adj_cnt);
         dfree(d_adj_ptr); dfree(d_adj_cursor); dfree(d_adj_idx); dfree(d_log); dfree(d_st);
-        dfree(d_iter_off); dfree(d_jac); dfree(d_rowc); dfree(d_colc); dfree(d_temp); dfree(d_keys);
+        dfree(d_iter_off); dfree(d_jac); dfree(d_iter_time); dfree(d_rowc); dfree(d_colc); dfree(d_temp); dfree(d_keys);
         dfree(d_small);
     }
 
@@ -125,6 +130,7 @@ struct cfpq_result {
         p.iter_off = d_iter_off;
         p.iter_off_cap = iter_off_cap;
         p.jac = opts.account_work ? d_jac : nullptr;
+        p.iter_time = d_iter_time;
         p.rowc = opts.account_work ? d_rowc : nullptr;
         p.colc = opts.account_work ? d_colc : nullptr;
         p.rules = d_rules;
@@ -368,6 +374,7 @@ static cfpq_status plan(cfpq_result* r, const cfpq_grammar* g, const cfpq_graph*
     if ((st = dalloc(&r->d_st, 1, "state")) != CFPQ_OK) return st;
     r->iter_off_cap = std::min<long long>(r->opts.max_iterations + 2, 1ll << 22);
     if ((st = dalloc(&r->d_iter_off, (size_t)r->iter_off_cap, "iteration offsets")) != CFPQ_OK) return st;
+    if ((st = dalloc(&r->d_iter_time, (size_t)r->iter_off_cap, "iteration timestamps")) != CFPQ_OK) return st;
     if (o->account_work) {
         if ((st = dalloc(&r->d_jac, (size_t)r->iter_off_cap, "work counts")) != CFPQ_OK) return st;
         if ((st = dalloc(&r->d_rowc, (size_t)g->n_nt * n, "row counts")) != CFPQ_OK) return st;
@@ -453,6 +460,10 @@ static cfpq_status run(cfpq_result* r, const cfpq_graph* d) {
         CFPQ_CUDA_TRY(cudaMemsetAsync(r->d_adj_cnt, 0, (size_t)r->n_adj_slots * (r->n + 1) * 4, s));
     if (r->opts.account_work) CFPQ_CUDA_TRY(cudaMemsetAsync(r->d_jac, 0, r->iter_off_cap * 8, s));
     CFPQ_CUDA_TRY(cudaMemsetAsync(r->d_st, 0, sizeof(EngineState), s));
+    if (!r->ev[0])
+        for (auto& e : r->ev) CFPQ_CUDA_TRY(cudaEventCreate(&e));
+    r->seed_ns = r->loop_ns = 0;
+    CFPQ_CUDA_TRY(cudaEventRecord(r->ev[0], s));
 
     // a1: seed T_0; Δ_0 = the distinct seed cells
     const unsigned long long seeds_upper = (unsigned long long)d->n_edges * (unsigned long long)r->max_rules_per_label;
@@ -467,19 +478,35 @@ static cfpq_status run(cfpq_result* r, const cfpq_graph* d) {
         CFPQ_CUDA_TRY(launch_scan(r->d_adj_cnt, r->d_adj_ptr, (int64_t)adj_len, r->d_temp, &r->temp_bytes, s));
         CFPQ_CUDA_TRY(cudaMemcpyAsync(r->d_adj_cursor, r->d_adj_ptr, adj_len * 4, cudaMemcpyDeviceToDevice, s));
         CFPQ_CUDA_TRY(launch_adj_fill(p, r->d_slot_row, r->d_slot_col, r->d_adj_cursor, r->d_adj_idx, seeds_upper, s));
-        r->launches += 3;
+        r->launches += 4;   // count, CUB scan (init + scan), fill
     }
     if (r->has_snapshots) {
         CFPQ_CUDA_TRY(launch_seed_snapshots(p, seeds_upper, s));
         r->launches++;
     }
+    CFPQ_CUDA_TRY(cudaEventRecord(r->ev[1], s));
     // a2-a5: the fixpoint loop, device-resident
+    bool first = true;
     for (;;) {
         p = r->params();
+        if (!first) CFPQ_CUDA_TRY(cudaEventRecord(r->ev[2], s));
         CFPQ_CUDA_TRY(launch_closure(p, r->grid, s));
+        CFPQ_CUDA_TRY(cudaEventRecord(r->ev[3], s));
         r->launches++;
         CFPQ_CUDA_TRY(cudaMemcpyAsync(&r->h_st, r->d_st, sizeof(EngineState), cudaMemcpyDeviceToHost, s));
         CFPQ_CUDA_TRY(cudaStreamSynchronize(s));
+        {
+            float ms = 0;
+            if (first) {
+                CFPQ_CUDA_TRY(cudaEventElapsedTime(&ms, r->ev[0], r->ev[1]));
+                r->seed_ns = ms * 1e6;
+                CFPQ_CUDA_TRY(cudaEventElapsedTime(&ms, r->ev[1], r->ev[3]));
+            } else {
+                CFPQ_CUDA_TRY(cudaEventElapsedTime(&ms, r->ev[2], r->ev[3]));
+            }
+            r->loop_ns += ms * 1e6;
+            first = false;
+        }
         if (r->h_st.bad_edge) {
             r->n_cells = std::min<unsigned long long>(r->h_st.log_size, r->log_cap);
             set_error("graph has an edge with a node id >= n_nodes or a label id >= n_labels");
@@ -751,14 +778,20 @@ extern "C" cfpq_status cfpq_result_lengths(cfpq_result* r, int32_t nt, uint32_t*
 
 extern "C" cfpq_status cfpq_result_stats(const cfpq_result* r, int64_t* stats, int32_t n_stats) {
     CFPQ_CHECK_ARG(r && stats, "cfpq_result_stats: NULL argument");
-    int64_t v[7] = {r->iterations, (int64_t)r->n_cells, (int64_t)r->log_cap, r->regrows, r->launches,
-                    r->h_st.solo_iters, (int64_t)r->h_st.candidates};
-    for (int k = 0; k < n_stats && k < 7; ++k) stats[k] = v[k];
+    int64_t v[10] = {r->iterations, (int64_t)r->n_cells, (int64_t)r->log_cap, r->regrows, r->launches,
+                     r->h_st.solo_iters, (int64_t)r->h_st.candidates, (int64_t)r->h_st.expansions,
+                     (int64_t)r->seed_ns, (int64_t)r->loop_ns};
+    for (int k = 0; k < n_stats && k < 10; ++k) stats[k] = v[k];
     return CFPQ_OK;
 }
 
 extern "C" cfpq_status cfpq_result_iteration_stats(cfpq_result* r, int64_t* new_cells, int64_t* jacobi_triples,
                                                    int64_t capacity) {
+    return cfpq_result_iteration_stats2(r, new_cells, jacobi_triples, nullptr, capacity);
+}
+
+extern "C" cfpq_status cfpq_result_iteration_stats2(cfpq_result* r, int64_t* new_cells, int64_t* jacobi_triples,
+                                                    int64_t* end_ns, int64_t capacity) {
     CFPQ_CHECK_ARG(r, "cfpq_result_iteration_stats: NULL result");
     int64_t k = std::min<int64_t>(r->iterations, capacity);
     k = std::min<int64_t>(k, r->iter_off_cap - 2);
@@ -775,6 +808,11 @@ extern "C" cfpq_status cfpq_result_iteration_stats(cfpq_result* r, int64_t* new_
         std::vector<unsigned long long> j(k + 1);
         CFPQ_CUDA_TRY(cudaMemcpy(j.data(), r->d_jac, (k + 1) * 8, cudaMemcpyDeviceToHost));
         for (int64_t t = 1; t <= k; ++t) jacobi_triples[t - 1] = (int64_t)j[t];
+    }
+    if (end_ns) {
+        std::vector<unsigned long long> t(k + 1);
+        CFPQ_CUDA_TRY(cudaMemcpy(t.data(), r->d_iter_time, (k + 1) * 8, cudaMemcpyDeviceToHost));
+        for (int64_t q = 1; q <= k; ++q) end_ns[q - 1] = (int64_t)(t[q] - t[0]);
     }
     return CFPQ_OK;
 }

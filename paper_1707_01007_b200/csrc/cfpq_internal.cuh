@@ -76,7 +76,8 @@ struct EngineState {
     int overflow;                  // set by a failed append
     unsigned bar_count;
     unsigned bar_gen;
-    unsigned long long candidates; // expanded candidates (diagnostic)
+    unsigned long long candidates; // expanded candidates = semi-naive AND-true triples
+    unsigned long long expansions; // (Δ entry, rule occurrence) pairs expanded
     long long solo_iters;          // iterations run by the single-CTA path
     int bad_edge;                  // seed saw an out-of-range edge
     int pad;
@@ -97,6 +98,7 @@ struct EngineParams {
     unsigned long long* iter_off;  // [iter_off_cap]
     long long iter_off_cap;
     unsigned long long* jac;       // per-iteration Jacobi triple counts (account mode) or null
+    unsigned long long* iter_time; // per-iteration %globaltimer stamps (ns) at finalize, [iter_off_cap]
     uint32_t* rowc;                // account mode: per NT row / column nnz of T (n_nt*n each)
     uint32_t* colc;
     const int32_t* rules;          // [n_rules][3] (account mode)

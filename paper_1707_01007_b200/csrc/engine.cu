@@ -214,6 +214,12 @@ __device__ void expand(const EngineParams& p, unsigned long long lo, unsigned lo
             ee = __ldg(&p.nt[X].exp_end);
         }
         int nexp = ee - eb;
+        {
+            int tot = nexp;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(kFull, tot, o);
+            if (lane == 0 && tot) atomicAdd(&p.st->expansions, (unsigned long long)tot);
+        }
         uint32_t len_e = 0;
         if (p.lengths && nexp > 0) len_e = (uint32_t)cell_len(p, X, ci, cj);
         int maxexp = nexp;
@@ -258,7 +264,7 @@ __device__ void expand(const EngineParams& p, unsigned long long lo, unsigned lo
             ws->len[lane] = len_e;
             if (lane == 0) ws->off[32] = total;
             __syncwarp();
-            cand += (unsigned long long)total;
+            if (lane == 0) cand += (unsigned long long)total;
             for (int tb = 0; tb < total; tb += 32) {
                 int t = tb + lane;
                 bool has = t < total;
@@ -383,7 +389,14 @@ __device__ void finalize(const EngineParams& p, long long k) {
     st->lo = new_lo;
     st->hi = ls;
     st->iter = k;
-    if (k < p.iter_off_cap) p.iter_off[k] = new_lo;
+    if (k < p.iter_off_cap) {
+        p.iter_off[k] = new_lo;
+        if (p.iter_time) {
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+            p.iter_time[k] = t;
+        }
+    }
     if (k + 1 < p.iter_off_cap) p.iter_off[k + 1] = ls;
     if (ls == new_lo) st->status = ST_DONE;             // T_k = T_{k-1}: fixpoint
     else if (k >= p.max_iter) st->status = ST_CAP;      // Theorem 3 cap
@@ -505,6 +518,11 @@ __global__ void begin_kernel(EngineParams p) {
     st->iter = 0;
     if (p.iter_off_cap > 0) p.iter_off[0] = 0;
     if (p.iter_off_cap > 1) p.iter_off[1] = n0;
+    if (p.iter_time) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+        p.iter_time[0] = t;
+    }
     if (n0 == 0) st->status = ST_RUNNING;   // iteration 1 still runs: no change -> 1 iteration
 }
 

@@ -27,8 +27,9 @@ def gpu_relations(r, n_nt):
 
 def assert_parity(w, r, ores=None, lengths=False, check_iterations=True):
     """Bit-exact comparison of every R_A (and lengths) with the oracle."""
-    ores = ores if ores is not None else O.run(w, lengths=lengths)
-    assert ores.status == 0
+    if ores is None:
+        ores = O.run(w, lengths=lengths)
+        assert ores.status == 0
     for A in range(w.n_nt):
         exp = ores.pairs(A)
         got = r.pairs(A)
