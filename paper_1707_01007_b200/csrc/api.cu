@@ -76,6 +76,8 @@ struct cfpq_result {
     int32_t* d_adj_ptr = nullptr;
     int32_t* d_adj_cursor = nullptr;
     int32_t* d_adj_idx = nullptr;
+    int4* d_adj_ell = nullptr;
+    int32_t n_exps = 0;
     int64_t adj_idx_cap = 0;
     uint64_t* d_log = nullptr;
     unsigned long long log_cap = 0;
@@ -111,7 +113,7 @@ struct cfpq_result {
             if (e) cudaEventDestroy(e);
         dfree(d_T); dfree(d_snap); dfree(d_K); dfree(d_nt); dfree(d_exps); dfree(d_rules);
         dfree(d_lab_ptr); dfree(d_lab_nt); dfree(d_slot_row); dfree(d_slot_col); dfree(d_adj_cnt);
-        dfree(d_adj_ptr); dfree(d_adj_cursor); dfree(d_adj_idx); dfree(d_log); dfree(d_st);
+        dfree(d_adj_ptr); dfree(d_adj_cursor); dfree(d_adj_idx); dfree(d_adj_ell); dfree(d_log); dfree(d_st);
         dfree(d_iter_off); dfree(d_jac); dfree(d_iter_time); dfree(d_rowc); dfree(d_colc); dfree(d_temp); dfree(d_keys);
         dfree(d_small);
     }
@@ -123,6 +125,7 @@ struct cfpq_result {
         p.Wp = Wp;
         p.nt = d_nt;
         p.exps = d_exps;
+        p.n_exps = n_exps;
         p.adj_idx = d_adj_idx;
         p.log = d_log;
         p.log_cap = log_cap;
@@ -338,6 +341,7 @@ static cfpq_status plan(cfpq_result* r, const cfpq_grammar* g, const cfpq_graph*
     if ((st = dalloc(&r->d_adj_cnt, adj_len, "adjacency counts")) != CFPQ_OK) return st;
     if ((st = dalloc(&r->d_adj_ptr, adj_len + 1, "adjacency pointers")) != CFPQ_OK) return st;
     if ((st = dalloc(&r->d_adj_cursor, adj_len, "adjacency cursor")) != CFPQ_OK) return st;
+    if ((st = dalloc(&r->d_adj_ell, (size_t)slots * n, "adjacency ELL heads")) != CFPQ_OK) return st;
     if ((st = dalloc(&r->d_slot_row, g->n_nt, "slots")) != CFPQ_OK) return st;
     if ((st = dalloc(&r->d_slot_col, g->n_nt, "slots")) != CFPQ_OK) return st;
     CFPQ_CUDA_TRY(cudaMemcpyAsync(r->d_slot_row, slot_row.data(), g->n_nt * 4, cudaMemcpyHostToDevice, r->stream));
@@ -353,10 +357,13 @@ static cfpq_status plan(cfpq_result* r, const cfpq_grammar* g, const cfpq_graph*
         t.K = (lengths && !g->is_const[A]) ? r->d_K + (size_t)(key_i++) * n * n : nullptr;
         t.csr_ptr = slot_row[A] >= 0 ? r->d_adj_ptr + (size_t)slot_row[A] * (n + 1) : nullptr;
         t.csc_ptr = slot_col[A] >= 0 ? r->d_adj_ptr + (size_t)slot_col[A] * (n + 1) : nullptr;
+        t.csr_ell = slot_row[A] >= 0 ? r->d_adj_ell + (size_t)slot_row[A] * n : nullptr;
+        t.csc_ell = slot_col[A] >= 0 ? r->d_adj_ell + (size_t)slot_col[A] * n : nullptr;
         t.needs_snapshot = (t.S || t.ST) ? 1 : 0;
     }
     if ((st = dalloc(&r->d_nt, g->n_nt, "NT table")) != CFPQ_OK) return st;
     CFPQ_CUDA_TRY(cudaMemcpyAsync(r->d_nt, r->h_nt.data(), g->n_nt * sizeof(NTInfo), cudaMemcpyHostToDevice, r->stream));
+    r->n_exps = (int32_t)exps.size();
     if ((st = dalloc(&r->d_exps, exps.size(), "expansions")) != CFPQ_OK) return st;
     if (!exps.empty())
         CFPQ_CUDA_TRY(cudaMemcpyAsync(r->d_exps, exps.data(), exps.size() * sizeof(Expansion), cudaMemcpyHostToDevice,
@@ -478,7 +485,8 @@ static cfpq_status run(cfpq_result* r, const cfpq_graph* d) {
         CFPQ_CUDA_TRY(launch_scan(r->d_adj_cnt, r->d_adj_ptr, (int64_t)adj_len, r->d_temp, &r->temp_bytes, s));
         CFPQ_CUDA_TRY(cudaMemcpyAsync(r->d_adj_cursor, r->d_adj_ptr, adj_len * 4, cudaMemcpyDeviceToDevice, s));
         CFPQ_CUDA_TRY(launch_adj_fill(p, r->d_slot_row, r->d_slot_col, r->d_adj_cursor, r->d_adj_idx, seeds_upper, s));
-        r->launches += 4;   // count, CUB scan (init + scan), fill
+        CFPQ_CUDA_TRY(launch_adj_ell(r->d_adj_ptr, r->d_adj_idx, r->d_adj_ell, r->n_adj_slots, (int32_t)r->n, s));
+        r->launches += 5;   // count, CUB scan (init + scan), fill, ELL heads
     }
     if (r->has_snapshots) {
         CFPQ_CUDA_TRY(launch_seed_snapshots(p, seeds_upper, s));

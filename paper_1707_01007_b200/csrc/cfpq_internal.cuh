@@ -62,6 +62,8 @@ struct NTInfo {
     uint64_t* K;          // single-path keys (or null: preterminal -> length 1)
     const int32_t* csr_ptr;  // n+1 (or null)
     const int32_t* csc_ptr;  // n+1 (or null)
+    const int4* csr_ell;     // n ELL heads {beg, deg, nb0, nb1} of the CSR rows (or null)
+    const int4* csc_ell;     // n ELL heads of the CSC columns (or null)
     int32_t exp_begin, exp_end;   // expansions of Δ entries of this NT
     int32_t is_const;
     int32_t needs_snapshot;       // S and/or ST present
@@ -91,6 +93,7 @@ struct EngineParams {
     int64_t Wp;                    // words per bit-matrix row
     const NTInfo* nt;              // [n_nt]
     const Expansion* exps;
+    int32_t n_exps;
     const int32_t* adj_idx;        // concatenated CSR/CSC index array
     uint64_t* log;
     unsigned long long log_cap;
@@ -156,6 +159,8 @@ cudaError_t launch_adj_fill(const EngineParams& p, const int32_t* slot_row, cons
                             int32_t* cursor, int32_t* idx, unsigned long long n_seed_upper, cudaStream_t s);
 cudaError_t launch_clear_log(const EngineParams& p, unsigned long long n_cells, cudaStream_t s);
 cudaError_t launch_begin(const EngineParams& p, cudaStream_t s);
+cudaError_t launch_adj_ell(const int32_t* ptr, const int32_t* idx, int4* ell, int64_t n_slots, int32_t n,
+                           cudaStream_t s);
 cudaError_t launch_seed_snapshots(const EngineParams& p, unsigned long long n_seed_upper, cudaStream_t s);
 int closure_kernel_blocks_per_sm();
 int closure_kernel_block_size();

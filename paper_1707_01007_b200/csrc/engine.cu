@@ -9,14 +9,20 @@
 //   Δ_B entry (i,r)  -> (i,j) for every j with C ∈ T_{k-1}[r][j]
 //   Δ_C entry (r,j)  -> (i,j) for every i with B ∈ T_{k-1}[i][r]
 // Preterminals (LHS of no binary rule) never change after seeding, so their rows
-// and columns come from CSR/CSC built once; only rules whose two operands both
-// change need row/column snapshots of T_{k-1}.
+// and columns come from adjacency lists built once (ELL head {beg, deg, nb0, nb1}
+// + CSR tail); only rules whose two operands both change need row/column
+// snapshots of T_{k-1}.
 //
 // One persistent cooperative kernel runs the whole fixpoint loop (no host round
 // trip per iteration): one grid barrier per iteration, the last CTA to arrive
 // closes the iteration (changed <=> Δ_k non-empty).  When |Δ| is small the
 // iteration is run by CTA 0 alone with __syncthreads() only (the a^n b^n worst
 // case adds one cell per iteration for 2pq+1 iterations, SURVEY V-2).
+//
+// Latency structure of one 32-entry chunk (one warp): load the entries, load the
+// ELL heads of all their rule occurrences, issue all bit/key atomics, then stage
+// the new cells in a per-warp shared-memory buffer that is appended to the global
+// log with one atomic per <= kBuf cells.
 #include <cooperative_groups.h>
 #include <cub/cub.cuh>
 
@@ -26,6 +32,11 @@ namespace cfpq {
 
 constexpr int kBlock = 512;
 constexpr int kWarps = kBlock / 32;
+constexpr int kSeedBlock = 256;
+constexpr int kBuf = 128;            // per-warp staging capacity (cells)
+constexpr int kSmemNT = 64;          // NT / expansion tables cached in shared memory
+constexpr int kSmemExp = 256;
+constexpr int kPre = 2;              // rule occurrences prefetched per entry
 constexpr unsigned kFull = 0xffffffffu;
 
 // ------------------------------------------------------------------------------------------
@@ -44,83 +55,124 @@ __device__ __forceinline__ uint32_t ldcg32(const uint32_t* p) {
 __device__ __forceinline__ unsigned long long ld_volatile_u64(const unsigned long long* p) {
     return *(volatile const unsigned long long*)p;
 }
+__device__ __forceinline__ unsigned long long globaltimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ unsigned lanemask_lt(int lane) { return (1u << lane) - 1u; }
 
-struct WarpScratch {
+struct __align__(16) WarpScratch {
+    uint64_t buf[kBuf];   // staged new cells
     int32_t off[33];
     int32_t beg[32];
     uint32_t A[32];
     uint32_t fixed[32];   // bit 31 set: the fixed coordinate is j (R kinds), else i (L kinds)
     uint32_t len[32];
+    int32_t nbuf;
 };
 
 // Length of an existing cell (X,i,j): preterminal cells have length 1 (P:393 seed),
 // others read their key (final for every cell of T_{k-1}).
-__device__ __forceinline__ uint64_t cell_len(const EngineParams& p, uint32_t X, uint32_t i, uint32_t j) {
-    const uint64_t* K = p.nt[X].K;
+__device__ __forceinline__ uint64_t cell_len(const EngineParams& p, const NTInfo* nt, uint32_t X, uint32_t i,
+                                             uint32_t j) {
+    const uint64_t* K = nt[X].K;
     if (K == nullptr) return 1;
     return ldcg64(K + (size_t)i * (size_t)p.n + j) & 0xffffffffull;
 }
 
-// Warp-uniform: every lane calls with its optional candidate (A,i,j,len).
-// A candidate is new iff it flips its bit (relational) or turns its key from EMPTY
-// (lengths); new cells are appended to the log (Δ_k) with one atomic per warp.
-__device__ __forceinline__ void emit(const EngineParams& p, bool has, uint32_t A, uint32_t i, uint32_t j,
-                                     uint64_t len, long long k, int lane) {
-    bool disc = false;
-    uint32_t* word = nullptr;
-    uint32_t bit = 0;
-    uint64_t* key = nullptr;
-    if (has) {
-        word = p.nt[A].T + (size_t)i * (size_t)p.Wp + (j >> 5);
-        bit = 1u << (j & 31);
-        if (p.lengths && p.nt[A].K != nullptr) {
-            if (len > 0xffffffffull) {
-                p.st->status = ST_LEN_OVERFLOW;   // reported at the next barrier
-                len = 0xffffffffull;
-            }
-            key = p.nt[A].K + (size_t)i * (size_t)p.n + j;
-            uint64_t kv = ((uint64_t)k << 32) | len;
-            uint64_t old = atomicMin((unsigned long long*)key, (unsigned long long)kv);
-            disc = (old == kEmptyKey);
-        } else {
-            uint32_t old = atomicOr(word, bit);
-            disc = !(old & bit);
+// Insert candidate (A,i,j) of length len into T_k; true iff the cell is new:
+// relational -> the bit flips; single-path -> the key leaves EMPTY (atomicMin on
+// (iteration<<32 | length): first write wins across iterations, min within one).
+__device__ __forceinline__ bool try_insert(const EngineParams& p, const NTInfo* nt, bool has, uint32_t A, uint32_t i,
+                                           uint32_t j, uint64_t len, long long k) {
+    if (!has) return false;
+    uint64_t* K = nt[A].K;
+    if (p.lengths && K != nullptr) {
+        if (len > 0xffffffffull) {
+            *(volatile int*)&p.st->status = ST_LEN_OVERFLOW;   // reported at the next barrier
+            len = 0xffffffffull;
         }
+        uint64_t kv = ((uint64_t)k << 32) | len;
+        uint64_t old = atomicMin((unsigned long long*)(K + (size_t)i * (size_t)p.n + j), (unsigned long long)kv);
+        return old == kEmptyKey;
     }
-    unsigned mask = __ballot_sync(kFull, disc);
-    if (mask == 0) return;
-    int leader = __ffs(mask) - 1;
+    uint32_t bit = 1u << (j & 31);
+    uint32_t old = atomicOr(nt[A].T + (size_t)i * (size_t)p.Wp + (j >> 5), bit);
+    return !(old & bit);
+}
+
+// Append the warp's staged cells to the log (one atomic per flush).  A cell that
+// does not fit is rolled back so that a re-run of the iteration (after the host
+// grows the log) rediscovers it; appended cells stay set and are not re-appended.
+__device__ __forceinline__ void flush(const EngineParams& p, const NTInfo* nt, WarpScratch* ws, int lane) {
+    int nb = ws->nbuf;
+    if (nb == 0) return;
     unsigned long long base = 0;
-    if (lane == leader) base = atomicAdd(&p.st->log_size, (unsigned long long)__popc(mask));
-    base = __shfl_sync(kFull, base, leader);
-    if (disc) {
-        unsigned long long idx = base + __popc(mask & ((1u << lane) - 1u));
+    if (lane == 0) base = atomicAdd(&p.st->log_size, (unsigned long long)nb);
+    base = __shfl_sync(kFull, base, 0);
+    for (int t = lane; t < nb; t += 32) {
+        uint64_t c = ws->buf[t];
+        unsigned long long idx = base + (unsigned long long)t;
+        uint32_t A = cell_nt(c), i = cell_i(c), j = cell_j(c);
+        uint64_t* K = p.lengths ? nt[A].K : nullptr;
+        uint32_t* word = nt[A].T + (size_t)i * (size_t)p.Wp + (j >> 5);
+        uint32_t bit = 1u << (j & 31);
         if (idx < p.log_cap) {
-            p.log[idx] = pack_cell(A, i, j);
-            if (key != nullptr) atomicOr(word, bit);
+            p.log[idx] = c;
+            if (K != nullptr) atomicOr(word, bit);   // the bit matrix mirrors the keys
             if (p.rowc != nullptr) {
                 atomicAdd(p.rowc + (size_t)A * p.n + i, 1u);
                 atomicAdd(p.colc + (size_t)A * p.n + j, 1u);
             }
         } else {
-            // roll back: a re-run of this iteration (after the host grows the log)
-            // rediscovers the cell; appended cells stay set and are not re-appended.
-            if (key != nullptr) atomicExch((unsigned long long*)key, (unsigned long long)kEmptyKey);
+            if (K != nullptr) atomicExch((unsigned long long*)(K + (size_t)i * (size_t)p.n + j),
+                                         (unsigned long long)kEmptyKey);
             else atomicAnd(word, ~bit);
             *(volatile int*)&p.st->overflow = 1;
         }
     }
+    __syncwarp();
+    if (lane == 0) ws->nbuf = 0;
+    __syncwarp();
+}
+
+// Warp-uniform: stage the lanes' new cells (disc) in the warp buffer.
+__device__ __forceinline__ void stage(const EngineParams& p, const NTInfo* nt, WarpScratch* ws, int lane, bool disc,
+                                      uint32_t A, uint32_t i, uint32_t j) {
+    unsigned mask = __ballot_sync(kFull, disc);
+    if (mask == 0) return;
+    int cnt = __popc(mask);
+    int nb = ws->nbuf;
+    if (nb + cnt > kBuf) {
+        flush(p, nt, ws, lane);
+        nb = 0;
+    }
+    if (disc) ws->buf[nb + __popc(mask & lanemask_lt(lane))] = pack_cell(A, i, j);
+    __syncwarp();
+    if (lane == 0) ws->nbuf = nb + cnt;
+    __syncwarp();
+}
+
+__device__ __forceinline__ void emit(const EngineParams& p, const NTInfo* nt, WarpScratch* ws, int lane, bool has,
+                                     uint32_t A, uint32_t i, uint32_t j, uint64_t len, long long k) {
+    bool d = try_insert(p, nt, has, A, i, j, len, k);
+    stage(p, nt, ws, lane, d, A, i, j);
 }
 
 // ------------------------------------------------------------------------------------------
 // Seeding (Alg. 1 lines 6-7): T_ij ∪= {A | A -> x} for every (i,x,j) ∈ E.
 // Parallel edges accumulate; duplicate edges dedupe through the bit test.
 // ------------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) seed_kernel(EngineParams p, const int32_t* __restrict__ edges,
-                                                   int64_t n_edges, const int32_t* __restrict__ lab_ptr,
-                                                   const int32_t* __restrict__ lab_nt, int32_t n_labels,
-                                                   int32_t max_rules) {
+__global__ void __launch_bounds__(kSeedBlock) seed_kernel(EngineParams p, const int32_t* __restrict__ edges,
+                                                          int64_t n_edges, const int32_t* __restrict__ lab_ptr,
+                                                          const int32_t* __restrict__ lab_nt, int32_t n_labels,
+                                                          int32_t max_rules) {
+    __shared__ WarpScratch wsa[kSeedBlock / 32];
     const int lane = threadIdx.x & 31;
+    WarpScratch* ws = &wsa[threadIdx.x >> 5];
+    if (lane == 0) ws->nbuf = 0;
+    __syncwarp();
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n_edges; base += stride) {
         int64_t e = base + threadIdx.x;
@@ -141,9 +193,10 @@ __global__ void __launch_bounds__(256) seed_kernel(EngineParams p, const int32_t
         for (int t = 0; t < max_rules; ++t) {
             bool has = valid && (rb + t < re);
             uint32_t A = has ? (uint32_t)__ldg(lab_nt + rb + t) : 0u;
-            emit(p, has, A, (uint32_t)s, (uint32_t)d, 1, 0, lane);
+            emit(p, p.nt, ws, lane, has, A, (uint32_t)s, (uint32_t)d, 1, 0);
         }
     }
+    flush(p, p.nt, ws, lane);
 }
 
 // CSR / CSC of preterminals from the seed cells Δ_0 = log[0, n_seed).
@@ -175,6 +228,23 @@ __global__ void adj_fill_kernel(EngineParams p, const int32_t* __restrict__ slot
     }
 }
 
+// ELL heads: ell[s][r] = {beg, deg, first neighbour, second neighbour} of slot s, row r.
+__global__ void adj_ell_kernel(const int32_t* __restrict__ ptr, const int32_t* __restrict__ idx, int4* ell,
+                               int64_t n_rows_total, int32_t n) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n_rows_total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        int64_t s = t / n, r = t - s * n;
+        const int32_t* pp = ptr + s * (int64_t)(n + 1);
+        int32_t b = pp[r], e = pp[r + 1];
+        int4 v;
+        v.x = b;
+        v.y = e - b;
+        v.z = e - b > 0 ? idx[b] : -1;
+        v.w = e - b > 1 ? idx[b + 1] : -1;
+        ell[t] = v;
+    }
+}
+
 // Clear the cells of a previous run (bitmaps, snapshots, keys, counters) in O(|log|).
 __global__ void clear_log_kernel(EngineParams p, unsigned long long n_cells) {
     for (unsigned long long e = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; e < n_cells;
@@ -197,120 +267,169 @@ __global__ void clear_log_kernel(EngineParams p, unsigned long long n_cells) {
 // Closure kernel pieces
 // ------------------------------------------------------------------------------------------
 
+__device__ __forceinline__ void cand_coords(uint32_t fx, int32_t nb, uint32_t& i, uint32_t& j) {
+    if (fx & 0x80000000u) {
+        i = (uint32_t)nb;
+        j = fx & 0x7fffffffu;
+    } else {
+        i = fx;
+        j = (uint32_t)nb;
+    }
+}
+
+// Neighbours beyond the ELL head (deg > 2): warp-wide exclusive scan of the tail
+// lengths, load-balanced over the 32 lanes (hub rows are spread over the warp).
+__device__ void expand_tail(const EngineParams& p, const NTInfo* nt, WarpScratch* ws, int lane, int4 el, uint32_t A,
+                            uint32_t fx, uint32_t len_e, long long k) {
+    int32_t beg = el.x + 2;
+    int32_t deg = el.y > 2 ? el.y - 2 : 0;
+    int incl = deg;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        int v = __shfl_up_sync(kFull, incl, o);
+        if (lane >= o) incl += v;
+    }
+    int total = __shfl_sync(kFull, incl, 31);
+    if (total == 0) return;
+    ws->off[lane] = incl - deg;
+    ws->beg[lane] = beg;
+    ws->A[lane] = A;
+    ws->fixed[lane] = fx;
+    ws->len[lane] = len_e;
+    if (lane == 0) ws->off[32] = total;
+    __syncwarp();
+    for (int tb = 0; tb < total; tb += 32) {
+        int t = tb + lane;
+        bool has = t < total;
+        uint32_t cA = 0, oi = 0, oj = 0;
+        uint64_t clen = 0;
+        if (has) {
+            int l = 0;
+#pragma unroll
+            for (int step = 16; step > 0; step >>= 1)
+                if (ws->off[l + step] <= t) l += step;
+            int32_t nbv = __ldg(p.adj_idx + ws->beg[l] + (t - ws->off[l]));
+            cA = ws->A[l];
+            cand_coords(ws->fixed[l], nbv, oi, oj);
+            clen = (uint64_t)ws->len[l] + 1ull;   // the preterminal operand has length 1
+        }
+        emit(p, nt, ws, lane, has, cA, oi, oj, clen, k);
+    }
+    __syncwarp();
+}
+
+// ELL head of expansion ex for entry (ci, cj).
+__device__ __forceinline__ int4 load_head(const NTInfo* nt, const Expansion& ex, uint32_t ci, uint32_t cj,
+                                          uint32_t& A, uint32_t& fx) {
+    A = (uint32_t)ex.A;
+    if (ex.kind == EXP_L_CONST) {          // Δ_B entry (i, r=cj): row r of preterminal C
+        fx = ci;
+        return __ldg(nt[ex.other].csr_ell + cj);
+    }
+    fx = cj | 0x80000000u;                 // Δ_C entry (r=ci, j): column r of preterminal B
+    return __ldg(nt[ex.other].csc_ell + ci);
+}
+
 // Expand the Δ entries log[lo,hi) of iteration k.  Work unit = a chunk of 32
-// consecutive entries per warp; warps [warp0, warp0+nwarps) stride over chunks.
-__device__ void expand(const EngineParams& p, unsigned long long lo, unsigned long long hi, long long k,
-                       int warp, int nwarps, int lane, WarpScratch* ws) {
-    unsigned long long cand = 0;
+// consecutive entries per warp; warps [warp, warp+nwarps) stride over chunks.
+__device__ void expand(const EngineParams& p, const NTInfo* nt, const Expansion* exps, unsigned long long lo,
+                       unsigned long long hi, long long k, int warp, int nwarps, int lane, WarpScratch* ws,
+                       unsigned long long& dcand, unsigned long long& dexp) {
     for (unsigned long long cbase = lo + (unsigned long long)warp * 32ull; cbase < hi;
          cbase += (unsigned long long)nwarps * 32ull) {
         unsigned long long e = cbase + lane;
         bool valid = e < hi;
         uint64_t cell = valid ? ldcg64(p.log + e) : 0ull;
         uint32_t X = cell_nt(cell), ci = cell_i(cell), cj = cell_j(cell);
-        int eb = 0, ee = 0;
+        int eb = 0, nexp = 0;
         if (valid) {
-            eb = __ldg(&p.nt[X].exp_begin);
-            ee = __ldg(&p.nt[X].exp_end);
+            eb = nt[X].exp_begin;
+            nexp = nt[X].exp_end - eb;
         }
-        int nexp = ee - eb;
-        {
-            int tot = nexp;
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(kFull, tot, o);
-            if (lane == 0 && tot) atomicAdd(&p.st->expansions, (unsigned long long)tot);
-        }
+        dexp += (unsigned long long)nexp;
         uint32_t len_e = 0;
-        if (p.lengths && nexp > 0) len_e = (uint32_t)cell_len(p, X, ci, cj);
+        if (p.lengths && nexp > 0) len_e = (uint32_t)cell_len(p, nt, X, ci, cj);
         int maxexp = nexp;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) maxexp = max(maxexp, __shfl_xor_sync(kFull, maxexp, o));
-        unsigned var_mask = 0;   // bit x: this lane's expansion x is a var kind
-        for (int x = 0; x < maxexp; ++x) {
-            int32_t beg = 0, deg = 0;
-            uint32_t A = 0, fixed = 0;
+        if (maxexp == 0) continue;
+
+        // ---- preterminal-operand occurrences 0..kPre-1: all loads, then all atomics ----
+        unsigned var_mask = 0;
+        int4 el[kPre];
+        uint32_t eA[kPre], efx[kPre];
+#pragma unroll
+        for (int x = 0; x < kPre; ++x) {
+            el[x] = make_int4(0, 0, -1, -1);
+            eA[x] = 0;
+            efx[x] = 0;
             if (x < nexp) {
-                Expansion ex = p.exps[eb + x];
-                if (ex.kind == EXP_L_CONST) {
-                    const int32_t* ptr = p.nt[ex.other].csr_ptr;   // C's row r = cj
-                    beg = __ldg(ptr + cj);
-                    deg = __ldg(ptr + cj + 1) - beg;
-                    fixed = ci;
-                    A = ex.A;
-                } else if (ex.kind == EXP_R_CONST) {
-                    const int32_t* ptr = p.nt[ex.other].csc_ptr;   // B's column r = ci
-                    beg = __ldg(ptr + ci);
-                    deg = __ldg(ptr + ci + 1) - beg;
-                    fixed = cj | 0x80000000u;
-                    A = ex.A;
-                } else if (x < 32) {
-                    var_mask |= 1u << x;
-                }
+                Expansion ex = exps[eb + x];
+                if (ex.kind == EXP_L_CONST || ex.kind == EXP_R_CONST) el[x] = load_head(nt, ex, ci, cj, eA[x], efx[x]);
+                else var_mask |= 1u << x;
             }
-            // warp-wide exclusive scan of the degrees: a load-balanced expansion of all
-            // 32 lanes' neighbour lists (hub rows are spread over the warp)
-            int incl = deg;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                int v = __shfl_up_sync(kFull, incl, o);
-                if (lane >= o) incl += v;
-            }
-            int total = __shfl_sync(kFull, incl, 31);
-            if (total == 0) continue;
-            ws->off[lane] = incl - deg;
-            ws->beg[lane] = beg;
-            ws->A[lane] = A;
-            ws->fixed[lane] = fixed;
-            ws->len[lane] = len_e;
-            if (lane == 0) ws->off[32] = total;
-            __syncwarp();
-            if (lane == 0) cand += (unsigned long long)total;
-            for (int tb = 0; tb < total; tb += 32) {
-                int t = tb + lane;
-                bool has = t < total;
-                uint32_t cA = 0, oi = 0, oj = 0;
-                uint64_t clen = 0;
-                if (has) {
-                    int l = 0;
-#pragma unroll
-                    for (int step = 16; step > 0; step >>= 1)
-                        if (ws->off[l + step] <= t) l += step;
-                    int32_t nb = __ldg(p.adj_idx + ws->beg[l] + (t - ws->off[l]));
-                    uint32_t fx = ws->fixed[l];
-                    cA = ws->A[l];
-                    if (fx & 0x80000000u) {
-                        oi = (uint32_t)nb;
-                        oj = fx & 0x7fffffffu;
-                    } else {
-                        oi = fx;
-                        oj = (uint32_t)nb;
-                    }
-                    clen = (uint64_t)ws->len[l] + 1ull;   // the preterminal operand has length 1
-                }
-                emit(p, has, cA, oi, oj, clen, k, lane);
-            }
-            __syncwarp();
         }
-        // rules whose other operand also changes: scan the snapshot row, warp-cooperative
+        bool d0[kPre], d1[kPre];
+        uint32_t ci0[kPre], cj0[kPre], ci1[kPre], cj1[kPre];
+#pragma unroll
+        for (int x = 0; x < kPre; ++x) {
+            cand_coords(efx[x], el[x].z, ci0[x], cj0[x]);
+            cand_coords(efx[x], el[x].w, ci1[x], cj1[x]);
+            d0[x] = try_insert(p, nt, el[x].y > 0, eA[x], ci0[x], cj0[x], (uint64_t)len_e + 1ull, k);
+            d1[x] = try_insert(p, nt, el[x].y > 1, eA[x], ci1[x], cj1[x], (uint64_t)len_e + 1ull, k);
+            dcand += (unsigned long long)el[x].y;
+        }
+        bool any_tail = false;
+#pragma unroll
+        for (int x = 0; x < kPre; ++x) {
+            if (x < maxexp) {
+                stage(p, nt, ws, lane, d0[x], eA[x], ci0[x], cj0[x]);
+                stage(p, nt, ws, lane, d1[x], eA[x], ci1[x], cj1[x]);
+                any_tail |= el[x].y > 2;
+            }
+        }
+        if (__any_sync(kFull, any_tail)) {
+#pragma unroll
+            for (int x = 0; x < kPre; ++x)
+                if (x < maxexp) expand_tail(p, nt, ws, lane, el[x], eA[x], efx[x], len_e, k);
+        }
+        // ---- occurrences kPre.. (rare: NTs on the RHS of many rules) ----
+        for (int x = kPre; x < maxexp; ++x) {
+            int4 h = make_int4(0, 0, -1, -1);
+            uint32_t A = 0, fx = 0;
+            if (x < nexp) {
+                Expansion ex = exps[eb + x];
+                if (ex.kind == EXP_L_CONST || ex.kind == EXP_R_CONST) h = load_head(nt, ex, ci, cj, A, fx);
+                else if (x < 32) var_mask |= 1u << x;
+            }
+            uint32_t a0, b0, a1, b1;
+            cand_coords(fx, h.z, a0, b0);
+            cand_coords(fx, h.w, a1, b1);
+            bool q0 = try_insert(p, nt, h.y > 0, A, a0, b0, (uint64_t)len_e + 1ull, k);
+            bool q1 = try_insert(p, nt, h.y > 1, A, a1, b1, (uint64_t)len_e + 1ull, k);
+            dcand += (unsigned long long)h.y;
+            stage(p, nt, ws, lane, q0, A, a0, b0);
+            stage(p, nt, ws, lane, q1, A, a1, b1);
+            if (__any_sync(kFull, h.y > 2)) expand_tail(p, nt, ws, lane, h, A, fx, len_e, k);
+        }
+        // ---- rules whose other operand also changes: scan the snapshot row, warp-cooperative ----
         unsigned any_var = __ballot_sync(kFull, var_mask != 0);
         while (any_var) {
             int src = __ffs(any_var) - 1;
             any_var &= any_var - 1;
             unsigned vm = __shfl_sync(kFull, var_mask, src);
-            uint32_t sX = __shfl_sync(kFull, X, src);
             uint32_t si = __shfl_sync(kFull, ci, src);
             uint32_t sj = __shfl_sync(kFull, cj, src);
             uint32_t slen = __shfl_sync(kFull, len_e, src);
             int seb = __shfl_sync(kFull, eb, src);
-            (void)sX;
             while (vm) {
                 int x = __ffs(vm) - 1;
                 vm &= vm - 1;
-                Expansion ex = p.exps[seb + x];
+                Expansion ex = exps[seb + x];
                 const uint32_t* row;
                 bool left = ex.kind == EXP_L_VAR;
-                if (left) row = p.nt[ex.other].S + (size_t)sj * p.Wp;    // S_C row r = sj
-                else row = p.nt[ex.other].ST + (size_t)si * p.Wp;        // ST_B row r = si
+                if (left) row = nt[ex.other].S + (size_t)sj * p.Wp;    // S_C row r = sj
+                else row = nt[ex.other].ST + (size_t)si * p.Wp;        // ST_B row r = si
                 const int64_t wn = (p.n + 31) >> 5;
                 for (int64_t w0 = 0; w0 < wn; w0 += 32) {
                     int64_t w = w0 + lane;
@@ -326,31 +445,31 @@ __device__ void expand(const EngineParams& p, unsigned long long lo, unsigned lo
                             if (left) {
                                 oi = si;
                                 oj = v;
-                                if (p.lengths) clen = (uint64_t)slen + cell_len(p, ex.other, sj, v);
+                                if (p.lengths) clen = (uint64_t)slen + cell_len(p, nt, ex.other, sj, v);
                             } else {
                                 oi = v;
                                 oj = sj;
-                                if (p.lengths) clen = cell_len(p, ex.other, v, si) + (uint64_t)slen;
+                                if (p.lengths) clen = cell_len(p, nt, ex.other, v, si) + (uint64_t)slen;
                             }
-                            ++cand;
+                            ++dcand;
                         }
-                        emit(p, has, (uint32_t)ex.A, oi, oj, clen, k, lane);
+                        emit(p, nt, ws, lane, has, (uint32_t)ex.A, oi, oj, clen, k);
                     }
                 }
             }
         }
     }
-    if (cand) atomicAdd(&p.st->candidates, cand);
+    flush(p, nt, ws, lane);
 }
 
 // Fold Δ_k = log[lo,hi) into the snapshots S (row) and ST (transposed).
-__device__ void apply_snapshots(const EngineParams& p, unsigned long long lo, unsigned long long hi, long long tid,
-                                long long nthreads) {
+__device__ void apply_snapshots(const EngineParams& p, const NTInfo* nt, unsigned long long lo, unsigned long long hi,
+                                long long tid, long long nthreads) {
     for (unsigned long long e = lo + (unsigned long long)tid; e < hi; e += (unsigned long long)nthreads) {
         uint64_t c = ldcg64(p.log + e);
         uint32_t A = cell_nt(c), i = cell_i(c), j = cell_j(c);
-        uint32_t* S = p.nt[A].S;
-        uint32_t* ST = p.nt[A].ST;
+        uint32_t* S = nt[A].S;
+        uint32_t* ST = nt[A].ST;
         if (S) atomicOr(S + (size_t)i * p.Wp + (j >> 5), 1u << (j & 31));
         if (ST) atomicOr(ST + (size_t)j * p.Wp + (i >> 5), 1u << (i & 31));
     }
@@ -373,37 +492,49 @@ __device__ void account(const EngineParams& p, long long k, long long tid, long 
     if ((threadIdx.x & 31) == 0 && acc && k < p.iter_off_cap) atomicAdd(p.jac + k, acc);
 }
 
-// Close iteration k (single thread): Δ_k = log[hi, log_size).
-__device__ void finalize(const EngineParams& p, long long k) {
+struct LoopState {
+    unsigned long long lo, hi;
+    long long iter;
+    int status;
+};
+
+// Close iteration k: Δ_k = log[hi, log_size).  Single thread.  `s` is updated; the
+// caller publishes it (fenced) when other CTAs must see it.
+__device__ void close_iteration(const EngineParams& p, long long k, LoopState& s) {
     EngineState* st = p.st;
-    __threadfence();
     unsigned long long ls = ld_volatile_u64(&st->log_size);
     int ov = *(volatile int*)&st->overflow;
     int status = *(volatile int*)&st->status;
-    if (status == ST_LEN_OVERFLOW) return;
-    if (ov) {
-        st->status = ST_OVERFLOW;   // keep lo/hi/iter: the host grows the log and re-runs k
+    if (status == ST_LEN_OVERFLOW) {
+        s.status = ST_LEN_OVERFLOW;
         return;
     }
-    unsigned long long new_lo = st->hi;
-    st->lo = new_lo;
-    st->hi = ls;
-    st->iter = k;
+    if (ov) {
+        s.status = ST_OVERFLOW;   // keep lo/hi/iter: the host grows the log and re-runs k
+        return;
+    }
+    s.lo = s.hi;
+    s.hi = ls;
+    s.iter = k;
     if (k < p.iter_off_cap) {
-        p.iter_off[k] = new_lo;
-        if (p.iter_time) {
-            unsigned long long t;
-            asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-            p.iter_time[k] = t;
-        }
+        p.iter_off[k] = s.lo;
+        if (p.iter_time) p.iter_time[k] = globaltimer();
     }
     if (k + 1 < p.iter_off_cap) p.iter_off[k + 1] = ls;
-    if (ls == new_lo) st->status = ST_DONE;             // T_k = T_{k-1}: fixpoint
-    else if (k >= p.max_iter) st->status = ST_CAP;      // Theorem 3 cap
+    if (ls == s.lo) s.status = ST_DONE;             // T_k = T_{k-1}: fixpoint
+    else if (k >= p.max_iter) s.status = ST_CAP;    // Theorem 3 cap
+}
+
+__device__ void publish(const EngineParams& p, const LoopState& s) {
+    EngineState* st = p.st;
+    st->lo = s.lo;
+    st->hi = s.hi;
+    st->iter = s.iter;
+    *(volatile int*)&st->status = s.status;
     __threadfence();
 }
 
-// Grid barrier; the last CTA to arrive runs finalize(k) (if k >= 0) before release.
+// Grid barrier; the last CTA to arrive closes iteration k (if k >= 0) before release.
 __device__ bool grid_barrier(const EngineParams& p, long long k) {
     __syncthreads();
     __shared__ int s_timeout;
@@ -415,7 +546,15 @@ __device__ bool grid_barrier(const EngineParams& p, long long k) {
         __threadfence();
         unsigned arrived = atomicAdd(&st->bar_count, 1u);
         if (arrived == (unsigned)p.nblocks - 1u) {
-            if (k >= 0) finalize(p, k);
+            if (k >= 0) {
+                LoopState s;
+                s.lo = ld_volatile_u64(&st->lo);
+                s.hi = ld_volatile_u64(&st->hi);
+                s.iter = *(volatile long long*)&st->iter;
+                s.status = *(volatile int*)&st->status;
+                close_iteration(p, k, s);
+                publish(p, s);
+            }
             st->bar_count = 0u;
             __threadfence();
             atomicAdd(&st->bar_gen, 1u);
@@ -423,7 +562,7 @@ __device__ bool grid_barrier(const EngineParams& p, long long k) {
             long long t0 = clock64();
             while (*gen == my) {
                 __nanosleep(64);
-                if (clock64() - t0 > 40000000000ll) {   // ~20 s watchdog: never hang the GPU
+                if (clock64() - t0 > 60000000000ll) {   // ~30 s watchdog: never hang the GPU
                     s_timeout = 1;
                     break;
                 }
@@ -435,53 +574,67 @@ __device__ bool grid_barrier(const EngineParams& p, long long k) {
     return s_timeout == 0;
 }
 
-__global__ void __launch_bounds__(kBlock) closure_kernel(EngineParams p) {
+__global__ void __launch_bounds__(kBlock, 2) closure_kernel(EngineParams p) {
     __shared__ WarpScratch ws[kWarps];
-    __shared__ unsigned long long s_lo, s_hi;
-    __shared__ long long s_iter;
-    __shared__ int s_status;
+    __shared__ NTInfo s_nt[kSmemNT];
+    __shared__ Expansion s_exp[kSmemExp];
+    __shared__ LoopState s_state;
+    __shared__ long long s_solo;
     const int lane = threadIdx.x & 31;
     const int wib = threadIdx.x >> 5;
     EngineState* st = p.st;
+    // NT / expansion tables into shared memory (fences invalidate L1 every iteration)
+    const bool small = p.n_nt <= kSmemNT && p.n_exps <= kSmemExp;
+    if (small) {
+        for (int t = threadIdx.x; t < p.n_nt; t += kBlock) s_nt[t] = p.nt[t];
+        for (int t = threadIdx.x; t < p.n_exps; t += kBlock) s_exp[t] = p.exps[t];
+    }
+    const NTInfo* nt = small ? s_nt : p.nt;
+    const Expansion* exps = small ? s_exp : p.exps;
+    if (lane == 0) ws[wib].nbuf = 0;
+    if (threadIdx.x == 0) s_solo = 0;
+    __syncthreads();
+    unsigned long long dcand = 0, dexp = 0;
     for (;;) {
         if (threadIdx.x == 0) {
-            s_lo = ld_volatile_u64(&st->lo);
-            s_hi = ld_volatile_u64(&st->hi);
-            s_iter = *(volatile long long*)&st->iter;
-            s_status = *(volatile int*)&st->status;
+            s_state.lo = ld_volatile_u64(&st->lo);
+            s_state.hi = ld_volatile_u64(&st->hi);
+            s_state.iter = *(volatile long long*)&st->iter;
+            s_state.status = *(volatile int*)&st->status;
         }
         __syncthreads();
-        unsigned long long lo = s_lo, hi = s_hi;
-        long long k = s_iter + 1;
-        if (s_status != ST_RUNNING) break;
+        LoopState s = s_state;
         __syncthreads();
-        if ((long long)(hi - lo) <= (long long)p.solo_max) {
-            // ---------------- single-CTA iterations ----------------
+        if (s.status != ST_RUNNING) break;
+        long long k = s.iter + 1;
+        if ((long long)(s.hi - s.lo) <= (long long)p.solo_max) {
+            // ---------------- single-CTA iterations (no fences, no grid barrier) ----------------
             if (blockIdx.x == 0) {
                 for (;;) {
                     if (p.jac) {
                         account(p, k, threadIdx.x, kBlock);
                         __syncthreads();
                     }
-                    expand(p, lo, hi, k, wib, kWarps, lane, &ws[wib]);
+                    expand(p, nt, exps, s.lo, s.hi, k, wib, kWarps, lane, &ws[wib], dcand, dexp);
                     __syncthreads();
                     if (threadIdx.x == 0) {
-                        finalize(p, k);
-                        st->solo_iters += 1;
-                        s_lo = st->lo;
-                        s_hi = st->hi;
-                        s_status = st->status;
+                        close_iteration(p, k, s_state);
+                        s_solo += 1;
                     }
                     __syncthreads();
-                    if (s_status != ST_RUNNING) break;
-                    lo = s_lo;
-                    hi = s_hi;
+                    s = s_state;
+                    if (s.status != ST_RUNNING) break;
                     if (p.has_snapshots) {
-                        apply_snapshots(p, lo, hi, threadIdx.x, kBlock);
+                        apply_snapshots(p, nt, s.lo, s.hi, threadIdx.x, kBlock);
                         __syncthreads();
                     }
                     ++k;
-                    if ((long long)(hi - lo) > (long long)p.solo_max) break;
+                    if ((long long)(s.hi - s.lo) > (long long)p.solo_max) break;
+                }
+                if (threadIdx.x == 0) {
+                    publish(p, s_state);
+                    atomicAdd((unsigned long long*)&st->solo_iters, (unsigned long long)s_solo);
+                    s_solo = 0;
                 }
             }
             if (!grid_barrier(p, -1)) return;
@@ -494,18 +647,28 @@ __global__ void __launch_bounds__(kBlock) closure_kernel(EngineParams p) {
             account(p, k, gtid, gthreads);
             if (!grid_barrier(p, -1)) return;
         }
-        expand(p, lo, hi, k, blockIdx.x * kWarps + wib, gridDim.x * kWarps, lane, &ws[wib]);
+        expand(p, nt, exps, s.lo, s.hi, k, blockIdx.x * kWarps + wib, gridDim.x * kWarps, lane, &ws[wib], dcand, dexp);
         if (!grid_barrier(p, k)) return;
         if (p.has_snapshots) {
             if (threadIdx.x == 0) {
-                s_lo = ld_volatile_u64(&st->lo);
-                s_hi = ld_volatile_u64(&st->hi);
-                s_status = *(volatile int*)&st->status;
+                s_state.lo = ld_volatile_u64(&st->lo);
+                s_state.hi = ld_volatile_u64(&st->hi);
+                s_state.status = *(volatile int*)&st->status;
             }
             __syncthreads();
-            if (s_status == ST_RUNNING) apply_snapshots(p, s_lo, s_hi, gtid, gthreads);
+            if (s_state.status == ST_RUNNING) apply_snapshots(p, nt, s_state.lo, s_state.hi, gtid, gthreads);
             if (!grid_barrier(p, -1)) return;
         }
+    }
+    // diagnostics: one atomic per warp per launch
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        dcand += __shfl_xor_sync(kFull, dcand, o);
+        dexp += __shfl_xor_sync(kFull, dexp, o);
+    }
+    if (lane == 0) {
+        if (dcand) atomicAdd(&st->candidates, dcand);
+        if (dexp) atomicAdd(&st->expansions, dexp);
     }
 }
 
@@ -518,17 +681,12 @@ __global__ void begin_kernel(EngineParams p) {
     st->iter = 0;
     if (p.iter_off_cap > 0) p.iter_off[0] = 0;
     if (p.iter_off_cap > 1) p.iter_off[1] = n0;
-    if (p.iter_time) {
-        unsigned long long t;
-        asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-        p.iter_time[0] = t;
-    }
-    if (n0 == 0) st->status = ST_RUNNING;   // iteration 1 still runs: no change -> 1 iteration
+    if (p.iter_time) p.iter_time[0] = globaltimer();
 }
 
 // Δ_0 into the snapshots (one launch after seeding).
 __global__ void seed_snapshots_kernel(EngineParams p) {
-    apply_snapshots(p, 0, ld_volatile_u64(&p.st->hi), (long long)blockIdx.x * blockDim.x + threadIdx.x,
+    apply_snapshots(p, p.nt, 0, ld_volatile_u64(&p.st->hi), (long long)blockIdx.x * blockDim.x + threadIdx.x,
                     (long long)gridDim.x * blockDim.x);
 }
 
@@ -547,8 +705,8 @@ cudaError_t launch_seed(const int32_t* edges, int64_t n_edges, int32_t n_nodes, 
                         const EngineParams& p, cudaStream_t s) {
     (void)n_nodes;
     if (n_edges > 0 && max_rules_per_label > 0)
-        seed_kernel<<<grid_for(n_edges, 256), 256, 0, s>>>(p, edges, n_edges, lab_ptr, lab_nt, n_labels,
-                                                            max_rules_per_label);
+        seed_kernel<<<grid_for(n_edges, kSeedBlock), kSeedBlock, 0, s>>>(p, edges, n_edges, lab_ptr, lab_nt, n_labels,
+                                                                          max_rules_per_label);
     return cudaGetLastError();
 }
 
@@ -562,6 +720,13 @@ cudaError_t launch_adj_fill(const EngineParams& p, const int32_t* slot_row, cons
                             int32_t* cursor, int32_t* idx, unsigned long long n_seed, cudaStream_t s) {
     if (n_seed)
         adj_fill_kernel<<<grid_for((int64_t)n_seed, 256), 256, 0, s>>>(p, slot_row, slot_col, cursor, idx);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_adj_ell(const int32_t* ptr, const int32_t* idx, int4* ell, int64_t n_slots, int32_t n,
+                           cudaStream_t s) {
+    int64_t rows = n_slots * (int64_t)n;
+    if (rows) adj_ell_kernel<<<grid_for(rows, 256), 256, 0, s>>>(ptr, idx, ell, rows, n);
     return cudaGetLastError();
 }
 
