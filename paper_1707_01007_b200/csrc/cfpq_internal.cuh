@@ -76,13 +76,15 @@ struct EngineState {
     long long iter;                // iterations completed
     int status;                    // ST_*
     int overflow;                  // set by a failed append
-    unsigned bar_count;
-    unsigned bar_gen;
+    int len_overflow;              // set by a single-path length > 2^32-1
+    int bad_edge;                  // seed saw an out-of-range edge
     unsigned long long candidates; // expanded candidates = semi-naive AND-true triples
     unsigned long long expansions; // (Δ entry, rule occurrence) pairs expanded
     long long solo_iters;          // iterations run by the single-CTA path
-    int bad_edge;                  // seed saw an out-of-range edge
-    int pad;
+    unsigned long long pad0[7];
+    unsigned bar_count;            // grid-barrier words, on their own 128-byte line
+    unsigned bar_gen;
+    unsigned pad1[30];
 };
 
 enum : int { ST_RUNNING = 0, ST_DONE = 1, ST_OVERFLOW = 2, ST_CAP = 3, ST_LEN_OVERFLOW = 4 };

@@ -33,7 +33,8 @@ namespace cfpq {
 constexpr int kBlock = 512;
 constexpr int kWarps = kBlock / 32;
 constexpr int kSeedBlock = 256;
-constexpr int kBuf = 128;            // per-warp staging capacity (cells)
+constexpr int kBuf = 64;             // per-warp staging capacity (cells)
+constexpr int kSoloMax = 1024;       // max |Δ| mirrored in shared memory by the single-CTA path
 constexpr int kSmemNT = 64;          // NT / expansion tables cached in shared memory
 constexpr int kSmemExp = 256;
 constexpr int kPre = 2;              // rule occurrences prefetched per entry
@@ -62,6 +63,18 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 }
 __device__ __forceinline__ unsigned lanemask_lt(int lane) { return (1u << lane) - 1u; }
 
+// Where new cells go: the log append counter and the error flags live in global memory
+// for grid-wide iterations and in shared memory for single-CTA iterations; the single-
+// CTA path also mirrors Δ_k into shared memory (mirror[idx - mirror_base]).
+struct Sink {
+    unsigned long long* counter;
+    int* overflow;
+    int* len_overflow;
+    uint64_t* mirror;
+    unsigned long long mirror_base;
+    unsigned long long mirror_cap;
+};
+
 struct __align__(16) WarpScratch {
     uint64_t buf[kBuf];   // staged new cells
     int32_t off[33];
@@ -84,13 +97,13 @@ __device__ __forceinline__ uint64_t cell_len(const EngineParams& p, const NTInfo
 // Insert candidate (A,i,j) of length len into T_k; true iff the cell is new:
 // relational -> the bit flips; single-path -> the key leaves EMPTY (atomicMin on
 // (iteration<<32 | length): first write wins across iterations, min within one).
-__device__ __forceinline__ bool try_insert(const EngineParams& p, const NTInfo* nt, bool has, uint32_t A, uint32_t i,
-                                           uint32_t j, uint64_t len, long long k) {
+__device__ __forceinline__ bool try_insert(const EngineParams& p, const NTInfo* nt, const Sink& sk, bool has,
+                                           uint32_t A, uint32_t i, uint32_t j, uint64_t len, long long k) {
     if (!has) return false;
     uint64_t* K = nt[A].K;
     if (p.lengths && K != nullptr) {
         if (len > 0xffffffffull) {
-            *(volatile int*)&p.st->status = ST_LEN_OVERFLOW;   // reported at the next barrier
+            *(volatile int*)sk.len_overflow = 1;   // reported when the iteration closes
             len = 0xffffffffull;
         }
         uint64_t kv = ((uint64_t)k << 32) | len;
@@ -105,11 +118,12 @@ __device__ __forceinline__ bool try_insert(const EngineParams& p, const NTInfo* 
 // Append the warp's staged cells to the log (one atomic per flush).  A cell that
 // does not fit is rolled back so that a re-run of the iteration (after the host
 // grows the log) rediscovers it; appended cells stay set and are not re-appended.
-__device__ __forceinline__ void flush(const EngineParams& p, const NTInfo* nt, WarpScratch* ws, int lane) {
+__device__ __forceinline__ void flush(const EngineParams& p, const NTInfo* nt, const Sink& sk, WarpScratch* ws,
+                                      int lane) {
     int nb = ws->nbuf;
     if (nb == 0) return;
     unsigned long long base = 0;
-    if (lane == 0) base = atomicAdd(&p.st->log_size, (unsigned long long)nb);
+    if (lane == 0) base = atomicAdd(sk.counter, (unsigned long long)nb);
     base = __shfl_sync(kFull, base, 0);
     for (int t = lane; t < nb; t += 32) {
         uint64_t c = ws->buf[t];
@@ -120,6 +134,7 @@ __device__ __forceinline__ void flush(const EngineParams& p, const NTInfo* nt, W
         uint32_t bit = 1u << (j & 31);
         if (idx < p.log_cap) {
             p.log[idx] = c;
+            if (sk.mirror != nullptr && idx - sk.mirror_base < sk.mirror_cap) sk.mirror[idx - sk.mirror_base] = c;
             if (K != nullptr) atomicOr(word, bit);   // the bit matrix mirrors the keys
             if (p.rowc != nullptr) {
                 atomicAdd(p.rowc + (size_t)A * p.n + i, 1u);
@@ -129,7 +144,7 @@ __device__ __forceinline__ void flush(const EngineParams& p, const NTInfo* nt, W
             if (K != nullptr) atomicExch((unsigned long long*)(K + (size_t)i * (size_t)p.n + j),
                                          (unsigned long long)kEmptyKey);
             else atomicAnd(word, ~bit);
-            *(volatile int*)&p.st->overflow = 1;
+            *(volatile int*)sk.overflow = 1;
         }
     }
     __syncwarp();
@@ -138,14 +153,14 @@ __device__ __forceinline__ void flush(const EngineParams& p, const NTInfo* nt, W
 }
 
 // Warp-uniform: stage the lanes' new cells (disc) in the warp buffer.
-__device__ __forceinline__ void stage(const EngineParams& p, const NTInfo* nt, WarpScratch* ws, int lane, bool disc,
-                                      uint32_t A, uint32_t i, uint32_t j) {
+__device__ __forceinline__ void stage(const EngineParams& p, const NTInfo* nt, const Sink& sk, WarpScratch* ws,
+                                      int lane, bool disc, uint32_t A, uint32_t i, uint32_t j) {
     unsigned mask = __ballot_sync(kFull, disc);
     if (mask == 0) return;
     int cnt = __popc(mask);
     int nb = ws->nbuf;
     if (nb + cnt > kBuf) {
-        flush(p, nt, ws, lane);
+        flush(p, nt, sk, ws, lane);
         nb = 0;
     }
     if (disc) ws->buf[nb + __popc(mask & lanemask_lt(lane))] = pack_cell(A, i, j);
@@ -154,10 +169,22 @@ __device__ __forceinline__ void stage(const EngineParams& p, const NTInfo* nt, W
     __syncwarp();
 }
 
-__device__ __forceinline__ void emit(const EngineParams& p, const NTInfo* nt, WarpScratch* ws, int lane, bool has,
-                                     uint32_t A, uint32_t i, uint32_t j, uint64_t len, long long k) {
-    bool d = try_insert(p, nt, has, A, i, j, len, k);
-    stage(p, nt, ws, lane, d, A, i, j);
+__device__ __forceinline__ void emit(const EngineParams& p, const NTInfo* nt, const Sink& sk, WarpScratch* ws,
+                                     int lane, bool has, uint32_t A, uint32_t i, uint32_t j, uint64_t len,
+                                     long long k) {
+    bool d = try_insert(p, nt, sk, has, A, i, j, len, k);
+    stage(p, nt, sk, ws, lane, d, A, i, j);
+}
+
+__device__ __forceinline__ Sink global_sink(const EngineParams& p) {
+    Sink sk;
+    sk.counter = &p.st->log_size;
+    sk.overflow = &p.st->overflow;
+    sk.len_overflow = &p.st->len_overflow;
+    sk.mirror = nullptr;
+    sk.mirror_base = 0;
+    sk.mirror_cap = 0;
+    return sk;
 }
 
 // ------------------------------------------------------------------------------------------
@@ -171,6 +198,7 @@ __global__ void __launch_bounds__(kSeedBlock) seed_kernel(EngineParams p, const 
     __shared__ WarpScratch wsa[kSeedBlock / 32];
     const int lane = threadIdx.x & 31;
     WarpScratch* ws = &wsa[threadIdx.x >> 5];
+    const Sink sk = global_sink(p);
     if (lane == 0) ws->nbuf = 0;
     __syncwarp();
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -193,10 +221,10 @@ __global__ void __launch_bounds__(kSeedBlock) seed_kernel(EngineParams p, const 
         for (int t = 0; t < max_rules; ++t) {
             bool has = valid && (rb + t < re);
             uint32_t A = has ? (uint32_t)__ldg(lab_nt + rb + t) : 0u;
-            emit(p, p.nt, ws, lane, has, A, (uint32_t)s, (uint32_t)d, 1, 0);
+            emit(p, p.nt, sk, ws, lane, has, A, (uint32_t)s, (uint32_t)d, 1, 0);
         }
     }
-    flush(p, p.nt, ws, lane);
+    flush(p, p.nt, sk, ws, lane);
 }
 
 // CSR / CSC of preterminals from the seed cells Δ_0 = log[0, n_seed).
@@ -279,8 +307,8 @@ __device__ __forceinline__ void cand_coords(uint32_t fx, int32_t nb, uint32_t& i
 
 // Neighbours beyond the ELL head (deg > 2): warp-wide exclusive scan of the tail
 // lengths, load-balanced over the 32 lanes (hub rows are spread over the warp).
-__device__ void expand_tail(const EngineParams& p, const NTInfo* nt, WarpScratch* ws, int lane, int4 el, uint32_t A,
-                            uint32_t fx, uint32_t len_e, long long k) {
+__device__ void expand_tail(const EngineParams& p, const NTInfo* nt, const Sink& sk, WarpScratch* ws, int lane, int4 el,
+                            uint32_t A, uint32_t fx, uint32_t len_e, long long k) {
     int32_t beg = el.x + 2;
     int32_t deg = el.y > 2 ? el.y - 2 : 0;
     int incl = deg;
@@ -313,7 +341,7 @@ __device__ void expand_tail(const EngineParams& p, const NTInfo* nt, WarpScratch
             cand_coords(ws->fixed[l], nbv, oi, oj);
             clen = (uint64_t)ws->len[l] + 1ull;   // the preterminal operand has length 1
         }
-        emit(p, nt, ws, lane, has, cA, oi, oj, clen, k);
+        emit(p, nt, sk, ws, lane, has, cA, oi, oj, clen, k);
     }
     __syncwarp();
 }
@@ -332,14 +360,16 @@ __device__ __forceinline__ int4 load_head(const NTInfo* nt, const Expansion& ex,
 
 // Expand the Δ entries log[lo,hi) of iteration k.  Work unit = a chunk of 32
 // consecutive entries per warp; warps [warp, warp+nwarps) stride over chunks.
-__device__ void expand(const EngineParams& p, const NTInfo* nt, const Expansion* exps, unsigned long long lo,
-                       unsigned long long hi, long long k, int warp, int nwarps, int lane, WarpScratch* ws,
-                       unsigned long long& dcand, unsigned long long& dexp) {
+// `src` = shared-memory copy of log[lo,hi) (single-CTA path) or null (read the log).
+__device__ void expand(const EngineParams& p, const NTInfo* nt, const Expansion* exps, const Sink& sk,
+                       const uint64_t* src, unsigned long long lo, unsigned long long hi, long long k, int warp,
+                       int nwarps, int lane, WarpScratch* ws, unsigned long long& dcand, unsigned long long& dexp) {
     for (unsigned long long cbase = lo + (unsigned long long)warp * 32ull; cbase < hi;
          cbase += (unsigned long long)nwarps * 32ull) {
         unsigned long long e = cbase + lane;
         bool valid = e < hi;
-        uint64_t cell = valid ? ldcg64(p.log + e) : 0ull;
+        uint64_t cell = 0ull;
+        if (valid) cell = src ? src[e - lo] : ldcg64(p.log + e);
         uint32_t X = cell_nt(cell), ci = cell_i(cell), cj = cell_j(cell);
         int eb = 0, nexp = 0;
         if (valid) {
@@ -375,23 +405,23 @@ __device__ void expand(const EngineParams& p, const NTInfo* nt, const Expansion*
         for (int x = 0; x < kPre; ++x) {
             cand_coords(efx[x], el[x].z, ci0[x], cj0[x]);
             cand_coords(efx[x], el[x].w, ci1[x], cj1[x]);
-            d0[x] = try_insert(p, nt, el[x].y > 0, eA[x], ci0[x], cj0[x], (uint64_t)len_e + 1ull, k);
-            d1[x] = try_insert(p, nt, el[x].y > 1, eA[x], ci1[x], cj1[x], (uint64_t)len_e + 1ull, k);
+            d0[x] = try_insert(p, nt, sk, el[x].y > 0, eA[x], ci0[x], cj0[x], (uint64_t)len_e + 1ull, k);
+            d1[x] = try_insert(p, nt, sk, el[x].y > 1, eA[x], ci1[x], cj1[x], (uint64_t)len_e + 1ull, k);
             dcand += (unsigned long long)el[x].y;
         }
         bool any_tail = false;
 #pragma unroll
         for (int x = 0; x < kPre; ++x) {
             if (x < maxexp) {
-                stage(p, nt, ws, lane, d0[x], eA[x], ci0[x], cj0[x]);
-                stage(p, nt, ws, lane, d1[x], eA[x], ci1[x], cj1[x]);
+                stage(p, nt, sk, ws, lane, d0[x], eA[x], ci0[x], cj0[x]);
+                stage(p, nt, sk, ws, lane, d1[x], eA[x], ci1[x], cj1[x]);
                 any_tail |= el[x].y > 2;
             }
         }
         if (__any_sync(kFull, any_tail)) {
 #pragma unroll
             for (int x = 0; x < kPre; ++x)
-                if (x < maxexp) expand_tail(p, nt, ws, lane, el[x], eA[x], efx[x], len_e, k);
+                if (x < maxexp) expand_tail(p, nt, sk, ws, lane, el[x], eA[x], efx[x], len_e, k);
         }
         // ---- occurrences kPre.. (rare: NTs on the RHS of many rules) ----
         for (int x = kPre; x < maxexp; ++x) {
@@ -405,12 +435,12 @@ __device__ void expand(const EngineParams& p, const NTInfo* nt, const Expansion*
             uint32_t a0, b0, a1, b1;
             cand_coords(fx, h.z, a0, b0);
             cand_coords(fx, h.w, a1, b1);
-            bool q0 = try_insert(p, nt, h.y > 0, A, a0, b0, (uint64_t)len_e + 1ull, k);
-            bool q1 = try_insert(p, nt, h.y > 1, A, a1, b1, (uint64_t)len_e + 1ull, k);
+            bool q0 = try_insert(p, nt, sk, h.y > 0, A, a0, b0, (uint64_t)len_e + 1ull, k);
+            bool q1 = try_insert(p, nt, sk, h.y > 1, A, a1, b1, (uint64_t)len_e + 1ull, k);
             dcand += (unsigned long long)h.y;
-            stage(p, nt, ws, lane, q0, A, a0, b0);
-            stage(p, nt, ws, lane, q1, A, a1, b1);
-            if (__any_sync(kFull, h.y > 2)) expand_tail(p, nt, ws, lane, h, A, fx, len_e, k);
+            stage(p, nt, sk, ws, lane, q0, A, a0, b0);
+            stage(p, nt, sk, ws, lane, q1, A, a1, b1);
+            if (__any_sync(kFull, h.y > 2)) expand_tail(p, nt, sk, ws, lane, h, A, fx, len_e, k);
         }
         // ---- rules whose other operand also changes: scan the snapshot row, warp-cooperative ----
         unsigned any_var = __ballot_sync(kFull, var_mask != 0);
@@ -453,20 +483,20 @@ __device__ void expand(const EngineParams& p, const NTInfo* nt, const Expansion*
                             }
                             ++dcand;
                         }
-                        emit(p, nt, ws, lane, has, (uint32_t)ex.A, oi, oj, clen, k);
+                        emit(p, nt, sk, ws, lane, has, (uint32_t)ex.A, oi, oj, clen, k);
                     }
                 }
             }
         }
     }
-    flush(p, nt, ws, lane);
+    flush(p, nt, sk, ws, lane);
 }
 
 // Fold Δ_k = log[lo,hi) into the snapshots S (row) and ST (transposed).
-__device__ void apply_snapshots(const EngineParams& p, const NTInfo* nt, unsigned long long lo, unsigned long long hi,
-                                long long tid, long long nthreads) {
+__device__ void apply_snapshots(const EngineParams& p, const NTInfo* nt, const uint64_t* src, unsigned long long lo,
+                                unsigned long long hi, long long tid, long long nthreads) {
     for (unsigned long long e = lo + (unsigned long long)tid; e < hi; e += (unsigned long long)nthreads) {
-        uint64_t c = ldcg64(p.log + e);
+        uint64_t c = src ? src[e - lo] : ldcg64(p.log + e);
         uint32_t A = cell_nt(c), i = cell_i(c), j = cell_j(c);
         uint32_t* S = nt[A].S;
         uint32_t* ST = nt[A].ST;
@@ -498,14 +528,11 @@ struct LoopState {
     int status;
 };
 
-// Close iteration k: Δ_k = log[hi, log_size).  Single thread.  `s` is updated; the
-// caller publishes it (fenced) when other CTAs must see it.
-__device__ void close_iteration(const EngineParams& p, long long k, LoopState& s) {
-    EngineState* st = p.st;
-    unsigned long long ls = ld_volatile_u64(&st->log_size);
-    int ov = *(volatile int*)&st->overflow;
-    int status = *(volatile int*)&st->status;
-    if (status == ST_LEN_OVERFLOW) {
+// Close iteration k: Δ_k = log[hi, ls).  Single thread; `s` is updated and the caller
+// publishes it (fenced) when other CTAs must see it.
+__device__ void close_iteration(const EngineParams& p, long long k, LoopState& s, unsigned long long ls, int ov,
+                                int lov) {
+    if (lov) {
         s.status = ST_LEN_OVERFLOW;
         return;
     }
@@ -552,7 +579,8 @@ __device__ bool grid_barrier(const EngineParams& p, long long k) {
                 s.hi = ld_volatile_u64(&st->hi);
                 s.iter = *(volatile long long*)&st->iter;
                 s.status = *(volatile int*)&st->status;
-                close_iteration(p, k, s);
+                close_iteration(p, k, s, ld_volatile_u64(&st->log_size), *(volatile int*)&st->overflow,
+                                *(volatile int*)&st->len_overflow);
                 publish(p, s);
             }
             st->bar_count = 0u;
@@ -578,7 +606,10 @@ __global__ void __launch_bounds__(kBlock, 2) closure_kernel(EngineParams p) {
     __shared__ WarpScratch ws[kWarps];
     __shared__ NTInfo s_nt[kSmemNT];
     __shared__ Expansion s_exp[kSmemExp];
+    __shared__ uint64_t s_delta[2][kSoloMax];
     __shared__ LoopState s_state;
+    __shared__ unsigned long long s_ls;
+    __shared__ int s_ov, s_lov;
     __shared__ long long s_solo;
     const int lane = threadIdx.x & 31;
     const int wib = threadIdx.x >> 5;
@@ -591,6 +622,7 @@ __global__ void __launch_bounds__(kBlock, 2) closure_kernel(EngineParams p) {
     }
     const NTInfo* nt = small ? s_nt : p.nt;
     const Expansion* exps = small ? s_exp : p.exps;
+    const Sink gsink = global_sink(p);
     if (lane == 0) ws[wib].nbuf = 0;
     if (threadIdx.x == 0) s_solo = 0;
     __syncthreads();
@@ -608,30 +640,53 @@ __global__ void __launch_bounds__(kBlock, 2) closure_kernel(EngineParams p) {
         if (s.status != ST_RUNNING) break;
         long long k = s.iter + 1;
         if ((long long)(s.hi - s.lo) <= (long long)p.solo_max) {
-            // ---------------- single-CTA iterations (no fences, no grid barrier) ----------------
+            // ------------- single-CTA iterations: Δ, counter and flags in shared memory -------------
             if (blockIdx.x == 0) {
+                int cur = 0;
+                if (threadIdx.x == 0) {
+                    s_ls = ld_volatile_u64(&st->log_size);
+                    s_ov = 0;
+                    s_lov = 0;
+                }
+                if (s.hi - s.lo <= (unsigned long long)kSoloMax)
+                    for (unsigned long long e = s.lo + threadIdx.x; e < s.hi; e += kBlock)
+                        s_delta[cur][e - s.lo] = ldcg64(p.log + e);
+                __syncthreads();
                 for (;;) {
                     if (p.jac) {
                         account(p, k, threadIdx.x, kBlock);
                         __syncthreads();
                     }
-                    expand(p, nt, exps, s.lo, s.hi, k, wib, kWarps, lane, &ws[wib], dcand, dexp);
+                    Sink sk;
+                    sk.counter = &s_ls;
+                    sk.overflow = &s_ov;
+                    sk.len_overflow = &s_lov;
+                    sk.mirror = s_delta[cur ^ 1];
+                    sk.mirror_base = s.hi;
+                    sk.mirror_cap = kSoloMax;
+                    const uint64_t* src = (s.hi - s.lo <= (unsigned long long)kSoloMax) ? s_delta[cur] : nullptr;
+                    expand(p, nt, exps, sk, src, s.lo, s.hi, k, wib, kWarps, lane, &ws[wib], dcand, dexp);
                     __syncthreads();
                     if (threadIdx.x == 0) {
-                        close_iteration(p, k, s_state);
+                        close_iteration(p, k, s_state, s_ls, s_ov, s_lov);
                         s_solo += 1;
                     }
                     __syncthreads();
                     s = s_state;
                     if (s.status != ST_RUNNING) break;
+                    cur ^= 1;
                     if (p.has_snapshots) {
-                        apply_snapshots(p, nt, s.lo, s.hi, threadIdx.x, kBlock);
+                        const uint64_t* sn = (s.hi - s.lo <= (unsigned long long)kSoloMax) ? s_delta[cur] : nullptr;
+                        apply_snapshots(p, nt, sn, s.lo, s.hi, threadIdx.x, kBlock);
                         __syncthreads();
                     }
                     ++k;
                     if ((long long)(s.hi - s.lo) > (long long)p.solo_max) break;
                 }
                 if (threadIdx.x == 0) {
+                    st->log_size = s_ls;   // the other CTAs are parked at the grid barrier
+                    if (s_ov) st->overflow = 1;
+                    if (s_lov) st->len_overflow = 1;
                     publish(p, s_state);
                     atomicAdd((unsigned long long*)&st->solo_iters, (unsigned long long)s_solo);
                     s_solo = 0;
@@ -647,7 +702,8 @@ __global__ void __launch_bounds__(kBlock, 2) closure_kernel(EngineParams p) {
             account(p, k, gtid, gthreads);
             if (!grid_barrier(p, -1)) return;
         }
-        expand(p, nt, exps, s.lo, s.hi, k, blockIdx.x * kWarps + wib, gridDim.x * kWarps, lane, &ws[wib], dcand, dexp);
+        expand(p, nt, exps, gsink, nullptr, s.lo, s.hi, k, blockIdx.x * kWarps + wib, gridDim.x * kWarps, lane,
+               &ws[wib], dcand, dexp);
         if (!grid_barrier(p, k)) return;
         if (p.has_snapshots) {
             if (threadIdx.x == 0) {
@@ -656,7 +712,8 @@ __global__ void __launch_bounds__(kBlock, 2) closure_kernel(EngineParams p) {
                 s_state.status = *(volatile int*)&st->status;
             }
             __syncthreads();
-            if (s_state.status == ST_RUNNING) apply_snapshots(p, nt, s_state.lo, s_state.hi, gtid, gthreads);
+            if (s_state.status == ST_RUNNING)
+                apply_snapshots(p, nt, nullptr, s_state.lo, s_state.hi, gtid, gthreads);
             if (!grid_barrier(p, -1)) return;
         }
     }
@@ -686,7 +743,7 @@ __global__ void begin_kernel(EngineParams p) {
 
 // Δ_0 into the snapshots (one launch after seeding).
 __global__ void seed_snapshots_kernel(EngineParams p) {
-    apply_snapshots(p, p.nt, 0, ld_volatile_u64(&p.st->hi), (long long)blockIdx.x * blockDim.x + threadIdx.x,
+    apply_snapshots(p, p.nt, nullptr, 0, ld_volatile_u64(&p.st->hi), (long long)blockIdx.x * blockDim.x + threadIdx.x,
                     (long long)gridDim.x * blockDim.x);
 }
 
