@@ -112,7 +112,10 @@ typedef struct {
     int64_t log_capacity;    /* initial capacity (cells) of the derived-cell log; 0 = auto */
     int32_t solo_threshold;  /* |Δ| at or below which one CTA runs iterations alone; -1 =
                                 auto (1024), 0 = only for an empty Δ                       */
-    int32_t reserved[7];     /* must be zero                                               */
+    int32_t record_times;    /* 1: record a device timestamp per iteration (diagnostics,
+                                cfpq_result_iteration_stats2)                              */
+    int32_t max_ctas;        /* diagnostics: limit the closure kernel's grid (0 = full)    */
+    int32_t reserved[5];     /* must be zero                                               */
 } cfpq_options;
 
 CFPQ_API void cfpq_options_default(cfpq_options* o);
@@ -167,7 +170,8 @@ CFPQ_API cfpq_status cfpq_result_lengths(cfpq_result* r, int32_t nt, uint32_t* d
  *   in single-CTA mode, [6] candidates expanded (semi-naive AND-true triples),
  *   [7] (Δ entry, rule occurrence) expansions, [8] device time of the seed phase (seed,
  *   adjacency build, snapshot seeding) in ns, [9] device time of the fixpoint-loop
- *   kernel launches in ns (CUDA events on the closure stream).
+ *   kernel launches in ns (CUDA events on the closure stream), [10] CTAs of the closure
+ *   kernel, [11..17] single-CTA phase cycle counters (only with record_times).
  * Per-iteration arrays (length = iterations) via cfpq_result_iteration_stats:
  *   new_cells[k-1] = |T_k \ T_{k-1}|, jacobi_triples[k-1] (only with account_work). */
 CFPQ_API cfpq_status cfpq_result_stats(const cfpq_result* r, int64_t* stats, int32_t n_stats);

@@ -45,7 +45,8 @@ class Options(ctypes.Structure):
                 ("max_iterations", ctypes.c_int64), ("cuda_stream", ctypes.c_void_p),
                 ("world_size", ctypes.c_int32), ("rank", ctypes.c_int32),
                 ("nccl_unique_id", ctypes.c_void_p), ("log_capacity", ctypes.c_int64),
-                ("solo_threshold", ctypes.c_int32), ("reserved", ctypes.c_int32 * 7)]
+                ("solo_threshold", ctypes.c_int32), ("record_times", ctypes.c_int32),
+                ("max_ctas", ctypes.c_int32), ("reserved", ctypes.c_int32 * 5)]
 
 
 _lib = None
@@ -178,7 +179,8 @@ class Graph:
 
 
 def options(semantics: int = 0, schedule: int = 0, path_policy: int = 0, account_work: bool = False,
-            max_iterations: int = 0, stream=None, log_capacity: int = 0, solo_threshold: int = -1) -> Options:
+            max_iterations: int = 0, stream=None, log_capacity: int = 0, solo_threshold: int = -1,
+            record_times: bool = False, max_ctas: int = 0) -> Options:
     o = Options()
     load().cfpq_options_default(ctypes.byref(o))
     o.semantics, o.schedule, o.path_policy = int(semantics), int(schedule), int(path_policy)
@@ -187,6 +189,8 @@ def options(semantics: int = 0, schedule: int = 0, path_policy: int = 0, account
     o.cuda_stream = _stream_ptr(stream)
     o.log_capacity = int(log_capacity)
     o.solo_threshold = int(solo_threshold)
+    o.record_times = int(bool(record_times))
+    o.max_ctas = int(max_ctas)
     return o
 
 
@@ -257,10 +261,11 @@ class Result:
         return buf[: w.value]
 
     def stats(self) -> dict:
-        v = (ctypes.c_int64 * 10)()
-        _check(load().cfpq_result_stats(self._h, v, 10), "cfpq_result_stats")
+        v = (ctypes.c_int64 * 18)()
+        _check(load().cfpq_result_stats(self._h, v, 18), "cfpq_result_stats")
         keys = ["iterations", "cells", "log_capacity", "regrows", "launches", "solo_iterations", "candidates",
-                "expansions", "seed_ns", "loop_ns"]
+                "expansions", "seed_ns", "loop_ns", "ctas", "prof_loop", "prof_expand", "prof_bar1",
+                "prof_close", "prof_4", "prof_head", "prof_atomic"]
         return dict(zip(keys, list(v)))
 
     def iteration_stats(self, work: bool = False) -> Tuple[np.ndarray, Optional[np.ndarray]]:

@@ -133,7 +133,7 @@ struct cfpq_result {
         p.iter_off = d_iter_off;
         p.iter_off_cap = iter_off_cap;
         p.jac = opts.account_work ? d_jac : nullptr;
-        p.iter_time = d_iter_time;
+        p.iter_time = opts.record_times ? d_iter_time : nullptr;
         p.rowc = opts.account_work ? d_rowc : nullptr;
         p.colc = opts.account_work ? d_colc : nullptr;
         p.rules = d_rules;
@@ -143,6 +143,7 @@ struct cfpq_result {
         p.solo_max = opts.solo_threshold;
         p.has_snapshots = has_snapshots;
         p.nblocks = grid;
+        p.profile = opts.record_times;
         return p;
     }
 };
@@ -405,6 +406,7 @@ static cfpq_status plan(cfpq_result* r, const cfpq_grammar* g, const cfpq_graph*
         return CFPQ_E_CUDA;
     }
     r->grid = sms * bps;
+    if (o->max_ctas > 0 && o->max_ctas < r->grid) r->grid = o->max_ctas;
     return CFPQ_OK;
 }
 
@@ -608,6 +610,7 @@ extern "C" cfpq_status cfpq_closure_reuse(const cfpq_grammar* g, const cfpq_grap
     r->opts.cuda_stream = o->cuda_stream;
     if (o->max_iterations > 0) r->opts.max_iterations = o->max_iterations;
     if (o->solo_threshold >= 0) r->opts.solo_threshold = o->solo_threshold;
+    r->opts.record_times = o->record_times;
     return run(r, d);
 }
 
@@ -644,7 +647,7 @@ static unsigned long long log_end(cfpq_result* r, int64_t k, cfpq_status* st) {
 static cfpq_status counts_upto(cfpq_result* r, unsigned long long end, std::vector<int64_t>& out) {
     cudaStream_t s = r->stream;
     CFPQ_CUDA_TRY(cudaMemsetAsync(r->d_small, 0, (r->n_nt + 2) * 8, s));
-    CFPQ_CUDA_TRY(launch_nt_histogram(r->d_log, end, r->d_small, s));
+    CFPQ_CUDA_TRY(launch_nt_histogram(r->d_log, end, r->d_small, r->n_nt, s));
     std::vector<unsigned long long> h(r->n_nt);
     CFPQ_CUDA_TRY(cudaMemcpyAsync(h.data(), r->d_small, r->n_nt * 8, cudaMemcpyDeviceToHost, s));
     CFPQ_CUDA_TRY(cudaStreamSynchronize(s));
@@ -786,10 +789,13 @@ extern "C" cfpq_status cfpq_result_lengths(cfpq_result* r, int32_t nt, uint32_t*
 
 extern "C" cfpq_status cfpq_result_stats(const cfpq_result* r, int64_t* stats, int32_t n_stats) {
     CFPQ_CHECK_ARG(r && stats, "cfpq_result_stats: NULL argument");
-    int64_t v[10] = {r->iterations, (int64_t)r->n_cells, (int64_t)r->log_cap, r->regrows, r->launches,
+    int64_t v[18] = {r->iterations, (int64_t)r->n_cells, (int64_t)r->log_cap, r->regrows, r->launches,
                      r->h_st.solo_iters, (int64_t)r->h_st.candidates, (int64_t)r->h_st.expansions,
-                     (int64_t)r->seed_ns, (int64_t)r->loop_ns};
-    for (int k = 0; k < n_stats && k < 10; ++k) stats[k] = v[k];
+                     (int64_t)r->seed_ns, (int64_t)r->loop_ns, (int64_t)r->grid,
+                     (int64_t)r->h_st.prof[0], (int64_t)r->h_st.prof[1], (int64_t)r->h_st.prof[2],
+                     (int64_t)r->h_st.prof[3], (int64_t)r->h_st.prof[4], (int64_t)r->h_st.prof[5],
+                     (int64_t)r->h_st.prof[6]};
+    for (int k = 0; k < n_stats && k < 18; ++k) stats[k] = v[k];
     return CFPQ_OK;
 }
 

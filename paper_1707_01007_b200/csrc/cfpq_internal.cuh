@@ -81,10 +81,12 @@ struct EngineState {
     unsigned long long candidates; // expanded candidates = semi-naive AND-true triples
     unsigned long long expansions; // (Δ entry, rule occurrence) pairs expanded
     long long solo_iters;          // iterations run by the single-CTA path
-    unsigned long long pad0[7];
+    unsigned long long prof[7];    // single-CTA phase cycle counters (record_times diagnostics)
     unsigned bar_count;            // grid-barrier words, on their own 128-byte line
     unsigned bar_gen;
-    unsigned pad1[30];
+    unsigned long long snap_ls[2]; // log size when iteration k closed (slot k&1)
+    int snap_flags[2];             // bit 0 overflow, bit 1 length overflow (slot k&1)
+    unsigned pad1[22];
 };
 
 enum : int { ST_RUNNING = 0, ST_DONE = 1, ST_OVERFLOW = 2, ST_CAP = 3, ST_LEN_OVERFLOW = 4 };
@@ -113,6 +115,7 @@ struct EngineParams {
     int32_t solo_max;              // |Δ| <= solo_max -> single-CTA iterations
     int32_t has_snapshots;
     int32_t nblocks;
+    int32_t profile;               // accumulate single-CTA phase cycles into EngineState::prof
 };
 
 // ------------------------------------------------------------------------------------------
@@ -168,7 +171,7 @@ int closure_kernel_blocks_per_sm();
 int closure_kernel_block_size();
 cudaError_t launch_closure(const EngineParams& p, int grid, cudaStream_t s);
 
-cudaError_t launch_nt_histogram(const uint64_t* log, unsigned long long n, unsigned long long* counts,
+cudaError_t launch_nt_histogram(const uint64_t* log, unsigned long long n, unsigned long long* counts, int n_nt,
                                 cudaStream_t s);
 cudaError_t launch_filter_nt(const uint64_t* log, unsigned long long n, uint32_t A, uint64_t* keys,
                              unsigned long long* count, cudaStream_t s);

@@ -30,7 +30,7 @@
 
 namespace cfpq {
 
-constexpr int kBlock = 512;
+constexpr int kBlock = 1024;
 constexpr int kWarps = kBlock / 32;
 constexpr int kSeedBlock = 256;
 constexpr int kBuf = 64;             // per-warp staging capacity (cells)
@@ -92,6 +92,21 @@ __device__ __forceinline__ uint64_t cell_len(const EngineParams& p, const NTInfo
     const uint64_t* K = nt[X].K;
     if (K == nullptr) return 1;
     return ldcg64(K + (size_t)i * (size_t)p.n + j) & 0xffffffffull;
+}
+
+// Warp-level deduplication of candidates: lanes holding the same cell (e.g. the hub
+// cell (owl:Class, owl:Class) reached from thousands of classes) elect the lowest lane,
+// which carries the minimum length; same-address atomics would serialise in L2.
+__device__ __forceinline__ bool warp_dedup(const EngineParams& p, const Sink& sk, bool has, uint32_t A, uint32_t i,
+                                           uint32_t j, uint64_t& len, int lane) {
+    uint64_t key = has ? pack_cell(A, i, j) : ~0ull;   // ~0 is never a cell (node ids < 2^27 - 1)
+    unsigned peers = __match_any_sync(kFull, key);
+    if (p.lengths) {
+        if (has && len > 0xffffffffull) *(volatile int*)sk.len_overflow = 1;
+        uint32_t l = (uint32_t)(len > 0xffffffffull ? 0xffffffffull : len);
+        len = __reduce_min_sync(peers, l);
+    }
+    return has && (__ffs(peers) - 1 == lane);
 }
 
 // Insert candidate (A,i,j) of length len into T_k; true iff the cell is new:
@@ -172,7 +187,8 @@ __device__ __forceinline__ void stage(const EngineParams& p, const NTInfo* nt, c
 __device__ __forceinline__ void emit(const EngineParams& p, const NTInfo* nt, const Sink& sk, WarpScratch* ws,
                                      int lane, bool has, uint32_t A, uint32_t i, uint32_t j, uint64_t len,
                                      long long k) {
-    bool d = try_insert(p, nt, sk, has, A, i, j, len, k);
+    bool keep = warp_dedup(p, sk, has, A, i, j, len, lane);
+    bool d = try_insert(p, nt, sk, keep, A, i, j, len, k);
     stage(p, nt, sk, ws, lane, d, A, i, j);
 }
 
@@ -405,8 +421,11 @@ __device__ void expand(const EngineParams& p, const NTInfo* nt, const Expansion*
         for (int x = 0; x < kPre; ++x) {
             cand_coords(efx[x], el[x].z, ci0[x], cj0[x]);
             cand_coords(efx[x], el[x].w, ci1[x], cj1[x]);
-            d0[x] = try_insert(p, nt, sk, el[x].y > 0, eA[x], ci0[x], cj0[x], (uint64_t)len_e + 1ull, k);
-            d1[x] = try_insert(p, nt, sk, el[x].y > 1, eA[x], ci1[x], cj1[x], (uint64_t)len_e + 1ull, k);
+            uint64_t l0 = (uint64_t)len_e + 1ull, l1 = l0;
+            bool k0 = warp_dedup(p, sk, el[x].y > 0, eA[x], ci0[x], cj0[x], l0, lane);
+            bool k1 = warp_dedup(p, sk, el[x].y > 1, eA[x], ci1[x], cj1[x], l1, lane);
+            d0[x] = try_insert(p, nt, sk, k0, eA[x], ci0[x], cj0[x], l0, k);
+            d1[x] = try_insert(p, nt, sk, k1, eA[x], ci1[x], cj1[x], l1, k);
             dcand += (unsigned long long)el[x].y;
         }
         bool any_tail = false;
@@ -435,8 +454,11 @@ __device__ void expand(const EngineParams& p, const NTInfo* nt, const Expansion*
             uint32_t a0, b0, a1, b1;
             cand_coords(fx, h.z, a0, b0);
             cand_coords(fx, h.w, a1, b1);
-            bool q0 = try_insert(p, nt, sk, h.y > 0, A, a0, b0, (uint64_t)len_e + 1ull, k);
-            bool q1 = try_insert(p, nt, sk, h.y > 1, A, a1, b1, (uint64_t)len_e + 1ull, k);
+            uint64_t l0 = (uint64_t)len_e + 1ull, l1 = l0;
+            bool k0 = warp_dedup(p, sk, h.y > 0, A, a0, b0, l0, lane);
+            bool k1 = warp_dedup(p, sk, h.y > 1, A, a1, b1, l1, lane);
+            bool q0 = try_insert(p, nt, sk, k0, A, a0, b0, l0, k);
+            bool q1 = try_insert(p, nt, sk, k1, A, a1, b1, l1, k);
             dcand += (unsigned long long)h.y;
             stage(p, nt, sk, ws, lane, q0, A, a0, b0);
             stage(p, nt, sk, ws, lane, q1, A, a1, b1);
@@ -528,26 +550,44 @@ struct LoopState {
     int status;
 };
 
-// Close iteration k: Δ_k = log[hi, ls).  Single thread; `s` is updated and the caller
-// publishes it (fenced) when other CTAs must see it.
-__device__ void close_iteration(const EngineParams& p, long long k, LoopState& s, unsigned long long ls, int ov,
-                                int lov) {
-    if (lov) {
+// ---- memory-model primitives for the grid barrier (release/acquire at gpu scope) ----
+__device__ __forceinline__ unsigned atom_add_acq_rel(unsigned* p, unsigned v) {
+    unsigned old;
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+    return old;
+}
+__device__ __forceinline__ void red_add_release(unsigned* p, unsigned v) {
+    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void fence_acq_rel() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+
+// Close iteration k from the log size `ls` and the error flags: Δ_k = log[hi, ls).
+// Every CTA runs this on identical inputs and reaches the identical state.
+__device__ __forceinline__ void close_iteration(const EngineParams& p, long long k, LoopState& s, unsigned long long ls,
+                                                int flags, bool record) {
+    if (flags & 2) {
         s.status = ST_LEN_OVERFLOW;
         return;
     }
-    if (ov) {
+    if (flags & 1) {
         s.status = ST_OVERFLOW;   // keep lo/hi/iter: the host grows the log and re-runs k
         return;
     }
     s.lo = s.hi;
     s.hi = ls;
     s.iter = k;
-    if (k < p.iter_off_cap) {
-        p.iter_off[k] = s.lo;
-        if (p.iter_time) p.iter_time[k] = globaltimer();
+    if (record) {
+        if (k < p.iter_off_cap) {
+            p.iter_off[k] = s.lo;
+            if (p.iter_time) p.iter_time[k] = globaltimer();
+        }
+        if (k + 1 < p.iter_off_cap) p.iter_off[k + 1] = ls;
     }
-    if (k + 1 < p.iter_off_cap) p.iter_off[k + 1] = ls;
     if (ls == s.lo) s.status = ST_DONE;             // T_k = T_{k-1}: fixpoint
     else if (k >= p.max_iter) s.status = ST_CAP;    // Theorem 3 cap
 }
@@ -557,142 +597,320 @@ __device__ void publish(const EngineParams& p, const LoopState& s) {
     st->lo = s.lo;
     st->hi = s.hi;
     st->iter = s.iter;
-    *(volatile int*)&st->status = s.status;
-    __threadfence();
+    st->status = s.status;
+    fence_acq_rel();
 }
 
-// Grid barrier; the last CTA to arrive closes iteration k (if k >= 0) before release.
+// Grid barrier (generation counter, release/acquire).  If k >= 0 the last CTA to
+// arrive snapshots the log size and error flags of iteration k into slot k&1 before
+// releasing, so every CTA can close the iteration locally afterwards.
 __device__ bool grid_barrier(const EngineParams& p, long long k) {
-    __syncthreads();
     __shared__ int s_timeout;
+    __syncthreads();
     if (threadIdx.x == 0) {
         s_timeout = 0;
         EngineState* st = p.st;
-        volatile unsigned* gen = &st->bar_gen;
-        unsigned my = *gen;
-        __threadfence();
-        unsigned arrived = atomicAdd(&st->bar_count, 1u);
+        unsigned my = *(volatile unsigned*)&st->bar_gen;
+        unsigned arrived = atom_add_acq_rel(&st->bar_count, 1u);
         if (arrived == (unsigned)p.nblocks - 1u) {
             if (k >= 0) {
-                LoopState s;
-                s.lo = ld_volatile_u64(&st->lo);
-                s.hi = ld_volatile_u64(&st->hi);
-                s.iter = *(volatile long long*)&st->iter;
-                s.status = *(volatile int*)&st->status;
-                close_iteration(p, k, s, ld_volatile_u64(&st->log_size), *(volatile int*)&st->overflow,
-                                *(volatile int*)&st->len_overflow);
-                publish(p, s);
+                int f = (*(volatile int*)&st->overflow ? 1 : 0) | (*(volatile int*)&st->len_overflow ? 2 : 0);
+                st->snap_ls[k & 1] = ld_volatile_u64(&st->log_size);
+                st->snap_flags[k & 1] = f;
             }
             st->bar_count = 0u;
-            __threadfence();
-            atomicAdd(&st->bar_gen, 1u);
+            red_add_release(&st->bar_gen, 1u);
         } else {
             long long t0 = clock64();
-            while (*gen == my) {
-                __nanosleep(64);
+            unsigned ns = 0;
+            while (ld_acquire_u32(&st->bar_gen) == my) {
+                if (ns) __nanosleep(ns);
+                ns = ns ? (ns < 2048u ? ns * 2u : 2048u) : 32u;   // exponential backoff, <= ~2 µs
                 if (clock64() - t0 > 60000000000ll) {   // ~30 s watchdog: never hang the GPU
                     s_timeout = 1;
                     break;
                 }
             }
         }
-        __threadfence();
     }
     __syncthreads();
     return s_timeout == 0;
 }
 
-__global__ void __launch_bounds__(kBlock, 2) closure_kernel(EngineParams p) {
-    __shared__ WarpScratch ws[kWarps];
-    __shared__ NTInfo s_nt[kSmemNT];
-    __shared__ Expansion s_exp[kSmemExp];
-    __shared__ uint64_t s_delta[2][kSoloMax];
-    __shared__ LoopState s_state;
-    __shared__ unsigned long long s_ls;
-    __shared__ int s_ov, s_lov;
-    __shared__ long long s_solo;
+// Single-CTA iterations (|Δ| <= solo_max): one thread per Δ entry, Δ mirrored in
+// shared memory, appends counted in shared memory.  Counters and error flags rotate
+// over three slots (k mod 3) so that ONE __syncthreads() per iteration suffices: every
+// thread reads slot k after the barrier and closes the iteration itself; slot k+1 is
+// reset by thread 0 during iteration k, after every thread has read it (at iteration
+// k-2's close, before the barrier of k-1).
+struct SoloShared {
+    uint64_t delta[2][kSoloMax];
+    unsigned cnt[3];
+    int ov[3], lov[3];
+    long long solo;
+};
+
+__device__ __forceinline__ void solo_append(const EngineParams& p, const NTInfo* nt, SoloShared& so, int slot,
+                                            unsigned long long base, uint64_t* mirror, uint32_t A, uint32_t i,
+                                            uint32_t j) {
+    unsigned long long idx = base + atomicAdd(&so.cnt[slot], 1u);
+    uint64_t c = pack_cell(A, i, j);
+    uint64_t* K = p.lengths ? nt[A].K : nullptr;
+    uint32_t* word = nt[A].T + (size_t)i * (size_t)p.Wp + (j >> 5);
+    uint32_t bit = 1u << (j & 31);
+    if (idx < p.log_cap) {
+        p.log[idx] = c;
+        if (idx - base < (unsigned long long)kSoloMax) mirror[idx - base] = c;
+        if (K != nullptr) atomicOr(word, bit);
+        if (p.rowc != nullptr) {
+            atomicAdd(p.rowc + (size_t)A * p.n + i, 1u);
+            atomicAdd(p.colc + (size_t)A * p.n + j, 1u);
+        }
+    } else {
+        if (K != nullptr) atomicExch((unsigned long long*)(K + (size_t)i * (size_t)p.n + j), (unsigned long long)kEmptyKey);
+        else atomicAnd(word, ~bit);
+        so.ov[slot] = 1;
+    }
+}
+
+// Issue the bit/key atomic of a candidate; returns whether the cell is new.
+__device__ __forceinline__ bool solo_try(const EngineParams& p, const NTInfo* nt, SoloShared& so, int slot, uint32_t A,
+                                         uint32_t i, uint32_t j, uint64_t len, long long k) {
+    uint64_t* K = nt[A].K;
+    if (p.lengths && K != nullptr) {
+        if (len > 0xffffffffull) {
+            so.lov[slot] = 1;
+            len = 0xffffffffull;
+        }
+        uint64_t old = atomicMin((unsigned long long*)(K + (size_t)i * (size_t)p.n + j),
+                                 (unsigned long long)(((uint64_t)k << 32) | len));
+        return old == kEmptyKey;
+    }
+    uint32_t bit = 1u << (j & 31);
+    return !(atomicOr(nt[A].T + (size_t)i * (size_t)p.Wp + (j >> 5), bit) & bit);
+}
+
+// Prefetch into L1 the ELL head that the next iteration reads for candidate (A,i,j)
+// if it becomes new (its first two rule occurrences); overlaps with the bit atomic.
+__device__ __forceinline__ void prefetch_next(const NTInfo* nt, const Expansion* exps, uint32_t A, uint32_t i,
+                                              uint32_t j) {
+    int eb = nt[A].exp_begin, ee = nt[A].exp_end;
+    for (int x = eb; x < ee && x < eb + 2; ++x) {
+        Expansion ex = exps[x];
+        const int4* a = nullptr;
+        if (ex.kind == EXP_L_CONST) a = nt[ex.other].csr_ell + j;
+        else if (ex.kind == EXP_R_CONST) a = nt[ex.other].csc_ell + i;
+        if (a) asm volatile("prefetch.global.L1 [%0];" ::"l"(a));
+    }
+}
+
+__device__ void solo_expand(const EngineParams& p, const NTInfo* nt, const Expansion* exps, SoloShared& so,
+                            const uint64_t* src, unsigned long long lo, unsigned long long hi, long long k, int slot,
+                            uint64_t* mirror, unsigned long long& dcand, unsigned long long& dexp,
+                            long long* pacc = nullptr) {
+    long long t0 = pacc ? clock64() : 0;
+    for (unsigned long long e = lo + threadIdx.x; e < hi; e += kBlock) {
+        uint64_t cell = src ? src[e - lo] : ldcg64(p.log + e);
+        uint32_t X = cell_nt(cell), ci = cell_i(cell), cj = cell_j(cell);
+        int eb = nt[X].exp_begin, ee = nt[X].exp_end;
+        dexp += (unsigned long long)(ee - eb);
+        uint64_t len_e = (p.lengths && ee > eb) ? cell_len(p, nt, X, ci, cj) : 0;
+        for (int x = eb; x < ee; ++x) {
+            Expansion ex = exps[x];
+            if (ex.kind == EXP_L_CONST || ex.kind == EXP_R_CONST) {
+                uint32_t A, fx;
+                int4 h = load_head(nt, ex, ci, cj, A, fx);
+                dcand += (unsigned long long)h.y;
+                uint32_t a0, b0, a1, b1;
+                cand_coords(fx, h.z, a0, b0);
+                cand_coords(fx, h.w, a1, b1);
+                if (pacc) {
+                    long long t = clock64() + (h.y < -1 ? 1 : 0);   // depends on the head: waits for it
+                    pacc[5] += t - t0;
+                    t0 = t;
+                }
+                bool n0 = h.y > 0 && solo_try(p, nt, so, slot, A, a0, b0, len_e + 1, k);
+                bool n1 = h.y > 1 && solo_try(p, nt, so, slot, A, a1, b1, len_e + 1, k);
+                if (pacc) {
+                    long long t = clock64() + (n0 ? 1 : 0) + (n1 ? 1 : 0);
+                    pacc[6] += t - t0;
+                    t0 = t;
+                }
+                if (h.y > 0) prefetch_next(nt, exps, A, a0, b0);
+                if (h.y > 1) prefetch_next(nt, exps, A, a1, b1);
+                if (n0) solo_append(p, nt, so, slot, hi, mirror, A, a0, b0);
+                if (n1) solo_append(p, nt, so, slot, hi, mirror, A, a1, b1);
+                for (int t = 2; t < h.y; ++t) {
+                    uint32_t a, b;
+                    cand_coords(fx, __ldg(p.adj_idx + h.x + t), a, b);
+                    if (solo_try(p, nt, so, slot, A, a, b, len_e + 1, k)) solo_append(p, nt, so, slot, hi, mirror, A, a, b);
+                }
+            } else {
+                const bool left = ex.kind == EXP_L_VAR;
+                const uint32_t* row = left ? nt[ex.other].S + (size_t)cj * p.Wp : nt[ex.other].ST + (size_t)ci * p.Wp;
+                const int64_t wn = (p.n + 31) >> 5;
+                for (int64_t w = 0; w < wn; ++w) {
+                    uint32_t bits = ldcg32(row + w);
+                    while (bits) {
+                        int b = __ffs(bits) - 1;
+                        bits &= bits - 1u;
+                        uint32_t v = (uint32_t)(w * 32 + b);
+                        uint32_t oi = left ? ci : v, oj = left ? v : cj;
+                        uint64_t clen = 0;
+                        if (p.lengths)
+                            clen = left ? len_e + cell_len(p, nt, ex.other, cj, v) : cell_len(p, nt, ex.other, v, ci) + len_e;
+                        ++dcand;
+                        if (solo_try(p, nt, so, slot, (uint32_t)ex.A, oi, oj, clen, k))
+                            solo_append(p, nt, so, slot, hi, mirror, (uint32_t)ex.A, oi, oj);
+                    }
+                }
+            }
+        }
+    }
+}
+
+// Dynamic shared memory of the closure kernel.
+struct ClosureShared {
+    WarpScratch ws[kWarps];
+    NTInfo nt[kSmemNT];
+    Expansion exp[kSmemExp];
+    SoloShared solo;
+    LoopState state;
+};
+
+__global__ void __launch_bounds__(kBlock, 1) closure_kernel(EngineParams p) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    ClosureShared& S = *reinterpret_cast<ClosureShared*>(smem_raw);
     const int lane = threadIdx.x & 31;
     const int wib = threadIdx.x >> 5;
     EngineState* st = p.st;
-    // NT / expansion tables into shared memory (fences invalidate L1 every iteration)
+    // NT / expansion tables into shared memory (loads stay on-chip across iterations)
     const bool small = p.n_nt <= kSmemNT && p.n_exps <= kSmemExp;
     if (small) {
-        for (int t = threadIdx.x; t < p.n_nt; t += kBlock) s_nt[t] = p.nt[t];
-        for (int t = threadIdx.x; t < p.n_exps; t += kBlock) s_exp[t] = p.exps[t];
+        for (int t = threadIdx.x; t < p.n_nt; t += kBlock) S.nt[t] = p.nt[t];
+        for (int t = threadIdx.x; t < p.n_exps; t += kBlock) S.exp[t] = p.exps[t];
     }
-    const NTInfo* nt = small ? s_nt : p.nt;
-    const Expansion* exps = small ? s_exp : p.exps;
+    const NTInfo* nt = small ? S.nt : p.nt;
+    const Expansion* exps = small ? S.exp : p.exps;
     const Sink gsink = global_sink(p);
-    if (lane == 0) ws[wib].nbuf = 0;
-    if (threadIdx.x == 0) s_solo = 0;
+    if (lane == 0) S.ws[wib].nbuf = 0;
+    if (threadIdx.x == 0) {
+        S.solo.solo = 0;
+        S.state.lo = ld_volatile_u64(&st->lo);
+        S.state.hi = ld_volatile_u64(&st->hi);
+        S.state.iter = *(volatile long long*)&st->iter;
+        S.state.status = *(volatile int*)&st->status;
+    }
     __syncthreads();
+    LoopState s = S.state;   // identical in every CTA
     unsigned long long dcand = 0, dexp = 0;
-    for (;;) {
-        if (threadIdx.x == 0) {
-            s_state.lo = ld_volatile_u64(&st->lo);
-            s_state.hi = ld_volatile_u64(&st->hi);
-            s_state.iter = *(volatile long long*)&st->iter;
-            s_state.status = *(volatile int*)&st->status;
-        }
-        __syncthreads();
-        LoopState s = s_state;
-        __syncthreads();
-        if (s.status != ST_RUNNING) break;
+    bool aborted = false;
+    while (s.status == ST_RUNNING) {
         long long k = s.iter + 1;
         if ((long long)(s.hi - s.lo) <= (long long)p.solo_max) {
-            // ------------- single-CTA iterations: Δ, counter and flags in shared memory -------------
+            // ------------- single-CTA iterations (see SoloShared) -------------
             if (blockIdx.x == 0) {
+                SoloShared& so = S.solo;
                 int cur = 0;
-                if (threadIdx.x == 0) {
-                    s_ls = ld_volatile_u64(&st->log_size);
-                    s_ov = 0;
-                    s_lov = 0;
-                }
+                const unsigned long long ls0 = ld_volatile_u64(&st->log_size);
                 if (s.hi - s.lo <= (unsigned long long)kSoloMax)
                     for (unsigned long long e = s.lo + threadIdx.x; e < s.hi; e += kBlock)
-                        s_delta[cur][e - s.lo] = ldcg64(p.log + e);
+                        so.delta[cur][e - s.lo] = ldcg64(p.log + e);
+                {
+                    // cells of Δ_k appended before a log-overflow re-run of iteration k
+                    unsigned long long end = ls0 < s.hi + kSoloMax ? ls0 : s.hi + kSoloMax;
+                    for (unsigned long long e = s.hi + threadIdx.x; e < end; e += kBlock)
+                        so.delta[cur ^ 1][e - s.hi] = ldcg64(p.log + e);
+                }
+                if (threadIdx.x == 0) {
+                    for (int q = 0; q < 3; ++q) {
+                        so.cnt[q] = 0u;
+                        so.ov[q] = 0;
+                        so.lov[q] = 0;
+                    }
+                    so.cnt[k % 3] = (unsigned)(ls0 - s.hi);
+                }
                 __syncthreads();
+                unsigned long long last_ls = ls0;
+                long long tp = clock64();
+                long long pacc[7] = {0, 0, 0, 0, 0, 0, 0};
+                const bool prof = p.profile && threadIdx.x == 0;
+                int slot = (int)(k % 3);
                 for (;;) {
+                    const int nx = slot == 2 ? 0 : slot + 1;
                     if (p.jac) {
                         account(p, k, threadIdx.x, kBlock);
                         __syncthreads();
                     }
-                    Sink sk;
-                    sk.counter = &s_ls;
-                    sk.overflow = &s_ov;
-                    sk.len_overflow = &s_lov;
-                    sk.mirror = s_delta[cur ^ 1];
-                    sk.mirror_base = s.hi;
-                    sk.mirror_cap = kSoloMax;
-                    const uint64_t* src = (s.hi - s.lo <= (unsigned long long)kSoloMax) ? s_delta[cur] : nullptr;
-                    expand(p, nt, exps, sk, src, s.lo, s.hi, k, wib, kWarps, lane, &ws[wib], dcand, dexp);
-                    __syncthreads();
+                    if (prof) {
+                        long long t = clock64();
+                        pacc[0] += t - tp;   // loop overhead
+                        tp = t;
+                    }
+                    const uint64_t* src = (s.hi - s.lo <= (unsigned long long)kSoloMax) ? so.delta[cur] : nullptr;
+                    solo_expand(p, nt, exps, so, src, s.lo, s.hi, k, slot, so.delta[cur ^ 1], dcand, dexp,
+                                prof ? pacc : nullptr);
                     if (threadIdx.x == 0) {
-                        close_iteration(p, k, s_state, s_ls, s_ov, s_lov);
-                        s_solo += 1;
+                        so.cnt[nx] = 0u;
+                        so.ov[nx] = 0;
+                        so.lov[nx] = 0;
+                        so.solo += 1;
+                    }
+                    if (prof) {
+                        long long t = clock64();
+                        pacc[1] += t - tp;   // expand (thread 0's share)
+                        tp = t;
                     }
                     __syncthreads();
-                    s = s_state;
+                    if (prof) {
+                        long long t = clock64();
+                        pacc[2] += t - tp;   // the barrier
+                        tp = t;
+                    }
+                    const unsigned long long ls = s.hi + so.cnt[slot];
+                    const int f = (so.ov[slot] ? 1 : 0) | (so.lov[slot] ? 2 : 0);
+                    last_ls = ls;
+                    close_iteration(p, k, s, ls, f, threadIdx.x == 0);
+                    if (prof) {
+                        long long t = clock64();
+                        pacc[3] += t - tp;   // close
+                        tp = t;
+                    }
                     if (s.status != ST_RUNNING) break;
                     cur ^= 1;
                     if (p.has_snapshots) {
-                        const uint64_t* sn = (s.hi - s.lo <= (unsigned long long)kSoloMax) ? s_delta[cur] : nullptr;
+                        const uint64_t* sn = (s.hi - s.lo <= (unsigned long long)kSoloMax) ? so.delta[cur] : nullptr;
                         apply_snapshots(p, nt, sn, s.lo, s.hi, threadIdx.x, kBlock);
                         __syncthreads();
                     }
                     ++k;
+                    slot = nx;
                     if ((long long)(s.hi - s.lo) > (long long)p.solo_max) break;
                 }
+                if (prof)
+                    for (int q = 0; q < 7; ++q) st->prof[q] += pacc[q];
                 if (threadIdx.x == 0) {
-                    st->log_size = s_ls;   // the other CTAs are parked at the grid barrier
-                    if (s_ov) st->overflow = 1;
-                    if (s_lov) st->len_overflow = 1;
-                    publish(p, s_state);
-                    atomicAdd((unsigned long long*)&st->solo_iters, (unsigned long long)s_solo);
-                    s_solo = 0;
+                    st->log_size = last_ls;   // the other CTAs are parked at the grid barrier
+                    if (so.ov[slot]) st->overflow = 1;
+                    if (so.lov[slot]) st->len_overflow = 1;
+                    atomicAdd((unsigned long long*)&st->solo_iters, (unsigned long long)so.solo);
+                    so.solo = 0;
+                    publish(p, s);
                 }
             }
-            if (!grid_barrier(p, -1)) return;
+            if (!grid_barrier(p, -1)) {
+                aborted = true;
+                break;
+            }
+            if (threadIdx.x == 0) {
+                S.state.lo = ld_volatile_u64(&st->lo);
+                S.state.hi = ld_volatile_u64(&st->hi);
+                S.state.iter = *(volatile long long*)&st->iter;
+                S.state.status = *(volatile int*)&st->status;
+            }
+            __syncthreads();
+            s = S.state;
+            __syncthreads();
             continue;
         }
         // ---------------- grid-wide iteration k ----------------
@@ -700,23 +918,42 @@ __global__ void __launch_bounds__(kBlock, 2) closure_kernel(EngineParams p) {
         const long long gthreads = (long long)gridDim.x * kBlock;
         if (p.jac) {
             account(p, k, gtid, gthreads);
-            if (!grid_barrier(p, -1)) return;
+            if (!grid_barrier(p, -1)) {
+                aborted = true;
+                break;
+            }
         }
         expand(p, nt, exps, gsink, nullptr, s.lo, s.hi, k, blockIdx.x * kWarps + wib, gridDim.x * kWarps, lane,
-               &ws[wib], dcand, dexp);
-        if (!grid_barrier(p, k)) return;
-        if (p.has_snapshots) {
-            if (threadIdx.x == 0) {
-                s_state.lo = ld_volatile_u64(&st->lo);
-                s_state.hi = ld_volatile_u64(&st->hi);
-                s_state.status = *(volatile int*)&st->status;
+               &S.ws[wib], dcand, dexp);
+        if (!grid_barrier(p, k)) {
+            aborted = true;
+            break;
+        }
+        if (threadIdx.x == 0) {
+            LoopState t = s;
+            close_iteration(p, k, t, ld_volatile_u64(&st->snap_ls[k & 1]), *(volatile int*)&st->snap_flags[k & 1],
+                            blockIdx.x == 0);
+            S.state = t;
+        }
+        __syncthreads();
+        LoopState prev = s;
+        s = S.state;
+        __syncthreads();
+        if (s.status == ST_OVERFLOW || s.status == ST_LEN_OVERFLOW) {
+            // keep the pre-iteration range for the host's re-run
+            s.lo = prev.lo;
+            s.hi = prev.hi;
+            s.iter = prev.iter;
+        }
+        if (p.has_snapshots && s.status == ST_RUNNING) {
+            apply_snapshots(p, nt, nullptr, s.lo, s.hi, gtid, gthreads);
+            if (!grid_barrier(p, -1)) {
+                aborted = true;
+                break;
             }
-            __syncthreads();
-            if (s_state.status == ST_RUNNING)
-                apply_snapshots(p, nt, nullptr, s_state.lo, s_state.hi, gtid, gthreads);
-            if (!grid_barrier(p, -1)) return;
         }
     }
+    if (!aborted && blockIdx.x == 0 && threadIdx.x == 0) publish(p, s);
     // diagnostics: one atomic per warp per launch
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -728,6 +965,8 @@ __global__ void __launch_bounds__(kBlock, 2) closure_kernel(EngineParams p) {
         if (dexp) atomicAdd(&st->expansions, dexp);
     }
 }
+
+size_t closure_kernel_smem() { return sizeof(ClosureShared); }
 
 // After seeding: Δ_0 = log[0, log_size) (T_0), iteration 0 complete.
 __global__ void begin_kernel(EngineParams p) {
@@ -806,13 +1045,17 @@ int closure_kernel_block_size() { return kBlock; }
 
 int closure_kernel_blocks_per_sm() {
     int nb = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, closure_kernel, kBlock, 0) != cudaSuccess) return 0;
+    const size_t smem = sizeof(ClosureShared);
+    if (cudaFuncSetAttribute(closure_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+        return 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, closure_kernel, kBlock, smem) != cudaSuccess) return 0;
     return nb;
 }
 
 cudaError_t launch_closure(const EngineParams& p, int grid, cudaStream_t s) {
     void* args[] = {(void*)&p};
-    return cudaLaunchCooperativeKernel((const void*)closure_kernel, dim3(grid), dim3(kBlock), args, 0, s);
+    return cudaLaunchCooperativeKernel((const void*)closure_kernel, dim3(grid), dim3(kBlock), args,
+                                       sizeof(ClosureShared), s);
 }
 
 }  // namespace cfpq

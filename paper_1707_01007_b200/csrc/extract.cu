@@ -6,12 +6,20 @@
 
 namespace cfpq {
 
+// Per-NT cell counts: block-private shared-memory histogram, one global atomic per
+// (block, NT) — a single global counter per NT serialises millions of atomics.
 __global__ void nt_histogram_kernel(const uint64_t* __restrict__ log, unsigned long long n,
-                                    unsigned long long* counts) {
+                                    unsigned long long* counts, int n_nt) {
+    extern __shared__ unsigned int hist[];
+    for (int t = threadIdx.x; t < n_nt; t += blockDim.x) hist[t] = 0u;
+    __syncthreads();
     for (unsigned long long e = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; e < n;
          e += (unsigned long long)gridDim.x * blockDim.x) {
-        atomicAdd(counts + cell_nt(__ldg((const unsigned long long*)log + e)), 1ull);
+        atomicAdd(hist + cell_nt(__ldg((const unsigned long long*)log + e)), 1u);
     }
+    __syncthreads();
+    for (int t = threadIdx.x; t < n_nt; t += blockDim.x)
+        if (hist[t]) atomicAdd(counts + t, (unsigned long long)hist[t]);
 }
 
 __global__ void filter_nt_kernel(const uint64_t* __restrict__ log, unsigned long long n, uint32_t A,
@@ -53,9 +61,9 @@ static int grid_for(unsigned long long work) {
     return (int)g;
 }
 
-cudaError_t launch_nt_histogram(const uint64_t* log, unsigned long long n, unsigned long long* counts,
+cudaError_t launch_nt_histogram(const uint64_t* log, unsigned long long n, unsigned long long* counts, int n_nt,
                                 cudaStream_t s) {
-    if (n) nt_histogram_kernel<<<grid_for(n), 256, 0, s>>>(log, n, counts);
+    if (n) nt_histogram_kernel<<<grid_for(n), 256, n_nt * sizeof(unsigned int), s>>>(log, n, counts, n_nt);
     return cudaGetLastError();
 }
 

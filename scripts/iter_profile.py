@@ -12,9 +12,9 @@ w = {"config4": lambda: I.config4_workload(), "config3": lambda: I.anbn_workload
 g = C.Grammar.from_workload(w)
 d = C.Graph(w.n_nodes, torch.from_numpy(w.edges).cuda())
 for solo in solos:
-    r = C.closure(g, d, solo_threshold=solo)
+    r = C.closure(g, d, solo_threshold=solo, record_times=True)
     for _ in range(3):
-        C.closure_reuse(g, d, r, solo_threshold=solo)
+        C.closure_reuse(g, d, r, solo_threshold=solo, record_times=True)
     st = r.stats()
     nc, _ = r.iteration_stats()
     t = r.iteration_times()
@@ -28,3 +28,6 @@ for solo in solos:
     else:
         dt = np.diff(np.concatenate([[0], t])) / 1e3
         print("  per-iter us: median", np.median(dt), "mean", dt.mean(), "max", dt.max())
+    r2 = C.closure(g, d, solo_threshold=solo)
+    C.closure_reuse(g, d, r2, solo_threshold=solo)
+    print(f"  without timestamps: loop_ms={r2.stats()['loop_ns']/1e6:.3f}")
