@@ -105,6 +105,14 @@ struct cfpq_result {
     std::vector<int64_t> counts;
     bool counts_valid = false;
     bool ran = false;
+    // dense (tcgen05) engine state
+    bool dense_mode = false;
+    DenseEngine* dense = nullptr;
+    uint32_t* d_Tn = nullptr;                 // second bit-matrix buffer of the outputs
+    std::vector<uint32_t*> Tbase, Tcur, Tnxt;  // per NT
+    std::vector<int64_t> dense_new;           // new cells per iteration
+    int32_t* d_rowcnt = nullptr;              // bitmap extraction scratch [n+1]
+    int32_t* d_rowoff = nullptr;
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
     double seed_ns = 0, loop_ns = 0;
 
@@ -115,7 +123,8 @@ struct cfpq_result {
         dfree(d_lab_ptr); dfree(d_lab_nt); dfree(d_slot_row); dfree(d_slot_col); dfree(d_adj_cnt);
         dfree(d_adj_ptr); dfree(d_adj_cursor); dfree(d_adj_idx); dfree(d_adj_ell); dfree(d_log); dfree(d_st);
         dfree(d_iter_off); dfree(d_jac); dfree(d_iter_time); dfree(d_rowc); dfree(d_colc); dfree(d_temp); dfree(d_keys);
-        dfree(d_small);
+        dfree(d_small); dfree(d_Tn); dfree(d_rowcnt); dfree(d_rowoff);
+        if (dense) dense_destroy(dense);
     }
 
     EngineParams params() const {
@@ -397,6 +406,22 @@ static cfpq_status plan(cfpq_result* r, const cfpq_grammar* g, const cfpq_graph*
     r->temp_bytes = std::max<size_t>(tb, 1 << 16);
     if ((st = dalloc((uint8_t**)&r->d_temp, r->temp_bytes, "temp")) != CFPQ_OK) return st;
 
+    r->Tbase.assign(g->n_nt, nullptr);
+    for (int A = 0; A < g->n_nt; ++A) r->Tbase[A] = r->h_nt[A].T;
+    if (o->path_policy == 2) {
+        r->dense_mode = true;
+        std::string err;
+        r->dense = dense_create((int32_t)n, g->n_nt, r->Wp, g->rules, g->is_const, r->stream, &err);
+        if (!r->dense) {
+            set_error(err);
+            return CFPQ_E_CUDA;
+        }
+        int n_out = (int)dense_outputs(r->dense).size();
+        if ((st = dalloc(&r->d_Tn, mat_words * std::max(n_out, 1), "dense next bit matrices")) != CFPQ_OK) return st;
+        CFPQ_CUDA_TRY(cudaMemsetAsync(r->d_Tn, 0, mat_words * std::max(n_out, 1) * 4, r->stream));
+    }
+    if ((st = dalloc(&r->d_rowcnt, (size_t)n + 1, "row counts")) != CFPQ_OK) return st;
+    if ((st = dalloc(&r->d_rowoff, (size_t)n + 1, "row offsets")) != CFPQ_OK) return st;
     int dev = 0, sms = 0;
     CFPQ_CUDA_TRY(cudaGetDevice(&dev));
     CFPQ_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
@@ -451,6 +476,64 @@ static cfpq_status grow_log(cfpq_result* r, unsigned long long reached) {
     return CFPQ_OK;
 }
 
+// Dense engine loop (path_policy 2): host-driven Jacobi iterations, one tcgen05 product
+// launch (+ packs) per iteration; T and Tn swap roles after every iteration.
+static cfpq_status run_dense(cfpq_result* r) {
+    cudaStream_t s = r->stream;
+    // seeding is done; Δ_0 is in the log
+    CFPQ_CUDA_TRY(cudaMemcpyAsync(&r->h_st, r->d_st, sizeof(EngineState), cudaMemcpyDeviceToHost, s));
+    CFPQ_CUDA_TRY(cudaStreamSynchronize(s));
+    if (r->h_st.bad_edge) {
+        set_error("graph has an edge with a node id >= n_nodes or a label id >= n_labels");
+        return CFPQ_E_INVAL;
+    }
+    r->n_cells = std::min<unsigned long long>(r->h_st.log_size, r->log_cap);
+    const auto& outs = dense_outputs(r->dense);
+    r->Tcur = r->Tbase;
+    r->Tnxt.assign(r->n_nt, nullptr);
+    const size_t mw = (size_t)r->n * (size_t)r->Wp;
+    for (size_t q = 0; q < outs.size(); ++q) r->Tnxt[outs[q]] = r->d_Tn + q * mw;
+    r->dense_new.clear();
+    int64_t k = 0;
+    bool capped = false;
+    cudaEvent_t e0 = r->ev[2], e1 = r->ev[3];
+    CFPQ_CUDA_TRY(cudaEventRecord(e0, s));
+    for (;;) {
+        ++k;
+        unsigned long long nw = 0;
+        int launches = 0;
+        CFPQ_CUDA_TRY(dense_step(r->dense, r->Tcur.data(), r->Tnxt.data(), k == 1, s, &nw, nullptr, &launches));
+        r->launches += launches;
+        r->dense_new.push_back((int64_t)nw);
+        for (int A : outs) std::swap(r->Tcur[A], r->Tnxt[A]);
+        if (nw == 0) break;   // T_k = T_{k-1}
+        if (k >= r->opts.max_iterations) {
+            capped = true;
+            break;
+        }
+    }
+    CFPQ_CUDA_TRY(cudaEventRecord(e1, s));
+    CFPQ_CUDA_TRY(cudaEventSynchronize(e1));
+    {
+        float ms = 0;
+        CFPQ_CUDA_TRY(cudaEventElapsedTime(&ms, r->ev[0], r->ev[1]));
+        r->seed_ns = ms * 1e6;
+        CFPQ_CUDA_TRY(cudaEventElapsedTime(&ms, e0, e1));
+        r->loop_ns = ms * 1e6;
+    }
+    r->iterations = k;
+    for (int A = 0; A < r->n_nt; ++A) r->h_nt[A].T = r->Tcur[A];
+    CFPQ_CUDA_TRY(cudaMemcpyAsync(r->d_nt, r->h_nt.data(), r->n_nt * sizeof(NTInfo), cudaMemcpyHostToDevice, s));
+    CFPQ_CUDA_TRY(cudaStreamSynchronize(s));
+    r->h_st.iter = k;
+    r->h_st.status = capped ? ST_CAP : ST_DONE;
+    if (capped) {
+        set_error("max_iterations reached before the fixpoint");
+        return CFPQ_E_NOT_CONVERGED;
+    }
+    return CFPQ_OK;
+}
+
 static cfpq_status run(cfpq_result* r, const cfpq_graph* d) {
     cudaStream_t s = r->stream;
     r->launches = 0;
@@ -458,6 +541,16 @@ static cfpq_status run(cfpq_result* r, const cfpq_graph* d) {
     cfpq_status st = size_for_graph(r, d);
     if (st != CFPQ_OK) return st;
     EngineParams p = r->params();
+    if (r->dense_mode && r->ran) {
+        // the dense engine rewrites whole matrices: restore the base buffers and clear them
+        for (int A = 0; A < r->n_nt; ++A) r->h_nt[A].T = r->Tbase[A];
+        CFPQ_CUDA_TRY(cudaMemcpyAsync(r->d_nt, r->h_nt.data(), r->n_nt * sizeof(NTInfo), cudaMemcpyHostToDevice, s));
+        const size_t mw = (size_t)r->n * (size_t)r->Wp;
+        CFPQ_CUDA_TRY(cudaMemsetAsync(r->d_T, 0, mw * r->n_nt * 4, s));
+        CFPQ_CUDA_TRY(cudaMemsetAsync(r->d_Tn, 0, mw * std::max<size_t>(dense_outputs(r->dense).size(), 1) * 4, s));
+        r->n_cells = 0;
+        p = r->params();
+    }
     // clear what a previous run derived (bitmaps, snapshots, keys, counters): O(|log|)
     if (r->ran && r->n_cells) {
         CFPQ_CUDA_TRY(launch_clear_log(p, r->n_cells, s));
@@ -495,6 +588,7 @@ static cfpq_status run(cfpq_result* r, const cfpq_graph* d) {
         r->launches++;
     }
     CFPQ_CUDA_TRY(cudaEventRecord(r->ev[1], s));
+    if (r->dense_mode) return run_dense(r);
     // a2-a5: the fixpoint loop, device-resident
     bool first = true;
     for (;;) {
@@ -567,8 +661,12 @@ static cfpq_status check_inputs(const cfpq_grammar* g, const cfpq_graph* d, cons
     CFPQ_CHECK_ARG(o->semantics == 0 || o->semantics == 1, "cfpq_closure: semantics must be 0 or 1");
     CFPQ_CHECK_ARG(o->schedule == 0 || o->schedule == 1, "cfpq_closure: schedule must be 0 (jacobi) or 1 (seminaive)");
     CFPQ_CHECK_ARG(o->world_size <= 1, "cfpq_closure: world_size > 1 is not supported by this build");
-    if (o->path_policy == 2 || o->path_policy == 3) {
-        set_error("cfpq_closure: path_policy 2 (tensor) / 3 (rows) not available in this build");
+    if (o->path_policy == 3) {
+        set_error("cfpq_closure: path_policy 3 (rows) not available in this build");
+        return CFPQ_E_UNSUPPORTED;
+    }
+    if (o->path_policy == 2 && o->semantics == 1) {
+        set_error("cfpq_closure: single-path lengths need the sparse engine (min-plus is not a Boolean product)");
         return CFPQ_E_UNSUPPORTED;
     }
     CFPQ_CHECK_ARG(o->path_policy >= 0 && o->path_policy <= 3, "cfpq_closure: bad path_policy");
@@ -600,7 +698,7 @@ extern "C" cfpq_status cfpq_closure_reuse(const cfpq_grammar* g, const cfpq_grap
     if (st != CFPQ_OK) return st;
     CFPQ_CHECK_ARG(d->n_nodes == r->n && g->n_nt == r->n_nt && g->n_labels == r->n_labels &&
                        g->rules.size() == r->rules.size() && o->semantics == r->opts.semantics &&
-                       o->account_work == r->opts.account_work,
+                       o->account_work == r->opts.account_work && (o->path_policy == 2) == r->dense_mode,
                    "cfpq_closure_reuse: grammar/graph/options differ from the result's plan");
     for (size_t k = 0; k < g->rules.size(); ++k)
         CFPQ_CHECK_ARG(g->rules[k].A == r->rules[k].A && g->rules[k].B == r->rules[k].B && g->rules[k].C == r->rules[k].C,
@@ -655,9 +753,22 @@ static cfpq_status counts_upto(cfpq_result* r, unsigned long long end, std::vect
     return CFPQ_OK;
 }
 
+// |R_A| from the bit matrix (dense-engine results)
+static cfpq_status bitmap_count(cfpq_result* r, int32_t nt, int64_t* out) {
+    cudaStream_t s = r->stream;
+    CFPQ_CUDA_TRY(cudaMemsetAsync(r->d_small, 0, 8, s));
+    CFPQ_CUDA_TRY(launch_bitmap_rowcount(r->h_nt[nt].T, (int32_t)r->n, r->Wp, nullptr, r->d_small, s));
+    unsigned long long v = 0;
+    CFPQ_CUDA_TRY(cudaMemcpyAsync(&v, r->d_small, 8, cudaMemcpyDeviceToHost, s));
+    CFPQ_CUDA_TRY(cudaStreamSynchronize(s));
+    *out = (int64_t)v;
+    return CFPQ_OK;
+}
+
 extern "C" cfpq_status cfpq_result_count(cfpq_result* r, int32_t nt, int64_t* out) {
     CFPQ_CHECK_ARG(r && out, "cfpq_result_count: NULL argument");
     CFPQ_CHECK_ARG(nt >= 0 && nt < r->n_nt, "cfpq_result_count: NT id out of range");
+    if (r->dense_mode) return bitmap_count(r, nt, out);
     if (!r->counts_valid) {
         cfpq_status st = counts_upto(r, r->n_cells, r->counts);
         if (st != CFPQ_OK) return st;
@@ -671,6 +782,11 @@ extern "C" cfpq_status cfpq_result_count_at(cfpq_result* r, int32_t nt, int64_t 
     CFPQ_CHECK_ARG(r && out, "cfpq_result_count_at: NULL argument");
     CFPQ_CHECK_ARG(nt >= 0 && nt < r->n_nt, "cfpq_result_count_at: NT id out of range");
     CFPQ_CHECK_ARG(k >= 0, "cfpq_result_count_at: k < 0");
+    if (r->dense_mode && k < r->iterations) {
+        set_error("per-iteration states are kept only by the sparse engine");
+        return CFPQ_E_UNSUPPORTED;
+    }
+    if (r->dense_mode) return bitmap_count(r, nt, out);
     cfpq_status st;
     unsigned long long end = log_end(r, k, &st);
     if (st != CFPQ_OK) return st;
@@ -714,10 +830,56 @@ static cfpq_status sorted_keys(cfpq_result* r, int32_t nt, unsigned long long en
     return CFPQ_OK;
 }
 
+static cfpq_status bitmap_pairs(cfpq_result* r, int32_t nt, int32_t* dst, int64_t capacity, int32_t on_dev,
+                                int64_t* written) {
+    cudaStream_t s = r->stream;
+    const int64_t n = r->n;
+    CFPQ_CUDA_TRY(cudaMemsetAsync(r->d_small, 0, 8, s));
+    CFPQ_CUDA_TRY(cudaMemsetAsync(r->d_rowcnt + n, 0, 4, s));
+    CFPQ_CUDA_TRY(launch_bitmap_rowcount(r->h_nt[nt].T, (int32_t)n, r->Wp, r->d_rowcnt, r->d_small, s));
+    unsigned long long m = 0;
+    CFPQ_CUDA_TRY(cudaMemcpyAsync(&m, r->d_small, 8, cudaMemcpyDeviceToHost, s));
+    CFPQ_CUDA_TRY(cudaStreamSynchronize(s));
+    *written = (int64_t)m;
+    CFPQ_CHECK_ARG((int64_t)m <= capacity, "cfpq_result_pairs: capacity < |R_A|");
+    CFPQ_CHECK_ARG(m == 0 || dst != nullptr, "cfpq_result_pairs: dst is NULL");
+    if (m == 0) return CFPQ_OK;
+    size_t need = 0;
+    CFPQ_CUDA_TRY(launch_scan(nullptr, nullptr, n + 1, nullptr, &need, s));
+    if (need > r->temp_bytes) {
+        dfree(r->d_temp);
+        cfpq_status st = dalloc((uint8_t**)&r->d_temp, need, "scan temp");
+        if (st != CFPQ_OK) return st;
+        r->temp_bytes = need;
+    }
+    CFPQ_CUDA_TRY(launch_scan(r->d_rowcnt, r->d_rowoff, n + 1, r->d_temp, &r->temp_bytes, s));
+    int32_t* tmp = dst;
+    if (!on_dev) {
+        if (m + 1 > r->keys_cap) {
+            dfree(r->d_keys);
+            cfpq_status st = dalloc(&r->d_keys, m + 1, "extraction scratch");
+            if (st != CFPQ_OK) return st;
+            r->keys_cap = m + 1;
+        }
+        tmp = (int32_t*)r->d_keys;
+    }
+    CFPQ_CUDA_TRY(launch_bitmap_pairs(r->h_nt[nt].T, (int32_t)n, r->Wp, r->d_rowoff, tmp, s));
+    if (!on_dev) CFPQ_CUDA_TRY(cudaMemcpyAsync(dst, tmp, m * 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    CFPQ_CUDA_TRY(cudaStreamSynchronize(s));
+    return CFPQ_OK;
+}
+
 static cfpq_status pairs_impl(cfpq_result* r, int32_t nt, int64_t k, int32_t* dst, int64_t capacity, int32_t on_dev,
                               int64_t* written) {
     CFPQ_CHECK_ARG(r && written, "cfpq_result_pairs: NULL argument");
     CFPQ_CHECK_ARG(nt >= 0 && nt < r->n_nt, "cfpq_result_pairs: NT id out of range");
+    if (r->dense_mode) {
+        if (k >= 0 && k < r->iterations) {
+            set_error("per-iteration states are kept only by the sparse engine");
+            return CFPQ_E_UNSUPPORTED;
+        }
+        return bitmap_pairs(r, nt, dst, capacity, on_dev, written);
+    }
     cfpq_status st;
     unsigned long long end = log_end(r, k, &st);
     if (st != CFPQ_OK) return st;
@@ -810,6 +972,15 @@ extern "C" cfpq_status cfpq_result_iteration_stats2(cfpq_result* r, int64_t* new
     int64_t k = std::min<int64_t>(r->iterations, capacity);
     k = std::min<int64_t>(k, r->iter_off_cap - 2);
     if (k <= 0) return CFPQ_OK;
+    if (r->dense_mode) {
+        if (new_cells)
+            for (int64_t t = 0; t < k; ++t) new_cells[t] = r->dense_new[t];
+        if (jacobi_triples || end_ns) {
+            set_error("work counts / iteration times are recorded by the sparse engine only");
+            return CFPQ_E_UNSUPPORTED;
+        }
+        return CFPQ_OK;
+    }
     std::vector<unsigned long long> off(k + 2);
     CFPQ_CUDA_TRY(cudaMemcpy(off.data(), r->d_iter_off, (k + 2) * 8, cudaMemcpyDeviceToHost));
     if (new_cells)

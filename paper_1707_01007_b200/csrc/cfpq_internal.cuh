@@ -182,5 +182,18 @@ cudaError_t launch_gather_lengths(const uint64_t* keys, unsigned long long n, co
                                   uint32_t* out, cudaStream_t s);
 cudaError_t launch_scan(const int32_t* in, int32_t* out, int64_t n, void* temp, size_t* temp_bytes,
                         cudaStream_t s);
+cudaError_t launch_bitmap_rowcount(const uint32_t* T, int32_t n, int64_t Wp, int32_t* rowcnt,
+                                   unsigned long long* total, cudaStream_t s);
+cudaError_t launch_bitmap_pairs(const uint32_t* T, int32_t n, int64_t Wp, const int32_t* rowoff, int32_t* pairs,
+                                cudaStream_t s);
+
+// dense (tcgen05) engine, dense.cu
+struct DenseEngine;
+DenseEngine* dense_create(int32_t n, int32_t n_nt, int64_t Wp, const std::vector<Rule3>& rules,
+                          const std::vector<int32_t>& is_const, cudaStream_t s, std::string* err);
+void dense_destroy(DenseEngine* e);
+cudaError_t dense_step(DenseEngine* e, uint32_t* const* T, uint32_t* const* Tn, bool first, cudaStream_t s,
+                       unsigned long long* new_total, std::vector<unsigned long long>* per_nt, int* launches);
+const std::vector<int32_t>& dense_outputs(const DenseEngine* e);
 
 }  // namespace cfpq

@@ -1,0 +1,555 @@
+// Dense (tensor-core) closure iteration for sm_100a: tcgen05 int8 MMA on 0/1 tiles.
+//
+// One Jacobi loop body of Algorithm 1, T_k = T_{k-1} ∪ (T_{k-1} × T_{k-1}), with
+// the product evaluated as |N|^2-style Boolean matrix products (Valiant's view):
+// for every non-preterminal A,
+//     P_A[i][j] = Σ_{A->BC} Σ_r T_B[i][r] · T_C[r][j]   (integer, exact: ≤ |rules|·n < 2^31)
+//     T_k,A[i][j] = T_{k-1},A[i][j] ∨ (P_A[i][j] > 0)        (N1·N2 per rule, ∪ over r)
+// Operands are 0/1 bytes (T8 = row-major copy of T_B, T8T = transposed copy of T_C, both
+// K-major for the UMMA), staged by TMA into 128B-swizzled shared memory; the s32
+// accumulator lives in TMEM (128 lanes x 256 columns); the epilogue thresholds it to bits,
+// ORs the old bits, writes T_k into the other bit-matrix buffer and counts new cells.
+// Empty 128x128 operand tiles are skipped (tile-occupancy "skip list").
+//
+// Roles per CTA (persistent over output tiles (A, I, J), 128 x 256 each):
+//   warp 0 : TMA producer (one elected lane)      -> full[s]
+//   warp 1 : TMEM allocator + MMA issuer (one lane) -> empty[s], tmem_full
+//   warps 2-5 : epilogue (TMEM -> registers -> bits)   -> tmem_empty
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include "cfpq_internal.cuh"
+
+namespace cfpq {
+
+constexpr int kTM = 128;                 // UMMA M (rows of the output tile)
+constexpr int kTN = 256;                 // UMMA N (columns of the output tile)
+constexpr int kTK = 128;                 // K bytes per pipeline stage (one 128B swizzle row)
+constexpr int kUK = 32;                  // K per tcgen05.mma kind::i8
+constexpr int kStages = 4;
+constexpr int kABytes = kTM * kTK;       // 16 KiB
+constexpr int kBBytes = kTN * kTK;       // 32 KiB
+constexpr int kStageBytes = kABytes + kBBytes;
+constexpr int kDenseThreads = 192;       // 6 warps
+constexpr int kTmemCols = 256;
+
+struct DenseRule {   // A -> B C, operand slots into the packed arrays
+    int32_t A, B, C, pad;
+};
+
+struct DenseParams {
+    int32_t n, np;                 // nodes, padded to a multiple of 256
+    int64_t Wp;                    // words per bit-matrix row
+    int32_t n_out;                 // non-preterminal NTs (outputs)
+    const int32_t* out_nt;         // [n_out] NT ids
+    const int32_t* rule_ptr;       // [n_out+1] rules of each output NT
+    const DenseRule* rules;        // B, C = NT ids
+    const uint32_t* const* T;      // [n_nt] current bit matrices (T_{k-1})
+    uint32_t* const* Tn;           // [n_nt] next bit matrices (T_k); only outputs
+    const uint8_t* occ;            // [n_nt][nt_tiles][nt_tiles] 128x128 tile occupancy
+    int32_t nt_tiles;              // np / 128
+    unsigned long long* new_cells; // [n_nt + 1] new cells per NT, [n_nt] = total
+    int32_t n_nt;
+    unsigned long long mma_tiles;  // diagnostics (unused on device)
+};
+
+// ------------------------------------------------------------------------------------------
+// PTX helpers
+// ------------------------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t addr = smem_u32(bar);
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(addr),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int x, int y) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+            smem_u32(dst)),
+        "l"(map), "r"(smem_u32(bar)), "r"(x), "r"(y)
+        : "memory");
+}
+__device__ __forceinline__ void tmem_alloc(uint32_t* dst_smem, uint32_t ncols) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst_smem)),
+                 "r"(ncols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+}
+__device__ __forceinline__ void tmem_dealloc(uint32_t taddr, uint32_t ncols) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols));
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void umma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                        uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+          "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+          "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// K-major operand tile in 128B-swizzled shared memory (rows of 128 bytes, 8-row atoms
+// 1024 B apart): start>>4, LBO = 1 (unused for swizzled K-major), SBO = 1024>>4,
+// version 1 (sm_100), layout SWIZZLE_128B = 2.
+__device__ __forceinline__ uint64_t kmajor_sw128_desc(uint32_t smem_addr) {
+    uint64_t d = 0;
+    d |= (uint64_t)((smem_addr & 0x3FFFF) >> 4);
+    d |= (uint64_t)1 << 16;
+    d |= (uint64_t)(1024 >> 4) << 32;
+    d |= (uint64_t)1 << 46;
+    d |= (uint64_t)2 << 61;
+    return d;
+}
+
+// kind::i8 instruction descriptor: D s32, A/B unsigned 8-bit, both K-major, M=128, N=256.
+__host__ __device__ constexpr uint32_t idesc_i8(int M, int N) {
+    return (2u << 4) | (0u << 7) | (0u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+// ------------------------------------------------------------------------------------------
+// Pack: bits -> 0/1 bytes (row-major T8 and transposed T8T) + 128x128 tile occupancy.
+// One CTA (256 threads) per 128x128 tile of one NT.
+// ------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) pack_kernel(const uint32_t* __restrict__ T, int32_t n, int64_t Wp, int32_t np,
+                                                   uint8_t* T8, uint8_t* T8T, uint8_t* occ, int32_t nt_tiles) {
+    __shared__ uint32_t bits[kTM][4];
+    __shared__ int any;
+    const int tI = blockIdx.y, tK = blockIdx.x;
+    if (threadIdx.x == 0) any = 0;
+    for (int t = threadIdx.x; t < kTM * 4; t += 256) {
+        int r = t >> 2, w = t & 3;
+        int row = tI * kTM + r;
+        int64_t word = (int64_t)tK * 4 + w;
+        uint32_t v = 0;
+        if (row < n && word * 32 < n) v = __ldg(T + (size_t)row * Wp + word);
+        bits[r][w] = v;
+    }
+    __syncthreads();
+    int local_any = 0;
+    for (int t = threadIdx.x; t < kTM * 4; t += 256) local_any |= bits[t >> 2][t & 3] != 0;
+    if (local_any) any = 1;
+    // row-major bytes: thread handles 16 consecutive columns of one row (4 uint4 stores per thread)
+    if (T8) {
+        for (int t = threadIdx.x; t < kTM * 8; t += 256) {
+            int r = t >> 3, c16 = t & 7;   // columns c16*16 .. +15
+            uint32_t w = bits[r][c16 >> 1] >> ((c16 & 1) * 16);
+            uint32_t o[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                uint32_t b = w >> (q * 4);
+                o[q] = (b & 1u) | ((b >> 1) & 1u) << 8 | ((b >> 2) & 1u) << 16 | ((b >> 3) & 1u) << 24;
+            }
+            *reinterpret_cast<uint4*>(T8 + (size_t)(tI * kTM + r) * np + tK * kTM + c16 * 16) =
+                make_uint4(o[0], o[1], o[2], o[3]);
+        }
+    }
+    // transposed bytes: output row c (= column c of the tile), 16 consecutive source rows
+    if (T8T) {
+        for (int t = threadIdx.x; t < kTM * 8; t += 256) {
+            int c = t >> 3, r16 = t & 7;
+            uint32_t o[4] = {0, 0, 0, 0};
+#pragma unroll
+            for (int q = 0; q < 16; ++q) {
+                uint32_t b = (bits[r16 * 16 + q][c >> 5] >> (c & 31)) & 1u;
+                o[q >> 2] |= b << ((q & 3) * 8);
+            }
+            *reinterpret_cast<uint4*>(T8T + (size_t)(tK * kTM + c) * np + tI * kTM + r16 * 16) =
+                make_uint4(o[0], o[1], o[2], o[3]);
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && occ) occ[(size_t)tI * nt_tiles + tK] = any ? 1 : 0;
+}
+
+// ------------------------------------------------------------------------------------------
+// The tcgen05 product kernel
+// ------------------------------------------------------------------------------------------
+struct TileIter {   // walks the (A, I, J) output tiles of this CTA
+    int32_t tiles_per_nt, n_i, n_j;
+};
+
+__device__ __forceinline__ bool kblock_live(const DenseParams& p, const DenseRule& r, int I, int J, int K) {
+    const size_t tt = (size_t)p.nt_tiles * p.nt_tiles;
+    const uint8_t* oB = p.occ + (size_t)r.B * tt;
+    const uint8_t* oC = p.occ + (size_t)r.C * tt;
+    if (!__ldg(oB + (size_t)I * p.nt_tiles + K)) return false;
+    // B operand = T_C rows K-block, columns J*256 .. +255 = two 128x128 tiles of T_C
+    return __ldg(oC + (size_t)K * p.nt_tiles + 2 * J) || __ldg(oC + (size_t)K * p.nt_tiles + 2 * J + 1);
+}
+
+__global__ void __launch_bounds__(kDenseThreads, 1)
+    dense_kernel(DenseParams p, const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                 const int64_t* __restrict__ mapA_row, const int64_t* __restrict__ mapB_row) {
+    // mapA_row[X] = first row of NT X inside the stacked T8 tensor (tmA), mapB_row likewise
+    // for the stacked T8T tensor (tmB); -1 if X is not packed.
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sA = smem;                                  // [kStages][kABytes]
+    uint8_t* sB = smem + kStages * kABytes;              // [kStages][kBBytes]
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
+    uint64_t* empty = full + kStages;
+    uint64_t* tmem_full = empty + kStages;
+    uint64_t* tmem_empty = tmem_full + 1;
+    uint32_t* tmem_base_smem = reinterpret_cast<uint32_t*>(tmem_empty + 1);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int n_i = p.np / kTM, n_j = p.np / kTN;
+    const int tiles_per_nt = n_i * n_j;
+    const int total_tiles = tiles_per_nt * p.n_out;
+    const int n_k = p.np / kTK;
+
+    if (warp == 0 && lane == 0) {
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        mbar_init(tmem_full, 1);
+        mbar_init(tmem_empty, 128);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
+    }
+    if (warp == 1) tmem_alloc(tmem_base_smem, kTmemCols);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_base_smem;
+
+    if (warp == 0) {
+        // ------------------------------- TMA producer -------------------------------
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+                const int o = t / tiles_per_nt, rem = t - o * tiles_per_nt;
+                const int I = rem / n_j, J = rem - (rem / n_j) * n_j;
+                for (int q = p.rule_ptr[o]; q < p.rule_ptr[o + 1]; ++q) {
+                    const DenseRule r = p.rules[q];
+                    const int64_t arow = __ldg(mapA_row + r.B) + (int64_t)I * kTM;
+                    const int64_t brow = __ldg(mapB_row + r.C) + (int64_t)J * kTN;
+                    for (int K = 0; K < n_k; ++K) {
+                        if (!kblock_live(p, r, I, J, K)) continue;
+                        mbar_wait(&empty[stage], phase ^ 1);
+                        mbar_expect_tx(&full[stage], kStageBytes);
+                        tma_load_2d(sA + stage * kABytes, &tmA, &full[stage], K * kTK, (int)arow);
+                        tma_load_2d(sB + stage * kBBytes, &tmB, &full[stage], K * kTK, (int)brow);
+                        if (++stage == kStages) {
+                            stage = 0;
+                            phase ^= 1;
+                        }
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ------------------------------- MMA issuer -------------------------------
+        const uint32_t idesc = idesc_i8(kTM, kTN);
+        int stage = 0;
+        uint32_t phase = 0;
+        uint32_t tphase = 0;
+        for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+            const int o = t / tiles_per_nt, rem = t - o * tiles_per_nt;
+            const int I = rem / n_j, J = rem - (rem / n_j) * n_j;
+            // the epilogue must have drained the accumulator of the previous tile
+            mbar_wait(tmem_empty, tphase ^ 1);
+            tc_fence_after();
+            uint32_t acc = 0;
+            for (int q = p.rule_ptr[o]; q < p.rule_ptr[o + 1]; ++q) {
+                const DenseRule r = p.rules[q];
+                for (int K = 0; K < n_k; ++K) {
+                    if (!kblock_live(p, r, I, J, K)) continue;
+                    mbar_wait(&full[stage], phase);
+                    tc_fence_after();
+                    if (lane == 0) {
+                        const uint32_t a0 = smem_u32(sA + stage * kABytes);
+                        const uint32_t b0 = smem_u32(sB + stage * kBBytes);
+#pragma unroll
+                        for (int kk = 0; kk < kTK / kUK; ++kk) {
+                            umma_i8(tmem_base, kmajor_sw128_desc(a0 + kk * kUK), kmajor_sw128_desc(b0 + kk * kUK),
+                                    idesc, acc);
+                            acc = 1;
+                        }
+                        umma_commit(&empty[stage]);   // frees the smem stage when these MMAs finish
+                    }
+                    __syncwarp();
+                    if (++stage == kStages) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+            if (lane == 0) {
+                if (acc) umma_commit(tmem_full);   // arrives when all MMAs of the tile completed
+                else mbar_arrive(tmem_full);       // no live K block: the epilogue uses zeros
+            }
+            __syncwarp();
+            tphase ^= 1;
+        }
+    } else {
+        // ------------------------------- epilogue (warps 2..5) -------------------------------
+        const int quarter = warp & 3;            // TMEM lanes 32*quarter .. +31 are this warp's
+        uint32_t tphase = 0;
+        unsigned long long my_new = 0;
+        for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+            const int o = t / tiles_per_nt, rem = t - o * tiles_per_nt;
+            const int I = rem / n_j, J = rem - (rem / n_j) * n_j;
+            const int A = p.out_nt[o];
+            bool live = false;
+            for (int q = p.rule_ptr[o]; q < p.rule_ptr[o + 1] && !live; ++q)
+                for (int K = 0; K < n_k && !live; ++K) live = kblock_live(p, p.rules[q], I, J, K);
+            mbar_wait(tmem_full, tphase);
+            tc_fence_after();
+            const int row = I * kTM + quarter * 32 + lane;
+            const uint32_t* told = p.T[A] + (size_t)row * p.Wp;
+            uint32_t* tnew = p.Tn[A] + (size_t)row * p.Wp;
+            unsigned long long cnt = 0;
+#pragma unroll 1
+            for (int c = 0; c < kTN / 32; ++c) {
+                uint32_t word = 0;
+                if (live) {
+                    uint32_t v[32];
+                    tmem_ld32(tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(c * 32), v);
+#pragma unroll
+                    for (int b = 0; b < 32; ++b) word |= (v[b] != 0u ? 1u : 0u) << b;
+                }
+                const int64_t wi = (int64_t)J * (kTN / 32) + c;
+                if (row < p.n && wi < p.Wp) {
+                    uint32_t old = __ldg(told + wi);
+                    tnew[wi] = old | word;
+                    cnt += __popc(word & ~old);
+                }
+            }
+            tc_fence_before();
+            mbar_arrive(tmem_empty);
+            tphase ^= 1;
+#pragma unroll
+            for (int s = 16; s > 0; s >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, s);
+            if (lane == 0 && cnt) atomicAdd(p.new_cells + A, cnt);
+            my_new += cnt;
+        }
+        if (lane == 0 && my_new) atomicAdd(p.new_cells + p.n_nt, my_new);
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) tmem_dealloc(tmem_base, kTmemCols);
+}
+
+// ------------------------------------------------------------------------------------------
+// host side
+// ------------------------------------------------------------------------------------------
+static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        cudaDriverEntryPointQueryResult q;
+        void* p = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = (PFN_cuTensorMapEncodeTiled_v12000)p;
+    }
+    return fn;
+}
+
+// 2D uint8 tensor [rows][np] with a (128 x box_rows) box, 128B swizzle.
+static bool make_map(CUtensorMap* m, const uint8_t* base, int64_t rows, int64_t np, int box_rows) {
+    auto enc = get_encode();
+    if (!enc) return false;
+    cuuint64_t dims[2] = {(cuuint64_t)np, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)np};
+    cuuint32_t box[2] = {(cuuint32_t)kTK, (cuuint32_t)box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, (void*)base, dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+size_t dense_smem_bytes() { return (size_t)kStages * kStageBytes + 1024 + 256; }
+
+struct DenseEngine {
+    int32_t n = 0, np = 0, nt_tiles = 0, n_nt = 0;
+    int64_t Wp = 0;
+    std::vector<int32_t> is_const, packA, packB;   // packA[X]: X is a left operand (T8), packB: right (T8T)
+    std::vector<int64_t> h_mapA, h_mapB;
+    uint8_t* T8 = nullptr;
+    uint8_t* T8T = nullptr;
+    uint8_t* occ = nullptr;
+    int64_t* mapA_row = nullptr;
+    int64_t* mapB_row = nullptr;
+    int32_t* out_nt = nullptr;
+    int32_t* rule_ptr = nullptr;
+    DenseRule* rules = nullptr;
+    const uint32_t** Tptr = nullptr;
+    uint32_t** Tnptr = nullptr;
+    unsigned long long* new_cells = nullptr;
+    int32_t n_out = 0;
+    std::vector<int32_t> h_out;
+    CUtensorMap tmA, tmB;
+    int grid = 0;
+    ~DenseEngine() {
+        cudaFree(T8); cudaFree(T8T); cudaFree(occ); cudaFree(mapA_row); cudaFree(mapB_row); cudaFree(out_nt);
+        cudaFree(rule_ptr); cudaFree(rules); cudaFree(Tptr); cudaFree(Tnptr); cudaFree(new_cells);
+    }
+};
+
+void dense_destroy(DenseEngine* e) { delete e; }
+
+DenseEngine* dense_create(int32_t n, int32_t n_nt, int64_t Wp, const std::vector<Rule3>& rules,
+                          const std::vector<int32_t>& is_const, cudaStream_t s, std::string* err) {
+    DenseEngine* e = new DenseEngine();
+    e->n = n;
+    e->n_nt = n_nt;
+    e->Wp = Wp;
+    e->np = ((n + kTN - 1) / kTN) * kTN;
+    if (e->np == 0) e->np = kTN;
+    e->nt_tiles = e->np / kTM;
+    e->is_const = is_const;
+    e->packA.assign(n_nt, 0);
+    e->packB.assign(n_nt, 0);
+    std::vector<std::vector<DenseRule>> by(n_nt);
+    for (auto& r : rules) {
+        by[r.A].push_back(DenseRule{r.A, r.B, r.C, 0});
+        e->packA[r.B] = 1;
+        e->packB[r.C] = 1;
+    }
+    std::vector<int32_t> rp(1, 0);
+    std::vector<DenseRule> rl;
+    for (int A = 0; A < n_nt; ++A) {
+        if (by[A].empty()) continue;
+        e->h_out.push_back(A);
+        for (auto& r : by[A]) rl.push_back(r);
+        rp.push_back((int32_t)rl.size());
+    }
+    e->n_out = (int32_t)e->h_out.size();
+    int na = 0, nb = 0;
+    e->h_mapA.assign(n_nt, -1);
+    e->h_mapB.assign(n_nt, -1);
+    for (int X = 0; X < n_nt; ++X) {
+        if (e->packA[X]) e->h_mapA[X] = (int64_t)(na++) * e->np;
+        if (e->packB[X]) e->h_mapB[X] = (int64_t)(nb++) * e->np;
+    }
+    auto fail = [&](const char* what, cudaError_t c) {
+        if (err) *err = std::string("dense engine: ") + what + ": " + cudaGetErrorString(c);
+        cudaGetLastError();
+        delete e;
+        return (DenseEngine*)nullptr;
+    };
+    const size_t pack = (size_t)e->np * e->np;
+    cudaError_t c;
+    if ((c = cudaMalloc(&e->T8, std::max<size_t>(1, pack * na))) != cudaSuccess) return fail("T8", c);
+    if ((c = cudaMalloc(&e->T8T, std::max<size_t>(1, pack * nb))) != cudaSuccess) return fail("T8T", c);
+    if ((c = cudaMalloc(&e->occ, (size_t)n_nt * e->nt_tiles * e->nt_tiles)) != cudaSuccess) return fail("occ", c);
+    if ((c = cudaMemsetAsync(e->occ, 0, (size_t)n_nt * e->nt_tiles * e->nt_tiles, s)) != cudaSuccess) return fail("occ", c);
+    if ((c = cudaMalloc(&e->mapA_row, n_nt * 8)) != cudaSuccess) return fail("maps", c);
+    if ((c = cudaMalloc(&e->mapB_row, n_nt * 8)) != cudaSuccess) return fail("maps", c);
+    if ((c = cudaMalloc(&e->out_nt, std::max(1, e->n_out) * 4)) != cudaSuccess) return fail("tables", c);
+    if ((c = cudaMalloc(&e->rule_ptr, rp.size() * 4)) != cudaSuccess) return fail("tables", c);
+    if ((c = cudaMalloc(&e->rules, std::max<size_t>(1, rl.size()) * sizeof(DenseRule))) != cudaSuccess) return fail("tables", c);
+    if ((c = cudaMalloc(&e->Tptr, n_nt * sizeof(void*))) != cudaSuccess) return fail("tables", c);
+    if ((c = cudaMalloc(&e->Tnptr, n_nt * sizeof(void*))) != cudaSuccess) return fail("tables", c);
+    if ((c = cudaMalloc(&e->new_cells, (n_nt + 1) * 8)) != cudaSuccess) return fail("counters", c);
+    cudaMemcpyAsync(e->mapA_row, e->h_mapA.data(), n_nt * 8, cudaMemcpyHostToDevice, s);
+    cudaMemcpyAsync(e->mapB_row, e->h_mapB.data(), n_nt * 8, cudaMemcpyHostToDevice, s);
+    if (e->n_out) cudaMemcpyAsync(e->out_nt, e->h_out.data(), e->n_out * 4, cudaMemcpyHostToDevice, s);
+    cudaMemcpyAsync(e->rule_ptr, rp.data(), rp.size() * 4, cudaMemcpyHostToDevice, s);
+    if (!rl.empty()) cudaMemcpyAsync(e->rules, rl.data(), rl.size() * sizeof(DenseRule), cudaMemcpyHostToDevice, s);
+    if (!make_map(&e->tmA, e->T8, (int64_t)std::max(na, 1) * e->np, e->np, kTM) ||
+        !make_map(&e->tmB, e->T8T, (int64_t)std::max(nb, 1) * e->np, e->np, kTN)) {
+        if (err) *err = "dense engine: cuTensorMapEncodeTiled failed";
+        delete e;
+        return nullptr;
+    }
+    if ((c = cudaFuncSetAttribute(dense_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dense_smem_bytes())) !=
+        cudaSuccess)
+        return fail("smem attribute", c);
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int total = e->n_out * (e->np / kTM) * (e->np / kTN);
+    e->grid = std::max(1, std::min(sms, total));
+    return e;
+}
+
+// One Jacobi iteration: T (T_{k-1}, all NTs) -> Tn (T_k, outputs).  Returns the new cells
+// of iteration k (total and per NT) on the host.
+cudaError_t dense_step(DenseEngine* e, uint32_t* const* T, uint32_t* const* Tn, bool first, cudaStream_t s,
+                       unsigned long long* new_total, std::vector<unsigned long long>* per_nt, int* launches) {
+    const size_t pack = (size_t)e->np * e->np;
+    for (int X = 0; X < e->n_nt; ++X) {
+        if (!(e->packA[X] || e->packB[X])) continue;
+        if (!first && e->is_const[X]) continue;   // preterminals never change after seeding
+        uint8_t* a = e->packA[X] ? e->T8 + (size_t)(e->h_mapA[X] / e->np) * pack : nullptr;
+        uint8_t* b = e->packB[X] ? e->T8T + (size_t)(e->h_mapB[X] / e->np) * pack : nullptr;
+        dim3 grid(e->nt_tiles, e->nt_tiles);
+        pack_kernel<<<grid, 256, 0, s>>>(T[X], e->n, e->Wp, e->np, a, b,
+                                         e->occ + (size_t)X * e->nt_tiles * e->nt_tiles, e->nt_tiles);
+        if (launches) ++*launches;
+    }
+    cudaError_t c;
+    if ((c = cudaMemcpyAsync((void*)e->Tptr, T, e->n_nt * sizeof(void*), cudaMemcpyHostToDevice, s)) != cudaSuccess)
+        return c;
+    if ((c = cudaMemcpyAsync((void*)e->Tnptr, Tn, e->n_nt * sizeof(void*), cudaMemcpyHostToDevice, s)) != cudaSuccess)
+        return c;
+    if ((c = cudaMemsetAsync(e->new_cells, 0, (e->n_nt + 1) * 8, s)) != cudaSuccess) return c;
+    DenseParams p{};
+    p.n = e->n;
+    p.np = e->np;
+    p.Wp = e->Wp;
+    p.n_out = e->n_out;
+    p.out_nt = e->out_nt;
+    p.rule_ptr = e->rule_ptr;
+    p.rules = e->rules;
+    p.T = e->Tptr;
+    p.Tn = e->Tnptr;
+    p.occ = e->occ;
+    p.nt_tiles = e->nt_tiles;
+    p.new_cells = e->new_cells;
+    p.n_nt = e->n_nt;
+    if (e->n_out) {
+        dense_kernel<<<e->grid, kDenseThreads, dense_smem_bytes(), s>>>(p, e->tmA, e->tmB, e->mapA_row, e->mapB_row);
+        if ((c = cudaGetLastError()) != cudaSuccess) return c;
+        if (launches) ++*launches;
+    }
+    std::vector<unsigned long long> h(e->n_nt + 1);
+    if ((c = cudaMemcpyAsync(h.data(), e->new_cells, (e->n_nt + 1) * 8, cudaMemcpyDeviceToHost, s)) != cudaSuccess)
+        return c;
+    if ((c = cudaStreamSynchronize(s)) != cudaSuccess) return c;
+    *new_total = h[e->n_nt];
+    if (per_nt) per_nt->assign(h.begin(), h.end() - 1);
+    return cudaSuccess;
+}
+
+const std::vector<int32_t>& dense_outputs(const DenseEngine* e) { return e->h_out; }
+
+}  // namespace cfpq

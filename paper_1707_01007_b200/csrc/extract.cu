@@ -54,6 +54,76 @@ __global__ void gather_lengths_kernel(const uint64_t* __restrict__ keys, unsigne
     }
 }
 
+// ---- bit-matrix extraction (results of the dense engine, which keeps no cell log) ----
+// one warp per row: popcount of row i -> rowcnt[i]
+__global__ void bitmap_rowcount_kernel(const uint32_t* __restrict__ T, int32_t n, int64_t wn, int64_t Wp,
+                                       int32_t* rowcnt, unsigned long long* total) {
+    const int lane = threadIdx.x & 31;
+    unsigned long long acc = 0;
+    for (int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; row < n;
+         row += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        int c = 0;
+        for (int64_t w = lane; w < wn; w += 32) c += __popc(__ldg(T + (size_t)row * Wp + w));
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+        if (lane == 0) {
+            if (rowcnt) rowcnt[row] = c;
+            acc += (unsigned long long)c;
+        }
+    }
+    if (lane == 0 && acc) atomicAdd(total, acc);
+}
+
+// one warp per row: write (i,j) of the set bits of row i, ascending, from rowoff[i]
+__global__ void bitmap_pairs_kernel(const uint32_t* __restrict__ T, int32_t n, int64_t wn, int64_t Wp,
+                                    const int32_t* __restrict__ rowoff, int32_t* pairs) {
+    const int lane = threadIdx.x & 31;
+    for (int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; row < n;
+         row += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        int64_t base = rowoff[row];
+        for (int64_t w0 = 0; w0 < wn; w0 += 32) {
+            int64_t w = w0 + lane;
+            uint32_t bits = w < wn ? __ldg(T + (size_t)row * Wp + w) : 0u;
+            int c = __popc(bits);
+            int incl = c;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                int v = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += v;
+            }
+            int64_t at = base + incl - c;
+            while (bits) {
+                int b = __ffs(bits) - 1;
+                bits &= bits - 1u;
+                pairs[2 * at] = (int32_t)row;
+                pairs[2 * at + 1] = (int32_t)(w * 32 + b);
+                ++at;
+            }
+            base += __shfl_sync(0xffffffffu, incl, 31);
+        }
+    }
+}
+
+cudaError_t launch_bitmap_rowcount(const uint32_t* T, int32_t n, int64_t Wp, int32_t* rowcnt,
+                                   unsigned long long* total, cudaStream_t s) {
+    if (n) {
+        int64_t blocks = ((int64_t)n * 32 + 255) / 256;
+        if (blocks > 148 * 16) blocks = 148 * 16;
+        bitmap_rowcount_kernel<<<(int)blocks, 256, 0, s>>>(T, n, (n + 31) / 32, Wp, rowcnt, total);
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_bitmap_pairs(const uint32_t* T, int32_t n, int64_t Wp, const int32_t* rowoff, int32_t* pairs,
+                                cudaStream_t s) {
+    if (n) {
+        int64_t blocks = ((int64_t)n * 32 + 255) / 256;
+        if (blocks > 148 * 16) blocks = 148 * 16;
+        bitmap_pairs_kernel<<<(int)blocks, 256, 0, s>>>(T, n, (n + 31) / 32, Wp, rowoff, pairs);
+    }
+    return cudaGetLastError();
+}
+
 static int grid_for(unsigned long long work) {
     unsigned long long g = (work + 255) / 256;
     if (g < 1) g = 1;

@@ -1,0 +1,102 @@
+"""GPU parity of the dense tensor-core engine (path_policy = 2: tcgen05 int8 MMA on 0/1
+tiles, TMA-staged, TMEM accumulators, thresholded to bits) against the oracle."""
+from collections import deque
+
+import numpy as np
+import pytest
+
+import inputs as I
+import oracle as O
+from tests.gpu_util import assert_parity, cuda_ok, gpu_closure
+
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not cuda_ok(), reason="needs a CUDA device")]
+
+
+def _bfs_closure_pairs(n, edges):
+    adj = [[] for _ in range(n)]
+    for s, _, d in edges:
+        adj[s].append(d)
+    out = []
+    for s in range(n):
+        seen = set(adj[s])
+        dq = deque(adj[s])
+        while dq:
+            u = dq.popleft()
+            for v in adj[u]:
+                if v not in seen:
+                    seen.add(v)
+                    dq.append(v)
+        out += [(s, v) for v in sorted(seen)]
+    return np.array(out, dtype=np.int32).reshape(-1, 2)
+
+
+def test_tensor_example_and_iterations(example_golden):
+    g = example_golden
+    w = I.bind("example", I.same_generation_grammar(), 3, g["edges"], "S")
+    r, _, _ = gpu_closure(w, path_policy=2)
+    assert r.iterations == 6
+    ores = assert_parity(w, r)
+    nc, _ = r.iteration_stats()
+    assert nc.tolist() == ores.stats()["new_bits"].tolist()
+
+
+@pytest.mark.parametrize("n,d", [(64, 1), (150, 2), (300, 1), (257, 3)])
+def test_tensor_dense_stress_parity(n, d):
+    """S -> S S | a (both operands change): several 128x256 tiles and K blocks, ragged n."""
+    w = I.dense_stress_workload(n, d, seed=n)
+    r, _, _ = gpu_closure(w, path_policy=2)
+    ores = assert_parity(w, r)
+    nc, _ = r.iteration_stats()
+    assert nc.tolist() == ores.stats()["new_bits"].tolist()
+
+
+@pytest.mark.parametrize("n,d", [(1000, 2), (2048, 1), (1537, 4)])
+def test_tensor_dense_stress_bfs(n, d):
+    """Larger n against the textbook BFS transitive closure (the pin of S -> S S | a)."""
+    w = I.dense_stress_workload(n, d, seed=7)
+    r, _, _ = gpu_closure(w, path_policy=2)
+    assert np.array_equal(r.pairs(0), _bfs_closure_pairs(n, w.edges.tolist()))
+
+
+def test_tensor_random_parity():
+    for s in range(60):
+        w = I.random_workload(40_000 + s, max_nodes=40, max_edges=120, max_nt=5, max_bin=10, max_term=5)
+        r, _, _ = gpu_closure(w, path_policy=2)
+        ores = assert_parity(w, r)
+        nc, _ = r.iteration_stats()
+        assert nc.tolist() == ores.stats()["new_bits"].tolist(), w.name
+
+
+@pytest.mark.parametrize("query", ["q1", "q2", "union"])
+def test_tensor_ontology_parity(query):
+    w = I.ontology_workload(query, 600, depth=6, seed=2)
+    r, _, _ = gpu_closure(w, path_policy=2)
+    assert_parity(w, r)
+
+
+def test_tensor_anbn_and_reuse():
+    from paper_1707_01007_b200 import cfpq as C
+    w = I.anbn_workload(3, 5)
+    g = C.Grammar.from_workload(w)
+    d = C.Graph(w.n_nodes, w.edges)
+    r = C.closure(g, d, path_policy=2)
+    assert r.iterations == 2 * 3 * 5 + 1
+    assert_parity(w, r)
+    C.closure_reuse(g, d, r, path_policy=2)
+    assert_parity(w, r)
+    w2 = I.anbn_workload(3, 5)
+    w2.edges = w2.edges[::-1].copy()
+    d.set_edges(w2.edges)
+    C.closure_reuse(g, d, r, path_policy=2)
+    assert_parity(w2, r)
+
+
+def test_tensor_empty_and_lengths_rejected():
+    from paper_1707_01007_b200 import cfpq as C
+    w = I.bind("empty", I.dense_stress_grammar(), 10, [], "S")
+    r, _, _ = gpu_closure(w, path_policy=2)
+    assert r.iterations == 1 and r.count(0) == 0
+    w2 = I.dense_stress_workload(20, 1)
+    with pytest.raises(C.CfpqError) as e:
+        gpu_closure(w2, path_policy=2, semantics=1)
+    assert e.value.status == C.CFPQ_E_UNSUPPORTED
