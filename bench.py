@@ -61,12 +61,17 @@ def make_workload(name: str, seed: int):
         desc = {"workload": "config2: Q1 on 8 disjoint copies of a pizza-sized (1980 triples) ontology graph",
                 "grammar": "same-generation G' (P:279-296)"}
     elif name == "configS":
-        w = I.dense_stress_workload(4096, 2, seed)
-        desc = {"workload": "configS: S->SS|a on G(n=4096, m=2n)", "grammar": "S->SS|a"}
+        w = I.dense_stress_workload(16384, 2, seed)
+        desc = {"workload": "configS: S->SS|a on G(n=16384, m=2n), dense tcgen05 int8 engine", "grammar": "S->SS|a"}
     else:
         raise SystemExit(f"unknown workload {name}")
     desc.update({"n_nodes": w.n_nodes, "n_edges": int(len(w.edges)), "seed": seed})
     return w, desc
+
+
+def policy_for(name):
+    """Dense var x var grammar -> the tcgen05 engine; the paper's grammars -> sparse engine."""
+    return 2 if name == "configS" else 0
 
 
 def jacobi_ops(w, name, g, d, C, stream):
@@ -76,7 +81,8 @@ def jacobi_ops(w, name, g, d, C, stream):
         p, q = w.meta["p"], w.meta["q"]
         it = 2 * p * q + 1
         return 2 * it * (it + 1) // 2
-    r = C.closure(g, d, account_work=True, stream=stream, semantics=int(name == "config5"))
+    r = C.closure(g, d, account_work=True, stream=stream, semantics=int(name == "config5"),
+                  path_policy=policy_for(name))
     _, jt = r.iteration_stats(work=True)
     return 2 * int(jt.sum())
 
@@ -166,6 +172,52 @@ def ncu_traffic(workload: str):
         return None
 
 
+def int8_peak():
+    """Dense int8 tensor peak = measured bf16 (MEASURED_PEAKS.json) x the nominal int8/bf16 ratio (2)."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return 2.0 * float(d["bf16_tflops"]), 2.0 * float(d["bf16_tflops_sustained"]), "measured bf16 x 2 (nominal int8/bf16)"
+    except Exception:
+        return 2.0 * 1590.0, 2.0 * 1400.0, "fallback bf16 x 2 (B200_PROFILING.md)"
+
+
+def tensor_roofline(stats, step_ms):
+    """Issued tensor work of the dense engine: 2*128*256*128 int8 ops per k-block, over the
+    device time of the fixpoint loop (all tcgen05 product launches + packs of every iteration)."""
+    ops = stats["mma_kblocks"] * 2 * 128 * 256 * 128
+    loop_s = stats["loop_ns"] * 1e-9
+    burst, sustained, src = int8_peak()
+    achieved = ops / loop_s / 1e12
+    return {"bound": "tensor", "achieved": achieved, "peak": burst, "unit": "TFLOP/s", "frac": achieved / burst,
+            "frac_of_sustained": achieved / sustained, "traffic": ncu_traffic("configS"),
+            "kernel": "cfpq::dense_kernel (tcgen05.mma kind::i8)", "loop_ms": loop_s * 1e3,
+            "share_of_step": loop_s * 1e3 / step_ms, "issued_int8_ops": ops, "peak_source": src,
+            "note": "int8 TOPS reported in the TFLOP/s slot; issued work counts whole 128x256x128 tiles (zeros inside tiles included)"}
+
+
+def supplementary_tensor(C, stream, steps=3):
+    """Config S (S->SS|a, n=16384) on the tcgen05 engine: the tensor-path roofline beside the
+    headline line (untimed by the driver's contract; its own CUDA-event timing)."""
+    import inputs as I
+    import torch
+    w = I.dense_stress_workload(16384, 2, 0)
+    g = C.Grammar.from_workload(w)
+    d = C.Graph(w.n_nodes, torch.from_numpy(w.edges).cuda(), stream=stream)
+    r = C.closure(g, d, path_policy=2, stream=stream)
+    C.closure_reuse(g, d, r, path_policy=2, stream=stream)
+    t = []
+    st = None
+    for _ in range(steps):
+        C.closure_reuse(g, d, r, path_policy=2, stream=stream)
+        st = r.stats()
+        t.append(st["loop_ns"] + st["seed_ns"])
+    ms = statistics.mean(t) * 1e-6
+    roof = tensor_roofline(st, ms)
+    return {"workload": "configS: S->SS|a, G(16384, 32768)", "closure_ms": ms, "iterations": r.iterations,
+            "cells": r.count(0), "roofline": roof}
+
+
 # ------------------------------------------------------------------------------------------
 # reference arm: the CPU oracle as it stands, on a bounded sample of the workload
 # ------------------------------------------------------------------------------------------
@@ -179,7 +231,7 @@ def oracle_sample(name: str, seed: int):
     if name == "config2":
         return (I.ontology_workload("q1", int(1980 / 2.28), depth=8, seed=seed, n_triples=1980),
                 "one pizza-sized copy (1980 triples) of the config-2 graph: full closure")
-    return I.dense_stress_workload(256, 2, seed), "S->SS|a on G(256, 512): full closure"
+    return I.dense_stress_workload(320, 2, seed), "S->SS|a on G(320, 640): full closure"
 
 
 def time_oracle(name: str, seed: int, reps: int = 1):
@@ -234,6 +286,7 @@ def main():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-supplementary", action="store_true")
     ap.add_argument("--solo", type=int, default=-1)
     args = ap.parse_args()
     if args.impl == "reference":
@@ -261,9 +314,11 @@ def main():
     edges_dev = torch.from_numpy(w.edges).cuda()
     d = C.Graph(w.n_nodes, edges_dev, stream=stream)
     ops = jacobi_ops(w, args.workload, g, d, C, stream)
-    r = C.closure(g, d, stream=stream, semantics=int(lengths), solo_threshold=args.solo)
+    pol = policy_for(args.workload)
+    r = C.closure(g, d, stream=stream, semantics=int(lengths), solo_threshold=args.solo, path_policy=pol)
     iterations = r.iterations
     cells = r.stats()["cells"]
+    cells_total = sum(r.count(A) for A in range(w.n_nt)) if pol == 2 else cells
     results_start = r.count(w.start)
     nc, _ = r.iteration_stats()
     delta0 = int(cells - nc.sum())
@@ -271,7 +326,7 @@ def main():
     # L2 flush buffer (> 126 MB L2), written between timed steps, outside the events
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
     for _ in range(args.warmup):
-        C.closure_reuse(g, d, r, stream=stream, semantics=int(lengths), solo_threshold=args.solo)
+        C.closure_reuse(g, d, r, stream=stream, semantics=int(lengths), solo_threshold=args.solo, path_policy=pol)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -285,7 +340,7 @@ def main():
         for _ in range(args.steps):
             flush.fill_(1)
             ev0.record(stream)
-            C.closure_reuse(g, d, r, stream=stream, semantics=int(lengths), solo_threshold=args.solo)
+            C.closure_reuse(g, d, r, stream=stream, semantics=int(lengths), solo_threshold=args.solo, path_policy=pol)
             ev1.record(stream)
             ev1.synchronize()
             step_ms.append(ev0.elapsed_time(ev1))
@@ -317,19 +372,22 @@ def main():
     # (entry, rule) expansion (two adjacency offsets), 12 B per candidate (4 B adjacency
     # index + 4 B read + 4 B write of its bit-matrix word), 8 B per appended cell;
     # single-path adds 16 B per candidate (key read+write) and 8 B per entry (own key).
+    peak, peak_src = hbm_peak()
+    if pol == 2:
+        roofline = tensor_roofline(stats, total_ms / args.steps)
     cand, exps = stats["candidates"], stats["expansions"]
     new_cells = cells - delta0
     alg_bytes = 8 * cells + 8 * exps + 12 * cand + 8 * new_cells
     if lengths:
         alg_bytes += 16 * cand + 8 * cells
     loop_s = statistics.mean(loop_ns) * 1e-9
-    peak, peak_src = hbm_peak()
-    achieved = alg_bytes / loop_s / 1e9
-    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": ncu_traffic(args.workload), "kernel": "cfpq::closure_kernel",
-                "kernel_ms": loop_s * 1e3, "share_of_step": (loop_s * 1e3) / (total_ms / args.steps),
-                "alg_bytes_per_launch": alg_bytes, "peak_source": peak_src,
-                "note": "latency-bound at this size (SURVEY V-9): ~20 iterations of ~1e5 new cells"}
+    if pol != 2:
+        achieved = alg_bytes / loop_s / 1e9
+        roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                    "traffic": ncu_traffic(args.workload), "kernel": "cfpq::closure_kernel",
+                    "kernel_ms": loop_s * 1e3, "share_of_step": (loop_s * 1e3) / (total_ms / args.steps),
+                    "alg_bytes_per_launch": alg_bytes, "peak_source": peak_src,
+                    "note": "latency-bound at this size (SURVEY V-9): ~20 iterations of ~1e5 new cells"}
 
     # ---- end to end through the public API with host buffers ----
     e2e = None
@@ -342,7 +400,7 @@ def main():
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             d.set_edges(pinned, stream=stream)
-            C.closure_reuse(g, d, r, stream=stream, semantics=int(lengths), solo_threshold=args.solo)
+            C.closure_reuse(g, d, r, stream=stream, semantics=int(lengths), solo_threshold=args.solo, path_policy=pol)
             pairs = r.pairs(w.start)
             t1 = time.perf_counter()
             if it >= args.warmup:
@@ -353,6 +411,13 @@ def main():
             dist.all_reduce(e_total, op=dist.ReduceOp.MAX)
         e2e = {"value": ops_all / float(e_total.item()) / 1e9, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "ms_per_step": 1e3 * float(e_total.item()) / len(ts)}
+
+    supp = None
+    if rank == 0 and world == 1 and args.workload == "config4" and not args.no_supplementary:
+        try:
+            supp = {"tensor_path": supplementary_tensor(C, stream)}
+        except Exception as ex:   # never lose the headline line over the supplement
+            supp = {"tensor_path_error": repr(ex)}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -365,14 +430,14 @@ def main():
                 "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "u32 bit-words (boolean)",
                 "data": "synthetic",
-                "config": {**desc, "iterations": iterations, "cells": int(cells),
+                "config": {**desc, "iterations": iterations, "cells": int(cells_total),
                            "results_start_nt": int(results_start), "useful_ops_per_step": int(ops),
                            "l2": "flushed between steps (512 MiB write outside the timed events)",
                            "parallelism": f"{world} independent replicas (seed+rank)" if world > 1 else "1 GPU",
-                           "engine": "sparse semi-naive persistent kernel",
+                           "engine": "dense tcgen05 int8" if pol == 2 else "sparse semi-naive persistent kernel",
                            "seed_phase_ms": statistics.mean(seed_ns) * 1e-6},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-                "gpu_launches": int(launches), "clocks": clk.summary()}
+                "gpu_launches": int(launches), "clocks": clk.summary(), "supplementary": supp}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

@@ -171,7 +171,8 @@ CFPQ_API cfpq_status cfpq_result_lengths(cfpq_result* r, int32_t nt, uint32_t* d
  *   [7] (Δ entry, rule occurrence) expansions, [8] device time of the seed phase (seed,
  *   adjacency build, snapshot seeding) in ns, [9] device time of the fixpoint-loop
  *   kernel launches in ns (CUDA events on the closure stream), [10] CTAs of the closure
- *   kernel, [11..17] single-CTA phase cycle counters (only with record_times).
+ *   kernel, [11..17] single-CTA phase cycle counters (only with record_times), [18] tcgen05
+ *   k-blocks issued by the dense engine (each 128x256x128 int8 MMA work = 2^23 ops).
  * Per-iteration arrays (length = iterations) via cfpq_result_iteration_stats:
  *   new_cells[k-1] = |T_k \ T_{k-1}|, jacobi_triples[k-1] (only with account_work). */
 CFPQ_API cfpq_status cfpq_result_stats(const cfpq_result* r, int64_t* stats, int32_t n_stats);

@@ -111,6 +111,8 @@ struct cfpq_result {
     uint32_t* d_Tn = nullptr;                 // second bit-matrix buffer of the outputs
     std::vector<uint32_t*> Tbase, Tcur, Tnxt;  // per NT
     std::vector<int64_t> dense_new;           // new cells per iteration
+    std::vector<int64_t> dense_jac;           // Jacobi AND-true triples per iteration (account_work)
+    unsigned long long dense_kb = 0;          // issued 128x256x128 int8 MMA k-blocks
     int32_t* d_rowcnt = nullptr;              // bitmap extraction scratch [n+1]
     int32_t* d_rowoff = nullptr;
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
@@ -496,12 +498,19 @@ static cfpq_status run_dense(cfpq_result* r) {
     r->dense_new.clear();
     int64_t k = 0;
     bool capped = false;
+    r->dense_jac.clear();
+    dense_kblocks(r->dense, true);
     cudaEvent_t e0 = r->ev[2], e1 = r->ev[3];
     CFPQ_CUDA_TRY(cudaEventRecord(e0, s));
     for (;;) {
         ++k;
         unsigned long long nw = 0;
         int launches = 0;
+        if (r->opts.account_work) {
+            unsigned long long jt = 0;
+            CFPQ_CUDA_TRY(dense_account(r->dense, r->Tcur.data(), r->rules, s, &jt));
+            r->dense_jac.push_back((int64_t)jt);
+        }
         CFPQ_CUDA_TRY(dense_step(r->dense, r->Tcur.data(), r->Tnxt.data(), k == 1, s, &nw, nullptr, &launches));
         r->launches += launches;
         r->dense_new.push_back((int64_t)nw);
@@ -522,6 +531,7 @@ static cfpq_status run_dense(cfpq_result* r) {
         r->loop_ns = ms * 1e6;
     }
     r->iterations = k;
+    r->dense_kb = dense_kblocks(r->dense, false);
     for (int A = 0; A < r->n_nt; ++A) r->h_nt[A].T = r->Tcur[A];
     CFPQ_CUDA_TRY(cudaMemcpyAsync(r->d_nt, r->h_nt.data(), r->n_nt * sizeof(NTInfo), cudaMemcpyHostToDevice, s));
     CFPQ_CUDA_TRY(cudaStreamSynchronize(s));
@@ -951,13 +961,13 @@ extern "C" cfpq_status cfpq_result_lengths(cfpq_result* r, int32_t nt, uint32_t*
 
 extern "C" cfpq_status cfpq_result_stats(const cfpq_result* r, int64_t* stats, int32_t n_stats) {
     CFPQ_CHECK_ARG(r && stats, "cfpq_result_stats: NULL argument");
-    int64_t v[18] = {r->iterations, (int64_t)r->n_cells, (int64_t)r->log_cap, r->regrows, r->launches,
+    int64_t v[19] = {r->iterations, (int64_t)r->n_cells, (int64_t)r->log_cap, r->regrows, r->launches,
                      r->h_st.solo_iters, (int64_t)r->h_st.candidates, (int64_t)r->h_st.expansions,
                      (int64_t)r->seed_ns, (int64_t)r->loop_ns, (int64_t)r->grid,
                      (int64_t)r->h_st.prof[0], (int64_t)r->h_st.prof[1], (int64_t)r->h_st.prof[2],
                      (int64_t)r->h_st.prof[3], (int64_t)r->h_st.prof[4], (int64_t)r->h_st.prof[5],
-                     (int64_t)r->h_st.prof[6]};
-    for (int k = 0; k < n_stats && k < 18; ++k) stats[k] = v[k];
+                     (int64_t)r->h_st.prof[6], (int64_t)r->dense_kb};
+    for (int k = 0; k < n_stats && k < 19; ++k) stats[k] = v[k];
     return CFPQ_OK;
 }
 
@@ -975,8 +985,15 @@ extern "C" cfpq_status cfpq_result_iteration_stats2(cfpq_result* r, int64_t* new
     if (r->dense_mode) {
         if (new_cells)
             for (int64_t t = 0; t < k; ++t) new_cells[t] = r->dense_new[t];
-        if (jacobi_triples || end_ns) {
-            set_error("work counts / iteration times are recorded by the sparse engine only");
+        if (jacobi_triples) {
+            if ((int64_t)r->dense_jac.size() < k) {
+                set_error("cfpq_result_iteration_stats: run with account_work = 1 for work counts");
+                return CFPQ_E_INVAL;
+            }
+            for (int64_t t = 0; t < k; ++t) jacobi_triples[t] = r->dense_jac[t];
+        }
+        if (end_ns) {
+            set_error("iteration times are recorded by the sparse engine only");
             return CFPQ_E_UNSUPPORTED;
         }
         return CFPQ_OK;

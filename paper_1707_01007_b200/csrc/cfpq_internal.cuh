@@ -195,5 +195,8 @@ void dense_destroy(DenseEngine* e);
 cudaError_t dense_step(DenseEngine* e, uint32_t* const* T, uint32_t* const* Tn, bool first, cudaStream_t s,
                        unsigned long long* new_total, std::vector<unsigned long long>* per_nt, int* launches);
 const std::vector<int32_t>& dense_outputs(const DenseEngine* e);
+unsigned long long dense_kblocks(DenseEngine* e, bool reset);
+cudaError_t dense_account(DenseEngine* e, uint32_t* const* T, const std::vector<Rule3>& rules, cudaStream_t s,
+                          unsigned long long* out);
 
 }  // namespace cfpq

@@ -286,10 +286,12 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
             mbar_wait(tmem_empty, tphase ^ 1);
             tc_fence_after();
             uint32_t acc = 0;
+            unsigned long long kb_issued = 0;
             for (int q = p.rule_ptr[o]; q < p.rule_ptr[o + 1]; ++q) {
                 const DenseRule r = p.rules[q];
                 for (int K = 0; K < n_k; ++K) {
                     if (!kblock_live(p, r, I, J, K)) continue;
+                    ++kb_issued;
                     mbar_wait(&full[stage], phase);
                     tc_fence_after();
                     if (lane == 0) {
@@ -311,6 +313,7 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
                 }
             }
             if (lane == 0) {
+                if (kb_issued) atomicAdd(p.new_cells + p.n_nt + 1, kb_issued);
                 if (acc) umma_commit(tmem_full);   // arrives when all MMAs of the tile completed
                 else mbar_arrive(tmem_full);       // no live K block: the epilogue uses zeros
             }
@@ -417,7 +420,10 @@ struct DenseEngine {
     std::vector<int32_t> h_out;
     CUtensorMap tmA, tmB;
     int grid = 0;
+    unsigned long long kblocks_total = 0;
+    uint32_t* cnt = nullptr;   // accounting scratch
     ~DenseEngine() {
+        cudaFree(cnt);
         cudaFree(T8); cudaFree(T8T); cudaFree(occ); cudaFree(mapA_row); cudaFree(mapB_row); cudaFree(out_nt);
         cudaFree(rule_ptr); cudaFree(rules); cudaFree(Tptr); cudaFree(Tnptr); cudaFree(new_cells);
     }
@@ -478,7 +484,7 @@ DenseEngine* dense_create(int32_t n, int32_t n_nt, int64_t Wp, const std::vector
     if ((c = cudaMalloc(&e->rules, std::max<size_t>(1, rl.size()) * sizeof(DenseRule))) != cudaSuccess) return fail("tables", c);
     if ((c = cudaMalloc(&e->Tptr, n_nt * sizeof(void*))) != cudaSuccess) return fail("tables", c);
     if ((c = cudaMalloc(&e->Tnptr, n_nt * sizeof(void*))) != cudaSuccess) return fail("tables", c);
-    if ((c = cudaMalloc(&e->new_cells, (n_nt + 1) * 8)) != cudaSuccess) return fail("counters", c);
+    if ((c = cudaMalloc(&e->new_cells, (n_nt + 2) * 8)) != cudaSuccess) return fail("counters", c);
     cudaMemcpyAsync(e->mapA_row, e->h_mapA.data(), n_nt * 8, cudaMemcpyHostToDevice, s);
     cudaMemcpyAsync(e->mapB_row, e->h_mapB.data(), n_nt * 8, cudaMemcpyHostToDevice, s);
     if (e->n_out) cudaMemcpyAsync(e->out_nt, e->h_out.data(), e->n_out * 4, cudaMemcpyHostToDevice, s);
@@ -521,7 +527,7 @@ cudaError_t dense_step(DenseEngine* e, uint32_t* const* T, uint32_t* const* Tn, 
         return c;
     if ((c = cudaMemcpyAsync((void*)e->Tnptr, Tn, e->n_nt * sizeof(void*), cudaMemcpyHostToDevice, s)) != cudaSuccess)
         return c;
-    if ((c = cudaMemsetAsync(e->new_cells, 0, (e->n_nt + 1) * 8, s)) != cudaSuccess) return c;
+    if ((c = cudaMemsetAsync(e->new_cells, 0, (e->n_nt + 2) * 8, s)) != cudaSuccess) return c;
     DenseParams p{};
     p.n = e->n;
     p.np = e->np;
@@ -541,12 +547,86 @@ cudaError_t dense_step(DenseEngine* e, uint32_t* const* T, uint32_t* const* Tn, 
         if ((c = cudaGetLastError()) != cudaSuccess) return c;
         if (launches) ++*launches;
     }
-    std::vector<unsigned long long> h(e->n_nt + 1);
-    if ((c = cudaMemcpyAsync(h.data(), e->new_cells, (e->n_nt + 1) * 8, cudaMemcpyDeviceToHost, s)) != cudaSuccess)
+    std::vector<unsigned long long> h(e->n_nt + 2);
+    if ((c = cudaMemcpyAsync(h.data(), e->new_cells, (e->n_nt + 2) * 8, cudaMemcpyDeviceToHost, s)) != cudaSuccess)
         return c;
     if ((c = cudaStreamSynchronize(s)) != cudaSuccess) return c;
     *new_total = h[e->n_nt];
-    if (per_nt) per_nt->assign(h.begin(), h.end() - 1);
+    e->kblocks_total += h[e->n_nt + 1];
+    if (per_nt) per_nt->assign(h.begin(), h.begin() + e->n_nt);
+    return cudaSuccess;
+}
+
+// Issued MMA k-blocks (128 x 256 x 128 int8 each) since the last reset.
+unsigned long long dense_kblocks(DenseEngine* e, bool reset) {
+    unsigned long long v = e->kblocks_total;
+    if (reset) e->kblocks_total = 0;
+    return v;
+}
+
+// ---- Jacobi work accounting (untimed diagnostics): Σ_rules Σ_r |col r of T_B| · |row r of T_C| ----
+__global__ void colcount_kernel(const uint32_t* __restrict__ T, int32_t n, int64_t Wp, int32_t rows_per, uint32_t* cnt) {
+    int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;   // column word
+    if (w * 32 >= n) return;
+    uint32_t c[32];
+#pragma unroll
+    for (int b = 0; b < 32; ++b) c[b] = 0;
+    int r0 = blockIdx.y * rows_per, r1 = min(n, r0 + rows_per);
+    for (int r = r0; r < r1; ++r) {
+        uint32_t v = __ldg(T + (size_t)r * Wp + w);
+#pragma unroll
+        for (int b = 0; b < 32; ++b) c[b] += (v >> b) & 1u;
+    }
+#pragma unroll
+    for (int b = 0; b < 32; ++b)
+        if (c[b] && w * 32 + b < n) atomicAdd(cnt + w * 32 + b, c[b]);
+}
+
+__global__ void rowcount_kernel(const uint32_t* __restrict__ T, int32_t n, int64_t Wp, uint32_t* cnt) {
+    int lane = threadIdx.x & 31;
+    for (int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; row < n;
+         row += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        uint32_t c = 0;
+        for (int64_t w = lane; w * 32 < n; w += 32) c += __popc(__ldg(T + (size_t)row * Wp + w));
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+        if (lane == 0) cnt[row] = c;
+    }
+}
+
+__global__ void dot_kernel(const uint32_t* __restrict__ a, const uint32_t* __restrict__ b, int32_t n,
+                           unsigned long long* out) {
+    unsigned long long acc = 0;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x)
+        acc += (unsigned long long)a[t] * b[t];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0 && acc) atomicAdd(out, acc);
+}
+
+cudaError_t dense_account(DenseEngine* e, uint32_t* const* T, const std::vector<Rule3>& rules, cudaStream_t s,
+                          unsigned long long* out) {
+    cudaError_t c;
+    if (!e->cnt) {
+        if ((c = cudaMalloc(&e->cnt, (size_t)2 * e->n * 4 + 64)) != cudaSuccess) return c;
+    }
+    uint32_t* colB = e->cnt;
+    uint32_t* rowC = e->cnt + e->n;
+    unsigned long long* acc = (unsigned long long*)(e->cnt + 2 * (size_t)e->n);
+    acc = (unsigned long long*)(((uintptr_t)acc + 7) & ~uintptr_t(7));
+    if ((c = cudaMemsetAsync(acc, 0, 8, s)) != cudaSuccess) return c;
+    const int rows_per = 1024;
+    for (auto& r : rules) {
+        if ((c = cudaMemsetAsync(colB, 0, (size_t)e->n * 4, s)) != cudaSuccess) return c;
+        dim3 g((unsigned)(((e->n + 31) / 32 + 127) / 128), (unsigned)((e->n + rows_per - 1) / rows_per));
+        colcount_kernel<<<g, 128, 0, s>>>(T[r.B], e->n, e->Wp, rows_per, colB);
+        rowcount_kernel<<<148 * 8, 256, 0, s>>>(T[r.C], e->n, e->Wp, rowC);
+        dot_kernel<<<148 * 4, 256, 0, s>>>(colB, rowC, e->n, acc);
+    }
+    unsigned long long v = 0;
+    if ((c = cudaMemcpyAsync(&v, acc, 8, cudaMemcpyDeviceToHost, s)) != cudaSuccess) return c;
+    if ((c = cudaStreamSynchronize(s)) != cudaSuccess) return c;
+    *out = v;
     return cudaSuccess;
 }
 

@@ -84,12 +84,15 @@ def main():
     for name, (c, t) in sorted(L.items(), key=lambda x: -x[1][1]):
         lines.append(f"| `{name}` | {c} | {t:.1f} | {100 * t / T:.1f}% |")
     lines += ["", "(units of gpu__time_duration.sum as reported by ncu: ns or us per the CSV)", "",
-              "## closure_kernel (full set)", "", "| metric | value |", "|---|---|"]
+              "## profiled kernel (full set)", "", "| metric | value |", "|---|---|"]
     for k in ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
               "gpu__compute_memory_throughput.avg.pct_of_peak_sustained_elapsed",
               "sm__throughput.avg.pct_of_peak_sustained_elapsed", "sm__warps_active.avg.pct_of_peak_sustained_active",
               "launch__registers_per_thread", "launch__grid_size", "launch__block_size",
-              "lts__t_sectors_srcunit_tex_op_atom.sum", "smsp__inst_executed.sum"]:
+              "lts__t_sectors_srcunit_tex_op_atom.sum", "smsp__inst_executed.sum",
+              "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
+              "sm__inst_executed_pipe_uniform.avg.pct_of_peak_sustained_active",
+              "lts__t_bytes.sum", "l1tex__t_bytes.sum"]:
         if k in m:
             lines.append(f"| {k} | {m[k][0]} {m[k][1]} |")
     for (sec, name), (v, u) in d.items():
@@ -101,7 +104,7 @@ def main():
         lines.append(f"| {share:.1f}% | {idx} | `{src}` |")
     with open(prefix + ".md", "w") as f:
         f.write("\n".join(lines) + "\n")
-    tj = os.path.join(os.path.dirname(prefix), "closure_kernel_traffic.json")
+    tj = os.path.join(os.path.dirname(prefix), "closure_kernel_traffic.json")   # per-workload dominant kernel
     try:
         data = json.load(open(tj))
     except Exception:

@@ -44,10 +44,11 @@ def test_tensor_example_and_iterations(example_golden):
 def test_tensor_dense_stress_parity(n, d):
     """S -> S S | a (both operands change): several 128x256 tiles and K blocks, ragged n."""
     w = I.dense_stress_workload(n, d, seed=n)
-    r, _, _ = gpu_closure(w, path_policy=2)
+    r, _, _ = gpu_closure(w, path_policy=2, account_work=True)
     ores = assert_parity(w, r)
-    nc, _ = r.iteration_stats()
+    nc, jt = r.iteration_stats(work=True)
     assert nc.tolist() == ores.stats()["new_bits"].tolist()
+    assert jt.tolist() == ores.stats()["jacobi_triples"].tolist()
 
 
 @pytest.mark.parametrize("n,d", [(1000, 2), (2048, 1), (1537, 4)])
