@@ -308,14 +308,26 @@ def main():
     stream = torch.cuda.current_stream()
     dev_index = torch.cuda.current_device()
 
-    w, desc = make_workload(args.workload, args.seed + rank)
+    # config S shards ONE problem by row blocks over NCCL (strong scaling); the other
+    # workloads close one independent seeded problem per GPU (weak scaling, no collective)
+    sharded = args.workload == "configS" and world > 1
+    w, desc = make_workload(args.workload, args.seed + (0 if sharded else rank))
+    shard_kw = {}
+    if sharded:
+        uid = torch.zeros(128, dtype=torch.uint8, device="cuda")
+        if rank == 0:
+            uid.copy_(torch.tensor(list(C.nccl_unique_id()), dtype=torch.uint8))
+        dist.broadcast(uid, src=0)
+        shard_kw = {"world_size": world, "rank": rank, "nccl_unique_id": bytes(uid.cpu().tolist())}
     lengths = args.workload == "config5"
     g = C.Grammar.from_workload(w)
     edges_dev = torch.from_numpy(w.edges).cuda()
     d = C.Graph(w.n_nodes, edges_dev, stream=stream)
     ops = jacobi_ops(w, args.workload, g, d, C, stream)
+    if sharded:
+        ops = ops // world   # one problem split over the ranks: count its work once in total
     pol = policy_for(args.workload)
-    r = C.closure(g, d, stream=stream, semantics=int(lengths), solo_threshold=args.solo, path_policy=pol)
+    r = C.closure(g, d, stream=stream, semantics=int(lengths), solo_threshold=args.solo, path_policy=pol, **shard_kw)
     iterations = r.iterations
     cells = r.stats()["cells"]
     cells_total = sum(r.count(A) for A in range(w.n_nt)) if pol == 2 else cells
@@ -326,7 +338,8 @@ def main():
     # L2 flush buffer (> 126 MB L2), written between timed steps, outside the events
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
     for _ in range(args.warmup):
-        C.closure_reuse(g, d, r, stream=stream, semantics=int(lengths), solo_threshold=args.solo, path_policy=pol)
+        C.closure_reuse(g, d, r, stream=stream, semantics=int(lengths), solo_threshold=args.solo, path_policy=pol,
+                            **shard_kw)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -340,7 +353,8 @@ def main():
         for _ in range(args.steps):
             flush.fill_(1)
             ev0.record(stream)
-            C.closure_reuse(g, d, r, stream=stream, semantics=int(lengths), solo_threshold=args.solo, path_policy=pol)
+            C.closure_reuse(g, d, r, stream=stream, semantics=int(lengths), solo_threshold=args.solo, path_policy=pol,
+                            **shard_kw)
             ev1.record(stream)
             ev1.synchronize()
             step_ms.append(ev0.elapsed_time(ev1))
@@ -400,7 +414,8 @@ def main():
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             d.set_edges(pinned, stream=stream)
-            C.closure_reuse(g, d, r, stream=stream, semantics=int(lengths), solo_threshold=args.solo, path_policy=pol)
+            C.closure_reuse(g, d, r, stream=stream, semantics=int(lengths), solo_threshold=args.solo, path_policy=pol,
+                            **shard_kw)
             pairs = r.pairs(w.start)
             t1 = time.perf_counter()
             if it >= args.warmup:
@@ -428,12 +443,15 @@ def main():
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "u32 bit-words (boolean)",
+                "scaling": "strong" if sharded else "weak", "vs_baseline": None,
+                "dtype": "int8 0/1 tiles -> s32 (tcgen05)" if pol == 2 else "u32 bit-words (boolean)",
                 "data": "synthetic",
                 "config": {**desc, "iterations": iterations, "cells": int(cells_total),
                            "results_start_nt": int(results_start), "useful_ops_per_step": int(ops),
                            "l2": "flushed between steps (512 MiB write outside the timed events)",
-                           "parallelism": f"{world} independent replicas (seed+rank)" if world > 1 else "1 GPU",
+                           "parallelism": (f"row-block sharded over {world} GPUs (NCCL all-gather per iteration)"
+                                           if sharded else f"{world} independent replicas (seed+rank)")
+                           if world > 1 else "1 GPU",
                            "engine": "dense tcgen05 int8" if pol == 2 else "sparse semi-naive persistent kernel",
                            "seed_phase_ms": statistics.mean(seed_ns) * 1e-6},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,

@@ -106,16 +106,22 @@ typedef struct {
                                 (the work of Alg. 1 line 9 on sparse operands); slower     */
     int64_t max_iterations;  /* 0 = |V|^2 |N| + 1 (Theorem 3)                   */
     void*   cuda_stream;     /* cudaStream_t to run on (NULL = default stream)             */
-    int32_t world_size;      /* 1 = single GPU                                             */
+    int32_t world_size;      /* > 1: this process is `rank` of world_size GPUs; every T_A is
+                                row-block sharded (cfpq_shard_rows) and the blocks are
+                                all-gathered over NCCL after every iteration (dense engine,
+                                path_policy 2).  Every rank passes identical inputs.         */
     int32_t rank;
-    const void* nccl_unique_id;  /* reserved for world_size > 1                            */
+    const void* nccl_unique_id;  /* world_size > 1: the 128-byte ncclUniqueId from
+                                cfpq_nccl_unique_id on one rank, broadcast to all ranks      */
     int64_t log_capacity;    /* initial capacity (cells) of the derived-cell log; 0 = auto */
     int32_t solo_threshold;  /* |Δ| at or below which one CTA runs iterations alone; -1 =
                                 auto (1024), 0 = only for an empty Δ                       */
     int32_t record_times;    /* 1: record a device timestamp per iteration (diagnostics,
                                 cfpq_result_iteration_stats2)                              */
     int32_t max_ctas;        /* diagnostics: limit the closure kernel's grid (0 = full)    */
-    int32_t reserved[5];     /* must be zero                                               */
+    int32_t reserved_emulate;/* testing: > 1 runs that many row-block shards in this process
+                                on one GPU (the multi-GPU partition without NCCL)           */
+    int32_t reserved[4];     /* must be zero                                               */
 } cfpq_options;
 
 CFPQ_API void cfpq_options_default(cfpq_options* o);
@@ -182,6 +188,16 @@ CFPQ_API cfpq_status cfpq_result_iteration_stats(cfpq_result* r, int64_t* new_ce
  * the end of iteration k (iterations past 2^22 are not recorded). */
 CFPQ_API cfpq_status cfpq_result_iteration_stats2(cfpq_result* r, int64_t* new_cells, int64_t* jacobi_triples,
                                                   int64_t* end_ns, int64_t capacity);
+
+/* Multi-GPU bootstrap: write a fresh ncclUniqueId (128 bytes) into out[bytes].  NCCL is
+ * loaded at run time (libnccl.so.2); CFPQ_E_NCCL if it is unavailable. */
+CFPQ_API cfpq_status cfpq_nccl_unique_id(void* out, int64_t bytes);
+
+/* Rows [row_lo, row_hi) of every T_A that `rank` of world_size computes under row-block
+ * sharding (blocks of 128-row tiles; "matrix multiplication in the main loop ... may
+ * be performed on different GPGPU independently").  Pure host function. */
+CFPQ_API cfpq_status cfpq_shard_rows(int64_t n_nodes, int32_t world_size, int32_t rank, int64_t* row_lo,
+                                     int64_t* row_hi);
 
 /* Thread-local message describing the last non-OK status. */
 CFPQ_API const char* cfpq_last_error(void);

@@ -29,7 +29,7 @@ EXPORTS = [
     "cfpq_result_destroy", "cfpq_result_iterations", "cfpq_result_count", "cfpq_result_count_at",
     "cfpq_result_pairs", "cfpq_result_pairs_at", "cfpq_result_matrix", "cfpq_result_lengths",
     "cfpq_result_stats", "cfpq_result_iteration_stats", "cfpq_result_iteration_stats2", "cfpq_last_error",
-    "cfpq_version",
+    "cfpq_version", "cfpq_nccl_unique_id", "cfpq_shard_rows",
 ]
 
 
@@ -46,7 +46,8 @@ class Options(ctypes.Structure):
                 ("world_size", ctypes.c_int32), ("rank", ctypes.c_int32),
                 ("nccl_unique_id", ctypes.c_void_p), ("log_capacity", ctypes.c_int64),
                 ("solo_threshold", ctypes.c_int32), ("record_times", ctypes.c_int32),
-                ("max_ctas", ctypes.c_int32), ("reserved", ctypes.c_int32 * 5)]
+                ("max_ctas", ctypes.c_int32), ("emulate_ranks", ctypes.c_int32),
+                ("reserved", ctypes.c_int32 * 4)]
 
 
 _lib = None
@@ -84,6 +85,8 @@ def load() -> ctypes.CDLL:
         "cfpq_result_iteration_stats2": (i32, [vp, vp, vp, vp, i64]),
         "cfpq_last_error": (ctypes.c_char_p, []),
         "cfpq_version": (ctypes.c_char_p, []),
+        "cfpq_nccl_unique_id": (i32, [vp, i64]),
+        "cfpq_shard_rows": (i32, [i64, i32, i32, P(i64), P(i64)]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -180,7 +183,8 @@ class Graph:
 
 def options(semantics: int = 0, schedule: int = 0, path_policy: int = 0, account_work: bool = False,
             max_iterations: int = 0, stream=None, log_capacity: int = 0, solo_threshold: int = -1,
-            record_times: bool = False, max_ctas: int = 0) -> Options:
+            record_times: bool = False, max_ctas: int = 0, world_size: int = 1, rank: int = 0,
+            nccl_unique_id=None, emulate_ranks: int = 0) -> Options:
     o = Options()
     load().cfpq_options_default(ctypes.byref(o))
     o.semantics, o.schedule, o.path_policy = int(semantics), int(schedule), int(path_policy)
@@ -191,7 +195,29 @@ def options(semantics: int = 0, schedule: int = 0, path_policy: int = 0, account
     o.solo_threshold = int(solo_threshold)
     o.record_times = int(bool(record_times))
     o.max_ctas = int(max_ctas)
+    o.world_size = int(world_size)
+    o.rank = int(rank)
+    o.emulate_ranks = int(emulate_ranks)
+    if nccl_unique_id is not None:
+        buf = ctypes.create_string_buffer(bytes(nccl_unique_id), 128)
+        o._uid = buf                     # keep alive with the options
+        o.nccl_unique_id = ctypes.cast(buf, ctypes.c_void_p)
     return o
+
+
+def nccl_unique_id() -> bytes:
+    """cfpq_nccl_unique_id: 128 bytes to broadcast to every rank (torch.distributed)."""
+    buf = ctypes.create_string_buffer(128)
+    _check(load().cfpq_nccl_unique_id(buf, 128), "cfpq_nccl_unique_id")
+    return buf.raw
+
+
+def shard_rows(n_nodes: int, world_size: int, rank: int) -> Tuple[int, int]:
+    """cfpq_shard_rows: the row block [lo, hi) that `rank` computes."""
+    lo, hi = ctypes.c_int64(), ctypes.c_int64()
+    _check(load().cfpq_shard_rows(int(n_nodes), int(world_size), int(rank), ctypes.byref(lo), ctypes.byref(hi)),
+           "cfpq_shard_rows")
+    return lo.value, hi.value
 
 
 class Result:

@@ -113,6 +113,12 @@ struct cfpq_result {
     std::vector<int64_t> dense_new;           // new cells per iteration
     std::vector<int64_t> dense_jac;           // Jacobi AND-true triples per iteration (account_work)
     unsigned long long dense_kb = 0;          // issued 128x256x128 int8 MMA k-blocks
+    int32_t n_ranks = 1;                      // row-block shards (NCCL ranks or emulated)
+    int32_t my_rank = 0;
+    bool emulated = false;
+    void* comm = nullptr;                     // ncclComm_t (world_size > 1)
+    int64_t rows_alloc = 0;                   // bit-matrix rows allocated (>= n, multiple of blocks)
+    int64_t block_rows = 0;                   // rows per shard block (dense engine)
     int32_t* d_rowcnt = nullptr;              // bitmap extraction scratch [n+1]
     int32_t* d_rowoff = nullptr;
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
@@ -127,6 +133,7 @@ struct cfpq_result {
         dfree(d_iter_off); dfree(d_jac); dfree(d_iter_time); dfree(d_rowc); dfree(d_colc); dfree(d_temp); dfree(d_keys);
         dfree(d_small); dfree(d_Tn); dfree(d_rowcnt); dfree(d_rowoff);
         if (dense) dense_destroy(dense);
+        if (comm) nccl_comm_destroy(comm);
     }
 
     EngineParams params() const {
@@ -323,7 +330,25 @@ static cfpq_status plan(cfpq_result* r, const cfpq_grammar* g, const cfpq_graph*
         r->max_rules_per_label = std::max(r->max_rules_per_label, lab_ptr[x + 1] - lab_ptr[x]);
 
     cfpq_status st;
-    const size_t mat_words = (size_t)n * (size_t)r->Wp;
+    const bool use_nccl = o->nccl_unique_id != nullptr && o->path_policy == 2;
+    r->n_ranks = o->world_size > 1 ? o->world_size : (o->reserved_emulate > 1 ? o->reserved_emulate : 1);
+    r->emulated = !use_nccl && r->n_ranks > 1;
+    r->my_rank = o->world_size > 1 ? o->rank : 0;
+    r->rows_alloc = n;
+    if (o->path_policy == 2) {
+        int64_t tlo, thi;
+        dense_partition(n, r->n_ranks, 0, &tlo, &thi, &r->block_rows);
+        r->rows_alloc = std::max<int64_t>(n, r->block_rows * r->n_ranks);
+    }
+    if (use_nccl) {
+        std::string err;
+        r->comm = nccl_comm_create(o->nccl_unique_id, r->n_ranks, r->my_rank, &err);
+        if (!r->comm) {
+            set_error(err);
+            return CFPQ_E_NCCL;
+        }
+    }
+    const size_t mat_words = (size_t)r->rows_alloc * (size_t)r->Wp;
     if ((st = dalloc(&r->d_T, mat_words * g->n_nt, "T bit matrices")) != CFPQ_OK) return st;
     CFPQ_CUDA_TRY(cudaMemsetAsync(r->d_T, 0, mat_words * g->n_nt * 4, r->stream));
     int n_snap = 0;
@@ -493,8 +518,10 @@ static cfpq_status run_dense(cfpq_result* r) {
     const auto& outs = dense_outputs(r->dense);
     r->Tcur = r->Tbase;
     r->Tnxt.assign(r->n_nt, nullptr);
-    const size_t mw = (size_t)r->n * (size_t)r->Wp;
+    const size_t mw = (size_t)r->rows_alloc * (size_t)r->Wp;
     for (size_t q = 0; q < outs.size(); ++q) r->Tnxt[outs[q]] = r->d_Tn + q * mw;
+    const int64_t tiles = dense_row_tiles(r->dense);
+    std::vector<uint32_t*> out_mats(outs.size());
     r->dense_new.clear();
     int64_t k = 0;
     bool capped = false;
@@ -511,7 +538,31 @@ static cfpq_status run_dense(cfpq_result* r) {
             CFPQ_CUDA_TRY(dense_account(r->dense, r->Tcur.data(), r->rules, s, &jt));
             r->dense_jac.push_back((int64_t)jt);
         }
-        CFPQ_CUDA_TRY(dense_step(r->dense, r->Tcur.data(), r->Tnxt.data(), k == 1, s, &nw, nullptr, &launches));
+        CFPQ_CUDA_TRY(dense_begin(r->dense, r->Tcur.data(), r->Tnxt.data(), k == 1, s, &launches));
+        if (r->n_ranks == 1 && !r->comm) {
+            CFPQ_CUDA_TRY(dense_product(r->dense, 0, tiles, s, &launches));
+        } else if (r->emulated) {
+            // P row-block shards in one process: each writes its rows of the shared T_k
+            for (int g = 0; g < r->n_ranks; ++g) {
+                int64_t lo, hi, br;
+                dense_partition(r->n, r->n_ranks, g, &lo, &hi, &br);
+                CFPQ_CUDA_TRY(dense_product(r->dense, lo, hi, s, &launches));
+            }
+        } else {
+            int64_t lo, hi, br;
+            dense_partition(r->n, r->n_ranks, r->my_rank, &lo, &hi, &br);
+            CFPQ_CUDA_TRY(dense_product(r->dense, lo, hi, s, &launches));
+            // all-gather every rank's row block of T_k, sum the new-cell counts (the
+            // "changed" flag) — one NCCL group over NVLink per iteration
+            for (size_t q = 0; q < outs.size(); ++q) out_mats[q] = r->Tnxt[outs[q]];
+            std::string err;
+            if (!nccl_exchange_rows(r->comm, out_mats.data(), (int)outs.size(), (size_t)br * r->Wp, r->my_rank,
+                                    dense_total_counter(r->dense), s, &err)) {
+                set_error(err);
+                return CFPQ_E_NCCL;
+            }
+        }
+        CFPQ_CUDA_TRY(dense_finish(r->dense, s, &nw));
         r->launches += launches;
         r->dense_new.push_back((int64_t)nw);
         for (int A : outs) std::swap(r->Tcur[A], r->Tnxt[A]);
@@ -555,7 +606,7 @@ static cfpq_status run(cfpq_result* r, const cfpq_graph* d) {
         // the dense engine rewrites whole matrices: restore the base buffers and clear them
         for (int A = 0; A < r->n_nt; ++A) r->h_nt[A].T = r->Tbase[A];
         CFPQ_CUDA_TRY(cudaMemcpyAsync(r->d_nt, r->h_nt.data(), r->n_nt * sizeof(NTInfo), cudaMemcpyHostToDevice, s));
-        const size_t mw = (size_t)r->n * (size_t)r->Wp;
+        const size_t mw = (size_t)r->rows_alloc * (size_t)r->Wp;
         CFPQ_CUDA_TRY(cudaMemsetAsync(r->d_T, 0, mw * r->n_nt * 4, s));
         CFPQ_CUDA_TRY(cudaMemsetAsync(r->d_Tn, 0, mw * std::max<size_t>(dense_outputs(r->dense).size(), 1) * 4, s));
         r->n_cells = 0;
@@ -670,7 +721,16 @@ static cfpq_status check_inputs(const cfpq_grammar* g, const cfpq_graph* d, cons
     CFPQ_CHECK_ARG(g != nullptr && d != nullptr && o != nullptr, "cfpq_closure: NULL grammar/graph/options");
     CFPQ_CHECK_ARG(o->semantics == 0 || o->semantics == 1, "cfpq_closure: semantics must be 0 or 1");
     CFPQ_CHECK_ARG(o->schedule == 0 || o->schedule == 1, "cfpq_closure: schedule must be 0 (jacobi) or 1 (seminaive)");
-    CFPQ_CHECK_ARG(o->world_size <= 1, "cfpq_closure: world_size > 1 is not supported by this build");
+    CFPQ_CHECK_ARG(o->world_size >= 0 && o->reserved_emulate >= 0, "cfpq_closure: bad world_size / emulate_ranks");
+    if ((o->world_size > 1 || o->reserved_emulate > 1) && o->path_policy != 2) {
+        set_error("cfpq_closure: row-block sharding is implemented for the dense engine (path_policy 2); "
+                  "the sparse engine runs one problem per GPU");
+        return CFPQ_E_UNSUPPORTED;
+    }
+    if (o->world_size > 1) {
+        CFPQ_CHECK_ARG(o->rank >= 0 && o->rank < o->world_size, "cfpq_closure: rank out of range");
+        CFPQ_CHECK_ARG(o->nccl_unique_id != nullptr, "cfpq_closure: world_size > 1 needs nccl_unique_id");
+    }
     if (o->path_policy == 3) {
         set_error("cfpq_closure: path_policy 3 (rows) not available in this build");
         return CFPQ_E_UNSUPPORTED;
@@ -1020,6 +1080,28 @@ extern "C" cfpq_status cfpq_result_iteration_stats2(cfpq_result* r, int64_t* new
 }
 
 extern "C" const char* cfpq_last_error(void) { return g_last_error.c_str(); }
+
+extern "C" cfpq_status cfpq_nccl_unique_id(void* out, int64_t bytes) {
+    CFPQ_CHECK_ARG(out != nullptr, "cfpq_nccl_unique_id: out is NULL");
+    CFPQ_CHECK_ARG(bytes >= (int64_t)nccl_unique_id_bytes(), "cfpq_nccl_unique_id: buffer smaller than 128 bytes");
+    std::string err;
+    if (!nccl_unique_id(out, &err)) {
+        set_error(err);
+        return CFPQ_E_NCCL;
+    }
+    return CFPQ_OK;
+}
+
+extern "C" cfpq_status cfpq_shard_rows(int64_t n_nodes, int32_t world_size, int32_t rank, int64_t* row_lo,
+                                       int64_t* row_hi) {
+    CFPQ_CHECK_ARG(row_lo && row_hi, "cfpq_shard_rows: NULL argument");
+    CFPQ_CHECK_ARG(n_nodes >= 0 && world_size >= 1 && rank >= 0 && rank < world_size, "cfpq_shard_rows: bad argument");
+    int64_t lo, hi, br;
+    dense_partition(n_nodes, world_size, rank, &lo, &hi, &br);
+    *row_lo = std::min<int64_t>(lo * 128, n_nodes);
+    *row_hi = std::min<int64_t>(hi * 128, n_nodes);
+    return CFPQ_OK;
+}
 
 extern "C" const char* cfpq_version(void) {
     return "libcfpq 0.1 sm_100a (sparse semi-naive persistent engine)";

@@ -192,8 +192,21 @@ struct DenseEngine;
 DenseEngine* dense_create(int32_t n, int32_t n_nt, int64_t Wp, const std::vector<Rule3>& rules,
                           const std::vector<int32_t>& is_const, cudaStream_t s, std::string* err);
 void dense_destroy(DenseEngine* e);
-cudaError_t dense_step(DenseEngine* e, uint32_t* const* T, uint32_t* const* Tn, bool first, cudaStream_t s,
-                       unsigned long long* new_total, std::vector<unsigned long long>* per_nt, int* launches);
+cudaError_t dense_begin(DenseEngine* e, uint32_t* const* T, uint32_t* const* Tn, bool first, cudaStream_t s,
+                        int* launches);
+cudaError_t dense_product(DenseEngine* e, int64_t i_lo, int64_t i_hi, cudaStream_t s, int* launches);
+cudaError_t dense_finish(DenseEngine* e, cudaStream_t s, unsigned long long* new_total);
+unsigned long long* dense_total_counter(DenseEngine* e);
+int64_t dense_row_tiles(const DenseEngine* e);
+
+// multi-GPU plumbing, comm.cu
+bool nccl_unique_id(void* out, std::string* err);
+size_t nccl_unique_id_bytes();
+void* nccl_comm_create(const void* id_bytes, int world, int rank, std::string* err);
+void nccl_comm_destroy(void* comm);
+bool nccl_exchange_rows(void* comm, uint32_t* const* mats, int n_mats, size_t block_words, int rank,
+                        unsigned long long* counter, cudaStream_t s, std::string* err);
+void dense_partition(int64_t n, int world, int rank, int64_t* tile_lo, int64_t* tile_hi, int64_t* block_rows);
 const std::vector<int32_t>& dense_outputs(const DenseEngine* e);
 unsigned long long dense_kblocks(DenseEngine* e, bool reset);
 cudaError_t dense_account(DenseEngine* e, uint32_t* const* T, const std::vector<Rule3>& rules, cudaStream_t s,

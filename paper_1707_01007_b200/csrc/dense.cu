@@ -50,7 +50,7 @@ struct DenseParams {
     int32_t nt_tiles;              // np / 128
     unsigned long long* new_cells; // [n_nt + 1] new cells per NT, [n_nt] = total
     int32_t n_nt;
-    unsigned long long mma_tiles;  // diagnostics (unused on device)
+    int32_t i_lo, i_hi;            // row-tile range of this rank (row-block sharding)
 };
 
 // ------------------------------------------------------------------------------------------
@@ -225,7 +225,8 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
     uint32_t* tmem_base_smem = reinterpret_cast<uint32_t*>(tmem_empty + 1);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int n_i = p.np / kTM, n_j = p.np / kTN;
+    const int n_j = p.np / kTN;
+    const int n_i = p.i_hi - p.i_lo;
     const int tiles_per_nt = n_i * n_j;
     const int total_tiles = tiles_per_nt * p.n_out;
     const int n_k = p.np / kTK;
@@ -254,7 +255,7 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
             uint32_t phase = 0;
             for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
                 const int o = t / tiles_per_nt, rem = t - o * tiles_per_nt;
-                const int I = rem / n_j, J = rem - (rem / n_j) * n_j;
+                const int I = p.i_lo + rem / n_j, J = rem - (rem / n_j) * n_j;
                 for (int q = p.rule_ptr[o]; q < p.rule_ptr[o + 1]; ++q) {
                     const DenseRule r = p.rules[q];
                     const int64_t arow = __ldg(mapA_row + r.B) + (int64_t)I * kTM;
@@ -281,7 +282,7 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
         uint32_t tphase = 0;
         for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
             const int o = t / tiles_per_nt, rem = t - o * tiles_per_nt;
-            const int I = rem / n_j, J = rem - (rem / n_j) * n_j;
+            const int I = p.i_lo + rem / n_j, J = rem - (rem / n_j) * n_j;
             // the epilogue must have drained the accumulator of the previous tile
             mbar_wait(tmem_empty, tphase ^ 1);
             tc_fence_after();
@@ -327,7 +328,7 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
         unsigned long long my_new = 0;
         for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
             const int o = t / tiles_per_nt, rem = t - o * tiles_per_nt;
-            const int I = rem / n_j, J = rem - (rem / n_j) * n_j;
+            const int I = p.i_lo + rem / n_j, J = rem - (rem / n_j) * n_j;
             const int A = p.out_nt[o];
             bool live = false;
             for (int q = p.rule_ptr[o]; q < p.rule_ptr[o + 1] && !live; ++q)
@@ -507,10 +508,12 @@ DenseEngine* dense_create(int32_t n, int32_t n_nt, int64_t Wp, const std::vector
     return e;
 }
 
-// One Jacobi iteration: T (T_{k-1}, all NTs) -> Tn (T_k, outputs).  Returns the new cells
-// of iteration k (total and per NT) on the host.
-cudaError_t dense_step(DenseEngine* e, uint32_t* const* T, uint32_t* const* Tn, bool first, cudaStream_t s,
-                       unsigned long long* new_total, std::vector<unsigned long long>* per_nt, int* launches) {
+// One Jacobi iteration in three parts (so that a multi-GPU exchange can sit between the
+// product and the read-back): begin = packs of the operands of T_{k-1} + counter reset;
+// product = T_k rows of row tiles [i_lo, i_hi) of every output; finish = read the new-cell
+// counters (device -> host).
+cudaError_t dense_begin(DenseEngine* e, uint32_t* const* T, uint32_t* const* Tn, bool first, cudaStream_t s,
+                        int* launches) {
     const size_t pack = (size_t)e->np * e->np;
     for (int X = 0; X < e->n_nt; ++X) {
         if (!(e->packA[X] || e->packB[X])) continue;
@@ -523,11 +526,16 @@ cudaError_t dense_step(DenseEngine* e, uint32_t* const* T, uint32_t* const* Tn, 
         if (launches) ++*launches;
     }
     cudaError_t c;
+    if ((c = cudaGetLastError()) != cudaSuccess) return c;
     if ((c = cudaMemcpyAsync((void*)e->Tptr, T, e->n_nt * sizeof(void*), cudaMemcpyHostToDevice, s)) != cudaSuccess)
         return c;
     if ((c = cudaMemcpyAsync((void*)e->Tnptr, Tn, e->n_nt * sizeof(void*), cudaMemcpyHostToDevice, s)) != cudaSuccess)
         return c;
-    if ((c = cudaMemsetAsync(e->new_cells, 0, (e->n_nt + 2) * 8, s)) != cudaSuccess) return c;
+    return cudaMemsetAsync(e->new_cells, 0, (e->n_nt + 2) * 8, s);
+}
+
+cudaError_t dense_product(DenseEngine* e, int64_t i_lo, int64_t i_hi, cudaStream_t s, int* launches) {
+    if (e->n_out == 0 || i_hi <= i_lo) return cudaSuccess;
     DenseParams p{};
     p.n = e->n;
     p.np = e->np;
@@ -542,20 +550,31 @@ cudaError_t dense_step(DenseEngine* e, uint32_t* const* T, uint32_t* const* Tn, 
     p.nt_tiles = e->nt_tiles;
     p.new_cells = e->new_cells;
     p.n_nt = e->n_nt;
-    if (e->n_out) {
-        dense_kernel<<<e->grid, kDenseThreads, dense_smem_bytes(), s>>>(p, e->tmA, e->tmB, e->mapA_row, e->mapB_row);
-        if ((c = cudaGetLastError()) != cudaSuccess) return c;
-        if (launches) ++*launches;
-    }
+    p.i_lo = (int32_t)i_lo;
+    p.i_hi = (int32_t)i_hi;
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t total = (int64_t)e->n_out * (i_hi - i_lo) * (e->np / kTN);
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(sms, total));
+    dense_kernel<<<grid, kDenseThreads, dense_smem_bytes(), s>>>(p, e->tmA, e->tmB, e->mapA_row, e->mapB_row);
+    if (launches) ++*launches;
+    return cudaGetLastError();
+}
+
+cudaError_t dense_finish(DenseEngine* e, cudaStream_t s, unsigned long long* new_total) {
     std::vector<unsigned long long> h(e->n_nt + 2);
+    cudaError_t c;
     if ((c = cudaMemcpyAsync(h.data(), e->new_cells, (e->n_nt + 2) * 8, cudaMemcpyDeviceToHost, s)) != cudaSuccess)
         return c;
     if ((c = cudaStreamSynchronize(s)) != cudaSuccess) return c;
     *new_total = h[e->n_nt];
     e->kblocks_total += h[e->n_nt + 1];
-    if (per_nt) per_nt->assign(h.begin(), h.begin() + e->n_nt);
     return cudaSuccess;
 }
+
+unsigned long long* dense_total_counter(DenseEngine* e) { return e->new_cells + e->n_nt; }
+int64_t dense_row_tiles(const DenseEngine* e) { return e->nt_tiles; }
 
 // Issued MMA k-blocks (128 x 256 x 128 int8 each) since the last reset.
 unsigned long long dense_kblocks(DenseEngine* e, bool reset) {

@@ -101,3 +101,27 @@ def test_tensor_empty_and_lengths_rejected():
     with pytest.raises(C.CfpqError) as e:
         gpu_closure(w2, path_policy=2, semantics=1)
     assert e.value.status == C.CFPQ_E_UNSUPPORTED
+
+
+@pytest.mark.parametrize("ranks", [2, 3, 8])
+def test_tensor_row_block_shards_emulated(ranks):
+    """Row-block sharding of the dense engine (the multi-GPU partition, §8(e)) emulated with
+    `ranks` shards in one process: identical closure, iterations and per-iteration counts."""
+    for w in (I.dense_stress_workload(700, 2, seed=ranks), I.random_workload(50_000 + ranks, max_nodes=300,
+                                                                               max_edges=900, max_nt=5, max_bin=10,
+                                                                               max_term=5, n_labels=4),
+              I.ontology_workload("union", 500, depth=5, seed=ranks)):
+        r, _, _ = gpu_closure(w, path_policy=2, emulate_ranks=ranks)
+        ores = assert_parity(w, r)
+        nc, _ = r.iteration_stats()
+        assert nc.tolist() == ores.stats()["new_bits"].tolist()
+
+
+def test_tensor_nccl_single_rank_path():
+    """The NCCL exchange path (dlopen'ed libnccl, ncclCommInitRank, grouped in-place
+    all-gather of the row blocks + all-reduce of the new-cell count) with one rank."""
+    from paper_1707_01007_b200 import cfpq as C
+    uid = C.nccl_unique_id()
+    w = I.dense_stress_workload(500, 2, seed=3)
+    r, _, _ = gpu_closure(w, path_policy=2, world_size=1, rank=0, nccl_unique_id=uid)
+    assert_parity(w, r)
