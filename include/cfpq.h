@@ -100,8 +100,10 @@ typedef struct {
                                 8*n^2 bytes of device memory per non-preterminal NT.     */
     int32_t schedule;        /* 0 jacobi: per-iteration states equal Alg. 1's T_k;
                                 1 seminaive: same states, same as 0 in this library       */
-    int32_t path_policy;     /* 0 auto, 1 sparse (index-list semi-naive), 2 tensor (tcgen05
-                                int8 dense), 3 rows (bit-row full-operand, paper-faithful) */
+    int32_t path_policy;     /* 0 auto: sparse, switching to tensor when Δ turns dense and a
+                                rule has two changing operands; 1 sparse (index-list semi-
+                                naive); 2 tensor (tcgen05 int8 dense); 3 rows (bit-row full-
+                                operand, paper-faithful)                                     */
     int32_t account_work;    /* 1: also record per-iteration Jacobi AND-true triple counts
                                 (the work of Alg. 1 line 9 on sparse operands); slower     */
     int64_t max_iterations;  /* 0 = |V|^2 |N| + 1 (Theorem 3)                   */
@@ -178,7 +180,9 @@ CFPQ_API cfpq_status cfpq_result_lengths(cfpq_result* r, int32_t nt, uint32_t* d
  *   adjacency build, snapshot seeding) in ns, [9] device time of the fixpoint-loop
  *   kernel launches in ns (CUDA events on the closure stream), [10] CTAs of the closure
  *   kernel, [11..17] single-CTA phase cycle counters (only with record_times), [18] tcgen05
- *   k-blocks issued by the dense engine (each 128x256x128 int8 MMA work = 2^23 ops).
+ *   k-blocks issued by the dense engine (each 128x256x128 int8 MMA work = 2^23 ops),
+ *   [19] 1 if the last closure finished on the dense engine (path_policy 2, or the auto
+ *   policy switched to it once Δ became dense).
  * Per-iteration arrays (length = iterations) via cfpq_result_iteration_stats:
  *   new_cells[k-1] = |T_k \ T_{k-1}|, jacobi_triples[k-1] (only with account_work). */
 CFPQ_API cfpq_status cfpq_result_stats(const cfpq_result* r, int64_t* stats, int32_t n_stats);

@@ -287,11 +287,11 @@ class Result:
         return buf[: w.value]
 
     def stats(self) -> dict:
-        v = (ctypes.c_int64 * 19)()
-        _check(load().cfpq_result_stats(self._h, v, 19), "cfpq_result_stats")
+        v = (ctypes.c_int64 * 20)()
+        _check(load().cfpq_result_stats(self._h, v, 20), "cfpq_result_stats")
         keys = ["iterations", "cells", "log_capacity", "regrows", "launches", "solo_iterations", "candidates",
                 "expansions", "seed_ns", "loop_ns", "ctas", "prof_loop", "prof_expand", "prof_bar1",
-                "prof_close", "prof_4", "prof_head", "prof_atomic", "mma_kblocks"]
+                "prof_close", "prof_4", "prof_head", "prof_atomic", "mma_kblocks", "dense_finish"]
         return dict(zip(keys, list(v)))
 
     def iteration_stats(self, work: bool = False) -> Tuple[np.ndarray, Optional[np.ndarray]]:

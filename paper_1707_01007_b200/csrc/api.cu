@@ -101,12 +101,15 @@ struct cfpq_result {
     int64_t iterations = 0;
     unsigned long long n_cells = 0;
     int64_t regrows = 0;
+    int64_t switched = 0;
     int64_t launches = 0;
     std::vector<int64_t> counts;
     bool counts_valid = false;
     bool ran = false;
     // dense (tcgen05) engine state
-    bool dense_mode = false;
+    bool dense_mode = false;                  // the last (or current) run finished on the dense engine
+    unsigned long long switch_cells = 0;      // auto policy: sparse -> dense when |Δ_k| exceeds this
+    std::vector<int32_t> is_const;
     DenseEngine* dense = nullptr;
     uint32_t* d_Tn = nullptr;                 // second bit-matrix buffer of the outputs
     std::vector<uint32_t*> Tbase, Tcur, Tnxt;  // per NT
@@ -162,6 +165,7 @@ struct cfpq_result {
         p.has_snapshots = has_snapshots;
         p.nblocks = grid;
         p.profile = opts.record_times;
+        p.switch_cells = switch_cells;
         return p;
     }
 };
@@ -262,6 +266,24 @@ extern "C" void cfpq_options_default(cfpq_options* o) {
     memset(o, 0, sizeof(*o));
     o->world_size = 1;
     o->solo_threshold = -1;
+}
+
+// Create the dense engine and the second bit-matrix buffer of its outputs (at plan time
+// for path_policy 2, at the first switch for the auto policy).
+static cfpq_status ensure_dense(cfpq_result* r) {
+    if (r->dense) return CFPQ_OK;
+    std::string err;
+    r->dense = dense_create((int32_t)r->n, r->n_nt, r->Wp, r->rules, r->is_const, r->stream, &err);
+    if (!r->dense) {
+        set_error(err);
+        return CFPQ_E_CUDA;
+    }
+    const size_t mat_words = (size_t)r->rows_alloc * (size_t)r->Wp;
+    int n_out = (int)dense_outputs(r->dense).size();
+    cfpq_status st = dalloc(&r->d_Tn, mat_words * std::max(n_out, 1), "dense next bit matrices");
+    if (st != CFPQ_OK) return st;
+    CFPQ_CUDA_TRY(cudaMemsetAsync(r->d_Tn, 0, mat_words * std::max(n_out, 1) * 4, r->stream));
+    return CFPQ_OK;
 }
 
 // ------------------------------------------------------------------------------------------
@@ -435,17 +457,15 @@ static cfpq_status plan(cfpq_result* r, const cfpq_grammar* g, const cfpq_graph*
 
     r->Tbase.assign(g->n_nt, nullptr);
     for (int A = 0; A < g->n_nt; ++A) r->Tbase[A] = r->h_nt[A].T;
+    r->is_const = g->is_const;
     if (o->path_policy == 2) {
-        r->dense_mode = true;
-        std::string err;
-        r->dense = dense_create((int32_t)n, g->n_nt, r->Wp, g->rules, g->is_const, r->stream, &err);
-        if (!r->dense) {
-            set_error(err);
-            return CFPQ_E_CUDA;
-        }
-        int n_out = (int)dense_outputs(r->dense).size();
-        if ((st = dalloc(&r->d_Tn, mat_words * std::max(n_out, 1), "dense next bit matrices")) != CFPQ_OK) return st;
-        CFPQ_CUDA_TRY(cudaMemsetAsync(r->d_Tn, 0, mat_words * std::max(n_out, 1) * 4, r->stream));
+        if ((st = ensure_dense(r)) != CFPQ_OK) return st;
+    } else if (o->path_policy == 0 && o->semantics == 0) {
+        // auto: rules whose two operands both change are row scans for the sparse engine;
+        // once |Δ| is dense (> n^2/256 cells, at least 4096) the tcgen05 engine takes over
+        bool varvar = false;
+        for (auto& rl : g->rules) varvar |= !g->is_const[rl.B] && !g->is_const[rl.C];
+        if (varvar) r->switch_cells = std::max<unsigned long long>(4096ull, (unsigned long long)n * n / 256);
     }
     if ((st = dalloc(&r->d_rowcnt, (size_t)n + 1, "row counts")) != CFPQ_OK) return st;
     if ((st = dalloc(&r->d_rowoff, (size_t)n + 1, "row offsets")) != CFPQ_OK) return st;
@@ -505,16 +525,23 @@ static cfpq_status grow_log(cfpq_result* r, unsigned long long reached) {
 
 // Dense engine loop (path_policy 2): host-driven Jacobi iterations, one tcgen05 product
 // launch (+ packs) per iteration; T and Tn swap roles after every iteration.
-static cfpq_status run_dense(cfpq_result* r) {
+static cfpq_status run_dense(cfpq_result* r, int64_t start_k) {
     cudaStream_t s = r->stream;
-    // seeding is done; Δ_0 is in the log
+    // seeding (and start_k sparse iterations) done; their cells are in the log
     CFPQ_CUDA_TRY(cudaMemcpyAsync(&r->h_st, r->d_st, sizeof(EngineState), cudaMemcpyDeviceToHost, s));
     CFPQ_CUDA_TRY(cudaStreamSynchronize(s));
     if (r->h_st.bad_edge) {
         set_error("graph has an edge with a node id >= n_nodes or a label id >= n_labels");
         return CFPQ_E_INVAL;
     }
+    r->dense_mode = true;
     r->n_cells = std::min<unsigned long long>(r->h_st.log_size, r->log_cap);
+    std::vector<int64_t> sparse_new;   // new cells of the sparse iterations 1..start_k
+    if (start_k > 0) {
+        std::vector<unsigned long long> off(start_k + 2);
+        CFPQ_CUDA_TRY(cudaMemcpy(off.data(), r->d_iter_off, (start_k + 2) * 8, cudaMemcpyDeviceToHost));
+        for (int64_t t = 1; t <= start_k; ++t) sparse_new.push_back((int64_t)(off[t + 1] - off[t]));
+    }
     const auto& outs = dense_outputs(r->dense);
     r->Tcur = r->Tbase;
     r->Tnxt.assign(r->n_nt, nullptr);
@@ -522,10 +549,15 @@ static cfpq_status run_dense(cfpq_result* r) {
     for (size_t q = 0; q < outs.size(); ++q) r->Tnxt[outs[q]] = r->d_Tn + q * mw;
     const int64_t tiles = dense_row_tiles(r->dense);
     std::vector<uint32_t*> out_mats(outs.size());
-    r->dense_new.clear();
-    int64_t k = 0;
+    r->dense_new = sparse_new;
+    int64_t k = start_k;
     bool capped = false;
     r->dense_jac.clear();
+    if (r->opts.account_work && start_k > 0) {
+        std::vector<unsigned long long> j(start_k + 1);
+        CFPQ_CUDA_TRY(cudaMemcpy(j.data(), r->d_jac, (start_k + 1) * 8, cudaMemcpyDeviceToHost));
+        for (int64_t t = 1; t <= start_k; ++t) r->dense_jac.push_back((int64_t)j[t]);
+    }
     dense_kblocks(r->dense, true);
     cudaEvent_t e0 = r->ev[2], e1 = r->ev[3];
     CFPQ_CUDA_TRY(cudaEventRecord(e0, s));
@@ -538,7 +570,7 @@ static cfpq_status run_dense(cfpq_result* r) {
             CFPQ_CUDA_TRY(dense_account(r->dense, r->Tcur.data(), r->rules, s, &jt));
             r->dense_jac.push_back((int64_t)jt);
         }
-        CFPQ_CUDA_TRY(dense_begin(r->dense, r->Tcur.data(), r->Tnxt.data(), k == 1, s, &launches));
+        CFPQ_CUDA_TRY(dense_begin(r->dense, r->Tcur.data(), r->Tnxt.data(), k == start_k + 1, s, &launches));
         if (r->n_ranks == 1 && !r->comm) {
             CFPQ_CUDA_TRY(dense_product(r->dense, 0, tiles, s, &launches));
         } else if (r->emulated) {
@@ -576,10 +608,13 @@ static cfpq_status run_dense(cfpq_result* r) {
     CFPQ_CUDA_TRY(cudaEventSynchronize(e1));
     {
         float ms = 0;
-        CFPQ_CUDA_TRY(cudaEventElapsedTime(&ms, r->ev[0], r->ev[1]));
-        r->seed_ns = ms * 1e6;
+        if (start_k == 0) {
+            CFPQ_CUDA_TRY(cudaEventElapsedTime(&ms, r->ev[0], r->ev[1]));
+            r->seed_ns = ms * 1e6;
+            r->loop_ns = 0;
+        }
         CFPQ_CUDA_TRY(cudaEventElapsedTime(&ms, e0, e1));
-        r->loop_ns = ms * 1e6;
+        r->loop_ns += ms * 1e6;
     }
     r->iterations = k;
     r->dense_kb = dense_kblocks(r->dense, false);
@@ -603,15 +638,22 @@ static cfpq_status run(cfpq_result* r, const cfpq_graph* d) {
     if (st != CFPQ_OK) return st;
     EngineParams p = r->params();
     if (r->dense_mode && r->ran) {
+        // the previous run ended on the dense engine, which rewrites whole matrices
         // the dense engine rewrites whole matrices: restore the base buffers and clear them
         for (int A = 0; A < r->n_nt; ++A) r->h_nt[A].T = r->Tbase[A];
         CFPQ_CUDA_TRY(cudaMemcpyAsync(r->d_nt, r->h_nt.data(), r->n_nt * sizeof(NTInfo), cudaMemcpyHostToDevice, s));
         const size_t mw = (size_t)r->rows_alloc * (size_t)r->Wp;
         CFPQ_CUDA_TRY(cudaMemsetAsync(r->d_T, 0, mw * r->n_nt * 4, s));
         CFPQ_CUDA_TRY(cudaMemsetAsync(r->d_Tn, 0, mw * std::max<size_t>(dense_outputs(r->dense).size(), 1) * 4, s));
+        if (r->d_snap) {
+            int n_snap = 0;
+            for (auto& t : r->h_nt) n_snap += (t.S ? 1 : 0) + (t.ST ? 1 : 0);
+            CFPQ_CUDA_TRY(cudaMemsetAsync(r->d_snap, 0, mw * n_snap * 4, s));
+        }
         r->n_cells = 0;
         p = r->params();
     }
+    r->dense_mode = false;
     // clear what a previous run derived (bitmaps, snapshots, keys, counters): O(|log|)
     if (r->ran && r->n_cells) {
         CFPQ_CUDA_TRY(launch_clear_log(p, r->n_cells, s));
@@ -649,7 +691,7 @@ static cfpq_status run(cfpq_result* r, const cfpq_graph* d) {
         r->launches++;
     }
     CFPQ_CUDA_TRY(cudaEventRecord(r->ev[1], s));
-    if (r->dense_mode) return run_dense(r);
+    if (r->opts.path_policy == 2) return run_dense(r, 0);
     // a2-a5: the fixpoint loop, device-resident
     bool first = true;
     for (;;) {
@@ -698,6 +740,12 @@ static cfpq_status run(cfpq_result* r, const cfpq_graph* d) {
     }
     r->iterations = r->h_st.iter;
     r->n_cells = std::min<unsigned long long>(r->h_st.log_size, r->log_cap);
+    if (r->h_st.status == ST_SWITCH) {
+        // Δ became dense: continue Alg. 1 from T_k on the tcgen05 engine (same states)
+        if ((st = ensure_dense(r)) != CFPQ_OK) return st;
+        r->switched++;
+        return run_dense(r, r->h_st.iter);
+    }
     if (r->h_st.status == ST_CAP) {
         set_error("max_iterations reached before the fixpoint");
         return CFPQ_E_NOT_CONVERGED;
@@ -768,7 +816,7 @@ extern "C" cfpq_status cfpq_closure_reuse(const cfpq_grammar* g, const cfpq_grap
     if (st != CFPQ_OK) return st;
     CFPQ_CHECK_ARG(d->n_nodes == r->n && g->n_nt == r->n_nt && g->n_labels == r->n_labels &&
                        g->rules.size() == r->rules.size() && o->semantics == r->opts.semantics &&
-                       o->account_work == r->opts.account_work && (o->path_policy == 2) == r->dense_mode,
+                       o->account_work == r->opts.account_work && o->path_policy == r->opts.path_policy,
                    "cfpq_closure_reuse: grammar/graph/options differ from the result's plan");
     for (size_t k = 0; k < g->rules.size(); ++k)
         CFPQ_CHECK_ARG(g->rules[k].A == r->rules[k].A && g->rules[k].B == r->rules[k].B && g->rules[k].C == r->rules[k].C,
@@ -1021,13 +1069,13 @@ extern "C" cfpq_status cfpq_result_lengths(cfpq_result* r, int32_t nt, uint32_t*
 
 extern "C" cfpq_status cfpq_result_stats(const cfpq_result* r, int64_t* stats, int32_t n_stats) {
     CFPQ_CHECK_ARG(r && stats, "cfpq_result_stats: NULL argument");
-    int64_t v[19] = {r->iterations, (int64_t)r->n_cells, (int64_t)r->log_cap, r->regrows, r->launches,
+    int64_t v[20] = {r->iterations, (int64_t)r->n_cells, (int64_t)r->log_cap, r->regrows, r->launches,
                      r->h_st.solo_iters, (int64_t)r->h_st.candidates, (int64_t)r->h_st.expansions,
                      (int64_t)r->seed_ns, (int64_t)r->loop_ns, (int64_t)r->grid,
                      (int64_t)r->h_st.prof[0], (int64_t)r->h_st.prof[1], (int64_t)r->h_st.prof[2],
                      (int64_t)r->h_st.prof[3], (int64_t)r->h_st.prof[4], (int64_t)r->h_st.prof[5],
-                     (int64_t)r->h_st.prof[6], (int64_t)r->dense_kb};
-    for (int k = 0; k < n_stats && k < 19; ++k) stats[k] = v[k];
+                     (int64_t)r->h_st.prof[6], (int64_t)r->dense_kb, (int64_t)r->dense_mode};
+    for (int k = 0; k < n_stats && k < 20; ++k) stats[k] = v[k];
     return CFPQ_OK;
 }
 

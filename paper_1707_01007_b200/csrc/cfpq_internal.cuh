@@ -89,7 +89,7 @@ struct EngineState {
     unsigned pad1[22];
 };
 
-enum : int { ST_RUNNING = 0, ST_DONE = 1, ST_OVERFLOW = 2, ST_CAP = 3, ST_LEN_OVERFLOW = 4 };
+enum : int { ST_RUNNING = 0, ST_DONE = 1, ST_OVERFLOW = 2, ST_CAP = 3, ST_LEN_OVERFLOW = 4, ST_SWITCH = 5 };
 
 struct EngineParams {
     int32_t n;
@@ -116,6 +116,7 @@ struct EngineParams {
     int32_t has_snapshots;
     int32_t nblocks;
     int32_t profile;               // accumulate single-CTA phase cycles into EngineState::prof
+    unsigned long long switch_cells;  // |Δ_k| above which the loop stops for the dense engine (0 = never)
 };
 
 // ------------------------------------------------------------------------------------------

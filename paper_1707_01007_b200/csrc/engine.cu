@@ -590,6 +590,7 @@ __device__ __forceinline__ void close_iteration(const EngineParams& p, long long
     }
     if (ls == s.lo) s.status = ST_DONE;             // T_k = T_{k-1}: fixpoint
     else if (k >= p.max_iter) s.status = ST_CAP;    // Theorem 3 cap
+    else if (p.switch_cells && ls - s.lo > p.switch_cells) s.status = ST_SWITCH;   // dense Δ: tensor engine
 }
 
 __device__ void publish(const EngineParams& p, const LoopState& s) {

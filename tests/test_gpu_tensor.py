@@ -107,10 +107,10 @@ def test_tensor_empty_and_lengths_rejected():
 def test_tensor_row_block_shards_emulated(ranks):
     """Row-block sharding of the dense engine (the multi-GPU partition, §8(e)) emulated with
     `ranks` shards in one process: identical closure, iterations and per-iteration counts."""
-    for w in (I.dense_stress_workload(700, 2, seed=ranks), I.random_workload(50_000 + ranks, max_nodes=300,
-                                                                               max_edges=900, max_nt=5, max_bin=10,
+    for w in (I.dense_stress_workload(400, 2, seed=ranks), I.random_workload(50_000 + ranks, max_nodes=200,
+                                                                               max_edges=600, max_nt=5, max_bin=10,
                                                                                max_term=5, n_labels=4),
-              I.ontology_workload("union", 500, depth=5, seed=ranks)):
+              I.ontology_workload("union", 400, depth=5, seed=ranks)):
         r, _, _ = gpu_closure(w, path_policy=2, emulate_ranks=ranks)
         ores = assert_parity(w, r)
         nc, _ = r.iteration_stats()
@@ -125,3 +125,21 @@ def test_tensor_nccl_single_rank_path():
     w = I.dense_stress_workload(500, 2, seed=3)
     r, _, _ = gpu_closure(w, path_policy=2, world_size=1, rank=0, nccl_unique_id=uid)
     assert_parity(w, r)
+
+
+@pytest.mark.parametrize("n,d", [(300, 2), (400, 1)])
+def test_auto_policy_switches_to_tensor(n, d):
+    """Auto policy: sparse iterations while Δ is small, then the tcgen05 engine once Δ is
+    dense (rule S -> S S has two changing operands); same fixpoint, iterations and counts."""
+    w = I.dense_stress_workload(n, d, seed=11)
+    r, _, _ = gpu_closure(w, account_work=True)
+    assert r.stats()["dense_finish"] == 1
+    ores = assert_parity(w, r)
+    nc, jt = r.iteration_stats(work=True)
+    assert nc.tolist() == ores.stats()["new_bits"].tolist()
+    assert jt.tolist() == ores.stats()["jacobi_triples"].tolist()
+    # the paper's grammars (all rules have a preterminal operand) never switch
+    w2 = I.ontology_workload("union", 800, depth=6, seed=1)
+    r2, _, _ = gpu_closure(w2)
+    assert r2.stats()["dense_finish"] == 0
+    assert_parity(w2, r2)
