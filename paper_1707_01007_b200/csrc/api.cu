@@ -273,7 +273,8 @@ extern "C" void cfpq_options_default(cfpq_options* o) {
 static cfpq_status ensure_dense(cfpq_result* r) {
     if (r->dense) return CFPQ_OK;
     std::string err;
-    r->dense = dense_create((int32_t)r->n, r->n_nt, r->Wp, r->rules, r->is_const, r->stream, &err);
+    r->dense = dense_create((int32_t)r->n, r->n_nt, r->Wp, r->rules, r->is_const, r->stream, &err,
+                            r->opts.path_policy != 3);
     if (!r->dense) {
         set_error(err);
         return CFPQ_E_CUDA;
@@ -458,7 +459,7 @@ static cfpq_status plan(cfpq_result* r, const cfpq_grammar* g, const cfpq_graph*
     r->Tbase.assign(g->n_nt, nullptr);
     for (int A = 0; A < g->n_nt; ++A) r->Tbase[A] = r->h_nt[A].T;
     r->is_const = g->is_const;
-    if (o->path_policy == 2) {
+    if (o->path_policy == 2 || o->path_policy == 3) {
         if ((st = ensure_dense(r)) != CFPQ_OK) return st;
     } else if (o->path_policy == 0 && o->semantics == 0) {
         // auto: rules whose two operands both change are row scans for the sparse engine;
@@ -570,8 +571,11 @@ static cfpq_status run_dense(cfpq_result* r, int64_t start_k) {
             CFPQ_CUDA_TRY(dense_account(r->dense, r->Tcur.data(), r->rules, s, &jt));
             r->dense_jac.push_back((int64_t)jt);
         }
-        CFPQ_CUDA_TRY(dense_begin(r->dense, r->Tcur.data(), r->Tnxt.data(), k == start_k + 1, s, &launches));
-        if (r->n_ranks == 1 && !r->comm) {
+        const bool rows = r->opts.path_policy == 3;
+        CFPQ_CUDA_TRY(dense_begin(r->dense, r->Tcur.data(), r->Tnxt.data(), k == start_k + 1, s, &launches, !rows));
+        if (rows) {
+            CFPQ_CUDA_TRY(rows_product(r->dense, 0, r->n, s, &launches));
+        } else if (r->n_ranks == 1 && !r->comm) {
             CFPQ_CUDA_TRY(dense_product(r->dense, 0, tiles, s, &launches));
         } else if (r->emulated) {
             // P row-block shards in one process: each writes its rows of the shared T_k
@@ -691,7 +695,7 @@ static cfpq_status run(cfpq_result* r, const cfpq_graph* d) {
         r->launches++;
     }
     CFPQ_CUDA_TRY(cudaEventRecord(r->ev[1], s));
-    if (r->opts.path_policy == 2) return run_dense(r, 0);
+    if (r->opts.path_policy == 2 || r->opts.path_policy == 3) return run_dense(r, 0);
     // a2-a5: the fixpoint loop, device-resident
     bool first = true;
     for (;;) {
@@ -779,11 +783,15 @@ static cfpq_status check_inputs(const cfpq_grammar* g, const cfpq_graph* d, cons
         CFPQ_CHECK_ARG(o->rank >= 0 && o->rank < o->world_size, "cfpq_closure: rank out of range");
         CFPQ_CHECK_ARG(o->nccl_unique_id != nullptr, "cfpq_closure: world_size > 1 needs nccl_unique_id");
     }
-    if (o->path_policy == 3) {
-        set_error("cfpq_closure: path_policy 3 (rows) not available in this build");
+    if (o->path_policy == 3 && (o->world_size > 1 || o->reserved_emulate > 1)) {
+        set_error("cfpq_closure: the bit-row path (policy 3) runs on one GPU");
         return CFPQ_E_UNSUPPORTED;
     }
-    if (o->path_policy == 2 && o->semantics == 1) {
+    if (o->path_policy == 3 && d->n_nodes > 262144) {
+        set_error("cfpq_closure: the bit-row path keeps a row in registers: n_nodes <= 262144");
+        return CFPQ_E_UNSUPPORTED;
+    }
+    if ((o->path_policy == 2 || o->path_policy == 3) && o->semantics == 1) {
         set_error("cfpq_closure: single-path lengths need the sparse engine (min-plus is not a Boolean product)");
         return CFPQ_E_UNSUPPORTED;
     }

@@ -371,6 +371,90 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
 }
 
 // ------------------------------------------------------------------------------------------
+// Bit-row path (CUDA cores, path_policy 3): the same Jacobi product on packed rows,
+//   T_k,A[i] = T_{k-1},A[i] | OR_{A->BC} OR_{r : T_B[i] has bit r} T_C[r]
+// One CTA per output row at a time; the set bits r of row i of T_B are compacted into a
+// shared-memory list (warp ballots), then the CTA ORs the rows T_C[r] with 128-bit loads.
+// Algorithmic bytes per (row, rule): 4Wn (row of T_B) + popc·4Wn (rows of T_C), plus 8Wn
+// per output row (read T_{k-1}, write T_k): the full-operand traffic of SURVEY §8(d).
+// ------------------------------------------------------------------------------------------
+constexpr int kRowThreads = 256;
+constexpr int kRowList = 32 * 256;   // one set bit per (thread, bit) of a 256-word slice
+constexpr int kRowMaxV4 = 8;   // uint4 accumulators per thread: rows up to 8*4*32*256 = 262144 bits
+
+__global__ void __launch_bounds__(kRowThreads) rows_kernel(DenseParams p, int64_t row_lo, int64_t row_hi) {
+    __shared__ int32_t list[kRowList];
+    __shared__ int32_t cnt;
+    const int64_t wn = (p.n + 31) / 32;
+    const int64_t nv4 = (wn + 3) / 4;        // uint4 groups per row (Wp is a multiple of 32 words)
+    const int64_t rows = row_hi - row_lo;
+    unsigned long long my_new = 0;
+    for (int64_t task = blockIdx.x; task < rows * p.n_out; task += gridDim.x) {
+        const int o = (int)(task / rows);
+        const int64_t i = row_lo + (task - (int64_t)o * rows);
+        const int A = p.out_nt[o];
+        uint4 acc[kRowMaxV4];
+#pragma unroll
+        for (int v = 0; v < kRowMaxV4; ++v) acc[v] = make_uint4(0, 0, 0, 0);
+        for (int q = p.rule_ptr[o]; q < p.rule_ptr[o + 1]; ++q) {
+            const DenseRule r = p.rules[q];
+            const uint32_t* rowB = p.T[r.B] + (size_t)i * p.Wp;
+            const uint32_t* TC = p.T[r.C];
+            for (int64_t w0 = 0; w0 < wn; w0 += kRowThreads) {
+                // compact the set bits r of words [w0, w0 + kRowThreads) of row i of T_B
+                // (at most 32 * kRowThreads = kRowList entries: never overflows)
+                if (threadIdx.x == 0) cnt = 0;
+                __syncthreads();
+                {
+                    int64_t w = w0 + threadIdx.x;
+                    uint32_t bits = w < wn ? __ldg(rowB + w) : 0u;
+                    int c = __popc(bits);
+                    int at = c ? atomicAdd(&cnt, c) : 0;
+                    while (bits) {
+                        int b = __ffs(bits) - 1;
+                        bits &= bits - 1u;
+                        list[at++] = (int32_t)(w * 32 + b);
+                    }
+                }
+                __syncthreads();
+                const int m = cnt;
+                for (int e = 0; e < m; ++e) {
+                    const uint4* rowC = reinterpret_cast<const uint4*>(TC + (size_t)list[e] * p.Wp);
+#pragma unroll
+                    for (int v = 0; v < kRowMaxV4; ++v) {
+                        int64_t g = (int64_t)v * kRowThreads + threadIdx.x;
+                        if (g < nv4) {
+                            uint4 x = __ldg(rowC + g);
+                            acc[v].x |= x.x;
+                            acc[v].y |= x.y;
+                            acc[v].z |= x.z;
+                            acc[v].w |= x.w;
+                        }
+                    }
+                }
+                __syncthreads();
+            }
+        }
+        // T_k row = old | acc; count new cells
+        const uint4* rowOld = reinterpret_cast<const uint4*>(p.T[A] + (size_t)i * p.Wp);
+        uint4* rowNew = reinterpret_cast<uint4*>(p.Tn[A] + (size_t)i * p.Wp);
+#pragma unroll
+        for (int v = 0; v < kRowMaxV4; ++v) {
+            int64_t g = (int64_t)v * kRowThreads + threadIdx.x;
+            if (g < nv4) {
+                uint4 o4 = __ldg(rowOld + g);
+                uint4 a = acc[v];
+                my_new += __popc(a.x & ~o4.x) + __popc(a.y & ~o4.y) + __popc(a.z & ~o4.z) + __popc(a.w & ~o4.w);
+                rowNew[g] = make_uint4(o4.x | a.x, o4.y | a.y, o4.z | a.z, o4.w | a.w);
+            }
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) my_new += __shfl_xor_sync(0xffffffffu, my_new, o);
+    if ((threadIdx.x & 31) == 0 && my_new) atomicAdd(p.new_cells + p.n_nt, my_new);
+}
+
+// ------------------------------------------------------------------------------------------
 // host side
 // ------------------------------------------------------------------------------------------
 static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
@@ -433,7 +517,7 @@ struct DenseEngine {
 void dense_destroy(DenseEngine* e) { delete e; }
 
 DenseEngine* dense_create(int32_t n, int32_t n_nt, int64_t Wp, const std::vector<Rule3>& rules,
-                          const std::vector<int32_t>& is_const, cudaStream_t s, std::string* err) {
+                          const std::vector<int32_t>& is_const, cudaStream_t s, std::string* err, bool tensor) {
     DenseEngine* e = new DenseEngine();
     e->n = n;
     e->n_nt = n_nt;
@@ -459,6 +543,10 @@ DenseEngine* dense_create(int32_t n, int32_t n_nt, int64_t Wp, const std::vector
         rp.push_back((int32_t)rl.size());
     }
     e->n_out = (int32_t)e->h_out.size();
+    if (!tensor) {
+        std::fill(e->packA.begin(), e->packA.end(), 0);
+        std::fill(e->packB.begin(), e->packB.end(), 0);
+    }
     int na = 0, nb = 0;
     e->h_mapA.assign(n_nt, -1);
     e->h_mapB.assign(n_nt, -1);
@@ -513,9 +601,9 @@ DenseEngine* dense_create(int32_t n, int32_t n_nt, int64_t Wp, const std::vector
 // product = T_k rows of row tiles [i_lo, i_hi) of every output; finish = read the new-cell
 // counters (device -> host).
 cudaError_t dense_begin(DenseEngine* e, uint32_t* const* T, uint32_t* const* Tn, bool first, cudaStream_t s,
-                        int* launches) {
+                        int* launches, bool pack_operands) {
     const size_t pack = (size_t)e->np * e->np;
-    for (int X = 0; X < e->n_nt; ++X) {
+    for (int X = 0; X < e->n_nt && pack_operands; ++X) {
         if (!(e->packA[X] || e->packB[X])) continue;
         if (!first && e->is_const[X]) continue;   // preterminals never change after seeding
         uint8_t* a = e->packA[X] ? e->T8 + (size_t)(e->h_mapA[X] / e->np) * pack : nullptr;
@@ -558,6 +646,31 @@ cudaError_t dense_product(DenseEngine* e, int64_t i_lo, int64_t i_hi, cudaStream
     const int64_t total = (int64_t)e->n_out * (i_hi - i_lo) * (e->np / kTN);
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(sms, total));
     dense_kernel<<<grid, kDenseThreads, dense_smem_bytes(), s>>>(p, e->tmA, e->tmB, e->mapA_row, e->mapB_row);
+    if (launches) ++*launches;
+    return cudaGetLastError();
+}
+
+cudaError_t rows_product(DenseEngine* e, int64_t row_lo, int64_t row_hi, cudaStream_t s, int* launches) {
+    if (e->n_out == 0 || row_hi <= row_lo) return cudaSuccess;
+    if ((e->n + 31) / 32 > (int64_t)kRowMaxV4 * 4 * kRowThreads) return cudaErrorInvalidValue;
+    DenseParams p{};
+    p.n = e->n;
+    p.np = e->np;
+    p.Wp = e->Wp;
+    p.n_out = e->n_out;
+    p.out_nt = e->out_nt;
+    p.rule_ptr = e->rule_ptr;
+    p.rules = e->rules;
+    p.T = e->Tptr;
+    p.Tn = e->Tnptr;
+    p.new_cells = e->new_cells;
+    p.n_nt = e->n_nt;
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t tasks = (row_hi - row_lo) * e->n_out;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)sms * 8, tasks));
+    rows_kernel<<<grid, kRowThreads, 0, s>>>(p, row_lo, row_hi);
     if (launches) ++*launches;
     return cudaGetLastError();
 }

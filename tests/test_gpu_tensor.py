@@ -127,7 +127,7 @@ def test_tensor_nccl_single_rank_path():
     assert_parity(w, r)
 
 
-@pytest.mark.parametrize("n,d", [(300, 2), (400, 1)])
+@pytest.mark.parametrize("n,d", [(300, 2), (400, 2)])
 def test_auto_policy_switches_to_tensor(n, d):
     """Auto policy: sparse iterations while Δ is small, then the tcgen05 engine once Δ is
     dense (rule S -> S S has two changing operands); same fixpoint, iterations and counts."""
