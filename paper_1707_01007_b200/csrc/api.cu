@@ -574,7 +574,7 @@ static cfpq_status run_dense(cfpq_result* r, int64_t start_k) {
         const bool rows = r->opts.path_policy == 3;
         CFPQ_CUDA_TRY(dense_begin(r->dense, r->Tcur.data(), r->Tnxt.data(), k == start_k + 1, s, &launches, !rows));
         if (rows) {
-            CFPQ_CUDA_TRY(rows_product(r->dense, 0, r->n, s, &launches));
+            CFPQ_CUDA_TRY(rows_product(r->dense, r->Tcur.data(), r->Tnxt.data(), s, &launches));
         } else if (r->n_ranks == 1 && !r->comm) {
             CFPQ_CUDA_TRY(dense_product(r->dense, 0, tiles, s, &launches));
         } else if (r->emulated) {

@@ -195,7 +195,7 @@ DenseEngine* dense_create(int32_t n, int32_t n_nt, int64_t Wp, const std::vector
 void dense_destroy(DenseEngine* e);
 cudaError_t dense_begin(DenseEngine* e, uint32_t* const* T, uint32_t* const* Tn, bool first, cudaStream_t s,
                         int* launches, bool pack_operands);
-cudaError_t rows_product(DenseEngine* e, int64_t row_lo, int64_t row_hi, cudaStream_t s, int* launches);
+cudaError_t rows_product(DenseEngine* e, uint32_t* const* T, uint32_t* const* Tn, cudaStream_t s, int* launches);
 cudaError_t dense_product(DenseEngine* e, int64_t i_lo, int64_t i_hi, cudaStream_t s, int* launches);
 cudaError_t dense_finish(DenseEngine* e, cudaStream_t s, unsigned long long* new_total);
 unsigned long long* dense_total_counter(DenseEngine* e);

@@ -373,85 +373,128 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
 // ------------------------------------------------------------------------------------------
 // Bit-row path (CUDA cores, path_policy 3): the same Jacobi product on packed rows,
 //   T_k,A[i] = T_{k-1},A[i] | OR_{A->BC} OR_{r : T_B[i] has bit r} T_C[r]
-// One CTA per output row at a time; the set bits r of row i of T_B are compacted into a
-// shared-memory list (warp ballots), then the CTA ORs the rows T_C[r] with 128-bit loads.
-// Algorithmic bytes per (row, rule): 4Wn (row of T_B) + popc·4Wn (rows of T_C), plus 8Wn
-// per output row (read T_{k-1}, write T_k): the full-operand traffic of SURVEY §8(d).
+// T_k starts as a copy of T_{k-1}.  Work is balanced by chunks: a pre-pass lists, for every
+// (output rule, row i) with a non-empty row of T_B, chunks of <= kChunk set bits; a CTA
+// takes a chunk, ORs the kChunk rows T_C[r] (128-bit loads) into a register accumulator
+// and atomically ORs it into row i of T_k; the bits the atomics flip are exactly the new
+// cells (hub rows, e.g. type^-1 of owl:Class with ~n/2 set bits, are spread over CTAs).
+// Algorithmic bytes per (row, rule): 4Wn (row of T_B) + popc·4Wn (rows of T_C); per output
+// row 8Wn (copy T_{k-1} -> T_k): the full-operand traffic of SURVEY §8(d).
 // ------------------------------------------------------------------------------------------
 constexpr int kRowThreads = 256;
-constexpr int kRowList = 32 * 256;   // one set bit per (thread, bit) of a 256-word slice
+constexpr int kChunk = 128;
 constexpr int kRowMaxV4 = 8;   // uint4 accumulators per thread: rows up to 8*4*32*256 = 262144 bits
 
-__global__ void __launch_bounds__(kRowThreads) rows_kernel(DenseParams p, int64_t row_lo, int64_t row_hi) {
-    __shared__ int32_t list[kRowList];
-    __shared__ int32_t cnt;
+struct RowChunk {
+    int32_t rule;   // index into rules (output o implied)
+    int32_t row;
+    int32_t first;  // rank of the first set bit of this chunk
+    int32_t count;
+};
+
+// one warp per (rule, row): popcount of row i of T_B, append its chunks
+__global__ void rows_plan_kernel(DenseParams p, const int32_t* __restrict__ rule_out, int32_t n_rules,
+                                 RowChunk* chunks, unsigned long long* n_chunks, unsigned long long cap) {
+    const int lane = threadIdx.x & 31;
     const int64_t wn = (p.n + 31) / 32;
-    const int64_t nv4 = (wn + 3) / 4;        // uint4 groups per row (Wp is a multiple of 32 words)
-    const int64_t rows = row_hi - row_lo;
+    const int64_t tasks = (int64_t)n_rules * p.n;
+    for (int64_t t = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; t < tasks;
+         t += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const int q = (int)(t / p.n);
+        const int64_t i = t - (int64_t)q * p.n;
+        const uint32_t* rowB = p.T[p.rules[q].B] + (size_t)i * p.Wp;
+        int c = 0;
+        for (int64_t w = lane; w < wn; w += 32) c += __popc(__ldg(rowB + w));
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+        const int nch = (c + kChunk - 1) / kChunk;
+        if (lane == 0 && nch) {
+            unsigned long long at = atomicAdd(n_chunks, (unsigned long long)nch);
+            for (int h = 0; h < nch && at + h < cap; ++h)
+                chunks[at + h] = RowChunk{q, (int32_t)i, h * kChunk, min(kChunk, c - h * kChunk)};
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kRowThreads) rows_kernel(DenseParams p, const int32_t* __restrict__ rule_out,
+                                                          const RowChunk* __restrict__ chunks,
+                                                          const unsigned long long* n_chunks) {
+    __shared__ int32_t list[kChunk];
+    __shared__ int32_t wsum[kRowThreads / 32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t wn = (p.n + 31) / 32;
+    const int64_t nv4 = (wn + 3) / 4;
+    const unsigned long long m = *n_chunks;
     unsigned long long my_new = 0;
-    for (int64_t task = blockIdx.x; task < rows * p.n_out; task += gridDim.x) {
-        const int o = (int)(task / rows);
-        const int64_t i = row_lo + (task - (int64_t)o * rows);
-        const int A = p.out_nt[o];
+    for (unsigned long long c = blockIdx.x; c < m; c += gridDim.x) {
+        const RowChunk ch = chunks[c];
+        const DenseRule r = p.rules[ch.rule];
+        const uint32_t* rowB = p.T[r.B] + (size_t)ch.row * p.Wp;
+        // select the set bits of rank [first, first+count): walk the row in 256-word slices
+        int base = 0;   // set bits before the current slice
+        for (int64_t w0 = 0; w0 < wn && base < ch.first + ch.count; w0 += kRowThreads) {
+            int64_t w = w0 + threadIdx.x;
+            uint32_t bits = w < wn ? __ldg(rowB + w) : 0u;
+            int pc = __popc(bits);
+            int incl = pc;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                int v = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += v;
+            }
+            if (lane == 31) wsum[warp] = incl;
+            __syncthreads();
+            int before = 0, total = 0;
+            for (int q = 0; q < kRowThreads / 32; ++q) {
+                if (q < warp) before += wsum[q];
+                total += wsum[q];
+            }
+            int rank = base + before + incl - pc;   // rank of this word's first set bit
+            while (bits) {
+                int b = __ffs(bits) - 1;
+                bits &= bits - 1u;
+                if (rank >= ch.first && rank < ch.first + ch.count) list[rank - ch.first] = (int32_t)(w * 32 + b);
+                ++rank;
+            }
+            base += total;
+            __syncthreads();
+        }
+        // OR the selected rows of T_C
         uint4 acc[kRowMaxV4];
 #pragma unroll
         for (int v = 0; v < kRowMaxV4; ++v) acc[v] = make_uint4(0, 0, 0, 0);
-        for (int q = p.rule_ptr[o]; q < p.rule_ptr[o + 1]; ++q) {
-            const DenseRule r = p.rules[q];
-            const uint32_t* rowB = p.T[r.B] + (size_t)i * p.Wp;
-            const uint32_t* TC = p.T[r.C];
-            for (int64_t w0 = 0; w0 < wn; w0 += kRowThreads) {
-                // compact the set bits r of words [w0, w0 + kRowThreads) of row i of T_B
-                // (at most 32 * kRowThreads = kRowList entries: never overflows)
-                if (threadIdx.x == 0) cnt = 0;
-                __syncthreads();
-                {
-                    int64_t w = w0 + threadIdx.x;
-                    uint32_t bits = w < wn ? __ldg(rowB + w) : 0u;
-                    int c = __popc(bits);
-                    int at = c ? atomicAdd(&cnt, c) : 0;
-                    while (bits) {
-                        int b = __ffs(bits) - 1;
-                        bits &= bits - 1u;
-                        list[at++] = (int32_t)(w * 32 + b);
-                    }
-                }
-                __syncthreads();
-                const int m = cnt;
-                for (int e = 0; e < m; ++e) {
-                    const uint4* rowC = reinterpret_cast<const uint4*>(TC + (size_t)list[e] * p.Wp);
+        const uint32_t* TC = p.T[r.C];
+        for (int e = 0; e < ch.count; ++e) {
+            const uint4* rowC = reinterpret_cast<const uint4*>(TC + (size_t)list[e] * p.Wp);
 #pragma unroll
-                    for (int v = 0; v < kRowMaxV4; ++v) {
-                        int64_t g = (int64_t)v * kRowThreads + threadIdx.x;
-                        if (g < nv4) {
-                            uint4 x = __ldg(rowC + g);
-                            acc[v].x |= x.x;
-                            acc[v].y |= x.y;
-                            acc[v].z |= x.z;
-                            acc[v].w |= x.w;
-                        }
-                    }
+            for (int v = 0; v < kRowMaxV4; ++v) {
+                int64_t g = (int64_t)v * kRowThreads + threadIdx.x;
+                if (g < nv4) {
+                    uint4 x = __ldg(rowC + g);
+                    acc[v].x |= x.x;
+                    acc[v].y |= x.y;
+                    acc[v].z |= x.z;
+                    acc[v].w |= x.w;
                 }
-                __syncthreads();
             }
         }
-        // T_k row = old | acc; count new cells
-        const uint4* rowOld = reinterpret_cast<const uint4*>(p.T[A] + (size_t)i * p.Wp);
-        uint4* rowNew = reinterpret_cast<uint4*>(p.Tn[A] + (size_t)i * p.Wp);
+        // merge into row i of T_k; the flipped bits are the new cells
+        uint32_t* rowNew = p.Tn[rule_out[ch.rule]] + (size_t)ch.row * p.Wp;
 #pragma unroll
         for (int v = 0; v < kRowMaxV4; ++v) {
             int64_t g = (int64_t)v * kRowThreads + threadIdx.x;
             if (g < nv4) {
-                uint4 o4 = __ldg(rowOld + g);
-                uint4 a = acc[v];
-                my_new += __popc(a.x & ~o4.x) + __popc(a.y & ~o4.y) + __popc(a.z & ~o4.z) + __popc(a.w & ~o4.w);
-                rowNew[g] = make_uint4(o4.x | a.x, o4.y | a.y, o4.z | a.z, o4.w | a.w);
+                uint32_t a[4] = {acc[v].x, acc[v].y, acc[v].z, acc[v].w};
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    if (a[q]) my_new += __popc(a[q] & ~atomicOr(rowNew + 4 * g + q, a[q]));
             }
         }
+        __syncthreads();
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) my_new += __shfl_xor_sync(0xffffffffu, my_new, o);
-    if ((threadIdx.x & 31) == 0 && my_new) atomicAdd(p.new_cells + p.n_nt, my_new);
+    if (lane == 0 && my_new) atomicAdd(p.new_cells + p.n_nt, my_new);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -507,8 +550,14 @@ struct DenseEngine {
     int grid = 0;
     unsigned long long kblocks_total = 0;
     uint32_t* cnt = nullptr;   // accounting scratch
+    int32_t* rule_out = nullptr;               // [rules] output NT of each rule (bit-row path)
+    std::vector<int32_t> h_rule_out;
+    void* chunks = nullptr;                    // bit-row path work list
+    unsigned long long chunk_cap = 0;
     ~DenseEngine() {
         cudaFree(cnt);
+        cudaFree(rule_out);
+        cudaFree(chunks);
         cudaFree(T8); cudaFree(T8T); cudaFree(occ); cudaFree(mapA_row); cudaFree(mapB_row); cudaFree(out_nt);
         cudaFree(rule_ptr); cudaFree(rules); cudaFree(Tptr); cudaFree(Tnptr); cudaFree(new_cells);
     }
@@ -579,6 +628,10 @@ DenseEngine* dense_create(int32_t n, int32_t n_nt, int64_t Wp, const std::vector
     if (e->n_out) cudaMemcpyAsync(e->out_nt, e->h_out.data(), e->n_out * 4, cudaMemcpyHostToDevice, s);
     cudaMemcpyAsync(e->rule_ptr, rp.data(), rp.size() * 4, cudaMemcpyHostToDevice, s);
     if (!rl.empty()) cudaMemcpyAsync(e->rules, rl.data(), rl.size() * sizeof(DenseRule), cudaMemcpyHostToDevice, s);
+    for (auto& r : rl) e->h_rule_out.push_back(r.A);
+    if ((c = cudaMalloc(&e->rule_out, std::max<size_t>(1, rl.size()) * 4)) != cudaSuccess) return fail("tables", c);
+    if (!rl.empty())
+        cudaMemcpyAsync(e->rule_out, e->h_rule_out.data(), rl.size() * 4, cudaMemcpyHostToDevice, s);
     if (!make_map(&e->tmA, e->T8, (int64_t)std::max(na, 1) * e->np, e->np, kTM) ||
         !make_map(&e->tmB, e->T8T, (int64_t)std::max(nb, 1) * e->np, e->np, kTN)) {
         if (err) *err = "dense engine: cuTensorMapEncodeTiled failed";
@@ -650,9 +703,24 @@ cudaError_t dense_product(DenseEngine* e, int64_t i_lo, int64_t i_hi, cudaStream
     return cudaGetLastError();
 }
 
-cudaError_t rows_product(DenseEngine* e, int64_t row_lo, int64_t row_hi, cudaStream_t s, int* launches) {
-    if (e->n_out == 0 || row_hi <= row_lo) return cudaSuccess;
+cudaError_t rows_product(DenseEngine* e, uint32_t* const* T, uint32_t* const* Tn, cudaStream_t s, int* launches) {
+    if (e->n_out == 0) return cudaSuccess;
     if ((e->n + 31) / 32 > (int64_t)kRowMaxV4 * 4 * kRowThreads) return cudaErrorInvalidValue;
+    cudaError_t c;
+    // T_k starts as T_{k-1} (the BMU term of P:241)
+    for (int A : e->h_out)
+        if ((c = cudaMemcpyAsync(Tn[A], T[A], (size_t)e->n * e->Wp * 4, cudaMemcpyDeviceToDevice, s)) != cudaSuccess)
+            return c;
+    const int32_t n_rules = (int32_t)e->h_rule_out.size();
+    // chunk capacity: each (rule, row) has at most ceil(n / kChunk) chunks; grow lazily
+    const unsigned long long worst = (unsigned long long)n_rules * e->n * ((e->n + kChunk - 1) / kChunk);
+    const unsigned long long want = std::min<unsigned long long>(worst, std::max<unsigned long long>(
+        e->chunk_cap, (unsigned long long)n_rules * e->n * 2 + 1024));
+    if (want > e->chunk_cap) {
+        cudaFree(e->chunks);
+        if ((c = cudaMalloc(&e->chunks, want * sizeof(RowChunk))) != cudaSuccess) return c;
+        e->chunk_cap = want;
+    }
     DenseParams p{};
     p.n = e->n;
     p.np = e->np;
@@ -665,14 +733,22 @@ cudaError_t rows_product(DenseEngine* e, int64_t row_lo, int64_t row_hi, cudaStr
     p.Tn = e->Tnptr;
     p.new_cells = e->new_cells;
     p.n_nt = e->n_nt;
-    int dev = 0, sms = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int64_t tasks = (row_hi - row_lo) * e->n_out;
-    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)sms * 8, tasks));
-    rows_kernel<<<grid, kRowThreads, 0, s>>>(p, row_lo, row_hi);
-    if (launches) ++*launches;
-    return cudaGetLastError();
+    unsigned long long* nch = e->new_cells + e->n_nt + 1;   // reuse the k-block slot as the chunk counter
+    for (int attempt = 0; attempt < 2; ++attempt) {
+        if ((c = cudaMemsetAsync(nch, 0, 8, s)) != cudaSuccess) return c;
+        rows_plan_kernel<<<148 * 8, 256, 0, s>>>(p, e->rule_out, n_rules, (RowChunk*)e->chunks, nch, e->chunk_cap);
+        unsigned long long got = 0;
+        if ((c = cudaMemcpyAsync(&got, nch, 8, cudaMemcpyDeviceToHost, s)) != cudaSuccess) return c;
+        if ((c = cudaStreamSynchronize(s)) != cudaSuccess) return c;
+        if (got <= e->chunk_cap) break;
+        cudaFree(e->chunks);
+        e->chunk_cap = got + got / 4;
+        if ((c = cudaMalloc(&e->chunks, e->chunk_cap * sizeof(RowChunk))) != cudaSuccess) return c;
+    }
+    rows_kernel<<<148 * 8, kRowThreads, 0, s>>>(p, e->rule_out, (const RowChunk*)e->chunks, nch);
+    if (launches) *launches += 2;
+    if ((c = cudaGetLastError()) != cudaSuccess) return c;
+    return cudaMemsetAsync(nch, 0, 8, s);
 }
 
 cudaError_t dense_finish(DenseEngine* e, cudaStream_t s, unsigned long long* new_total) {
