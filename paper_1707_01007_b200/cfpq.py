@@ -250,14 +250,16 @@ class Result:
         _check(load().cfpq_result_count_at(self._h, int(A), int(k), ctypes.byref(v)), "cfpq_result_count_at")
         return v.value
 
-    def pairs(self, A: int, out=None) -> np.ndarray:
-        """R_A as int32 [m,2] ascending; `out` may be a CUDA int32 tensor [>=m,2]."""
-        m = self.count(A)
+    def pairs(self, A: int, out=None):
+        """R_A as int32 [m,2] ascending (numpy).  `out` may be an int32 torch tensor [cap,2] on
+        the device or in (pinned) host memory; then the pairs are written there and a view of
+        its first |R_A| rows is returned."""
         w = ctypes.c_int64()
         if out is not None:
-            _check(load().cfpq_result_pairs(self._h, int(A), _ptr(out), int(out.shape[0]), 1, ctypes.byref(w)),
-                   "cfpq_result_pairs")
+            _check(load().cfpq_result_pairs(self._h, int(A), _ptr(out), int(out.shape[0]), int(_is_device(out)),
+                                            ctypes.byref(w)), "cfpq_result_pairs")
             return out[: w.value]
+        m = self.count(A)
         buf = np.zeros((m, 2), dtype=np.int32)
         _check(load().cfpq_result_pairs(self._h, int(A), _ptr(buf), m, 0, ctypes.byref(w)), "cfpq_result_pairs")
         return buf[: w.value]
