@@ -31,7 +31,7 @@ constexpr int kABytes = kTM * kTK;       // 16 KiB
 constexpr int kBBytes = kTN * kTK;       // 32 KiB
 constexpr int kStageBytes = kABytes + kBBytes;
 constexpr int kDenseThreads = 192;       // 6 warps
-constexpr int kTmemCols = 256;
+constexpr int kTmemCols = 512;          // two 256-column s32 accumulators
 
 struct DenseRule {   // A -> B C, operand slots into the packed arrays
     int32_t A, B, C, pad;
@@ -209,6 +209,22 @@ __device__ __forceinline__ bool kblock_live(const DenseParams& p, const DenseRul
     return __ldg(oC + (size_t)K * p.nt_tiles + 2 * J) || __ldg(oC + (size_t)K * p.nt_tiles + 2 * J + 1);
 }
 
+// Output tile t of this rank -> (output o, row tile I, column tile J).  Tiles of one output
+// are walked in groups of kGroup row tiles, columns outer: a wave of ~148 CTAs then covers
+// a kGroup x ~18 patch whose operand blocks (A: kGroup*128 rows, B: ~18*256 rows of the
+// packs) fit in L2 together, instead of a 2-3 x 64 strip that streams all of B per wave.
+constexpr int kGroup = 8;
+__device__ __forceinline__ void tile_coords(const DenseParams& p, int t, int tiles_per_nt, int n_i, int n_j, int& o,
+                                            int& I, int& J) {
+    o = t / tiles_per_nt;
+    const int rem = t - o * tiles_per_nt;
+    const int g = rem / (kGroup * n_j);
+    const int within = rem - g * (kGroup * n_j);
+    const int rows_g = min(kGroup, n_i - g * kGroup);
+    I = p.i_lo + g * kGroup + within % rows_g;
+    J = within / rows_g;
+}
+
 __global__ void __launch_bounds__(kDenseThreads, 1)
     dense_kernel(DenseParams p, const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                  const int64_t* __restrict__ mapA_row, const int64_t* __restrict__ mapB_row) {
@@ -220,9 +236,9 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
     uint8_t* sB = smem + kStages * kABytes;              // [kStages][kBBytes]
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
     uint64_t* empty = full + kStages;
-    uint64_t* tmem_full = empty + kStages;
-    uint64_t* tmem_empty = tmem_full + 1;
-    uint32_t* tmem_base_smem = reinterpret_cast<uint32_t*>(tmem_empty + 1);
+    uint64_t* tmem_full = empty + kStages;         // [2] accumulator stages (double-buffered TMEM)
+    uint64_t* tmem_empty = tmem_full + 2;          // [2]
+    uint32_t* tmem_base_smem = reinterpret_cast<uint32_t*>(tmem_empty + 2);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int n_j = p.np / kTN;
@@ -236,8 +252,10 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
         }
-        mbar_init(tmem_full, 1);
-        mbar_init(tmem_empty, 128);
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&tmem_full[a], 1);
+            mbar_init(&tmem_empty[a], 128);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
@@ -254,8 +272,8 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
             int stage = 0;
             uint32_t phase = 0;
             for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
-                const int o = t / tiles_per_nt, rem = t - o * tiles_per_nt;
-                const int I = p.i_lo + rem / n_j, J = rem - (rem / n_j) * n_j;
+                int o, I, J;
+                tile_coords(p, t, tiles_per_nt, n_i, n_j, o, I, J);
                 for (int q = p.rule_ptr[o]; q < p.rule_ptr[o + 1]; ++q) {
                     const DenseRule r = p.rules[q];
                     const int64_t arow = __ldg(mapA_row + r.B) + (int64_t)I * kTM;
@@ -279,12 +297,14 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
         const uint32_t idesc = idesc_i8(kTM, kTN);
         int stage = 0;
         uint32_t phase = 0;
-        uint32_t tphase = 0;
+        int as = 0;              // accumulator stage of this tile
+        uint32_t tphase = 0;     // phase of the stage's barriers
         for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
-            const int o = t / tiles_per_nt, rem = t - o * tiles_per_nt;
-            const int I = p.i_lo + rem / n_j, J = rem - (rem / n_j) * n_j;
-            // the epilogue must have drained the accumulator of the previous tile
-            mbar_wait(tmem_empty, tphase ^ 1);
+            int o, I, J;
+            tile_coords(p, t, tiles_per_nt, n_i, n_j, o, I, J);
+            const uint32_t tmem_acc = tmem_base + (uint32_t)(as * 256);
+            // the epilogue must have drained this accumulator (tile t-2)
+            mbar_wait(&tmem_empty[as], tphase ^ 1);
             tc_fence_after();
             uint32_t acc = 0;
             unsigned long long kb_issued = 0;
@@ -300,7 +320,7 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
                         const uint32_t b0 = smem_u32(sB + stage * kBBytes);
 #pragma unroll
                         for (int kk = 0; kk < kTK / kUK; ++kk) {
-                            umma_i8(tmem_base, kmajor_sw128_desc(a0 + kk * kUK), kmajor_sw128_desc(b0 + kk * kUK),
+                            umma_i8(tmem_acc, kmajor_sw128_desc(a0 + kk * kUK), kmajor_sw128_desc(b0 + kk * kUK),
                                     idesc, acc);
                             acc = 1;
                         }
@@ -315,25 +335,29 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
             }
             if (lane == 0) {
                 if (kb_issued) atomicAdd(p.new_cells + p.n_nt + 1, kb_issued);
-                if (acc) umma_commit(tmem_full);   // arrives when all MMAs of the tile completed
-                else mbar_arrive(tmem_full);       // no live K block: the epilogue uses zeros
+                if (acc) umma_commit(&tmem_full[as]);   // arrives when all MMAs of the tile completed
+                else mbar_arrive(&tmem_full[as]);       // no live K block: the epilogue uses zeros
             }
             __syncwarp();
-            tphase ^= 1;
+            if (++as == 2) {
+                as = 0;
+                tphase ^= 1;
+            }
         }
     } else {
         // ------------------------------- epilogue (warps 2..5) -------------------------------
         const int quarter = warp & 3;            // TMEM lanes 32*quarter .. +31 are this warp's
+        int as = 0;
         uint32_t tphase = 0;
         unsigned long long my_new = 0;
         for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
-            const int o = t / tiles_per_nt, rem = t - o * tiles_per_nt;
-            const int I = p.i_lo + rem / n_j, J = rem - (rem / n_j) * n_j;
+            int o, I, J;
+            tile_coords(p, t, tiles_per_nt, n_i, n_j, o, I, J);
             const int A = p.out_nt[o];
             bool live = false;
             for (int q = p.rule_ptr[o]; q < p.rule_ptr[o + 1] && !live; ++q)
                 for (int K = 0; K < n_k && !live; ++K) live = kblock_live(p, p.rules[q], I, J, K);
-            mbar_wait(tmem_full, tphase);
+            mbar_wait(&tmem_full[as], tphase);
             tc_fence_after();
             const int row = I * kTM + quarter * 32 + lane;
             const uint32_t* told = p.T[A] + (size_t)row * p.Wp;
@@ -344,7 +368,7 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
                 uint32_t word = 0;
                 if (live) {
                     uint32_t v[32];
-                    tmem_ld32(tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(c * 32), v);
+                    tmem_ld32(tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(as * 256 + c * 32), v);
 #pragma unroll
                     for (int b = 0; b < 32; ++b) word |= (v[b] != 0u ? 1u : 0u) << b;
                 }
@@ -356,8 +380,11 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
                 }
             }
             tc_fence_before();
-            mbar_arrive(tmem_empty);
-            tphase ^= 1;
+            mbar_arrive(&tmem_empty[as]);
+            if (++as == 2) {
+                as = 0;
+                tphase ^= 1;
+            }
 #pragma unroll
             for (int s = 16; s > 0; s >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, s);
             if (lane == 0 && cnt) atomicAdd(p.new_cells + A, cnt);
