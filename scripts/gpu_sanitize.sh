@@ -1,0 +1,6 @@
+python -c "import __graft_entry__ as g; g.build()"
+for tool in memcheck racecheck synccheck; do
+  echo "== $tool"
+  timeout 1200 compute-sanitizer --tool $tool --error-exitcode 9 --print-limit 20 python scripts/sanitize.py > gpurun_out/sanitize_$tool.txt 2>&1
+  echo "rc=$?"; tail -4 gpurun_out/sanitize_$tool.txt
+done

@@ -1,0 +1,29 @@
+"""Small closures on every engine, for compute-sanitizer (memcheck / racecheck / synccheck)."""
+import sys, os
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import inputs as I
+import oracle as O
+from paper_1707_01007_b200 import cfpq as C
+
+def run(w, **kw):
+    g = C.Grammar.from_workload(w)
+    d = C.Graph(w.n_nodes, w.edges)
+    r = C.closure(g, d, **kw)
+    o = O.run(w, lengths=kw.get("semantics", 0) == 1)
+    for A in range(w.n_nt):
+        assert np.array_equal(r.pairs(A), o.pairs(A)), (w.name, kw)
+    return r
+
+cases = [(I.example_workload(), dict()), (I.example_workload(), dict(semantics=1)),
+         (I.anbn_workload(3, 5), dict(semantics=1)),
+         (I.ontology_workload("union", 300, depth=5, seed=1), dict(solo_threshold=0)),
+         (I.ontology_workload("union", 300, depth=5, seed=1), dict(log_capacity=64)),
+         (I.dense_stress_workload(100, 2), dict(semantics=1)),
+         (I.dense_stress_workload(200, 2), dict(path_policy=2)),
+         (I.dense_stress_workload(200, 2), dict(path_policy=3)),
+         (I.dense_stress_workload(150, 2), dict(path_policy=2, emulate_ranks=2)),
+         (I.dense_stress_workload(300, 2), dict())]
+for w, kw in cases:
+    run(w, **kw)
+    print("ok", w.name, kw, flush=True)
