@@ -184,7 +184,7 @@ class Graph:
 def options(semantics: int = 0, schedule: int = 0, path_policy: int = 0, account_work: bool = False,
             max_iterations: int = 0, stream=None, log_capacity: int = 0, solo_threshold: int = -1,
             record_times: bool = False, max_ctas: int = 0, world_size: int = 1, rank: int = 0,
-            nccl_unique_id=None, emulate_ranks: int = 0) -> Options:
+            nccl_unique_id=None, emulate_ranks: int = 0, flags: int = 0) -> Options:
     o = Options()
     load().cfpq_options_default(ctypes.byref(o))
     o.semantics, o.schedule, o.path_policy = int(semantics), int(schedule), int(path_policy)
@@ -198,6 +198,7 @@ def options(semantics: int = 0, schedule: int = 0, path_policy: int = 0, account
     o.world_size = int(world_size)
     o.rank = int(rank)
     o.emulate_ranks = int(emulate_ranks)
+    o.reserved[0] = int(flags)
     if nccl_unique_id is not None:
         buf = ctypes.create_string_buffer(bytes(nccl_unique_id), 128)
         o._uid = buf                     # keep alive with the options

@@ -166,6 +166,7 @@ struct cfpq_result {
         p.nblocks = grid;
         p.profile = opts.record_times;
         p.switch_cells = switch_cells;
+        p.precheck = opts.reserved[0] & 1;
         return p;
     }
 };

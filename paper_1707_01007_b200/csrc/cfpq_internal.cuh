@@ -117,6 +117,7 @@ struct EngineParams {
     int32_t nblocks;
     int32_t profile;               // accumulate single-CTA phase cycles into EngineState::prof
     unsigned long long switch_cells;  // |Δ_k| above which the loop stops for the dense engine (0 = never)
+    int32_t precheck;              // read a candidate's word before its atomicOr (hot cells)
 };
 
 // ------------------------------------------------------------------------------------------

@@ -33,7 +33,7 @@ namespace cfpq {
 constexpr int kBlock = 1024;
 constexpr int kWarps = kBlock / 32;
 constexpr int kSeedBlock = 256;
-constexpr int kBuf = 64;             // per-warp staging capacity (cells)
+constexpr int kBuf = 128;            // per-warp staging capacity (cells)
 constexpr int kSoloMax = 1024;       // max |Δ| mirrored in shared memory by the single-CTA path
 constexpr int kSmemNT = 64;          // NT / expansion tables cached in shared memory
 constexpr int kSmemExp = 256;
@@ -126,7 +126,9 @@ __device__ __forceinline__ bool try_insert(const EngineParams& p, const NTInfo* 
         return old == kEmptyKey;
     }
     uint32_t bit = 1u << (j & 31);
-    uint32_t old = atomicOr(nt[A].T + (size_t)i * (size_t)p.Wp + (j >> 5), bit);
+    uint32_t* word = nt[A].T + (size_t)i * (size_t)p.Wp + (j >> 5);
+    if (p.precheck && (ldcg32(word) & bit)) return false;   // already set: no RMW on a hot word
+    uint32_t old = atomicOr(word, bit);
     return !(old & bit);
 }
 
@@ -379,7 +381,8 @@ __device__ __forceinline__ int4 load_head(const NTInfo* nt, const Expansion& ex,
 // `src` = shared-memory copy of log[lo,hi) (single-CTA path) or null (read the log).
 __device__ void expand(const EngineParams& p, const NTInfo* nt, const Expansion* exps, const Sink& sk,
                        const uint64_t* src, unsigned long long lo, unsigned long long hi, long long k, int warp,
-                       int nwarps, int lane, WarpScratch* ws, unsigned long long& dcand, unsigned long long& dexp) {
+                       int nwarps, int lane, WarpScratch* ws, unsigned long long& dcand, unsigned long long& dexp,
+                       bool final_flush = true) {
     for (unsigned long long cbase = lo + (unsigned long long)warp * 32ull; cbase < hi;
          cbase += (unsigned long long)nwarps * 32ull) {
         unsigned long long e = cbase + lane;
@@ -511,7 +514,57 @@ __device__ void expand(const EngineParams& p, const NTInfo* nt, const Expansion*
             }
         }
     }
-    flush(p, nt, sk, ws, lane);
+    if (final_flush) flush(p, nt, sk, ws, lane);
+}
+
+// End of a grid-wide expansion: the CTA appends all warps' staged cells with ONE global
+// atomic (thousands of warps ending the iteration together would otherwise serialise on
+// the log counter).
+__device__ void cta_flush(const EngineParams& p, const NTInfo* nt, const Sink& sk, WarpScratch* ws_all, int wib,
+                          int lane, unsigned long long* s_base, int32_t* s_prefix) {
+    __syncthreads();
+    if (wib == 0) {
+        int nb = lane < kWarps ? ws_all[lane].nbuf : 0;
+        int incl = nb;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            int v = __shfl_up_sync(kFull, incl, o);
+            if (lane >= o) incl += v;
+        }
+        if (lane < kWarps) s_prefix[lane] = incl - nb;
+        int tot = __shfl_sync(kFull, incl, 31);
+        unsigned long long b = 0;
+        if (lane == 0 && tot) b = atomicAdd(sk.counter, (unsigned long long)tot);
+        if (lane == 0) *s_base = b;
+    }
+    __syncthreads();
+    WarpScratch* ws = &ws_all[wib];
+    const int nb = ws->nbuf;
+    const unsigned long long base = *s_base + (unsigned long long)s_prefix[wib];
+    for (int t = lane; t < nb; t += 32) {
+        uint64_t c = ws->buf[t];
+        unsigned long long idx = base + (unsigned long long)t;
+        uint32_t A = cell_nt(c), i = cell_i(c), j = cell_j(c);
+        uint64_t* K = p.lengths ? nt[A].K : nullptr;
+        uint32_t* word = nt[A].T + (size_t)i * (size_t)p.Wp + (j >> 5);
+        uint32_t bit = 1u << (j & 31);
+        if (idx < p.log_cap) {
+            p.log[idx] = c;
+            if (K != nullptr) atomicOr(word, bit);
+            if (p.rowc != nullptr) {
+                atomicAdd(p.rowc + (size_t)A * p.n + i, 1u);
+                atomicAdd(p.colc + (size_t)A * p.n + j, 1u);
+            }
+        } else {
+            if (K != nullptr) atomicExch((unsigned long long*)(K + (size_t)i * (size_t)p.n + j),
+                                         (unsigned long long)kEmptyKey);
+            else atomicAnd(word, ~bit);
+            *(volatile int*)sk.overflow = 1;
+        }
+    }
+    __syncwarp();
+    if (lane == 0) ws->nbuf = 0;
+    __syncwarp();
 }
 
 // Fold Δ_k = log[lo,hi) into the snapshots S (row) and ST (transposed).
@@ -625,8 +678,10 @@ __device__ bool grid_barrier(const EngineParams& p, long long k) {
             long long t0 = clock64();
             unsigned ns = 0;
             while (ld_acquire_u32(&st->bar_gen) == my) {
+                // poll at L2 latency for ~20 µs (grid iterations), then back off (a
+                // single-CTA phase can park the other CTAs for a long time)
                 if (ns) __nanosleep(ns);
-                ns = ns ? (ns < 2048u ? ns * 2u : 2048u) : 32u;   // exponential backoff, <= ~2 µs
+                if (clock64() - t0 > 40000) ns = ns ? (ns < 2048u ? ns * 2u : 2048u) : 64u;
                 if (clock64() - t0 > 60000000000ll) {   // ~30 s watchdog: never hang the GPU
                     s_timeout = 1;
                     break;
@@ -772,6 +827,8 @@ __device__ void solo_expand(const EngineParams& p, const NTInfo* nt, const Expan
 
 // Dynamic shared memory of the closure kernel.
 struct ClosureShared {
+    unsigned long long flush_base;
+    int32_t flush_prefix[kWarps];
     WarpScratch ws[kWarps];
     NTInfo nt[kSmemNT];
     Expansion exp[kSmemExp];
@@ -925,7 +982,8 @@ __global__ void __launch_bounds__(kBlock, 1) closure_kernel(EngineParams p) {
             }
         }
         expand(p, nt, exps, gsink, nullptr, s.lo, s.hi, k, blockIdx.x * kWarps + wib, gridDim.x * kWarps, lane,
-               &S.ws[wib], dcand, dexp);
+               &S.ws[wib], dcand, dexp, false);
+        cta_flush(p, nt, gsink, S.ws, wib, lane, &S.flush_base, S.flush_prefix);
         if (!grid_barrier(p, k)) {
             aborted = true;
             break;
