@@ -99,7 +99,11 @@ typedef struct {
     int32_t semantics;       /* 0 relational; 1 single-path lengths. Lengths need
                                 8*n^2 bytes of device memory per non-preterminal NT.     */
     int32_t schedule;        /* 0 jacobi: per-iteration states equal Alg. 1's T_k;
-                                1 seminaive: same states, same as 0 in this library       */
+                                1 seminaive: same states, same as 0 in this library;
+                                2 asynchronous: cells are expanded as soon as they appear,
+                                no iteration barriers; same fixpoint T^cf (monotone
+                                operator), no per-iteration states (iterations = 0);
+                                relational semantics, sparse engine, |N| <= 512            */
     int32_t path_policy;     /* 0 auto: sparse, switching to tensor when Δ turns dense and a
                                 rule has two changing operands; 1 sparse (index-list semi-
                                 naive); 2 tensor (tcgen05 int8 dense); 3 rows (bit-row full-

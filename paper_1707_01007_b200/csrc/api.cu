@@ -635,6 +635,52 @@ static cfpq_status run_dense(cfpq_result* r, int64_t start_k) {
     return CFPQ_OK;
 }
 
+// Asynchronous schedule (schedule 2, relational): one barrier-free worklist kernel; on a
+// log overflow the host grows the log and the kernel re-expands the whole (still valid,
+// flagged) log from slot 0 — idempotent, since re-derived cells are already set.
+static cfpq_status run_async(cfpq_result* r, unsigned long long seeds_upper) {
+    cudaStream_t s = r->stream;
+    bool first = true;
+    for (;;) {
+        EngineParams p = r->params();
+        CFPQ_CUDA_TRY(launch_async(p, r->grid, s, first, seeds_upper));
+        CFPQ_CUDA_TRY(cudaEventRecord(r->ev[3], s));
+        r->launches += first ? 2 : 1;
+        CFPQ_CUDA_TRY(cudaMemcpyAsync(&r->h_st, r->d_st, sizeof(EngineState), cudaMemcpyDeviceToHost, s));
+        CFPQ_CUDA_TRY(cudaStreamSynchronize(s));
+        first = false;
+        if (r->h_st.bad_edge) {
+            r->n_cells = std::min<unsigned long long>(r->h_st.log_size, r->log_cap);
+            CFPQ_CUDA_TRY(launch_strip_flags(r->d_log, 0, r->n_cells, s));
+            set_error("graph has an edge with a node id >= n_nodes or a label id >= n_labels");
+            return CFPQ_E_INVAL;
+        }
+        if (!r->h_st.overflow) break;
+        unsigned long long old_cap = r->log_cap;
+        cfpq_status st = grow_log(r, r->h_st.log_size);
+        if (st != CFPQ_OK) return st;
+        CFPQ_CUDA_TRY(cudaMemsetAsync(r->d_log + old_cap, 0, (r->log_cap - old_cap) * 8, s));
+        EngineState fix = r->h_st;
+        fix.log_size = std::min<unsigned long long>(r->h_st.log_size, old_cap);
+        fix.overflow = 0;
+        fix.async_head = 0;
+        fix.async_done = 0;
+        CFPQ_CUDA_TRY(cudaMemcpyAsync(r->d_st, &fix, sizeof(EngineState), cudaMemcpyHostToDevice, s));
+    }
+    r->n_cells = std::min<unsigned long long>(r->h_st.log_size, r->log_cap);
+    CFPQ_CUDA_TRY(launch_strip_flags(r->d_log, 0, r->n_cells, s));
+    {
+        float ms = 0;
+        CFPQ_CUDA_TRY(cudaEventElapsedTime(&ms, r->ev[0], r->ev[1]));
+        r->seed_ns = ms * 1e6;
+        CFPQ_CUDA_TRY(cudaEventElapsedTime(&ms, r->ev[1], r->ev[3]));
+        r->loop_ns = ms * 1e6;
+    }
+    CFPQ_CUDA_TRY(cudaStreamSynchronize(s));
+    r->iterations = 0;   // no loop bodies: the asynchronous schedule has no iteration structure
+    return CFPQ_OK;
+}
+
 static cfpq_status run(cfpq_result* r, const cfpq_graph* d) {
     cudaStream_t s = r->stream;
     r->launches = 0;
@@ -670,6 +716,8 @@ static cfpq_status run(cfpq_result* r, const cfpq_graph* d) {
         CFPQ_CUDA_TRY(cudaMemsetAsync(r->d_adj_cnt, 0, (size_t)r->n_adj_slots * (r->n + 1) * 4, s));
     if (r->opts.account_work) CFPQ_CUDA_TRY(cudaMemsetAsync(r->d_jac, 0, r->iter_off_cap * 8, s));
     CFPQ_CUDA_TRY(cudaMemsetAsync(r->d_st, 0, sizeof(EngineState), s));
+    const bool async = r->opts.schedule == 2;
+    if (async) CFPQ_CUDA_TRY(cudaMemsetAsync(r->d_log, 0, r->log_cap * 8, s));   // valid flags start clear
     if (!r->ev[0])
         for (auto& e : r->ev) CFPQ_CUDA_TRY(cudaEventCreate(&e));
     r->seed_ns = r->loop_ns = 0;
@@ -697,6 +745,7 @@ static cfpq_status run(cfpq_result* r, const cfpq_graph* d) {
     }
     CFPQ_CUDA_TRY(cudaEventRecord(r->ev[1], s));
     if (r->opts.path_policy == 2 || r->opts.path_policy == 3) return run_dense(r, 0);
+    if (async) return run_async(r, seeds_upper);
     // a2-a5: the fixpoint loop, device-resident
     bool first = true;
     for (;;) {
@@ -773,7 +822,11 @@ static cfpq_status run(cfpq_result* r, const cfpq_graph* d) {
 static cfpq_status check_inputs(const cfpq_grammar* g, const cfpq_graph* d, const cfpq_options* o) {
     CFPQ_CHECK_ARG(g != nullptr && d != nullptr && o != nullptr, "cfpq_closure: NULL grammar/graph/options");
     CFPQ_CHECK_ARG(o->semantics == 0 || o->semantics == 1, "cfpq_closure: semantics must be 0 or 1");
-    CFPQ_CHECK_ARG(o->schedule == 0 || o->schedule == 1, "cfpq_closure: schedule must be 0 (jacobi) or 1 (seminaive)");
+    CFPQ_CHECK_ARG(o->schedule >= 0 && o->schedule <= 2, "cfpq_closure: schedule must be 0, 1 or 2");
+    if (o->schedule == 2 && (o->semantics != 0 || o->path_policy > 1 || g->n_nt > 512)) {
+        set_error("cfpq_closure: schedule 2 (asynchronous) is relational, sparse-engine only, |N| <= 512");
+        return CFPQ_E_UNSUPPORTED;
+    }
     CFPQ_CHECK_ARG(o->world_size >= 0 && o->reserved_emulate >= 0, "cfpq_closure: bad world_size / emulate_ranks");
     if ((o->world_size > 1 || o->reserved_emulate > 1) && o->path_policy != 2) {
         set_error("cfpq_closure: row-block sharding is implemented for the dense engine (path_policy 2); "
@@ -836,6 +889,11 @@ extern "C" cfpq_status cfpq_closure_reuse(const cfpq_grammar* g, const cfpq_grap
     if (o->max_iterations > 0) r->opts.max_iterations = o->max_iterations;
     if (o->solo_threshold >= 0) r->opts.solo_threshold = o->solo_threshold;
     r->opts.record_times = o->record_times;
+    if (o->schedule == 2 && (r->opts.semantics != 0 || r->n_nt > 512)) {
+        set_error("cfpq_closure_reuse: schedule 2 is relational with |N| <= 512");
+        return CFPQ_E_UNSUPPORTED;
+    }
+    r->opts.schedule = o->schedule;
     return run(r, d);
 }
 

@@ -81,7 +81,9 @@ struct EngineState {
     unsigned long long candidates; // expanded candidates = semi-naive AND-true triples
     unsigned long long expansions; // (Δ entry, rule occurrence) pairs expanded
     long long solo_iters;          // iterations run by the single-CTA path
-    unsigned long long prof[7];    // single-CTA phase cycle counters (record_times diagnostics)
+    unsigned long long prof[5];    // single-CTA phase cycle counters (record_times diagnostics)
+    unsigned long long async_head; // asynchronous schedule: next log slot to claim
+    unsigned long long async_done; // asynchronous schedule: log entries fully expanded
     unsigned bar_count;            // grid-barrier words, on their own 128-byte line
     unsigned bar_gen;
     unsigned long long snap_ls[2]; // log size when iteration k closed (slot k&1)
@@ -118,6 +120,7 @@ struct EngineParams {
     int32_t profile;               // accumulate single-CTA phase cycles into EngineState::prof
     unsigned long long switch_cells;  // |Δ_k| above which the loop stops for the dense engine (0 = never)
     int32_t precheck;              // read a candidate's word before its atomicOr (hot cells)
+    unsigned long long async_init; // asynchronous schedule: log entries < this are valid unflagged
 };
 
 // ------------------------------------------------------------------------------------------
@@ -166,6 +169,9 @@ cudaError_t launch_adj_fill(const EngineParams& p, const int32_t* slot_row, cons
                             int32_t* cursor, int32_t* idx, unsigned long long n_seed_upper, cudaStream_t s);
 cudaError_t launch_clear_log(const EngineParams& p, unsigned long long n_cells, cudaStream_t s);
 cudaError_t launch_begin(const EngineParams& p, cudaStream_t s);
+cudaError_t launch_async(const EngineParams& p, int grid, cudaStream_t s, bool flag_seeds,
+                         unsigned long long seeds_upper);
+cudaError_t launch_strip_flags(uint64_t* log, unsigned long long lo, unsigned long long hi, cudaStream_t s);
 cudaError_t launch_adj_ell(const int32_t* ptr, const int32_t* idx, int4* ell, int64_t n_slots, int32_t n,
                            cudaStream_t s);
 cudaError_t launch_seed_snapshots(const EngineParams& p, unsigned long long n_seed_upper, cudaStream_t s);

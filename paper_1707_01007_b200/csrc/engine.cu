@@ -67,6 +67,7 @@ __device__ __forceinline__ unsigned lanemask_lt(int lane) { return (1u << lane) 
 // for grid-wide iterations and in shared memory for single-CTA iterations; the single-
 // CTA path also mirrors Δ_k into shared memory (mirror[idx - mirror_base]).
 struct Sink {
+    uint64_t tag;                  // OR-ed into every appended entry (asynchronous schedule: valid flag)
     unsigned long long* counter;
     int* overflow;
     int* len_overflow;
@@ -150,8 +151,12 @@ __device__ __forceinline__ void flush(const EngineParams& p, const NTInfo* nt, c
         uint32_t* word = nt[A].T + (size_t)i * (size_t)p.Wp + (j >> 5);
         uint32_t bit = 1u << (j & 31);
         if (idx < p.log_cap) {
-            p.log[idx] = c;
+            p.log[idx] = c | sk.tag;
             if (sk.mirror != nullptr && idx - sk.mirror_base < sk.mirror_cap) sk.mirror[idx - sk.mirror_base] = c;
+            if (sk.tag) {   // asynchronous schedule: snapshots are live (any state <= T^cf is sound)
+                if (nt[A].S) atomicOr(nt[A].S + (size_t)i * p.Wp + (j >> 5), 1u << (j & 31));
+                if (nt[A].ST) atomicOr(nt[A].ST + (size_t)j * p.Wp + (i >> 5), 1u << (i & 31));
+            }
             if (K != nullptr) atomicOr(word, bit);   // the bit matrix mirrors the keys
             if (p.rowc != nullptr) {
                 atomicAdd(p.rowc + (size_t)A * p.n + i, 1u);
@@ -196,6 +201,7 @@ __device__ __forceinline__ void emit(const EngineParams& p, const NTInfo* nt, co
 
 __device__ __forceinline__ Sink global_sink(const EngineParams& p) {
     Sink sk;
+    sk.tag = 0;
     sk.counter = &p.st->log_size;
     sk.overflow = &p.st->overflow;
     sk.len_overflow = &p.st->len_overflow;
@@ -376,6 +382,136 @@ __device__ __forceinline__ int4 load_head(const NTInfo* nt, const Expansion& ex,
     return __ldg(nt[ex.other].csc_ell + ci);
 }
 
+// Expand one 32-entry chunk (one entry per lane, `valid` lanes only) of iteration k.
+__device__ __forceinline__ void expand_chunk(const EngineParams& p, const NTInfo* nt, const Expansion* exps,
+                                             const Sink& sk, uint64_t cell, bool valid, long long k, int lane,
+                                             WarpScratch* ws, unsigned long long& dcand, unsigned long long& dexp) {
+    uint32_t X = cell_nt(cell), ci = cell_i(cell), cj = cell_j(cell);
+    int eb = 0, nexp = 0;
+    if (valid) {
+        eb = nt[X].exp_begin;
+        nexp = nt[X].exp_end - eb;
+    }
+    dexp += (unsigned long long)nexp;
+    uint32_t len_e = 0;
+    if (p.lengths && nexp > 0) len_e = (uint32_t)cell_len(p, nt, X, ci, cj);
+    int maxexp = nexp;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) maxexp = max(maxexp, __shfl_xor_sync(kFull, maxexp, o));
+    if (maxexp == 0) return;
+
+    // ---- preterminal-operand occurrences 0..kPre-1: all loads, then all atomics ----
+    unsigned var_mask = 0;
+    int4 el[kPre];
+    uint32_t eA[kPre], efx[kPre];
+#pragma unroll
+    for (int x = 0; x < kPre; ++x) {
+        el[x] = make_int4(0, 0, -1, -1);
+        eA[x] = 0;
+        efx[x] = 0;
+        if (x < nexp) {
+            Expansion ex = exps[eb + x];
+            if (ex.kind == EXP_L_CONST || ex.kind == EXP_R_CONST) el[x] = load_head(nt, ex, ci, cj, eA[x], efx[x]);
+            else var_mask |= 1u << x;
+        }
+    }
+    bool d0[kPre], d1[kPre];
+    uint32_t ci0[kPre], cj0[kPre], ci1[kPre], cj1[kPre];
+#pragma unroll
+    for (int x = 0; x < kPre; ++x) {
+        cand_coords(efx[x], el[x].z, ci0[x], cj0[x]);
+        cand_coords(efx[x], el[x].w, ci1[x], cj1[x]);
+        uint64_t l0 = (uint64_t)len_e + 1ull, l1 = l0;
+        bool k0 = warp_dedup(p, sk, el[x].y > 0, eA[x], ci0[x], cj0[x], l0, lane);
+        bool k1 = warp_dedup(p, sk, el[x].y > 1, eA[x], ci1[x], cj1[x], l1, lane);
+        d0[x] = try_insert(p, nt, sk, k0, eA[x], ci0[x], cj0[x], l0, k);
+        d1[x] = try_insert(p, nt, sk, k1, eA[x], ci1[x], cj1[x], l1, k);
+        dcand += (unsigned long long)el[x].y;
+    }
+    bool any_tail = false;
+#pragma unroll
+    for (int x = 0; x < kPre; ++x) {
+        if (x < maxexp) {
+            stage(p, nt, sk, ws, lane, d0[x], eA[x], ci0[x], cj0[x]);
+            stage(p, nt, sk, ws, lane, d1[x], eA[x], ci1[x], cj1[x]);
+            any_tail |= el[x].y > 2;
+        }
+    }
+    if (__any_sync(kFull, any_tail)) {
+#pragma unroll
+        for (int x = 0; x < kPre; ++x)
+            if (x < maxexp) expand_tail(p, nt, sk, ws, lane, el[x], eA[x], efx[x], len_e, k);
+    }
+    // ---- occurrences kPre.. (rare: NTs on the RHS of many rules) ----
+    for (int x = kPre; x < maxexp; ++x) {
+        int4 h = make_int4(0, 0, -1, -1);
+        uint32_t A = 0, fx = 0;
+        if (x < nexp) {
+            Expansion ex = exps[eb + x];
+            if (ex.kind == EXP_L_CONST || ex.kind == EXP_R_CONST) h = load_head(nt, ex, ci, cj, A, fx);
+            else if (x < 32) var_mask |= 1u << x;
+        }
+        uint32_t a0, b0, a1, b1;
+        cand_coords(fx, h.z, a0, b0);
+        cand_coords(fx, h.w, a1, b1);
+        uint64_t l0 = (uint64_t)len_e + 1ull, l1 = l0;
+        bool k0 = warp_dedup(p, sk, h.y > 0, A, a0, b0, l0, lane);
+        bool k1 = warp_dedup(p, sk, h.y > 1, A, a1, b1, l1, lane);
+        bool q0 = try_insert(p, nt, sk, k0, A, a0, b0, l0, k);
+        bool q1 = try_insert(p, nt, sk, k1, A, a1, b1, l1, k);
+        dcand += (unsigned long long)h.y;
+        stage(p, nt, sk, ws, lane, q0, A, a0, b0);
+        stage(p, nt, sk, ws, lane, q1, A, a1, b1);
+        if (__any_sync(kFull, h.y > 2)) expand_tail(p, nt, sk, ws, lane, h, A, fx, len_e, k);
+    }
+    // ---- rules whose other operand also changes: scan the snapshot row, warp-cooperative ----
+    unsigned any_var = __ballot_sync(kFull, var_mask != 0);
+    while (any_var) {
+        int src = __ffs(any_var) - 1;
+        any_var &= any_var - 1;
+        unsigned vm = __shfl_sync(kFull, var_mask, src);
+        uint32_t si = __shfl_sync(kFull, ci, src);
+        uint32_t sj = __shfl_sync(kFull, cj, src);
+        uint32_t slen = __shfl_sync(kFull, len_e, src);
+        int seb = __shfl_sync(kFull, eb, src);
+        while (vm) {
+            int x = __ffs(vm) - 1;
+            vm &= vm - 1;
+            Expansion ex = exps[seb + x];
+            const uint32_t* row;
+            bool left = ex.kind == EXP_L_VAR;
+            if (left) row = nt[ex.other].S + (size_t)sj * p.Wp;    // S_C row r = sj
+            else row = nt[ex.other].ST + (size_t)si * p.Wp;        // ST_B row r = si
+            const int64_t wn = (p.n + 31) >> 5;
+            for (int64_t w0 = 0; w0 < wn; w0 += 32) {
+                int64_t w = w0 + lane;
+                uint32_t bits = (w < wn) ? ldcg32(row + w) : 0u;
+                while (__any_sync(kFull, bits != 0u)) {
+                    bool has = bits != 0u;
+                    uint32_t oi = 0, oj = 0;
+                    uint64_t clen = 0;
+                    if (has) {
+                        int b = __ffs(bits) - 1;
+                        bits &= bits - 1u;
+                        uint32_t v = (uint32_t)(w * 32 + b);
+                        if (left) {
+                            oi = si;
+                            oj = v;
+                            if (p.lengths) clen = (uint64_t)slen + cell_len(p, nt, ex.other, sj, v);
+                        } else {
+                            oi = v;
+                            oj = sj;
+                            if (p.lengths) clen = cell_len(p, nt, ex.other, v, si) + (uint64_t)slen;
+                        }
+                        ++dcand;
+                    }
+                    emit(p, nt, sk, ws, lane, has, (uint32_t)ex.A, oi, oj, clen, k);
+                }
+            }
+        }
+    }
+}
+
 // Expand the Δ entries log[lo,hi) of iteration k.  Work unit = a chunk of 32
 // consecutive entries per warp; warps [warp, warp+nwarps) stride over chunks.
 // `src` = shared-memory copy of log[lo,hi) (single-CTA path) or null (read the log).
@@ -389,130 +525,7 @@ __device__ void expand(const EngineParams& p, const NTInfo* nt, const Expansion*
         bool valid = e < hi;
         uint64_t cell = 0ull;
         if (valid) cell = src ? src[e - lo] : ldcg64(p.log + e);
-        uint32_t X = cell_nt(cell), ci = cell_i(cell), cj = cell_j(cell);
-        int eb = 0, nexp = 0;
-        if (valid) {
-            eb = nt[X].exp_begin;
-            nexp = nt[X].exp_end - eb;
-        }
-        dexp += (unsigned long long)nexp;
-        uint32_t len_e = 0;
-        if (p.lengths && nexp > 0) len_e = (uint32_t)cell_len(p, nt, X, ci, cj);
-        int maxexp = nexp;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) maxexp = max(maxexp, __shfl_xor_sync(kFull, maxexp, o));
-        if (maxexp == 0) continue;
-
-        // ---- preterminal-operand occurrences 0..kPre-1: all loads, then all atomics ----
-        unsigned var_mask = 0;
-        int4 el[kPre];
-        uint32_t eA[kPre], efx[kPre];
-#pragma unroll
-        for (int x = 0; x < kPre; ++x) {
-            el[x] = make_int4(0, 0, -1, -1);
-            eA[x] = 0;
-            efx[x] = 0;
-            if (x < nexp) {
-                Expansion ex = exps[eb + x];
-                if (ex.kind == EXP_L_CONST || ex.kind == EXP_R_CONST) el[x] = load_head(nt, ex, ci, cj, eA[x], efx[x]);
-                else var_mask |= 1u << x;
-            }
-        }
-        bool d0[kPre], d1[kPre];
-        uint32_t ci0[kPre], cj0[kPre], ci1[kPre], cj1[kPre];
-#pragma unroll
-        for (int x = 0; x < kPre; ++x) {
-            cand_coords(efx[x], el[x].z, ci0[x], cj0[x]);
-            cand_coords(efx[x], el[x].w, ci1[x], cj1[x]);
-            uint64_t l0 = (uint64_t)len_e + 1ull, l1 = l0;
-            bool k0 = warp_dedup(p, sk, el[x].y > 0, eA[x], ci0[x], cj0[x], l0, lane);
-            bool k1 = warp_dedup(p, sk, el[x].y > 1, eA[x], ci1[x], cj1[x], l1, lane);
-            d0[x] = try_insert(p, nt, sk, k0, eA[x], ci0[x], cj0[x], l0, k);
-            d1[x] = try_insert(p, nt, sk, k1, eA[x], ci1[x], cj1[x], l1, k);
-            dcand += (unsigned long long)el[x].y;
-        }
-        bool any_tail = false;
-#pragma unroll
-        for (int x = 0; x < kPre; ++x) {
-            if (x < maxexp) {
-                stage(p, nt, sk, ws, lane, d0[x], eA[x], ci0[x], cj0[x]);
-                stage(p, nt, sk, ws, lane, d1[x], eA[x], ci1[x], cj1[x]);
-                any_tail |= el[x].y > 2;
-            }
-        }
-        if (__any_sync(kFull, any_tail)) {
-#pragma unroll
-            for (int x = 0; x < kPre; ++x)
-                if (x < maxexp) expand_tail(p, nt, sk, ws, lane, el[x], eA[x], efx[x], len_e, k);
-        }
-        // ---- occurrences kPre.. (rare: NTs on the RHS of many rules) ----
-        for (int x = kPre; x < maxexp; ++x) {
-            int4 h = make_int4(0, 0, -1, -1);
-            uint32_t A = 0, fx = 0;
-            if (x < nexp) {
-                Expansion ex = exps[eb + x];
-                if (ex.kind == EXP_L_CONST || ex.kind == EXP_R_CONST) h = load_head(nt, ex, ci, cj, A, fx);
-                else if (x < 32) var_mask |= 1u << x;
-            }
-            uint32_t a0, b0, a1, b1;
-            cand_coords(fx, h.z, a0, b0);
-            cand_coords(fx, h.w, a1, b1);
-            uint64_t l0 = (uint64_t)len_e + 1ull, l1 = l0;
-            bool k0 = warp_dedup(p, sk, h.y > 0, A, a0, b0, l0, lane);
-            bool k1 = warp_dedup(p, sk, h.y > 1, A, a1, b1, l1, lane);
-            bool q0 = try_insert(p, nt, sk, k0, A, a0, b0, l0, k);
-            bool q1 = try_insert(p, nt, sk, k1, A, a1, b1, l1, k);
-            dcand += (unsigned long long)h.y;
-            stage(p, nt, sk, ws, lane, q0, A, a0, b0);
-            stage(p, nt, sk, ws, lane, q1, A, a1, b1);
-            if (__any_sync(kFull, h.y > 2)) expand_tail(p, nt, sk, ws, lane, h, A, fx, len_e, k);
-        }
-        // ---- rules whose other operand also changes: scan the snapshot row, warp-cooperative ----
-        unsigned any_var = __ballot_sync(kFull, var_mask != 0);
-        while (any_var) {
-            int src = __ffs(any_var) - 1;
-            any_var &= any_var - 1;
-            unsigned vm = __shfl_sync(kFull, var_mask, src);
-            uint32_t si = __shfl_sync(kFull, ci, src);
-            uint32_t sj = __shfl_sync(kFull, cj, src);
-            uint32_t slen = __shfl_sync(kFull, len_e, src);
-            int seb = __shfl_sync(kFull, eb, src);
-            while (vm) {
-                int x = __ffs(vm) - 1;
-                vm &= vm - 1;
-                Expansion ex = exps[seb + x];
-                const uint32_t* row;
-                bool left = ex.kind == EXP_L_VAR;
-                if (left) row = nt[ex.other].S + (size_t)sj * p.Wp;    // S_C row r = sj
-                else row = nt[ex.other].ST + (size_t)si * p.Wp;        // ST_B row r = si
-                const int64_t wn = (p.n + 31) >> 5;
-                for (int64_t w0 = 0; w0 < wn; w0 += 32) {
-                    int64_t w = w0 + lane;
-                    uint32_t bits = (w < wn) ? ldcg32(row + w) : 0u;
-                    while (__any_sync(kFull, bits != 0u)) {
-                        bool has = bits != 0u;
-                        uint32_t oi = 0, oj = 0;
-                        uint64_t clen = 0;
-                        if (has) {
-                            int b = __ffs(bits) - 1;
-                            bits &= bits - 1u;
-                            uint32_t v = (uint32_t)(w * 32 + b);
-                            if (left) {
-                                oi = si;
-                                oj = v;
-                                if (p.lengths) clen = (uint64_t)slen + cell_len(p, nt, ex.other, sj, v);
-                            } else {
-                                oi = v;
-                                oj = sj;
-                                if (p.lengths) clen = cell_len(p, nt, ex.other, v, si) + (uint64_t)slen;
-                            }
-                            ++dcand;
-                        }
-                        emit(p, nt, sk, ws, lane, has, (uint32_t)ex.A, oi, oj, clen, k);
-                    }
-                }
-            }
-        }
+        expand_chunk(p, nt, exps, sk, cell, valid, k, lane, ws, dcand, dexp);
     }
     if (final_flush) flush(p, nt, sk, ws, lane);
 }
@@ -1025,7 +1038,125 @@ __global__ void __launch_bounds__(kBlock, 1) closure_kernel(EngineParams p) {
     }
 }
 
+static int grid_for(int64_t work, int block);
 size_t closure_kernel_smem() { return sizeof(ClosureShared); }
+
+// ------------------------------------------------------------------------------------------
+// Asynchronous (chaotic) schedule, relational semantics only (schedule 2).
+// T ↦ T ∪ T×T is monotone, so ANY fair order of applying it reaches the same least
+// fixpoint T^cf; the per-iteration states of Alg. 1 are not reproduced.  Every warp claims
+// 32 log slots at a time and expands each entry as soon as it has been appended (entries
+// carry a valid flag, bit 63); no grid barrier at all.  Quiescence: a warp counts its
+// entries as done only after flushing the cells they produced, so done == appended (read
+// in that order) means nothing is pending or in flight.
+// ------------------------------------------------------------------------------------------
+constexpr uint64_t kValid = 1ull << 63;
+
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__global__ void __launch_bounds__(kBlock, 1) async_kernel(EngineParams p) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    ClosureShared& S = *reinterpret_cast<ClosureShared*>(smem_raw);
+    const int lane = threadIdx.x & 31;
+    const int wib = threadIdx.x >> 5;
+    EngineState* st = p.st;
+    const bool small = p.n_nt <= kSmemNT && p.n_exps <= kSmemExp;
+    if (small) {
+        for (int t = threadIdx.x; t < p.n_nt; t += kBlock) S.nt[t] = p.nt[t];
+        for (int t = threadIdx.x; t < p.n_exps; t += kBlock) S.exp[t] = p.exps[t];
+    }
+    const NTInfo* nt = small ? S.nt : p.nt;
+    const Expansion* exps = small ? S.exp : p.exps;
+    Sink sk = global_sink(p);
+    sk.tag = kValid;
+    WarpScratch* ws = &S.ws[wib];
+    if (lane == 0) ws->nbuf = 0;
+    __syncthreads();
+    unsigned long long dcand = 0, dexp = 0;
+    bool finished = false;
+    while (!finished) {
+        unsigned long long c = 0;
+        if (lane == 0) c = atomicAdd(&st->async_head, 32ull);
+        c = __shfl_sync(kFull, c, 0);
+        unsigned pending = kFull;
+        unsigned ns = 0;
+        while (pending) {
+            const unsigned long long e = c + lane;
+            bool ok = false;
+            uint64_t cell = 0;
+            if ((pending >> lane) & 1u) {
+                if (e < p.log_cap) {
+                    uint64_t v = ldcg64(p.log + e);
+                    ok = (v & kValid) != 0;
+                    cell = v & ~kValid;
+                }
+            }
+            const unsigned okm = __ballot_sync(kFull, ok);
+            if (okm) {
+                expand_chunk(p, nt, exps, sk, cell, ok, 0, lane, ws, dcand, dexp);
+                flush(p, nt, sk, ws, lane);   // produced cells are appended before ours count as done
+                if (lane == 0) {
+                    __threadfence();
+                    atomicAdd(&st->async_done, (unsigned long long)__popc(okm));
+                }
+                pending &= ~okm;
+                ns = 0;
+            } else {
+                int fin = 0;
+                if (lane == 0) {
+                    const unsigned long long d = ld_acquire_u64(&st->async_done);
+                    const unsigned long long t = ld_acquire_u64(&st->log_size);
+                    fin = (d == t) || *(volatile int*)&st->overflow || *(volatile int*)&st->bad_edge;
+                }
+                fin = __shfl_sync(kFull, fin, 0);
+                if (fin) {
+                    finished = true;
+                    break;
+                }
+                if (ns) __nanosleep(ns);
+                ns = ns ? (ns < 1024u ? ns * 2u : 1024u) : 64u;
+            }
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        dcand += __shfl_xor_sync(kFull, dcand, o);
+        dexp += __shfl_xor_sync(kFull, dexp, o);
+    }
+    if (lane == 0) {
+        if (dcand) atomicAdd(&st->candidates, dcand);
+        if (dexp) atomicAdd(&st->expansions, dexp);
+    }
+}
+
+__global__ void flag_seeds_kernel(EngineParams p) {
+    const unsigned long long n0 = ld_volatile_u64(&p.st->log_size);
+    for (unsigned long long e = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; e < n0;
+         e += (unsigned long long)gridDim.x * blockDim.x)
+        p.log[e] |= kValid;
+}
+
+__global__ void strip_flags_kernel(uint64_t* log, unsigned long long lo, unsigned long long hi) {
+    for (unsigned long long e = lo + blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; e < hi;
+         e += (unsigned long long)gridDim.x * blockDim.x)
+        log[e] &= ~kValid;
+}
+
+cudaError_t launch_async(const EngineParams& p, int grid, cudaStream_t s, bool flag_seeds,
+                         unsigned long long seeds_upper) {
+    if (flag_seeds && seeds_upper) flag_seeds_kernel<<<grid_for((int64_t)seeds_upper, 256), 256, 0, s>>>(p);
+    async_kernel<<<grid, kBlock, sizeof(ClosureShared), s>>>(p);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_strip_flags(uint64_t* log, unsigned long long lo, unsigned long long hi, cudaStream_t s) {
+    if (hi > lo) strip_flags_kernel<<<grid_for((int64_t)(hi - lo), 256), 256, 0, s>>>(log, lo, hi);
+    return cudaGetLastError();
+}
 
 // After seeding: Δ_0 = log[0, log_size) (T_0), iteration 0 complete.
 __global__ void begin_kernel(EngineParams p) {
@@ -1106,6 +1237,8 @@ int closure_kernel_blocks_per_sm() {
     int nb = 0;
     const size_t smem = sizeof(ClosureShared);
     if (cudaFuncSetAttribute(closure_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+        return 0;
+    if (cudaFuncSetAttribute(async_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
         return 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, closure_kernel, kBlock, smem) != cudaSuccess) return 0;
     return nb;
