@@ -81,7 +81,7 @@ struct EngineState {
     unsigned long long candidates; // expanded candidates = semi-naive AND-true triples
     unsigned long long expansions; // (Δ entry, rule occurrence) pairs expanded
     long long solo_iters;          // iterations run by the single-CTA path
-    unsigned long long prof[5];    // single-CTA phase cycle counters (record_times diagnostics)
+    unsigned long long prof[7];    // single-CTA phase cycle counters (record_times diagnostics)
     unsigned long long async_head; // asynchronous schedule: next log slot to claim
     unsigned long long async_done; // asynchronous schedule: log entries fully expanded
     unsigned bar_count;            // grid-barrier words, on their own 128-byte line

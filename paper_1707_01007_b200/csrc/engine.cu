@@ -759,6 +759,139 @@ __device__ __forceinline__ bool solo_try(const EngineParams& p, const NTInfo* nt
     return !(atomicOr(nt[A].T + (size_t)i * (size_t)p.Wp + (j >> 5), bit) & bit);
 }
 
+// ------------------------------------------------------------------------------------------
+// Warp-solo iterations (|Δ| <= 32): warp 0 of CTA 0 alone, one Δ entry per lane, no CTA
+// barrier (__syncwarp only), appends positioned by a shared counter of this warp only.
+// The a^n b^n worst case (one new cell per iteration, 2pq+1 iterations) lives here.
+// ------------------------------------------------------------------------------------------
+struct WarpSoloShared {
+    uint64_t nxt[32];
+    int cnt;
+    int ov, lov;
+};
+
+__device__ __forceinline__ bool ws_try(const EngineParams& p, const NTInfo* nt, uint32_t A, uint32_t i, uint32_t j,
+                                       uint64_t len, long long k, int* lov) {
+    uint64_t* K = nt[A].K;
+    if (p.lengths && K != nullptr) {
+        if (len > 0xffffffffull) {
+            *(volatile int*)lov = 1;
+            len = 0xffffffffull;
+        }
+        uint64_t old = atomicMin((unsigned long long*)(K + (size_t)i * (size_t)p.n + j),
+                                 (unsigned long long)(((uint64_t)k << 32) | len));
+        return old == kEmptyKey;
+    }
+    uint32_t bit = 1u << (j & 31);
+    return !(atomicOr(nt[A].T + (size_t)i * (size_t)p.Wp + (j >> 5), bit) & bit);
+}
+
+__device__ __forceinline__ void ws_append(const EngineParams& p, const NTInfo* nt, WarpSoloShared& w,
+                                          unsigned long long base, uint32_t A, uint32_t i, uint32_t j) {
+    const int pos = atomicAdd(&w.cnt, 1);
+    const unsigned long long idx = base + (unsigned long long)pos;
+    const uint64_t c = pack_cell(A, i, j);
+    uint64_t* K = p.lengths ? nt[A].K : nullptr;
+    uint32_t* word = nt[A].T + (size_t)i * (size_t)p.Wp + (j >> 5);
+    const uint32_t bit = 1u << (j & 31);
+    if (idx < p.log_cap) {
+        p.log[idx] = c;
+        if (pos < 32) w.nxt[pos] = c;
+        if (K != nullptr) atomicOr(word, bit);
+        if (p.rowc != nullptr) {
+            atomicAdd(p.rowc + (size_t)A * p.n + i, 1u);
+            atomicAdd(p.colc + (size_t)A * p.n + j, 1u);
+        }
+    } else {
+        if (K != nullptr) atomicExch((unsigned long long*)(K + (size_t)i * (size_t)p.n + j), (unsigned long long)kEmptyKey);
+        else atomicAnd(word, ~bit);
+        w.ov = 1;
+    }
+}
+
+// Runs iterations while |Δ| <= 32; returns with `s` closed at the last iteration run.
+__device__ void warp_solo(const EngineParams& p, const NTInfo* nt, const Expansion* exps, WarpSoloShared& w,
+                          LoopState& s, long long& iters, unsigned long long& dcand, unsigned long long& dexp) {
+    const int lane = threadIdx.x & 31;
+    long long k = s.iter + 1;
+    int m = (int)(s.hi - s.lo);
+    uint64_t cell = lane < m ? ldcg64(p.log + s.lo + lane) : 0ull;
+    for (;;) {
+        if (lane == 0) {
+            w.cnt = 0;
+            w.ov = 0;
+            w.lov = 0;
+        }
+        __syncwarp();
+        const unsigned long long base = s.hi;
+        if (lane < m) {
+            const uint32_t X = cell_nt(cell), ci = cell_i(cell), cj = cell_j(cell);
+            const int eb = nt[X].exp_begin, ee = nt[X].exp_end;
+            dexp += (unsigned long long)(ee - eb);
+            const uint64_t len_e = (p.lengths && ee > eb) ? cell_len(p, nt, X, ci, cj) : 0;
+            for (int x = eb; x < ee; ++x) {
+                const Expansion ex = exps[x];
+                if (ex.kind == EXP_L_CONST || ex.kind == EXP_R_CONST) {
+                    uint32_t A, fx;
+                    const int4 h = load_head(nt, ex, ci, cj, A, fx);
+                    dcand += (unsigned long long)h.y;
+                    uint32_t a0, b0, a1, b1;
+                    cand_coords(fx, h.z, a0, b0);
+                    cand_coords(fx, h.w, a1, b1);
+                    const bool n0 = h.y > 0 && ws_try(p, nt, A, a0, b0, len_e + 1, k, &w.lov);
+                    const bool n1 = h.y > 1 && ws_try(p, nt, A, a1, b1, len_e + 1, k, &w.lov);
+                    if (n0) ws_append(p, nt, w, base, A, a0, b0);
+                    if (n1) ws_append(p, nt, w, base, A, a1, b1);
+                    for (int t = 2; t < h.y; ++t) {
+                        uint32_t a, b;
+                        cand_coords(fx, __ldg(p.adj_idx + h.x + t), a, b);
+                        if (ws_try(p, nt, A, a, b, len_e + 1, k, &w.lov)) ws_append(p, nt, w, base, A, a, b);
+                    }
+                } else {
+                    const bool left = ex.kind == EXP_L_VAR;
+                    const uint32_t* row = left ? nt[ex.other].S + (size_t)cj * p.Wp : nt[ex.other].ST + (size_t)ci * p.Wp;
+                    const int64_t wn = (p.n + 31) >> 5;
+                    for (int64_t wd = 0; wd < wn; ++wd) {
+                        uint32_t bits = ldcg32(row + wd);
+                        while (bits) {
+                            const int b = __ffs(bits) - 1;
+                            bits &= bits - 1u;
+                            const uint32_t v = (uint32_t)(wd * 32 + b);
+                            const uint32_t oi = left ? ci : v, oj = left ? v : cj;
+                            uint64_t clen = 0;
+                            if (p.lengths)
+                                clen = left ? len_e + cell_len(p, nt, ex.other, cj, v) : cell_len(p, nt, ex.other, v, ci) + len_e;
+                            ++dcand;
+                            if (ws_try(p, nt, (uint32_t)ex.A, oi, oj, clen, k, &w.lov))
+                                ws_append(p, nt, w, base, (uint32_t)ex.A, oi, oj);
+                        }
+                    }
+                }
+            }
+        }
+        __syncwarp();
+        const int total = *(volatile int*)&w.cnt;
+        const int f = (*(volatile int*)&w.ov ? 1 : 0) | (*(volatile int*)&w.lov ? 2 : 0);
+        close_iteration(p, k, s, base + (unsigned long long)total, f, lane == 0);
+        ++iters;
+        if (s.status != ST_RUNNING) break;
+        if (p.has_snapshots) {
+            for (int q = lane; q < total; q += 32) {
+                const uint64_t c = q < 32 ? w.nxt[q] : ldcg64(p.log + s.lo + q);
+                const uint32_t A = cell_nt(c), i = cell_i(c), j = cell_j(c);
+                if (nt[A].S) atomicOr(nt[A].S + (size_t)i * p.Wp + (j >> 5), 1u << (j & 31));
+                if (nt[A].ST) atomicOr(nt[A].ST + (size_t)j * p.Wp + (i >> 5), 1u << (i & 31));
+            }
+            __syncwarp();
+        }
+        ++k;
+        if (total > 32 || total > p.solo_max) break;   // hand over to the CTA or grid paths
+        m = total;
+        cell = lane < m ? w.nxt[lane] : 0ull;
+        __syncwarp();
+    }
+}
+
 // Prefetch into L1 the ELL head that the next iteration reads for candidate (A,i,j)
 // if it becomes new (its first two rule occurrences); overlaps with the bit atomic.
 __device__ __forceinline__ void prefetch_next(const NTInfo* nt, const Expansion* exps, uint32_t A, uint32_t i,
@@ -840,6 +973,7 @@ __device__ void solo_expand(const EngineParams& p, const NTInfo* nt, const Expan
 
 // Dynamic shared memory of the closure kernel.
 struct ClosureShared {
+    WarpSoloShared wsolo;
     unsigned long long flush_base;
     int32_t flush_prefix[kWarps];
     WarpScratch ws[kWarps];
@@ -881,6 +1015,28 @@ __global__ void __launch_bounds__(kBlock, 1) closure_kernel(EngineParams p) {
         if ((long long)(s.hi - s.lo) <= (long long)p.solo_max) {
             // ------------- single-CTA iterations (see SoloShared) -------------
             if (blockIdx.x == 0) {
+                // warp-solo first while |Δ| <= 32 (not on the re-run of an overflowed iteration)
+                if (wib == 0 && s.hi - s.lo <= 32 && !p.jac && ld_volatile_u64(&st->log_size) == s.hi) {
+                    long long wi = 0;
+                    warp_solo(p, nt, exps, S.wsolo, s, wi, dcand, dexp);
+                    if (lane == 0) {
+                        unsigned long long ls = s.hi;
+                        if (s.status == ST_OVERFLOW || s.status == ST_LEN_OVERFLOW) {
+                            // s still holds iteration k's range; the counter went past the log
+                            ls = s.hi + (unsigned long long)S.wsolo.cnt;
+                            if (S.wsolo.ov) st->overflow = 1;
+                            if (S.wsolo.lov) st->len_overflow = 1;
+                        }
+                        st->log_size = ls;
+                        atomicAdd((unsigned long long*)&st->solo_iters, (unsigned long long)wi);
+                        S.state = s;
+                    }
+                }
+                __syncthreads();
+                s = S.state;
+                k = s.iter + 1;
+            }
+            if (blockIdx.x == 0 && s.status == ST_RUNNING && (long long)(s.hi - s.lo) <= (long long)p.solo_max) {
                 SoloShared& so = S.solo;
                 int cur = 0;
                 const unsigned long long ls0 = ld_volatile_u64(&st->log_size);
@@ -968,6 +1124,8 @@ __global__ void __launch_bounds__(kBlock, 1) closure_kernel(EngineParams p) {
                     so.solo = 0;
                     publish(p, s);
                 }
+            } else if (blockIdx.x == 0 && threadIdx.x == 0) {
+                publish(p, s);   // warp-solo ended the phase (done, or Δ grew past the CTA path)
             }
             if (!grid_barrier(p, -1)) {
                 aborted = true;
