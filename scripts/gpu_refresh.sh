@@ -1,0 +1,22 @@
+# refresh the round's bench lines and ncu evidence (run under gpurun)
+set -x
+python -c "import __graft_entry__ as g; g.build()"
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw,temperature.gpu --format=csv > gpurun_out/nvsmi.txt
+for W in config4 configS config3 config5 config2; do
+  timeout 900 python bench.py --workload $W --steps 10 --warmup 3 > gpurun_out/bench_$W.json 2> gpurun_out/bench_$W.err
+done
+timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_reference.json 2>&1
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_config4.csv \
+   python bench.py --workload config4 --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --no-supplementary > /dev/null 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:closure_kernel -s 5 -c 1 \
+   -o gpurun_out/prof_config4 python bench.py --workload config4 --steps 1 --warmup 3 --no-e2e --no-cpu-baseline --no-supplementary > gpurun_out/ncu_c4.txt 2>&1
+timeout 900 ncu --set full --clock-control none -k regex:rows_kernel -s 5 -c 1 -o gpurun_out/prof_rows \
+   python -c "
+import sys; sys.path.insert(0,'.')
+import torch, inputs as I
+from paper_1707_01007_b200 import cfpq as C
+w=I.config4_workload(); g=C.Grammar.from_workload(w); d=C.Graph(w.n_nodes, torch.from_numpy(w.edges).cuda())
+r=C.closure(g,d,path_policy=3)
+" > gpurun_out/ncu_rows.txt 2>&1
+tail -2 gpurun_out/ncu_c4.txt gpurun_out/ncu_rows.txt
+ls -la gpurun_out | head -40
