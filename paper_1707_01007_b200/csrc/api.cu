@@ -49,6 +49,27 @@ static void dfree(T*& p) {
     p = nullptr;
 }
 
+// A workspace bank: everything a closure derives into.  A reused result keeps two banks
+// and alternates: the next run starts on the clean bank while the previous run's cells are
+// cleared from the other bank on a side stream (O(|cells|) scattered stores, overlapped).
+struct Bank {
+    uint32_t* d_T = nullptr;
+    uint32_t* d_snap = nullptr;
+    uint64_t* d_K = nullptr;
+    NTInfo* d_nt = nullptr;
+    uint64_t* d_log = nullptr;
+    unsigned long long log_cap = 0;
+    unsigned long long n_cells = 0;
+    uint32_t* d_rowc = nullptr;
+    uint32_t* d_colc = nullptr;
+    std::vector<NTInfo> h_nt;
+    std::vector<uint32_t*> Tbase;
+    void release() {
+        dfree(d_T); dfree(d_snap); dfree(d_K); dfree(d_nt); dfree(d_log); dfree(d_rowc); dfree(d_colc);
+        log_cap = n_cells = 0;
+    }
+};
+
 struct cfpq_result {
     // shape
     int64_t n = 0;
@@ -127,7 +148,18 @@ struct cfpq_result {
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
     double seed_ns = 0, loop_ns = 0;
 
+    // second workspace bank (see Bank)
+    Bank spare;
+    bool have_spare = false, spare_failed = false;
+    cudaStream_t side = nullptr;
+    cudaEvent_t spare_clean = nullptr, main_done = nullptr;
+
     ~cfpq_result() {
+        if (side) cudaStreamSynchronize(side);
+        spare.release();
+        if (side) cudaStreamDestroy(side);
+        if (spare_clean) cudaEventDestroy(spare_clean);
+        if (main_done) cudaEventDestroy(main_done);
         for (auto& e : ev)
             if (e) cudaEventDestroy(e);
         dfree(d_T); dfree(d_snap); dfree(d_K); dfree(d_nt); dfree(d_exps); dfree(d_rules);
@@ -286,6 +318,73 @@ static cfpq_status ensure_dense(cfpq_result* r) {
     if (st != CFPQ_OK) return st;
     CFPQ_CUDA_TRY(cudaMemsetAsync(r->d_Tn, 0, mat_words * std::max(n_out, 1) * 4, r->stream));
     return CFPQ_OK;
+}
+
+static void swap_with(cfpq_result* r, Bank& b) {
+    std::swap(r->d_T, b.d_T);
+    std::swap(r->d_snap, b.d_snap);
+    std::swap(r->d_K, b.d_K);
+    std::swap(r->d_nt, b.d_nt);
+    std::swap(r->d_log, b.d_log);
+    std::swap(r->log_cap, b.log_cap);
+    std::swap(r->n_cells, b.n_cells);
+    std::swap(r->d_rowc, b.d_rowc);
+    std::swap(r->d_colc, b.d_colc);
+    std::swap(r->h_nt, b.h_nt);
+    std::swap(r->Tbase, b.Tbase);
+}
+
+// Allocate the second bank with the same shapes as the current one (zeroed bitmaps, EMPTY
+// keys).  Returns false (and the result keeps one bank) if the memory is not there.
+static bool make_spare(cfpq_result* r) {
+    Bank& b = r->spare;
+    const size_t mw = (size_t)r->rows_alloc * (size_t)r->Wp;
+    int n_snap = 0, n_key = 0;
+    for (auto& t : r->h_nt) {
+        n_snap += (t.S ? 1 : 0) + (t.ST ? 1 : 0);
+        n_key += t.K ? 1 : 0;
+    }
+    auto ok = [](cudaError_t e) {
+        if (e != cudaSuccess) cudaGetLastError();
+        return e == cudaSuccess;
+    };
+    cudaStream_t s = r->stream;
+    bool good = ok(cudaMalloc(&b.d_T, mw * r->n_nt * 4)) && ok(cudaMemsetAsync(b.d_T, 0, mw * r->n_nt * 4, s));
+    if (good && n_snap) good = ok(cudaMalloc(&b.d_snap, mw * n_snap * 4)) && ok(cudaMemsetAsync(b.d_snap, 0, mw * n_snap * 4, s));
+    if (good && n_key)
+        good = ok(cudaMalloc(&b.d_K, (size_t)r->n * r->n * n_key * 8)) &&
+               ok(cudaMemsetAsync(b.d_K, 0xff, (size_t)r->n * r->n * n_key * 8, s));
+    if (good) good = ok(cudaMalloc(&b.d_log, r->log_cap * 8));
+    if (good && r->d_rowc)
+        good = ok(cudaMalloc(&b.d_rowc, (size_t)r->n_nt * r->n * 4)) && ok(cudaMalloc(&b.d_colc, (size_t)r->n_nt * r->n * 4)) &&
+               ok(cudaMemsetAsync(b.d_rowc, 0, (size_t)r->n_nt * r->n * 4, s)) &&
+               ok(cudaMemsetAsync(b.d_colc, 0, (size_t)r->n_nt * r->n * 4, s));
+    if (good) good = ok(cudaMalloc(&b.d_nt, r->n_nt * sizeof(NTInfo)));
+    if (!good) {
+        b.release();
+        return false;
+    }
+    b.log_cap = r->log_cap;
+    b.n_cells = 0;
+    b.h_nt = r->h_nt;
+    b.Tbase.assign(r->n_nt, nullptr);
+    int snap_i = 0, key_i = 0;
+    for (int A = 0; A < r->n_nt; ++A) {
+        NTInfo& t = b.h_nt[A];
+        t.T = b.d_T + (size_t)A * mw;
+        if (t.S) t.S = b.d_snap + (size_t)(snap_i++) * mw;
+        if (t.ST) t.ST = b.d_snap + (size_t)(snap_i++) * mw;
+        if (t.K) t.K = b.d_K + (size_t)(key_i++) * r->n * r->n;
+        b.Tbase[A] = t.T;
+    }
+    if (!ok(cudaMemcpyAsync(b.d_nt, b.h_nt.data(), r->n_nt * sizeof(NTInfo), cudaMemcpyHostToDevice, s))) {
+        b.release();
+        return false;
+    }
+    if (!r->side && !ok(cudaStreamCreateWithFlags(&r->side, cudaStreamNonBlocking))) return false;
+    if (!r->spare_clean && !ok(cudaEventCreateWithFlags(&r->spare_clean, cudaEventDisableTiming))) return false;
+    if (!r->main_done && !ok(cudaEventCreateWithFlags(&r->main_done, cudaEventDisableTiming))) return false;
+    return true;
 }
 
 // ------------------------------------------------------------------------------------------
@@ -705,10 +804,42 @@ static cfpq_status run(cfpq_result* r, const cfpq_graph* d) {
         p = r->params();
     }
     r->dense_mode = false;
-    // clear what a previous run derived (bitmaps, snapshots, keys, counters): O(|log|)
+    // the previous run's cells (bitmaps, snapshots, keys, counters) must go: O(|log|).
+    // With two banks, switch to the clean bank and clear the old one on a side stream,
+    // overlapped with this run; else clear inline.
     if (r->ran && r->n_cells) {
-        CFPQ_CUDA_TRY(launch_clear_log(p, r->n_cells, s));
-        r->launches++;
+        if (!r->have_spare && !r->spare_failed && r->opts.path_policy < 2) {
+            r->have_spare = make_spare(r);
+            r->spare_failed = !r->have_spare;
+        }
+        if (r->have_spare) {
+            swap_with(r, r->spare);                       // current = clean bank
+            CFPQ_CUDA_TRY(cudaStreamWaitEvent(s, r->spare_clean, 0));   // its clear has finished
+            CFPQ_CUDA_TRY(cudaEventRecord(r->main_done, s));
+            CFPQ_CUDA_TRY(cudaStreamWaitEvent(r->side, r->main_done, 0));
+            // clear the bank of the previous run (now the spare) on the side stream
+            swap_with(r, r->spare);
+            EngineParams pc = r->params();                // parameters of the old bank
+            const unsigned long long old_cells = r->n_cells;
+            swap_with(r, r->spare);
+            CFPQ_CUDA_TRY(launch_clear_log(pc, old_cells, r->side));
+            CFPQ_CUDA_TRY(cudaEventRecord(r->spare_clean, r->side));
+            r->spare.n_cells = 0;
+            r->launches++;
+            st = size_for_graph(r, d);                    // the clean bank's log may be smaller
+            if (st != CFPQ_OK) return st;
+            if (r->log_cap < r->spare.log_cap) {          // the other bank's log grew last run
+                uint64_t* nl = nullptr;
+                if ((st = dalloc(&nl, r->spare.log_cap, "cell log")) != CFPQ_OK) return st;
+                dfree(r->d_log);
+                r->d_log = nl;
+                r->log_cap = r->spare.log_cap;
+            }
+            p = r->params();
+        } else {
+            CFPQ_CUDA_TRY(launch_clear_log(p, r->n_cells, s));
+            r->launches++;
+        }
     }
     r->ran = true;
     r->n_cells = 0;

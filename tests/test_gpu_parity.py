@@ -1,5 +1,6 @@
 """GPU parity: libcfpq (through its C-ABI / Python binding) against the oracle,
 element by element, bit-exact (integer work, so exact equality)."""
+import dataclasses
 from math import gcd
 
 import numpy as np
@@ -203,6 +204,43 @@ def test_reuse_and_set_edges():
     d.set_edges(w2.edges)
     C.closure_reuse(g, d, r)
     assert_parity(w2, r)
+
+
+def test_reuse_bank_rotation():
+    """Reused results alternate two workspace banks (the old one is cleared on a side
+    stream): many reuses over graphs of different sizes, a log that regrows in one bank
+    only, lengths semantics and the auto switch to the dense engine keep exact parity."""
+    from paper_1707_01007_b200 import cfpq as C
+    ws = [I.ontology_workload("union", 500, depth=6, seed=s) for s in range(3)]
+    ws.append(dataclasses.replace(ws[0], name="small", edges=ws[0].edges[: len(ws[0].edges) // 6].copy()))
+    ores = [O.run(w) for w in ws]
+    g = C.Grammar.from_workload(ws[0])
+    d = C.Graph(ws[0].n_nodes, ws[0].edges)
+    r = C.closure(g, d, log_capacity=64)
+    for rep in range(9):
+        k = [0, 1, 3, 2, 0, 0, 3, 1, 2][rep]
+        d.set_edges(ws[k].edges)
+        C.closure_reuse(g, d, r, log_capacity=64)
+        assert_parity(ws[k], r, ores[k])
+    wl = [I.anbn_workload(4, 6), I.anbn_workload(6, 4)]
+    gl = C.Grammar.from_workload(wl[0])
+    dl = C.Graph(wl[0].n_nodes, wl[0].edges)
+    rl = C.closure(gl, dl, semantics=1)
+    for rep in range(4):
+        w = wl[rep % 2]
+        dl.set_edges(w.edges)
+        C.closure_reuse(gl, dl, rl, semantics=1)
+        assert_parity(w, rl, lengths=True)
+    # auto policy: a sparse run, then one that switches to the dense engine, then sparse
+    wd = I.dense_stress_workload(300, 2, seed=11)
+    ws2 = I.dense_stress_workload(300, 1, seed=4)
+    gd = C.Grammar.from_workload(wd)
+    dd = C.Graph(wd.n_nodes, ws2.edges)
+    rd = C.closure(gd, dd)
+    for w in (ws2, wd, ws2, ws2, wd):
+        dd.set_edges(w.edges)
+        C.closure_reuse(gd, dd, rd)
+        assert_parity(w, rd)
 
 
 def test_device_edges():
