@@ -197,6 +197,14 @@ CFPQ_API cfpq_status cfpq_result_iteration_stats(cfpq_result* r, int64_t* new_ce
 CFPQ_API cfpq_status cfpq_result_iteration_stats2(cfpq_result* r, int64_t* new_cells, int64_t* jacobi_triples,
                                                   int64_t* end_ns, int64_t capacity);
 
+/* Diagnostics of a run with record_times = 1: cycles[(k-1)*4 + q] for grid-wide iteration k
+ * (SM clock cycles; 0 for iterations run by one CTA or warp):
+ *   q = 0  expansion of Δ_{k-1}, max over CTAs     q = 1  CTA flush of staged cells, max
+ *   q = 2  grid-barrier wait of the last CTA to arrive (min over CTAs)
+ *   q = 3  close of the iteration (range / flag update), max over CTAs
+ * capacity = number of iterations the caller's buffer holds (4 entries each). */
+CFPQ_API cfpq_status cfpq_result_iteration_phases(cfpq_result* r, int64_t* cycles, int64_t capacity);
+
 /* Multi-GPU bootstrap: write a fresh ncclUniqueId (128 bytes) into out[bytes].  NCCL is
  * loaded at run time (libnccl.so.2); CFPQ_E_NCCL if it is unavailable. */
 CFPQ_API cfpq_status cfpq_nccl_unique_id(void* out, int64_t bytes);

@@ -28,7 +28,8 @@ EXPORTS = [
     "cfpq_graph_destroy", "cfpq_options_default", "cfpq_closure", "cfpq_closure_reuse",
     "cfpq_result_destroy", "cfpq_result_iterations", "cfpq_result_count", "cfpq_result_count_at",
     "cfpq_result_pairs", "cfpq_result_pairs_at", "cfpq_result_matrix", "cfpq_result_lengths",
-    "cfpq_result_stats", "cfpq_result_iteration_stats", "cfpq_result_iteration_stats2", "cfpq_last_error",
+    "cfpq_result_stats", "cfpq_result_iteration_stats", "cfpq_result_iteration_stats2",
+    "cfpq_result_iteration_phases", "cfpq_last_error",
     "cfpq_version", "cfpq_nccl_unique_id", "cfpq_shard_rows",
 ]
 
@@ -83,6 +84,7 @@ def load() -> ctypes.CDLL:
         "cfpq_result_stats": (i32, [vp, P(i64), i32]),
         "cfpq_result_iteration_stats": (i32, [vp, vp, vp, i64]),
         "cfpq_result_iteration_stats2": (i32, [vp, vp, vp, vp, i64]),
+        "cfpq_result_iteration_phases": (i32, [vp, vp, i64]),
         "cfpq_last_error": (ctypes.c_char_p, []),
         "cfpq_version": (ctypes.c_char_p, []),
         "cfpq_nccl_unique_id": (i32, [vp, i64]),
@@ -311,6 +313,14 @@ class Result:
         t = np.zeros(k, dtype=np.int64)
         _check(load().cfpq_result_iteration_stats2(self._h, None, None, _ptr(t), k), "cfpq_result_iteration_stats2")
         return t
+
+    def iteration_phases(self) -> np.ndarray:
+        """[k, 4] SM cycles per grid-wide iteration: expand, CTA flush, barrier (last
+        arriver), close (record_times runs only)."""
+        k = self.iterations
+        c = np.zeros((k, 4), dtype=np.int64)
+        _check(load().cfpq_result_iteration_phases(self._h, _ptr(c), k), "cfpq_result_iteration_phases")
+        return c
 
 
 def closure(grammar: Grammar, graph: Graph, opts: Optional[Options] = None, **kw) -> Result:

@@ -107,6 +107,7 @@ struct cfpq_result {
     long long iter_off_cap = 0;
     unsigned long long* d_jac = nullptr;
     unsigned long long* d_iter_time = nullptr;
+    unsigned long long* d_phase = nullptr;
     uint32_t* d_rowc = nullptr;
     uint32_t* d_colc = nullptr;
     void* d_temp = nullptr;
@@ -165,7 +166,7 @@ struct cfpq_result {
         dfree(d_T); dfree(d_snap); dfree(d_K); dfree(d_nt); dfree(d_exps); dfree(d_rules);
         dfree(d_lab_ptr); dfree(d_lab_nt); dfree(d_slot_row); dfree(d_slot_col); dfree(d_adj_cnt);
         dfree(d_adj_ptr); dfree(d_adj_cursor); dfree(d_adj_idx); dfree(d_adj_ell); dfree(d_log); dfree(d_st);
-        dfree(d_iter_off); dfree(d_jac); dfree(d_iter_time); dfree(d_rowc); dfree(d_colc); dfree(d_temp); dfree(d_keys);
+        dfree(d_iter_off); dfree(d_jac); dfree(d_iter_time); dfree(d_phase); dfree(d_rowc); dfree(d_colc); dfree(d_temp); dfree(d_keys);
         dfree(d_small); dfree(d_Tn); dfree(d_rowcnt); dfree(d_rowoff);
         if (dense) dense_destroy(dense);
         if (comm) nccl_comm_destroy(comm);
@@ -187,6 +188,7 @@ struct cfpq_result {
         p.iter_off_cap = iter_off_cap;
         p.jac = opts.account_work ? d_jac : nullptr;
         p.iter_time = opts.record_times ? d_iter_time : nullptr;
+        p.phase = opts.record_times ? d_phase : nullptr;
         p.rowc = opts.account_work ? d_rowc : nullptr;
         p.colc = opts.account_work ? d_colc : nullptr;
         p.rules = d_rules;
@@ -542,6 +544,7 @@ static cfpq_status plan(cfpq_result* r, const cfpq_grammar* g, const cfpq_graph*
     r->iter_off_cap = std::min<long long>(r->opts.max_iterations + 2, 1ll << 22);
     if ((st = dalloc(&r->d_iter_off, (size_t)r->iter_off_cap, "iteration offsets")) != CFPQ_OK) return st;
     if ((st = dalloc(&r->d_iter_time, (size_t)r->iter_off_cap, "iteration timestamps")) != CFPQ_OK) return st;
+    if ((st = dalloc(&r->d_phase, (size_t)r->iter_off_cap * 4, "iteration phases")) != CFPQ_OK) return st;
     if (o->account_work) {
         if ((st = dalloc(&r->d_jac, (size_t)r->iter_off_cap, "work counts")) != CFPQ_OK) return st;
         if ((st = dalloc(&r->d_rowc, (size_t)g->n_nt * n, "row counts")) != CFPQ_OK) return st;
@@ -849,6 +852,7 @@ static cfpq_status run(cfpq_result* r, const cfpq_graph* d) {
     CFPQ_CUDA_TRY(cudaMemsetAsync(r->d_st, 0, sizeof(EngineState), s));
     const bool async = r->opts.schedule == 2;
     if (async) CFPQ_CUDA_TRY(cudaMemsetAsync(r->d_log, 0, r->log_cap * 8, s));   // valid flags start clear
+    if (r->opts.record_times) CFPQ_CUDA_TRY(cudaMemsetAsync(r->d_phase, 0, r->iter_off_cap * 32, s));
     if (!r->ev[0])
         for (auto& e : r->ev) CFPQ_CUDA_TRY(cudaEventCreate(&e));
     r->seed_ns = r->loop_ns = 0;
@@ -1322,6 +1326,22 @@ extern "C" cfpq_status cfpq_result_iteration_stats2(cfpq_result* r, int64_t* new
         CFPQ_CUDA_TRY(cudaMemcpy(t.data(), r->d_iter_time, (k + 1) * 8, cudaMemcpyDeviceToHost));
         for (int64_t q = 1; q <= k; ++q) end_ns[q - 1] = (int64_t)(t[q] - t[0]);
     }
+    return CFPQ_OK;
+}
+
+extern "C" cfpq_status cfpq_result_iteration_phases(cfpq_result* r, int64_t* cycles, int64_t capacity) {
+    CFPQ_CHECK_ARG(r != nullptr && cycles != nullptr, "cfpq_result_iteration_phases: NULL argument");
+    CFPQ_CHECK_ARG(r->opts.record_times, "cfpq_result_iteration_phases: run with record_times = 1");
+    const int64_t k = std::min<int64_t>(std::min<int64_t>(r->iterations, capacity), r->iter_off_cap - 1);
+    CFPQ_CUDA_TRY(cudaStreamSynchronize(r->stream));
+    std::vector<unsigned long long> ph((size_t)(k + 1) * 4);
+    CFPQ_CUDA_TRY(cudaMemcpy(ph.data(), r->d_phase, ph.size() * 8, cudaMemcpyDeviceToHost));
+    for (int64_t t = 1; t <= k; ++t)
+        for (int q = 0; q < 4; ++q) {
+            unsigned long long v = ph[(size_t)t * 4 + q];
+            if (q == 2) v = v ? ~v : 0ull;
+            cycles[(t - 1) * 4 + q] = (int64_t)v;
+        }
     return CFPQ_OK;
 }
 

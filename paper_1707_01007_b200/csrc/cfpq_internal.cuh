@@ -108,6 +108,7 @@ struct EngineParams {
     long long iter_off_cap;
     unsigned long long* jac;       // per-iteration Jacobi triple counts (account mode) or null
     unsigned long long* iter_time; // per-iteration %globaltimer stamps (ns) at finalize, [iter_off_cap]
+    unsigned long long* phase;     // diagnostics: per grid iteration [k][4] SM cycles (see closure_kernel)
     uint32_t* rowc;                // account mode: per NT row / column nnz of T (n_nt*n each)
     uint32_t* colc;
     const int32_t* rules;          // [n_rules][3] (account mode)

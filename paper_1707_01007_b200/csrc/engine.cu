@@ -1152,13 +1152,23 @@ __global__ void __launch_bounds__(kBlock, 1) closure_kernel(EngineParams p) {
                 break;
             }
         }
+        // diagnostics (p.phase): per iteration, max over CTAs of [0] expand, [1] CTA flush,
+        // [3] close; [2] = ~(min over CTAs of the barrier wait) = the last arriver's release
+        const bool ph = p.phase != nullptr && k < p.iter_off_cap;
+        long long c0 = ph ? clock64() : 0, c1 = 0, c2 = 0, c3 = 0;
         expand(p, nt, exps, gsink, nullptr, s.lo, s.hi, k, blockIdx.x * kWarps + wib, gridDim.x * kWarps, lane,
                &S.ws[wib], dcand, dexp, false);
+        if (ph) {
+            __syncthreads();
+            c1 = clock64();
+        }
         cta_flush(p, nt, gsink, S.ws, wib, lane, &S.flush_base, S.flush_prefix);
+        if (ph) c2 = clock64();
         if (!grid_barrier(p, k)) {
             aborted = true;
             break;
         }
+        if (ph) c3 = clock64();
         if (threadIdx.x == 0) {
             LoopState t = s;
             close_iteration(p, k, t, ld_volatile_u64(&st->snap_ls[k & 1]), *(volatile int*)&st->snap_flags[k & 1],
@@ -1169,6 +1179,13 @@ __global__ void __launch_bounds__(kBlock, 1) closure_kernel(EngineParams p) {
         LoopState prev = s;
         s = S.state;
         __syncthreads();
+        if (ph && threadIdx.x == 0) {
+            unsigned long long* q = p.phase + 4 * k;
+            atomicMax(q + 0, (unsigned long long)(c1 - c0));
+            atomicMax(q + 1, (unsigned long long)(c2 - c1));
+            atomicMax(q + 2, ~(unsigned long long)(c3 - c2));
+            atomicMax(q + 3, (unsigned long long)(clock64() - c3));
+        }
         if (s.status == ST_OVERFLOW || s.status == ST_LEN_OVERFLOW) {
             // keep the pre-iteration range for the host's re-run
             s.lo = prev.lo;
