@@ -127,7 +127,12 @@ typedef struct {
     int32_t max_ctas;        /* diagnostics: limit the closure kernel's grid (0 = full)    */
     int32_t reserved_emulate;/* testing: > 1 runs that many row-block shards in this process
                                 on one GPU (the multi-GPU partition without NCCL)           */
-    int32_t reserved[4];     /* must be zero                                               */
+    int32_t cell_set;        /* membership structure of the sparse engine: 0 auto (hashed
+                                where allowed and the bit matrices would exceed 1/4 of free
+                                HBM), 1 bit matrices, 2 hashed cell set (relational,
+                                path_policy 0/1, no rule whose two operands both change,
+                                |N| < 1024; else CFPQ_E_UNSUPPORTED)                         */
+    int32_t reserved[3];     /* must be zero                                               */
 } cfpq_options;
 
 CFPQ_API void cfpq_options_default(cfpq_options* o);
@@ -186,7 +191,8 @@ CFPQ_API cfpq_status cfpq_result_lengths(cfpq_result* r, int32_t nt, uint32_t* d
  *   kernel, [11..17] single-CTA phase cycle counters (only with record_times), [18] tcgen05
  *   k-blocks issued by the dense engine (each 128x256x128 int8 MMA work = 2^23 ops),
  *   [19] 1 if the last closure finished on the dense engine (path_policy 2, or the auto
- *   policy switched to it once Δ became dense).
+ *   policy switched to it once Δ became dense), [20] 1 if the cells were kept in the
+ *   hashed cell set (cell_set), [21] its capacity in slots.
  * Per-iteration arrays (length = iterations) via cfpq_result_iteration_stats:
  *   new_cells[k-1] = |T_k \ T_{k-1}|, jacobi_triples[k-1] (only with account_work). */
 CFPQ_API cfpq_status cfpq_result_stats(const cfpq_result* r, int64_t* stats, int32_t n_stats);

@@ -48,7 +48,8 @@ class Options(ctypes.Structure):
                 ("nccl_unique_id", ctypes.c_void_p), ("log_capacity", ctypes.c_int64),
                 ("solo_threshold", ctypes.c_int32), ("record_times", ctypes.c_int32),
                 ("max_ctas", ctypes.c_int32), ("emulate_ranks", ctypes.c_int32),
-                ("reserved", ctypes.c_int32 * 4)]
+                ("cell_set", ctypes.c_int32),
+                ("reserved", ctypes.c_int32 * 3)]
 
 
 _lib = None
@@ -186,7 +187,7 @@ class Graph:
 def options(semantics: int = 0, schedule: int = 0, path_policy: int = 0, account_work: bool = False,
             max_iterations: int = 0, stream=None, log_capacity: int = 0, solo_threshold: int = -1,
             record_times: bool = False, max_ctas: int = 0, world_size: int = 1, rank: int = 0,
-            nccl_unique_id=None, emulate_ranks: int = 0, flags: int = 0) -> Options:
+            nccl_unique_id=None, emulate_ranks: int = 0, flags: int = 0, cell_set: int = 0) -> Options:
     o = Options()
     load().cfpq_options_default(ctypes.byref(o))
     o.semantics, o.schedule, o.path_policy = int(semantics), int(schedule), int(path_policy)
@@ -201,6 +202,7 @@ def options(semantics: int = 0, schedule: int = 0, path_policy: int = 0, account
     o.rank = int(rank)
     o.emulate_ranks = int(emulate_ranks)
     o.reserved[0] = int(flags)
+    o.cell_set = int(cell_set)
     if nccl_unique_id is not None:
         buf = ctypes.create_string_buffer(bytes(nccl_unique_id), 128)
         o._uid = buf                     # keep alive with the options
@@ -292,11 +294,12 @@ class Result:
         return buf[: w.value]
 
     def stats(self) -> dict:
-        v = (ctypes.c_int64 * 20)()
-        _check(load().cfpq_result_stats(self._h, v, 20), "cfpq_result_stats")
+        v = (ctypes.c_int64 * 22)()
+        _check(load().cfpq_result_stats(self._h, v, 22), "cfpq_result_stats")
         keys = ["iterations", "cells", "log_capacity", "regrows", "launches", "solo_iterations", "candidates",
                 "expansions", "seed_ns", "loop_ns", "ctas", "prof_loop", "prof_expand", "prof_bar1",
-                "prof_close", "prof_4", "prof_head", "prof_atomic", "mma_kblocks", "dense_finish"]
+                "prof_close", "prof_4", "prof_head", "prof_atomic", "mma_kblocks", "dense_finish", "hashed",
+                "hash_capacity"]
         return dict(zip(keys, list(v)))
 
     def iteration_stats(self, work: bool = False) -> Tuple[np.ndarray, Optional[np.ndarray]]:

@@ -62,11 +62,14 @@ struct Bank {
     unsigned long long n_cells = 0;
     uint32_t* d_rowc = nullptr;
     uint32_t* d_colc = nullptr;
+    unsigned long long* d_hset = nullptr;
+    unsigned long long hcap = 0;
     std::vector<NTInfo> h_nt;
     std::vector<uint32_t*> Tbase;
     void release() {
         dfree(d_T); dfree(d_snap); dfree(d_K); dfree(d_nt); dfree(d_log); dfree(d_rowc); dfree(d_colc);
-        log_cap = n_cells = 0;
+        dfree(d_hset);
+        log_cap = n_cells = hcap = 0;
     }
 };
 
@@ -102,6 +105,10 @@ struct cfpq_result {
     int64_t adj_idx_cap = 0;
     uint64_t* d_log = nullptr;
     unsigned long long log_cap = 0;
+    // hashed cell set (see engine.cu): replaces the T bit matrices when `hashed`
+    bool hashed = false;
+    unsigned long long* d_hset = nullptr;
+    unsigned long long hcap = 0;              // slots, a power of two >= 2 * log_cap
     EngineState* d_st = nullptr;
     unsigned long long* d_iter_off = nullptr;
     long long iter_off_cap = 0;
@@ -166,7 +173,7 @@ struct cfpq_result {
         dfree(d_T); dfree(d_snap); dfree(d_K); dfree(d_nt); dfree(d_exps); dfree(d_rules);
         dfree(d_lab_ptr); dfree(d_lab_nt); dfree(d_slot_row); dfree(d_slot_col); dfree(d_adj_cnt);
         dfree(d_adj_ptr); dfree(d_adj_cursor); dfree(d_adj_idx); dfree(d_adj_ell); dfree(d_log); dfree(d_st);
-        dfree(d_iter_off); dfree(d_jac); dfree(d_iter_time); dfree(d_phase); dfree(d_rowc); dfree(d_colc); dfree(d_temp); dfree(d_keys);
+        dfree(d_iter_off); dfree(d_jac); dfree(d_iter_time); dfree(d_phase); dfree(d_hset); dfree(d_rowc); dfree(d_colc); dfree(d_temp); dfree(d_keys);
         dfree(d_small); dfree(d_Tn); dfree(d_rowcnt); dfree(d_rowoff);
         if (dense) dense_destroy(dense);
         if (comm) nccl_comm_destroy(comm);
@@ -201,6 +208,11 @@ struct cfpq_result {
         p.profile = opts.record_times;
         p.switch_cells = switch_cells;
         p.precheck = opts.reserved[0] & 1;
+        p.hset = hashed ? d_hset : nullptr;
+        p.hmask = hashed ? hcap - 1 : 0;
+        int lg = 0;
+        while (hashed && (1ull << lg) < hcap) ++lg;
+        p.hshift = 64 - lg;
         return p;
     }
 };
@@ -332,6 +344,8 @@ static void swap_with(cfpq_result* r, Bank& b) {
     std::swap(r->n_cells, b.n_cells);
     std::swap(r->d_rowc, b.d_rowc);
     std::swap(r->d_colc, b.d_colc);
+    std::swap(r->d_hset, b.d_hset);
+    std::swap(r->hcap, b.hcap);
     std::swap(r->h_nt, b.h_nt);
     std::swap(r->Tbase, b.Tbase);
 }
@@ -351,7 +365,11 @@ static bool make_spare(cfpq_result* r) {
         return e == cudaSuccess;
     };
     cudaStream_t s = r->stream;
-    bool good = ok(cudaMalloc(&b.d_T, mw * r->n_nt * 4)) && ok(cudaMemsetAsync(b.d_T, 0, mw * r->n_nt * 4, s));
+    bool good = true;
+    if (r->hashed)
+        good = ok(cudaMalloc(&b.d_hset, r->hcap * 8)) && ok(cudaMemsetAsync(b.d_hset, 0xff, r->hcap * 8, s));
+    else
+        good = ok(cudaMalloc(&b.d_T, mw * r->n_nt * 4)) && ok(cudaMemsetAsync(b.d_T, 0, mw * r->n_nt * 4, s));
     if (good && n_snap) good = ok(cudaMalloc(&b.d_snap, mw * n_snap * 4)) && ok(cudaMemsetAsync(b.d_snap, 0, mw * n_snap * 4, s));
     if (good && n_key)
         good = ok(cudaMalloc(&b.d_K, (size_t)r->n * r->n * n_key * 8)) &&
@@ -367,13 +385,14 @@ static bool make_spare(cfpq_result* r) {
         return false;
     }
     b.log_cap = r->log_cap;
+    b.hcap = r->hashed ? r->hcap : 0;
     b.n_cells = 0;
     b.h_nt = r->h_nt;
     b.Tbase.assign(r->n_nt, nullptr);
     int snap_i = 0, key_i = 0;
     for (int A = 0; A < r->n_nt; ++A) {
         NTInfo& t = b.h_nt[A];
-        t.T = b.d_T + (size_t)A * mw;
+        t.T = b.d_T ? b.d_T + (size_t)A * mw : nullptr;
         if (t.S) t.S = b.d_snap + (size_t)(snap_i++) * mw;
         if (t.ST) t.ST = b.d_snap + (size_t)(snap_i++) * mw;
         if (t.K) t.K = b.d_K + (size_t)(key_i++) * r->n * r->n;
@@ -474,10 +493,31 @@ static cfpq_status plan(cfpq_result* r, const cfpq_grammar* g, const cfpq_graph*
         }
     }
     const size_t mat_words = (size_t)r->rows_alloc * (size_t)r->Wp;
-    if ((st = dalloc(&r->d_T, mat_words * g->n_nt, "T bit matrices")) != CFPQ_OK) return st;
-    CFPQ_CUDA_TRY(cudaMemsetAsync(r->d_T, 0, mat_words * g->n_nt * 4, r->stream));
     int n_snap = 0;
     for (int A = 0; A < g->n_nt; ++A) n_snap += need_S[A] + need_ST[A];
+    // membership structure: the hashed cell set where nothing reads rows of T (relational,
+    // sparse engine, no var x var rule), else the bit matrices
+    const bool hash_ok = o->semantics == 0 && (o->path_policy == 0 || o->path_policy == 1) && n_snap == 0 &&
+                         g->n_nt < kMaxNT;
+    if (o->cell_set == 2 && !hash_ok) {
+        set_error("cell_set = 2 (hashed) needs relational semantics, the sparse engine, |N| < 1024 and no rule "
+                  "whose two operands both change");
+        return CFPQ_E_UNSUPPORTED;
+    }
+    // auto: the bit matrices are faster where they fit (config 4: 0.40 vs 0.52 ms loop; the
+    // hashed set halves DRAM traffic but the iteration is barrier/latency-bound), so the
+    // hashed set is chosen when the matrices would take more than a quarter of free HBM
+    bool want_hash = o->cell_set == 2;
+    if (o->cell_set == 0 && hash_ok) {
+        size_t free_b = 0, total_b = 0;
+        CFPQ_CUDA_TRY(cudaMemGetInfo(&free_b, &total_b));
+        want_hash = (double)mat_words * 4.0 * g->n_nt > 0.25 * (double)free_b;
+    }
+    r->hashed = hash_ok && want_hash;
+    if (!r->hashed) {
+        if ((st = dalloc(&r->d_T, mat_words * g->n_nt, "T bit matrices")) != CFPQ_OK) return st;
+        CFPQ_CUDA_TRY(cudaMemsetAsync(r->d_T, 0, mat_words * g->n_nt * 4, r->stream));
+    }
     r->has_snapshots = n_snap > 0;
     if (n_snap) {
         if ((st = dalloc(&r->d_snap, mat_words * n_snap, "snapshots")) != CFPQ_OK) return st;
@@ -513,7 +553,7 @@ static cfpq_status plan(cfpq_result* r, const cfpq_grammar* g, const cfpq_graph*
     int snap_i = 0, key_i = 0;
     for (int A = 0; A < g->n_nt; ++A) {
         NTInfo& t = r->h_nt[A];
-        t.T = r->d_T + (size_t)A * mat_words;
+        t.T = r->d_T ? r->d_T + (size_t)A * mat_words : nullptr;
         t.S = need_S[A] ? r->d_snap + (size_t)(snap_i++) * mat_words : nullptr;
         t.ST = need_ST[A] ? r->d_snap + (size_t)(snap_i++) * mat_words : nullptr;
         t.K = (lengths && !g->is_const[A]) ? r->d_K + (size_t)(key_i++) * n * n : nullptr;
@@ -586,6 +626,21 @@ static cfpq_status plan(cfpq_result* r, const cfpq_grammar* g, const cfpq_graph*
     return CFPQ_OK;
 }
 
+// Hashed cell set capacity: a power of two >= 2 x the log capacity (load <= 1/2 while the
+// log does not overflow).  A new table starts empty.
+static cfpq_status ensure_hash(cfpq_result* r) {
+    unsigned long long want = 1ull << 10;
+    while (want < 2 * r->log_cap) want <<= 1;
+    if (r->hcap >= want) return CFPQ_OK;
+    dfree(r->d_hset);
+    r->hcap = 0;
+    cfpq_status st = dalloc(&r->d_hset, want, "hashed cell set");
+    if (st != CFPQ_OK) return st;
+    r->hcap = want;
+    CFPQ_CUDA_TRY(cudaMemsetAsync(r->d_hset, 0xff, want * 8, r->stream));
+    return CFPQ_OK;
+}
+
 // Make sure the log and adjacency arrays can hold this graph's seeds.
 static cfpq_status size_for_graph(cfpq_result* r, const cfpq_graph* d) {
     const int64_t seeds_upper = d->n_edges * (int64_t)std::max(r->max_rules_per_label, 0);
@@ -602,6 +657,10 @@ static cfpq_status size_for_graph(cfpq_result* r, const cfpq_graph* d) {
         dfree(r->d_log);
         r->d_log = nl;
         r->log_cap = want;
+    }
+    if (r->hashed) {
+        cfpq_status st = ensure_hash(r);
+        if (st != CFPQ_OK) return st;
     }
     int64_t adj_want = std::max<int64_t>(2 * seeds_upper, 1);
     if (adj_want > r->adj_idx_cap) {
@@ -620,10 +679,22 @@ static cfpq_status grow_log(cfpq_result* r, unsigned long long reached) {
     if (st != CFPQ_OK) return st;
     CFPQ_CUDA_TRY(cudaMemcpyAsync(nl, r->d_log, r->log_cap * 8, cudaMemcpyDeviceToDevice, r->stream));
     CFPQ_CUDA_TRY(cudaStreamSynchronize(r->stream));
+    const unsigned long long old_cap = r->log_cap;
     dfree(r->d_log);
     r->d_log = nl;
     r->log_cap = want;
     r->regrows++;
+    if (r->hashed) {
+        // rebuild the table from the log's valid prefix: drops the cells that were inserted
+        // but did not fit the log (the re-run of the iteration rediscovers them)
+        dfree(r->d_hset);
+        r->hcap = 0;
+        cfpq_status st2 = ensure_hash(r);
+        if (st2 != CFPQ_OK) return st2;
+        const bool async = r->opts.schedule == 2;   // async entries carry a valid flag (bit 63)
+        const unsigned long long valid = std::min<unsigned long long>(reached, old_cap);
+        CFPQ_CUDA_TRY(launch_rehash(r->params(), valid, async ? ~(1ull << 63) : ~0ull, async ? 1 : 0, r->stream));
+    }
     return CFPQ_OK;
 }
 
@@ -810,7 +881,8 @@ static cfpq_status run(cfpq_result* r, const cfpq_graph* d) {
     // the previous run's cells (bitmaps, snapshots, keys, counters) must go: O(|log|).
     // With two banks, switch to the clean bank and clear the old one on a side stream,
     // overlapped with this run; else clear inline.
-    if (r->ran && r->n_cells) {
+    const bool log_clear = !r->hashed || r->opts.account_work;   // hashed: only counters to clear
+    if (r->ran && (r->n_cells || r->hashed)) {
         if (!r->have_spare && !r->spare_failed && r->opts.path_policy < 2) {
             r->have_spare = make_spare(r);
             r->spare_failed = !r->have_spare;
@@ -825,7 +897,8 @@ static cfpq_status run(cfpq_result* r, const cfpq_graph* d) {
             EngineParams pc = r->params();                // parameters of the old bank
             const unsigned long long old_cells = r->n_cells;
             swap_with(r, r->spare);
-            CFPQ_CUDA_TRY(launch_clear_log(pc, old_cells, r->side));
+            if (log_clear) CFPQ_CUDA_TRY(launch_clear_log(pc, old_cells, r->side));
+            if (r->hashed) CFPQ_CUDA_TRY(cudaMemsetAsync(r->spare.d_hset, 0xff, r->spare.hcap * 8, r->side));
             CFPQ_CUDA_TRY(cudaEventRecord(r->spare_clean, r->side));
             r->spare.n_cells = 0;
             r->launches++;
@@ -838,9 +911,11 @@ static cfpq_status run(cfpq_result* r, const cfpq_graph* d) {
                 r->d_log = nl;
                 r->log_cap = r->spare.log_cap;
             }
+            if (r->hashed && (st = ensure_hash(r)) != CFPQ_OK) return st;
             p = r->params();
         } else {
-            CFPQ_CUDA_TRY(launch_clear_log(p, r->n_cells, s));
+            if (log_clear) CFPQ_CUDA_TRY(launch_clear_log(p, r->n_cells, s));
+            if (r->hashed) CFPQ_CUDA_TRY(cudaMemsetAsync(r->d_hset, 0xff, r->hcap * 8, s));
             r->launches++;
         }
     }
@@ -985,6 +1060,7 @@ static cfpq_status check_inputs(const cfpq_grammar* g, const cfpq_graph* d, cons
         return CFPQ_E_UNSUPPORTED;
     }
     CFPQ_CHECK_ARG(o->path_policy >= 0 && o->path_policy <= 3, "cfpq_closure: bad path_policy");
+    CFPQ_CHECK_ARG(o->cell_set >= 0 && o->cell_set <= 2, "cfpq_closure: cell_set must be 0, 1 or 2");
     return CFPQ_OK;
 }
 
@@ -1013,7 +1089,8 @@ extern "C" cfpq_status cfpq_closure_reuse(const cfpq_grammar* g, const cfpq_grap
     if (st != CFPQ_OK) return st;
     CFPQ_CHECK_ARG(d->n_nodes == r->n && g->n_nt == r->n_nt && g->n_labels == r->n_labels &&
                        g->rules.size() == r->rules.size() && o->semantics == r->opts.semantics &&
-                       o->account_work == r->opts.account_work && o->path_policy == r->opts.path_policy,
+                       o->account_work == r->opts.account_work && o->path_policy == r->opts.path_policy &&
+                       o->cell_set == r->opts.cell_set,
                    "cfpq_closure_reuse: grammar/graph/options differ from the result's plan");
     for (size_t k = 0; k < g->rules.size(); ++k)
         CFPQ_CHECK_ARG(g->rules[k].A == r->rules[k].A && g->rules[k].B == r->rules[k].B && g->rules[k].C == r->rules[k].C,
@@ -1239,6 +1316,30 @@ extern "C" cfpq_status cfpq_result_matrix(cfpq_result* r, int32_t nt, uint32_t* 
     const int64_t wn = (r->n + 31) / 32;
     CFPQ_CHECK_ARG(row_stride_words >= wn, "cfpq_result_matrix: row_stride_words < ceil(n/32)");
     if (r->n == 0) return CFPQ_OK;
+    if (r->hashed) {
+        // no bit matrices: scatter A's cells from the log
+        cudaStream_t s = r->stream;
+        uint32_t* d = dst;
+        int64_t stride = row_stride_words;
+        uint32_t* tmp = nullptr;
+        if (!dst_is_device) {
+            cfpq_status st = dalloc(&tmp, (size_t)wn * r->n, "matrix scratch");
+            if (st != CFPQ_OK) return st;
+            d = tmp;
+            stride = wn;
+        }
+        CFPQ_CUDA_TRY(cudaMemset2DAsync(d, stride * 4, 0, wn * 4, r->n, s));
+        CFPQ_CUDA_TRY(launch_log_to_bitmap(r->d_log, r->n_cells, (uint32_t)nt, d, stride, s));
+        if (tmp) {
+            cudaError_t e = cudaMemcpy2DAsync(dst, row_stride_words * 4, tmp, wn * 4, wn * 4, r->n,
+                                              cudaMemcpyDeviceToHost, s);
+            if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+            dfree(tmp);
+            CFPQ_CUDA_TRY(e);
+        }
+        CFPQ_CUDA_TRY(cudaStreamSynchronize(s));
+        return CFPQ_OK;
+    }
     const uint32_t* src = r->h_nt[nt].T;
     CFPQ_CUDA_TRY(cudaMemcpy2DAsync(dst, row_stride_words * 4, src, r->Wp * 4, wn * 4, r->n,
                                     dst_is_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, r->stream));
@@ -1271,13 +1372,14 @@ extern "C" cfpq_status cfpq_result_lengths(cfpq_result* r, int32_t nt, uint32_t*
 
 extern "C" cfpq_status cfpq_result_stats(const cfpq_result* r, int64_t* stats, int32_t n_stats) {
     CFPQ_CHECK_ARG(r && stats, "cfpq_result_stats: NULL argument");
-    int64_t v[20] = {r->iterations, (int64_t)r->n_cells, (int64_t)r->log_cap, r->regrows, r->launches,
+    int64_t v[22] = {r->iterations, (int64_t)r->n_cells, (int64_t)r->log_cap, r->regrows, r->launches,
                      r->h_st.solo_iters, (int64_t)r->h_st.candidates, (int64_t)r->h_st.expansions,
                      (int64_t)r->seed_ns, (int64_t)r->loop_ns, (int64_t)r->grid,
                      (int64_t)r->h_st.prof[0], (int64_t)r->h_st.prof[1], (int64_t)r->h_st.prof[2],
                      (int64_t)r->h_st.prof[3], (int64_t)r->h_st.prof[4], (int64_t)r->h_st.prof[5],
-                     (int64_t)r->h_st.prof[6], (int64_t)r->dense_kb, (int64_t)r->dense_mode};
-    for (int k = 0; k < n_stats && k < 20; ++k) stats[k] = v[k];
+                     (int64_t)r->h_st.prof[6], (int64_t)r->dense_kb, (int64_t)r->dense_mode,
+                     (int64_t)r->hashed, (int64_t)r->hcap};
+    for (int k = 0; k < n_stats && k < 22; ++k) stats[k] = v[k];
     return CFPQ_OK;
 }
 

@@ -31,6 +31,8 @@ constexpr int kMaxNT = 1024;
 constexpr int kNodeBits = 27;
 constexpr uint64_t kNodeMask = (1ull << kNodeBits) - 1;
 constexpr uint64_t kEmptyKey = ~0ull;
+constexpr unsigned long long kHashEmpty = ~0ull;   // no cell packs to it (hashed mode needs |N| < 1024)
+constexpr int kHashMaxProbe = 4096;                // a longer run reports overflow: the host regrows
 
 __host__ __device__ inline uint64_t pack_cell(uint32_t A, uint32_t i, uint32_t j) {
     return ((uint64_t)A << (2 * kNodeBits)) | ((uint64_t)i << kNodeBits) | (uint64_t)j;
@@ -121,6 +123,12 @@ struct EngineParams {
     int32_t profile;               // accumulate single-CTA phase cycles into EngineState::prof
     unsigned long long switch_cells;  // |Δ_k| above which the loop stops for the dense engine (0 = never)
     int32_t precheck;              // read a candidate's word before its atomicOr (hot cells)
+    // hashed cell set (relational sparse runs without var x var rules): open addressing,
+    // linear probing over 64-bit packed cells, replaces the T bit matrices as the
+    // membership structure (see engine.cu, "Hashed cell set")
+    unsigned long long* hset;      // [hmask + 1] or null (bit matrices)
+    unsigned long long hmask;
+    int32_t hshift;                // 64 - log2(hmask + 1)
     unsigned long long async_init; // asynchronous schedule: log entries < this are valid unflagged
 };
 
@@ -168,6 +176,10 @@ cudaError_t launch_adj_count(const EngineParams& p, const int32_t* slot_row, con
                              int32_t* counts, unsigned long long n_seed_upper, cudaStream_t s);
 cudaError_t launch_adj_fill(const EngineParams& p, const int32_t* slot_row, const int32_t* slot_col,
                             int32_t* cursor, int32_t* idx, unsigned long long n_seed_upper, cudaStream_t s);
+cudaError_t launch_rehash(const EngineParams& p, unsigned long long n_cells, uint64_t cell_mask, int need_flag,
+                          cudaStream_t s);
+cudaError_t launch_log_to_bitmap(const uint64_t* log, unsigned long long n_cells, uint32_t A, uint32_t* dst,
+                                 int64_t stride_words, cudaStream_t s);
 cudaError_t launch_clear_log(const EngineParams& p, unsigned long long n_cells, cudaStream_t s);
 cudaError_t launch_begin(const EngineParams& p, cudaStream_t s);
 cudaError_t launch_async(const EngineParams& p, int grid, cudaStream_t s, bool flag_seeds,

@@ -113,6 +113,92 @@ __device__ __forceinline__ bool warp_dedup(const EngineParams& p, const Sink& sk
 // Insert candidate (A,i,j) of length len into T_k; true iff the cell is new:
 // relational -> the bit flips; single-path -> the key leaves EMPTY (atomicMin on
 // (iteration<<32 | length): first write wins across iterations, min within one).
+// ------------------------------------------------------------------------------------------
+// Hashed cell set.  At config-4 scale the bit matrices are |N| x 512 MiB and every candidate
+// is a random 4-byte atomic into them: the DRAM page / TLB misses cap the whole GPU at
+// ~20 G atomics/s (scripts/tlb_probe.cu).  The cells themselves are few (2.9 M at config 4),
+// so for relational runs whose rules all have a preterminal operand (no row scans of T)
+// the set of derived cells lives in an open-addressing table of packed cells sized
+// 2x the log (~64 MiB, L2-resident: ~130 G CAS/s).  Insert = atomicCAS(EMPTY -> cell)
+// along a linear probe run; "new" iff this CAS filled the slot.  No deletions: a cell
+// rolled back at log overflow stays in the table, and the host rebuilds the table from
+// the log's valid prefix (launch_rehash) before the iteration is re-run.
+// ------------------------------------------------------------------------------------------
+__device__ __forceinline__ bool hash_insert(const EngineParams& p, uint64_t c, int* ovf,
+                                            unsigned long long max_probe = kHashMaxProbe) {
+    unsigned long long h = (c * 0x9E3779B97F4A7C15ull) >> p.hshift;
+    for (unsigned long long probe = 0; probe < max_probe; ++probe) {
+        unsigned long long old = atomicCAS(p.hset + h, kHashEmpty, (unsigned long long)c);
+        if (old == kHashEmpty) return true;
+        if (old == c) return false;
+        h = (h + 1) & p.hmask;
+    }
+    *(volatile int*)ovf = 1;   // table too full: the host grows log + table and re-runs
+    return false;
+}
+
+// need_flag: asynchronous-schedule logs mark written entries with bit 63 (kValid)
+// N inserts with their home-slot CASes issued back to back (N round trips overlap, like
+// the N independent atomicOr of the bit-matrix path); collisions (~20% at load 1/2)
+// continue probing one by one.
+template <int N>
+__device__ __forceinline__ void hash_insert_n(const EngineParams& p, const uint64_t (&c)[N], const bool (&has)[N],
+                                              bool (&fresh)[N], int* ovf) {
+    unsigned long long h[N], old[N];
+#pragma unroll
+    for (int q = 0; q < N; ++q) {
+        h[q] = (c[q] * 0x9E3779B97F4A7C15ull) >> p.hshift;
+        old[q] = has[q] ? atomicCAS(p.hset + h[q], kHashEmpty, (unsigned long long)c[q]) : (unsigned long long)c[q];
+    }
+#pragma unroll
+    for (int q = 0; q < N; ++q) {
+        fresh[q] = old[q] == kHashEmpty;
+        if (!fresh[q] && old[q] != c[q]) {
+            unsigned long long hh = h[q];
+            fresh[q] = false;
+            for (int probe = 1; probe < kHashMaxProbe; ++probe) {
+                hh = (hh + 1) & p.hmask;
+                unsigned long long o = atomicCAS(p.hset + hh, kHashEmpty, (unsigned long long)c[q]);
+                if (o == kHashEmpty) {
+                    fresh[q] = true;
+                    break;
+                }
+                if (o == c[q]) break;
+                if (probe == kHashMaxProbe - 1) *(volatile int*)ovf = 1;
+            }
+        }
+    }
+}
+
+__device__ __forceinline__ void hash_pair(const EngineParams& p, bool has0, uint64_t c0, bool has1, uint64_t c1,
+                                          bool& n0, bool& n1, int* ovf) {
+    const uint64_t c[2] = {c0, c1};
+    const bool has[2] = {has0, has1};
+    bool f[2];
+    hash_insert_n<2>(p, c, has, f, ovf);
+    n0 = f[0];
+    n1 = f[1];
+}
+
+__global__ void rehash_kernel(EngineParams p, unsigned long long n_cells, uint64_t cell_mask, int need_flag) {
+    int dummy = 0;
+    for (unsigned long long e = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; e < n_cells;
+         e += (unsigned long long)gridDim.x * blockDim.x) {
+        const uint64_t c = ldcg64(p.log + e);
+        if (need_flag && !(c >> 63)) continue;
+        hash_insert(p, c & cell_mask, &dummy, p.hmask + 1);
+    }
+}
+
+__global__ void log_to_bitmap_kernel(const uint64_t* __restrict__ log, unsigned long long n_cells, uint32_t A,
+                                     uint32_t* dst, int64_t stride) {
+    for (unsigned long long e = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; e < n_cells;
+         e += (unsigned long long)gridDim.x * blockDim.x) {
+        uint64_t c = log[e];
+        if (cell_nt(c) == A) atomicOr(dst + (size_t)cell_i(c) * stride + (cell_j(c) >> 5), 1u << (cell_j(c) & 31));
+    }
+}
+
 __device__ __forceinline__ bool try_insert(const EngineParams& p, const NTInfo* nt, const Sink& sk, bool has,
                                            uint32_t A, uint32_t i, uint32_t j, uint64_t len, long long k) {
     if (!has) return false;
@@ -126,6 +212,8 @@ __device__ __forceinline__ bool try_insert(const EngineParams& p, const NTInfo* 
         uint64_t old = atomicMin((unsigned long long*)(K + (size_t)i * (size_t)p.n + j), (unsigned long long)kv);
         return old == kEmptyKey;
     }
+    // seeding (k = 0) may probe the whole table: it holds >= 2x the seed bound, so it ends
+    if (p.hset) return hash_insert(p, pack_cell(A, i, j), sk.overflow, k == 0 ? p.hmask + 1 : kHashMaxProbe);
     uint32_t bit = 1u << (j & 31);
     uint32_t* word = nt[A].T + (size_t)i * (size_t)p.Wp + (j >> 5);
     if (p.precheck && (ldcg32(word) & bit)) return false;   // already set: no RMW on a hot word
@@ -165,7 +253,7 @@ __device__ __forceinline__ void flush(const EngineParams& p, const NTInfo* nt, c
         } else {
             if (K != nullptr) atomicExch((unsigned long long*)(K + (size_t)i * (size_t)p.n + j),
                                          (unsigned long long)kEmptyKey);
-            else atomicAnd(word, ~bit);
+            else if (!p.hset) atomicAnd(word, ~bit);
             *(volatile int*)sk.overflow = 1;
         }
     }
@@ -304,7 +392,7 @@ __global__ void clear_log_kernel(EngineParams p, unsigned long long n_cells) {
         uint64_t c = p.log[e];
         uint32_t A = cell_nt(c), i = cell_i(c), j = cell_j(c);
         const NTInfo& nt = p.nt[A];
-        nt.T[(size_t)i * p.Wp + (j >> 5)] = 0u;
+        if (nt.T) nt.T[(size_t)i * p.Wp + (j >> 5)] = 0u;
         if (nt.S) nt.S[(size_t)i * p.Wp + (j >> 5)] = 0u;
         if (nt.ST) nt.ST[(size_t)j * p.Wp + (i >> 5)] = 0u;
         if (nt.K) nt.K[(size_t)i * p.n + j] = kEmptyKey;
@@ -417,16 +505,39 @@ __device__ __forceinline__ void expand_chunk(const EngineParams& p, const NTInfo
     }
     bool d0[kPre], d1[kPre];
     uint32_t ci0[kPre], cj0[kPre], ci1[kPre], cj1[kPre];
+    if (p.hset) {
+        // hashed cell set: all 2*kPre home-slot CASes in flight together
+        uint64_t hc[2 * kPre];
+        bool hk[2 * kPre], hf[2 * kPre];
 #pragma unroll
-    for (int x = 0; x < kPre; ++x) {
-        cand_coords(efx[x], el[x].z, ci0[x], cj0[x]);
-        cand_coords(efx[x], el[x].w, ci1[x], cj1[x]);
-        uint64_t l0 = (uint64_t)len_e + 1ull, l1 = l0;
-        bool k0 = warp_dedup(p, sk, el[x].y > 0, eA[x], ci0[x], cj0[x], l0, lane);
-        bool k1 = warp_dedup(p, sk, el[x].y > 1, eA[x], ci1[x], cj1[x], l1, lane);
-        d0[x] = try_insert(p, nt, sk, k0, eA[x], ci0[x], cj0[x], l0, k);
-        d1[x] = try_insert(p, nt, sk, k1, eA[x], ci1[x], cj1[x], l1, k);
-        dcand += (unsigned long long)el[x].y;
+        for (int x = 0; x < kPre; ++x) {
+            cand_coords(efx[x], el[x].z, ci0[x], cj0[x]);
+            cand_coords(efx[x], el[x].w, ci1[x], cj1[x]);
+            uint64_t l0 = 1ull, l1 = 1ull;
+            hk[2 * x] = warp_dedup(p, sk, el[x].y > 0, eA[x], ci0[x], cj0[x], l0, lane);
+            hk[2 * x + 1] = warp_dedup(p, sk, el[x].y > 1, eA[x], ci1[x], cj1[x], l1, lane);
+            hc[2 * x] = pack_cell(eA[x], ci0[x], cj0[x]);
+            hc[2 * x + 1] = pack_cell(eA[x], ci1[x], cj1[x]);
+            dcand += (unsigned long long)el[x].y;
+        }
+        hash_insert_n<2 * kPre>(p, hc, hk, hf, sk.overflow);
+#pragma unroll
+        for (int x = 0; x < kPre; ++x) {
+            d0[x] = hf[2 * x];
+            d1[x] = hf[2 * x + 1];
+        }
+    } else {
+#pragma unroll
+        for (int x = 0; x < kPre; ++x) {
+            cand_coords(efx[x], el[x].z, ci0[x], cj0[x]);
+            cand_coords(efx[x], el[x].w, ci1[x], cj1[x]);
+            uint64_t l0 = (uint64_t)len_e + 1ull, l1 = l0;
+            bool k0 = warp_dedup(p, sk, el[x].y > 0, eA[x], ci0[x], cj0[x], l0, lane);
+            bool k1 = warp_dedup(p, sk, el[x].y > 1, eA[x], ci1[x], cj1[x], l1, lane);
+            d0[x] = try_insert(p, nt, sk, k0, eA[x], ci0[x], cj0[x], l0, k);
+            d1[x] = try_insert(p, nt, sk, k1, eA[x], ci1[x], cj1[x], l1, k);
+            dcand += (unsigned long long)el[x].y;
+        }
     }
     bool any_tail = false;
 #pragma unroll
@@ -457,8 +568,13 @@ __device__ __forceinline__ void expand_chunk(const EngineParams& p, const NTInfo
         uint64_t l0 = (uint64_t)len_e + 1ull, l1 = l0;
         bool k0 = warp_dedup(p, sk, h.y > 0, A, a0, b0, l0, lane);
         bool k1 = warp_dedup(p, sk, h.y > 1, A, a1, b1, l1, lane);
-        bool q0 = try_insert(p, nt, sk, k0, A, a0, b0, l0, k);
-        bool q1 = try_insert(p, nt, sk, k1, A, a1, b1, l1, k);
+        bool q0, q1;
+        if (p.hset) {
+            hash_pair(p, k0, pack_cell(A, a0, b0), k1, pack_cell(A, a1, b1), q0, q1, sk.overflow);
+        } else {
+            q0 = try_insert(p, nt, sk, k0, A, a0, b0, l0, k);
+            q1 = try_insert(p, nt, sk, k1, A, a1, b1, l1, k);
+        }
         dcand += (unsigned long long)h.y;
         stage(p, nt, sk, ws, lane, q0, A, a0, b0);
         stage(p, nt, sk, ws, lane, q1, A, a1, b1);
@@ -571,7 +687,7 @@ __device__ void cta_flush(const EngineParams& p, const NTInfo* nt, const Sink& s
         } else {
             if (K != nullptr) atomicExch((unsigned long long*)(K + (size_t)i * (size_t)p.n + j),
                                          (unsigned long long)kEmptyKey);
-            else atomicAnd(word, ~bit);
+            else if (!p.hset) atomicAnd(word, ~bit);
             *(volatile int*)sk.overflow = 1;
         }
     }
@@ -737,7 +853,7 @@ __device__ __forceinline__ void solo_append(const EngineParams& p, const NTInfo*
         }
     } else {
         if (K != nullptr) atomicExch((unsigned long long*)(K + (size_t)i * (size_t)p.n + j), (unsigned long long)kEmptyKey);
-        else atomicAnd(word, ~bit);
+        else if (!p.hset) atomicAnd(word, ~bit);
         so.ov[slot] = 1;
     }
 }
@@ -755,6 +871,7 @@ __device__ __forceinline__ bool solo_try(const EngineParams& p, const NTInfo* nt
                                  (unsigned long long)(((uint64_t)k << 32) | len));
         return old == kEmptyKey;
     }
+    if (p.hset) return hash_insert(p, pack_cell(A, i, j), &so.ov[slot]);
     uint32_t bit = 1u << (j & 31);
     return !(atomicOr(nt[A].T + (size_t)i * (size_t)p.Wp + (j >> 5), bit) & bit);
 }
@@ -771,7 +888,7 @@ struct WarpSoloShared {
 };
 
 __device__ __forceinline__ bool ws_try(const EngineParams& p, const NTInfo* nt, uint32_t A, uint32_t i, uint32_t j,
-                                       uint64_t len, long long k, int* lov) {
+                                       uint64_t len, long long k, int* lov, int* ovf) {
     uint64_t* K = nt[A].K;
     if (p.lengths && K != nullptr) {
         if (len > 0xffffffffull) {
@@ -782,6 +899,7 @@ __device__ __forceinline__ bool ws_try(const EngineParams& p, const NTInfo* nt, 
                                  (unsigned long long)(((uint64_t)k << 32) | len));
         return old == kEmptyKey;
     }
+    if (p.hset) return hash_insert(p, pack_cell(A, i, j), ovf);
     uint32_t bit = 1u << (j & 31);
     return !(atomicOr(nt[A].T + (size_t)i * (size_t)p.Wp + (j >> 5), bit) & bit);
 }
@@ -804,7 +922,7 @@ __device__ __forceinline__ void ws_append(const EngineParams& p, const NTInfo* n
         }
     } else {
         if (K != nullptr) atomicExch((unsigned long long*)(K + (size_t)i * (size_t)p.n + j), (unsigned long long)kEmptyKey);
-        else atomicAnd(word, ~bit);
+        else if (!p.hset) atomicAnd(word, ~bit);
         w.ov = 1;
     }
 }
@@ -838,14 +956,19 @@ __device__ void warp_solo(const EngineParams& p, const NTInfo* nt, const Expansi
                     uint32_t a0, b0, a1, b1;
                     cand_coords(fx, h.z, a0, b0);
                     cand_coords(fx, h.w, a1, b1);
-                    const bool n0 = h.y > 0 && ws_try(p, nt, A, a0, b0, len_e + 1, k, &w.lov);
-                    const bool n1 = h.y > 1 && ws_try(p, nt, A, a1, b1, len_e + 1, k, &w.lov);
+                    bool n0, n1;
+                    if (p.hset) {
+                        hash_pair(p, h.y > 0, pack_cell(A, a0, b0), h.y > 1, pack_cell(A, a1, b1), n0, n1, &w.ov);
+                    } else {
+                        n0 = h.y > 0 && ws_try(p, nt, A, a0, b0, len_e + 1, k, &w.lov, &w.ov);
+                        n1 = h.y > 1 && ws_try(p, nt, A, a1, b1, len_e + 1, k, &w.lov, &w.ov);
+                    }
                     if (n0) ws_append(p, nt, w, base, A, a0, b0);
                     if (n1) ws_append(p, nt, w, base, A, a1, b1);
                     for (int t = 2; t < h.y; ++t) {
                         uint32_t a, b;
                         cand_coords(fx, __ldg(p.adj_idx + h.x + t), a, b);
-                        if (ws_try(p, nt, A, a, b, len_e + 1, k, &w.lov)) ws_append(p, nt, w, base, A, a, b);
+                        if (ws_try(p, nt, A, a, b, len_e + 1, k, &w.lov, &w.ov)) ws_append(p, nt, w, base, A, a, b);
                     }
                 } else {
                     const bool left = ex.kind == EXP_L_VAR;
@@ -862,7 +985,7 @@ __device__ void warp_solo(const EngineParams& p, const NTInfo* nt, const Expansi
                             if (p.lengths)
                                 clen = left ? len_e + cell_len(p, nt, ex.other, cj, v) : cell_len(p, nt, ex.other, v, ci) + len_e;
                             ++dcand;
-                            if (ws_try(p, nt, (uint32_t)ex.A, oi, oj, clen, k, &w.lov))
+                            if (ws_try(p, nt, (uint32_t)ex.A, oi, oj, clen, k, &w.lov, &w.ov))
                                 ws_append(p, nt, w, base, (uint32_t)ex.A, oi, oj);
                         }
                     }
@@ -931,8 +1054,13 @@ __device__ void solo_expand(const EngineParams& p, const NTInfo* nt, const Expan
                     pacc[5] += t - t0;
                     t0 = t;
                 }
-                bool n0 = h.y > 0 && solo_try(p, nt, so, slot, A, a0, b0, len_e + 1, k);
-                bool n1 = h.y > 1 && solo_try(p, nt, so, slot, A, a1, b1, len_e + 1, k);
+                bool n0, n1;
+                if (p.hset) {
+                    hash_pair(p, h.y > 0, pack_cell(A, a0, b0), h.y > 1, pack_cell(A, a1, b1), n0, n1, &so.ov[slot]);
+                } else {
+                    n0 = h.y > 0 && solo_try(p, nt, so, slot, A, a0, b0, len_e + 1, k);
+                    n1 = h.y > 1 && solo_try(p, nt, so, slot, A, a1, b1, len_e + 1, k);
+                }
                 if (pacc) {
                     long long t = clock64() + (n0 ? 1 : 0) + (n1 ? 1 : 0);
                     pacc[6] += t - t0;
@@ -1393,6 +1521,19 @@ cudaError_t launch_adj_ell(const int32_t* ptr, const int32_t* idx, int4* ell, in
 
 cudaError_t launch_clear_log(const EngineParams& p, unsigned long long n_cells, cudaStream_t s) {
     if (n_cells) clear_log_kernel<<<grid_for((int64_t)n_cells, 256), 256, 0, s>>>(p, n_cells);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_rehash(const EngineParams& p, unsigned long long n_cells, uint64_t cell_mask, int need_flag,
+                          cudaStream_t s) {
+    if (n_cells) rehash_kernel<<<grid_for((int64_t)n_cells, 256), 256, 0, s>>>(p, n_cells, cell_mask, need_flag);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_log_to_bitmap(const uint64_t* log, unsigned long long n_cells, uint32_t A, uint32_t* dst,
+                                 int64_t stride_words, cudaStream_t s) {
+    if (n_cells)
+        log_to_bitmap_kernel<<<grid_for((int64_t)n_cells, 256), 256, 0, s>>>(log, n_cells, A, dst, stride_words);
     return cudaGetLastError();
 }
 

@@ -17,11 +17,13 @@ pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not cuda_ok(), reason="needs a
 # Worked example: per-iteration states, k = 6, R_A, lengths
 # ------------------------------------------------------------------------------------------
 
+@pytest.mark.parametrize("cell_set", [1, 2])
 @pytest.mark.parametrize("solo", [-1, 0, 1 << 30])
-def test_example_per_iteration(example_golden, solo):
+def test_example_per_iteration(example_golden, solo, cell_set):
     g = example_golden
     w = I.bind("example", I.same_generation_grammar(), 3, g["edges"], "S")
-    r, _, _ = gpu_closure(w, solo_threshold=solo)
+    r, _, _ = gpu_closure(w, solo_threshold=solo, cell_set=cell_set)
+    assert r.stats()["hashed"] == (cell_set == 2)
     assert r.iterations == g["K"] == 6
     for k in range(0, 6):
         cells = {(i, j, w.nt_names[A]) for A in range(w.n_nt) for i, j in r.pairs_at(A, k).tolist()}
@@ -114,7 +116,8 @@ def test_random_parity_200():
     for s in range(200):
         w = I.random_workload(10_000 + s)
         lengths = s % 2 == 1
-        r, _, _ = gpu_closure(w, semantics=int(lengths), account_work=True)
+        # even seeds: auto cell set (hashed where allowed) and forced bit matrices alternate
+        r, _, _ = gpu_closure(w, semantics=int(lengths), account_work=True, cell_set=1 if s % 4 == 2 else 0)
         ores = assert_parity(w, r, lengths=lengths)
         nc, jt = r.iteration_stats(work=True)
         st = ores.stats()
