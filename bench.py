@@ -12,9 +12,12 @@ line 9 on sparse operands) / closure time; ms_per_step = closure time.
   python bench.py [--gpus N] [--steps K] [--warmup W] [--workload config4|config3|config5|config2|configS]
   python bench.py --impl reference ...   # the CPU oracle as the reference arm
 
-Multi-GPU (torchrun, N>1): one process per GPU, each closes its own seeded replica
-of the workload (independent problems, no data-path collective): "scaling": "weak";
-time = max over ranks of the device-timed region.
+Multi-GPU (torchrun, N>1): one process per GPU; time = max over ranks of the
+device-timed region.  config4 and configS close ONE problem row-block sharded over the
+ranks (north_star / SURVEY §8(e): every rank derives the cells of its rows; config4
+exchanges Δ_k as index lists, configS all-gathers the dense row blocks; NCCL every
+iteration): "scaling": "strong".  config2/3/5 (and config4 with --replicas) close one
+independent seeded replica per GPU with no data-path collective: "scaling": "weak".
 """
 from __future__ import annotations
 
@@ -321,6 +324,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-supplementary", action="store_true")
     ap.add_argument("--solo", type=int, default=-1)
+    ap.add_argument("--replicas", action="store_true",
+                    help="N>1: independent replicas instead of row-block sharding (config4)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -341,9 +346,9 @@ def main():
     stream = torch.cuda.current_stream()
     dev_index = torch.cuda.current_device()
 
-    # config S shards ONE problem by row blocks over NCCL (strong scaling); the other
-    # workloads close one independent seeded problem per GPU (weak scaling, no collective)
-    sharded = args.workload == "configS" and world > 1
+    # config S / config 4 shard ONE problem by row blocks over NCCL (strong scaling); the
+    # other workloads close one independent seeded problem per GPU (weak scaling)
+    sharded = world > 1 and (args.workload == "configS" or (args.workload == "config4" and not args.replicas))
     w, desc = make_workload(args.workload, args.seed + (0 if sharded else rank))
     shard_kw = {}
     if sharded:
@@ -490,7 +495,8 @@ def main():
                 "config": {**desc, "iterations": iterations, "cells": int(cells_total),
                            "results_start_nt": int(results_start), "useful_ops_per_step": int(ops),
                            "l2": "flushed between steps (512 MiB write outside the timed events)",
-                           "parallelism": (f"row-block sharded over {world} GPUs (NCCL all-gather per iteration)"
+                           "parallelism": (f"row-block sharded over {world} GPUs (NCCL all-gather per iteration"
+                                           + (": Δ index lists)" if pol != 2 else ": dense row blocks)")
                                            if sharded else f"{world} independent replicas (seed+rank)")
                            if world > 1 else "1 GPU",
                            "engine": "dense tcgen05 int8" if pol == 2 else "sparse semi-naive persistent kernel",

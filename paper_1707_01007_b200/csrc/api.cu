@@ -149,6 +149,9 @@ struct cfpq_result {
     int32_t my_rank = 0;
     bool emulated = false;
     void* comm = nullptr;                     // ncclComm_t (world_size > 1)
+    uint64_t* d_xbuf = nullptr;               // sparse sharding: Δ exchange buffer [ranks * max count]
+    size_t xbuf_cap = 0;
+    std::vector<int64_t> shard_new;           // sparse sharding: new cells per (iteration, rank), diagnostics
     int64_t rows_alloc = 0;                   // bit-matrix rows allocated (>= n, multiple of blocks)
     int64_t block_rows = 0;                   // rows per shard block (dense engine)
     int32_t* d_rowcnt = nullptr;              // bitmap extraction scratch [n+1]
@@ -173,7 +176,7 @@ struct cfpq_result {
         dfree(d_T); dfree(d_snap); dfree(d_K); dfree(d_nt); dfree(d_exps); dfree(d_rules);
         dfree(d_lab_ptr); dfree(d_lab_nt); dfree(d_slot_row); dfree(d_slot_col); dfree(d_adj_cnt);
         dfree(d_adj_ptr); dfree(d_adj_cursor); dfree(d_adj_idx); dfree(d_adj_ell); dfree(d_log); dfree(d_st);
-        dfree(d_iter_off); dfree(d_jac); dfree(d_iter_time); dfree(d_phase); dfree(d_hset); dfree(d_rowc); dfree(d_colc); dfree(d_temp); dfree(d_keys);
+        dfree(d_iter_off); dfree(d_jac); dfree(d_iter_time); dfree(d_phase); dfree(d_hset); dfree(d_xbuf); dfree(d_rowc); dfree(d_colc); dfree(d_temp); dfree(d_keys);
         dfree(d_small); dfree(d_Tn); dfree(d_rowcnt); dfree(d_rowoff);
         if (dense) dense_destroy(dense);
         if (comm) nccl_comm_destroy(comm);
@@ -208,6 +211,8 @@ struct cfpq_result {
         p.profile = opts.record_times;
         p.switch_cells = switch_cells;
         p.precheck = opts.reserved[0] & 1;
+        p.row_lo = 0;
+        p.row_hi = (uint32_t)n;
         p.hset = hashed ? d_hset : nullptr;
         p.hmask = hashed ? hcap - 1 : 0;
         int lg = 0;
@@ -474,7 +479,7 @@ static cfpq_status plan(cfpq_result* r, const cfpq_grammar* g, const cfpq_graph*
         r->max_rules_per_label = std::max(r->max_rules_per_label, lab_ptr[x + 1] - lab_ptr[x]);
 
     cfpq_status st;
-    const bool use_nccl = o->nccl_unique_id != nullptr && o->path_policy == 2;
+    const bool use_nccl = o->nccl_unique_id != nullptr && o->path_policy != 3;
     r->n_ranks = o->world_size > 1 ? o->world_size : (o->reserved_emulate > 1 ? o->reserved_emulate : 1);
     r->emulated = !use_nccl && r->n_ranks > 1;
     r->my_rank = o->world_size > 1 ? o->rank : 0;
@@ -672,7 +677,8 @@ static cfpq_status size_for_graph(cfpq_result* r, const cfpq_graph* d) {
     return CFPQ_OK;
 }
 
-static cfpq_status grow_log(cfpq_result* r, unsigned long long reached) {
+// `valid` = entries of the log that hold cells (default: the prefix below min(reached, cap)).
+static cfpq_status grow_log(cfpq_result* r, unsigned long long reached, unsigned long long valid = ~0ull) {
     unsigned long long want = std::max<unsigned long long>(2 * r->log_cap, reached + reached / 4 + 1024);
     uint64_t* nl = nullptr;
     cfpq_status st = dalloc(&nl, want, "cell log (grow)");
@@ -692,7 +698,7 @@ static cfpq_status grow_log(cfpq_result* r, unsigned long long reached) {
         cfpq_status st2 = ensure_hash(r);
         if (st2 != CFPQ_OK) return st2;
         const bool async = r->opts.schedule == 2;   // async entries carry a valid flag (bit 63)
-        const unsigned long long valid = std::min<unsigned long long>(reached, old_cap);
+        valid = std::min<unsigned long long>(valid, std::min<unsigned long long>(reached, old_cap));
         CFPQ_CUDA_TRY(launch_rehash(r->params(), valid, async ? ~(1ull << 63) : ~0ull, async ? 1 : 0, r->stream));
     }
     return CFPQ_OK;
@@ -854,6 +860,178 @@ static cfpq_status run_async(cfpq_result* r, unsigned long long seeds_upper) {
     return CFPQ_OK;
 }
 
+// Row-block sharded sparse engine (§8(e)).  Every rank holds the whole Δ list of
+// each iteration (identical set on every rank) and derives only the cells of the rows it
+// owns: for A -> B C with C preterminal, Δ_B(i,r) gives (A,i,k) in row i; with B preterminal,
+// Δ_C(r,j) gives (A,i,j) for the rows i of B's column r (rank-filtered).  Preterminals are
+// seeded on every rank (constant after iteration 0), so no row of another rank is read.
+// Per iteration: one launch of the closure kernel limited to iteration k and the rank's rows,
+// then the exchange: all-gather of the per-rank new-cell counts and of the cells (padded to
+// the largest count), appended to every rank's log in rank order = Δ_k; Σ counts == 0 is
+// the global no-change test of Alg. 1 line 8.  Emulated ranks (one process) run
+// the shards one after another on one shared log and membership set and exchange through
+// the same padded buffer and compaction copies.
+static cfpq_status run_sharded(cfpq_result* r) {
+    cudaStream_t s = r->stream;
+    const int P = r->n_ranks;
+    CFPQ_CUDA_TRY(cudaMemcpyAsync(&r->h_st, r->d_st, sizeof(EngineState), cudaMemcpyDeviceToHost, s));
+    CFPQ_CUDA_TRY(cudaStreamSynchronize(s));
+    if (r->h_st.bad_edge) {
+        r->n_cells = std::min<unsigned long long>(r->h_st.log_size, r->log_cap);
+        set_error("graph has an edge with a node id >= n_nodes or a label id >= n_labels");
+        return CFPQ_E_INVAL;
+    }
+    unsigned long long lo = 0, hi = r->h_st.hi;   // Δ_0 = every seed (seeded on every rank)
+    r->shard_new.clear();
+    long long k = 0;
+    std::vector<int64_t> row_lo(P), row_hi(P);
+    for (int g = 0; g < P; ++g) {
+        int64_t tlo, thi, br;
+        dense_partition(r->n, P, g, &tlo, &thi, &br);
+        row_lo[g] = std::min<int64_t>(tlo * 128, r->n);
+        row_hi[g] = std::min<int64_t>(thi * 128, r->n);
+    }
+    std::vector<unsigned long long> cnt(P, 0);
+    int status = ST_RUNNING;
+    while (status == ST_RUNNING) {
+        if (k >= r->opts.max_iterations) {
+            status = ST_CAP;
+            break;
+        }
+        ++k;   // iteration k expands Δ_{k-1} = log[lo, hi)
+        unsigned long long end = hi;
+        const int g_begin = r->emulated ? 0 : r->my_rank, g_end = r->emulated ? P : r->my_rank + 1;
+        std::fill(cnt.begin(), cnt.end(), 0ull);
+        for (int g = g_begin; g < g_end; ++g) {
+            unsigned long long start = end;
+            for (;;) {
+                EngineState es{};
+                es.lo = lo;
+                es.hi = hi;
+                es.iter = k - 1;
+                es.status = ST_RUNNING;
+                es.log_size = end;
+                CFPQ_CUDA_TRY(cudaMemcpyAsync(r->d_st, &es, sizeof(EngineState), cudaMemcpyHostToDevice, s));
+                EngineParams p = r->params();
+                p.row_lo = (uint32_t)row_lo[g];
+                p.row_hi = (uint32_t)row_hi[g];
+                p.max_iter = k;                       // exactly one loop body per launch
+                CFPQ_CUDA_TRY(launch_closure(p, r->grid, s));
+                r->launches++;
+                CFPQ_CUDA_TRY(cudaMemcpyAsync(&r->h_st, r->d_st, sizeof(EngineState), cudaMemcpyDeviceToHost, s));
+                CFPQ_CUDA_TRY(cudaStreamSynchronize(s));
+                if (r->h_st.status == ST_OVERFLOW || r->h_st.overflow) {
+                    const unsigned long long old_cap = r->log_cap;
+                    cfpq_status st = grow_log(r, r->h_st.log_size);
+                    if (st != CFPQ_OK) return st;
+                    end = std::min<unsigned long long>(r->h_st.log_size, old_cap);   // keep the valid prefix
+                    continue;
+                }
+                if (r->h_st.status != ST_DONE && r->h_st.status != ST_CAP) {
+                    set_error("closure kernel stopped without finishing the iteration (status " +
+                              std::to_string(r->h_st.status) + ")");
+                    return CFPQ_E_CUDA;
+                }
+                break;
+            }
+            end = r->h_st.log_size;
+            cnt[g] = end - start;
+        }
+        // ---- exchange: counts, then the cells (padded), appended in rank order ----
+        if (r->comm) {
+            uint64_t* dc = nullptr;
+            if (r->xbuf_cap < (size_t)P) {
+                dfree(r->d_xbuf);
+                cfpq_status st = dalloc(&r->d_xbuf, (size_t)P * 64, "exchange buffer");
+                if (st != CFPQ_OK) return st;
+                r->xbuf_cap = (size_t)P * 64;
+            }
+            dc = r->d_xbuf;
+            uint64_t mine = cnt[r->my_rank];
+            CFPQ_CUDA_TRY(cudaMemcpyAsync(dc + r->my_rank, &mine, 8, cudaMemcpyHostToDevice, s));
+            std::string err;
+            if (!nccl_allgather_u64(r->comm, dc, 1, r->my_rank, s, &err)) {
+                set_error(err);
+                return CFPQ_E_NCCL;
+            }
+            std::vector<uint64_t> hc(P);
+            CFPQ_CUDA_TRY(cudaMemcpyAsync(hc.data(), dc, 8 * P, cudaMemcpyDeviceToHost, s));
+            CFPQ_CUDA_TRY(cudaStreamSynchronize(s));
+            for (int g = 0; g < P; ++g) cnt[g] = hc[g];
+        }
+        unsigned long long tot = 0, mx = 0;
+        for (int g = 0; g < P; ++g) {
+            tot += cnt[g];
+            mx = std::max<unsigned long long>(mx, cnt[g]);
+        }
+        for (int g = 0; g < P; ++g) r->shard_new.push_back((int64_t)cnt[g]);
+        if ((P > 1 || r->comm) && tot > 0) {
+            if (hi + tot + 64 > r->log_cap) {
+                cfpq_status st = grow_log(r, hi + tot + 64, end);
+                if (st != CFPQ_OK) return st;
+            }
+            if (r->xbuf_cap < (size_t)P * mx) {
+                dfree(r->d_xbuf);
+                size_t want = std::max<size_t>((size_t)P * mx, (size_t)P * 64);
+                cfpq_status st = dalloc(&r->d_xbuf, want, "exchange buffer");
+                if (st != CFPQ_OK) return st;
+                r->xbuf_cap = want;
+            }
+            // each rank's new cells into its slot of the padded buffer
+            unsigned long long off = hi;
+            for (int g = g_begin; g < g_end; ++g) {
+                if (cnt[g])
+                    CFPQ_CUDA_TRY(cudaMemcpyAsync(r->d_xbuf + (size_t)g * mx, r->d_log + off, cnt[g] * 8,
+                                                  cudaMemcpyDeviceToDevice, s));
+                off += cnt[g];
+            }
+            if (r->comm) {
+                std::string err;
+                if (!nccl_allgather_u64(r->comm, r->d_xbuf, mx, r->my_rank, s, &err)) {
+                    set_error(err);
+                    return CFPQ_E_NCCL;
+                }
+            }
+            // compaction: Δ_k = rank 0's cells, rank 1's cells, ... at log[hi, hi + tot)
+            off = hi;
+            for (int g = 0; g < P; ++g) {
+                if (cnt[g])
+                    CFPQ_CUDA_TRY(cudaMemcpyAsync(r->d_log + off, r->d_xbuf + (size_t)g * mx, cnt[g] * 8,
+                                                  cudaMemcpyDeviceToDevice, s));
+                off += cnt[g];
+            }
+        }
+        // iteration offsets of the global log
+        unsigned long long offs[2] = {hi, hi + tot};
+        if (k + 1 < r->iter_off_cap)
+            CFPQ_CUDA_TRY(cudaMemcpyAsync(r->d_iter_off + k, offs, 16, cudaMemcpyHostToDevice, s));
+        lo = hi;
+        hi = hi + tot;
+        if (tot == 0) status = ST_DONE;
+    }
+    CFPQ_CUDA_TRY(cudaEventRecord(r->ev[3], s));
+    CFPQ_CUDA_TRY(cudaStreamSynchronize(s));
+    {
+        float ms = 0;
+        CFPQ_CUDA_TRY(cudaEventElapsedTime(&ms, r->ev[0], r->ev[1]));
+        r->seed_ns = ms * 1e6;
+        CFPQ_CUDA_TRY(cudaEventElapsedTime(&ms, r->ev[1], r->ev[3]));
+        r->loop_ns = ms * 1e6;
+    }
+    r->h_st.lo = lo;
+    r->h_st.hi = hi;
+    r->h_st.iter = k;
+    r->h_st.status = status;
+    r->h_st.log_size = hi;
+    r->iterations = k;
+    r->n_cells = hi;
+    if (status == ST_CAP) {
+        set_error("max_iterations reached before the fixpoint");
+        return CFPQ_E_NOT_CONVERGED;
+    }
+    return CFPQ_OK;
+}
+
 static cfpq_status run(cfpq_result* r, const cfpq_graph* d) {
     cudaStream_t s = r->stream;
     r->launches = 0;
@@ -956,6 +1134,7 @@ static cfpq_status run(cfpq_result* r, const cfpq_graph* d) {
     CFPQ_CUDA_TRY(cudaEventRecord(r->ev[1], s));
     if (r->opts.path_policy == 2 || r->opts.path_policy == 3) return run_dense(r, 0);
     if (async) return run_async(r, seeds_upper);
+    if (r->n_ranks > 1 || r->comm) return run_sharded(r);
     // a2-a5: the fixpoint loop, device-resident
     bool first = true;
     for (;;) {
@@ -1038,10 +1217,16 @@ static cfpq_status check_inputs(const cfpq_grammar* g, const cfpq_graph* d, cons
         return CFPQ_E_UNSUPPORTED;
     }
     CFPQ_CHECK_ARG(o->world_size >= 0 && o->reserved_emulate >= 0, "cfpq_closure: bad world_size / emulate_ranks");
-    if ((o->world_size > 1 || o->reserved_emulate > 1) && o->path_policy != 2) {
-        set_error("cfpq_closure: row-block sharding is implemented for the dense engine (path_policy 2); "
-                  "the sparse engine runs one problem per GPU");
-        return CFPQ_E_UNSUPPORTED;
+    if ((o->world_size > 1 || o->reserved_emulate > 1) && (o->path_policy == 0 || o->path_policy == 1)) {
+        // sparse-engine sharding: each rank derives the cells of its rows from the whole Δ
+        // list, so every rule needs a preterminal operand (no rows of T from other ranks)
+        bool varvar = false;
+        for (auto& rl : g->rules) varvar |= !g->is_const[rl.B] && !g->is_const[rl.C];
+        if (varvar || o->semantics != 0 || o->schedule == 2) {
+            set_error("cfpq_closure: row-block sharding of the sparse engine needs relational semantics, "
+                      "schedule 0/1 and a preterminal operand in every rule (use path_policy 2 otherwise)");
+            return CFPQ_E_UNSUPPORTED;
+        }
     }
     if (o->world_size > 1) {
         CFPQ_CHECK_ARG(o->rank >= 0 && o->rank < o->world_size, "cfpq_closure: rank out of range");

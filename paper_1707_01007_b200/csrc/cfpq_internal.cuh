@@ -129,6 +129,9 @@ struct EngineParams {
     unsigned long long* hset;      // [hmask + 1] or null (bit matrices)
     unsigned long long hmask;
     int32_t hshift;                // 64 - log2(hmask + 1)
+    // row-block sharding of the sparse engine: this launch derives only cells whose row
+    // i lies in [row_lo, row_hi) (the rows its rank owns); [0, n) when unsharded
+    uint32_t row_lo, row_hi;
     unsigned long long async_init; // asynchronous schedule: log entries < this are valid unflagged
 };
 
@@ -226,6 +229,7 @@ bool nccl_unique_id(void* out, std::string* err);
 size_t nccl_unique_id_bytes();
 void* nccl_comm_create(const void* id_bytes, int world, int rank, std::string* err);
 void nccl_comm_destroy(void* comm);
+bool nccl_allgather_u64(void* comm, uint64_t* buf, size_t count, int rank, cudaStream_t s, std::string* err);
 bool nccl_exchange_rows(void* comm, uint32_t* const* mats, int n_mats, size_t block_words, int rank,
                         unsigned long long* counter, cudaStream_t s, std::string* err);
 void dense_partition(int64_t n, int world, int rank, int64_t* tile_lo, int64_t* tile_hi, int64_t* block_rows);

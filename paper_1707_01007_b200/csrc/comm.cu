@@ -106,6 +106,17 @@ bool nccl_exchange_rows(void* comm, uint32_t* const* mats, int n_mats, size_t bl
     return true;
 }
 
+// In-place all-gather of `count` uint64 per rank: buf[rank*count, +count) -> every rank's
+// buf[0, world*count).  Used by the sparse engine's Δ exchange (counts, then cells).
+bool nccl_allgather_u64(void* comm, uint64_t* buf, size_t count, int rank, cudaStream_t s, std::string* err) {
+    ncclResult_t r = g_nccl.AllGather(buf + (size_t)rank * count, buf, count, ncclUint64, (ncclComm_t)comm, s);
+    if (r != ncclSuccess) {
+        if (err) *err = std::string("NCCL all-gather: ") + g_nccl.GetErrorString(r);
+        return false;
+    }
+    return true;
+}
+
 // Row-block partition of the dense engine: tiles of 128 rows, equal blocks of
 // ceil(tiles/world) tiles (the last ranks may own fewer or none).
 void dense_partition(int64_t n, int world, int rank, int64_t* tile_lo, int64_t* tile_hi, int64_t* block_rows) {

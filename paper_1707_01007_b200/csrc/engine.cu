@@ -148,7 +148,8 @@ __device__ __forceinline__ void hash_insert_n(const EngineParams& p, const uint6
 #pragma unroll
     for (int q = 0; q < N; ++q) {
         h[q] = (c[q] * 0x9E3779B97F4A7C15ull) >> p.hshift;
-        old[q] = has[q] ? atomicCAS(p.hset + h[q], kHashEmpty, (unsigned long long)c[q]) : (unsigned long long)c[q];
+        const bool own = cell_i(c[q]) >= p.row_lo && cell_i(c[q]) < p.row_hi;
+        old[q] = has[q] && own ? atomicCAS(p.hset + h[q], kHashEmpty, (unsigned long long)c[q]) : (unsigned long long)c[q];
     }
 #pragma unroll
     for (int q = 0; q < N; ++q) {
@@ -201,7 +202,7 @@ __global__ void log_to_bitmap_kernel(const uint64_t* __restrict__ log, unsigned 
 
 __device__ __forceinline__ bool try_insert(const EngineParams& p, const NTInfo* nt, const Sink& sk, bool has,
                                            uint32_t A, uint32_t i, uint32_t j, uint64_t len, long long k) {
-    if (!has) return false;
+    if (!has || i < p.row_lo || i >= p.row_hi) return false;   // rows owned by this shard only
     uint64_t* K = nt[A].K;
     if (p.lengths && K != nullptr) {
         if (len > 0xffffffffull) {
@@ -861,6 +862,7 @@ __device__ __forceinline__ void solo_append(const EngineParams& p, const NTInfo*
 // Issue the bit/key atomic of a candidate; returns whether the cell is new.
 __device__ __forceinline__ bool solo_try(const EngineParams& p, const NTInfo* nt, SoloShared& so, int slot, uint32_t A,
                                          uint32_t i, uint32_t j, uint64_t len, long long k) {
+    if (i < p.row_lo || i >= p.row_hi) return false;
     uint64_t* K = nt[A].K;
     if (p.lengths && K != nullptr) {
         if (len > 0xffffffffull) {
@@ -889,6 +891,7 @@ struct WarpSoloShared {
 
 __device__ __forceinline__ bool ws_try(const EngineParams& p, const NTInfo* nt, uint32_t A, uint32_t i, uint32_t j,
                                        uint64_t len, long long k, int* lov, int* ovf) {
+    if (i < p.row_lo || i >= p.row_hi) return false;
     uint64_t* K = nt[A].K;
     if (p.lengths && K != nullptr) {
         if (len > 0xffffffffull) {
