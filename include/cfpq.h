@@ -181,6 +181,19 @@ CFPQ_API cfpq_status cfpq_result_matrix(cfpq_result* r, int32_t nt, uint32_t* ds
 CFPQ_API cfpq_status cfpq_result_lengths(cfpq_result* r, int32_t nt, uint32_t* dst_len, int64_t capacity,
                                 int32_t dst_is_device, int64_t* written);
 
+/* Single-path witness ("a path can be found by a simple search"), rebuilt on
+ * the GPU from the recorded lengths (semantics = 1 only): out_edges[3*t .. 3*t+2] =
+ * (src, label, dst) of the t-th edge of a path i -> j of exactly *written = l_A(i,j) edges
+ * whose word A derives.  Split choice: the first binary rule A -> B C in (B, C) ascending
+ * order (rules are kept deduplicated and sorted, "P is a set") and the
+ * smallest node r with l_B(i,r) + l_C(r,j) = l; a length-1 cell takes the lowest-index edge
+ * (i, x, j) with A -> x.  d = the graph of the closure (its edges).  CFPQ_E_INVAL if (A,i,j)
+ * is not in R_A or capacity < l (*written still holds l for a second call).  dst on host
+ * or device. */
+CFPQ_API cfpq_status cfpq_result_witness(cfpq_result* r, const cfpq_graph* d, int32_t nt, int32_t i, int32_t j,
+                                         int32_t* out_edges, int64_t capacity, int32_t dst_is_device,
+                                         int64_t* written);
+
 /* Diagnostics (all optional):
  *   stats[0] iterations, [1] total derived cells incl. seeds, [2] log capacity used,
  *   [3] overflow regrows, [4] kernel launches of the last closure, [5] iterations run

@@ -29,7 +29,7 @@ EXPORTS = [
     "cfpq_result_destroy", "cfpq_result_iterations", "cfpq_result_count", "cfpq_result_count_at",
     "cfpq_result_pairs", "cfpq_result_pairs_at", "cfpq_result_matrix", "cfpq_result_lengths",
     "cfpq_result_stats", "cfpq_result_iteration_stats", "cfpq_result_iteration_stats2",
-    "cfpq_result_iteration_phases", "cfpq_last_error",
+    "cfpq_result_iteration_phases", "cfpq_result_witness", "cfpq_last_error",
     "cfpq_version", "cfpq_nccl_unique_id", "cfpq_shard_rows",
 ]
 
@@ -86,6 +86,7 @@ def load() -> ctypes.CDLL:
         "cfpq_result_iteration_stats": (i32, [vp, vp, vp, i64]),
         "cfpq_result_iteration_stats2": (i32, [vp, vp, vp, vp, i64]),
         "cfpq_result_iteration_phases": (i32, [vp, vp, i64]),
+        "cfpq_result_witness": (i32, [vp, vp, i32, i32, i32, vp, i64, i32, P(i64)]),
         "cfpq_last_error": (ctypes.c_char_p, []),
         "cfpq_version": (ctypes.c_char_p, []),
         "cfpq_nccl_unique_id": (i32, [vp, i64]),
@@ -316,6 +317,18 @@ class Result:
         t = np.zeros(k, dtype=np.int64)
         _check(load().cfpq_result_iteration_stats2(self._h, None, None, _ptr(t), k), "cfpq_result_iteration_stats2")
         return t
+
+    def witness(self, graph: "Graph", A: int, i: int, j: int) -> np.ndarray:
+        """cfpq_result_witness: int32 [l, 3] edges (src, label, dst) of a path i -> j of the
+        recorded single-path length l whose word A derives (semantics=1 runs)."""
+        n = ctypes.c_int64(0)
+        st = load().cfpq_result_witness(self._h, graph._h, int(A), int(i), int(j), None, 0, 0, ctypes.byref(n))
+        if n.value <= 0:
+            _check(st, "cfpq_result_witness")
+        out = np.zeros((n.value, 3), dtype=np.int32)
+        _check(load().cfpq_result_witness(self._h, graph._h, int(A), int(i), int(j), _ptr(out), n.value, 0,
+                                          ctypes.byref(n)), "cfpq_result_witness")
+        return out
 
     def iteration_phases(self) -> np.ndarray:
         """[k, 4] SM cycles per grid-wide iteration: expand, CTA flush, barrier (last

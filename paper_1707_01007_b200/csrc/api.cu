@@ -1616,6 +1616,102 @@ extern "C" cfpq_status cfpq_result_iteration_stats2(cfpq_result* r, int64_t* new
     return CFPQ_OK;
 }
 
+// Single-path witness on the GPU (witness.cu): the path of the recorded length of (A,i,j).
+extern "C" cfpq_status cfpq_result_witness(cfpq_result* r, const cfpq_graph* d, int32_t nt, int32_t i, int32_t j,
+                                           int32_t* out_edges, int64_t capacity, int32_t dst_is_device,
+                                           int64_t* written) {
+    CFPQ_CHECK_ARG(r && d && written, "cfpq_result_witness: NULL argument");
+    CFPQ_CHECK_ARG(r->opts.semantics == 1, "cfpq_result_witness: the closure ran with relational semantics");
+    CFPQ_CHECK_ARG(nt >= 0 && nt < r->n_nt, "cfpq_result_witness: NT id out of range");
+    CFPQ_CHECK_ARG(i >= 0 && i < r->n && j >= 0 && j < r->n, "cfpq_result_witness: node out of range");
+    CFPQ_CHECK_ARG(d->n_nodes == r->n, "cfpq_result_witness: graph differs from the result's");
+    cudaStream_t s = r->stream;
+    // the recorded length of (A,i,j)
+    uint64_t len = 0;
+    const NTInfo& t = r->h_nt[nt];
+    if (t.K) {
+        uint64_t v = 0;
+        CFPQ_CUDA_TRY(cudaMemcpyAsync(&v, t.K + (size_t)i * r->n + j, 8, cudaMemcpyDeviceToHost, s));
+        CFPQ_CUDA_TRY(cudaStreamSynchronize(s));
+        len = v == kEmptyKey ? 0 : (v & 0xffffffffull);
+    } else {
+        uint32_t w = 0;
+        CFPQ_CUDA_TRY(cudaMemcpyAsync(&w, t.T + (size_t)i * r->Wp + (j >> 5), 4, cudaMemcpyDeviceToHost, s));
+        CFPQ_CUDA_TRY(cudaStreamSynchronize(s));
+        len = (w >> (j & 31)) & 1u;
+    }
+    *written = (int64_t)len;
+    if (len == 0) {
+        set_error("cfpq_result_witness: (A, i, j) is not in R_A");
+        return CFPQ_E_INVAL;
+    }
+    CFPQ_CHECK_ARG((int64_t)len <= capacity, "cfpq_result_witness: capacity < path length");
+    CFPQ_CHECK_ARG(out_edges != nullptr, "cfpq_result_witness: out_edges is NULL");
+    // binary rules grouped by LHS (grammar order inside a group)
+    std::vector<int32_t> rule_ptr(r->n_nt + 1, 0), rule_ids(r->rules.size());
+    for (auto& rl : r->rules) rule_ptr[rl.A + 1]++;
+    for (int A = 0; A < r->n_nt; ++A) rule_ptr[A + 1] += rule_ptr[A];
+    {
+        std::vector<int32_t> cur(rule_ptr.begin(), rule_ptr.end() - 1);
+        for (size_t q = 0; q < r->rules.size(); ++q) rule_ids[cur[r->rules[q].A]++] = (int32_t)q;
+    }
+    const int64_t n = r->n;
+    int32_t *d_rp = nullptr, *d_ri = nullptr, *d_deg = nullptr, *d_ptr = nullptr, *d_cur = nullptr, *d_idx = nullptr;
+    int32_t* d_out = nullptr;
+    uint8_t* d_stack = nullptr;
+    long long* d_res = nullptr;
+    void* d_tmp = nullptr;
+    size_t tb = 0;
+    cfpq_status st = CFPQ_OK;
+    auto cleanup = [&]() {
+        dfree(d_rp); dfree(d_ri); dfree(d_deg); dfree(d_ptr); dfree(d_cur); dfree(d_idx); dfree(d_stack);
+        dfree(d_res);
+        if (!dst_is_device) dfree(d_out);
+        if (d_tmp) cudaFree(d_tmp);
+    };
+    const int64_t stack_cap = (int64_t)len + 2;
+    if ((st = dalloc(&d_rp, rule_ptr.size(), "witness rules")) != CFPQ_OK ||
+        (st = dalloc(&d_ri, std::max<size_t>(rule_ids.size(), 1), "witness rules")) != CFPQ_OK ||
+        (st = dalloc(&d_deg, (size_t)n + 1, "witness edge CSR")) != CFPQ_OK ||
+        (st = dalloc(&d_ptr, (size_t)n + 1, "witness edge CSR")) != CFPQ_OK ||
+        (st = dalloc(&d_cur, (size_t)n + 1, "witness edge CSR")) != CFPQ_OK ||
+        (st = dalloc(&d_idx, (size_t)std::max<int64_t>(d->n_edges, 1), "witness edge CSR")) != CFPQ_OK ||
+        (st = dalloc(&d_stack, (size_t)stack_cap * witness_frame_bytes(), "witness stack")) != CFPQ_OK ||
+        (st = dalloc(&d_res, 1, "witness result")) != CFPQ_OK) {
+        cleanup();
+        return st;
+    }
+    if (dst_is_device) d_out = out_edges;
+    else if ((st = dalloc(&d_out, (size_t)len * 3, "witness path")) != CFPQ_OK) {
+        cleanup();
+        return st;
+    }
+    cudaError_t e = cudaMemcpyAsync(d_rp, rule_ptr.data(), rule_ptr.size() * 4, cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess && !rule_ids.empty())
+        e = cudaMemcpyAsync(d_ri, rule_ids.data(), rule_ids.size() * 4, cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess) e = launch_scan(nullptr, nullptr, n + 1, nullptr, &tb, s);
+    if (e == cudaSuccess) e = cudaMalloc(&d_tmp, std::max<size_t>(tb, 256));
+    if (e == cudaSuccess)
+        e = launch_edge_csr(d->d_edges, d->n_edges, (int32_t)n, d_deg, d_ptr, d_cur, d_idx, d_tmp, &tb, s);
+    if (e == cudaSuccess)
+        e = launch_witness(r->params(), r->d_rules, d_rp, d_ri, d_ptr, d_idx, d->d_edges, r->d_lab_ptr, r->d_lab_nt,
+                           r->n_labels, d_stack, stack_cap, (uint32_t)nt, (uint32_t)i, (uint32_t)j, (uint32_t)len, d_out,
+                           (int64_t)len, d_res, s);
+    long long res = 0;
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&res, d_res, 8, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess && !dst_is_device)
+        e = cudaMemcpyAsync(out_edges, d_out, (size_t)len * 12, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    cleanup();
+    CFPQ_CUDA_TRY(e);
+    if (res != (long long)len) {
+        set_error("cfpq_result_witness: the recorded lengths do not rebuild a derivation (code " +
+                  std::to_string(res) + ")");
+        return CFPQ_E_CUDA;
+    }
+    return CFPQ_OK;
+}
+
 extern "C" cfpq_status cfpq_result_iteration_phases(cfpq_result* r, int64_t* cycles, int64_t capacity) {
     CFPQ_CHECK_ARG(r != nullptr && cycles != nullptr, "cfpq_result_iteration_phases: NULL argument");
     CFPQ_CHECK_ARG(r->opts.record_times, "cfpq_result_iteration_phases: run with record_times = 1");

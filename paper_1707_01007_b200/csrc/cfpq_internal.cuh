@@ -206,6 +206,14 @@ cudaError_t launch_gather_lengths(const uint64_t* keys, unsigned long long n, co
                                   uint32_t* out, cudaStream_t s);
 cudaError_t launch_scan(const int32_t* in, int32_t* out, int64_t n, void* temp, size_t* temp_bytes,
                         cudaStream_t s);
+cudaError_t launch_edge_csr(const int32_t* edges, int64_t n_edges, int32_t n, int32_t* deg, int32_t* ptr,
+                            int32_t* cursor, int32_t* idx, void* temp, size_t* temp_bytes, cudaStream_t s);
+cudaError_t launch_witness(const EngineParams& p, const int32_t* rules, const int32_t* rule_ptr,
+                           const int32_t* rule_ids, const int32_t* e_ptr, const int32_t* e_idx, const int32_t* edges,
+                           const int32_t* lab_ptr, const int32_t* lab_nt, int32_t n_labels, void* stack,
+                           int64_t stack_cap, uint32_t A, uint32_t i, uint32_t j, uint32_t len, int32_t* out,
+                           int64_t out_cap, long long* result, cudaStream_t s);
+size_t witness_frame_bytes();
 cudaError_t launch_bitmap_rowcount(const uint32_t* T, int32_t n, int64_t Wp, int32_t* rowcnt,
                                    unsigned long long* total, cudaStream_t s);
 cudaError_t launch_bitmap_pairs(const uint32_t* T, int32_t n, int64_t Wp, const int32_t* rowoff, int32_t* pairs,
