@@ -80,8 +80,8 @@ CFPQ_API void cfpq_grammar_destroy(cfpq_grammar* g);
  *          else device memory of the current device.  0 <= src,dst < n_nodes.
  *   Duplicate edges collapse (E is a set); parallel edges with different labels
  *   accumulate; labels without a terminal rule seed nothing.
- *   Edge validity (ranges) is checked on the host for host input; for device input
- *   the seed kernel checks it and cfpq_closure returns CFPQ_E_INVAL.
+ *   Edge validity (ranges) is checked on the device by the seed kernel for host and
+ *   device input alike: cfpq_closure returns CFPQ_E_INVAL for an out-of-range edge.
  * cfpq_graph_set_edges replaces the edge list of an existing graph (same n_nodes),
  * reusing its device buffer when it is large enough (the host->device copy of a
  * per-query upload).

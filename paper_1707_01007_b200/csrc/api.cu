@@ -164,6 +164,12 @@ struct cfpq_result {
     bool have_spare = false, spare_failed = false;
     cudaStream_t side = nullptr;
     cudaEvent_t spare_clean = nullptr, main_done = nullptr;
+    // in-kernel clear of the other bank (closure kernel, barrier idle time)
+    bool clr_active = false;
+    const uint64_t* clr_log = nullptr;
+    unsigned long long clr_n = 0;
+    const NTInfo* clr_nt = nullptr;
+    uint32_t *clr_rowc = nullptr, *clr_colc = nullptr;
 
     ~cfpq_result() {
         if (side) cudaStreamSynchronize(side);
@@ -213,6 +219,11 @@ struct cfpq_result {
         p.precheck = opts.reserved[0] & 1;
         p.row_lo = 0;
         p.row_hi = (uint32_t)n;
+        p.clr_n = clr_active ? clr_n : 0;
+        p.clr_log = clr_log;
+        p.clr_nt = clr_nt;
+        p.clr_rowc = clr_rowc;
+        p.clr_colc = clr_colc;
         p.hset = hashed ? d_hset : nullptr;
         p.hmask = hashed ? hcap - 1 : 0;
         int lg = 0;
@@ -264,13 +275,8 @@ static cfpq_status upload_edges(cfpq_graph* g, const int32_t* edges, int64_t n_e
                                 cudaStream_t s) {
     CFPQ_CHECK_ARG(n_edges >= 0, "edges: n_edges < 0");
     CFPQ_CHECK_ARG(n_edges == 0 || edges != nullptr, "edges: NULL pointer");
-    if (!on_device) {
-        for (int64_t e = 0; e < n_edges; ++e) {
-            int64_t a = edges[3 * e], b = edges[3 * e + 2];
-            CFPQ_CHECK_ARG(a >= 0 && a < g->n_nodes && b >= 0 && b < g->n_nodes && edges[3 * e + 1] >= 0,
-                           "edges: node or label id out of range (edge " + std::to_string(e) + ")");
-        }
-    }
+    // ranges are validated on the device by the seed kernel (cfpq_closure -> CFPQ_E_INVAL),
+    // for host and device input alike: no O(|E|) host pass on the per-query upload path
     if (n_edges > g->cap_edges) {
         dfree(g->d_edges);
         int64_t cap = std::max<int64_t>(n_edges, 1);
@@ -1034,6 +1040,7 @@ static cfpq_status run_sharded(cfpq_result* r) {
 
 static cfpq_status run(cfpq_result* r, const cfpq_graph* d) {
     cudaStream_t s = r->stream;
+    r->clr_active = false;
     r->launches = 0;
     r->counts_valid = false;
     cfpq_status st = size_for_graph(r, d);
@@ -1065,7 +1072,30 @@ static cfpq_status run(cfpq_result* r, const cfpq_graph* d) {
             r->have_spare = make_spare(r);
             r->spare_failed = !r->have_spare;
         }
-        if (r->have_spare) {
+        // the persistent closure kernel clears the other bank itself (barrier idle time)
+        const bool in_kernel = !r->hashed && r->opts.schedule != 2 && r->n_ranks == 1 && !r->comm &&
+                               r->opts.path_policy < 2 && (r->opts.reserved[0] & 2) == 0;
+        if (r->have_spare && in_kernel) {
+            swap_with(r, r->spare);                       // current = clean bank
+            CFPQ_CUDA_TRY(cudaStreamWaitEvent(s, r->spare_clean, 0));   // a side-stream clear, if any
+            r->clr_active = r->spare.n_cells > 0;
+            r->clr_log = r->spare.d_log;
+            r->clr_n = r->spare.n_cells;
+            r->clr_nt = r->spare.d_nt;
+            r->clr_rowc = r->spare.d_rowc;
+            r->clr_colc = r->spare.d_colc;
+            // spare.n_cells is zeroed once the first closure launch has drained the clear
+            st = size_for_graph(r, d);
+            if (st != CFPQ_OK) return st;
+            if (r->log_cap < r->spare.log_cap) {
+                uint64_t* nl = nullptr;
+                if ((st = dalloc(&nl, r->spare.log_cap, "cell log")) != CFPQ_OK) return st;
+                dfree(r->d_log);
+                r->d_log = nl;
+                r->log_cap = r->spare.log_cap;
+            }
+            p = r->params();
+        } else if (r->have_spare) {
             swap_with(r, r->spare);                       // current = clean bank
             CFPQ_CUDA_TRY(cudaStreamWaitEvent(s, r->spare_clean, 0));   // its clear has finished
             CFPQ_CUDA_TRY(cudaEventRecord(r->main_done, s));
@@ -1145,6 +1175,10 @@ static cfpq_status run(cfpq_result* r, const cfpq_graph* d) {
         r->launches++;
         CFPQ_CUDA_TRY(cudaMemcpyAsync(&r->h_st, r->d_st, sizeof(EngineState), cudaMemcpyDeviceToHost, s));
         CFPQ_CUDA_TRY(cudaStreamSynchronize(s));
+        if (r->clr_active && r->h_st.clr_cursor >= r->clr_n) {
+            r->spare.n_cells = 0;   // the other bank was cleared inside the kernel
+            r->clr_active = false;
+        }
         {
             float ms = 0;
             if (first) {
@@ -1380,6 +1414,14 @@ extern "C" cfpq_status cfpq_result_count_at(cfpq_result* r, int32_t nt, int64_t 
 }
 
 // sorted (i<<27|j) keys of NT `nt` among log[0,end) into r->d_keys; returns the count
+// Extraction keys are (i << bits) | j with bits = ceil(log2 n): the radix sort touches only
+// 2*bits key bits (4 passes at n = 65,536).
+static int key_bits(const cfpq_result* r) {
+    int bits = 1;
+    while ((1ll << bits) < r->n) ++bits;
+    return bits;
+}
+
 static cfpq_status sorted_keys(cfpq_result* r, int32_t nt, unsigned long long end, unsigned long long* count) {
     cudaStream_t s = r->stream;
     std::vector<int64_t> c;
@@ -1393,11 +1435,9 @@ static cfpq_status sorted_keys(cfpq_result* r, int32_t nt, unsigned long long en
         r->keys_cap = 2 * m + 2;
     }
     CFPQ_CUDA_TRY(cudaMemsetAsync(r->d_small + r->n_nt, 0, 8, s));
-    CFPQ_CUDA_TRY(launch_filter_nt(r->d_log, end, (uint32_t)nt, r->d_keys, r->d_small + r->n_nt, s));
+    CFPQ_CUDA_TRY(launch_filter_nt(r->d_log, end, (uint32_t)nt, r->d_keys, r->d_small + r->n_nt, key_bits(r), s));
     if (m > 1) {
-        int bits = 1;
-        while ((1ll << bits) < r->n) ++bits;
-        int end_bit = kNodeBits + bits;
+        int end_bit = 2 * key_bits(r);
         size_t need = 0;
         CFPQ_CUDA_TRY(sort_keys(r->d_keys, r->d_keys + m + 1, m, end_bit, nullptr, &need, s));
         if (need > r->temp_bytes) {
@@ -1475,7 +1515,7 @@ static cfpq_status pairs_impl(cfpq_result* r, int32_t nt, int64_t k, int32_t* ds
     cudaStream_t s = r->stream;
     // unpack into the upper half of the key scratch (2m int32 = m uint64), then copy out
     int32_t* tmp = on_dev ? dst : (int32_t*)(r->d_keys + m + 1);
-    CFPQ_CUDA_TRY(launch_unpack_pairs(r->d_keys, m, tmp, s));
+    CFPQ_CUDA_TRY(launch_unpack_pairs(r->d_keys, m, tmp, key_bits(r), s));
     if (!on_dev) {
         CFPQ_CUDA_TRY(cudaMemcpyAsync(dst, tmp, m * 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
     }
@@ -1549,7 +1589,7 @@ extern "C" cfpq_status cfpq_result_lengths(cfpq_result* r, int32_t nt, uint32_t*
     if (m == 0) return CFPQ_OK;
     cudaStream_t s = r->stream;
     uint32_t* tmp = dst_is_device ? dst_len : (uint32_t*)(r->d_keys + m + 1);
-    CFPQ_CUDA_TRY(launch_gather_lengths(r->d_keys, m, r->h_nt[nt].K, r->n, tmp, s));
+    CFPQ_CUDA_TRY(launch_gather_lengths(r->d_keys, m, r->h_nt[nt].K, r->n, tmp, key_bits(r), s));
     if (!dst_is_device) CFPQ_CUDA_TRY(cudaMemcpyAsync(dst_len, tmp, m * 4, cudaMemcpyDeviceToHost, s));
     CFPQ_CUDA_TRY(cudaStreamSynchronize(s));
     return CFPQ_OK;

@@ -90,7 +90,8 @@ struct EngineState {
     unsigned bar_gen;
     unsigned long long snap_ls[2]; // log size when iteration k closed (slot k&1)
     int snap_flags[2];             // bit 0 overflow, bit 1 length overflow (slot k&1)
-    unsigned pad1[22];
+    unsigned pad1[20];
+    unsigned long long clr_cursor; // in-kernel clear of the other bank: next cell to claim
 };
 
 enum : int { ST_RUNNING = 0, ST_DONE = 1, ST_OVERFLOW = 2, ST_CAP = 3, ST_LEN_OVERFLOW = 4, ST_SWITCH = 5 };
@@ -132,6 +133,13 @@ struct EngineParams {
     // row-block sharding of the sparse engine: this launch derives only cells whose row
     // i lies in [row_lo, row_hi) (the rows its rank owns); [0, n) when unsharded
     uint32_t row_lo, row_hi;
+    // the previous run's cells in the other workspace bank, cleared by CTAs that wait at
+    // a grid barrier (and drained at kernel end): clr_n = 0 when there is nothing to clear
+    const uint64_t* clr_log;
+    unsigned long long clr_n;
+    const NTInfo* clr_nt;
+    uint32_t* clr_rowc;
+    uint32_t* clr_colc;
     unsigned long long async_init; // asynchronous schedule: log entries < this are valid unflagged
 };
 
@@ -198,12 +206,12 @@ cudaError_t launch_closure(const EngineParams& p, int grid, cudaStream_t s);
 cudaError_t launch_nt_histogram(const uint64_t* log, unsigned long long n, unsigned long long* counts, int n_nt,
                                 cudaStream_t s);
 cudaError_t launch_filter_nt(const uint64_t* log, unsigned long long n, uint32_t A, uint64_t* keys,
-                             unsigned long long* count, cudaStream_t s);
+                             unsigned long long* count, int bits, cudaStream_t s);
 cudaError_t sort_keys(uint64_t* keys, uint64_t* keys_alt, unsigned long long n, int end_bit, void* temp,
                       size_t* temp_bytes, cudaStream_t s);
-cudaError_t launch_unpack_pairs(const uint64_t* keys, unsigned long long n, int32_t* pairs, cudaStream_t s);
+cudaError_t launch_unpack_pairs(const uint64_t* keys, unsigned long long n, int32_t* pairs, int bits, cudaStream_t s);
 cudaError_t launch_gather_lengths(const uint64_t* keys, unsigned long long n, const uint64_t* K, int64_t n_nodes,
-                                  uint32_t* out, cudaStream_t s);
+                                  uint32_t* out, int bits, cudaStream_t s);
 cudaError_t launch_scan(const int32_t* in, int32_t* out, int64_t n, void* temp, size_t* temp_bytes,
                         cudaStream_t s);
 cudaError_t launch_edge_csr(const int32_t* edges, int64_t n_edges, int32_t n, int32_t* deg, int32_t* ptr,

@@ -788,8 +788,96 @@ __device__ void publish(const EngineParams& p, const LoopState& s) {
 // Grid barrier (generation counter, release/acquire).  If k >= 0 the last CTA to
 // arrive snapshots the log size and error flags of iteration k into slot k&1 before
 // releasing, so every CTA can close the iteration locally afterwards.
+// ---- clearing the other bank's cells with otherwise idle barrier time ----
+constexpr unsigned long long kClrChunk = 2048;
+
+// Reset one claimed chunk of the previous run's cells (same work as clear_log_kernel).
+__device__ __forceinline__ void clear_chunk(const EngineParams& p, unsigned long long base) {
+    const unsigned long long end = min(base + kClrChunk, p.clr_n);
+    for (unsigned long long e = base + threadIdx.x; e < end; e += kBlock) {
+        const uint64_t c = ldcg64(p.clr_log + e);
+        const uint32_t A = cell_nt(c), i = cell_i(c), j = cell_j(c);
+        const NTInfo& t = p.clr_nt[A];
+        if (t.T) t.T[(size_t)i * p.Wp + (j >> 5)] = 0u;
+        if (t.S) t.S[(size_t)i * p.Wp + (j >> 5)] = 0u;
+        if (t.ST) t.ST[(size_t)j * p.Wp + (i >> 5)] = 0u;
+        if (t.K) t.K[(size_t)i * p.n + j] = kEmptyKey;
+        if (p.clr_rowc) {
+            p.clr_rowc[(size_t)A * p.n + i] = 0u;
+            p.clr_colc[(size_t)A * p.n + j] = 0u;
+        }
+    }
+}
+
+// Whole CTA: claim and clear chunks until none is left (kernel end).
+__device__ void clear_drain(const EngineParams& p) {
+    __shared__ unsigned long long s_base;
+    if (p.clr_n == 0) return;
+    for (;;) {
+        __syncthreads();
+        if (threadIdx.x == 0) s_base = atomicAdd(&p.st->clr_cursor, kClrChunk);
+        __syncthreads();
+        if (s_base >= p.clr_n) break;
+        clear_chunk(p, s_base);
+    }
+}
+
 __device__ bool grid_barrier(const EngineParams& p, long long k) {
     __shared__ int s_timeout;
+    if (p.clr_n) {
+        // CTAs that are not the last to arrive clear chunks of the other bank while they
+        // wait; the release is checked between chunks
+        __shared__ int s_go;
+        __shared__ unsigned s_my;
+        __shared__ unsigned long long s_base;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            s_timeout = 0;
+            s_go = 0;
+            EngineState* st = p.st;
+            s_my = *(volatile unsigned*)&st->bar_gen;
+            unsigned arrived = atom_add_acq_rel(&st->bar_count, 1u);
+            if (arrived == (unsigned)p.nblocks - 1u) {
+                if (k >= 0) {
+                    int f = (*(volatile int*)&st->overflow ? 1 : 0) | (*(volatile int*)&st->len_overflow ? 2 : 0);
+                    st->snap_ls[k & 1] = ld_volatile_u64(&st->log_size);
+                    st->snap_flags[k & 1] = f;
+                }
+                st->bar_count = 0u;
+                red_add_release(&st->bar_gen, 1u);
+                s_go = 1;
+            }
+        }
+        __syncthreads();
+        while (!s_go) {
+            if (threadIdx.x == 0)
+                s_base = ld_volatile_u64(&p.st->clr_cursor) < p.clr_n ? atomicAdd(&p.st->clr_cursor, kClrChunk)
+                                                                       : ~0ull;
+            __syncthreads();
+            const bool work = s_base < p.clr_n;
+            if (work) clear_chunk(p, s_base);
+            if (threadIdx.x == 0) {
+                if (ld_acquire_u32(&p.st->bar_gen) != s_my) {
+                    s_go = 1;
+                } else if (!work) {
+                    // nothing left to clear: plain wait
+                    long long t0 = clock64();
+                    unsigned ns = 0;
+                    while (ld_acquire_u32(&p.st->bar_gen) == s_my) {
+                        if (ns) __nanosleep(ns);
+                        if (clock64() - t0 > 40000) ns = ns ? (ns < 2048u ? ns * 2u : 2048u) : 64u;
+                        if (clock64() - t0 > 60000000000ll) {
+                            s_timeout = 1;
+                            break;
+                        }
+                    }
+                    s_go = 1;
+                }
+            }
+            __syncthreads();
+        }
+        return s_timeout == 0;
+    }
     __syncthreads();
     if (threadIdx.x == 0) {
         s_timeout = 0;
@@ -1332,6 +1420,7 @@ __global__ void __launch_bounds__(kBlock, 1) closure_kernel(EngineParams p) {
         }
     }
     if (!aborted && blockIdx.x == 0 && threadIdx.x == 0) publish(p, s);
+    if (!aborted) clear_drain(p);   // the other bank is clean when this launch ends
     // diagnostics: one atomic per warp per launch
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {

@@ -22,34 +22,42 @@ __global__ void nt_histogram_kernel(const uint64_t* __restrict__ log, unsigned l
         if (hist[t]) atomicAdd(counts + t, (unsigned long long)hist[t]);
 }
 
+// A's cells as compact keys (i << bits) | j (bits = ceil(log2 n)), so the radix sort runs
+// over 2*bits key bits only; one atomic per warp (warp-aggregated append).
 __global__ void filter_nt_kernel(const uint64_t* __restrict__ log, unsigned long long n, uint32_t A,
-                                 uint64_t* keys, unsigned long long* count) {
-    for (unsigned long long e = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; e < n;
-         e += (unsigned long long)gridDim.x * blockDim.x) {
-        uint64_t c = __ldg((const unsigned long long*)log + e);
-        if (cell_nt(c) == A) {
-            unsigned long long at = atomicAdd(count, 1ull);
-            keys[at] = c & ((1ull << (2 * kNodeBits)) - 1ull);   // (i << 27) | j
-        }
+                                 uint64_t* keys, unsigned long long* count, int bits) {
+    const int lane = threadIdx.x & 31;
+    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+    for (unsigned long long base = blockIdx.x * (unsigned long long)blockDim.x; base < n; base += stride) {
+        const unsigned long long e = base + threadIdx.x;
+        uint64_t c = e < n ? __ldg((const unsigned long long*)log + e) : ~0ull;
+        const bool hit = e < n && cell_nt(c) == A;
+        const unsigned mask = __ballot_sync(0xffffffffu, hit);
+        if (!mask) continue;
+        unsigned long long at = 0;
+        if (lane == 0) at = atomicAdd(count, (unsigned long long)__popc(mask));
+        at = __shfl_sync(0xffffffffu, at, 0);
+        if (hit) keys[at + __popc(mask & ((1u << lane) - 1u))] = ((uint64_t)cell_i(c) << bits) | cell_j(c);
     }
 }
 
-__global__ void unpack_pairs_kernel(const uint64_t* __restrict__ keys, unsigned long long n, int32_t* pairs) {
+__global__ void unpack_pairs_kernel(const uint64_t* __restrict__ keys, unsigned long long n, int32_t* pairs,
+                                    int bits) {
     for (unsigned long long e = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; e < n;
          e += (unsigned long long)gridDim.x * blockDim.x) {
         uint64_t k = keys[e];
-        pairs[2 * e] = (int32_t)cell_i(k);
-        pairs[2 * e + 1] = (int32_t)cell_j(k);
+        pairs[2 * e] = (int32_t)(k >> bits);
+        pairs[2 * e + 1] = (int32_t)(k & ((1ull << bits) - 1ull));
     }
 }
 
 __global__ void gather_lengths_kernel(const uint64_t* __restrict__ keys, unsigned long long n,
-                                      const uint64_t* __restrict__ K, int64_t n_nodes, uint32_t* out) {
+                                      const uint64_t* __restrict__ K, int64_t n_nodes, uint32_t* out, int bits) {
     for (unsigned long long e = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; e < n;
          e += (unsigned long long)gridDim.x * blockDim.x) {
         uint64_t k = keys[e];
         uint32_t l = 1;   // preterminal cells: length 1 (P:393 seed)
-        if (K) l = (uint32_t)(K[(size_t)cell_i(k) * (size_t)n_nodes + cell_j(k)] & 0xffffffffull);
+        if (K) l = (uint32_t)(K[(size_t)(k >> bits) * (size_t)n_nodes + (k & ((1ull << bits) - 1ull))] & 0xffffffffull);
         out[e] = l;
     }
 }
@@ -138,8 +146,8 @@ cudaError_t launch_nt_histogram(const uint64_t* log, unsigned long long n, unsig
 }
 
 cudaError_t launch_filter_nt(const uint64_t* log, unsigned long long n, uint32_t A, uint64_t* keys,
-                             unsigned long long* count, cudaStream_t s) {
-    if (n) filter_nt_kernel<<<grid_for(n), 256, 0, s>>>(log, n, A, keys, count);
+                             unsigned long long* count, int bits, cudaStream_t s) {
+    if (n) filter_nt_kernel<<<grid_for(n), 256, 0, s>>>(log, n, A, keys, count, bits);
     return cudaGetLastError();
 }
 
@@ -154,14 +162,14 @@ cudaError_t sort_keys(uint64_t* keys, uint64_t* keys_alt, unsigned long long n, 
     return e;
 }
 
-cudaError_t launch_unpack_pairs(const uint64_t* keys, unsigned long long n, int32_t* pairs, cudaStream_t s) {
-    if (n) unpack_pairs_kernel<<<grid_for(n), 256, 0, s>>>(keys, n, pairs);
+cudaError_t launch_unpack_pairs(const uint64_t* keys, unsigned long long n, int32_t* pairs, int bits, cudaStream_t s) {
+    if (n) unpack_pairs_kernel<<<grid_for(n), 256, 0, s>>>(keys, n, pairs, bits);
     return cudaGetLastError();
 }
 
 cudaError_t launch_gather_lengths(const uint64_t* keys, unsigned long long n, const uint64_t* K, int64_t n_nodes,
-                                  uint32_t* out, cudaStream_t s) {
-    if (n) gather_lengths_kernel<<<grid_for(n), 256, 0, s>>>(keys, n, K, n_nodes, out);
+                                  uint32_t* out, int bits, cudaStream_t s) {
+    if (n) gather_lengths_kernel<<<grid_for(n), 256, 0, s>>>(keys, n, K, n_nodes, out, bits);
     return cudaGetLastError();
 }
 

@@ -268,6 +268,26 @@ def test_bad_device_edge_rejected():
     assert ei.value.status == C.CFPQ_E_INVAL
 
 
+def test_bad_host_edge_rejected():
+    """Host edges are validated by the seed kernel too (no host pass on the upload path)."""
+    from paper_1707_01007_b200 import cfpq as C
+    w = I.example_workload()
+    g = C.Grammar.from_workload(w)
+    for bad in ([[0, 0, 1], [0, 0, 7]], [[0, 0, 1], [-1, 0, 1]], [[0, 9, 1]]):
+        d = C.Graph(3, np.array(bad, dtype=np.int32))
+        with pytest.raises(C.CfpqError) as ei:
+            C.closure(g, d)
+        assert ei.value.status == C.CFPQ_E_INVAL
+    d = C.Graph(3, w.edges)
+    r = C.closure(g, d)
+    d.set_edges(np.array([[0, 0, 1], [3, 0, 1]], dtype=np.int32))
+    with pytest.raises(C.CfpqError):
+        C.closure_reuse(g, d, r)
+    d.set_edges(w.edges)
+    C.closure_reuse(g, d, r)
+    assert_parity(w, r)
+
+
 def test_max_iterations_partial_state():
     w = I.anbn_workload(3, 5)
     ores = O.run(w, max_iterations=7)
