@@ -1422,31 +1422,40 @@ static int key_bits(const cfpq_result* r) {
     return bits;
 }
 
+static bool keys32(const cfpq_result* r) { return 2 * key_bits(r) <= 32; }
+
+// A's cells of log[0, end) as sorted compact keys in d_keys (uint32 if keys32(r)).  The
+// filter counts on the device; one read-back sizes the sort.
 static cfpq_status sorted_keys(cfpq_result* r, int32_t nt, unsigned long long end, unsigned long long* count) {
     cudaStream_t s = r->stream;
-    std::vector<int64_t> c;
-    cfpq_status st = counts_upto(r, end, c);
-    if (st != CFPQ_OK) return st;
-    unsigned long long m = (unsigned long long)c[nt];
-    if (2 * m + 2 > r->keys_cap) {
+    cfpq_status st;
+    if (2 * end + 2 > r->keys_cap) {
         dfree(r->d_keys);
-        st = dalloc(&r->d_keys, 2 * m + 2, "extraction keys");
+        st = dalloc(&r->d_keys, 2 * end + 2, "extraction keys");
         if (st != CFPQ_OK) return st;
-        r->keys_cap = 2 * m + 2;
+        r->keys_cap = 2 * end + 2;
     }
+    const int bits = key_bits(r);
+    const bool k32 = keys32(r);
     CFPQ_CUDA_TRY(cudaMemsetAsync(r->d_small + r->n_nt, 0, 8, s));
-    CFPQ_CUDA_TRY(launch_filter_nt(r->d_log, end, (uint32_t)nt, r->d_keys, r->d_small + r->n_nt, key_bits(r), s));
+    CFPQ_CUDA_TRY(launch_filter_nt(r->d_log, end, (uint32_t)nt, r->d_keys, r->d_small + r->n_nt, bits, k32, s));
+    unsigned long long m = 0;
+    CFPQ_CUDA_TRY(cudaMemcpyAsync(&m, r->d_small + r->n_nt, 8, cudaMemcpyDeviceToHost, s));
+    CFPQ_CUDA_TRY(cudaStreamSynchronize(s));
     if (m > 1) {
-        int end_bit = 2 * key_bits(r);
+        const int end_bit = 2 * bits;
         size_t need = 0;
-        CFPQ_CUDA_TRY(sort_keys(r->d_keys, r->d_keys + m + 1, m, end_bit, nullptr, &need, s));
+        uint32_t* k4 = reinterpret_cast<uint32_t*>(r->d_keys);
+        if (k32) CFPQ_CUDA_TRY(sort_keys32(k4, k4 + m, m, end_bit, nullptr, &need, s));
+        else CFPQ_CUDA_TRY(sort_keys(r->d_keys, r->d_keys + m + 1, m, end_bit, nullptr, &need, s));
         if (need > r->temp_bytes) {
             dfree(r->d_temp);
             st = dalloc((uint8_t**)&r->d_temp, need, "sort temp");
             if (st != CFPQ_OK) return st;
             r->temp_bytes = need;
         }
-        CFPQ_CUDA_TRY(sort_keys(r->d_keys, r->d_keys + m + 1, m, end_bit, r->d_temp, &r->temp_bytes, s));
+        if (k32) CFPQ_CUDA_TRY(sort_keys32(k4, k4 + m, m, end_bit, r->d_temp, &r->temp_bytes, s));
+        else CFPQ_CUDA_TRY(sort_keys(r->d_keys, r->d_keys + m + 1, m, end_bit, r->d_temp, &r->temp_bytes, s));
     }
     *count = m;
     return CFPQ_OK;
@@ -1515,7 +1524,7 @@ static cfpq_status pairs_impl(cfpq_result* r, int32_t nt, int64_t k, int32_t* ds
     cudaStream_t s = r->stream;
     // unpack into the upper half of the key scratch (2m int32 = m uint64), then copy out
     int32_t* tmp = on_dev ? dst : (int32_t*)(r->d_keys + m + 1);
-    CFPQ_CUDA_TRY(launch_unpack_pairs(r->d_keys, m, tmp, key_bits(r), s));
+    CFPQ_CUDA_TRY(launch_unpack_pairs(r->d_keys, m, tmp, key_bits(r), keys32(r), s));
     if (!on_dev) {
         CFPQ_CUDA_TRY(cudaMemcpyAsync(dst, tmp, m * 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
     }
@@ -1589,7 +1598,7 @@ extern "C" cfpq_status cfpq_result_lengths(cfpq_result* r, int32_t nt, uint32_t*
     if (m == 0) return CFPQ_OK;
     cudaStream_t s = r->stream;
     uint32_t* tmp = dst_is_device ? dst_len : (uint32_t*)(r->d_keys + m + 1);
-    CFPQ_CUDA_TRY(launch_gather_lengths(r->d_keys, m, r->h_nt[nt].K, r->n, tmp, key_bits(r), s));
+    CFPQ_CUDA_TRY(launch_gather_lengths(r->d_keys, m, r->h_nt[nt].K, r->n, tmp, key_bits(r), keys32(r), s));
     if (!dst_is_device) CFPQ_CUDA_TRY(cudaMemcpyAsync(dst_len, tmp, m * 4, cudaMemcpyDeviceToHost, s));
     CFPQ_CUDA_TRY(cudaStreamSynchronize(s));
     return CFPQ_OK;

@@ -205,13 +205,16 @@ cudaError_t launch_closure(const EngineParams& p, int grid, cudaStream_t s);
 
 cudaError_t launch_nt_histogram(const uint64_t* log, unsigned long long n, unsigned long long* counts, int n_nt,
                                 cudaStream_t s);
-cudaError_t launch_filter_nt(const uint64_t* log, unsigned long long n, uint32_t A, uint64_t* keys,
-                             unsigned long long* count, int bits, cudaStream_t s);
+cudaError_t launch_filter_nt(const uint64_t* log, unsigned long long n, uint32_t A, void* keys,
+                             unsigned long long* count, int bits, int k32, cudaStream_t s);
+cudaError_t sort_keys32(uint32_t* keys, uint32_t* keys_alt, unsigned long long n, int end_bit, void* temp,
+                        size_t* temp_bytes, cudaStream_t s);
 cudaError_t sort_keys(uint64_t* keys, uint64_t* keys_alt, unsigned long long n, int end_bit, void* temp,
                       size_t* temp_bytes, cudaStream_t s);
-cudaError_t launch_unpack_pairs(const uint64_t* keys, unsigned long long n, int32_t* pairs, int bits, cudaStream_t s);
-cudaError_t launch_gather_lengths(const uint64_t* keys, unsigned long long n, const uint64_t* K, int64_t n_nodes,
-                                  uint32_t* out, int bits, cudaStream_t s);
+cudaError_t launch_unpack_pairs(const void* keys, unsigned long long n, int32_t* pairs, int bits, int k32,
+                                cudaStream_t s);
+cudaError_t launch_gather_lengths(const void* keys, unsigned long long n, const uint64_t* K, int64_t n_nodes,
+                                  uint32_t* out, int bits, int k32, cudaStream_t s);
 cudaError_t launch_scan(const int32_t* in, int32_t* out, int64_t n, void* temp, size_t* temp_bytes,
                         cudaStream_t s);
 cudaError_t launch_edge_csr(const int32_t* edges, int64_t n_edges, int32_t n, int32_t* deg, int32_t* ptr,

@@ -23,39 +23,73 @@ __global__ void nt_histogram_kernel(const uint64_t* __restrict__ log, unsigned l
 }
 
 // A's cells as compact keys (i << bits) | j (bits = ceil(log2 n)), so the radix sort runs
-// over 2*bits key bits only; one atomic per warp (warp-aggregated append).
-__global__ void filter_nt_kernel(const uint64_t* __restrict__ log, unsigned long long n, uint32_t A,
-                                 uint64_t* keys, unsigned long long* count, int bits) {
-    const int lane = threadIdx.x & 31;
-    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
-    for (unsigned long long base = blockIdx.x * (unsigned long long)blockDim.x; base < n; base += stride) {
-        const unsigned long long e = base + threadIdx.x;
-        uint64_t c = e < n ? __ldg((const unsigned long long*)log + e) : ~0ull;
-        const bool hit = e < n && cell_nt(c) == A;
-        const unsigned mask = __ballot_sync(0xffffffffu, hit);
-        if (!mask) continue;
-        unsigned long long at = 0;
-        if (lane == 0) at = atomicAdd(count, (unsigned long long)__popc(mask));
-        at = __shfl_sync(0xffffffffu, at, 0);
-        if (hit) keys[at + __popc(mask & ((1u << lane) - 1u))] = ((uint64_t)cell_i(c) << bits) | cell_j(c);
+// over 2*bits key bits only; uint32 keys when 2*bits <= 32.  Each block filters a tile of
+// kFilterTile entries and appends its hits with ONE atomic (same-address atomics per warp
+// would serialise on the counter).
+constexpr int kFilterThreads = 256, kFilterPer = 8, kFilterTile = kFilterThreads * kFilterPer;
+
+__global__ void __launch_bounds__(kFilterThreads) filter_nt_kernel(const uint64_t* __restrict__ log,
+                                                                   unsigned long long n, uint32_t A, void* keys,
+                                                                   unsigned long long* count, int bits, int k32) {
+    __shared__ int wcnt[kFilterThreads / 32];
+    __shared__ unsigned long long s_base;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (unsigned long long tile = (unsigned long long)blockIdx.x * kFilterTile; tile < n;
+         tile += (unsigned long long)gridDim.x * kFilterTile) {
+        uint64_t c[kFilterPer];
+        unsigned hitm = 0;
+#pragma unroll
+        for (int q = 0; q < kFilterPer; ++q) {
+            const unsigned long long e = tile + (unsigned long long)q * kFilterThreads + threadIdx.x;
+            c[q] = e < n ? __ldg((const unsigned long long*)log + e) : ~0ull;
+            if (e < n && cell_nt(c[q]) == A) hitm |= 1u << q;
+        }
+        const int mine = __popc(hitm);
+        int incl = mine;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            int v = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += v;
+        }
+        if (lane == 31) wcnt[warp] = incl;
+        __syncthreads();
+        int before = 0, total = 0;
+#pragma unroll
+        for (int w = 0; w < kFilterThreads / 32; ++w) {
+            if (w < warp) before += wcnt[w];
+            total += wcnt[w];
+        }
+        if (threadIdx.x == 0) s_base = total ? atomicAdd(count, (unsigned long long)total) : 0ull;
+        __syncthreads();
+        unsigned long long at = s_base + (unsigned long long)(before + incl - mine);
+#pragma unroll
+        for (int q = 0; q < kFilterPer; ++q)
+            if (hitm & (1u << q)) {
+                const uint64_t key = ((uint64_t)cell_i(c[q]) << bits) | cell_j(c[q]);
+                if (k32) reinterpret_cast<uint32_t*>(keys)[at] = (uint32_t)key;
+                else reinterpret_cast<uint64_t*>(keys)[at] = key;
+                ++at;
+            }
+        __syncthreads();
     }
 }
 
-__global__ void unpack_pairs_kernel(const uint64_t* __restrict__ keys, unsigned long long n, int32_t* pairs,
-                                    int bits) {
+__global__ void unpack_pairs_kernel(const void* __restrict__ keys, unsigned long long n, int32_t* pairs,
+                                    int bits, int k32) {
     for (unsigned long long e = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; e < n;
          e += (unsigned long long)gridDim.x * blockDim.x) {
-        uint64_t k = keys[e];
+        uint64_t k = k32 ? (uint64_t)reinterpret_cast<const uint32_t*>(keys)[e] : reinterpret_cast<const uint64_t*>(keys)[e];
         pairs[2 * e] = (int32_t)(k >> bits);
         pairs[2 * e + 1] = (int32_t)(k & ((1ull << bits) - 1ull));
     }
 }
 
-__global__ void gather_lengths_kernel(const uint64_t* __restrict__ keys, unsigned long long n,
-                                      const uint64_t* __restrict__ K, int64_t n_nodes, uint32_t* out, int bits) {
+__global__ void gather_lengths_kernel(const void* __restrict__ keys, unsigned long long n,
+                                      const uint64_t* __restrict__ K, int64_t n_nodes, uint32_t* out, int bits,
+                                      int k32) {
     for (unsigned long long e = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; e < n;
          e += (unsigned long long)gridDim.x * blockDim.x) {
-        uint64_t k = keys[e];
+        uint64_t k = k32 ? (uint64_t)reinterpret_cast<const uint32_t*>(keys)[e] : reinterpret_cast<const uint64_t*>(keys)[e];
         uint32_t l = 1;   // preterminal cells: length 1 (P:393 seed)
         if (K) l = (uint32_t)(K[(size_t)(k >> bits) * (size_t)n_nodes + (k & ((1ull << bits) - 1ull))] & 0xffffffffull);
         out[e] = l;
@@ -145,9 +179,13 @@ cudaError_t launch_nt_histogram(const uint64_t* log, unsigned long long n, unsig
     return cudaGetLastError();
 }
 
-cudaError_t launch_filter_nt(const uint64_t* log, unsigned long long n, uint32_t A, uint64_t* keys,
-                             unsigned long long* count, int bits, cudaStream_t s) {
-    if (n) filter_nt_kernel<<<grid_for(n), 256, 0, s>>>(log, n, A, keys, count, bits);
+cudaError_t launch_filter_nt(const uint64_t* log, unsigned long long n, uint32_t A, void* keys,
+                             unsigned long long* count, int bits, int k32, cudaStream_t s) {
+    if (n) {
+        unsigned long long tiles = (n + kFilterTile - 1) / kFilterTile;
+        int g = (int)std::min<unsigned long long>(tiles, 148ull * 8);
+        filter_nt_kernel<<<g, kFilterThreads, 0, s>>>(log, n, A, keys, count, bits, k32);
+    }
     return cudaGetLastError();
 }
 
@@ -162,14 +200,25 @@ cudaError_t sort_keys(uint64_t* keys, uint64_t* keys_alt, unsigned long long n, 
     return e;
 }
 
-cudaError_t launch_unpack_pairs(const uint64_t* keys, unsigned long long n, int32_t* pairs, int bits, cudaStream_t s) {
-    if (n) unpack_pairs_kernel<<<grid_for(n), 256, 0, s>>>(keys, n, pairs, bits);
+// 32-bit variant of sort_keys (compact keys of graphs with n <= 65,536)
+cudaError_t sort_keys32(uint32_t* keys, uint32_t* keys_alt, unsigned long long n, int end_bit, void* temp,
+                        size_t* temp_bytes, cudaStream_t s) {
+    cub::DoubleBuffer<unsigned int> db(keys, keys_alt);
+    cudaError_t e = cub::DeviceRadixSort::SortKeys(temp, *temp_bytes, db, (int)n, 0, end_bit, s);
+    if (e != cudaSuccess || temp == nullptr) return e;
+    if (db.Current() != keys) e = cudaMemcpyAsync(keys, db.Current(), n * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s);
+    return e;
+}
+
+cudaError_t launch_unpack_pairs(const void* keys, unsigned long long n, int32_t* pairs, int bits, int k32,
+                                cudaStream_t s) {
+    if (n) unpack_pairs_kernel<<<grid_for(n), 256, 0, s>>>(keys, n, pairs, bits, k32);
     return cudaGetLastError();
 }
 
-cudaError_t launch_gather_lengths(const uint64_t* keys, unsigned long long n, const uint64_t* K, int64_t n_nodes,
-                                  uint32_t* out, int bits, cudaStream_t s) {
-    if (n) gather_lengths_kernel<<<grid_for(n), 256, 0, s>>>(keys, n, K, n_nodes, out, bits);
+cudaError_t launch_gather_lengths(const void* keys, unsigned long long n, const uint64_t* K, int64_t n_nodes,
+                                  uint32_t* out, int bits, int k32, cudaStream_t s) {
+    if (n) gather_lengths_kernel<<<grid_for(n), 256, 0, s>>>(keys, n, K, n_nodes, out, bits, k32);
     return cudaGetLastError();
 }
 
