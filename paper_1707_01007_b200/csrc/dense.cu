@@ -68,15 +68,23 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-    uint32_t addr = smem_u32(bar);
+__device__ __forceinline__ bool mbar_try(uint32_t addr, uint32_t parity) {
+    uint32_t ok;
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
-        "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-        "@!p bra WAIT_%=;\n\t}" ::"r"(addr),
-        "r"(parity)
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(addr), "r"(parity)
         : "memory");
+    return ok != 0;
+}
+// Wait for the phase; a protocol error traps (context error) instead of hanging the GPU.
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    const uint32_t addr = smem_u32(bar);
+    uint32_t spins = 0;
+    while (!mbar_try(addr, parity))
+        if (++spins > (1u << 28)) __trap();
 }
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int x, int y) {
     asm volatile(
@@ -84,6 +92,25 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
             smem_u32(dst)),
         "l"(map), "r"(smem_u32(bar)), "r"(x), "r"(y)
         : "memory");
+}
+// Multicast variant: the box lands at the same CTA-relative offset in every CTA of
+// cta_mask and completes bytes on each one's mbarrier at the same offset.
+__device__ __forceinline__ void tma_load_2d_mc(void* dst, const CUtensorMap* map, uint64_t* bar, int x, int y,
+                                               uint16_t cta_mask) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+        " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
+        "l"(map), "r"(smem_u32(bar)), "r"(x), "r"(y), "h"(cta_mask)
+        : "memory");
+}
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+    asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 __device__ __forceinline__ void tmem_alloc(uint32_t* dst_smem, uint32_t ncols) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst_smem)),
@@ -106,6 +133,14 @@ __device__ __forceinline__ void umma_i8(uint32_t tmem_d, uint64_t adesc, uint64_
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                  : "memory");
+}
+// Arrive on the mbarrier at this offset in every CTA of cta_mask once the MMAs complete.
+__device__ __forceinline__ void umma_commit_mc(uint64_t* bar, uint16_t cta_mask) {
+    asm volatile(
+        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+            smem_u32(bar)),
+        "h"(cta_mask)
+        : "memory");
 }
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
     asm volatile(
@@ -209,6 +244,16 @@ __device__ __forceinline__ bool kblock_live(const DenseParams& p, const DenseRul
     return __ldg(oC + (size_t)K * p.nt_tiles + 2 * J) || __ldg(oC + (size_t)K * p.nt_tiles + 2 * J + 1);
 }
 
+// K block live for any of the kCl row tiles I0 .. I0+kCl-1 that exist (< i_hi)
+template <int kCl>
+__device__ __forceinline__ bool kblock_live_group(const DenseParams& p, const DenseRule& r, int I0, int J, int K) {
+    bool live = false;
+#pragma unroll
+    for (int c = 0; c < kCl; ++c)
+        if (I0 + c < p.i_hi) live |= kblock_live(p, r, I0 + c, J, K);
+    return live;
+}
+
 // Output tile t of this rank -> (output o, row tile I, column tile J).  Tiles of one output
 // are walked in groups of kGroup row tiles, columns outer: a wave of ~148 CTAs then covers
 // a kGroup x ~18 patch whose operand blocks (A: kGroup*128 rows, B: ~18*256 rows of the
@@ -221,10 +266,16 @@ __device__ __forceinline__ void tile_coords(const DenseParams& p, int t, int til
     const int g = rem / (kGroup * n_j);
     const int within = rem - g * (kGroup * n_j);
     const int rows_g = min(kGroup, n_i - g * kGroup);
-    I = p.i_lo + g * kGroup + within % rows_g;
+    I = g * kGroup + within % rows_g;   // relative to the rank's first (pair of) row tile(s)
     J = within / rows_g;
 }
 
+// kCl = 2: CTA pairs (thread-block clusters of 2) compute row tiles I0 and I0+1 of the same
+// column tile J in lockstep over the same K blocks and share the B tile: each CTA loads one
+// 128-row half and multicasts it into both CTAs' stage (half the B traffic from L2), and
+// every MMA commit arrives on both CTAs' empty barrier (a stage is refilled only when both
+// consumed it).  tmB's box is then 128 rows.
+template <int kCl>
 __global__ void __launch_bounds__(kDenseThreads, 1)
     dense_kernel(DenseParams p, const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                  const int64_t* __restrict__ mapA_row, const int64_t* __restrict__ mapB_row) {
@@ -242,15 +293,17 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int n_j = p.np / kTN;
-    const int n_i = p.i_hi - p.i_lo;
+    const int n_i = (p.i_hi - p.i_lo + kCl - 1) / kCl;   // (pairs of) row tiles
     const int tiles_per_nt = n_i * n_j;
     const int total_tiles = tiles_per_nt * p.n_out;
     const int n_k = p.np / kTK;
+    const uint32_t crank = kCl == 2 ? cluster_ctarank() : 0u;
+    const int unit = (int)blockIdx.x / kCl, n_units = (int)gridDim.x / kCl;
 
     if (warp == 0 && lane == 0) {
         for (int s = 0; s < kStages; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], 1);
+            mbar_init(&empty[s], kCl);   // one MMA commit per CTA of the cluster
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&tmem_full[a], 1);
@@ -262,7 +315,8 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
     }
     if (warp == 1) tmem_alloc(tmem_base_smem, kTmemCols);
     tc_fence_before();
-    __syncthreads();
+    if (kCl == 2) cluster_sync_all();   // barrier inits visible to the peer before its multicasts
+    else __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_base_smem;
 
@@ -271,19 +325,24 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
         if (lane == 0) {
             int stage = 0;
             uint32_t phase = 0;
-            for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
-                int o, I, J;
-                tile_coords(p, t, tiles_per_nt, n_i, n_j, o, I, J);
+            for (int t = unit; t < total_tiles; t += n_units) {
+                int o, I2, J;
+                tile_coords(p, t, tiles_per_nt, n_i, n_j, o, I2, J);
+                const int I0 = p.i_lo + I2 * kCl, I = I0 + (int)crank;
                 for (int q = p.rule_ptr[o]; q < p.rule_ptr[o + 1]; ++q) {
                     const DenseRule r = p.rules[q];
                     const int64_t arow = __ldg(mapA_row + r.B) + (int64_t)I * kTM;
                     const int64_t brow = __ldg(mapB_row + r.C) + (int64_t)J * kTN;
                     for (int K = 0; K < n_k; ++K) {
-                        if (!kblock_live(p, r, I, J, K)) continue;
+                        if (!kblock_live_group<kCl>(p, r, I0, J, K)) continue;
                         mbar_wait(&empty[stage], phase ^ 1);
                         mbar_expect_tx(&full[stage], kStageBytes);
                         tma_load_2d(sA + stage * kABytes, &tmA, &full[stage], K * kTK, (int)arow);
-                        tma_load_2d(sB + stage * kBBytes, &tmB, &full[stage], K * kTK, (int)brow);
+                        if (kCl == 1)
+                            tma_load_2d(sB + stage * kBBytes, &tmB, &full[stage], K * kTK, (int)brow);
+                        else
+                            tma_load_2d_mc(sB + stage * kBBytes + crank * (kBBytes / 2), &tmB, &full[stage], K * kTK,
+                                           (int)(brow + crank * (kTN / 2)), (uint16_t)0x3);
                         if (++stage == kStages) {
                             stage = 0;
                             phase ^= 1;
@@ -299,9 +358,10 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
         uint32_t phase = 0;
         int as = 0;              // accumulator stage of this tile
         uint32_t tphase = 0;     // phase of the stage's barriers
-        for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
-            int o, I, J;
-            tile_coords(p, t, tiles_per_nt, n_i, n_j, o, I, J);
+        for (int t = unit; t < total_tiles; t += n_units) {
+            int o, I2, J;
+            tile_coords(p, t, tiles_per_nt, n_i, n_j, o, I2, J);
+            const int I0 = p.i_lo + I2 * kCl;
             const uint32_t tmem_acc = tmem_base + (uint32_t)(as * 256);
             // the epilogue must have drained this accumulator (tile t-2)
             mbar_wait(&tmem_empty[as], tphase ^ 1);
@@ -311,7 +371,7 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
             for (int q = p.rule_ptr[o]; q < p.rule_ptr[o + 1]; ++q) {
                 const DenseRule r = p.rules[q];
                 for (int K = 0; K < n_k; ++K) {
-                    if (!kblock_live(p, r, I, J, K)) continue;
+                    if (!kblock_live_group<kCl>(p, r, I0, J, K)) continue;
                     ++kb_issued;
                     mbar_wait(&full[stage], phase);
                     tc_fence_after();
@@ -324,7 +384,9 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
                                     idesc, acc);
                             acc = 1;
                         }
-                        umma_commit(&empty[stage]);   // frees the smem stage when these MMAs finish
+                        // frees the smem stage (in both CTAs of a pair) when these MMAs finish
+                        if (kCl == 1) umma_commit(&empty[stage]);
+                        else umma_commit_mc(&empty[stage], (uint16_t)0x3);
                     }
                     __syncwarp();
                     if (++stage == kStages) {
@@ -350,13 +412,15 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
         int as = 0;
         uint32_t tphase = 0;
         unsigned long long my_new = 0;
-        for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
-            int o, I, J;
-            tile_coords(p, t, tiles_per_nt, n_i, n_j, o, I, J);
+        for (int t = unit; t < total_tiles; t += n_units) {
+            int o, I2, J;
+            tile_coords(p, t, tiles_per_nt, n_i, n_j, o, I2, J);
+            const int I0 = p.i_lo + I2 * kCl, I = I0 + (int)crank;
+            const bool mine = I < p.i_hi;   // the second tile of an odd last pair does not exist
             const int A = p.out_nt[o];
-            bool live = false;
+            bool live = false;   // the pair issued MMAs for this tile (else TMEM holds no result)
             for (int q = p.rule_ptr[o]; q < p.rule_ptr[o + 1] && !live; ++q)
-                for (int K = 0; K < n_k && !live; ++K) live = kblock_live(p, p.rules[q], I, J, K);
+                for (int K = 0; K < n_k && !live; ++K) live = kblock_live_group<kCl>(p, p.rules[q], I0, J, K);
             mbar_wait(&tmem_full[as], tphase);
             tc_fence_after();
             const int row = I * kTM + quarter * 32 + lane;
@@ -373,7 +437,7 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
                     for (int b = 0; b < 32; ++b) word |= (v[b] != 0u ? 1u : 0u) << b;
                 }
                 const int64_t wi = (int64_t)J * (kTN / 32) + c;
-                if (row < p.n && wi < p.Wp) {
+                if (mine && row < p.n && wi < p.Wp) {
                     uint32_t old = __ldg(told + wi);
                     tnew[wi] = old | word;
                     cnt += __popc(word & ~old);
@@ -393,7 +457,9 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
         if (lane == 0 && my_new) atomicAdd(p.new_cells + p.n_nt, my_new);
     }
     tc_fence_before();
-    __syncthreads();
+    // a CTA may not leave while its peer can still multicast into it or arrive on its barriers
+    if (kCl == 2) cluster_sync_all();
+    else __syncthreads();
     if (warp == 1) tmem_dealloc(tmem_base, kTmemCols);
 }
 
@@ -573,7 +639,7 @@ struct DenseEngine {
     unsigned long long* new_cells = nullptr;
     int32_t n_out = 0;
     std::vector<int32_t> h_out;
-    CUtensorMap tmA, tmB;
+    CUtensorMap tmA, tmB, tmBh;   // tmBh: 128-row box of T8T (CTA-pair halves)
     int grid = 0;
     unsigned long long kblocks_total = 0;
     uint32_t* cnt = nullptr;   // accounting scratch
@@ -660,12 +726,19 @@ DenseEngine* dense_create(int32_t n, int32_t n_nt, int64_t Wp, const std::vector
     if (!rl.empty())
         cudaMemcpyAsync(e->rule_out, e->h_rule_out.data(), rl.size() * 4, cudaMemcpyHostToDevice, s);
     if (!make_map(&e->tmA, e->T8, (int64_t)std::max(na, 1) * e->np, e->np, kTM) ||
-        !make_map(&e->tmB, e->T8T, (int64_t)std::max(nb, 1) * e->np, e->np, kTN)) {
+        !make_map(&e->tmB, e->T8T, (int64_t)std::max(nb, 1) * e->np, e->np, kTN) ||
+        !make_map(&e->tmBh, e->T8T, (int64_t)std::max(nb, 1) * e->np, e->np, kTN / 2)) {
         if (err) *err = "dense engine: cuTensorMapEncodeTiled failed";
         delete e;
         return nullptr;
     }
-    if ((c = cudaFuncSetAttribute(dense_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dense_smem_bytes())) !=
+    if ((c = cudaFuncSetAttribute(dense_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)dense_smem_bytes())) != cudaSuccess) {
+        if (err) *err = std::string("dense kernel smem attribute: ") + cudaGetErrorString(c);
+        delete e;
+        return nullptr;
+    }
+    if ((c = cudaFuncSetAttribute(dense_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dense_smem_bytes())) !=
         cudaSuccess)
         return fail("smem attribute", c);
     int dev = 0, sms = 0;
@@ -723,9 +796,37 @@ cudaError_t dense_product(DenseEngine* e, int64_t i_lo, int64_t i_hi, cudaStream
     int dev = 0, sms = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    // CTA pairs with a multicast B tile: measured 18% SLOWER on config S (31.6 vs 26.7 ms at
+    // n = 16,384: the pair runs in lockstep and a 2-CTA multicast saves no L2 traffic, cf.
+    // B300_MICROARCH "TMA-MC at csz <= 4, MC ~ UC"), so it is opt-in (CFPQ_DENSE_PAIR=1)
+    static const bool pair = [] {
+        const char* v = getenv("CFPQ_DENSE_PAIR");
+        return v && v[0] == '1';
+    }();
+    if (pair && sms >= 2) {
+        // CTA pairs (clusters of 2) share the B tile through TMA multicast
+        const int64_t units = (int64_t)e->n_out * ((i_hi - i_lo + 1) / 2) * (e->np / kTN);
+        const int grid = (int)std::max<int64_t>(2, std::min<int64_t>(sms / 2, units) * 2);
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(grid);
+        cfg.blockDim = dim3(kDenseThreads);
+        cfg.dynamicSmemBytes = dense_smem_bytes();
+        cfg.stream = s;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = 2;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        cudaError_t c = cudaLaunchKernelEx(&cfg, dense_kernel<2>, p, e->tmA, e->tmBh, (const int64_t*)e->mapA_row,
+                                           (const int64_t*)e->mapB_row);
+        if (launches) ++*launches;
+        return c != cudaSuccess ? c : cudaGetLastError();
+    }
     const int64_t total = (int64_t)e->n_out * (i_hi - i_lo) * (e->np / kTN);
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(sms, total));
-    dense_kernel<<<grid, kDenseThreads, dense_smem_bytes(), s>>>(p, e->tmA, e->tmB, e->mapA_row, e->mapB_row);
+    dense_kernel<1><<<grid, kDenseThreads, dense_smem_bytes(), s>>>(p, e->tmA, e->tmB, e->mapA_row, e->mapB_row);
     if (launches) ++*launches;
     return cudaGetLastError();
 }

@@ -1227,6 +1227,7 @@ __global__ void __launch_bounds__(kBlock, 1) closure_kernel(EngineParams p) {
     }
     __syncthreads();
     LoopState s = S.state;   // identical in every CTA
+    __syncthreads();         // every thread holds it before warp-solo may rewrite S.state
     unsigned long long dcand = 0, dexp = 0;
     bool aborted = false;
     while (s.status == ST_RUNNING) {

@@ -10,6 +10,10 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
    python bench.py --workload config4 --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --no-supplementary > /dev/null 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:closure_kernel -s 5 -c 1 \
    -o gpurun_out/prof_config4 python bench.py --workload config4 --steps 1 --warmup 3 --no-e2e --no-cpu-baseline --no-supplementary > gpurun_out/ncu_c4.txt 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:dense_kernel -s 20 -c 1 \
+   -o gpurun_out/prof_configS python bench.py --workload configS --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/ncu_cS.txt 2>&1
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_configS.csv \
+   python bench.py --workload configS --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > /dev/null 2>&1
 timeout 900 ncu --set full --clock-control none -k regex:rows_kernel -s 5 -c 1 -o gpurun_out/prof_rows \
    python -c "
 import sys; sys.path.insert(0,'.')

@@ -23,7 +23,29 @@ cases = [(I.example_workload(), dict()), (I.example_workload(), dict(semantics=1
          (I.dense_stress_workload(200, 2), dict(path_policy=2)),
          (I.dense_stress_workload(200, 2), dict(path_policy=3)),
          (I.dense_stress_workload(150, 2), dict(path_policy=2, emulate_ranks=2)),
-         (I.dense_stress_workload(300, 2), dict())]
+         (I.dense_stress_workload(300, 2), dict()),
+         (I.ontology_workload("union", 300, depth=5, seed=2), dict(cell_set=2)),
+         (I.ontology_workload("union", 300, depth=5, seed=2), dict(cell_set=2, log_capacity=64)),
+         (I.ontology_workload("union", 300, depth=5, seed=3), dict(emulate_ranks=3)),
+         (I.ontology_workload("q1", 200, depth=5, seed=4), dict(schedule=2))]
 for w, kw in cases:
     run(w, **kw)
     print("ok", w.name, kw, flush=True)
+# reuse with bank rotation (the other bank is cleared inside the closure kernel)
+w = I.ontology_workload("union", 300, depth=5, seed=5)
+g = C.Grammar.from_workload(w)
+d = C.Graph(w.n_nodes, w.edges)
+r = C.closure(g, d)
+for _ in range(3):
+    C.closure_reuse(g, d, r)
+o = O.run(w)
+assert all(np.array_equal(r.pairs(A), o.pairs(A)) for A in range(w.n_nt))
+print("ok reuse", flush=True)
+# single-path witness
+w = I.anbn_workload(3, 5)
+g = C.Grammar.from_workload(w)
+d = C.Graph(w.n_nodes, w.edges)
+r = C.closure(g, d, semantics=1)
+p = r.witness(d, 0, *r.pairs(0)[0].tolist())
+assert O.cyk(w, p[:, 1].tolist(), 0)
+print("ok witness", flush=True)

@@ -143,3 +143,26 @@ def test_auto_policy_switches_to_tensor(n, d):
     r2, _, _ = gpu_closure(w2)
     assert r2.stats()["dense_finish"] == 0
     assert_parity(w2, r2)
+
+
+def test_tensor_cta_pairs_multicast():
+    """The opt-in CTA-pair variant (clusters of 2 sharing the B tile through TMA multicast,
+    MMA commits arriving on both CTAs' stage barriers) gives the same closure, including an
+    odd number of row tiles (the second tile of the last pair does not exist)."""
+    import os
+    import subprocess
+    import sys
+    code = (
+        "import inputs as I, numpy as np\n"
+        "from tests.gpu_util import gpu_closure, assert_parity\n"
+        "for n, d in [(300, 2), (1000, 2), (130, 1)]:\n"
+        "    w = I.dense_stress_workload(n, d, seed=n)\n"
+        "    r, _, _ = gpu_closure(w, path_policy=2)\n"
+        "    assert_parity(w, r)\n"
+        "    r, _, _ = gpu_closure(w, path_policy=2, emulate_ranks=3)\n"
+        "    assert_parity(w, r)\n"
+        "print('ok')\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, CFPQ_DENSE_PAIR="1", PYTHONPATH=root)
+    out = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
