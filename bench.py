@@ -221,22 +221,44 @@ def supplementary_tensor(C, stream, steps=3):
             "cells": r.count(0), "roofline": roof}
 
 
+def rows_alg_bytes(w, r_sparse):
+    """SURVEY §8(d) algorithmic bytes of the bit path, per production A->BC and iteration k
+    (Jacobi operands T_{k-1}): 4W x (distinct rows of the bitmap operand T_C read = nonempty
+    columns of T_{k-1,B}) + 2 x 4W x (distinct output rows modified = rows of A that gain
+    cells in iteration k) + 8 x nnz(T_{k-1,B}) (the sparse operand's index entries);
+    W = ceil(n/32) words per row.  The per-iteration sets come from the sparse run's log."""
+    import numpy as np
+    n = w.n_nodes
+    W = (n + 31) // 32
+    K = r_sparse.iterations
+    rules = [tuple(x) for x in np.unique(w.bin.reshape(-1, 3), axis=0).tolist()]
+    pairs = {}
+    def at(X, k):
+        if (X, k) not in pairs:
+            pairs[(X, k)] = r_sparse.pairs_at(X, k)
+        return pairs[(X, k)]
+    total = 0
+    for k in range(1, K + 1):
+        for A, B, _ in rules:
+            pb = at(B, k - 1)
+            cols = len(np.unique(pb[:, 1])) if len(pb) else 0
+            grown = 0
+            if len(at(A, k)):
+                # rows of A whose cell count grew from T_{k-1} to T_k
+                ca = np.bincount(at(A, k)[:, 0], minlength=n)
+                cb = np.bincount(at(A, k - 1)[:, 0], minlength=n) if len(at(A, k - 1)) else np.zeros(n, np.int64)
+                grown = int(np.count_nonzero(ca > cb))
+            total += 4 * W * cols + 2 * 4 * W * grown + 8 * len(pb)
+    return total
+
+
 def supplementary_rows(C, w, g, d, r_sparse, stream, steps=2):
     """Config 4 in the paper-faithful full-operand mode (path_policy 3, bit-row CUDA-core
-    products of Alg. 1 line 9 over whole matrices), with its HBM roofline.  Algorithmic
-    bytes per iteration k: for every output A, 8*Wn*n (read T_{k-1,A}, write T_k,A) and
-    for every rule A->BC, 4*Wn*n (every row of T_B) + 4*Wn*|T_{k-1,B}| (one row of T_C per
-    set bit of T_B); Wn = ceil(n/32).  |T_{k-1,B}| comes from the sparse run's log."""
+    products of Alg. 1 line 9 over whole matrices), with its HBM roofline on SURVEY §8(d)'s
+    algorithmic bytes (rows_alg_bytes)."""
     n = w.n_nodes
-    wn = (n + 31) // 32
     K = r_sparse.iterations
-    outs = sorted({int(a) for a, _, _ in w.bin.tolist()})
-    cnt = [[r_sparse.count_at(X, k) for X in range(w.n_nt)] for k in range(K)]
-    alg = 0
-    for k in range(1, K + 1):
-        alg += len(outs) * 8 * wn * n
-        for _, B, _ in w.bin.tolist():
-            alg += 4 * wn * n + 4 * wn * cnt[k - 1][B]
+    alg = rows_alg_bytes(w, r_sparse)
     r = C.closure(g, d, path_policy=3, stream=stream)
     t = []
     for _ in range(steps):
@@ -251,7 +273,8 @@ def supplementary_rows(C, w, g, d, r_sparse, stream, steps=2):
             "roofline": {"bound": "hbm", "achieved": alg / loop_s / 1e9, "peak": peak, "unit": "GB/s",
                          "frac": alg / loop_s / 1e9 / peak, "traffic": ncu_traffic("config4_rows"),
                          "kernel": "cfpq::rows_kernel", "alg_bytes": alg, "peak_source": src,
-                         "note": "rows of T_C re-read for every set bit of T_B: many hit L2, so frac can exceed 1"}}
+                         "note": "SURVEY 8(d) model: each distinct operand row read once, each modified output "
+                                 "row read+written once, 8 B per sparse-operand entry"}}
 
 
 # ------------------------------------------------------------------------------------------

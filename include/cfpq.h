@@ -132,7 +132,9 @@ typedef struct {
                                 HBM), 1 bit matrices, 2 hashed cell set (relational,
                                 path_policy 0/1, no rule whose two operands both change,
                                 |N| < 1024; else CFPQ_E_UNSUPPORTED)                         */
-    int32_t reserved[3];     /* must be zero                                               */
+    int32_t reserved[3];     /* reserved[0]: diagnostics flags (0 = defaults): bit 0 no bit
+                                precheck before the atomic, bit 1 clear the other bank on a side
+                                stream, bit 2 no reset of the bit words at the fixpoint; others 0 */
 } cfpq_options;
 
 CFPQ_API void cfpq_options_default(cfpq_options* o);

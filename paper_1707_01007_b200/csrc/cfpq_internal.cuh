@@ -124,6 +124,8 @@ struct EngineParams {
     int32_t profile;               // accumulate single-CTA phase cycles into EngineState::prof
     unsigned long long switch_cells;  // |Δ_k| above which the loop stops for the dense engine (0 = never)
     int32_t precheck;              // read a candidate's word before its atomicOr (hot cells)
+    int32_t self_clear;            // relational runs: at the fixpoint the kernel resets the words
+                                   // of all logged cells in T/S/ST (the results stay in the log)
     // hashed cell set (relational sparse runs without var x var rules): open addressing,
     // linear probing over 64-bit packed cells, replaces the T bit matrices as the
     // membership structure (see engine.cu, "Hashed cell set")

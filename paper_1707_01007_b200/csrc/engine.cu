@@ -1422,6 +1422,25 @@ __global__ void __launch_bounds__(kBlock, 1) closure_kernel(EngineParams p) {
     }
     if (!aborted && blockIdx.x == 0 && threadIdx.x == 0) publish(p, s);
     if (!aborted) clear_drain(p);   // the other bank is clean when this launch ends
+    if (!aborted && p.self_clear && (s.status == ST_DONE || s.status == ST_CAP)) {
+        // the relations are in the log: reset the bit words of every logged cell while they
+        // are still hot in L2, so the next run starts on clean matrices (no clear pass)
+        __syncthreads();
+        const unsigned long long n_cells = s.hi;
+        for (unsigned long long e = (unsigned long long)blockIdx.x * kBlock + threadIdx.x; e < n_cells;
+             e += (unsigned long long)gridDim.x * kBlock) {
+            const uint64_t c = ldcg64(p.log + e);
+            const uint32_t A = cell_nt(c), i = cell_i(c), j = cell_j(c);
+            const NTInfo& t = nt[A];
+            t.T[(size_t)i * p.Wp + (j >> 5)] = 0u;
+            if (t.S) t.S[(size_t)i * p.Wp + (j >> 5)] = 0u;
+            if (t.ST) t.ST[(size_t)j * p.Wp + (i >> 5)] = 0u;
+            if (p.rowc) {
+                p.rowc[(size_t)A * p.n + i] = 0u;
+                p.colc[(size_t)A * p.n + j] = 0u;
+            }
+        }
+    }
     // diagnostics: one atomic per warp per launch
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
