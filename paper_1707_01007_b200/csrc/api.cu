@@ -564,7 +564,6 @@ static cfpq_status plan(cfpq_result* r, const cfpq_grammar* g, const cfpq_graph*
     const size_t adj_len = (size_t)slots * (size_t)(n + 1);
     if ((st = dalloc(&r->d_adj_cnt, adj_len, "adjacency counts")) != CFPQ_OK) return st;
     if ((st = dalloc(&r->d_adj_ptr, adj_len + 1, "adjacency pointers")) != CFPQ_OK) return st;
-    if ((st = dalloc(&r->d_adj_cursor, adj_len, "adjacency cursor")) != CFPQ_OK) return st;
     if ((st = dalloc(&r->d_adj_ell, (size_t)slots * n, "adjacency ELL heads")) != CFPQ_OK) return st;
     if ((st = dalloc(&r->d_slot_row, g->n_nt, "slots")) != CFPQ_OK) return st;
     if ((st = dalloc(&r->d_slot_col, g->n_nt, "slots")) != CFPQ_OK) return st;
@@ -1160,17 +1159,20 @@ static cfpq_status run(cfpq_result* r, const cfpq_graph* d) {
     const unsigned long long seeds_upper = (unsigned long long)d->n_edges * (unsigned long long)r->max_rules_per_label;
     CFPQ_CUDA_TRY(launch_seed(d->d_edges, d->n_edges, (int32_t)r->n, r->d_lab_ptr, r->d_lab_nt, r->n_labels,
                               r->max_rules_per_label, p, s));
-    CFPQ_CUDA_TRY(launch_begin(p, s));
-    r->launches += 2;
-    // preterminal adjacency (CSR rows / CSC columns), built once per closure
+    r->launches += 1;
+    // preterminal adjacency (CSR rows / CSC columns + ELL heads), built once per closure:
+    // count (also opens iteration 1), scan, fill (+ ELL heads; consumes the counts)
     if (r->n_adj_slots) {
         const size_t adj_len = (size_t)r->n_adj_slots * (r->n + 1);
+        CFPQ_CUDA_TRY(cudaMemsetAsync(r->d_adj_ell, 0, (size_t)r->n_adj_slots * r->n * sizeof(int4), s));
         CFPQ_CUDA_TRY(launch_adj_count(p, r->d_slot_row, r->d_slot_col, r->d_adj_cnt, seeds_upper, s));
         CFPQ_CUDA_TRY(launch_scan(r->d_adj_cnt, r->d_adj_ptr, (int64_t)adj_len, r->d_temp, &r->temp_bytes, s));
-        CFPQ_CUDA_TRY(cudaMemcpyAsync(r->d_adj_cursor, r->d_adj_ptr, adj_len * 4, cudaMemcpyDeviceToDevice, s));
-        CFPQ_CUDA_TRY(launch_adj_fill(p, r->d_slot_row, r->d_slot_col, r->d_adj_cursor, r->d_adj_idx, seeds_upper, s));
-        CFPQ_CUDA_TRY(launch_adj_ell(r->d_adj_ptr, r->d_adj_idx, r->d_adj_ell, r->n_adj_slots, (int32_t)r->n, s));
-        r->launches += 5;   // count, CUB scan (init + scan), fill, ELL heads
+        CFPQ_CUDA_TRY(launch_adj_fill(p, r->d_slot_row, r->d_slot_col, r->d_adj_ptr, r->d_adj_cnt, r->d_adj_idx,
+                                      r->d_adj_ell, seeds_upper, s));
+        r->launches += 4;   // count, CUB scan (init + scan), fill
+    } else {
+        CFPQ_CUDA_TRY(launch_begin(p, s));
+        r->launches += 1;
     }
     if (r->has_snapshots) {
         CFPQ_CUDA_TRY(launch_seed_snapshots(p, seeds_upper, s));

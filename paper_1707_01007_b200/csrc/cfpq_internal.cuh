@@ -188,7 +188,8 @@ cudaError_t launch_seed(const int32_t* edges, int64_t n_edges, int32_t n_nodes, 
 cudaError_t launch_adj_count(const EngineParams& p, const int32_t* slot_row, const int32_t* slot_col,
                              int32_t* counts, unsigned long long n_seed_upper, cudaStream_t s);
 cudaError_t launch_adj_fill(const EngineParams& p, const int32_t* slot_row, const int32_t* slot_col,
-                            int32_t* cursor, int32_t* idx, unsigned long long n_seed_upper, cudaStream_t s);
+                            const int32_t* ptr, int32_t* counts, int32_t* idx, int4* ell, unsigned long long n_seed,
+                            cudaStream_t s);
 cudaError_t launch_rehash(const EngineParams& p, unsigned long long n_cells, uint64_t cell_mask, int need_flag,
                           cudaStream_t s);
 cudaError_t launch_log_to_bitmap(const uint64_t* log, unsigned long long n_cells, uint32_t A, uint32_t* dst,
@@ -198,8 +199,7 @@ cudaError_t launch_begin(const EngineParams& p, cudaStream_t s);
 cudaError_t launch_async(const EngineParams& p, int grid, cudaStream_t s, bool flag_seeds,
                          unsigned long long seeds_upper);
 cudaError_t launch_strip_flags(uint64_t* log, unsigned long long lo, unsigned long long hi, cudaStream_t s);
-cudaError_t launch_adj_ell(const int32_t* ptr, const int32_t* idx, int4* ell, int64_t n_slots, int32_t n,
-                           cudaStream_t s);
+
 cudaError_t launch_seed_snapshots(const EngineParams& p, unsigned long long n_seed_upper, cudaStream_t s);
 int closure_kernel_blocks_per_sm();
 int closure_kernel_block_size();

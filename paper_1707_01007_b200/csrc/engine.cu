@@ -343,9 +343,19 @@ __global__ void __launch_bounds__(kSeedBlock) seed_kernel(EngineParams p, const 
 // CSR / CSC of preterminals from the seed cells Δ_0 = log[0, n_seed).
 // slot_row[X] / slot_col[X] = offset (in units of (n+1)) of X's CSR / CSC pointer
 // array inside the concatenated count array, or -1.
+// Degree counts of the preterminal slots over the seed cells Δ_0 = log[0, n_seed); block 0
+// also opens iteration 1 (the work of begin_kernel: Δ_0 = [0, n_seed)).
 __global__ void adj_count_kernel(EngineParams p, const int32_t* __restrict__ slot_row,
                                  const int32_t* __restrict__ slot_col, int32_t* counts) {
-    const unsigned long long n_seed = ld_volatile_u64(&p.st->hi);
+    const unsigned long long n_seed = ld_volatile_u64(&p.st->log_size);
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        p.st->lo = 0;
+        p.st->hi = n_seed;
+        p.st->iter = 0;
+        if (p.iter_off_cap > 0) p.iter_off[0] = 0;
+        if (p.iter_off_cap > 1) p.iter_off[1] = n_seed;
+        if (p.iter_time) p.iter_time[0] = globaltimer();
+    }
     for (unsigned long long e = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; e < n_seed;
          e += (unsigned long long)gridDim.x * blockDim.x) {
         uint64_t c = p.log[e];
@@ -356,33 +366,39 @@ __global__ void adj_count_kernel(EngineParams p, const int32_t* __restrict__ slo
     }
 }
 
+// Scatter the neighbours into CSR order and write the ELL heads in the same pass: the
+// counts are consumed (atomicSub: slot ptr[r] + old - 1, so they end at zero), the entry
+// that lands in a row's first slot writes {beg, deg, nb0}, the second one nb1 (ell was
+// zeroed: deg 0 rows read {0, 0, 0, 0}).
+__device__ __forceinline__ void adj_place(const int32_t* __restrict__ ptr, int32_t* counts, int32_t* idx, int4* ell,
+                                          size_t slot_off, size_t ell_off, uint32_t row, int32_t nb) {
+    const int32_t beg = ptr[slot_off + row];
+    const int32_t old = atomicSub(counts + slot_off + row, 1);
+    const int32_t pos = beg + old - 1;
+    idx[pos] = nb;
+    int* e = reinterpret_cast<int*>(ell + ell_off + row);
+    if (old == 1) {
+        e[0] = beg;
+        e[1] = ptr[slot_off + row + 1] - beg;
+        e[2] = nb;
+    } else if (old == 2) {
+        e[3] = nb;
+    }
+}
+
 __global__ void adj_fill_kernel(EngineParams p, const int32_t* __restrict__ slot_row,
-                                const int32_t* __restrict__ slot_col, int32_t* cursor, int32_t* idx) {
+                                const int32_t* __restrict__ slot_col, const int32_t* __restrict__ ptr,
+                                int32_t* counts, int32_t* idx, int4* ell) {
     const unsigned long long n_seed = ld_volatile_u64(&p.st->hi);
     for (unsigned long long e = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; e < n_seed;
          e += (unsigned long long)gridDim.x * blockDim.x) {
         uint64_t c = p.log[e];
         uint32_t X = cell_nt(c);
         int32_t sr = __ldg(slot_row + X), sc = __ldg(slot_col + X);
-        if (sr >= 0) idx[atomicAdd(cursor + (size_t)sr * (p.n + 1) + cell_i(c), 1)] = (int32_t)cell_j(c);
-        if (sc >= 0) idx[atomicAdd(cursor + (size_t)sc * (p.n + 1) + cell_j(c), 1)] = (int32_t)cell_i(c);
-    }
-}
-
-// ELL heads: ell[s][r] = {beg, deg, first neighbour, second neighbour} of slot s, row r.
-__global__ void adj_ell_kernel(const int32_t* __restrict__ ptr, const int32_t* __restrict__ idx, int4* ell,
-                               int64_t n_rows_total, int32_t n) {
-    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n_rows_total;
-         t += (int64_t)gridDim.x * blockDim.x) {
-        int64_t s = t / n, r = t - s * n;
-        const int32_t* pp = ptr + s * (int64_t)(n + 1);
-        int32_t b = pp[r], e = pp[r + 1];
-        int4 v;
-        v.x = b;
-        v.y = e - b;
-        v.z = e - b > 0 ? idx[b] : -1;
-        v.w = e - b > 1 ? idx[b + 1] : -1;
-        ell[t] = v;
+        if (sr >= 0)
+            adj_place(ptr, counts, idx, ell, (size_t)sr * (p.n + 1), (size_t)sr * p.n, cell_i(c), (int32_t)cell_j(c));
+        if (sc >= 0)
+            adj_place(ptr, counts, idx, ell, (size_t)sc * (p.n + 1), (size_t)sc * p.n, cell_j(c), (int32_t)cell_i(c));
     }
 }
 
@@ -1613,21 +1629,16 @@ cudaError_t launch_seed(const int32_t* edges, int64_t n_edges, int32_t n_nodes, 
 
 cudaError_t launch_adj_count(const EngineParams& p, const int32_t* slot_row, const int32_t* slot_col,
                              int32_t* counts, unsigned long long n_seed, cudaStream_t s) {
-    if (n_seed) adj_count_kernel<<<grid_for((int64_t)n_seed, 256), 256, 0, s>>>(p, slot_row, slot_col, counts);
+    adj_count_kernel<<<grid_for((int64_t)std::max<unsigned long long>(n_seed, 1), 256), 256, 0, s>>>(p, slot_row,
+                                                                                                  slot_col, counts);
     return cudaGetLastError();
 }
 
 cudaError_t launch_adj_fill(const EngineParams& p, const int32_t* slot_row, const int32_t* slot_col,
-                            int32_t* cursor, int32_t* idx, unsigned long long n_seed, cudaStream_t s) {
+                            const int32_t* ptr, int32_t* counts, int32_t* idx, int4* ell, unsigned long long n_seed,
+                            cudaStream_t s) {
     if (n_seed)
-        adj_fill_kernel<<<grid_for((int64_t)n_seed, 256), 256, 0, s>>>(p, slot_row, slot_col, cursor, idx);
-    return cudaGetLastError();
-}
-
-cudaError_t launch_adj_ell(const int32_t* ptr, const int32_t* idx, int4* ell, int64_t n_slots, int32_t n,
-                           cudaStream_t s) {
-    int64_t rows = n_slots * (int64_t)n;
-    if (rows) adj_ell_kernel<<<grid_for(rows, 256), 256, 0, s>>>(ptr, idx, ell, rows, n);
+        adj_fill_kernel<<<grid_for((int64_t)n_seed, 256), 256, 0, s>>>(p, slot_row, slot_col, ptr, counts, idx, ell);
     return cudaGetLastError();
 }
 
