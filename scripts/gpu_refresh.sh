@@ -24,3 +24,5 @@ r=C.closure(g,d,path_policy=3)
 " > gpurun_out/ncu_rows.txt 2>&1
 tail -2 gpurun_out/ncu_c4.txt gpurun_out/ncu_rows.txt
 ls -la gpurun_out | head -40
+python scripts/phase_profile.py config4 > gpurun_out/phase_config4.txt 2>&1
+python scripts/e2e_breakdown.py > gpurun_out/e2e_config4.txt 2>&1
