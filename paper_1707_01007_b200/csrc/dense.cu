@@ -416,27 +416,43 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
             bool live = false;   // the pair issued MMAs for this tile (else TMEM holds no result)
             for (int q = p.rule_ptr[o]; q < p.rule_ptr[o + 1] && !live; ++q)
                 for (int K = 0; K < n_k && !live; ++K) live = kblock_live_group<kCl>(p, p.rules[q], I0, J, K);
+            // this row's 8 old words (32 contiguous bytes of T_{k-1}) load while the MMAs run
+            const int row = I * kTM + quarter * 32 + lane;
+            const bool wr = mine && row < p.n;
+            uint4 o0 = make_uint4(0, 0, 0, 0), o1 = o0;
+            if (wr) {
+                const uint4* src = reinterpret_cast<const uint4*>(p.T[A] + (size_t)row * p.Wp + (size_t)J * (kTN / 32));
+                o0 = __ldg(src);
+                o1 = __ldg(src + 1);
+            }
             mbar_wait(&tmem_full[as], tphase);
             tc_fence_after();
-            const int row = I * kTM + quarter * 32 + lane;
-            const uint32_t* told = p.T[A] + (size_t)row * p.Wp;
-            uint32_t* tnew = p.Tn[A] + (size_t)row * p.Wp;
-            unsigned long long cnt = 0;
+            uint32_t w[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+            if (live) {
 #pragma unroll 1
-            for (int c = 0; c < kTN / 32; ++c) {
-                uint32_t word = 0;
-                if (live) {
+                for (int c = 0; c < kTN / 32; ++c) {
                     uint32_t v[32];
                     tmem_ld32(tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(as * 256 + c * 32), v);
+                    uint32_t word = 0;
 #pragma unroll
                     for (int b = 0; b < 32; ++b) word |= (v[b] != 0u ? 1u : 0u) << b;
+#pragma unroll
+                    for (int q = 0; q < 8; ++q)
+                        if (q == c) w[q] = word;
                 }
-                const int64_t wi = (int64_t)J * (kTN / 32) + c;
-                if (mine && row < p.n && wi < p.Wp) {
-                    uint32_t old = __ldg(told + wi);
-                    tnew[wi] = old | word;
-                    cnt += __popc(word & ~old);
+            }
+            unsigned long long cnt = 0;
+            if (wr) {
+                const uint32_t old[8] = {o0.x, o0.y, o0.z, o0.w, o1.x, o1.y, o1.z, o1.w};
+                uint32_t nw[8];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    nw[q] = old[q] | w[q];
+                    cnt += __popc(w[q] & ~old[q]);
                 }
+                uint4* dst = reinterpret_cast<uint4*>(p.Tn[A] + (size_t)row * p.Wp + (size_t)J * (kTN / 32));
+                dst[0] = make_uint4(nw[0], nw[1], nw[2], nw[3]);
+                dst[1] = make_uint4(nw[4], nw[5], nw[6], nw[7]);
             }
             tc_fence_before();
             mbar_arrive(&tmem_empty[as]);
