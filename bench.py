@@ -13,11 +13,14 @@ line 9 on sparse operands) / closure time; ms_per_step = closure time.
   python bench.py --impl reference ...   # the CPU oracle as the reference arm
 
 Multi-GPU (torchrun, N>1): one process per GPU; time = max over ranks of the
-device-timed region.  config4 and configS close ONE problem row-block sharded over the
-ranks (north_star / SURVEY §8(e): every rank derives the cells of its rows; config4
-exchanges Δ_k as index lists, configS all-gathers the dense row blocks; NCCL every
-iteration): "scaling": "strong".  config2/3/5 (and config4 with --replicas) close one
-independent seeded replica per GPU with no data-path collective: "scaling": "weak".
+device-timed region.  configS closes ONE problem row-block sharded over the ranks
+(dense row blocks all-gathered over NCCL every iteration): "scaling": "strong".  config4's
+closure is latency-bound (~20 dependent iterations of ~25 us, SURVEY V-9), so its headline
+at N>1 is N independent seeded problems, one per GPU, no data-path collective ("scaling":
+"weak"); the row-block sharded closure of ONE config-4 problem (north_star / SURVEY §8(e):
+each rank derives the cells of its rows, Δ_k exchanged as index lists over NCCL) is timed
+beside it as supplementary.row_sharded, or as the headline with --sharded.  config2/3/5:
+replicas.
 """
 from __future__ import annotations
 
@@ -277,6 +280,40 @@ def supplementary_rows(C, w, g, d, r_sparse, stream, steps=2):
                                  "row read+written once, 8 B per sparse-operand entry"}}
 
 
+def supplementary_row_sharded(C, args, rank, world, stream, dist):
+    """Config 4 (seed args.seed) closed as ONE problem row-block sharded over the ranks: each
+    rank derives its rows' cells, Δ_k is all-gathered as index lists (NCCL) every iteration.
+    Time = max over ranks of the device-timed closure."""
+    import torch
+    w, _ = make_workload("config4", args.seed)
+    uid = torch.zeros(128, dtype=torch.uint8, device="cuda")
+    if rank == 0:
+        uid.copy_(torch.tensor(list(C.nccl_unique_id()), dtype=torch.uint8))
+    dist.broadcast(uid, src=0)
+    kw = {"world_size": world, "rank": rank, "nccl_unique_id": bytes(uid.cpu().tolist())}
+    g = C.Grammar.from_workload(w)
+    d = C.Graph(w.n_nodes, torch.from_numpy(w.edges).cuda(), stream=stream)
+    ops = jacobi_ops(w, "config4", g, d, C, stream)
+    r = C.closure(g, d, stream=stream, **kw)
+    for _ in range(args.warmup):
+        C.closure_reuse(g, d, r, stream=stream, **kw)
+    torch.cuda.synchronize()
+    dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        C.closure_reuse(g, d, r, stream=stream, **kw)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item()) / args.steps
+    return {"workload": "config4 seed %d, one problem over %d GPUs" % (args.seed, world), "ms_per_step": ms,
+            "value": ops / (ms * 1e-3) / 1e9, "unit": "Gop/s", "iterations": r.iterations,
+            "cells": int(r.stats()["cells"]), "scaling": "strong",
+            "note": "latency-bound: one collective round per iteration dominates (DESIGN §3.5)"}
+
+
 # ------------------------------------------------------------------------------------------
 # reference arm: the CPU oracle as it stands, on a bounded sample of the workload
 # ------------------------------------------------------------------------------------------
@@ -347,8 +384,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-supplementary", action="store_true")
     ap.add_argument("--solo", type=int, default=-1)
-    ap.add_argument("--replicas", action="store_true",
-                    help="N>1: independent replicas instead of row-block sharding (config4)")
+    ap.add_argument("--sharded", action="store_true",
+                    help="N>1, config4: headline = ONE problem row-block sharded over the ranks (strong)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -371,7 +408,7 @@ def main():
 
     # config S / config 4 shard ONE problem by row blocks over NCCL (strong scaling); the
     # other workloads close one independent seeded problem per GPU (weak scaling)
-    sharded = world > 1 and (args.workload == "configS" or (args.workload == "config4" and not args.replicas))
+    sharded = world > 1 and (args.workload == "configS" or (args.workload == "config4" and args.sharded))
     w, desc = make_workload(args.workload, args.seed + (0 if sharded else rank))
     shard_kw = {}
     if sharded:
@@ -492,6 +529,11 @@ def main():
                "d2h_bytes_per_step": int(d2h), "ms_per_step": 1e3 * float(e_total.item()) / len(ts)}
 
     supp = None
+    if world > 1 and args.workload == "config4" and not sharded and not args.no_supplementary:
+        # ONE config-4 problem row-block sharded over all ranks (every rank takes part)
+        rs = supplementary_row_sharded(C, args, rank, world, stream, dist)
+        if rank == 0:
+            supp = {"row_sharded": rs}
     if rank == 0 and world == 1 and args.workload == "config4" and not args.no_supplementary:
         supp = {}
         try:
