@@ -492,6 +492,10 @@ def main():
     alg_bytes = 8 * cells + 8 * exps + 12 * cand + 8 * new_cells
     if lengths:
         alg_bytes += 16 * cand + 8 * cells
+    elif not sharded:
+        # relational runs reset their bit words at the fixpoint inside the same launch:
+        # 8 B log read + 4 B word store per cell
+        alg_bytes += 12 * cells
     loop_s = statistics.mean(loop_ns) * 1e-9
     if pol != 2:
         achieved = alg_bytes / loop_s / 1e9
