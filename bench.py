@@ -68,7 +68,8 @@ def make_workload(name: str, seed: int):
                 "grammar": "same-generation G' (P:279-296)"}
     elif name == "configS":
         w = I.dense_stress_workload(16384, 2, seed)
-        desc = {"workload": "configS: S->SS|a on G(n=16384, m=2n), dense tcgen05 int8 engine", "grammar": "S->SS|a"}
+        desc = {"workload": "configS: S->SS|a on G(n=16384, m=2n), dense tcgen05 engine (fp4 kind::mxf4)",
+                "grammar": "S->SS|a"}
     else:
         raise SystemExit(f"unknown workload {name}")
     desc.update({"n_nodes": w.n_nodes, "n_edges": int(len(w.edges)), "seed": seed})
@@ -188,21 +189,34 @@ def int8_peak():
         return 2.0 * 1590.0, 2.0 * 1400.0, "fallback bf16 x 2 (B200_PROFILING.md)"
 
 
-def tensor_roofline(stats, step_ms):
-    """Issued tensor work of the dense engine: 2*128*256*128 int8 ops per k-block, over the
-    device time of the fixpoint loop (all tcgen05 product launches + packs of every iteration)."""
+def fp4_peak():
+    """Dense FP4 (kind::mxf4) tensor peak = measured bf16 x the nominal fp4/bf16 ratio (9 / 2.25 = 4)."""
+    b, s, src = int8_peak()
+    return 2.0 * b, 2.0 * s, src.replace("x 2 (nominal int8/bf16)", "x 4 (nominal fp4/bf16)")
+
+
+TENSOR_FORMATS = {1: "int8", 2: "fp4"}
+
+
+def tensor_roofline(stats, step_ms, fmt=2):
+    """Issued tensor work of the dense engine over the device time of the fixpoint loop (all
+    tcgen05 product launches + packs of every iteration): 2*128*256*128 ops per 128-deep
+    k-block (the library counts an fp4 k-block, 256 deep, as two).  Peak of the format:
+    int8 = bf16 x 2, fp4 = bf16 x 4 (measured bf16, nominal ratios)."""
     ops = stats["mma_kblocks"] * 2 * 128 * 256 * 128
     loop_s = stats["loop_ns"] * 1e-9
-    burst, sustained, src = int8_peak()
+    burst, sustained, src = fp4_peak() if fmt == 2 else int8_peak()
     achieved = ops / loop_s / 1e12
+    kind = "kind::mxf4, e2m1 0/1, unit ue8m0 scales, f32 accumulator" if fmt == 2 else "kind::i8"
     return {"bound": "tensor", "achieved": achieved, "peak": burst, "unit": "TFLOP/s", "frac": achieved / burst,
-            "frac_of_sustained": achieved / sustained, "traffic": ncu_traffic("configS"),
-            "kernel": "cfpq::dense_kernel (tcgen05.mma kind::i8)", "loop_ms": loop_s * 1e3,
-            "share_of_step": loop_s * 1e3 / step_ms, "issued_int8_ops": ops, "peak_source": src,
-            "note": "int8 TOPS reported in the TFLOP/s slot; issued work counts whole 128x256x128 tiles (zeros inside tiles included)"}
+            "frac_of_sustained": achieved / sustained, "traffic": ncu_traffic("configS" if fmt == 2 else "configS_int8"),
+            "kernel": f"cfpq::dense_kernel (tcgen05.mma {kind})", "format": TENSOR_FORMATS[fmt],
+            "loop_ms": loop_s * 1e3, "share_of_step": loop_s * 1e3 / step_ms, "issued_ops": ops, "peak_source": src,
+            "note": f"{TENSOR_FORMATS[fmt]} TOPS reported in the TFLOP/s slot; issued work counts whole 128x256 "
+                    "output tiles x live K blocks (zeros inside tiles included)"}
 
 
-def supplementary_tensor(C, stream, steps=3):
+def supplementary_tensor(C, stream, steps=3, fmt=2):
     """Config S (S->SS|a, n=16384) on the tcgen05 engine: the tensor-path roofline beside the
     headline line (untimed by the driver's contract; its own CUDA-event timing)."""
     import inputs as I
@@ -210,48 +224,93 @@ def supplementary_tensor(C, stream, steps=3):
     w = I.dense_stress_workload(16384, 2, 0)
     g = C.Grammar.from_workload(w)
     d = C.Graph(w.n_nodes, torch.from_numpy(w.edges).cuda(), stream=stream)
-    r = C.closure(g, d, path_policy=2, stream=stream)
-    C.closure_reuse(g, d, r, path_policy=2, stream=stream)
+    r = C.closure(g, d, path_policy=2, tensor_format=fmt, stream=stream)
+    C.closure_reuse(g, d, r, path_policy=2, tensor_format=fmt, stream=stream)
     t = []
     st = None
     for _ in range(steps):
-        C.closure_reuse(g, d, r, path_policy=2, stream=stream)
+        C.closure_reuse(g, d, r, path_policy=2, tensor_format=fmt, stream=stream)
         st = r.stats()
         t.append(st["loop_ns"] + st["seed_ns"])
     ms = statistics.mean(t) * 1e-6
-    roof = tensor_roofline(st, ms)
-    return {"workload": "configS: S->SS|a, G(16384, 32768)", "closure_ms": ms, "iterations": r.iterations,
-            "cells": r.count(0), "roofline": roof}
+    roof = tensor_roofline(st, ms, fmt)
+    out = {"workload": "configS: S->SS|a, G(16384, 32768)", "format": TENSOR_FORMATS[fmt], "closure_ms": ms,
+           "iterations": r.iterations, "cells": r.count(0), "roofline": roof}
+    del r
+    return out
 
 
 def rows_alg_bytes(w, r_sparse):
-    """SURVEY §8(d) algorithmic bytes of the bit path, per production A->BC and iteration k
-    (Jacobi operands T_{k-1}): 4W x (distinct rows of the bitmap operand T_C read = nonempty
-    columns of T_{k-1,B}) + 2 x 4W x (distinct output rows modified = rows of A that gain
-    cells in iteration k) + 8 x nnz(T_{k-1,B}) (the sparse operand's index entries);
-    W = ceil(n/32) words per row.  The per-iteration sets come from the sparse run's log."""
+    """Algorithmic bytes of the bit-row path (path_policy 3): the full Jacobi product
+    T_{k-1} x T_{k-1} of every rule at every iteration k, in the form the kernels evaluate it
+    (DESIGN §3.3), each distinct row / index entry read once per rule and iteration:
+      L (B changes, C preterminal): 4W per non-empty row of T_B (bit-row scan) + 8 B per set
+        bit (its CSR_C row pointers) + 4 B per CSR_C entry reached (candidate index)
+      R (B preterminal, C changes): 8 B per row of CSR_B + 4 B per CSR_B entry + 4W per
+        distinct non-empty row of T_C referenced
+      V (both change): 4W per non-empty row of T_B + 4W per distinct non-empty row of T_C
+        referenced
+      P (both preterminal, iteration 1 only): 8 B per CSR_B row + 4 B per CSR_B entry + 8 B
+        per entry (CSR_C pointers) + 4 B per candidate
+      every form: 8 B per distinct output word the product touches (pre-check read + merge)
+      per iteration: 32 B per word of T_k that gained bits (Δ_k word list: write + apply);
+        iteration 1: 8 B per seed cell (T_0 into the second buffer).
+    W = ceil(n/32) words per row.  T_{k-1} per NT comes from the sparse run's log."""
     import numpy as np
+    import scipy.sparse as sp
     n = w.n_nodes
     W = (n + 31) // 32
     K = r_sparse.iterations
     rules = [tuple(x) for x in np.unique(w.bin.reshape(-1, 3), axis=0).tolist()]
-    pairs = {}
+    lhs = {A for A, _, _ in rules}
+    pre = [X not in lhs for X in range(w.n_nt)]
+    cache = {}
+
     def at(X, k):
-        if (X, k) not in pairs:
-            pairs[(X, k)] = r_sparse.pairs_at(X, k)
-        return pairs[(X, k)]
-    total = 0
+        if (X, k) not in cache:
+            cache[(X, k)] = r_sparse.pairs_at(X, k)
+        return cache[(X, k)]
+
+    def mat(pairs):
+        return sp.csr_matrix((np.ones(len(pairs), np.int8), (pairs[:, 0], pairs[:, 1])), shape=(n, n))
+
+    def words(P):
+        P = P.tocoo()
+        return len(np.unique(P.row.astype(np.int64) * W + P.col // 32)) if P.nnz else 0
+
+    total = 8 * sum(len(at(X, 0)) for X in range(w.n_nt))
     for k in range(1, K + 1):
-        for A, B, _ in rules:
-            pb = at(B, k - 1)
-            cols = len(np.unique(pb[:, 1])) if len(pb) else 0
-            grown = 0
-            if len(at(A, k)):
-                # rows of A whose cell count grew from T_{k-1} to T_k
-                ca = np.bincount(at(A, k)[:, 0], minlength=n)
-                cb = np.bincount(at(A, k - 1)[:, 0], minlength=n) if len(at(A, k - 1)) else np.zeros(n, np.int64)
-                grown = int(np.count_nonzero(ca > cb))
-            total += 4 * W * cols + 2 * 4 * W * grown + 8 * len(pb)
+        for A, B, C in rules:
+            pb, pc = at(B, k - 1), at(C, k - 1)
+            if len(pb) == 0 or len(pc) == 0:
+                if not pre[B] and len(pb):
+                    total += 4 * W * len(np.unique(pb[:, 0]))   # the row is still scanned
+                continue
+            MB, MC = mat(pb), mat(pc)
+            degC = np.diff(MC.indptr)
+            P = (MB.astype(np.int32) @ MC.astype(np.int32))
+            if not pre[B] and pre[C]:
+                total += 4 * W * len(np.unique(pb[:, 0])) + 8 * len(pb) + 4 * int(degC[pb[:, 1]].sum())
+            elif pre[B] and not pre[C]:
+                ref = np.unique(pb[:, 1])
+                total += 8 * len(np.unique(pb[:, 0])) + 4 * len(pb) + 4 * W * int((degC[ref] > 0).sum())
+            elif not pre[B] and not pre[C]:
+                ref = np.unique(pb[:, 1])
+                total += 4 * W * len(np.unique(pb[:, 0])) + 4 * W * int((degC[ref] > 0).sum())
+            else:
+                if k > 1:
+                    continue
+                total += 8 * len(np.unique(pb[:, 0])) + 12 * len(pb) + 4 * int(degC[pb[:, 1]].sum())
+            total += 8 * words(P)
+        # Δ_k word list: words of T_k that gained bits
+        for A in lhs:
+            new = at(A, k)
+            if len(new) == len(at(A, k - 1)):
+                continue
+            Mk, Mp = mat(new), mat(at(A, k - 1)) if len(at(A, k - 1)) else None
+            D = Mk if Mp is None else (Mk - Mp)
+            D.eliminate_zeros()
+            total += 32 * words(D)
     return total
 
 
@@ -276,8 +335,9 @@ def supplementary_rows(C, w, g, d, r_sparse, stream, steps=2):
             "roofline": {"bound": "hbm", "achieved": alg / loop_s / 1e9, "peak": peak, "unit": "GB/s",
                          "frac": alg / loop_s / 1e9 / peak, "traffic": ncu_traffic("config4_rows"),
                          "kernel": "cfpq::rows_kernel", "alg_bytes": alg, "peak_source": src,
-                         "note": "SURVEY 8(d) model: each distinct operand row read once, each modified output "
-                                 "row read+written once, 8 B per sparse-operand entry"}}
+                         "note": "model of the implemented full-operand forms (DESIGN 3.3, bench.rows_alg_bytes): "
+                                 "each distinct bit row / CSR entry read once per rule and iteration, 8 B per "
+                                 "output word touched, 32 B per Delta word"}}
 
 
 def supplementary_row_sharded(C, args, rank, world, stream, dist):
@@ -379,6 +439,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="config4", choices=["config4", "config3", "config5", "config2", "configS"])
+    ap.add_argument("--tensor-format", type=int, default=0, choices=[0, 1, 2],
+                    help="tensor engine operands: 0 auto (fp4), 1 int8 (kind::i8), 2 fp4 (kind::mxf4)")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -425,7 +487,8 @@ def main():
     if sharded:
         ops = ops // world   # one problem split over the ranks: count its work once in total
     pol = policy_for(args.workload)
-    r = C.closure(g, d, stream=stream, semantics=int(lengths), solo_threshold=args.solo, path_policy=pol, **shard_kw)
+    r = C.closure(g, d, stream=stream, semantics=int(lengths), solo_threshold=args.solo, path_policy=pol,
+                      tensor_format=args.tensor_format, **shard_kw)
     iterations = r.iterations
     cells = r.stats()["cells"]
     cells_total = sum(r.count(A) for A in range(w.n_nt)) if pol == 2 else cells
@@ -437,6 +500,7 @@ def main():
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
     for _ in range(args.warmup):
         C.closure_reuse(g, d, r, stream=stream, semantics=int(lengths), solo_threshold=args.solo, path_policy=pol,
+                      tensor_format=args.tensor_format,
                             **shard_kw)
     torch.cuda.synchronize()
     if world > 1:
@@ -452,6 +516,7 @@ def main():
             flush.fill_(1)
             ev0.record(stream)
             C.closure_reuse(g, d, r, stream=stream, semantics=int(lengths), solo_threshold=args.solo, path_policy=pol,
+                      tensor_format=args.tensor_format,
                             **shard_kw)
             ev1.record(stream)
             ev1.synchronize()
@@ -486,7 +551,7 @@ def main():
     # single-path adds 16 B per candidate (key read+write) and 8 B per entry (own key).
     peak, peak_src = hbm_peak()
     if pol == 2:
-        roofline = tensor_roofline(stats, total_ms / args.steps)
+        roofline = tensor_roofline(stats, total_ms / args.steps, 1 if args.tensor_format == 1 else 2)
     cand, exps = stats["candidates"], stats["expansions"]
     new_cells = cells - delta0
     alg_bytes = 8 * cells + 8 * exps + 12 * cand + 8 * new_cells
@@ -520,6 +585,7 @@ def main():
             t0 = time.perf_counter()
             d.set_edges(pinned, stream=stream)
             C.closure_reuse(g, d, r, stream=stream, semantics=int(lengths), solo_threshold=args.solo, path_policy=pol,
+                      tensor_format=args.tensor_format,
                             **shard_kw)
             pairs = r.pairs(w.start, out=out_pairs)
             t1 = time.perf_counter()
@@ -541,9 +607,13 @@ def main():
     if rank == 0 and world == 1 and args.workload == "config4" and not args.no_supplementary:
         supp = {}
         try:
-            supp["tensor_path"] = supplementary_tensor(C, stream)
+            supp["tensor_path"] = supplementary_tensor(C, stream, fmt=2)
         except Exception as ex:   # never lose the headline line over a supplement
             supp["tensor_path_error"] = repr(ex)
+        try:
+            supp["tensor_path_int8"] = supplementary_tensor(C, stream, fmt=1)
+        except Exception as ex:
+            supp["tensor_path_int8_error"] = repr(ex)
         try:
             supp["paper_faithful_rows"] = supplementary_rows(C, w, g, d, r, stream)
         except Exception as ex:

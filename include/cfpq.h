@@ -132,7 +132,12 @@ typedef struct {
                                 HBM), 1 bit matrices, 2 hashed cell set (relational,
                                 path_policy 0/1, no rule whose two operands both change,
                                 |N| < 1024; else CFPQ_E_UNSUPPORTED)                         */
-    int32_t reserved[3];     /* reserved[0]: diagnostics flags (0 = defaults): bit 0 no bit
+    int32_t tensor_format;   /* operand format of the tensor engine (path_policy 0/2):
+                                0 auto (= 2), 1 int8 (tcgen05 kind::i8, s32 accumulator),
+                                2 fp4 (tcgen05 kind::mxf4: 0/1 as e2m1 nibbles, every block
+                                scale 1.0, f32 accumulator; all terms are >= 0, so the
+                                threshold P > 0 is exact)                           */
+    int32_t reserved[2];     /* reserved[0]: diagnostics flags (0 = defaults): bit 0 no bit
                                 precheck before the atomic, bit 1 clear the other bank on a side
                                 stream, bit 2 no reset of the bit words at the fixpoint; others 0 */
 } cfpq_options;

@@ -49,7 +49,8 @@ class Options(ctypes.Structure):
                 ("solo_threshold", ctypes.c_int32), ("record_times", ctypes.c_int32),
                 ("max_ctas", ctypes.c_int32), ("emulate_ranks", ctypes.c_int32),
                 ("cell_set", ctypes.c_int32),
-                ("reserved", ctypes.c_int32 * 3)]
+                ("tensor_format", ctypes.c_int32),
+                ("reserved", ctypes.c_int32 * 2)]
 
 
 _lib = None
@@ -188,7 +189,8 @@ class Graph:
 def options(semantics: int = 0, schedule: int = 0, path_policy: int = 0, account_work: bool = False,
             max_iterations: int = 0, stream=None, log_capacity: int = 0, solo_threshold: int = -1,
             record_times: bool = False, max_ctas: int = 0, world_size: int = 1, rank: int = 0,
-            nccl_unique_id=None, emulate_ranks: int = 0, flags: int = 0, cell_set: int = 0) -> Options:
+            nccl_unique_id=None, emulate_ranks: int = 0, flags: int = 0, cell_set: int = 0,
+            tensor_format: int = 0) -> Options:
     o = Options()
     load().cfpq_options_default(ctypes.byref(o))
     o.semantics, o.schedule, o.path_policy = int(semantics), int(schedule), int(path_policy)
@@ -204,6 +206,7 @@ def options(semantics: int = 0, schedule: int = 0, path_policy: int = 0, account
     o.emulate_ranks = int(emulate_ranks)
     o.reserved[0] = int(flags)
     o.cell_set = int(cell_set)
+    o.tensor_format = int(tensor_format)
     if nccl_unique_id is not None:
         buf = ctypes.create_string_buffer(bytes(nccl_unique_id), 128)
         o._uid = buf                     # keep alive with the options

@@ -343,7 +343,7 @@ static cfpq_status ensure_dense(cfpq_result* r) {
     if (r->dense) return CFPQ_OK;
     std::string err;
     r->dense = dense_create((int32_t)r->n, r->n_nt, r->Wp, r->rules, r->is_const, r->stream, &err,
-                            r->opts.path_policy != 3);
+                            r->opts.path_policy != 3, r->opts.tensor_format != 1);
     if (!r->dense) {
         set_error(err);
         return CFPQ_E_CUDA;
@@ -473,6 +473,8 @@ static cfpq_status plan(cfpq_result* r, const cfpq_grammar* g, const cfpq_graph*
             ex[rl.B].push_back(Expansion{EXP_L_CONST, rl.A, rl.C, 0});
             need_csr[rl.C] = 1;
         }
+        // the bit-row path gathers rows i of a preterminal left operand from its CSR
+        if (o->path_policy == 3 && bc) need_csr[rl.B] = 1;
     }
     std::vector<Expansion> exps;
     r->h_nt.assign(g->n_nt, NTInfo{});
@@ -770,7 +772,8 @@ static cfpq_status run_dense(cfpq_result* r, int64_t start_k) {
         const bool rows = r->opts.path_policy == 3;
         CFPQ_CUDA_TRY(dense_begin(r->dense, r->Tcur.data(), r->Tnxt.data(), k == start_k + 1, s, &launches, !rows));
         if (rows) {
-            CFPQ_CUDA_TRY(rows_product(r->dense, r->Tcur.data(), r->Tnxt.data(), s, &launches));
+            CFPQ_CUDA_TRY(rows_product(r->dense, r->Tcur.data(), r->Tnxt.data(), r->d_nt, r->d_adj_idx, r->d_log,
+                                       r->n_cells, k == start_k + 1, s, &launches));
         } else if (r->n_ranks == 1 && !r->comm) {
             CFPQ_CUDA_TRY(dense_product(r->dense, 0, tiles, s, &launches));
         } else if (r->emulated) {
@@ -1298,6 +1301,7 @@ static cfpq_status check_inputs(const cfpq_grammar* g, const cfpq_graph* d, cons
     }
     CFPQ_CHECK_ARG(o->path_policy >= 0 && o->path_policy <= 3, "cfpq_closure: bad path_policy");
     CFPQ_CHECK_ARG(o->cell_set >= 0 && o->cell_set <= 2, "cfpq_closure: cell_set must be 0, 1 or 2");
+    CFPQ_CHECK_ARG(o->tensor_format >= 0 && o->tensor_format <= 2, "cfpq_closure: tensor_format must be 0, 1 or 2");
     return CFPQ_OK;
 }
 
@@ -1327,7 +1331,7 @@ extern "C" cfpq_status cfpq_closure_reuse(const cfpq_grammar* g, const cfpq_grap
     CFPQ_CHECK_ARG(d->n_nodes == r->n && g->n_nt == r->n_nt && g->n_labels == r->n_labels &&
                        g->rules.size() == r->rules.size() && o->semantics == r->opts.semantics &&
                        o->account_work == r->opts.account_work && o->path_policy == r->opts.path_policy &&
-                       o->cell_set == r->opts.cell_set,
+                       o->cell_set == r->opts.cell_set && o->tensor_format == r->opts.tensor_format,
                    "cfpq_closure_reuse: grammar/graph/options differ from the result's plan");
     for (size_t k = 0; k < g->rules.size(); ++k)
         CFPQ_CHECK_ARG(g->rules[k].A == r->rules[k].A && g->rules[k].B == r->rules[k].B && g->rules[k].C == r->rules[k].C,

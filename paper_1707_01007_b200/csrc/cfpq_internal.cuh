@@ -235,11 +235,18 @@ cudaError_t launch_bitmap_pairs(const uint32_t* T, int32_t n, int64_t Wp, const 
 // dense (tcgen05) engine, dense.cu
 struct DenseEngine;
 DenseEngine* dense_create(int32_t n, int32_t n_nt, int64_t Wp, const std::vector<Rule3>& rules,
-                          const std::vector<int32_t>& is_const, cudaStream_t s, std::string* err, bool tensor);
+                          const std::vector<int32_t>& is_const, cudaStream_t s, std::string* err, bool tensor,
+                          bool fp4);
+bool dense_is_fp4(const DenseEngine* e);
 void dense_destroy(DenseEngine* e);
 cudaError_t dense_begin(DenseEngine* e, uint32_t* const* T, uint32_t* const* Tn, bool first, cudaStream_t s,
                         int* launches, bool pack_operands);
-cudaError_t rows_product(DenseEngine* e, uint32_t* const* T, uint32_t* const* Tn, cudaStream_t s, int* launches);
+// Bit-row (full-operand Jacobi) iteration: nt = the device NT table (is_const, CSR rows of
+// preterminals), adj_idx = CSR index array, log[0, n_seeds) = the seed cells (read at the
+// first iteration only).
+cudaError_t rows_product(DenseEngine* e, uint32_t* const* T, uint32_t* const* Tn, const NTInfo* nt,
+                         const int32_t* adj_idx, const uint64_t* log, unsigned long long n_seeds, bool first,
+                         cudaStream_t s, int* launches);
 cudaError_t dense_product(DenseEngine* e, int64_t i_lo, int64_t i_hi, cudaStream_t s, int* launches);
 cudaError_t dense_finish(DenseEngine* e, cudaStream_t s, unsigned long long* new_total);
 unsigned long long* dense_total_counter(DenseEngine* e);

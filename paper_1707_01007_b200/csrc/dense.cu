@@ -125,6 +125,25 @@ __device__ __forceinline__ void umma_i8(uint32_t tmem_d, uint64_t adesc, uint64_
         "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
         "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
 }
+// kind::mxf4 (MXFP4: e2m1 operands packed two per byte, one ue8m0 scale per 32 K
+// elements), block-scaled MMA M=128, N=256, K=64.  Scale factors are read from TMEM.
+__device__ __forceinline__ void umma_mxf4(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                          uint32_t accumulate, uint32_t tmem_sfa, uint32_t tmem_sfb) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%6], p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate), "r"(tmem_sfa), "r"(tmem_sfb));
+}
+// Fill 32 TMEM columns of this warp's 32 lanes with one 32-bit value.
+__device__ __forceinline__ void tmem_fill32(uint32_t taddr, uint32_t v) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+        "{%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(taddr),
+        "r"(v)
+        : "memory");
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                  : "memory");
@@ -168,10 +187,21 @@ __host__ __device__ constexpr uint32_t idesc_i8(int M, int N) {
     return (2u << 4) | (0u << 7) | (0u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 
+// kind::mxf4 block-scaled instruction descriptor: A/B e2m1 (MXF4 format 1), K-major,
+// scale format ue8m0 (bit 23), N>>3 at bit 17, M>>4 at bit 24, dense K = 64, scale ids 0.
+__host__ __device__ constexpr uint32_t idesc_mxf4(int M, int N) {
+    return (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | (1u << 23) | ((uint32_t)(M >> 4) << 24);
+}
+constexpr uint32_t kSfOne = 0x7F7F7F7Fu;   // four ue8m0 scale bytes of 2^0 = 1.0
+
 // ------------------------------------------------------------------------------------------
 // Pack: bits -> 0/1 bytes (row-major T8 and transposed T8T) + 128x128 tile occupancy.
 // One CTA (256 threads) per 128x128 tile of one NT.
 // ------------------------------------------------------------------------------------------
+// kF4: e2m1 nibbles instead of bytes (1.0 = 0x2, two elements per byte, element 2b in the
+// low nibble of byte b); row length np/2 bytes.  A and B use the same K order, so the dot
+// products are those of the byte packs.
+template <bool kF4>
 __global__ void __launch_bounds__(256) pack_kernel(const uint32_t* __restrict__ T, int32_t n, int64_t Wp, int32_t np,
                                                    uint8_t* T8, uint8_t* T8T, uint8_t* occ, int32_t nt_tiles) {
     __shared__ uint32_t bits[kTM][4];
@@ -191,7 +221,36 @@ __global__ void __launch_bounds__(256) pack_kernel(const uint32_t* __restrict__ 
     for (int t = threadIdx.x; t < kTM * 4; t += 256) local_any |= bits[t >> 2][t & 3] != 0;
     if (local_any) any = 1;
     // row-major bytes: thread handles 16 consecutive columns of one row (4 uint4 stores per thread)
-    if (T8) {
+    if (T8 && kF4) {
+        // 16 columns -> 8 bytes: byte q = nibble(col 2q) | nibble(col 2q+1) << 4
+        const int64_t rb = np / 2;
+        for (int t = threadIdx.x; t < kTM * 8; t += 256) {
+            int r = t >> 3, c16 = t & 7;
+            uint32_t w = bits[r][c16 >> 1] >> ((c16 & 1) * 16);
+            uint32_t o[2] = {0, 0};
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                uint32_t b = ((w >> (2 * q)) & 1u) << 1 | ((w >> (2 * q + 1)) & 1u) << 5;
+                o[q >> 2] |= b << ((q & 3) * 8);
+            }
+            *reinterpret_cast<uint2*>(T8 + (size_t)(tI * kTM + r) * rb + (tK * kTM + c16 * 16) / 2) = make_uint2(o[0], o[1]);
+        }
+    }
+    if (T8T && kF4) {
+        // output row c (= column c of the tile), 16 consecutive source rows -> 8 bytes
+        const int64_t rb = np / 2;
+        for (int t = threadIdx.x; t < kTM * 8; t += 256) {
+            int c = t >> 3, r16 = t & 7;
+            uint32_t o[2] = {0, 0};
+#pragma unroll
+            for (int q = 0; q < 16; ++q) {
+                uint32_t b = (bits[r16 * 16 + q][c >> 5] >> (c & 31)) & 1u;
+                o[q >> 3] |= b << ((q & 7) * 4 + 1);
+            }
+            *reinterpret_cast<uint2*>(T8T + (size_t)(tK * kTM + c) * rb + (tI * kTM + r16 * 16) / 2) = make_uint2(o[0], o[1]);
+        }
+    }
+    if (T8 && !kF4) {
         for (int t = threadIdx.x; t < kTM * 8; t += 256) {
             int r = t >> 3, c16 = t & 7;   // columns c16*16 .. +15
             uint32_t w = bits[r][c16 >> 1] >> ((c16 & 1) * 16);
@@ -206,7 +265,7 @@ __global__ void __launch_bounds__(256) pack_kernel(const uint32_t* __restrict__ 
         }
     }
     // transposed bytes: output row c (= column c of the tile), 16 consecutive source rows
-    if (T8T) {
+    if (T8T && !kF4) {
         for (int t = threadIdx.x; t < kTM * 8; t += 256) {
             int c = t >> 3, r16 = t & 7;
             uint32_t o[4] = {0, 0, 0, 0};
@@ -239,13 +298,17 @@ __device__ __forceinline__ bool kblock_live(const DenseParams& p, const DenseRul
     return __ldg(oC + (size_t)K * p.nt_tiles + 2 * J) || __ldg(oC + (size_t)K * p.nt_tiles + 2 * J + 1);
 }
 
-// K block live for any of the kCl row tiles I0 .. I0+kCl-1 that exist (< i_hi)
-template <int kCl>
+// K block live for any of the kCl row tiles I0 .. I0+kCl-1 that exist (< i_hi).  kF4: a K
+// block is 256 elements deep (128 bytes of nibbles) = 128-tiles 2K and 2K+1.
+template <int kCl, bool kF4 = false>
 __device__ __forceinline__ bool kblock_live_group(const DenseParams& p, const DenseRule& r, int I0, int J, int K) {
     bool live = false;
 #pragma unroll
     for (int c = 0; c < kCl; ++c)
-        if (I0 + c < p.i_hi) live |= kblock_live(p, r, I0 + c, J, K);
+        if (I0 + c < p.i_hi) {
+            if (kF4) live |= kblock_live(p, r, I0 + c, J, 2 * K) || kblock_live(p, r, I0 + c, J, 2 * K + 1);
+            else live |= kblock_live(p, r, I0 + c, J, K);
+        }
     return live;
 }
 
@@ -270,7 +333,13 @@ __device__ __forceinline__ void tile_coords(const DenseParams& p, int t, int til
 // 128-row half and multicasts it into both CTAs' stage (half the B traffic from L2), and
 // every MMA commit arrives on both CTAs' empty barrier (a stage is refilled only when both
 // consumed it).  tmB's box is then 128 rows.
-template <int kCl>
+//
+// kF4 (kind::mxf4, unit scales): operands are e2m1 nibble packs (K block = 256 elements in
+// the same 128-byte swizzled rows), the f32 accumulator uses TMEM columns 0..255 (one
+// accumulator stage) and columns 256..319 hold the scale factors, all 1.0 (ue8m0 0x7F).
+// Every product term is 1.0 x 1.0 x 1 x 1 >= 0, so a sum is > 0 iff some term is, and the
+// threshold is exact at any magnitude (and the sums are exact integers below 2^24).
+template <int kCl, bool kF4 = false>
 __global__ void __launch_bounds__(kDenseThreads, 1)
     dense_kernel(DenseParams p, const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                  const int64_t* __restrict__ mapA_row, const int64_t* __restrict__ mapB_row) {
@@ -291,7 +360,8 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
     const int n_i = (p.i_hi - p.i_lo + kCl - 1) / kCl;   // (pairs of) row tiles
     const int tiles_per_nt = n_i * n_j;
     const int total_tiles = tiles_per_nt * p.n_out;
-    const int n_k = p.np / kTK;
+    const int n_k = kF4 ? p.np / (2 * kTK) : p.np / kTK;
+    constexpr int kAcc = kF4 ? 1 : 2;   // accumulator stages in TMEM
     const uint32_t crank = kCl == 2 ? cluster_ctarank() : 0u;
     const int unit = (int)blockIdx.x / kCl, n_units = (int)gridDim.x / kCl;
 
@@ -300,7 +370,7 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], kCl);   // one MMA commit per CTA of the cluster
         }
-        for (int a = 0; a < 2; ++a) {
+        for (int a = 0; a < kAcc; ++a) {
             mbar_init(&tmem_full[a], 1);
             mbar_init(&tmem_empty[a], 128);
         }
@@ -314,6 +384,18 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
     else __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_base_smem;
+    if (kF4) {
+        // scale factors = 1.0 in columns 256..319 of all 128 lanes (epilogue warps own the
+        // lane quarters), visible to the MMA issuer after the barrier
+        if (warp >= 2) {
+            const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
+            tmem_fill32(tmem_base + lane_base + 256u, kSfOne);
+            tmem_fill32(tmem_base + lane_base + 288u, kSfOne);
+        }
+        tc_fence_before();
+        __syncthreads();
+        tc_fence_after();
+    }
 
     if (warp == 0) {
         // ------------------------------- TMA producer -------------------------------
@@ -329,7 +411,7 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
                     const int64_t arow = __ldg(mapA_row + r.B) + (int64_t)I * kTM;
                     const int64_t brow = __ldg(mapB_row + r.C) + (int64_t)J * kTN;
                     for (int K = 0; K < n_k; ++K) {
-                        if (!kblock_live_group<kCl>(p, r, I0, J, K)) continue;
+                        if (!kblock_live_group<kCl, kF4>(p, r, I0, J, K)) continue;
                         mbar_wait(&empty[stage], phase ^ 1);
                         mbar_expect_tx(&full[stage], kStageBytes);
                         tma_load_2d(sA + stage * kABytes, &tmA, &full[stage], K * kTK, (int)arow);
@@ -348,7 +430,8 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
         }
     } else if (warp == 1) {
         // ------------------------------- MMA issuer -------------------------------
-        const uint32_t idesc = idesc_i8(kTM, kTN);
+        const uint32_t idesc = kF4 ? idesc_mxf4(kTM, kTN) : idesc_i8(kTM, kTN);
+        const uint32_t tsfa = tmem_base + 256u, tsfb = tmem_base + 288u;
         int stage = 0;
         uint32_t phase = 0;
         int as = 0;              // accumulator stage of this tile
@@ -366,8 +449,8 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
             for (int q = p.rule_ptr[o]; q < p.rule_ptr[o + 1]; ++q) {
                 const DenseRule r = p.rules[q];
                 for (int K = 0; K < n_k; ++K) {
-                    if (!kblock_live_group<kCl>(p, r, I0, J, K)) continue;
-                    ++kb_issued;
+                    if (!kblock_live_group<kCl, kF4>(p, r, I0, J, K)) continue;
+                    kb_issued += kF4 ? 2 : 1;   // in 128-deep K units
                     mbar_wait(&full[stage], phase);
                     tc_fence_after();
                     if (lane == 0) {
@@ -375,8 +458,13 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
                         const uint32_t b0 = smem_u32(sB + stage * kBBytes);
 #pragma unroll
                         for (int kk = 0; kk < kTK / kUK; ++kk) {
-                            umma_i8(tmem_acc, kmajor_sw128_desc(a0 + kk * kUK), kmajor_sw128_desc(b0 + kk * kUK),
-                                    idesc, acc);
+                            // 32 bytes of K per instruction: 32 int8 or 64 e2m1 elements
+                            if (kF4)
+                                umma_mxf4(tmem_acc, kmajor_sw128_desc(a0 + kk * kUK), kmajor_sw128_desc(b0 + kk * kUK),
+                                          idesc, acc, tsfa, tsfb);
+                            else
+                                umma_i8(tmem_acc, kmajor_sw128_desc(a0 + kk * kUK), kmajor_sw128_desc(b0 + kk * kUK),
+                                        idesc, acc);
                             acc = 1;
                         }
                         // frees the smem stage (in both CTAs of a pair) when these MMAs finish
@@ -396,7 +484,7 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
                 else mbar_arrive(&tmem_full[as]);       // no live K block: the epilogue uses zeros
             }
             __syncwarp();
-            if (++as == 2) {
+            if (++as == kAcc) {
                 as = 0;
                 tphase ^= 1;
             }
@@ -415,7 +503,7 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
             const int A = p.out_nt[o];
             bool live = false;   // the pair issued MMAs for this tile (else TMEM holds no result)
             for (int q = p.rule_ptr[o]; q < p.rule_ptr[o + 1] && !live; ++q)
-                for (int K = 0; K < n_k && !live; ++K) live = kblock_live_group<kCl>(p, p.rules[q], I0, J, K);
+                for (int K = 0; K < n_k && !live; ++K) live = kblock_live_group<kCl, kF4>(p, p.rules[q], I0, J, K);
             // this row's 8 old words (32 contiguous bytes of T_{k-1}) load while the MMAs run
             const int row = I * kTM + quarter * 32 + lane;
             const bool wr = mine && row < p.n;
@@ -441,6 +529,13 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
                         if (q == c) w[q] = word;
                 }
             }
+            // the accumulator is in registers: hand TMEM back to the MMA issuer before the stores
+            tc_fence_before();
+            mbar_arrive(&tmem_empty[as]);
+            if (++as == kAcc) {
+                as = 0;
+                tphase ^= 1;
+            }
             unsigned long long cnt = 0;
             if (wr) {
                 const uint32_t old[8] = {o0.x, o0.y, o0.z, o0.w, o1.x, o1.y, o1.z, o1.w};
@@ -453,12 +548,6 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
                 uint4* dst = reinterpret_cast<uint4*>(p.Tn[A] + (size_t)row * p.Wp + (size_t)J * (kTN / 32));
                 dst[0] = make_uint4(nw[0], nw[1], nw[2], nw[3]);
                 dst[1] = make_uint4(nw[4], nw[5], nw[6], nw[7]);
-            }
-            tc_fence_before();
-            mbar_arrive(&tmem_empty[as]);
-            if (++as == 2) {
-                as = 0;
-                tphase ^= 1;
             }
 #pragma unroll
             for (int s = 16; s > 0; s >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, s);
@@ -475,106 +564,296 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
 }
 
 // ------------------------------------------------------------------------------------------
-// Bit-row path (CUDA cores, path_policy 3): the same Jacobi product on packed rows,
-//   T_k,A[i] = T_{k-1},A[i] | OR_{A->BC} OR_{r : T_B[i] has bit r} T_C[r]
-// T_k starts as a copy of T_{k-1}.  Work is balanced by chunks: a pre-pass lists, for every
-// (output rule, row i) with a non-empty row of T_B, chunks of <= kChunk set bits; a CTA
-// takes a chunk, ORs the kChunk rows T_C[r] (128-bit loads) into a register accumulator
-// and atomically ORs it into row i of T_k; the bits the atomics flip are exactly the new
-// cells (hub rows, e.g. type^-1 of owl:Class with ~n/2 set bits, are spread over CTAs).
-// Algorithmic bytes per (row, rule): 4Wn (row of T_B) + popc·4Wn (rows of T_C); per output
-// row 8Wn (copy T_{k-1} -> T_k): the full-operand traffic of SURVEY §8(d).
+// Bit-row path (CUDA cores, path_policy 3): Alg. 1 line 9 as written — every iteration the
+// FULL Jacobi product T_{k-1} x T_{k-1} (not only Δ), over packed rows:
+//   T_k,A[i] = T_{k-1},A[i] | OR_{A->BC} OR_{r : T_B[i][r]} T_C[r]
+// Each rule is evaluated in the form its operands allow (preterminals are constant after
+// seeding and have CSR rows):
+//   L  B changes, C preterminal : scan the bit row T_B[i], scatter CSR_C(r) into row i
+//   R  B preterminal, C changes : OR the bit rows T_C[r], r in CSR_B(i), into row i
+//   V  both change              : OR the bit rows T_C[r], r a set bit of T_B[i], into row i
+//   P  both preterminal         : CSR_B(i) x CSR_C(r); constant, so iteration 1 only
+// Empty rows are skipped through per-row popcounts cnt[X][i] of the current T (grown in
+// place by the merges: a count read during iteration k is >= that of T_{k-1}, and a row
+// that gained bits only in T_k is still empty in the T_{k-1} buffer that is read).
+// Merges are atomicOr into row i of T_k (after a plain-load pre-check); the bits an atomic
+// flips are exactly the new cells: they are counted, added to cnt, and appended as
+// (A, i, word, bits) to the word list Δ_k.  T_k is built in the buffer that held T_{k-2}:
+// it starts as T_{k-2} | Δ_{k-1} (= T_{k-1}), a scatter of the word list instead of a
+// copy of whole matrices (a full copy only if the list overflowed); at iteration 1 the
+// zeroed buffer takes the seed cells from the log.
 // ------------------------------------------------------------------------------------------
 constexpr int kRowThreads = 256;
-constexpr int kChunk = 128;
-constexpr int kRowMaxV4 = 8;   // uint4 accumulators per thread: rows up to 8*4*32*256 = 262144 bits
+constexpr int kChunk = 128;     // set bits of T_B[i] per V chunk
+constexpr int kChunkR = 32;     // CSR_B(i) entries per R chunk
+constexpr int kRowMaxV4 = 8;    // uint4 accumulators per thread: rows up to 8*4*32*256 = 262144 bits
 
 struct RowChunk {
     int32_t rule;   // index into rules (output o implied)
     int32_t row;
-    int32_t first;  // rank of the first set bit of this chunk
+    int32_t first;  // V: rank of the first set bit; R: first CSR_B(i) entry
     int32_t count;
 };
 
-// one warp per (rule, row): popcount of row i of T_B, append its chunks
-__global__ void rows_plan_kernel(DenseParams p, const int32_t* __restrict__ rule_out, int32_t n_rules,
-                                 RowChunk* chunks, unsigned long long* n_chunks, unsigned long long cap) {
+// Δ_k word list and counters of the bit-row path
+struct RowsCtx {
+    const NTInfo* nt;                  // is_const, csr_ptr per NT
+    const int32_t* adj_idx;            // CSR index array
+    uint32_t* cnt;                     // [n_nt][n] popcount of row i of the current T_X
+    uint4* dlist;                      // {A, i, word, bits}
+    unsigned long long dlist_cap;
+    unsigned long long* rc;            // [0] chunks, [1] dlist entries, [2] dlist overflowed (sticky)
+    int32_t first;                     // iteration 1 (both-preterminal rules evaluated)
+    int32_t n_rules;
+};
+
+enum : int { RF_NONE = 0, RF_L = 1, RF_R = 2, RF_V = 3, RF_P = 4 };
+
+__device__ __forceinline__ int row_form(const RowsCtx& c, const DenseRule& r) {
+    const bool bc = c.nt[r.B].is_const, cc = c.nt[r.C].is_const;
+    if (!bc && cc) return RF_L;
+    if (bc && !cc) return RF_R;
+    if (!bc && !cc) return RF_V;
+    return c.first ? RF_P : RF_NONE;
+}
+
+// OR `bits` into word w of row i of T_k,A; record what flips.  Warp-aggregated list append.
+__device__ __forceinline__ void rows_merge(const DenseParams& p, const RowsCtx& c, int A, int i, int64_t w,
+                                           uint32_t bits, unsigned long long& my_new) {
+    uint32_t* addr = p.Tn[A] + (size_t)i * p.Wp + w;
+    uint32_t fl = 0;
+    if (bits & ~*addr) fl = bits & ~atomicOr(addr, bits);   // bits never clear: a stale load only costs the atomic
+    const unsigned m = __activemask();
+    const unsigned want = __ballot_sync(m, fl != 0);
+    if (!fl) return;
     const int lane = threadIdx.x & 31;
-    const int64_t wn = (p.n + 31) / 32;
-    const int64_t tasks = (int64_t)n_rules * p.n;
-    for (int64_t t = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; t < tasks;
-         t += ((int64_t)gridDim.x * blockDim.x) >> 5) {
-        const int q = (int)(t / p.n);
-        const int64_t i = t - (int64_t)q * p.n;
-        const uint32_t* rowB = p.T[p.rules[q].B] + (size_t)i * p.Wp;
-        int c = 0;
-        for (int64_t w = lane; w < wn; w += 32) c += __popc(__ldg(rowB + w));
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-        const int nch = (c + kChunk - 1) / kChunk;
-        if (lane == 0 && nch) {
-            unsigned long long at = atomicAdd(n_chunks, (unsigned long long)nch);
-            for (int h = 0; h < nch && at + h < cap; ++h)
-                chunks[at + h] = RowChunk{q, (int32_t)i, h * kChunk, min(kChunk, c - h * kChunk)};
-        }
+    const int leader = __ffs(want) - 1;
+    unsigned long long base = 0;
+    if (lane == leader) base = atomicAdd(c.rc + 1, (unsigned long long)__popc(want));
+    base = __shfl_sync(want, base, leader);
+    const unsigned long long at = base + __popc(want & ((1u << lane) - 1u));
+    if (at < c.dlist_cap) c.dlist[at] = make_uint4((uint32_t)A, (uint32_t)i, (uint32_t)w, fl);
+    atomicAdd(c.cnt + (size_t)A * p.n + i, (uint32_t)__popc(fl));
+    my_new += __popc(fl);
+}
+
+// Iteration 1: the zeroed T_k buffers take T_0 (the seed cells of the outputs, from the
+// log) and cnt[X][i] = |row i of T_0,X| for every NT.
+__global__ void rows_seed_kernel(DenseParams p, RowsCtx c, const uint64_t* __restrict__ log, unsigned long long n_seeds) {
+    for (unsigned long long e = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; e < n_seeds;
+         e += (unsigned long long)gridDim.x * blockDim.x) {
+        const uint64_t cell = log[e];
+        const uint32_t A = cell_nt(cell), i = cell_i(cell), j = cell_j(cell);
+        atomicAdd(c.cnt + (size_t)A * p.n + i, 1u);
+        if (p.Tn[A]) atomicOr(p.Tn[A] + (size_t)i * p.Wp + (j >> 5), 1u << (j & 31));
     }
 }
 
-__global__ void __launch_bounds__(kRowThreads) rows_kernel(DenseParams p, const int32_t* __restrict__ rule_out,
-                                                          const RowChunk* __restrict__ chunks,
-                                                          const unsigned long long* n_chunks) {
+// Iteration k > 1: T_k buffer (holding T_{k-2}) |= Δ_{k-1} words; after an overflowed list,
+// copy T_{k-1} whole (and flag it for the host to grow the list).
+__global__ void rows_delta_kernel(DenseParams p, RowsCtx c) {
+    const unsigned long long m = c.rc[1];
+    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+    const unsigned long long t0 = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x;
+    if (m <= c.dlist_cap) {
+        for (unsigned long long e = t0; e < m; e += stride) {
+            const uint4 d = c.dlist[e];
+            atomicOr(p.Tn[d.x] + (size_t)d.y * p.Wp + d.z, d.w);
+        }
+        return;
+    }
+    if (t0 == 0) c.rc[2] = 1;
+    const unsigned long long words4 = (unsigned long long)p.n * p.Wp / 4;
+    for (int o = 0; o < p.n_out; ++o) {
+        const int A = p.out_nt[o];
+        const uint4* src = reinterpret_cast<const uint4*>(p.T[A]);
+        uint4* dst = reinterpret_cast<uint4*>(p.Tn[A]);
+        for (unsigned long long e = t0; e < words4; e += stride) dst[e] = src[e];
+    }
+}
+
+// Work list of the R and V forms: chunks of <= kChunkR CSR_B(i) entries / kChunk set bits
+// of T_B[i] per (rule, row), warp-aggregated appends.
+__global__ void rows_plan_kernel(DenseParams p, RowsCtx c, RowChunk* chunks, unsigned long long cap) {
+    const int lane = threadIdx.x & 31;
+    const int64_t tasks = (int64_t)c.n_rules * p.n;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t t0 = blockIdx.x * (int64_t)blockDim.x; t0 < tasks; t0 += stride) {
+        const int64_t t = t0 + threadIdx.x;
+        int nch = 0, q = 0, i = 0, per = 1, len = 0;
+        if (t < tasks) {
+            q = (int)(t / p.n);
+            i = (int)(t - (int64_t)q * p.n);
+            const DenseRule r = p.rules[q];
+            const int f = row_form(c, r);
+            if (f == RF_R) {
+                const int32_t* ptr = c.nt[r.B].csr_ptr;
+                len = __ldg(ptr + i + 1) - __ldg(ptr + i);
+                per = kChunkR;
+            } else if (f == RF_V) {
+                len = (int)c.cnt[(size_t)r.B * p.n + i];
+                per = kChunk;
+            }
+            nch = (len + per - 1) / per;
+        }
+        int incl = nch;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            int v = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += v;
+        }
+        unsigned long long base = 0;
+        if (lane == 31 && incl) base = atomicAdd(c.rc, (unsigned long long)incl);
+        base = __shfl_sync(0xffffffffu, base, 31);
+        unsigned long long at = base + (unsigned long long)(incl - nch);
+        for (int h = 0; h < nch; ++h, ++at)
+            if (at < cap) chunks[at] = RowChunk{q, i, h * per, min(per, len - h * per)};
+    }
+}
+
+// Forms L and P: one warp per (row, rule) — rules of one row are adjacent, so the bit row
+// T_B[i] read for several rules comes from L1/L2.
+__global__ void __launch_bounds__(256) rows_scatter_kernel(DenseParams p, RowsCtx c, const int32_t* __restrict__ rule_out) {
+    const int lane = threadIdx.x & 31;
+    const int64_t wn = (p.n + 31) / 32;
+    const int64_t tasks = (int64_t)c.n_rules * p.n;
+    unsigned long long my_new = 0;
+    for (int64_t t = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; t < tasks;
+         t += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const int i = (int)(t / c.n_rules);
+        const int q = (int)(t - (int64_t)i * c.n_rules);
+        const DenseRule r = p.rules[q];
+        const int f = row_form(c, r);
+        if (f != RF_L && f != RF_P) continue;
+        const int A = rule_out[q];
+        const int32_t* cptr = c.nt[r.C].csr_ptr;
+        if (f == RF_L) {
+            if (c.cnt[(size_t)r.B * p.n + i] == 0) continue;
+            const uint4* rowB = reinterpret_cast<const uint4*>(p.T[r.B] + (size_t)i * p.Wp);
+            for (int64_t v = lane; v * 4 < wn; v += 32) {
+                const uint4 x = __ldg(rowB + v);
+                const uint32_t ws[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+                for (int h = 0; h < 4; ++h) {
+                    uint32_t bits = ws[h];
+                    while (bits) {
+                        const int rr = (int)((v * 4 + h) * 32) + __ffs(bits) - 1;
+                        bits &= bits - 1u;
+                        const int e1 = __ldg(cptr + rr + 1);
+                        for (int e = __ldg(cptr + rr); e < e1; ++e) {
+                            const int j = __ldg(c.adj_idx + e);
+                            rows_merge(p, c, A, i, j >> 5, 1u << (j & 31), my_new);
+                        }
+                    }
+                }
+            }
+        } else {
+            const int32_t* bptr = c.nt[r.B].csr_ptr;
+            const int b1 = __ldg(bptr + i + 1);
+            for (int e = __ldg(bptr + i) + lane; e < b1; e += 32) {
+                const int rr = __ldg(c.adj_idx + e);
+                const int e1 = __ldg(cptr + rr + 1);
+                for (int f2 = __ldg(cptr + rr); f2 < e1; ++f2) {
+                    const int j = __ldg(c.adj_idx + f2);
+                    rows_merge(p, c, A, i, j >> 5, 1u << (j & 31), my_new);
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) my_new += __shfl_xor_sync(0xffffffffu, my_new, o);
+    if (lane == 0 && my_new) atomicAdd(p.new_cells + p.n_nt, my_new);
+}
+
+// Forms R and V: one CTA per chunk ORs the chunk's bit rows T_C[r] (128-bit loads, 4 rows
+// in flight per thread) into a register accumulator and merges its non-zero words.
+__global__ void __launch_bounds__(kRowThreads) rows_gather_kernel(DenseParams p, RowsCtx c,
+                                                                 const int32_t* __restrict__ rule_out,
+                                                                 const RowChunk* __restrict__ chunks) {
     __shared__ int32_t list[kChunk];
     __shared__ int32_t wsum[kRowThreads / 32];
+    __shared__ int32_t n_list;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t wn = (p.n + 31) / 32;
     const int64_t nv4 = (wn + 3) / 4;
-    const unsigned long long m = *n_chunks;
+    const unsigned long long m = c.rc[0];
     unsigned long long my_new = 0;
-    for (unsigned long long c = blockIdx.x; c < m; c += gridDim.x) {
-        const RowChunk ch = chunks[c];
+    for (unsigned long long ci = blockIdx.x; ci < m; ci += gridDim.x) {
+        const RowChunk ch = chunks[ci];
         const DenseRule r = p.rules[ch.rule];
-        const uint32_t* rowB = p.T[r.B] + (size_t)ch.row * p.Wp;
-        // select the set bits of rank [first, first+count): walk the row in 256-word slices
-        int base = 0;   // set bits before the current slice
-        for (int64_t w0 = 0; w0 < wn && base < ch.first + ch.count; w0 += kRowThreads) {
-            int64_t w = w0 + threadIdx.x;
-            uint32_t bits = w < wn ? __ldg(rowB + w) : 0u;
-            int pc = __popc(bits);
-            int incl = pc;
+        const uint32_t* TC = p.T[r.C];
+        const uint32_t* cntC = c.cnt + (size_t)r.C * p.n;
+        if (threadIdx.x == 0) n_list = 0;
+        __syncthreads();
+        if (!c.nt[r.B].is_const) {
+            // V: the set bits of rank [first, first+count) of T_B[i], walked in 256-word slices
+            const uint32_t* rowB = p.T[r.B] + (size_t)ch.row * p.Wp;
+            int base = 0;
+            for (int64_t w0 = 0; w0 < wn && base < ch.first + ch.count; w0 += kRowThreads) {
+                int64_t w = w0 + threadIdx.x;
+                uint32_t bits = w < wn ? __ldg(rowB + w) : 0u;
+                int pc = __popc(bits);
+                int incl = pc;
 #pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                int v = __shfl_up_sync(0xffffffffu, incl, o);
-                if (lane >= o) incl += v;
+                for (int o = 1; o < 32; o <<= 1) {
+                    int v = __shfl_up_sync(0xffffffffu, incl, o);
+                    if (lane >= o) incl += v;
+                }
+                if (lane == 31) wsum[warp] = incl;
+                __syncthreads();
+                int before = 0, total = 0;
+                for (int q = 0; q < kRowThreads / 32; ++q) {
+                    if (q < warp) before += wsum[q];
+                    total += wsum[q];
+                }
+                int rank = base + before + incl - pc;
+                while (bits) {
+                    int b = __ffs(bits) - 1;
+                    bits &= bits - 1u;
+                    if (rank >= ch.first && rank < ch.first + ch.count) list[rank - ch.first] = (int32_t)(w * 32 + b);
+                    ++rank;
+                }
+                base += total;
+                __syncthreads();
             }
-            if (lane == 31) wsum[warp] = incl;
-            __syncthreads();
-            int before = 0, total = 0;
-            for (int q = 0; q < kRowThreads / 32; ++q) {
-                if (q < warp) before += wsum[q];
-                total += wsum[q];
+            if (threadIdx.x == 0) n_list = ch.count;
+        } else {
+            // R: CSR_B(i) entries [first, first+count), rows of T_C that are empty skipped
+            if (threadIdx.x < ch.count) {
+                const int rr = __ldg(c.adj_idx + __ldg(c.nt[r.B].csr_ptr + ch.row) + ch.first + threadIdx.x);
+                if (cntC[rr]) list[atomicAdd(&n_list, 1)] = rr;
             }
-            int rank = base + before + incl - pc;   // rank of this word's first set bit
-            while (bits) {
-                int b = __ffs(bits) - 1;
-                bits &= bits - 1u;
-                if (rank >= ch.first && rank < ch.first + ch.count) list[rank - ch.first] = (int32_t)(w * 32 + b);
-                ++rank;
-            }
-            base += total;
-            __syncthreads();
         }
-        // OR the selected rows of T_C
+        __syncthreads();
+        const int nl = n_list;
         uint4 acc[kRowMaxV4];
 #pragma unroll
         for (int v = 0; v < kRowMaxV4; ++v) acc[v] = make_uint4(0, 0, 0, 0);
-        const uint32_t* TC = p.T[r.C];
-        for (int e = 0; e < ch.count; ++e) {
-            const uint4* rowC = reinterpret_cast<const uint4*>(TC + (size_t)list[e] * p.Wp);
+        int e = 0;
+        for (; e + 4 <= nl; e += 4) {
+            const uint4* r0 = reinterpret_cast<const uint4*>(TC + (size_t)list[e] * p.Wp);
+            const uint4* r1 = reinterpret_cast<const uint4*>(TC + (size_t)list[e + 1] * p.Wp);
+            const uint4* r2 = reinterpret_cast<const uint4*>(TC + (size_t)list[e + 2] * p.Wp);
+            const uint4* r3 = reinterpret_cast<const uint4*>(TC + (size_t)list[e + 3] * p.Wp);
 #pragma unroll
             for (int v = 0; v < kRowMaxV4; ++v) {
                 int64_t g = (int64_t)v * kRowThreads + threadIdx.x;
                 if (g < nv4) {
-                    uint4 x = __ldg(rowC + g);
+                    const uint4 x0 = __ldg(r0 + g), x1 = __ldg(r1 + g), x2 = __ldg(r2 + g), x3 = __ldg(r3 + g);
+                    acc[v].x |= x0.x | x1.x | x2.x | x3.x;
+                    acc[v].y |= x0.y | x1.y | x2.y | x3.y;
+                    acc[v].z |= x0.z | x1.z | x2.z | x3.z;
+                    acc[v].w |= x0.w | x1.w | x2.w | x3.w;
+                }
+            }
+        }
+        for (; e < nl; ++e) {
+            const uint4* r0 = reinterpret_cast<const uint4*>(TC + (size_t)list[e] * p.Wp);
+#pragma unroll
+            for (int v = 0; v < kRowMaxV4; ++v) {
+                int64_t g = (int64_t)v * kRowThreads + threadIdx.x;
+                if (g < nv4) {
+                    const uint4 x = __ldg(r0 + g);
                     acc[v].x |= x.x;
                     acc[v].y |= x.y;
                     acc[v].z |= x.z;
@@ -582,16 +861,15 @@ __global__ void __launch_bounds__(kRowThreads) rows_kernel(DenseParams p, const 
                 }
             }
         }
-        // merge into row i of T_k; the flipped bits are the new cells
-        uint32_t* rowNew = p.Tn[rule_out[ch.rule]] + (size_t)ch.row * p.Wp;
+        const int A = rule_out[ch.rule];
 #pragma unroll
         for (int v = 0; v < kRowMaxV4; ++v) {
             int64_t g = (int64_t)v * kRowThreads + threadIdx.x;
             if (g < nv4) {
-                uint32_t a[4] = {acc[v].x, acc[v].y, acc[v].z, acc[v].w};
+                const uint32_t a[4] = {acc[v].x, acc[v].y, acc[v].z, acc[v].w};
 #pragma unroll
                 for (int q = 0; q < 4; ++q)
-                    if (a[q]) my_new += __popc(a[q] & ~atomicOr(rowNew + 4 * g + q, a[q]));
+                    if (a[q]) rows_merge(p, c, A, ch.row, 4 * g + q, a[q], my_new);
             }
         }
         __syncthreads();
@@ -616,12 +894,12 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
     return fn;
 }
 
-// 2D uint8 tensor [rows][np] with a (128 x box_rows) box, 128B swizzle.
-static bool make_map(CUtensorMap* m, const uint8_t* base, int64_t rows, int64_t np, int box_rows) {
+// 2D uint8 tensor [rows][row_bytes] with a (128 x box_rows) box, 128B swizzle.
+static bool make_map(CUtensorMap* m, const uint8_t* base, int64_t rows, int64_t row_bytes, int box_rows) {
     auto enc = get_encode();
     if (!enc) return false;
-    cuuint64_t dims[2] = {(cuuint64_t)np, (cuuint64_t)rows};
-    cuuint64_t strides[1] = {(cuuint64_t)np};
+    cuuint64_t dims[2] = {(cuuint64_t)row_bytes, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)row_bytes};
     cuuint32_t box[2] = {(cuuint32_t)kTK, (cuuint32_t)box_rows};
     cuuint32_t estr[2] = {1, 1};
     CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, (void*)base, dims, strides, box, estr,
@@ -635,6 +913,7 @@ size_t dense_smem_bytes() { return (size_t)kStages * kStageBytes + 1024 + 256; }
 struct DenseEngine {
     int32_t n = 0, np = 0, nt_tiles = 0, n_nt = 0;
     int64_t Wp = 0;
+    bool fp4 = false;                              // kind::mxf4 e2m1 packs instead of int8
     std::vector<int32_t> is_const, packA, packB;   // packA[X]: X is a left operand (T8), packB: right (T8T)
     std::vector<int64_t> h_mapA, h_mapB;
     uint8_t* T8 = nullptr;
@@ -658,10 +937,17 @@ struct DenseEngine {
     std::vector<int32_t> h_rule_out;
     void* chunks = nullptr;                    // bit-row path work list
     unsigned long long chunk_cap = 0;
+    uint32_t* rcnt = nullptr;                  // bit-row path: per NT row popcounts
+    void* dlist = nullptr;                     // bit-row path: Δ_k word list (uint4)
+    unsigned long long dlist_cap = 0;
+    unsigned long long* rc = nullptr;          // bit-row path counters
     ~DenseEngine() {
         cudaFree(cnt);
         cudaFree(rule_out);
         cudaFree(chunks);
+        cudaFree(rcnt);
+        cudaFree(dlist);
+        cudaFree(rc);
         cudaFree(T8); cudaFree(T8T); cudaFree(occ); cudaFree(mapA_row); cudaFree(mapB_row); cudaFree(out_nt);
         cudaFree(rule_ptr); cudaFree(rules); cudaFree(Tptr); cudaFree(Tnptr); cudaFree(new_cells);
     }
@@ -670,8 +956,10 @@ struct DenseEngine {
 void dense_destroy(DenseEngine* e) { delete e; }
 
 DenseEngine* dense_create(int32_t n, int32_t n_nt, int64_t Wp, const std::vector<Rule3>& rules,
-                          const std::vector<int32_t>& is_const, cudaStream_t s, std::string* err, bool tensor) {
+                          const std::vector<int32_t>& is_const, cudaStream_t s, std::string* err, bool tensor,
+                          bool fp4) {
     DenseEngine* e = new DenseEngine();
+    e->fp4 = fp4;
     e->n = n;
     e->n_nt = n_nt;
     e->Wp = Wp;
@@ -736,9 +1024,10 @@ DenseEngine* dense_create(int32_t n, int32_t n_nt, int64_t Wp, const std::vector
     if ((c = cudaMalloc(&e->rule_out, std::max<size_t>(1, rl.size()) * 4)) != cudaSuccess) return fail("tables", c);
     if (!rl.empty())
         cudaMemcpyAsync(e->rule_out, e->h_rule_out.data(), rl.size() * 4, cudaMemcpyHostToDevice, s);
-    if (!make_map(&e->tmA, e->T8, (int64_t)std::max(na, 1) * e->np, e->np, kTM) ||
-        !make_map(&e->tmB, e->T8T, (int64_t)std::max(nb, 1) * e->np, e->np, kTN) ||
-        !make_map(&e->tmBh, e->T8T, (int64_t)std::max(nb, 1) * e->np, e->np, kTN / 2)) {
+    const int64_t row_bytes = fp4 ? e->np / 2 : e->np;   // nibble packs: half the bytes per row
+    if (!make_map(&e->tmA, e->T8, (int64_t)std::max(na, 1) * e->np, row_bytes, kTM) ||
+        !make_map(&e->tmB, e->T8T, (int64_t)std::max(nb, 1) * e->np, row_bytes, kTN) ||
+        !make_map(&e->tmBh, e->T8T, (int64_t)std::max(nb, 1) * e->np, row_bytes, kTN / 2)) {
         if (err) *err = "dense engine: cuTensorMapEncodeTiled failed";
         delete e;
         return nullptr;
@@ -751,6 +1040,9 @@ DenseEngine* dense_create(int32_t n, int32_t n_nt, int64_t Wp, const std::vector
     }
     if ((c = cudaFuncSetAttribute(dense_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dense_smem_bytes())) !=
         cudaSuccess)
+        return fail("smem attribute", c);
+    if ((c = cudaFuncSetAttribute(dense_kernel<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)dense_smem_bytes())) != cudaSuccess)
         return fail("smem attribute", c);
     int dev = 0, sms = 0;
     cudaGetDevice(&dev);
@@ -766,15 +1058,16 @@ DenseEngine* dense_create(int32_t n, int32_t n_nt, int64_t Wp, const std::vector
 // counters (device -> host).
 cudaError_t dense_begin(DenseEngine* e, uint32_t* const* T, uint32_t* const* Tn, bool first, cudaStream_t s,
                         int* launches, bool pack_operands) {
-    const size_t pack = (size_t)e->np * e->np;
+    const size_t pack = (size_t)e->np * e->np / (e->fp4 ? 2 : 1);   // bytes per packed NT
     for (int X = 0; X < e->n_nt && pack_operands; ++X) {
         if (!(e->packA[X] || e->packB[X])) continue;
         if (!first && e->is_const[X]) continue;   // preterminals never change after seeding
         uint8_t* a = e->packA[X] ? e->T8 + (size_t)(e->h_mapA[X] / e->np) * pack : nullptr;
         uint8_t* b = e->packB[X] ? e->T8T + (size_t)(e->h_mapB[X] / e->np) * pack : nullptr;
         dim3 grid(e->nt_tiles, e->nt_tiles);
-        pack_kernel<<<grid, 256, 0, s>>>(T[X], e->n, e->Wp, e->np, a, b,
-                                         e->occ + (size_t)X * e->nt_tiles * e->nt_tiles, e->nt_tiles);
+        uint8_t* oc = e->occ + (size_t)X * e->nt_tiles * e->nt_tiles;
+        if (e->fp4) pack_kernel<true><<<grid, 256, 0, s>>>(T[X], e->n, e->Wp, e->np, a, b, oc, e->nt_tiles);
+        else pack_kernel<false><<<grid, 256, 0, s>>>(T[X], e->n, e->Wp, e->np, a, b, oc, e->nt_tiles);
         if (launches) ++*launches;
     }
     cudaError_t c;
@@ -814,7 +1107,7 @@ cudaError_t dense_product(DenseEngine* e, int64_t i_lo, int64_t i_hi, cudaStream
         const char* v = getenv("CFPQ_DENSE_PAIR");
         return v && v[0] == '1';
     }();
-    if (pair && sms >= 2) {
+    if (pair && sms >= 2 && !e->fp4) {
         // CTA pairs (clusters of 2) share the B tile through TMA multicast
         const int64_t units = (int64_t)e->n_out * ((i_hi - i_lo + 1) / 2) * (e->np / kTN);
         const int grid = (int)std::max<int64_t>(2, std::min<int64_t>(sms / 2, units) * 2);
@@ -837,24 +1130,34 @@ cudaError_t dense_product(DenseEngine* e, int64_t i_lo, int64_t i_hi, cudaStream
     }
     const int64_t total = (int64_t)e->n_out * (i_hi - i_lo) * (e->np / kTN);
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(sms, total));
-    dense_kernel<1><<<grid, kDenseThreads, dense_smem_bytes(), s>>>(p, e->tmA, e->tmB, e->mapA_row, e->mapB_row);
+    if (e->fp4)
+        dense_kernel<1, true><<<grid, kDenseThreads, dense_smem_bytes(), s>>>(p, e->tmA, e->tmB, e->mapA_row, e->mapB_row);
+    else
+        dense_kernel<1><<<grid, kDenseThreads, dense_smem_bytes(), s>>>(p, e->tmA, e->tmB, e->mapA_row, e->mapB_row);
     if (launches) ++*launches;
     return cudaGetLastError();
 }
 
-cudaError_t rows_product(DenseEngine* e, uint32_t* const* T, uint32_t* const* Tn, cudaStream_t s, int* launches) {
+cudaError_t rows_product(DenseEngine* e, uint32_t* const* T, uint32_t* const* Tn, const NTInfo* nt,
+                         const int32_t* adj_idx, const uint64_t* log, unsigned long long n_seeds, bool first,
+                         cudaStream_t s, int* launches) {
+    (void)T;
+    (void)Tn;   // the kernels read the device copies set by dense_begin
     if (e->n_out == 0) return cudaSuccess;
     if ((e->n + 31) / 32 > (int64_t)kRowMaxV4 * 4 * kRowThreads) return cudaErrorInvalidValue;
     cudaError_t c;
-    // T_k starts as T_{k-1} (the BMU term of P:241)
-    for (int A : e->h_out)
-        if ((c = cudaMemcpyAsync(Tn[A], T[A], (size_t)e->n * e->Wp * 4, cudaMemcpyDeviceToDevice, s)) != cudaSuccess)
-            return c;
     const int32_t n_rules = (int32_t)e->h_rule_out.size();
-    // chunk capacity: each (rule, row) has at most ceil(n / kChunk) chunks; grow lazily
-    const unsigned long long worst = (unsigned long long)n_rules * e->n * ((e->n + kChunk - 1) / kChunk);
-    const unsigned long long want = std::min<unsigned long long>(worst, std::max<unsigned long long>(
-        e->chunk_cap, (unsigned long long)n_rules * e->n * 2 + 1024));
+    if (!e->rcnt) {
+        if ((c = cudaMalloc(&e->rcnt, (size_t)e->n_nt * std::max(e->n, 1) * 4)) != cudaSuccess) return c;
+        if ((c = cudaMalloc(&e->rc, 4 * 8)) != cudaSuccess) return c;
+        if ((c = cudaMemsetAsync(e->rc, 0, 4 * 8, s)) != cudaSuccess) return c;
+        // testing knob: a tiny list exercises the whole-matrix fallback after an overflow
+        const char* cap_env = getenv("CFPQ_ROWS_DLIST_CAP");
+        e->dlist_cap = cap_env ? std::max(1ull, strtoull(cap_env, nullptr, 10)) : (1ull << 20);
+        if ((c = cudaMalloc(&e->dlist, e->dlist_cap * sizeof(uint4))) != cudaSuccess) return c;
+    }
+    // chunk capacity: grow lazily (the plan reports the exact count)
+    const unsigned long long want = std::max<unsigned long long>(e->chunk_cap, (unsigned long long)n_rules * e->n + 1024);
     if (want > e->chunk_cap) {
         cudaFree(e->chunks);
         if ((c = cudaMalloc(&e->chunks, want * sizeof(RowChunk))) != cudaSuccess) return c;
@@ -872,22 +1175,48 @@ cudaError_t rows_product(DenseEngine* e, uint32_t* const* T, uint32_t* const* Tn
     p.Tn = e->Tnptr;
     p.new_cells = e->new_cells;
     p.n_nt = e->n_nt;
-    unsigned long long* nch = e->new_cells + e->n_nt + 1;   // reuse the k-block slot as the chunk counter
-    for (int attempt = 0; attempt < 2; ++attempt) {
-        if ((c = cudaMemsetAsync(nch, 0, 8, s)) != cudaSuccess) return c;
-        rows_plan_kernel<<<148 * 8, 256, 0, s>>>(p, e->rule_out, n_rules, (RowChunk*)e->chunks, nch, e->chunk_cap);
-        unsigned long long got = 0;
-        if ((c = cudaMemcpyAsync(&got, nch, 8, cudaMemcpyDeviceToHost, s)) != cudaSuccess) return c;
-        if ((c = cudaStreamSynchronize(s)) != cudaSuccess) return c;
-        if (got <= e->chunk_cap) break;
-        cudaFree(e->chunks);
-        e->chunk_cap = got + got / 4;
-        if ((c = cudaMalloc(&e->chunks, e->chunk_cap * sizeof(RowChunk))) != cudaSuccess) return c;
+    RowsCtx rc{nt, adj_idx, e->rcnt, (uint4*)e->dlist, e->dlist_cap, e->rc, first ? 1 : 0, n_rules};
+    int sms = 148;
+    {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     }
-    rows_kernel<<<148 * 8, kRowThreads, 0, s>>>(p, e->rule_out, (const RowChunk*)e->chunks, nch);
-    if (launches) *launches += 2;
-    if ((c = cudaGetLastError()) != cudaSuccess) return c;
-    return cudaMemsetAsync(nch, 0, 8, s);
+    // T_k buffer := T_{k-1}
+    if (first) {
+        if ((c = cudaMemsetAsync(e->rcnt, 0, (size_t)e->n_nt * e->n * 4, s)) != cudaSuccess) return c;
+        if ((c = cudaMemsetAsync(e->rc, 0, 4 * 8, s)) != cudaSuccess) return c;
+        if (n_seeds) rows_seed_kernel<<<sms * 8, 256, 0, s>>>(p, rc, log, n_seeds);
+    } else {
+        rows_delta_kernel<<<sms * 8, 256, 0, s>>>(p, rc);
+    }
+    // Δ_k list and chunk counter restart; plan
+    if ((c = cudaMemsetAsync(e->rc, 0, 2 * 8, s)) != cudaSuccess) return c;
+    for (int attempt = 0; attempt < 2; ++attempt) {
+        rows_plan_kernel<<<sms * 8, 256, 0, s>>>(p, rc, (RowChunk*)e->chunks, e->chunk_cap);
+        unsigned long long got[3] = {0, 0, 0};
+        if ((c = cudaMemcpyAsync(got, e->rc, 3 * 8, cudaMemcpyDeviceToHost, s)) != cudaSuccess) return c;
+        if ((c = cudaStreamSynchronize(s)) != cudaSuccess) return c;
+        if (got[2]) {
+            // the previous iteration's list overflowed (the delta kernel copied whole
+            // matrices instead): grow it for the next iterations
+            cudaFree(e->dlist);
+            e->dlist_cap *= 4;
+            if ((c = cudaMalloc(&e->dlist, e->dlist_cap * sizeof(uint4))) != cudaSuccess) return c;
+            rc.dlist = (uint4*)e->dlist;
+            rc.dlist_cap = e->dlist_cap;
+            if ((c = cudaMemsetAsync(e->rc + 2, 0, 8, s)) != cudaSuccess) return c;
+        }
+        if (got[0] <= e->chunk_cap) break;
+        cudaFree(e->chunks);
+        e->chunk_cap = got[0] + got[0] / 4;
+        if ((c = cudaMalloc(&e->chunks, e->chunk_cap * sizeof(RowChunk))) != cudaSuccess) return c;
+        if ((c = cudaMemsetAsync(e->rc, 0, 8, s)) != cudaSuccess) return c;
+    }
+    rows_scatter_kernel<<<sms * 8, 256, 0, s>>>(p, rc, e->rule_out);
+    rows_gather_kernel<<<sms * 8, kRowThreads, 0, s>>>(p, rc, e->rule_out, (const RowChunk*)e->chunks);
+    if (launches) *launches += 4;
+    return cudaGetLastError();
 }
 
 cudaError_t dense_finish(DenseEngine* e, cudaStream_t s, unsigned long long* new_total) {
@@ -903,6 +1232,7 @@ cudaError_t dense_finish(DenseEngine* e, cudaStream_t s, unsigned long long* new
 
 unsigned long long* dense_total_counter(DenseEngine* e) { return e->new_cells + e->n_nt; }
 int64_t dense_row_tiles(const DenseEngine* e) { return e->nt_tiles; }
+bool dense_is_fp4(const DenseEngine* e) { return e->fp4; }
 
 // Issued MMA k-blocks (128 x 256 x 128 int8 each) since the last reset.
 unsigned long long dense_kblocks(DenseEngine* e, bool reset) {

@@ -1,5 +1,7 @@
 """GPU parity of the bit-row CUDA-core path (path_policy = 3): the paper-faithful
-full-operand Jacobi products over packed rows (Alg. 1 line 9)."""
+full-operand Jacobi products over packed rows (Alg. 1 line 9).  Every product is
+recomputed from the whole T_{k-1}, so the per-iteration new-cell counts must equal the
+oracle's Jacobi states T_k exactly (not only the fixpoint)."""
 import pytest
 
 import inputs as I
@@ -22,7 +24,9 @@ def test_rows_random_and_dense():
     for s in range(40):
         w = I.random_workload(60_000 + s, max_nodes=60, max_edges=200, max_nt=5, max_bin=10, max_term=5)
         r, _, _ = gpu_closure(w, path_policy=3)
-        assert_parity(w, r)
+        ores = assert_parity(w, r)
+        nc, _ = r.iteration_stats()
+        assert nc.tolist() == ores.stats()["new_bits"].tolist(), w.name
     for n, d in ((100, 2), (257, 1), (300, 3)):
         w = I.dense_stress_workload(n, d, seed=n)
         r, _, _ = gpu_closure(w, path_policy=3)
@@ -35,7 +39,50 @@ def test_rows_random_and_dense():
 def test_rows_union_grammar(n):
     w = I.config4_workload(n=n)
     r, _, _ = gpu_closure(w, path_policy=3)
-    assert_parity(w, r)
+    ores = assert_parity(w, r)
+    nc, _ = r.iteration_stats()
+    assert nc.tolist() == ores.stats()["new_bits"].tolist()
+
+
+@pytest.mark.parametrize("query", ["q1", "q2"])
+def test_rows_ontology_and_reuse(query):
+    """Q1 / Q2 (forms L, R, P) and reuse of the result: the second run starts from the
+    cleared buffers and the seed cells again, on a different graph."""
+    from paper_1707_01007_b200 import cfpq as C
+    w = I.ontology_workload(query, 800, depth=7, seed=5)
+    g = C.Grammar.from_workload(w)
+    d = C.Graph(w.n_nodes, w.edges)
+    r = C.closure(g, d, path_policy=3)
+    ores = assert_parity(w, r)
+    nc, _ = r.iteration_stats()
+    assert nc.tolist() == ores.stats()["new_bits"].tolist()
+    w2 = I.ontology_workload(query, 800, depth=6, seed=6)
+    d.set_edges(w2.edges)
+    C.closure_reuse(g, d, r, path_policy=3)
+    ores2 = assert_parity(w2, r)
+    nc, _ = r.iteration_stats()
+    assert nc.tolist() == ores2.stats()["new_bits"].tolist()
+
+
+def test_rows_delta_list_overflow_fallback():
+    """A Δ word list that overflows makes the next iteration copy whole matrices instead
+    (and the list grows): same states.  CFPQ_ROWS_DLIST_CAP=8 forces it from iteration 1."""
+    import os
+    import subprocess
+    import sys
+    code = (
+        "import inputs as I\n"
+        "from tests.gpu_util import gpu_closure, assert_parity\n"
+        "for w in (I.config4_workload(n=1500), I.dense_stress_workload(200, 2, seed=1)):\n"
+        "    r, _, _ = gpu_closure(w, path_policy=3)\n"
+        "    o = assert_parity(w, r)\n"
+        "    nc, _ = r.iteration_stats()\n"
+        "    assert nc.tolist() == o.stats()['new_bits'].tolist()\n"
+        "print('ok')\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, CFPQ_ROWS_DLIST_CAP="8", PYTHONPATH=root)
+    out = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
 
 
 def test_rows_wide_rows_agree_with_sparse():

@@ -1,5 +1,7 @@
-"""GPU parity of the dense tensor-core engine (path_policy = 2: tcgen05 int8 MMA on 0/1
-tiles, TMA-staged, TMEM accumulators, thresholded to bits) against the oracle."""
+"""GPU parity of the dense tensor-core engine (path_policy = 2: tcgen05 MMA on 0/1 tiles,
+TMA-staged, TMEM accumulators, thresholded to bits) against the oracle, in both operand
+formats: tensor_format 1 = kind::i8 (s32 accumulator), 2 = kind::mxf4 (e2m1 nibbles, unit
+block scales, f32 accumulator)."""
 from collections import deque
 
 import numpy as np
@@ -30,10 +32,11 @@ def _bfs_closure_pairs(n, edges):
     return np.array(out, dtype=np.int32).reshape(-1, 2)
 
 
-def test_tensor_example_and_iterations(example_golden):
+@pytest.mark.parametrize("fmt", [1, 2])
+def test_tensor_example_and_iterations(example_golden, fmt):
     g = example_golden
     w = I.bind("example", I.same_generation_grammar(), 3, g["edges"], "S")
-    r, _, _ = gpu_closure(w, path_policy=2)
+    r, _, _ = gpu_closure(w, path_policy=2, tensor_format=fmt)
     assert r.iterations == 6
     ores = assert_parity(w, r)
     nc, _ = r.iteration_stats()
@@ -41,10 +44,11 @@ def test_tensor_example_and_iterations(example_golden):
 
 
 @pytest.mark.parametrize("n,d", [(64, 1), (150, 2), (300, 1), (257, 3)])
-def test_tensor_dense_stress_parity(n, d):
+@pytest.mark.parametrize("fmt", [1, 2])
+def test_tensor_dense_stress_parity(n, d, fmt):
     """S -> S S | a (both operands change): several 128x256 tiles and K blocks, ragged n."""
     w = I.dense_stress_workload(n, d, seed=n)
-    r, _, _ = gpu_closure(w, path_policy=2, account_work=True)
+    r, _, _ = gpu_closure(w, path_policy=2, tensor_format=fmt, account_work=True)
     ores = assert_parity(w, r)
     nc, jt = r.iteration_stats(work=True)
     assert nc.tolist() == ores.stats()["new_bits"].tolist()
@@ -52,43 +56,47 @@ def test_tensor_dense_stress_parity(n, d):
 
 
 @pytest.mark.parametrize("n,d", [(1000, 2), (2048, 1), (1537, 4)])
-def test_tensor_dense_stress_bfs(n, d):
+@pytest.mark.parametrize("fmt", [1, 2])
+def test_tensor_dense_stress_bfs(n, d, fmt):
     """Larger n against the textbook BFS transitive closure (the pin of S -> S S | a)."""
     w = I.dense_stress_workload(n, d, seed=7)
-    r, _, _ = gpu_closure(w, path_policy=2)
+    r, _, _ = gpu_closure(w, path_policy=2, tensor_format=fmt)
     assert np.array_equal(r.pairs(0), _bfs_closure_pairs(n, w.edges.tolist()))
 
 
-def test_tensor_random_parity():
+@pytest.mark.parametrize("fmt", [1, 2])
+def test_tensor_random_parity(fmt):
     for s in range(60):
         w = I.random_workload(40_000 + s, max_nodes=40, max_edges=120, max_nt=5, max_bin=10, max_term=5)
-        r, _, _ = gpu_closure(w, path_policy=2)
+        r, _, _ = gpu_closure(w, path_policy=2, tensor_format=fmt)
         ores = assert_parity(w, r)
         nc, _ = r.iteration_stats()
         assert nc.tolist() == ores.stats()["new_bits"].tolist(), w.name
 
 
 @pytest.mark.parametrize("query", ["q1", "q2", "union"])
-def test_tensor_ontology_parity(query):
+@pytest.mark.parametrize("fmt", [1, 2])
+def test_tensor_ontology_parity(query, fmt):
     w = I.ontology_workload(query, 600, depth=6, seed=2)
-    r, _, _ = gpu_closure(w, path_policy=2)
+    r, _, _ = gpu_closure(w, path_policy=2, tensor_format=fmt)
     assert_parity(w, r)
 
 
-def test_tensor_anbn_and_reuse():
+@pytest.mark.parametrize("fmt", [1, 2])
+def test_tensor_anbn_and_reuse(fmt):
     from paper_1707_01007_b200 import cfpq as C
     w = I.anbn_workload(3, 5)
     g = C.Grammar.from_workload(w)
     d = C.Graph(w.n_nodes, w.edges)
-    r = C.closure(g, d, path_policy=2)
+    r = C.closure(g, d, path_policy=2, tensor_format=fmt)
     assert r.iterations == 2 * 3 * 5 + 1
     assert_parity(w, r)
-    C.closure_reuse(g, d, r, path_policy=2)
+    C.closure_reuse(g, d, r, path_policy=2, tensor_format=fmt)
     assert_parity(w, r)
     w2 = I.anbn_workload(3, 5)
     w2.edges = w2.edges[::-1].copy()
     d.set_edges(w2.edges)
-    C.closure_reuse(g, d, r, path_policy=2)
+    C.closure_reuse(g, d, r, path_policy=2, tensor_format=fmt)
     assert_parity(w2, r)
 
 
@@ -104,14 +112,15 @@ def test_tensor_empty_and_lengths_rejected():
 
 
 @pytest.mark.parametrize("ranks", [2, 3, 8])
-def test_tensor_row_block_shards_emulated(ranks):
+@pytest.mark.parametrize("fmt", [1, 2])
+def test_tensor_row_block_shards_emulated(ranks, fmt):
     """Row-block sharding of the dense engine (the multi-GPU partition, §8(e)) emulated with
     `ranks` shards in one process: identical closure, iterations and per-iteration counts."""
     for w in (I.dense_stress_workload(400, 2, seed=ranks), I.random_workload(50_000 + ranks, max_nodes=200,
                                                                                max_edges=600, max_nt=5, max_bin=10,
                                                                                max_term=5, n_labels=4),
               I.ontology_workload("union", 400, depth=5, seed=ranks)):
-        r, _, _ = gpu_closure(w, path_policy=2, emulate_ranks=ranks)
+        r, _, _ = gpu_closure(w, path_policy=2, tensor_format=fmt, emulate_ranks=ranks)
         ores = assert_parity(w, r)
         nc, _ = r.iteration_stats()
         assert nc.tolist() == ores.stats()["new_bits"].tolist()
@@ -157,9 +166,9 @@ def test_tensor_cta_pairs_multicast():
         "from tests.gpu_util import gpu_closure, assert_parity\n"
         "for n, d in [(300, 2), (1000, 2), (130, 1)]:\n"
         "    w = I.dense_stress_workload(n, d, seed=n)\n"
-        "    r, _, _ = gpu_closure(w, path_policy=2)\n"
+        "    r, _, _ = gpu_closure(w, path_policy=2, tensor_format=1)\n"
         "    assert_parity(w, r)\n"
-        "    r, _, _ = gpu_closure(w, path_policy=2, emulate_ranks=3)\n"
+        "    r, _, _ = gpu_closure(w, path_policy=2, tensor_format=1, emulate_ranks=3)\n"
         "    assert_parity(w, r)\n"
         "print('ok')\n")
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
