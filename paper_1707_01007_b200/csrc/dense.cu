@@ -564,6 +564,290 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
 }
 
 // ------------------------------------------------------------------------------------------
+// 2-SM variant (cta_group::2): a CTA pair computes a 256 x 256 output tile with M=256 UMMAs
+// issued by the even CTA.  Each CTA stages its own 128 rows of A and its 128-row half of B
+// (32 KiB per K block instead of 48: a third less L2->SMEM traffic per MMA and 6 stages of
+// buffering instead of 4); the TMA of both CTAs completes on the leader's full barrier, the
+// leader's commits arrive on both CTAs' empty / accumulator barriers (multicast), and each
+// CTA's epilogue reads its own 128 TMEM lanes (rows) x 256 columns and arrives on the
+// leader's accumulator-empty barrier.  Same tile order, skip list and epilogue as above.
+// ------------------------------------------------------------------------------------------
+constexpr int kStages2 = 6;
+constexpr int kBHalf = (kTN / 2) * kTK;             // 16 KiB: this CTA's half of the B tile
+constexpr int kStage2Bytes = kABytes + kBHalf;       // 32 KiB
+
+__device__ __forceinline__ uint32_t mapa_cta(uint32_t smem_addr, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_addr), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx_remote(uint32_t cluster_addr, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.release.cluster.shared::cluster.b64 _, [%0], %1;" ::"r"(cluster_addr),
+                 "r"(bytes)
+                 : "memory");
+}
+// TMA into this CTA's smem, completing bytes on an mbarrier of either CTA of the pair
+__device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* map, uint32_t bar_cluster, int x, int y) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+            smem_u32(dst)),
+        "l"(map), "r"(bar_cluster), "r"(x), "r"(y)
+        : "memory");
+}
+__device__ __forceinline__ void umma2_mxf4(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                           uint32_t accumulate, uint32_t tmem_sfa, uint32_t tmem_sfb) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%6], p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate), "r"(tmem_sfa), "r"(tmem_sfb));
+}
+__device__ __forceinline__ void umma2_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                         uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void umma2_commit_mc(uint64_t* bar, uint16_t cta_mask) {
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+            smem_u32(bar)),
+        "h"(cta_mask)
+        : "memory");
+}
+
+size_t dense2_smem_bytes() { return (size_t)kStages2 * kStage2Bytes + 1024 + 256; }
+
+template <bool kF4>
+__global__ void __launch_bounds__(kDenseThreads, 1)
+    dense2sm_kernel(DenseParams p, const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmBh,
+                    const int64_t* __restrict__ mapA_row, const int64_t* __restrict__ mapB_row) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sA = smem;                                  // [kStages2][kABytes]
+    uint8_t* sB = smem + kStages2 * kABytes;             // [kStages2][kBHalf]
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages2 * kStage2Bytes);
+    uint64_t* empty = full + kStages2;
+    uint64_t* tmem_full = empty + kStages2;        // [kAcc]
+    uint64_t* tmem_empty = tmem_full + 2;          // [kAcc] (leader's is the one used)
+    uint32_t* tmem_base_smem = reinterpret_cast<uint32_t*>(tmem_empty + 2);
+
+    constexpr int kAcc = kF4 ? 1 : 2;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int n_j = p.np / kTN;
+    const int n_i = (p.i_hi - p.i_lo + 1) / 2;        // pairs of row tiles
+    const int tiles_per_nt = n_i * n_j;
+    const int total_tiles = tiles_per_nt * p.n_out;
+    const int n_k = kF4 ? p.np / (2 * kTK) : p.np / kTK;
+    const uint32_t crank = cluster_ctarank();
+    const bool leader = crank == 0;
+    const int unit = (int)blockIdx.x / 2, n_units = (int)gridDim.x / 2;
+
+    if (warp == 0 && lane == 0) {
+        for (int s = 0; s < kStages2; ++s) {
+            mbar_init(&full[s], 2);    // both CTAs' producers arrive (with their bytes) on the leader's
+            mbar_init(&empty[s], 1);   // the leader's MMA commit (multicast)
+        }
+        for (int a = 0; a < kAcc; ++a) {
+            mbar_init(&tmem_full[a], 1);
+            mbar_init(&tmem_empty[a], 8);   // one per epilogue warp of both CTAs
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&tmBh) : "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_base_smem)),
+                     "r"(kTmemCols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    }
+    tc_fence_before();
+    cluster_sync_all();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_base_smem;
+    if (kF4) {
+        if (warp >= 2) {
+            const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
+            tmem_fill32(tmem_base + lane_base + 256u, kSfOne);
+            tmem_fill32(tmem_base + lane_base + 288u, kSfOne);
+        }
+        tc_fence_before();
+        cluster_sync_all();   // both CTAs' scale factors before the first pair MMA
+        tc_fence_after();
+    }
+
+    if (warp == 0) {
+        // ------------------------------- TMA producer (both CTAs) -------------------------------
+        if (lane == 0) {
+            const uint32_t full0 = mapa_cta(smem_u32(&full[0]), 0);   // leader's full barriers
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int t = unit; t < total_tiles; t += n_units) {
+                int o, I2, J;
+                tile_coords(p, t, tiles_per_nt, n_i, n_j, o, I2, J);
+                const int I0 = p.i_lo + I2 * 2, I = I0 + (int)crank;
+                for (int q = p.rule_ptr[o]; q < p.rule_ptr[o + 1]; ++q) {
+                    const DenseRule r = p.rules[q];
+                    const int64_t arow = __ldg(mapA_row + r.B) + (int64_t)I * kTM;
+                    const int64_t brow = __ldg(mapB_row + r.C) + (int64_t)J * kTN + (int64_t)crank * (kTN / 2);
+                    for (int K = 0; K < n_k; ++K) {
+                        if (!kblock_live_group<2, kF4>(p, r, I0, J, K)) continue;
+                        mbar_wait(&empty[stage], phase ^ 1);
+                        const uint32_t fb = full0 + (uint32_t)(stage * 8);
+                        mbar_expect_tx_remote(fb, kStage2Bytes);
+                        tma_load_2d_pair(sA + stage * kABytes, &tmA, fb, K * kTK, (int)arow);
+                        tma_load_2d_pair(sB + stage * kBHalf, &tmBh, fb, K * kTK, (int)brow);
+                        if (++stage == kStages2) {
+                            stage = 0;
+                            phase ^= 1;
+                        }
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ------------------------------- MMA issuer (leader CTA only) -------------------------------
+        if (leader) {
+            const uint32_t idesc = kF4 ? idesc_mxf4(2 * kTM, kTN) : idesc_i8(2 * kTM, kTN);
+            const uint32_t tsfa = tmem_base + 256u, tsfb = tmem_base + 288u;
+            int stage = 0;
+            uint32_t phase = 0;
+            int as = 0;
+            uint32_t tphase = 0;
+            for (int t = unit; t < total_tiles; t += n_units) {
+                int o, I2, J;
+                tile_coords(p, t, tiles_per_nt, n_i, n_j, o, I2, J);
+                const int I0 = p.i_lo + I2 * 2;
+                const uint32_t tmem_acc = tmem_base + (uint32_t)(as * 256);
+                mbar_wait(&tmem_empty[as], tphase ^ 1);
+                tc_fence_after();
+                uint32_t acc = 0;
+                unsigned long long kb_issued = 0;
+                for (int q = p.rule_ptr[o]; q < p.rule_ptr[o + 1]; ++q) {
+                    const DenseRule r = p.rules[q];
+                    for (int K = 0; K < n_k; ++K) {
+                        if (!kblock_live_group<2, kF4>(p, r, I0, J, K)) continue;
+                        kb_issued += kF4 ? 4 : 2;   // 128x256x128 units: two row tiles, fp4 twice as deep
+                        mbar_wait(&full[stage], phase);
+                        tc_fence_after();
+                        if (lane == 0) {
+                            const uint32_t a0 = smem_u32(sA + stage * kABytes);
+                            const uint32_t b0 = smem_u32(sB + stage * kBHalf);
+#pragma unroll
+                            for (int kk = 0; kk < kTK / kUK; ++kk) {
+                                if (kF4)
+                                    umma2_mxf4(tmem_acc, kmajor_sw128_desc(a0 + kk * kUK), kmajor_sw128_desc(b0 + kk * kUK),
+                                               idesc, acc, tsfa, tsfb);
+                                else
+                                    umma2_i8(tmem_acc, kmajor_sw128_desc(a0 + kk * kUK), kmajor_sw128_desc(b0 + kk * kUK),
+                                             idesc, acc);
+                                acc = 1;
+                            }
+                            umma2_commit_mc(&empty[stage], (uint16_t)0x3);
+                        }
+                        __syncwarp();
+                        if (++stage == kStages2) {
+                            stage = 0;
+                            phase ^= 1;
+                        }
+                    }
+                }
+                if (lane == 0) {
+                    if (kb_issued) atomicAdd(p.new_cells + p.n_nt + 1, kb_issued);
+                    if (acc) {
+                        umma2_commit_mc(&tmem_full[as], (uint16_t)0x3);
+                    } else {
+                        // no live K block: both epilogues proceed on zeros
+                        mbar_arrive(&tmem_full[as]);
+                        mbar_arrive_remote(mapa_cta(smem_u32(&tmem_full[as]), 1));
+                    }
+                }
+                __syncwarp();
+                if (++as == kAcc) {
+                    as = 0;
+                    tphase ^= 1;
+                }
+            }
+        }
+    } else {
+        // ------------------------------- epilogue (warps 2..5, both CTAs) -------------------------------
+        const int quarter = warp & 3;
+        int as = 0;
+        uint32_t tphase = 0;
+        unsigned long long my_new = 0;
+        const uint32_t empty0 = mapa_cta(smem_u32(&tmem_empty[0]), 0);
+        for (int t = unit; t < total_tiles; t += n_units) {
+            int o, I2, J;
+            tile_coords(p, t, tiles_per_nt, n_i, n_j, o, I2, J);
+            const int I0 = p.i_lo + I2 * 2, I = I0 + (int)crank;
+            const bool mine = I < p.i_hi;
+            const int A = p.out_nt[o];
+            bool live = false;
+            for (int q = p.rule_ptr[o]; q < p.rule_ptr[o + 1] && !live; ++q)
+                for (int K = 0; K < n_k && !live; ++K) live = kblock_live_group<2, kF4>(p, p.rules[q], I0, J, K);
+            const int row = I * kTM + quarter * 32 + lane;
+            const bool wr = mine && row < p.n;
+            uint4 o0 = make_uint4(0, 0, 0, 0), o1 = o0;
+            if (wr) {
+                const uint4* src = reinterpret_cast<const uint4*>(p.T[A] + (size_t)row * p.Wp + (size_t)J * (kTN / 32));
+                o0 = __ldg(src);
+                o1 = __ldg(src + 1);
+            }
+            mbar_wait(&tmem_full[as], tphase);
+            tc_fence_after();
+            uint32_t w[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+            if (live) {
+#pragma unroll 1
+                for (int c = 0; c < kTN / 32; ++c) {
+                    uint32_t v[32];
+                    tmem_ld32(tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(as * 256 + c * 32), v);
+                    uint32_t word = 0;
+#pragma unroll
+                    for (int b = 0; b < 32; ++b) word |= (v[b] != 0u ? 1u : 0u) << b;
+#pragma unroll
+                    for (int q = 0; q < 8; ++q)
+                        if (q == c) w[q] = word;
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_remote(empty0 + (uint32_t)(as * 8));
+            if (++as == kAcc) {
+                as = 0;
+                tphase ^= 1;
+            }
+            unsigned long long cnt = 0;
+            if (wr) {
+                const uint32_t old[8] = {o0.x, o0.y, o0.z, o0.w, o1.x, o1.y, o1.z, o1.w};
+                uint32_t nw[8];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    nw[q] = old[q] | w[q];
+                    cnt += __popc(w[q] & ~old[q]);
+                }
+                uint4* dst = reinterpret_cast<uint4*>(p.Tn[A] + (size_t)row * p.Wp + (size_t)J * (kTN / 32));
+                dst[0] = make_uint4(nw[0], nw[1], nw[2], nw[3]);
+                dst[1] = make_uint4(nw[4], nw[5], nw[6], nw[7]);
+            }
+#pragma unroll
+            for (int s = 16; s > 0; s >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, s);
+            if (lane == 0 && cnt) atomicAdd(p.new_cells + A, cnt);
+            my_new += cnt;
+        }
+        if (lane == 0 && my_new) atomicAdd(p.new_cells + p.n_nt, my_new);
+    }
+    tc_fence_before();
+    cluster_sync_all();   // all MMAs consumed, all epilogues done in both CTAs
+    if (warp == 1)
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(kTmemCols));
+}
+
+// ------------------------------------------------------------------------------------------
 // Bit-row path (CUDA cores, path_policy 3): Alg. 1 line 9 as written — every iteration the
 // FULL Jacobi product T_{k-1} x T_{k-1} (not only Δ), over packed rows:
 //   T_k,A[i] = T_{k-1},A[i] | OR_{A->BC} OR_{r : T_B[i][r]} T_C[r]
@@ -587,6 +871,8 @@ constexpr int kRowThreads = 256;
 constexpr int kChunk = 128;     // set bits of T_B[i] per V chunk
 constexpr int kChunkR = 32;     // CSR_B(i) entries per R chunk
 constexpr int kRowMaxV4 = 8;    // uint4 accumulators per thread: rows up to 8*4*32*256 = 262144 bits
+constexpr int kScanBatch = 4;   // 128-bit loads per lane in flight in the L-form row scan
+
 
 struct RowChunk {
     int32_t rule;   // index into rules (output o implied)
@@ -602,7 +888,8 @@ struct RowsCtx {
     uint32_t* cnt;                     // [n_nt][n] popcount of row i of the current T_X
     uint4* dlist;                      // {A, i, word, bits}
     unsigned long long dlist_cap;
-    unsigned long long* rc;            // [0] chunks, [1] dlist entries, [2] dlist overflowed (sticky)
+    unsigned long long* rc;            // [0] R chunks, [1] dlist entries, [2] dlist overflowed (sticky),
+                                       // [3] V chunks, [4] L/P tasks
     int32_t first;                     // iteration 1 (both-preterminal rules evaluated)
     int32_t n_rules;
 };
@@ -672,18 +959,21 @@ __global__ void rows_delta_kernel(DenseParams p, RowsCtx c) {
     }
 }
 
-// Work list of the R and V forms: chunks of <= kChunkR CSR_B(i) entries / kChunk set bits
-// of T_B[i] per (rule, row), warp-aggregated appends.
+// Work lists of the R and V forms: chunks of <= kChunkR CSR_B(i) entries (list R at
+// chunks[0, rc[0])) / kChunk set bits of T_B[i] (list V at chunks[cap, cap + rc[3])) per
+// (rule, row), warp-aggregated appends.
 __global__ void rows_plan_kernel(DenseParams p, RowsCtx c, RowChunk* chunks, unsigned long long cap) {
     const int lane = threadIdx.x & 31;
     const int64_t tasks = (int64_t)c.n_rules * p.n;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t t0 = blockIdx.x * (int64_t)blockDim.x; t0 < tasks; t0 += stride) {
         const int64_t t = t0 + threadIdx.x;
-        int nch = 0, q = 0, i = 0, per = 1, len = 0;
+        int nch = 0, q = 0, i = 0, per = 1, len = 0, isv = 0, lp = 0;
         if (t < tasks) {
-            q = (int)(t / p.n);
-            i = (int)(t - (int64_t)q * p.n);
+            // row-major: the rules of one row are adjacent in every list, so a bit row read
+            // for two rules (e.g. S5 -> S P_sc and S6 -> S P_t) is re-read from L2
+            i = (int)(t / c.n_rules);
+            q = (int)(t - (int64_t)i * c.n_rules);
             const DenseRule r = p.rules[q];
             const int f = row_form(c, r);
             if (f == RF_R) {
@@ -693,61 +983,152 @@ __global__ void rows_plan_kernel(DenseParams p, RowsCtx c, RowChunk* chunks, uns
             } else if (f == RF_V) {
                 len = (int)c.cnt[(size_t)r.B * p.n + i];
                 per = kChunk;
+                isv = 1;
+            } else if (f == RF_L) {
+                lp = c.cnt[(size_t)r.B * p.n + i] != 0;
+            } else if (f == RF_P) {
+                const int32_t* ptr = c.nt[r.B].csr_ptr;
+                lp = __ldg(ptr + i + 1) > __ldg(ptr + i);
             }
             nch = (len + per - 1) / per;
         }
-        int incl = nch;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            int v = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += v;
+        {
+            // L / P task (row, rule): one entry
+            const unsigned want = __ballot_sync(0xffffffffu, lp);
+            unsigned long long base = 0;
+            if (lane == 0 && want) base = atomicAdd(c.rc + 4, (unsigned long long)__popc(want));
+            base = __shfl_sync(0xffffffffu, base, 0);
+            const unsigned long long at = base + __popc(want & ((1u << lane) - 1u));
+            if (lp && at < cap) chunks[2 * cap + at] = RowChunk{q, i, 0, 0};
         }
-        unsigned long long base = 0;
-        if (lane == 31 && incl) base = atomicAdd(c.rc, (unsigned long long)incl);
-        base = __shfl_sync(0xffffffffu, base, 31);
-        unsigned long long at = base + (unsigned long long)(incl - nch);
-        for (int h = 0; h < nch; ++h, ++at)
-            if (at < cap) chunks[at] = RowChunk{q, i, h * per, min(per, len - h * per)};
+#pragma unroll
+        for (int lst = 0; lst < 2; ++lst) {
+            const int mine = (isv == lst) ? nch : 0;
+            int incl = mine;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                int v = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += v;
+            }
+            unsigned long long base = 0;
+            if (lane == 31 && incl) base = atomicAdd(c.rc + (lst ? 3 : 0), (unsigned long long)incl);
+            base = __shfl_sync(0xffffffffu, base, 31);
+            unsigned long long at = base + (unsigned long long)(incl - mine);
+            RowChunk* out = chunks + (lst ? cap : 0);
+            for (int h = 0; h < mine; ++h, ++at)
+                if (at < cap) out[at] = RowChunk{q, i, h * per, min(per, len - h * per)};
+        }
     }
 }
 
-// Forms L and P: one warp per (row, rule) — rules of one row are adjacent, so the bit row
-// T_B[i] read for several rules comes from L1/L2.
-__global__ void __launch_bounds__(256) rows_scatter_kernel(DenseParams p, RowsCtx c, const int32_t* __restrict__ rule_out) {
+// Form R, one warp per (chunk, row slice of 32 * NVW uint4): lane e holds CSR_B(i) entry
+// e, the non-empty rows T_C[r] are ORed one after another with NVW 128-bit loads per lane
+// in flight, then the non-zero words of the slice are merged.  No CTA barriers.
+template <int NVW>
+__global__ void __launch_bounds__(256, 3) rows_rgather_kernel(DenseParams p, RowsCtx c, const int32_t* __restrict__ rule_out,
+                                                           const RowChunk* __restrict__ chunks) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nv4 = ((p.n + 31) / 32 + 3) / 4;
+    const int parts = (int)((nv4 + 32 * NVW - 1) / (32 * NVW));   // row slices of 32*NVW uint4
+    const unsigned long long m = c.rc[0] * (unsigned long long)parts;
+    unsigned long long my_new = 0;
+    for (unsigned long long ti = (blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x) >> 5; ti < m;
+         ti += ((unsigned long long)gridDim.x * blockDim.x) >> 5) {
+        const unsigned long long ci = ti / parts;
+        const int64_t vbase = (int64_t)(ti - ci * parts) * 32 * NVW;
+        const RowChunk ch = chunks[ci];
+        const DenseRule r = p.rules[ch.rule];
+        int rr = 0;
+        bool ok = false;
+        if (lane < ch.count) {
+            rr = __ldg(c.adj_idx + __ldg(c.nt[r.B].csr_ptr + ch.row) + ch.first + lane);
+            ok = c.cnt[(size_t)r.C * p.n + rr] != 0;
+        }
+        unsigned todo = __ballot_sync(0xffffffffu, ok);
+        if (!todo) continue;
+        uint4 acc[NVW];
+#pragma unroll
+        for (int b = 0; b < NVW; ++b) acc[b] = make_uint4(0, 0, 0, 0);
+        const uint4* TC = reinterpret_cast<const uint4*>(p.T[r.C]);
+        const int64_t wp4 = p.Wp / 4;
+        while (todo) {
+            const int src_lane = __ffs(todo) - 1;
+            todo &= todo - 1u;
+            const int row = __shfl_sync(0xffffffffu, rr, src_lane);
+            const uint4* rowC = TC + (size_t)row * wp4;
+#pragma unroll
+            for (int b = 0; b < NVW; ++b) {
+                const int64_t v = vbase + (int64_t)b * 32 + lane;
+                if (v < nv4) {
+                    const uint4 x = __ldg(rowC + v);
+                    acc[b].x |= x.x;
+                    acc[b].y |= x.y;
+                    acc[b].z |= x.z;
+                    acc[b].w |= x.w;
+                }
+            }
+        }
+        const int A = rule_out[ch.rule];
+#pragma unroll
+        for (int b = 0; b < NVW; ++b) {
+            const int64_t v = vbase + (int64_t)b * 32 + lane;
+            const uint32_t a[4] = {acc[b].x, acc[b].y, acc[b].z, acc[b].w};
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                if (a[q]) rows_merge(p, c, A, ch.row, 4 * v + q, a[q], my_new);
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) my_new += __shfl_xor_sync(0xffffffffu, my_new, o);
+    if (lane == 0 && my_new) atomicAdd(p.new_cells + p.n_nt, my_new);
+}
+
+// Forms L and P: one warp per (rule, row) task of the plan's list (rows with work only).
+// Latency-bound chains (CSR pointers -> index -> pre-check -> atomic): many warps resident.
+__global__ void __launch_bounds__(256, 4) rows_scatter_kernel(DenseParams p, RowsCtx c, const int32_t* __restrict__ rule_out,
+                                                              const RowChunk* __restrict__ tasks) {
     const int lane = threadIdx.x & 31;
     const int64_t wn = (p.n + 31) / 32;
-    const int64_t tasks = (int64_t)c.n_rules * p.n;
+    const unsigned long long m = c.rc[4];
     unsigned long long my_new = 0;
-    for (int64_t t = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; t < tasks;
-         t += ((int64_t)gridDim.x * blockDim.x) >> 5) {
-        const int i = (int)(t / c.n_rules);
-        const int q = (int)(t - (int64_t)i * c.n_rules);
+    for (unsigned long long t = (blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x) >> 5; t < m;
+         t += ((unsigned long long)gridDim.x * blockDim.x) >> 5) {
+        const RowChunk tk = tasks[t];
+        const int i = tk.row, q = tk.rule;
         const DenseRule r = p.rules[q];
-        const int f = row_form(c, r);
-        if (f != RF_L && f != RF_P) continue;
         const int A = rule_out[q];
         const int32_t* cptr = c.nt[r.C].csr_ptr;
-        if (f == RF_L) {
-            if (c.cnt[(size_t)r.B * p.n + i] == 0) continue;
+        if (!c.nt[r.B].is_const) {
+            // L: scan the bit row T_B[i] (T_{k-1}), scatter CSR_C(r) of every set bit r
             const uint4* rowB = reinterpret_cast<const uint4*>(p.T[r.B] + (size_t)i * p.Wp);
-            for (int64_t v = lane; v * 4 < wn; v += 32) {
-                const uint4 x = __ldg(rowB + v);
-                const uint32_t ws[4] = {x.x, x.y, x.z, x.w};
+            const int64_t nv4 = (wn + 3) / 4;
+            for (int64_t v0 = lane; v0 < nv4; v0 += 32 * kScanBatch) {
+                // kScanBatch independent 128-bit loads in flight, then the set bits
+                uint4 x[kScanBatch];
 #pragma unroll
-                for (int h = 0; h < 4; ++h) {
-                    uint32_t bits = ws[h];
-                    while (bits) {
-                        const int rr = (int)((v * 4 + h) * 32) + __ffs(bits) - 1;
-                        bits &= bits - 1u;
-                        const int e1 = __ldg(cptr + rr + 1);
-                        for (int e = __ldg(cptr + rr); e < e1; ++e) {
-                            const int j = __ldg(c.adj_idx + e);
-                            rows_merge(p, c, A, i, j >> 5, 1u << (j & 31), my_new);
+                for (int b = 0; b < kScanBatch; ++b)
+                    x[b] = v0 + b * 32 < nv4 ? __ldg(rowB + v0 + b * 32) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+                for (int b = 0; b < kScanBatch; ++b) {
+                    if (!(x[b].x | x[b].y | x[b].z | x[b].w)) continue;
+                    const int64_t v = v0 + b * 32;
+                    const uint32_t ws[4] = {x[b].x, x[b].y, x[b].z, x[b].w};
+                    for (int h = 0; h < 4; ++h) {
+                        uint32_t bits = ws[h];
+                        while (bits) {
+                            const int rr = (int)((v * 4 + h) * 32) + __ffs(bits) - 1;
+                            bits &= bits - 1u;
+                            const int e1 = __ldg(cptr + rr + 1);
+                            for (int e = __ldg(cptr + rr); e < e1; ++e) {
+                                const int j = __ldg(c.adj_idx + e);
+                                rows_merge(p, c, A, i, j >> 5, 1u << (j & 31), my_new);
+                            }
                         }
                     }
                 }
             }
         } else {
+            // P: CSR_B(i) x CSR_C(r) (iteration 1 only)
             const int32_t* bptr = c.nt[r.B].csr_ptr;
             const int b1 = __ldg(bptr + i + 1);
             for (int e = __ldg(bptr + i) + lane; e < b1; e += 32) {
@@ -767,16 +1148,17 @@ __global__ void __launch_bounds__(256) rows_scatter_kernel(DenseParams p, RowsCt
 
 // Forms R and V: one CTA per chunk ORs the chunk's bit rows T_C[r] (128-bit loads, 4 rows
 // in flight per thread) into a register accumulator and merges its non-zero words.
+template <int NV>   // uint4 accumulators per thread (>= ceil(row uint4s / kRowThreads))
 __global__ void __launch_bounds__(kRowThreads) rows_gather_kernel(DenseParams p, RowsCtx c,
                                                                  const int32_t* __restrict__ rule_out,
-                                                                 const RowChunk* __restrict__ chunks) {
+                                                                 const RowChunk* __restrict__ chunks, int counter) {
     __shared__ int32_t list[kChunk];
     __shared__ int32_t wsum[kRowThreads / 32];
     __shared__ int32_t n_list;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t wn = (p.n + 31) / 32;
     const int64_t nv4 = (wn + 3) / 4;
-    const unsigned long long m = c.rc[0];
+    const unsigned long long m = c.rc[counter];
     unsigned long long my_new = 0;
     for (unsigned long long ci = blockIdx.x; ci < m; ci += gridDim.x) {
         const RowChunk ch = chunks[ci];
@@ -826,9 +1208,9 @@ __global__ void __launch_bounds__(kRowThreads) rows_gather_kernel(DenseParams p,
         }
         __syncthreads();
         const int nl = n_list;
-        uint4 acc[kRowMaxV4];
+        uint4 acc[NV];
 #pragma unroll
-        for (int v = 0; v < kRowMaxV4; ++v) acc[v] = make_uint4(0, 0, 0, 0);
+        for (int v = 0; v < NV; ++v) acc[v] = make_uint4(0, 0, 0, 0);
         int e = 0;
         for (; e + 4 <= nl; e += 4) {
             const uint4* r0 = reinterpret_cast<const uint4*>(TC + (size_t)list[e] * p.Wp);
@@ -836,7 +1218,7 @@ __global__ void __launch_bounds__(kRowThreads) rows_gather_kernel(DenseParams p,
             const uint4* r2 = reinterpret_cast<const uint4*>(TC + (size_t)list[e + 2] * p.Wp);
             const uint4* r3 = reinterpret_cast<const uint4*>(TC + (size_t)list[e + 3] * p.Wp);
 #pragma unroll
-            for (int v = 0; v < kRowMaxV4; ++v) {
+            for (int v = 0; v < NV; ++v) {
                 int64_t g = (int64_t)v * kRowThreads + threadIdx.x;
                 if (g < nv4) {
                     const uint4 x0 = __ldg(r0 + g), x1 = __ldg(r1 + g), x2 = __ldg(r2 + g), x3 = __ldg(r3 + g);
@@ -850,7 +1232,7 @@ __global__ void __launch_bounds__(kRowThreads) rows_gather_kernel(DenseParams p,
         for (; e < nl; ++e) {
             const uint4* r0 = reinterpret_cast<const uint4*>(TC + (size_t)list[e] * p.Wp);
 #pragma unroll
-            for (int v = 0; v < kRowMaxV4; ++v) {
+            for (int v = 0; v < NV; ++v) {
                 int64_t g = (int64_t)v * kRowThreads + threadIdx.x;
                 if (g < nv4) {
                     const uint4 x = __ldg(r0 + g);
@@ -863,7 +1245,7 @@ __global__ void __launch_bounds__(kRowThreads) rows_gather_kernel(DenseParams p,
         }
         const int A = rule_out[ch.rule];
 #pragma unroll
-        for (int v = 0; v < kRowMaxV4; ++v) {
+        for (int v = 0; v < NV; ++v) {
             int64_t g = (int64_t)v * kRowThreads + threadIdx.x;
             if (g < nv4) {
                 const uint32_t a[4] = {acc[v].x, acc[v].y, acc[v].z, acc[v].w};
@@ -938,6 +1320,8 @@ struct DenseEngine {
     void* chunks = nullptr;                    // bit-row path work list
     unsigned long long chunk_cap = 0;
     uint32_t* rcnt = nullptr;                  // bit-row path: per NT row popcounts
+    std::vector<DenseRule> h_rules;            // rules in output order (host copy)
+    bool forms_known = false, has_r = false, has_v = false;
     void* dlist = nullptr;                     // bit-row path: Δ_k word list (uint4)
     unsigned long long dlist_cap = 0;
     unsigned long long* rc = nullptr;          // bit-row path counters
@@ -1021,6 +1405,7 @@ DenseEngine* dense_create(int32_t n, int32_t n_nt, int64_t Wp, const std::vector
     cudaMemcpyAsync(e->rule_ptr, rp.data(), rp.size() * 4, cudaMemcpyHostToDevice, s);
     if (!rl.empty()) cudaMemcpyAsync(e->rules, rl.data(), rl.size() * sizeof(DenseRule), cudaMemcpyHostToDevice, s);
     for (auto& r : rl) e->h_rule_out.push_back(r.A);
+    e->h_rules = rl;
     if ((c = cudaMalloc(&e->rule_out, std::max<size_t>(1, rl.size()) * 4)) != cudaSuccess) return fail("tables", c);
     if (!rl.empty())
         cudaMemcpyAsync(e->rule_out, e->h_rule_out.data(), rl.size() * 4, cudaMemcpyHostToDevice, s);
@@ -1043,6 +1428,15 @@ DenseEngine* dense_create(int32_t n, int32_t n_nt, int64_t Wp, const std::vector
         return fail("smem attribute", c);
     if ((c = cudaFuncSetAttribute(dense_kernel<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)dense_smem_bytes())) != cudaSuccess)
+        return fail("smem attribute", c);
+    if ((c = cudaFuncSetAttribute(dense_kernel<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)dense_smem_bytes())) != cudaSuccess)
+        return fail("smem attribute", c);
+    if ((c = cudaFuncSetAttribute(dense2sm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)dense2_smem_bytes())) != cudaSuccess)
+        return fail("smem attribute", c);
+    if ((c = cudaFuncSetAttribute(dense2sm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)dense2_smem_bytes())) != cudaSuccess)
         return fail("smem attribute", c);
     int dev = 0, sms = 0;
     cudaGetDevice(&dev);
@@ -1107,7 +1501,36 @@ cudaError_t dense_product(DenseEngine* e, int64_t i_lo, int64_t i_hi, cudaStream
         const char* v = getenv("CFPQ_DENSE_PAIR");
         return v && v[0] == '1';
     }();
-    if (pair && sms >= 2 && !e->fp4) {
+    // 2-SM pairs (cta_group::2, M = 256): the default for fp4 (CFPQ_DENSE_2SM=0 turns it
+    // off, =1 also turns it on for int8)
+    static const int two_sm = [] {
+        const char* v = getenv("CFPQ_DENSE_2SM");
+        return v ? (v[0] == '1' ? 1 : 0) : -1;
+    }();
+    const bool use2 = (two_sm == 1 || (two_sm == -1 && e->fp4)) && sms >= 2 && !pair;
+    if (use2) {
+        const int64_t units = (int64_t)e->n_out * ((i_hi - i_lo + 1) / 2) * (e->np / kTN);
+        const int grid = (int)std::max<int64_t>(2, std::min<int64_t>(sms / 2, units) * 2);
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(grid);
+        cfg.blockDim = dim3(kDenseThreads);
+        cfg.dynamicSmemBytes = dense2_smem_bytes();
+        cfg.stream = s;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = 2;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        cudaError_t c = e->fp4 ? cudaLaunchKernelEx(&cfg, dense2sm_kernel<true>, p, e->tmA, e->tmBh,
+                                                    (const int64_t*)e->mapA_row, (const int64_t*)e->mapB_row)
+                               : cudaLaunchKernelEx(&cfg, dense2sm_kernel<false>, p, e->tmA, e->tmBh,
+                                                    (const int64_t*)e->mapA_row, (const int64_t*)e->mapB_row);
+        if (launches) ++*launches;
+        return c != cudaSuccess ? c : cudaGetLastError();
+    }
+    if (pair && sms >= 2) {
         // CTA pairs (clusters of 2) share the B tile through TMA multicast
         const int64_t units = (int64_t)e->n_out * ((i_hi - i_lo + 1) / 2) * (e->np / kTN);
         const int grid = (int)std::max<int64_t>(2, std::min<int64_t>(sms / 2, units) * 2);
@@ -1123,8 +1546,10 @@ cudaError_t dense_product(DenseEngine* e, int64_t i_lo, int64_t i_hi, cudaStream
         attr[0].val.clusterDim.z = 1;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
-        cudaError_t c = cudaLaunchKernelEx(&cfg, dense_kernel<2>, p, e->tmA, e->tmBh, (const int64_t*)e->mapA_row,
-                                           (const int64_t*)e->mapB_row);
+        cudaError_t c = e->fp4 ? cudaLaunchKernelEx(&cfg, dense_kernel<2, true>, p, e->tmA, e->tmBh,
+                                                    (const int64_t*)e->mapA_row, (const int64_t*)e->mapB_row)
+                               : cudaLaunchKernelEx(&cfg, dense_kernel<2>, p, e->tmA, e->tmBh, (const int64_t*)e->mapA_row,
+                                                    (const int64_t*)e->mapB_row);
         if (launches) ++*launches;
         return c != cudaSuccess ? c : cudaGetLastError();
     }
@@ -1138,6 +1563,14 @@ cudaError_t dense_product(DenseEngine* e, int64_t i_lo, int64_t i_hi, cudaStream
     return cudaGetLastError();
 }
 
+// grid = resident CTAs (grid-stride kernels: no queue of CTAs that start late)
+template <typename K>
+static int resident_grid(K kernel, int threads, int sms) {
+    int per = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kernel, threads, 0) != cudaSuccess || per < 1) per = 1;
+    return sms * per;
+}
+
 cudaError_t rows_product(DenseEngine* e, uint32_t* const* T, uint32_t* const* Tn, const NTInfo* nt,
                          const int32_t* adj_idx, const uint64_t* log, unsigned long long n_seeds, bool first,
                          cudaStream_t s, int* launches) {
@@ -1149,8 +1582,8 @@ cudaError_t rows_product(DenseEngine* e, uint32_t* const* T, uint32_t* const* Tn
     const int32_t n_rules = (int32_t)e->h_rule_out.size();
     if (!e->rcnt) {
         if ((c = cudaMalloc(&e->rcnt, (size_t)e->n_nt * std::max(e->n, 1) * 4)) != cudaSuccess) return c;
-        if ((c = cudaMalloc(&e->rc, 4 * 8)) != cudaSuccess) return c;
-        if ((c = cudaMemsetAsync(e->rc, 0, 4 * 8, s)) != cudaSuccess) return c;
+        if ((c = cudaMalloc(&e->rc, 8 * 8)) != cudaSuccess) return c;
+        if ((c = cudaMemsetAsync(e->rc, 0, 8 * 8, s)) != cudaSuccess) return c;
         // testing knob: a tiny list exercises the whole-matrix fallback after an overflow
         const char* cap_env = getenv("CFPQ_ROWS_DLIST_CAP");
         e->dlist_cap = cap_env ? std::max(1ull, strtoull(cap_env, nullptr, 10)) : (1ull << 20);
@@ -1160,8 +1593,16 @@ cudaError_t rows_product(DenseEngine* e, uint32_t* const* T, uint32_t* const* Tn
     const unsigned long long want = std::max<unsigned long long>(e->chunk_cap, (unsigned long long)n_rules * e->n + 1024);
     if (want > e->chunk_cap) {
         cudaFree(e->chunks);
-        if ((c = cudaMalloc(&e->chunks, want * sizeof(RowChunk))) != cudaSuccess) return c;
+        if ((c = cudaMalloc(&e->chunks, 3 * want * sizeof(RowChunk))) != cudaSuccess) return c;   // lists R, V, L/P
         e->chunk_cap = want;
+    }
+    if (!e->forms_known) {
+        for (size_t q = 0; q < e->h_rules.size(); ++q) {
+            const bool bc = e->is_const[e->h_rules[q].B], cc = e->is_const[e->h_rules[q].C];
+            e->has_r |= bc && !cc;
+            e->has_v |= !bc && !cc;
+        }
+        e->forms_known = true;
     }
     DenseParams p{};
     p.n = e->n;
@@ -1185,17 +1626,18 @@ cudaError_t rows_product(DenseEngine* e, uint32_t* const* T, uint32_t* const* Tn
     // T_k buffer := T_{k-1}
     if (first) {
         if ((c = cudaMemsetAsync(e->rcnt, 0, (size_t)e->n_nt * e->n * 4, s)) != cudaSuccess) return c;
-        if ((c = cudaMemsetAsync(e->rc, 0, 4 * 8, s)) != cudaSuccess) return c;
+        if ((c = cudaMemsetAsync(e->rc, 0, 8 * 8, s)) != cudaSuccess) return c;
         if (n_seeds) rows_seed_kernel<<<sms * 8, 256, 0, s>>>(p, rc, log, n_seeds);
     } else {
         rows_delta_kernel<<<sms * 8, 256, 0, s>>>(p, rc);
     }
     // Δ_k list and chunk counter restart; plan
     if ((c = cudaMemsetAsync(e->rc, 0, 2 * 8, s)) != cudaSuccess) return c;
+    if ((c = cudaMemsetAsync(e->rc + 3, 0, 2 * 8, s)) != cudaSuccess) return c;
     for (int attempt = 0; attempt < 2; ++attempt) {
         rows_plan_kernel<<<sms * 8, 256, 0, s>>>(p, rc, (RowChunk*)e->chunks, e->chunk_cap);
-        unsigned long long got[3] = {0, 0, 0};
-        if ((c = cudaMemcpyAsync(got, e->rc, 3 * 8, cudaMemcpyDeviceToHost, s)) != cudaSuccess) return c;
+        unsigned long long got[5] = {0, 0, 0, 0, 0};
+        if ((c = cudaMemcpyAsync(got, e->rc, 5 * 8, cudaMemcpyDeviceToHost, s)) != cudaSuccess) return c;
         if ((c = cudaStreamSynchronize(s)) != cudaSuccess) return c;
         if (got[2]) {
             // the previous iteration's list overflowed (the delta kernel copied whole
@@ -1207,15 +1649,32 @@ cudaError_t rows_product(DenseEngine* e, uint32_t* const* T, uint32_t* const* Tn
             rc.dlist_cap = e->dlist_cap;
             if ((c = cudaMemsetAsync(e->rc + 2, 0, 8, s)) != cudaSuccess) return c;
         }
-        if (got[0] <= e->chunk_cap) break;
+        const unsigned long long need = std::max(got[0], std::max(got[3], got[4]));
+        if (need <= e->chunk_cap) break;
         cudaFree(e->chunks);
-        e->chunk_cap = got[0] + got[0] / 4;
-        if ((c = cudaMalloc(&e->chunks, e->chunk_cap * sizeof(RowChunk))) != cudaSuccess) return c;
+        e->chunk_cap = need + need / 4;
+        if ((c = cudaMalloc(&e->chunks, 3 * e->chunk_cap * sizeof(RowChunk))) != cudaSuccess) return c;
         if ((c = cudaMemsetAsync(e->rc, 0, 8, s)) != cudaSuccess) return c;
+        if ((c = cudaMemsetAsync(e->rc + 3, 0, 2 * 8, s)) != cudaSuccess) return c;
     }
-    rows_scatter_kernel<<<sms * 8, 256, 0, s>>>(p, rc, e->rule_out);
-    rows_gather_kernel<<<sms * 8, kRowThreads, 0, s>>>(p, rc, e->rule_out, (const RowChunk*)e->chunks);
-    if (launches) *launches += 4;
+    rows_scatter_kernel<<<resident_grid(rows_scatter_kernel, 256, sms), 256, 0, s>>>(p, rc, e->rule_out,
+                                                                                 (const RowChunk*)e->chunks + 2 * e->chunk_cap);
+    const int64_t nv4 = ((e->n + 31) / 32 + 3) / 4;
+    const int nv = (int)((nv4 + kRowThreads - 1) / kRowThreads);
+    const RowChunk* chR = (const RowChunk*)e->chunks;
+    const RowChunk* chV = chR + e->chunk_cap;
+    auto cta_gather = [&](const RowChunk* ch, int counter) {
+        if (nv <= 1) rows_gather_kernel<1><<<sms * 8, kRowThreads, 0, s>>>(p, rc, e->rule_out, ch, counter);
+        else if (nv <= 2) rows_gather_kernel<2><<<sms * 8, kRowThreads, 0, s>>>(p, rc, e->rule_out, ch, counter);
+        else if (nv <= 4) rows_gather_kernel<4><<<sms * 8, kRowThreads, 0, s>>>(p, rc, e->rule_out, ch, counter);
+        else rows_gather_kernel<8><<<sms * 8, kRowThreads, 0, s>>>(p, rc, e->rule_out, ch, counter);
+    };
+    if (e->has_v) cta_gather(chV, 3);
+    if (e->has_r) {
+        // R chunks: a warp per (chunk, row slice of 32 x 8 uint4 = 32,768 bits)
+        rows_rgather_kernel<8><<<resident_grid(rows_rgather_kernel<8>, 256, sms), 256, 0, s>>>(p, rc, e->rule_out, chR);
+    }
+    if (launches) *launches += 3 + (e->has_v ? 1 : 0) + (e->has_r ? 1 : 0);
     return cudaGetLastError();
 }
 
