@@ -650,7 +650,7 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
 
     if (warp == 0 && lane == 0) {
         for (int s = 0; s < kStages2; ++s) {
-            mbar_init(&full[s], 2);    // both CTAs' producers arrive (with their bytes) on the leader's
+            mbar_init(&full[s], 1);    // the leader's producer arrives with both CTAs' bytes
             mbar_init(&empty[s], 1);   // the leader's MMA commit (multicast)
         }
         for (int a = 0; a < kAcc; ++a) {
@@ -699,7 +699,10 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
                         if (!kblock_live_group<2, kF4>(p, r, I0, J, K)) continue;
                         mbar_wait(&empty[stage], phase ^ 1);
                         const uint32_t fb = full0 + (uint32_t)(stage * 8);
-                        mbar_expect_tx_remote(fb, kStage2Bytes);
+                        // no cluster-scope arrive from the peer: its TMA bytes complete on the
+                        // leader's barrier, whose one arrival expects both CTAs' bytes (the
+                        // transaction count may go transiently negative)
+                        if (leader) mbar_expect_tx(&full[stage], 2 * kStage2Bytes);
                         tma_load_2d_pair(sA + stage * kABytes, &tmA, fb, K * kTK, (int)arow);
                         tma_load_2d_pair(sB + stage * kBHalf, &tmBh, fb, K * kTK, (int)brow);
                         if (++stage == kStages2) {
@@ -1501,13 +1504,13 @@ cudaError_t dense_product(DenseEngine* e, int64_t i_lo, int64_t i_hi, cudaStream
         const char* v = getenv("CFPQ_DENSE_PAIR");
         return v && v[0] == '1';
     }();
-    // 2-SM pairs (cta_group::2, M = 256): the default for fp4 (CFPQ_DENSE_2SM=0 turns it
-    // off, =1 also turns it on for int8)
-    static const int two_sm = [] {
+    // 2-SM pairs (cta_group::2, M = 256), opt-in (CFPQ_DENSE_2SM=1): measured SLOWER than
+    // one CTA per SM on config S (fp4 16.5 vs 13.3 ms, int8 27.6 vs 21.9 ms at n = 16,384)
+    static const bool two_sm = [] {
         const char* v = getenv("CFPQ_DENSE_2SM");
-        return v ? (v[0] == '1' ? 1 : 0) : -1;
+        return v && v[0] == '1';
     }();
-    const bool use2 = (two_sm == 1 || (two_sm == -1 && e->fp4)) && sms >= 2 && !pair;
+    const bool use2 = two_sm && sms >= 2 && !pair;
     if (use2) {
         const int64_t units = (int64_t)e->n_out * ((i_hi - i_lo + 1) / 2) * (e->np / kTN);
         const int grid = (int)std::max<int64_t>(2, std::min<int64_t>(sms / 2, units) * 2);

@@ -175,3 +175,30 @@ def test_tensor_cta_pairs_multicast():
     env = dict(os.environ, CFPQ_DENSE_PAIR="1", PYTHONPATH=root)
     out = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
     assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
+
+
+def test_tensor_2sm_pairs():
+    """The opt-in 2-SM variant (cta_group::2, M = 256 UMMAs issued by the even CTA of a pair;
+    each CTA stages its A rows and half of B; TMA bytes of both CTAs complete on the
+    leader's barrier) in both formats, including the emulated row-block shards."""
+    import os
+    import subprocess
+    import sys
+    code = (
+        "import inputs as I\n"
+        "from tests.gpu_util import gpu_closure, assert_parity\n"
+        "for fmt in (1, 2):\n"
+        "    for n, d in [(300, 2), (700, 2), (130, 1)]:\n"
+        "        w = I.dense_stress_workload(n, d, seed=n)\n"
+        "        r, _, _ = gpu_closure(w, path_policy=2, tensor_format=fmt)\n"
+        "        o = assert_parity(w, r)\n"
+        "        nc, _ = r.iteration_stats()\n"
+        "        assert nc.tolist() == o.stats()['new_bits'].tolist()\n"
+        "    w = I.ontology_workload('union', 500, depth=5, seed=3)\n"
+        "    r, _, _ = gpu_closure(w, path_policy=2, tensor_format=fmt, emulate_ranks=3)\n"
+        "    assert_parity(w, r)\n"
+        "print('ok')\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, CFPQ_DENSE_2SM="1", PYTHONPATH=root)
+    out = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=900)
+    assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
