@@ -630,7 +630,9 @@ def main():
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
                 "scaling": "strong" if sharded else "weak", "vs_baseline": None,
-                "dtype": "int8 0/1 tiles -> s32 (tcgen05)" if pol == 2 else "u32 bit-words (boolean)",
+                "dtype": (("int8 0/1 tiles -> s32 (tcgen05 kind::i8)" if args.tensor_format == 1 else
+                           "e2m1 (fp4) 0/1 tiles, unit ue8m0 scales -> f32 (tcgen05 kind::mxf4)")
+                          if pol == 2 else "u32 bit-words (boolean)"),
                 "data": "synthetic",
                 "config": {**desc, "iterations": iterations, "cells": int(cells_total),
                            "results_start_nt": int(results_start), "useful_ops_per_step": int(ops),

@@ -106,7 +106,7 @@ typedef struct {
                                 relational semantics, sparse engine, |N| <= 512            */
     int32_t path_policy;     /* 0 auto: sparse, switching to tensor when Δ turns dense and a
                                 rule has two changing operands; 1 sparse (index-list semi-
-                                naive); 2 tensor (tcgen05 int8 dense); 3 rows (bit-row full-
+                                naive); 2 tensor (tcgen05 dense, tensor_format); 3 rows (bit-row full-
                                 operand, paper-faithful)                                     */
     int32_t account_work;    /* 1: also record per-iteration Jacobi AND-true triple counts
                                 (the work of Alg. 1 line 9 on sparse operands); slower     */
@@ -209,7 +209,8 @@ CFPQ_API cfpq_status cfpq_result_witness(cfpq_result* r, const cfpq_graph* d, in
  *   adjacency build, snapshot seeding) in ns, [9] device time of the fixpoint-loop
  *   kernel launches in ns (CUDA events on the closure stream), [10] CTAs of the closure
  *   kernel, [11..17] single-CTA phase cycle counters (only with record_times), [18] tcgen05
- *   k-blocks issued by the dense engine (each 128x256x128 int8 MMA work = 2^23 ops),
+ *   k-blocks issued by the dense engine, in 128x256x128 units of MMA work = 2^23 ops (an fp4
+ *   k-block, 256 deep, counts 2),
  *   [19] 1 if the last closure finished on the dense engine (path_policy 2, or the auto
  *   policy switched to it once Δ became dense), [20] 1 if the cells were kept in the
  *   hashed cell set (cell_set), [21] its capacity in slots.

@@ -182,6 +182,18 @@ __device__ __forceinline__ uint64_t kmajor_sw128_desc(uint32_t smem_addr) {
     return d;
 }
 
+// K-major operand tile with 64-byte rows in 64B-swizzled shared memory (8-row atoms 512 B
+// apart): SBO = 512>>4, layout SWIZZLE_64B = 4.
+__device__ __forceinline__ uint64_t kmajor_sw64_desc(uint32_t smem_addr) {
+    uint64_t d = 0;
+    d |= (uint64_t)((smem_addr & 0x3FFFF) >> 4);
+    d |= (uint64_t)1 << 16;
+    d |= (uint64_t)(512 >> 4) << 32;
+    d |= (uint64_t)1 << 46;
+    d |= (uint64_t)4 << 61;
+    return d;
+}
+
 // kind::i8 instruction descriptor: D s32, A/B unsigned 8-bit, both K-major, M=128, N=256.
 __host__ __device__ constexpr uint32_t idesc_i8(int M, int N) {
     return (2u << 4) | (0u << 7) | (0u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
@@ -339,7 +351,7 @@ __device__ __forceinline__ void tile_coords(const DenseParams& p, int t, int til
 // accumulator stage) and columns 256..319 hold the scale factors, all 1.0 (ue8m0 0x7F).
 // Every product term is 1.0 x 1.0 x 1 x 1 >= 0, so a sum is > 0 iff some term is, and the
 // threshold is exact at any magnitude (and the sums are exact integers below 2^24).
-template <int kCl, bool kF4 = false>
+template <int kCl, bool kF4 = false, int kKB = kTK>
 __global__ void __launch_bounds__(kDenseThreads, 1)
     dense_kernel(DenseParams p, const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                  const int64_t* __restrict__ mapA_row, const int64_t* __restrict__ mapB_row) {
@@ -347,11 +359,15 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
     // for the stacked T8T tensor (tmB); -1 if X is not packed.
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint8_t* sA = smem;                                  // [kStages][kABytes]
-    uint8_t* sB = smem + kStages * kABytes;              // [kStages][kBBytes]
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
-    uint64_t* empty = full + kStages;
-    uint64_t* tmem_full = empty + kStages;         // [2] accumulator stages (double-buffered TMEM)
+    // kKB = K bytes per stage: 128 (SWIZZLE_128B rows, 4 stages) or 64 (SWIZZLE_64B rows,
+    // 9 stages of half the bytes: more of the smem ring in flight ahead of the MMA)
+    constexpr int S_ = kKB == 128 ? kStages : 9;
+    constexpr int AB_ = kTM * kKB, BB_ = kTN * kKB, SB_ = AB_ + BB_;
+    uint8_t* sA = smem;                                  // [S_][AB_]
+    uint8_t* sB = smem + S_ * AB_;                       // [S_][BB_]
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + S_ * SB_);
+    uint64_t* empty = full + S_;
+    uint64_t* tmem_full = empty + S_;              // [2] accumulator stages (double-buffered TMEM)
     uint64_t* tmem_empty = tmem_full + 2;          // [2]
     uint32_t* tmem_base_smem = reinterpret_cast<uint32_t*>(tmem_empty + 2);
 
@@ -360,13 +376,14 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
     const int n_i = (p.i_hi - p.i_lo + kCl - 1) / kCl;   // (pairs of) row tiles
     const int tiles_per_nt = n_i * n_j;
     const int total_tiles = tiles_per_nt * p.n_out;
-    const int n_k = kF4 ? p.np / (2 * kTK) : p.np / kTK;
+    const int n_k = kF4 ? p.np / (2 * kKB) : p.np / kKB;
+    static_assert(kKB == 128 || (kKB == 64 && kF4 && kCl == 1), "64-byte K blocks: fp4, one CTA");
     constexpr int kAcc = kF4 ? 1 : 2;   // accumulator stages in TMEM
     const uint32_t crank = kCl == 2 ? cluster_ctarank() : 0u;
     const int unit = (int)blockIdx.x / kCl, n_units = (int)gridDim.x / kCl;
 
     if (warp == 0 && lane == 0) {
-        for (int s = 0; s < kStages; ++s) {
+        for (int s = 0; s < S_; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], kCl);   // one MMA commit per CTA of the cluster
         }
@@ -411,16 +428,16 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
                     const int64_t arow = __ldg(mapA_row + r.B) + (int64_t)I * kTM;
                     const int64_t brow = __ldg(mapB_row + r.C) + (int64_t)J * kTN;
                     for (int K = 0; K < n_k; ++K) {
-                        if (!kblock_live_group<kCl, kF4>(p, r, I0, J, K)) continue;
+                        if (!(kKB == 64 ? kblock_live_group<kCl, false>(p, r, I0, J, K) : kblock_live_group<kCl, kF4>(p, r, I0, J, K))) continue;
                         mbar_wait(&empty[stage], phase ^ 1);
-                        mbar_expect_tx(&full[stage], kStageBytes);
-                        tma_load_2d(sA + stage * kABytes, &tmA, &full[stage], K * kTK, (int)arow);
+                        mbar_expect_tx(&full[stage], SB_);
+                        tma_load_2d(sA + stage * AB_, &tmA, &full[stage], K * kKB, (int)arow);
                         if (kCl == 1)
-                            tma_load_2d(sB + stage * kBBytes, &tmB, &full[stage], K * kTK, (int)brow);
+                            tma_load_2d(sB + stage * BB_, &tmB, &full[stage], K * kKB, (int)brow);
                         else
-                            tma_load_2d_mc(sB + stage * kBBytes + crank * (kBBytes / 2), &tmB, &full[stage], K * kTK,
+                            tma_load_2d_mc(sB + stage * BB_ + crank * (BB_ / 2), &tmB, &full[stage], K * kKB,
                                            (int)(brow + crank * (kTN / 2)), (uint16_t)0x3);
-                        if (++stage == kStages) {
+                        if (++stage == S_) {
                             stage = 0;
                             phase ^= 1;
                         }
@@ -449,22 +466,22 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
             for (int q = p.rule_ptr[o]; q < p.rule_ptr[o + 1]; ++q) {
                 const DenseRule r = p.rules[q];
                 for (int K = 0; K < n_k; ++K) {
-                    if (!kblock_live_group<kCl, kF4>(p, r, I0, J, K)) continue;
-                    kb_issued += kF4 ? 2 : 1;   // in 128-deep K units
+                    if (!(kKB == 64 ? kblock_live_group<kCl, false>(p, r, I0, J, K) : kblock_live_group<kCl, kF4>(p, r, I0, J, K))) continue;
+                    kb_issued += kF4 ? (kKB == 128 ? 2 : 1) : 1;   // in 128-deep K units
                     mbar_wait(&full[stage], phase);
                     tc_fence_after();
                     if (lane == 0) {
-                        const uint32_t a0 = smem_u32(sA + stage * kABytes);
-                        const uint32_t b0 = smem_u32(sB + stage * kBBytes);
+                        const uint32_t a0 = smem_u32(sA + stage * AB_);
+                        const uint32_t b0 = smem_u32(sB + stage * BB_);
 #pragma unroll
-                        for (int kk = 0; kk < kTK / kUK; ++kk) {
+                        for (int kk = 0; kk < kKB / kUK; ++kk) {
                             // 32 bytes of K per instruction: 32 int8 or 64 e2m1 elements
+                            const uint64_t ad = kKB == 128 ? kmajor_sw128_desc(a0 + kk * kUK) : kmajor_sw64_desc(a0 + kk * kUK);
+                            const uint64_t bd = kKB == 128 ? kmajor_sw128_desc(b0 + kk * kUK) : kmajor_sw64_desc(b0 + kk * kUK);
                             if (kF4)
-                                umma_mxf4(tmem_acc, kmajor_sw128_desc(a0 + kk * kUK), kmajor_sw128_desc(b0 + kk * kUK),
-                                          idesc, acc, tsfa, tsfb);
+                                umma_mxf4(tmem_acc, ad, bd, idesc, acc, tsfa, tsfb);
                             else
-                                umma_i8(tmem_acc, kmajor_sw128_desc(a0 + kk * kUK), kmajor_sw128_desc(b0 + kk * kUK),
-                                        idesc, acc);
+                                umma_i8(tmem_acc, ad, bd, idesc, acc);
                             acc = 1;
                         }
                         // frees the smem stage (in both CTAs of a pair) when these MMAs finish
@@ -472,7 +489,7 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
                         else umma_commit_mc(&empty[stage], (uint16_t)0x3);
                     }
                     __syncwarp();
-                    if (++stage == kStages) {
+                    if (++stage == S_) {
                         stage = 0;
                         phase ^= 1;
                     }
@@ -503,7 +520,7 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
             const int A = p.out_nt[o];
             bool live = false;   // the pair issued MMAs for this tile (else TMEM holds no result)
             for (int q = p.rule_ptr[o]; q < p.rule_ptr[o + 1] && !live; ++q)
-                for (int K = 0; K < n_k && !live; ++K) live = kblock_live_group<kCl, kF4>(p, p.rules[q], I0, J, K);
+                for (int K = 0; K < n_k && !live; ++K) live = (kKB == 64 ? kblock_live_group<kCl, false>(p, p.rules[q], I0, J, K) : kblock_live_group<kCl, kF4>(p, p.rules[q], I0, J, K));
             // this row's 8 old words (32 contiguous bytes of T_{k-1}) load while the MMAs run
             const int row = I * kTM + quarter * 32 + lane;
             const bool wr = mine && row < p.n;
@@ -1280,20 +1297,23 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 }
 
 // 2D uint8 tensor [rows][row_bytes] with a (128 x box_rows) box, 128B swizzle.
-static bool make_map(CUtensorMap* m, const uint8_t* base, int64_t rows, int64_t row_bytes, int box_rows) {
+static bool make_map(CUtensorMap* m, const uint8_t* base, int64_t rows, int64_t row_bytes, int box_rows,
+                     int box_bytes = kTK) {
     auto enc = get_encode();
     if (!enc) return false;
     cuuint64_t dims[2] = {(cuuint64_t)row_bytes, (cuuint64_t)rows};
     cuuint64_t strides[1] = {(cuuint64_t)row_bytes};
-    cuuint32_t box[2] = {(cuuint32_t)kTK, (cuuint32_t)box_rows};
+    cuuint32_t box[2] = {(cuuint32_t)box_bytes, (cuuint32_t)box_rows};
     cuuint32_t estr[2] = {1, 1};
     CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, (void*)base, dims, strides, box, estr,
-                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, box_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
 }
 
 size_t dense_smem_bytes() { return (size_t)kStages * kStageBytes + 1024 + 256; }
+size_t dense64_smem_bytes() { return (size_t)9 * (kTM + kTN) * 64 + 1024 + 256; }
 
 struct DenseEngine {
     int32_t n = 0, np = 0, nt_tiles = 0, n_nt = 0;
@@ -1315,6 +1335,7 @@ struct DenseEngine {
     int32_t n_out = 0;
     std::vector<int32_t> h_out;
     CUtensorMap tmA, tmB, tmBh;   // tmBh: 128-row box of T8T (CTA-pair halves)
+    CUtensorMap tmA64, tmB64;     // 64-byte K boxes (SWIZZLE_64B) for the 9-stage fp4 variant
     int grid = 0;
     unsigned long long kblocks_total = 0;
     uint32_t* cnt = nullptr;   // accounting scratch
@@ -1415,7 +1436,9 @@ DenseEngine* dense_create(int32_t n, int32_t n_nt, int64_t Wp, const std::vector
     const int64_t row_bytes = fp4 ? e->np / 2 : e->np;   // nibble packs: half the bytes per row
     if (!make_map(&e->tmA, e->T8, (int64_t)std::max(na, 1) * e->np, row_bytes, kTM) ||
         !make_map(&e->tmB, e->T8T, (int64_t)std::max(nb, 1) * e->np, row_bytes, kTN) ||
-        !make_map(&e->tmBh, e->T8T, (int64_t)std::max(nb, 1) * e->np, row_bytes, kTN / 2)) {
+        !make_map(&e->tmBh, e->T8T, (int64_t)std::max(nb, 1) * e->np, row_bytes, kTN / 2) ||
+        !make_map(&e->tmA64, e->T8, (int64_t)std::max(na, 1) * e->np, row_bytes, kTM, 64) ||
+        !make_map(&e->tmB64, e->T8T, (int64_t)std::max(nb, 1) * e->np, row_bytes, kTN, 64)) {
         if (err) *err = "dense engine: cuTensorMapEncodeTiled failed";
         delete e;
         return nullptr;
@@ -1434,6 +1457,9 @@ DenseEngine* dense_create(int32_t n, int32_t n_nt, int64_t Wp, const std::vector
         return fail("smem attribute", c);
     if ((c = cudaFuncSetAttribute(dense_kernel<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)dense_smem_bytes())) != cudaSuccess)
+        return fail("smem attribute", c);
+    if ((c = cudaFuncSetAttribute(dense_kernel<1, true, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)dense64_smem_bytes())) != cudaSuccess)
         return fail("smem attribute", c);
     if ((c = cudaFuncSetAttribute(dense2sm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)dense2_smem_bytes())) != cudaSuccess)
@@ -1558,7 +1584,15 @@ cudaError_t dense_product(DenseEngine* e, int64_t i_lo, int64_t i_hi, cudaStream
     }
     const int64_t total = (int64_t)e->n_out * (i_hi - i_lo) * (e->np / kTN);
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(sms, total));
-    if (e->fp4)
+    // 64-byte K blocks, 9 stages (fp4; CFPQ_DENSE_K64=1)
+    static const bool k64 = [] {
+        const char* v = getenv("CFPQ_DENSE_K64");
+        return v && v[0] == '1';
+    }();
+    if (e->fp4 && k64)
+        dense_kernel<1, true, 64><<<grid, kDenseThreads, dense64_smem_bytes(), s>>>(p, e->tmA64, e->tmB64, e->mapA_row,
+                                                                                   e->mapB_row);
+    else if (e->fp4)
         dense_kernel<1, true><<<grid, kDenseThreads, dense_smem_bytes(), s>>>(p, e->tmA, e->tmB, e->mapA_row, e->mapB_row);
     else
         dense_kernel<1><<<grid, kDenseThreads, dense_smem_bytes(), s>>>(p, e->tmA, e->tmB, e->mapA_row, e->mapB_row);
