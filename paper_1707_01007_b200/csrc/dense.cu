@@ -182,18 +182,6 @@ __device__ __forceinline__ uint64_t kmajor_sw128_desc(uint32_t smem_addr) {
     return d;
 }
 
-// K-major operand tile with 64-byte rows in 64B-swizzled shared memory (8-row atoms 512 B
-// apart): SBO = 512>>4, layout SWIZZLE_64B = 4.
-__device__ __forceinline__ uint64_t kmajor_sw64_desc(uint32_t smem_addr) {
-    uint64_t d = 0;
-    d |= (uint64_t)((smem_addr & 0x3FFFF) >> 4);
-    d |= (uint64_t)1 << 16;
-    d |= (uint64_t)(512 >> 4) << 32;
-    d |= (uint64_t)1 << 46;
-    d |= (uint64_t)4 << 61;
-    return d;
-}
-
 // kind::i8 instruction descriptor: D s32, A/B unsigned 8-bit, both K-major, M=128, N=256.
 __host__ __device__ constexpr uint32_t idesc_i8(int M, int N) {
     return (2u << 4) | (0u << 7) | (0u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
@@ -213,85 +201,83 @@ constexpr uint32_t kSfOne = 0x7F7F7F7Fu;   // four ue8m0 scale bytes of 2^0 = 1.
 // kF4: e2m1 nibbles instead of bytes (1.0 = 0x2, two elements per byte, element 2b in the
 // low nibble of byte b); row length np/2 bytes.  A and B use the same K order, so the dot
 // products are those of the byte packs.
+//
+// One CTA of 128 threads per 128x128 tile: thread t holds the 128 bits of tile row t (one
+// 16-byte load).  Row-major pack: each thread expands its own bits.  Transposed pack: one
+// warp ballot per column gives that column's 32 row bits of the warp's 32 rows, expanded
+// by lane (column mod 32) — no shared-memory transpose.
+__device__ __forceinline__ uint32_t spread8_nib(uint32_t x) {   // 8 bits -> 8 nibbles of value 0x2
+    x &= 0xFFu;
+    x = (x | (x << 12)) & 0x000F000Fu;
+    x = (x | (x << 6)) & 0x03030303u;
+    x = (x | (x << 3)) & 0x11111111u;
+    return x << 1;
+}
+__device__ __forceinline__ uint32_t spread4_byte(uint32_t x) {   // 4 bits -> 4 bytes of value 1
+    return ((x & 0xFu) * 0x00204081u) & 0x01010101u;
+}
+
 template <bool kF4>
-__global__ void __launch_bounds__(256) pack_kernel(const uint32_t* __restrict__ T, int32_t n, int64_t Wp, int32_t np,
+__global__ void __launch_bounds__(128) pack_kernel(const uint32_t* __restrict__ T, int32_t n, int64_t Wp, int32_t np,
                                                    uint8_t* T8, uint8_t* T8T, uint8_t* occ, int32_t nt_tiles) {
-    __shared__ uint32_t bits[kTM][4];
     __shared__ int any;
     const int tI = blockIdx.y, tK = blockIdx.x;
-    if (threadIdx.x == 0) any = 0;
-    for (int t = threadIdx.x; t < kTM * 4; t += 256) {
-        int r = t >> 2, w = t & 3;
-        int row = tI * kTM + r;
-        int64_t word = (int64_t)tK * 4 + w;
-        uint32_t v = 0;
-        if (row < n && word * 32 < n) v = __ldg(T + (size_t)row * Wp + word);
-        bits[r][w] = v;
-    }
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    if (t == 0) any = 0;
+    const int row = tI * kTM + t;
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (row < n && (int64_t)tK * kTM < n) v = __ldg(reinterpret_cast<const uint4*>(T + (size_t)row * Wp) + tK);
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
     __syncthreads();
-    int local_any = 0;
-    for (int t = threadIdx.x; t < kTM * 4; t += 256) local_any |= bits[t >> 2][t & 3] != 0;
-    if (local_any) any = 1;
-    // row-major bytes: thread handles 16 consecutive columns of one row (4 uint4 stores per thread)
-    if (T8 && kF4) {
-        // 16 columns -> 8 bytes: byte q = nibble(col 2q) | nibble(col 2q+1) << 4
-        const int64_t rb = np / 2;
-        for (int t = threadIdx.x; t < kTM * 8; t += 256) {
-            int r = t >> 3, c16 = t & 7;
-            uint32_t w = bits[r][c16 >> 1] >> ((c16 & 1) * 16);
-            uint32_t o[2] = {0, 0};
+    if (__any_sync(0xffffffffu, (v.x | v.y | v.z | v.w) != 0) && lane == 0) any = 1;
+    const int64_t rb = kF4 ? np / 2 : np;   // bytes per packed row
+    if (T8) {
+        uint8_t* dst = T8 + (size_t)row * rb + (size_t)tK * kTM / (kF4 ? 2 : 1);
+        if (kF4) {
+            uint32_t o[16];
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+#pragma unroll
+                for (int h = 0; h < 4; ++h) o[q * 4 + h] = spread8_nib(w[q] >> (8 * h));
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                reinterpret_cast<uint4*>(dst)[q] = make_uint4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
+        } else {
 #pragma unroll
             for (int q = 0; q < 8; ++q) {
-                uint32_t b = ((w >> (2 * q)) & 1u) << 1 | ((w >> (2 * q + 1)) & 1u) << 5;
-                o[q >> 2] |= b << ((q & 3) * 8);
+                const uint32_t x = w[q >> 1] >> ((q & 1) * 16);
+                reinterpret_cast<uint4*>(dst)[q] =
+                    make_uint4(spread4_byte(x), spread4_byte(x >> 4), spread4_byte(x >> 8), spread4_byte(x >> 12));
             }
-            *reinterpret_cast<uint2*>(T8 + (size_t)(tI * kTM + r) * rb + (tK * kTM + c16 * 16) / 2) = make_uint2(o[0], o[1]);
         }
     }
-    if (T8T && kF4) {
-        // output row c (= column c of the tile), 16 consecutive source rows -> 8 bytes
-        const int64_t rb = np / 2;
-        for (int t = threadIdx.x; t < kTM * 8; t += 256) {
-            int c = t >> 3, r16 = t & 7;
-            uint32_t o[2] = {0, 0};
+    if (T8T) {
+        // column c of the tile = packed row tK*128 + c; this warp's 32 source rows are
+        // elements tI*128 + 32*warp .. +31 of it.  32 ballots per group of 32 columns: lane j
+        // keeps column 32g + j's mask, then the whole warp stores once.
 #pragma unroll
-            for (int q = 0; q < 16; ++q) {
-                uint32_t b = (bits[r16 * 16 + q][c >> 5] >> (c & 31)) & 1u;
-                o[q >> 3] |= b << ((q & 7) * 4 + 1);
-            }
-            *reinterpret_cast<uint2*>(T8T + (size_t)(tK * kTM + c) * rb + (tI * kTM + r16 * 16) / 2) = make_uint2(o[0], o[1]);
-        }
-    }
-    if (T8 && !kF4) {
-        for (int t = threadIdx.x; t < kTM * 8; t += 256) {
-            int r = t >> 3, c16 = t & 7;   // columns c16*16 .. +15
-            uint32_t w = bits[r][c16 >> 1] >> ((c16 & 1) * 16);
-            uint32_t o[4];
+        for (int g = 0; g < kTM / 32; ++g) {
+            uint32_t mine = 0;
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                uint32_t b = w >> (q * 4);
-                o[q] = (b & 1u) | ((b >> 1) & 1u) << 8 | ((b >> 2) & 1u) << 16 | ((b >> 3) & 1u) << 24;
+            for (int j = 0; j < 32; ++j) {
+                const uint32_t m = __ballot_sync(0xffffffffu, (w[g] >> j) & 1u);
+                if (lane == j) mine = m;
             }
-            *reinterpret_cast<uint4*>(T8 + (size_t)(tI * kTM + r) * np + tK * kTM + c16 * 16) =
-                make_uint4(o[0], o[1], o[2], o[3]);
-        }
-    }
-    // transposed bytes: output row c (= column c of the tile), 16 consecutive source rows
-    if (T8T && !kF4) {
-        for (int t = threadIdx.x; t < kTM * 8; t += 256) {
-            int c = t >> 3, r16 = t & 7;
-            uint32_t o[4] = {0, 0, 0, 0};
-#pragma unroll
-            for (int q = 0; q < 16; ++q) {
-                uint32_t b = (bits[r16 * 16 + q][c >> 5] >> (c & 31)) & 1u;
-                o[q >> 2] |= b << ((q & 3) * 8);
+            uint8_t* dst = T8T + (size_t)(tK * kTM + 32 * g + lane) * rb + ((size_t)tI * kTM + 32 * warp) / (kF4 ? 2 : 1);
+            if (kF4) {
+                *reinterpret_cast<uint4*>(dst) =
+                    make_uint4(spread8_nib(mine), spread8_nib(mine >> 8), spread8_nib(mine >> 16), spread8_nib(mine >> 24));
+            } else {
+                uint4* d4 = reinterpret_cast<uint4*>(dst);
+                d4[0] = make_uint4(spread4_byte(mine), spread4_byte(mine >> 4), spread4_byte(mine >> 8),
+                                   spread4_byte(mine >> 12));
+                d4[1] = make_uint4(spread4_byte(mine >> 16), spread4_byte(mine >> 20), spread4_byte(mine >> 24),
+                                   spread4_byte(mine >> 28));
             }
-            *reinterpret_cast<uint4*>(T8T + (size_t)(tK * kTM + c) * np + tI * kTM + r16 * 16) =
-                make_uint4(o[0], o[1], o[2], o[3]);
         }
     }
     __syncthreads();
-    if (threadIdx.x == 0 && occ) occ[(size_t)tI * nt_tiles + tK] = any ? 1 : 0;
+    if (t == 0 && occ) occ[(size_t)tI * nt_tiles + tK] = any ? 1 : 0;
 }
 
 // ------------------------------------------------------------------------------------------
@@ -351,7 +337,7 @@ __device__ __forceinline__ void tile_coords(const DenseParams& p, int t, int til
 // accumulator stage) and columns 256..319 hold the scale factors, all 1.0 (ue8m0 0x7F).
 // Every product term is 1.0 x 1.0 x 1 x 1 >= 0, so a sum is > 0 iff some term is, and the
 // threshold is exact at any magnitude (and the sums are exact integers below 2^24).
-template <int kCl, bool kF4 = false, int kKB = kTK>
+template <int kCl, bool kF4 = false>
 __global__ void __launch_bounds__(kDenseThreads, 1)
     dense_kernel(DenseParams p, const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                  const int64_t* __restrict__ mapA_row, const int64_t* __restrict__ mapB_row) {
@@ -359,10 +345,7 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
     // for the stacked T8T tensor (tmB); -1 if X is not packed.
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    // kKB = K bytes per stage: 128 (SWIZZLE_128B rows, 4 stages) or 64 (SWIZZLE_64B rows,
-    // 9 stages of half the bytes: more of the smem ring in flight ahead of the MMA)
-    constexpr int S_ = kKB == 128 ? kStages : 9;
-    constexpr int AB_ = kTM * kKB, BB_ = kTN * kKB, SB_ = AB_ + BB_;
+    constexpr int kKB = kTK, S_ = kStages, AB_ = kABytes, BB_ = kBBytes, SB_ = kStageBytes;
     uint8_t* sA = smem;                                  // [S_][AB_]
     uint8_t* sB = smem + S_ * AB_;                       // [S_][BB_]
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + S_ * SB_);
@@ -377,7 +360,6 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
     const int tiles_per_nt = n_i * n_j;
     const int total_tiles = tiles_per_nt * p.n_out;
     const int n_k = kF4 ? p.np / (2 * kKB) : p.np / kKB;
-    static_assert(kKB == 128 || (kKB == 64 && kF4 && kCl == 1), "64-byte K blocks: fp4, one CTA");
     constexpr int kAcc = kF4 ? 1 : 2;   // accumulator stages in TMEM
     const uint32_t crank = kCl == 2 ? cluster_ctarank() : 0u;
     const int unit = (int)blockIdx.x / kCl, n_units = (int)gridDim.x / kCl;
@@ -428,7 +410,7 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
                     const int64_t arow = __ldg(mapA_row + r.B) + (int64_t)I * kTM;
                     const int64_t brow = __ldg(mapB_row + r.C) + (int64_t)J * kTN;
                     for (int K = 0; K < n_k; ++K) {
-                        if (!(kKB == 64 ? kblock_live_group<kCl, false>(p, r, I0, J, K) : kblock_live_group<kCl, kF4>(p, r, I0, J, K))) continue;
+                        if (!kblock_live_group<kCl, kF4>(p, r, I0, J, K)) continue;
                         mbar_wait(&empty[stage], phase ^ 1);
                         mbar_expect_tx(&full[stage], SB_);
                         tma_load_2d(sA + stage * AB_, &tmA, &full[stage], K * kKB, (int)arow);
@@ -466,8 +448,8 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
             for (int q = p.rule_ptr[o]; q < p.rule_ptr[o + 1]; ++q) {
                 const DenseRule r = p.rules[q];
                 for (int K = 0; K < n_k; ++K) {
-                    if (!(kKB == 64 ? kblock_live_group<kCl, false>(p, r, I0, J, K) : kblock_live_group<kCl, kF4>(p, r, I0, J, K))) continue;
-                    kb_issued += kF4 ? (kKB == 128 ? 2 : 1) : 1;   // in 128-deep K units
+                    if (!kblock_live_group<kCl, kF4>(p, r, I0, J, K)) continue;
+                    kb_issued += kF4 ? 2 : 1;   // in 128-deep K units
                     mbar_wait(&full[stage], phase);
                     tc_fence_after();
                     if (lane == 0) {
@@ -476,8 +458,7 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
 #pragma unroll
                         for (int kk = 0; kk < kKB / kUK; ++kk) {
                             // 32 bytes of K per instruction: 32 int8 or 64 e2m1 elements
-                            const uint64_t ad = kKB == 128 ? kmajor_sw128_desc(a0 + kk * kUK) : kmajor_sw64_desc(a0 + kk * kUK);
-                            const uint64_t bd = kKB == 128 ? kmajor_sw128_desc(b0 + kk * kUK) : kmajor_sw64_desc(b0 + kk * kUK);
+                            const uint64_t ad = kmajor_sw128_desc(a0 + kk * kUK), bd = kmajor_sw128_desc(b0 + kk * kUK);
                             if (kF4)
                                 umma_mxf4(tmem_acc, ad, bd, idesc, acc, tsfa, tsfb);
                             else
@@ -520,7 +501,7 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
             const int A = p.out_nt[o];
             bool live = false;   // the pair issued MMAs for this tile (else TMEM holds no result)
             for (int q = p.rule_ptr[o]; q < p.rule_ptr[o + 1] && !live; ++q)
-                for (int K = 0; K < n_k && !live; ++K) live = (kKB == 64 ? kblock_live_group<kCl, false>(p, p.rules[q], I0, J, K) : kblock_live_group<kCl, kF4>(p, p.rules[q], I0, J, K));
+                for (int K = 0; K < n_k && !live; ++K) live = kblock_live_group<kCl, kF4>(p, p.rules[q], I0, J, K);
             // this row's 8 old words (32 contiguous bytes of T_{k-1}) load while the MMAs run
             const int row = I * kTM + quarter * 32 + lane;
             const bool wr = mine && row < p.n;
@@ -1120,6 +1101,8 @@ __global__ void __launch_bounds__(256, 4) rows_scatter_kernel(DenseParams p, Row
         const int32_t* cptr = c.nt[r.C].csr_ptr;
         if (!c.nt[r.B].is_const) {
             // L: scan the bit row T_B[i] (T_{k-1}), scatter CSR_C(r) of every set bit r
+            // (one warp per (row, rule): separate warps for two rules of one row run in
+            // parallel, the second read of the row hits L2)
             const uint4* rowB = reinterpret_cast<const uint4*>(p.T[r.B] + (size_t)i * p.Wp);
             const int64_t nv4 = (wn + 3) / 4;
             for (int64_t v0 = lane; v0 < nv4; v0 += 32 * kScanBatch) {
@@ -1297,23 +1280,20 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 }
 
 // 2D uint8 tensor [rows][row_bytes] with a (128 x box_rows) box, 128B swizzle.
-static bool make_map(CUtensorMap* m, const uint8_t* base, int64_t rows, int64_t row_bytes, int box_rows,
-                     int box_bytes = kTK) {
+static bool make_map(CUtensorMap* m, const uint8_t* base, int64_t rows, int64_t row_bytes, int box_rows) {
     auto enc = get_encode();
     if (!enc) return false;
     cuuint64_t dims[2] = {(cuuint64_t)row_bytes, (cuuint64_t)rows};
     cuuint64_t strides[1] = {(cuuint64_t)row_bytes};
-    cuuint32_t box[2] = {(cuuint32_t)box_bytes, (cuuint32_t)box_rows};
+    cuuint32_t box[2] = {(cuuint32_t)kTK, (cuuint32_t)box_rows};
     cuuint32_t estr[2] = {1, 1};
     CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, (void*)base, dims, strides, box, estr,
-                     CU_TENSOR_MAP_INTERLEAVE_NONE, box_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
-                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
 }
 
 size_t dense_smem_bytes() { return (size_t)kStages * kStageBytes + 1024 + 256; }
-size_t dense64_smem_bytes() { return (size_t)9 * (kTM + kTN) * 64 + 1024 + 256; }
 
 struct DenseEngine {
     int32_t n = 0, np = 0, nt_tiles = 0, n_nt = 0;
@@ -1335,7 +1315,6 @@ struct DenseEngine {
     int32_t n_out = 0;
     std::vector<int32_t> h_out;
     CUtensorMap tmA, tmB, tmBh;   // tmBh: 128-row box of T8T (CTA-pair halves)
-    CUtensorMap tmA64, tmB64;     // 64-byte K boxes (SWIZZLE_64B) for the 9-stage fp4 variant
     int grid = 0;
     unsigned long long kblocks_total = 0;
     uint32_t* cnt = nullptr;   // accounting scratch
@@ -1436,9 +1415,7 @@ DenseEngine* dense_create(int32_t n, int32_t n_nt, int64_t Wp, const std::vector
     const int64_t row_bytes = fp4 ? e->np / 2 : e->np;   // nibble packs: half the bytes per row
     if (!make_map(&e->tmA, e->T8, (int64_t)std::max(na, 1) * e->np, row_bytes, kTM) ||
         !make_map(&e->tmB, e->T8T, (int64_t)std::max(nb, 1) * e->np, row_bytes, kTN) ||
-        !make_map(&e->tmBh, e->T8T, (int64_t)std::max(nb, 1) * e->np, row_bytes, kTN / 2) ||
-        !make_map(&e->tmA64, e->T8, (int64_t)std::max(na, 1) * e->np, row_bytes, kTM, 64) ||
-        !make_map(&e->tmB64, e->T8T, (int64_t)std::max(nb, 1) * e->np, row_bytes, kTN, 64)) {
+        !make_map(&e->tmBh, e->T8T, (int64_t)std::max(nb, 1) * e->np, row_bytes, kTN / 2)) {
         if (err) *err = "dense engine: cuTensorMapEncodeTiled failed";
         delete e;
         return nullptr;
@@ -1457,9 +1434,6 @@ DenseEngine* dense_create(int32_t n, int32_t n_nt, int64_t Wp, const std::vector
         return fail("smem attribute", c);
     if ((c = cudaFuncSetAttribute(dense_kernel<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)dense_smem_bytes())) != cudaSuccess)
-        return fail("smem attribute", c);
-    if ((c = cudaFuncSetAttribute(dense_kernel<1, true, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)dense64_smem_bytes())) != cudaSuccess)
         return fail("smem attribute", c);
     if ((c = cudaFuncSetAttribute(dense2sm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)dense2_smem_bytes())) != cudaSuccess)
@@ -1489,8 +1463,8 @@ cudaError_t dense_begin(DenseEngine* e, uint32_t* const* T, uint32_t* const* Tn,
         uint8_t* b = e->packB[X] ? e->T8T + (size_t)(e->h_mapB[X] / e->np) * pack : nullptr;
         dim3 grid(e->nt_tiles, e->nt_tiles);
         uint8_t* oc = e->occ + (size_t)X * e->nt_tiles * e->nt_tiles;
-        if (e->fp4) pack_kernel<true><<<grid, 256, 0, s>>>(T[X], e->n, e->Wp, e->np, a, b, oc, e->nt_tiles);
-        else pack_kernel<false><<<grid, 256, 0, s>>>(T[X], e->n, e->Wp, e->np, a, b, oc, e->nt_tiles);
+        if (e->fp4) pack_kernel<true><<<grid, 128, 0, s>>>(T[X], e->n, e->Wp, e->np, a, b, oc, e->nt_tiles);
+        else pack_kernel<false><<<grid, 128, 0, s>>>(T[X], e->n, e->Wp, e->np, a, b, oc, e->nt_tiles);
         if (launches) ++*launches;
     }
     cudaError_t c;
@@ -1584,15 +1558,7 @@ cudaError_t dense_product(DenseEngine* e, int64_t i_lo, int64_t i_hi, cudaStream
     }
     const int64_t total = (int64_t)e->n_out * (i_hi - i_lo) * (e->np / kTN);
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(sms, total));
-    // 64-byte K blocks, 9 stages (fp4; CFPQ_DENSE_K64=1)
-    static const bool k64 = [] {
-        const char* v = getenv("CFPQ_DENSE_K64");
-        return v && v[0] == '1';
-    }();
-    if (e->fp4 && k64)
-        dense_kernel<1, true, 64><<<grid, kDenseThreads, dense64_smem_bytes(), s>>>(p, e->tmA64, e->tmB64, e->mapA_row,
-                                                                                   e->mapB_row);
-    else if (e->fp4)
+    if (e->fp4)
         dense_kernel<1, true><<<grid, kDenseThreads, dense_smem_bytes(), s>>>(p, e->tmA, e->tmB, e->mapA_row, e->mapB_row);
     else
         dense_kernel<1><<<grid, kDenseThreads, dense_smem_bytes(), s>>>(p, e->tmA, e->tmB, e->mapA_row, e->mapB_row);
@@ -1694,6 +1660,7 @@ cudaError_t rows_product(DenseEngine* e, uint32_t* const* T, uint32_t* const* Tn
         if ((c = cudaMemsetAsync(e->rc, 0, 8, s)) != cudaSuccess) return c;
         if ((c = cudaMemsetAsync(e->rc + 3, 0, 2 * 8, s)) != cudaSuccess) return c;
     }
+    // 4 CTAs x 8 warps per SM (measured: 6 or 8 CTAs with fewer registers are not faster)
     rows_scatter_kernel<<<resident_grid(rows_scatter_kernel, 256, sms), 256, 0, s>>>(p, rc, e->rule_out,
                                                                                  (const RowChunk*)e->chunks + 2 * e->chunk_cap);
     const int64_t nv4 = ((e->n + 31) / 32 + 3) / 4;
