@@ -871,6 +871,7 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
 constexpr int kRowThreads = 256;
 constexpr int kChunk = 128;     // set bits of T_B[i] per V chunk
 constexpr int kChunkR = 32;     // CSR_B(i) entries per R chunk
+constexpr int kChunkL = 64;     // set bits of T_B[i] per L chunk
 constexpr int kRowMaxV4 = 8;    // uint4 accumulators per thread: rows up to 8*4*32*256 = 262144 bits
 constexpr int kScanBatch = 4;   // 128-bit loads per lane in flight in the L-form row scan
 
@@ -969,7 +970,7 @@ __global__ void rows_plan_kernel(DenseParams p, RowsCtx c, RowChunk* chunks, uns
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t t0 = blockIdx.x * (int64_t)blockDim.x; t0 < tasks; t0 += stride) {
         const int64_t t = t0 + threadIdx.x;
-        int nch = 0, q = 0, i = 0, per = 1, len = 0, isv = 0, lp = 0;
+        int nch = 0, q = 0, i = 0, per = 1, len = 0, isv = 0, lp = 0, lpl = 0;
         if (t < tasks) {
             // row-major: the rules of one row are adjacent in every list, so a bit row read
             // for two rules (e.g. S5 -> S P_sc and S6 -> S P_t) is re-read from L2
@@ -986,7 +987,9 @@ __global__ void rows_plan_kernel(DenseParams p, RowsCtx c, RowChunk* chunks, uns
                 per = kChunk;
                 isv = 1;
             } else if (f == RF_L) {
-                lp = c.cnt[(size_t)r.B * p.n + i] != 0;
+                // chunks of <= kChunkL set bits of T_B[i] (hub rows over many warps)
+                lp = (int)((c.cnt[(size_t)r.B * p.n + i] + kChunkL - 1) / kChunkL);
+                lpl = (int)c.cnt[(size_t)r.B * p.n + i];
             } else if (f == RF_P) {
                 const int32_t* ptr = c.nt[r.B].csr_ptr;
                 lp = __ldg(ptr + i + 1) > __ldg(ptr + i);
@@ -994,13 +997,19 @@ __global__ void rows_plan_kernel(DenseParams p, RowsCtx c, RowChunk* chunks, uns
             nch = (len + per - 1) / per;
         }
         {
-            // L / P task (row, rule): one entry
-            const unsigned want = __ballot_sync(0xffffffffu, lp);
+            // L chunks (rank ranges of the set bits of T_B[i]) / one P task per row
+            int incl = lp;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                int v = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += v;
+            }
             unsigned long long base = 0;
-            if (lane == 0 && want) base = atomicAdd(c.rc + 4, (unsigned long long)__popc(want));
-            base = __shfl_sync(0xffffffffu, base, 0);
-            const unsigned long long at = base + __popc(want & ((1u << lane) - 1u));
-            if (lp && at < cap) chunks[2 * cap + at] = RowChunk{q, i, 0, 0};
+            if (lane == 31 && incl) base = atomicAdd(c.rc + 4, (unsigned long long)incl);
+            base = __shfl_sync(0xffffffffu, base, 31);
+            unsigned long long at = base + (unsigned long long)(incl - lp);
+            for (int h = 0; h < lp; ++h, ++at)
+                if (at < cap) chunks[2 * cap + at] = RowChunk{q, i, h * kChunkL, lpl ? min(kChunkL, lpl - h * kChunkL) : 0};
         }
 #pragma unroll
         for (int lst = 0; lst < 2; ++lst) {
@@ -1084,10 +1093,11 @@ __global__ void __launch_bounds__(256, 3) rows_rgather_kernel(DenseParams p, Row
     if (lane == 0 && my_new) atomicAdd(p.new_cells + p.n_nt, my_new);
 }
 
-// Forms L and P: one warp per (rule, row) task of the plan's list (rows with work only).
+// Forms L and P: one warp per task of the plan's list: an L chunk (<= kChunkL set bits of one row of T_B)
 // Latency-bound chains (CSR pointers -> index -> pre-check -> atomic): many warps resident.
 __global__ void __launch_bounds__(256, 4) rows_scatter_kernel(DenseParams p, RowsCtx c, const int32_t* __restrict__ rule_out,
                                                               const RowChunk* __restrict__ tasks) {
+    __shared__ int32_t wlist[8][kChunkL];   // per warp: the chunk's selected set bits
     const int lane = threadIdx.x & 31;
     const int64_t wn = (p.n + 31) / 32;
     const unsigned long long m = c.rc[4];
@@ -1100,36 +1110,57 @@ __global__ void __launch_bounds__(256, 4) rows_scatter_kernel(DenseParams p, Row
         const int A = rule_out[q];
         const int32_t* cptr = c.nt[r.C].csr_ptr;
         if (!c.nt[r.B].is_const) {
-            // L: scan the bit row T_B[i] (T_{k-1}), scatter CSR_C(r) of every set bit r
-            // (one warp per (row, rule): separate warps for two rules of one row run in
-            // parallel, the second read of the row hits L2)
+            // L: select the set bits of rank [first, first+count) of the bit row T_B[i]
+            // (T_{k-1}; four 128-bit loads per lane in flight, warp prefix counts) into a
+            // per-warp list, then every lane takes list entries: a hub row's bits spread over
+            // many warps and all 32 lanes, not over the lanes that happen to hold its words
             const uint4* rowB = reinterpret_cast<const uint4*>(p.T[r.B] + (size_t)i * p.Wp);
             const int64_t nv4 = (wn + 3) / 4;
-            for (int64_t v0 = lane; v0 < nv4; v0 += 32 * kScanBatch) {
-                // kScanBatch independent 128-bit loads in flight, then the set bits
+            int32_t* lst = wlist[threadIdx.x >> 5];
+            int base = 0;   // set bits before the current batch
+            for (int64_t v0 = lane; v0 - lane < nv4 && base < tk.first + tk.count; v0 += 32 * kScanBatch) {
                 uint4 x[kScanBatch];
 #pragma unroll
                 for (int b = 0; b < kScanBatch; ++b)
                     x[b] = v0 + b * 32 < nv4 ? __ldg(rowB + v0 + b * 32) : make_uint4(0, 0, 0, 0);
 #pragma unroll
                 for (int b = 0; b < kScanBatch; ++b) {
-                    if (!(x[b].x | x[b].y | x[b].z | x[b].w)) continue;
-                    const int64_t v = v0 + b * 32;
-                    const uint32_t ws[4] = {x[b].x, x[b].y, x[b].z, x[b].w};
-                    for (int h = 0; h < 4; ++h) {
-                        uint32_t bits = ws[h];
-                        while (bits) {
-                            const int rr = (int)((v * 4 + h) * 32) + __ffs(bits) - 1;
-                            bits &= bits - 1u;
-                            const int e1 = __ldg(cptr + rr + 1);
-                            for (int e = __ldg(cptr + rr); e < e1; ++e) {
-                                const int j = __ldg(c.adj_idx + e);
-                                rows_merge(p, c, A, i, j >> 5, 1u << (j & 31), my_new);
+                    const int pc = __popc(x[b].x) + __popc(x[b].y) + __popc(x[b].z) + __popc(x[b].w);
+                    int incl = pc;
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        int v = __shfl_up_sync(0xffffffffu, incl, o);
+                        if (lane >= o) incl += v;
+                    }
+                    const int total = __shfl_sync(0xffffffffu, incl, 31);
+                    int rank = base + incl - pc;
+                    if (pc && rank < tk.first + tk.count && rank + pc > tk.first) {
+                        const int64_t v = v0 + b * 32;
+                        const uint32_t ws[4] = {x[b].x, x[b].y, x[b].z, x[b].w};
+                        for (int h = 0; h < 4; ++h) {
+                            uint32_t bits = ws[h];
+                            while (bits) {
+                                const int bit = __ffs(bits) - 1;
+                                bits &= bits - 1u;
+                                if (rank >= tk.first && rank < tk.first + tk.count)
+                                    lst[rank - tk.first] = (int)((v * 4 + h) * 32) + bit;
+                                ++rank;
                             }
                         }
                     }
+                    base += total;
                 }
             }
+            __syncwarp();
+            for (int e = lane; e < tk.count; e += 32) {
+                const int rr = lst[e];
+                const int e1 = __ldg(cptr + rr + 1);
+                for (int f2 = __ldg(cptr + rr); f2 < e1; ++f2) {
+                    const int j = __ldg(c.adj_idx + f2);
+                    rows_merge(p, c, A, i, j >> 5, 1u << (j & 31), my_new);
+                }
+            }
+            __syncwarp();
         } else {
             // P: CSR_B(i) x CSR_C(r) (iteration 1 only)
             const int32_t* bptr = c.nt[r.B].csr_ptr;

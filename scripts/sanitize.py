@@ -1,4 +1,6 @@
-"""Small closures on every engine, for compute-sanitizer (memcheck / racecheck / synccheck)."""
+"""Small closures on every engine, for compute-sanitizer (memcheck / racecheck / synccheck):
+sparse, hashed, sharded, async, tensor (fp4 and int8; CFPQ_DENSE_2SM=1 / CFPQ_DENSE_PAIR=1 for
+the cluster variants), bit rows (forms L, R, V, P)."""
 import sys, os
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
@@ -20,9 +22,13 @@ cases = [(I.example_workload(), dict()), (I.example_workload(), dict(semantics=1
          (I.ontology_workload("union", 300, depth=5, seed=1), dict(solo_threshold=0)),
          (I.ontology_workload("union", 300, depth=5, seed=1), dict(log_capacity=64)),
          (I.dense_stress_workload(100, 2), dict(semantics=1)),
-         (I.dense_stress_workload(200, 2), dict(path_policy=2)),
+         (I.dense_stress_workload(200, 2), dict(path_policy=2, tensor_format=1)),
+         (I.dense_stress_workload(200, 2), dict(path_policy=2, tensor_format=2)),
          (I.dense_stress_workload(200, 2), dict(path_policy=3)),
+         (I.ontology_workload("q1", 300, depth=5, seed=6), dict(path_policy=3)),
+         (I.ontology_workload("union", 300, depth=5, seed=7), dict(path_policy=3)),
          (I.dense_stress_workload(150, 2), dict(path_policy=2, emulate_ranks=2)),
+         (I.dense_stress_workload(150, 2), dict(path_policy=2, tensor_format=1, emulate_ranks=2)),
          (I.dense_stress_workload(300, 2), dict()),
          (I.ontology_workload("union", 300, depth=5, seed=2), dict(cell_set=2)),
          (I.ontology_workload("union", 300, depth=5, seed=2), dict(cell_set=2, log_capacity=64)),
