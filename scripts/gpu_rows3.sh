@@ -11,13 +11,13 @@ for _ in range(3): C.closure_reuse(g,d,r,path_policy=3); print(r.stats()['loop_n
 nc,_=r.iteration_stats(); nc1,_=r1.iteration_stats()
 print(json.dumps({'same': nc.tolist()==nc1.tolist()}))
 "
-CFPQ_ROWS_NO_TMA=1 timeout 300 python -c "
+timeout 300 python -c "
 import sys, json; sys.path.insert(0,'.')
 import torch, inputs as I
 from paper_1707_01007_b200 import cfpq as C
 w=I.config4_workload(); g=C.Grammar.from_workload(w); d=C.Graph(w.n_nodes, torch.from_numpy(w.edges).cuda())
 r=C.closure(g,d,path_policy=3)
-for _ in range(3): C.closure_reuse(g,d,r,path_policy=3); print('no-tma', r.stats()['loop_ns']/1e6)
+for _ in range(3): C.closure_reuse(g,d,r,path_policy=3); print('again', r.stats()['loop_ns']/1e6)
 "
 timeout 900 python -m pytest tests/test_gpu_rows.py -q -x 2>&1 | tail -4
 timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
