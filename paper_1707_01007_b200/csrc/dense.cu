@@ -964,8 +964,22 @@ __global__ void rows_delta_kernel(DenseParams p, RowsCtx c) {
 // Work lists of the R and V forms: chunks of <= kChunkR CSR_B(i) entries (list R at
 // chunks[0, rc[0])) / kChunk set bits of T_B[i] (list V at chunks[cap, cap + rc[3])) per
 // (rule, row), warp-aggregated appends.
+constexpr int kPlanRules = 64;   // rule forms cached in shared memory up to this many rules
+
 __global__ void rows_plan_kernel(DenseParams p, RowsCtx c, RowChunk* chunks, unsigned long long cap) {
+    __shared__ int32_t s_form[kPlanRules], s_B[kPlanRules];
+    __shared__ const int32_t* s_ptr[kPlanRules];
     const int lane = threadIdx.x & 31;
+    const bool cached = c.n_rules <= kPlanRules;
+    if (cached) {
+        for (int q = threadIdx.x; q < c.n_rules; q += blockDim.x) {
+            const DenseRule r = p.rules[q];
+            s_form[q] = row_form(c, r);
+            s_B[q] = r.B;
+            s_ptr[q] = c.nt[r.B].csr_ptr;
+        }
+        __syncthreads();
+    }
     const int64_t tasks = (int64_t)c.n_rules * p.n;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t t0 = blockIdx.x * (int64_t)blockDim.x; t0 < tasks; t0 += stride) {
@@ -974,12 +988,27 @@ __global__ void rows_plan_kernel(DenseParams p, RowsCtx c, RowChunk* chunks, uns
         if (t < tasks) {
             // row-major: the rules of one row are adjacent in every list, so a bit row read
             // for two rules (e.g. S5 -> S P_sc and S6 -> S P_t) is re-read from L2
-            i = (int)(t / c.n_rules);
-            q = (int)(t - (int64_t)i * c.n_rules);
-            const DenseRule r = p.rules[q];
-            const int f = row_form(c, r);
+            if (tasks < (1ll << 31)) {
+                i = (int)((uint32_t)t / (uint32_t)c.n_rules);
+                q = (int)((uint32_t)t - (uint32_t)i * (uint32_t)c.n_rules);
+            } else {
+                i = (int)(t / c.n_rules);
+                q = (int)(t - (int64_t)i * c.n_rules);
+            }
+            DenseRule r;
+            int f;
+            const int32_t* bptr;
+            if (cached) {
+                f = s_form[q];
+                r.B = s_B[q];
+                bptr = s_ptr[q];
+            } else {
+                r = p.rules[q];
+                f = row_form(c, r);
+                bptr = c.nt[r.B].csr_ptr;
+            }
             if (f == RF_R) {
-                const int32_t* ptr = c.nt[r.B].csr_ptr;
+                const int32_t* ptr = bptr;
                 len = __ldg(ptr + i + 1) - __ldg(ptr + i);
                 per = kChunkR;
             } else if (f == RF_V) {
@@ -991,7 +1020,7 @@ __global__ void rows_plan_kernel(DenseParams p, RowsCtx c, RowChunk* chunks, uns
                 lp = (int)((c.cnt[(size_t)r.B * p.n + i] + kChunkL - 1) / kChunkL);
                 lpl = (int)c.cnt[(size_t)r.B * p.n + i];
             } else if (f == RF_P) {
-                const int32_t* ptr = c.nt[r.B].csr_ptr;
+                const int32_t* ptr = bptr;
                 lp = __ldg(ptr + i + 1) > __ldg(ptr + i);
             }
             nch = (len + per - 1) / per;
@@ -1035,7 +1064,7 @@ __global__ void rows_plan_kernel(DenseParams p, RowsCtx c, RowChunk* chunks, uns
 // e, the non-empty rows T_C[r] are ORed one after another with NVW 128-bit loads per lane
 // in flight, then the non-zero words of the slice are merged.  No CTA barriers.
 template <int NVW>
-__global__ void __launch_bounds__(256, 3) rows_rgather_kernel(DenseParams p, RowsCtx c, const int32_t* __restrict__ rule_out,
+__global__ void __launch_bounds__(256, NVW <= 2 ? 8 : 3) rows_rgather_kernel(DenseParams p, RowsCtx c, const int32_t* __restrict__ rule_out,
                                                            const RowChunk* __restrict__ chunks) {
     const int lane = threadIdx.x & 31;
     const int64_t nv4 = ((p.n + 31) / 32 + 3) / 4;
@@ -1706,8 +1735,9 @@ cudaError_t rows_product(DenseEngine* e, uint32_t* const* T, uint32_t* const* Tn
     };
     if (e->has_v) cta_gather(chV, 3);
     if (e->has_r) {
-        // R chunks: a warp per (chunk, row slice of 32 x 8 uint4 = 32,768 bits)
-        rows_rgather_kernel<8><<<resident_grid(rows_rgather_kernel<8>, 256, sms), 256, 0, s>>>(p, rc, e->rule_out, chR);
+        // R chunks: a warp per (chunk, row slice of 32 x 2 uint4 = 1 KiB): many light warps
+        // (config 4: 10.2 ms closure; 4 / 8 / 16 uint4 per lane: 10.7 / 11.8 / 16.0 ms; 1: 11.5 ms)
+        rows_rgather_kernel<2><<<resident_grid(rows_rgather_kernel<2>, 256, sms), 256, 0, s>>>(p, rc, e->rule_out, chR);
     }
     if (launches) *launches += 3 + (e->has_v ? 1 : 0) + (e->has_r ? 1 : 0);
     return cudaGetLastError();
