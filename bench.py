@@ -200,10 +200,11 @@ TENSOR_FORMATS = {1: "int8", 2: "fp4"}
 
 def tensor_roofline(stats, step_ms, fmt=2):
     """Issued tensor work of the dense engine over the device time of the fixpoint loop (all
-    tcgen05 product launches + packs of every iteration): 2*128*256*128 ops per 128-deep
-    k-block (the library counts an fp4 k-block, 256 deep, as two).  Peak of the format:
+    tcgen05 product launches + packs of every iteration): the library counts issued MMA work in
+    units of 128 x 32 x 128 multiply-adds (2*128*32*128 ops; an M=128 x N=256 int8 k-block is
+    8 units, a 256-deep fp4 k-block 16).  Peak of the format:
     int8 = bf16 x 2, fp4 = bf16 x 4 (measured bf16, nominal ratios)."""
-    ops = stats["mma_kblocks"] * 2 * 128 * 256 * 128
+    ops = stats["mma_kblocks"] * 2 * 128 * 32 * 128
     loop_s = stats["loop_ns"] * 1e-9
     burst, sustained, src = fp4_peak() if fmt == 2 else int8_peak()
     achieved = ops / loop_s / 1e12
@@ -212,8 +213,8 @@ def tensor_roofline(stats, step_ms, fmt=2):
             "frac_of_sustained": achieved / sustained, "traffic": ncu_traffic("configS" if fmt == 2 else "configS_int8"),
             "kernel": f"cfpq::dense_kernel (tcgen05.mma {kind})", "format": TENSOR_FORMATS[fmt],
             "loop_ms": loop_s * 1e3, "share_of_step": loop_s * 1e3 / step_ms, "issued_ops": ops, "peak_source": src,
-            "note": f"{TENSOR_FORMATS[fmt]} TOPS reported in the TFLOP/s slot; issued work counts whole 128x256 "
-                    "output tiles x live K blocks (zeros inside tiles included)"}
+            "note": f"{TENSOR_FORMATS[fmt]} TOPS reported in the TFLOP/s slot; issued work counts whole output "
+                    "tiles x live K blocks (zeros inside tiles included)"}
 
 
 def supplementary_tensor(C, stream, steps=3, fmt=2):

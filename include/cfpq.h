@@ -209,8 +209,8 @@ CFPQ_API cfpq_status cfpq_result_witness(cfpq_result* r, const cfpq_graph* d, in
  *   adjacency build, snapshot seeding) in ns, [9] device time of the fixpoint-loop
  *   kernel launches in ns (CUDA events on the closure stream), [10] CTAs of the closure
  *   kernel, [11..17] single-CTA phase cycle counters (only with record_times), [18] tcgen05
- *   k-blocks issued by the dense engine, in 128x256x128 units of MMA work = 2^23 ops (an fp4
- *   k-block, 256 deep, counts 2),
+ *   MMA work issued by the dense engine, in units of 128 x 32 x 128 multiply-adds = 2^20 ops (an
+ *   M=128 x N=256 x K=128 int8 k-block counts 8; fp4 k-blocks are 256 deep),
  *   [19] 1 if the last closure finished on the dense engine (path_policy 2, or the auto
  *   policy switched to it once Δ became dense), [20] 1 if the cells were kept in the
  *   hashed cell set (cell_set), [21] its capacity in slots.

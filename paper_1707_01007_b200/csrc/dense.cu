@@ -449,7 +449,7 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
                 const DenseRule r = p.rules[q];
                 for (int K = 0; K < n_k; ++K) {
                     if (!kblock_live_group<kCl, kF4>(p, r, I0, J, K)) continue;
-                    kb_issued += kF4 ? 2 : 1;   // in 128-deep K units
+                    kb_issued += (kTN / 32) * (kF4 ? 2 : 1);   // in 128 x 32 x 128 units of MMA work
                     mbar_wait(&full[stage], phase);
                     tc_fence_after();
                     if (lane == 0) {
@@ -733,7 +733,7 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
                     const DenseRule r = p.rules[q];
                     for (int K = 0; K < n_k; ++K) {
                         if (!kblock_live_group<2, kF4>(p, r, I0, J, K)) continue;
-                        kb_issued += kF4 ? 4 : 2;   // 128x256x128 units: two row tiles, fp4 twice as deep
+                        kb_issued += 2 * (kTN / 32) * (kF4 ? 2 : 1);   // 128x32x128 units: two row tiles, fp4 twice as deep
                         mbar_wait(&full[stage], phase);
                         tc_fence_after();
                         if (lane == 0) {

@@ -15,7 +15,7 @@ for n, fmt in [(n, f) for n in ns for f in fmts]:
         C.closure_reuse(g, d, r, path_policy=2, tensor_format=fmt)
     st = r.stats()
     nc, _ = r.iteration_stats()
-    ops = st["mma_kblocks"] * 2 * 128 * 256 * 128
+    ops = st["mma_kblocks"] * 2 * 128 * 32 * 128
     t = st["loop_ns"] * 1e-9
     print(json.dumps({"n": n, "fmt": fmt, "iters": r.iterations, "loop_ms": t * 1e3, "seed_ms": st["seed_ns"] / 1e6,
                       "kblocks": st["mma_kblocks"], "issued_TOPS": ops / t / 1e12,
