@@ -310,6 +310,17 @@ __device__ __forceinline__ bool kblock_live_group(const DenseParams& p, const De
     return live;
 }
 
+// Live K blocks K0 .. K0+31 of (rule, row tile(s) I0, column tile J) as a bit mask: every lane
+// checks one K block (its occupancy loads in parallel with the other lanes'), one ballot.
+// The whole warp must call it.
+template <int kCl, bool kF4>
+__device__ __forceinline__ uint32_t live_mask32(const DenseParams& p, const DenseRule& r, int I0, int J, int K0,
+                                                int n_k) {
+    const int K = K0 + (int)(threadIdx.x & 31);
+    const bool lv = K < n_k && kblock_live_group<kCl, kF4>(p, r, I0, J, K);
+    return __ballot_sync(0xffffffffu, lv);
+}
+
 // Output tile t of this rank -> (output o, row tile I, column tile J).  Tiles of one output
 // are walked in groups of kGroup row tiles, columns outer: a wave of ~148 CTAs then covers
 // a kGroup x ~18 patch whose operand blocks (A: kGroup*128 rows, B: ~18*256 rows of the
@@ -398,32 +409,38 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
 
     if (warp == 0) {
         // ------------------------------- TMA producer -------------------------------
-        if (lane == 0) {
-            int stage = 0;
-            uint32_t phase = 0;
-            for (int t = unit; t < total_tiles; t += n_units) {
-                int o, I2, J;
-                tile_coords(p, t, tiles_per_nt, n_i, n_j, o, I2, J);
-                const int I0 = p.i_lo + I2 * kCl, I = I0 + (int)crank;
-                for (int q = p.rule_ptr[o]; q < p.rule_ptr[o + 1]; ++q) {
-                    const DenseRule r = p.rules[q];
-                    const int64_t arow = __ldg(mapA_row + r.B) + (int64_t)I * kTM;
-                    const int64_t brow = __ldg(mapB_row + r.C) + (int64_t)J * kTN;
-                    for (int K = 0; K < n_k; ++K) {
-                        if (!kblock_live_group<kCl, kF4>(p, r, I0, J, K)) continue;
-                        mbar_wait(&empty[stage], phase ^ 1);
-                        mbar_expect_tx(&full[stage], SB_);
-                        tma_load_2d(sA + stage * AB_, &tmA, &full[stage], K * kKB, (int)arow);
-                        if (kCl == 1)
-                            tma_load_2d(sB + stage * BB_, &tmB, &full[stage], K * kKB, (int)brow);
-                        else
-                            tma_load_2d_mc(sB + stage * BB_ + crank * (BB_ / 2), &tmB, &full[stage], K * kKB,
-                                           (int)(brow + crank * (kTN / 2)), (uint16_t)0x3);
-                        if (++stage == S_) {
-                            stage = 0;
-                            phase ^= 1;
+        // the warp computes the skip list 32 K blocks at a time; lane 0 issues the loads
+        int stage = 0;
+        uint32_t phase = 0;
+        for (int t = unit; t < total_tiles; t += n_units) {
+            int o, I2, J;
+            tile_coords(p, t, tiles_per_nt, n_i, n_j, o, I2, J);
+            const int I0 = p.i_lo + I2 * kCl, I = I0 + (int)crank;
+            for (int q = p.rule_ptr[o]; q < p.rule_ptr[o + 1]; ++q) {
+                const DenseRule r = p.rules[q];
+                const int64_t arow = __ldg(mapA_row + r.B) + (int64_t)I * kTM;
+                const int64_t brow = __ldg(mapB_row + r.C) + (int64_t)J * kTN;
+                for (int K0 = 0; K0 < n_k; K0 += 32) {
+                    uint32_t m = live_mask32<kCl, kF4>(p, r, I0, J, K0, n_k);
+                    if (lane == 0) {
+                        while (m) {
+                            const int K = K0 + __ffs(m) - 1;
+                            m &= m - 1u;
+                            mbar_wait(&empty[stage], phase ^ 1);
+                            mbar_expect_tx(&full[stage], SB_);
+                            tma_load_2d(sA + stage * AB_, &tmA, &full[stage], K * kKB, (int)arow);
+                            if (kCl == 1)
+                                tma_load_2d(sB + stage * BB_, &tmB, &full[stage], K * kKB, (int)brow);
+                            else
+                                tma_load_2d_mc(sB + stage * BB_ + crank * (BB_ / 2), &tmB, &full[stage], K * kKB,
+                                               (int)(brow + crank * (kTN / 2)), (uint16_t)0x3);
+                            if (++stage == S_) {
+                                stage = 0;
+                                phase ^= 1;
+                            }
                         }
                     }
+                    __syncwarp();
                 }
             }
         }
@@ -447,8 +464,10 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
             unsigned long long kb_issued = 0;
             for (int q = p.rule_ptr[o]; q < p.rule_ptr[o + 1]; ++q) {
                 const DenseRule r = p.rules[q];
-                for (int K = 0; K < n_k; ++K) {
-                    if (!kblock_live_group<kCl, kF4>(p, r, I0, J, K)) continue;
+                for (int K0 = 0; K0 < n_k; K0 += 32) {
+                uint32_t m = live_mask32<kCl, kF4>(p, r, I0, J, K0, n_k);
+                while (m) {
+                    m &= m - 1u;
                     kb_issued += (kTN / 32) * (kF4 ? 2 : 1);   // in 128 x 32 x 128 units of MMA work
                     mbar_wait(&full[stage], phase);
                     tc_fence_after();
@@ -474,6 +493,7 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
                         stage = 0;
                         phase ^= 1;
                     }
+                }
                 }
             }
             if (lane == 0) {
@@ -501,7 +521,7 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
             const int A = p.out_nt[o];
             bool live = false;   // the pair issued MMAs for this tile (else TMEM holds no result)
             for (int q = p.rule_ptr[o]; q < p.rule_ptr[o + 1] && !live; ++q)
-                for (int K = 0; K < n_k && !live; ++K) live = kblock_live_group<kCl, kF4>(p, p.rules[q], I0, J, K);
+                for (int K0 = 0; K0 < n_k && !live; K0 += 32) live = live_mask32<kCl, kF4>(p, p.rules[q], I0, J, K0, n_k) != 0;
             // this row's 8 old words (32 contiguous bytes of T_{k-1}) load while the MMAs run
             const int row = I * kTM + quarter * 32 + lane;
             const bool wr = mine && row < p.n;
@@ -681,7 +701,7 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
 
     if (warp == 0) {
         // ------------------------------- TMA producer (both CTAs) -------------------------------
-        if (lane == 0) {
+        {
             const uint32_t full0 = mapa_cta(smem_u32(&full[0]), 0);   // leader's full barriers
             int stage = 0;
             uint32_t phase = 0;
@@ -693,8 +713,12 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
                     const DenseRule r = p.rules[q];
                     const int64_t arow = __ldg(mapA_row + r.B) + (int64_t)I * kTM;
                     const int64_t brow = __ldg(mapB_row + r.C) + (int64_t)J * kTN + (int64_t)crank * (kTN / 2);
-                    for (int K = 0; K < n_k; ++K) {
-                        if (!kblock_live_group<2, kF4>(p, r, I0, J, K)) continue;
+                    for (int K0 = 0; K0 < n_k; K0 += 32) {
+                    uint32_t m = live_mask32<2, kF4>(p, r, I0, J, K0, n_k);
+                    if (lane == 0)
+                    while (m) {
+                        const int K = K0 + __ffs(m) - 1;
+                        m &= m - 1u;
                         mbar_wait(&empty[stage], phase ^ 1);
                         const uint32_t fb = full0 + (uint32_t)(stage * 8);
                         // no cluster-scope arrive from the peer: its TMA bytes complete on the
@@ -707,6 +731,8 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
                             stage = 0;
                             phase ^= 1;
                         }
+                    }
+                    __syncwarp();
                     }
                 }
             }
@@ -731,8 +757,10 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
                 unsigned long long kb_issued = 0;
                 for (int q = p.rule_ptr[o]; q < p.rule_ptr[o + 1]; ++q) {
                     const DenseRule r = p.rules[q];
-                    for (int K = 0; K < n_k; ++K) {
-                        if (!kblock_live_group<2, kF4>(p, r, I0, J, K)) continue;
+                    for (int K0 = 0; K0 < n_k; K0 += 32) {
+                    uint32_t m = live_mask32<2, kF4>(p, r, I0, J, K0, n_k);
+                    while (m) {
+                        m &= m - 1u;
                         kb_issued += 2 * (kTN / 32) * (kF4 ? 2 : 1);   // 128x32x128 units: two row tiles, fp4 twice as deep
                         mbar_wait(&full[stage], phase);
                         tc_fence_after();
@@ -756,6 +784,7 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
                             stage = 0;
                             phase ^= 1;
                         }
+                    }
                     }
                 }
                 if (lane == 0) {
@@ -790,7 +819,7 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
             const int A = p.out_nt[o];
             bool live = false;
             for (int q = p.rule_ptr[o]; q < p.rule_ptr[o + 1] && !live; ++q)
-                for (int K = 0; K < n_k && !live; ++K) live = kblock_live_group<2, kF4>(p, p.rules[q], I0, J, K);
+                for (int K0 = 0; K0 < n_k && !live; K0 += 32) live = live_mask32<2, kF4>(p, p.rules[q], I0, J, K0, n_k) != 0;
             const int row = I * kTM + quarter * 32 + lane;
             const bool wr = mine && row < p.n;
             uint4 o0 = make_uint4(0, 0, 0, 0), o1 = o0;
