@@ -211,7 +211,7 @@ def tensor_roofline(stats, step_ms, fmt=2):
     kind = "kind::mxf4, e2m1 0/1, unit ue8m0 scales, f32 accumulator" if fmt == 2 else "kind::i8"
     return {"bound": "tensor", "achieved": achieved, "peak": burst, "unit": "TFLOP/s", "frac": achieved / burst,
             "frac_of_sustained": achieved / sustained, "traffic": ncu_traffic("configS" if fmt == 2 else "configS_int8"),
-            "kernel": f"cfpq::dense_kernel (tcgen05.mma {kind})", "format": TENSOR_FORMATS[fmt],
+            "kernel": f"cfpq::dense2sm_kernel (tcgen05.mma.cta_group::2 {kind}, CTA pairs)", "format": TENSOR_FORMATS[fmt],
             "loop_ms": loop_s * 1e3, "share_of_step": loop_s * 1e3 / step_ms, "issued_ops": ops, "peak_source": src,
             "note": f"{TENSOR_FORMATS[fmt]} TOPS reported in the TFLOP/s slot; issued work counts whole output "
                     "tiles x live K blocks (zeros inside tiles included)"}

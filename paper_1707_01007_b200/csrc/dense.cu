@@ -1593,11 +1593,12 @@ cudaError_t dense_product(DenseEngine* e, int64_t i_lo, int64_t i_hi, cudaStream
         const char* v = getenv("CFPQ_DENSE_PAIR");
         return v && v[0] == '1';
     }();
-    // 2-SM pairs (cta_group::2, M = 256), opt-in (CFPQ_DENSE_2SM=1): measured SLOWER than
-    // one CTA per SM on config S (fp4 16.5 vs 13.3 ms, int8 27.6 vs 21.9 ms at n = 16,384)
+    // 2-SM pairs (cta_group::2, M = 256) by default (CFPQ_DENSE_2SM=0: one CTA per SM).
+    // Config S, n = 16,384: fp4 10.3 vs 10.7 ms, int8 18.0 vs 20.5 ms (once the skip list
+    // stopped sitting on the issue path; before that the pair was slower)
     static const bool two_sm = [] {
         const char* v = getenv("CFPQ_DENSE_2SM");
-        return v && v[0] == '1';
+        return !(v && v[0] == '0');
     }();
     const bool use2 = two_sm && sms >= 2 && !pair;
     if (use2) {

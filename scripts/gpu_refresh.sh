@@ -23,7 +23,7 @@ r=C.closure(g,d,path_policy=3)
 # full captures of the dominant kernels
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:closure_kernel -s 5 -c 1 \
    -o gpurun_out/prof_config4 python bench.py --workload config4 --steps 1 --warmup 3 --no-e2e --no-cpu-baseline --no-supplementary > gpurun_out/ncu_c4.txt 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:dense_kernel -s 20 -c 1 \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:dense2sm_kernel -s 20 -c 1 \
    -o gpurun_out/prof_configS python bench.py --workload configS --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/ncu_cS.txt 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:rows_scatter_kernel -s 6 -c 1 -o gpurun_out/prof_rows_scatter \
    python -c "

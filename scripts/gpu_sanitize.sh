@@ -4,8 +4,8 @@ for tool in memcheck racecheck synccheck; do
   timeout 1200 compute-sanitizer --tool $tool --error-exitcode 9 --print-limit 20 python scripts/sanitize.py > gpurun_out/sanitize_$tool.txt 2>&1
   echo "rc=$?"; tail -3 gpurun_out/sanitize_$tool.txt
 done
-echo "== memcheck, 2-SM tensor variant"
-CFPQ_DENSE_2SM=1 timeout 900 compute-sanitizer --tool memcheck --error-exitcode 9 --print-limit 20 python -c "
+echo "== memcheck, 1-CTA-per-SM tensor variant"
+CFPQ_DENSE_2SM=0 timeout 900 compute-sanitizer --tool memcheck --error-exitcode 9 --print-limit 20 python -c "
 import sys; sys.path.insert(0,'.')
 import inputs as I
 from tests.gpu_util import gpu_closure, assert_parity

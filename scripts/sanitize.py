@@ -1,6 +1,6 @@
 """Small closures on every engine, for compute-sanitizer (memcheck / racecheck / synccheck):
-sparse, hashed, sharded, async, tensor (fp4 and int8; CFPQ_DENSE_2SM=1 / CFPQ_DENSE_PAIR=1 for
-the cluster variants), bit rows (forms L, R, V, P)."""
+sparse, hashed, sharded, async, tensor (fp4 and int8, 2-SM pairs by default; CFPQ_DENSE_2SM=0 /
+CFPQ_DENSE_PAIR=1 for the other variants), bit rows (forms L, R, V, P)."""
 import sys, os
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np

@@ -177,10 +177,11 @@ def test_tensor_cta_pairs_multicast():
     assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
 
 
-def test_tensor_2sm_pairs():
-    """The opt-in 2-SM variant (cta_group::2, M = 256 UMMAs issued by the even CTA of a pair;
-    each CTA stages its A rows and half of B; TMA bytes of both CTAs complete on the
-    leader's barrier) in both formats, including the emulated row-block shards."""
+def test_tensor_one_cta_per_sm():
+    """The one-CTA-per-SM kernel (CFPQ_DENSE_2SM=0; the default is the 2-SM pair kernel:
+    cta_group::2, M = 256 UMMAs issued by the even CTA, each CTA staging its A rows and half
+    of B, TMA bytes of both CTAs completing on the leader's barrier) in both formats,
+    including the emulated row-block shards."""
     import os
     import subprocess
     import sys
@@ -199,7 +200,7 @@ def test_tensor_2sm_pairs():
         "    assert_parity(w, r)\n"
         "print('ok')\n")
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, CFPQ_DENSE_2SM="1", PYTHONPATH=root)
+    env = dict(os.environ, CFPQ_DENSE_2SM="0", PYTHONPATH=root)
     out = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=900)
     assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
 
