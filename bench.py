@@ -642,7 +642,7 @@ def main():
                                            + (": Δ index lists)" if pol != 2 else ": dense row blocks)")
                                            if sharded else f"{world} independent replicas (seed+rank)")
                            if world > 1 else "1 GPU",
-                           "engine": "dense tcgen05 int8" if pol == 2 else "sparse semi-naive persistent kernel",
+                           "engine": ("dense tcgen05 int8 (kind::i8)" if args.tensor_format == 1 else "dense tcgen05 fp4 (kind::mxf4)") + ", CTA pairs" if pol == 2 else "sparse semi-naive persistent kernel",
                            "seed_phase_ms": statistics.mean(seed_ns) * 1e-6},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": int(launches), "clocks": clk.summary(), "supplementary": supp}
