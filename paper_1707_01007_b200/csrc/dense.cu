@@ -220,6 +220,11 @@ __device__ __forceinline__ uint32_t spread4_byte(uint32_t x) {   // 4 bits -> 4 
 template <bool kF4>
 __global__ void __launch_bounds__(128) pack_kernel(const uint32_t* __restrict__ T, int32_t n, int64_t Wp, int32_t np,
                                                    uint8_t* T8, uint8_t* T8T, uint8_t* occ, int32_t nt_tiles) {
+    // both packs of the tile are built in shared memory, then copied out with consecutive
+    // lanes on consecutive 16-byte pieces of the same output rows (coalesced stores)
+    constexpr int kRB = kF4 ? kTM / 2 : kTM;   // bytes of one packed tile row (64 fp4, 128 int8)
+    __shared__ __align__(16) uint8_t s_rm[kTM * kRB];   // row-major pack of the tile
+    __shared__ __align__(16) uint8_t s_tr[kTM * kRB];   // transposed pack of the tile
     __shared__ int any;
     const int tI = blockIdx.y, tK = blockIdx.x;
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
@@ -230,31 +235,24 @@ __global__ void __launch_bounds__(128) pack_kernel(const uint32_t* __restrict__ 
     const uint32_t w[4] = {v.x, v.y, v.z, v.w};
     __syncthreads();
     if (__any_sync(0xffffffffu, (v.x | v.y | v.z | v.w) != 0) && lane == 0) any = 1;
-    const int64_t rb = kF4 ? np / 2 : np;   // bytes per packed row
+    const int64_t rb = kF4 ? np / 2 : np;   // bytes per packed row in HBM
     if (T8) {
-        uint8_t* dst = T8 + (size_t)row * rb + (size_t)tK * kTM / (kF4 ? 2 : 1);
+        uint4* dst = reinterpret_cast<uint4*>(s_rm + t * kRB);
         if (kF4) {
-            uint32_t o[16];
 #pragma unroll
             for (int q = 0; q < 4; ++q)
-#pragma unroll
-                for (int h = 0; h < 4; ++h) o[q * 4 + h] = spread8_nib(w[q] >> (8 * h));
-#pragma unroll
-            for (int q = 0; q < 4; ++q)
-                reinterpret_cast<uint4*>(dst)[q] = make_uint4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
+                dst[q] = make_uint4(spread8_nib(w[q]), spread8_nib(w[q] >> 8), spread8_nib(w[q] >> 16),
+                                    spread8_nib(w[q] >> 24));
         } else {
 #pragma unroll
             for (int q = 0; q < 8; ++q) {
                 const uint32_t x = w[q >> 1] >> ((q & 1) * 16);
-                reinterpret_cast<uint4*>(dst)[q] =
-                    make_uint4(spread4_byte(x), spread4_byte(x >> 4), spread4_byte(x >> 8), spread4_byte(x >> 12));
+                dst[q] = make_uint4(spread4_byte(x), spread4_byte(x >> 4), spread4_byte(x >> 8), spread4_byte(x >> 12));
             }
         }
     }
     if (T8T) {
-        // column c of the tile = packed row tK*128 + c; this warp's 32 source rows are
-        // elements tI*128 + 32*warp .. +31 of it.  32 ballots per group of 32 columns: lane j
-        // keeps column 32g + j's mask, then the whole warp stores once.
+        // column c = 32g + j: one ballot gives the warp's 32 row bits; lane j keeps its column
 #pragma unroll
         for (int g = 0; g < kTM / 32; ++g) {
             uint32_t mine = 0;
@@ -263,12 +261,12 @@ __global__ void __launch_bounds__(128) pack_kernel(const uint32_t* __restrict__ 
                 const uint32_t m = __ballot_sync(0xffffffffu, (w[g] >> j) & 1u);
                 if (lane == j) mine = m;
             }
-            uint8_t* dst = T8T + (size_t)(tK * kTM + 32 * g + lane) * rb + ((size_t)tI * kTM + 32 * warp) / (kF4 ? 2 : 1);
+            uint8_t* d = s_tr + (32 * g + lane) * kRB + (32 * warp) / (kF4 ? 2 : 1);
             if (kF4) {
-                *reinterpret_cast<uint4*>(dst) =
+                *reinterpret_cast<uint4*>(d) =
                     make_uint4(spread8_nib(mine), spread8_nib(mine >> 8), spread8_nib(mine >> 16), spread8_nib(mine >> 24));
             } else {
-                uint4* d4 = reinterpret_cast<uint4*>(dst);
+                uint4* d4 = reinterpret_cast<uint4*>(d);
                 d4[0] = make_uint4(spread4_byte(mine), spread4_byte(mine >> 4), spread4_byte(mine >> 8),
                                    spread4_byte(mine >> 12));
                 d4[1] = make_uint4(spread4_byte(mine >> 16), spread4_byte(mine >> 20), spread4_byte(mine >> 24),
@@ -277,6 +275,19 @@ __global__ void __launch_bounds__(128) pack_kernel(const uint32_t* __restrict__ 
         }
     }
     __syncthreads();
+    // copy out: kRB/16 pieces per row, consecutive threads on consecutive pieces
+    constexpr int kPieces = kTM * kRB / 16;
+    const size_t col_byte = (size_t)tK * kRB;
+    const size_t tcol_byte = (size_t)tI * kRB;
+    for (int e = t; e < kPieces; e += 128) {
+        const int r = e / (kRB / 16), pc = e % (kRB / 16);
+        if (T8)
+            *reinterpret_cast<uint4*>(T8 + (size_t)(tI * kTM + r) * rb + col_byte + pc * 16) =
+                reinterpret_cast<const uint4*>(s_rm + r * kRB)[pc];
+        if (T8T)
+            *reinterpret_cast<uint4*>(T8T + (size_t)(tK * kTM + r) * rb + tcol_byte + pc * 16) =
+                reinterpret_cast<const uint4*>(s_tr + r * kRB)[pc];
+    }
     if (t == 0 && occ) occ[(size_t)tI * nt_tiles + tK] = any ? 1 : 0;
 }
 
@@ -998,7 +1009,9 @@ constexpr int kPlanRules = 64;   // rule forms cached in shared memory up to thi
 __global__ void rows_plan_kernel(DenseParams p, RowsCtx c, RowChunk* chunks, unsigned long long cap) {
     __shared__ int32_t s_form[kPlanRules], s_B[kPlanRules];
     __shared__ const int32_t* s_ptr[kPlanRules];
-    const int lane = threadIdx.x & 31;
+    __shared__ int32_t s_wsum[3][32];
+    __shared__ unsigned long long s_base[3];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const bool cached = c.n_rules <= kPlanRules;
     if (cached) {
         for (int q = threadIdx.x; q < c.n_rules; q += blockDim.x) {
@@ -1054,38 +1067,45 @@ __global__ void rows_plan_kernel(DenseParams p, RowsCtx c, RowChunk* chunks, uns
             }
             nch = (len + per - 1) / per;
         }
-        {
-            // L chunks (rank ranges of the set bits of T_B[i]) / one P task per row
-            int incl = lp;
+        // three lists: 0 = R chunks (rc[0]), 1 = V chunks (rc[3]), 2 = L chunks / P tasks (rc[4]).
+        // Warp inclusive scans, then one atomic per list per CTA (not per warp: the three
+        // counters are hot), bases handed back through shared memory
+        const int cntv[3] = {isv ? 0 : nch, isv ? nch : 0, lp};
+        int incl[3];
+#pragma unroll
+        for (int l = 0; l < 3; ++l) {
+            incl[l] = cntv[l];
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
-                int v = __shfl_up_sync(0xffffffffu, incl, o);
-                if (lane >= o) incl += v;
+                int v = __shfl_up_sync(0xffffffffu, incl[l], o);
+                if (lane >= o) incl[l] += v;
             }
-            unsigned long long base = 0;
-            if (lane == 31 && incl) base = atomicAdd(c.rc + 4, (unsigned long long)incl);
-            base = __shfl_sync(0xffffffffu, base, 31);
-            unsigned long long at = base + (unsigned long long)(incl - lp);
-            for (int h = 0; h < lp; ++h, ++at)
-                if (at < cap) chunks[2 * cap + at] = RowChunk{q, i, h * kChunkL, lpl ? min(kChunkL, lpl - h * kChunkL) : 0};
+            if (lane == 31) s_wsum[l][warp] = incl[l];
         }
+        __syncthreads();
+        if (threadIdx.x < 3) {
+            const int l = threadIdx.x;
+            unsigned long long tot = 0;
+            for (int q2 = 0; q2 < (int)(blockDim.x >> 5); ++q2) tot += (unsigned long long)s_wsum[l][q2];
+            s_base[l] = tot ? atomicAdd(c.rc + (l == 0 ? 0 : (l == 1 ? 3 : 4)), tot) : 0ull;
+        }
+        __syncthreads();
 #pragma unroll
-        for (int lst = 0; lst < 2; ++lst) {
-            const int mine = (isv == lst) ? nch : 0;
-            int incl = mine;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                int v = __shfl_up_sync(0xffffffffu, incl, o);
-                if (lane >= o) incl += v;
+        for (int l = 0; l < 3; ++l) {
+            unsigned long long at = s_base[l];
+            for (int q2 = 0; q2 < warp; ++q2) at += (unsigned long long)s_wsum[l][q2];
+            at += (unsigned long long)(incl[l] - cntv[l]);
+            if (l < 2) {
+                RowChunk* out = chunks + (l ? cap : 0);
+                for (int h = 0; h < cntv[l]; ++h, ++at)
+                    if (at < cap) out[at] = RowChunk{q, i, h * per, min(per, len - h * per)};
+            } else {
+                for (int h = 0; h < lp; ++h, ++at)
+                    if (at < cap)
+                        chunks[2 * cap + at] = RowChunk{q, i, h * kChunkL, lpl ? min(kChunkL, lpl - h * kChunkL) : 0};
             }
-            unsigned long long base = 0;
-            if (lane == 31 && incl) base = atomicAdd(c.rc + (lst ? 3 : 0), (unsigned long long)incl);
-            base = __shfl_sync(0xffffffffu, base, 31);
-            unsigned long long at = base + (unsigned long long)(incl - mine);
-            RowChunk* out = chunks + (lst ? cap : 0);
-            for (int h = 0; h < mine; ++h, ++at)
-                if (at < cap) out[at] = RowChunk{q, i, h * per, min(per, len - h * per)};
         }
+        __syncthreads();   // s_wsum / s_base are rewritten by the next iteration
     }
 }
 
