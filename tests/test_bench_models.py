@@ -41,3 +41,17 @@ def test_rows_alg_bytes_union_grammar_runs():
     # at least one bit-row scan per iteration of a non-empty S row (form L)
     assert total >= 4 * W * s.iterations
     assert isinstance(total, (int, np.integer))
+
+
+def test_tensor_roofline_accounting():
+    """bench.tensor_roofline: issued MMA work is counted in 128 x 32 x 128 units (an M=128 x
+    N=256 x K=128 int8 k-block = 8 units, a 256-deep fp4 k-block = 16), the fp4 peak is twice
+    the int8 one (nominal fp4 / int8 = 9 / 4.5), both derived from the same bf16 figure."""
+    stats = {"mma_kblocks": 8 * 1000, "loop_ns": 1e6}
+    r8 = bench.tensor_roofline(stats, 1.0, fmt=1)
+    r4 = bench.tensor_roofline(stats, 1.0, fmt=2)
+    ops = 1000 * 2 * 128 * 256 * 128
+    assert r8["issued_ops"] == ops and r4["issued_ops"] == ops
+    assert abs(r8["achieved"] - ops / 1e-3 / 1e12) < 1e-6
+    assert abs(r4["peak"] - 2 * r8["peak"]) < 1e-6
+    assert abs(r4["frac_of_nominal"] * 9000.0 - r8["frac_of_nominal"] * 4500.0) < 1e-6
