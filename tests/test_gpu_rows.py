@@ -119,3 +119,17 @@ def test_config4_full_size_engines_agree():
         rq, _, _ = gpu_closure(wq, path_policy=1)
         A = w.nt_names.index("S_Q1" if q == "q1" else "S_Q2")
         assert np.array_equal(rq.pairs(wq.start), r1.pairs(A)), q
+
+
+def test_rows_wider_than_config4():
+    """n = 100,003 (ragged, 3,126 words per row: more scan batches per L chunk and 13 row
+    slices per R chunk than config 4's 8 KiB rows): Q1 on the bit-row path equals the sparse
+    engine, per iteration."""
+    import numpy as np
+    w = I.ontology_workload("q1", 100_003, depth=9, seed=11)
+    r3, _, _ = gpu_closure(w, path_policy=3)
+    r1, _, _ = gpu_closure(w, path_policy=1)
+    assert r3.iterations == r1.iterations
+    assert r3.iteration_stats()[0].tolist() == r1.iteration_stats()[0].tolist()
+    for A in range(w.n_nt):
+        assert np.array_equal(r3.pairs(A), r1.pairs(A)), w.nt_names[A]
