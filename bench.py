@@ -5,22 +5,27 @@ One step = one full closure of the workload: seed T_0 from the edges
 run T <- T ∪ T×T to the fixpoint, inputs resident in HBM.  Default
 workload = SURVEY §8(d) config 4: the 10-NT Q1∪Q2 union grammar on a 64k-node
 ontology-shaped graph (the largest config, the one BASELINE's metric quotes at
-1/2/4/8 GPUs).  value = effective boolean Gop/s = 2 x (AND-true triples of the
-Jacobi products T_{k-1} x T_{k-1} summed over iterations, i.e. the work of Alg. 1
-line 9 on sparse operands) / closure time; ms_per_step = closure time.
+1/2/4/8 GPUs).
+
+value = effective boolean Gop/s of the EXECUTED schedule (SURVEY §8(d) "useful boolean
+ops ... summed over the semi-naive pairs"): 2 x the (Δ entry, neighbour) pairs the
+semi-naive engine expands (stats.candidates: AND-true triples of Δ_B x T_C and T_B x Δ_C
+on the operand sides the engine expands) / closure time.  The dense tensor engine executes
+full Jacobi products, so its numerator is 2 x the AND-true triples of T_{k-1} x T_{k-1}.
+The Jacobi-equivalent rate (2 x AND-true triples of Alg. 1 line 9 on sparse operands,
+identical for every exact schedule) is reported beside it as `jacobi_equivalent`.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--workload config4|config3|config5|config2|configS]
   python bench.py --impl reference ...   # the CPU oracle as the reference arm
 
 Multi-GPU (torchrun, N>1): one process per GPU; time = max over ranks of the
-device-timed region.  configS closes ONE problem row-block sharded over the ranks
-(dense row blocks all-gathered over NCCL every iteration): "scaling": "strong".  config4's
-closure is latency-bound (~20 dependent iterations of ~25 us, SURVEY V-9), so its headline
-at N>1 is N independent seeded problems, one per GPU, no data-path collective ("scaling":
-"weak"); the row-block sharded closure of ONE config-4 problem (north_star / SURVEY §8(e):
-each rank derives the cells of its rows, Δ_k exchanged as index lists over NCCL) is timed
-beside it as supplementary.row_sharded, or as the headline with --sharded.  config2/3/5:
-replicas.
+device-timed region.  config 4 and config S close ONE problem row-block sharded over the
+ranks ("scaling": "strong"): config 4 on the sparse engine (each rank derives the cells
+of its rows, Δ_k exchanged as index lists over NCCL every iteration) with the
+paper-faithful bit-row engine sharded the same way as a supplement (Δ word lists
+exchanged); config S on the tcgen05 engine (row blocks all-gathered).  N independent
+seeded replicas are timed as a supplement (--replicas makes them the headline).
+config2/3/5: replicas.
 """
 from __future__ import annotations
 
@@ -345,48 +350,43 @@ def supplementary_rows(C, w, g, d, r_sparse, stream, steps=2):
                                  "output word touched, 32 B per Delta word"}}
 
 
-def supplementary_row_sharded(C, args, rank, world, stream, dist):
-    """Config 4 (seed args.seed) closed as ONE problem row-block sharded over the ranks: each
-    rank derives its rows' cells, Δ_k is all-gathered as index lists (NCCL) every iteration.
-    Time = max over ranks of the device-timed closure."""
+def supplementary_replicas(C, args, rank, world, stream, dist):
+    """N > 1: N independent seeded config-4 problems (seed + rank), one per GPU, single-GPU
+    engine, no data-path collective ("scaling": "weak").  Time = max over ranks."""
     import torch
-    w, _ = make_workload("config4", args.seed)
-    uid = torch.zeros(128, dtype=torch.uint8, device="cuda")
-    if rank == 0:
-        uid.copy_(torch.tensor(list(C.nccl_unique_id()), dtype=torch.uint8))
-    dist.broadcast(uid, src=0)
-    kw = {"world_size": world, "rank": rank, "nccl_unique_id": bytes(uid.cpu().tolist())}
+    w, _ = make_workload(args.workload, args.seed + rank)
     g = C.Grammar.from_workload(w)
     d = C.Graph(w.n_nodes, torch.from_numpy(w.edges).cuda(), stream=stream)
-    ops = jacobi_ops(w, "config4", g, d, C, stream)
-    r = C.closure(g, d, stream=stream, **kw)
+    r = C.closure(g, d, stream=stream)
+    useful = 2 * int(r.stats()["candidates"])
     for _ in range(args.warmup):
-        C.closure_reuse(g, d, r, stream=stream, **kw)
+        C.closure_reuse(g, d, r, stream=stream)
     torch.cuda.synchronize()
     dist.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(args.steps):
-        C.closure_reuse(g, d, r, stream=stream, **kw)
+        C.closure_reuse(g, d, r, stream=stream)
     e1.record(stream)
     torch.cuda.synchronize()
-    t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms = float(t.item()) / args.steps
-    return {"workload": "config4 seed %d, one problem over %d GPUs" % (args.seed, world), "ms_per_step": ms,
-            "value": ops / (ms * 1e-3) / 1e9, "unit": "Gop/s", "iterations": r.iterations,
-            "cells": int(r.stats()["cells"]), "scaling": "strong",
-            "note": "latency-bound: one collective round per iteration dominates (DESIGN §3.5)"}
+    t = torch.tensor([e0.elapsed_time(e1), float(useful)], dtype=torch.float64, device="cuda")
+    tm, us = t[0:1].clone(), t[1:2].clone()
+    dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+    dist.all_reduce(us, op=dist.ReduceOp.SUM)
+    ms = float(tm.item()) / args.steps
+    return {"workload": "%d independent config-4 problems (seed + rank), one per GPU" % world, "ms_per_step": ms,
+            "value": float(us.item()) / (ms * 1e-3) / 1e9, "unit": "Gop/s", "scaling": "weak"}
 
 
 # ------------------------------------------------------------------------------------------
-# reference arm: the CPU oracle as it stands, on a bounded sample of the workload
+# CPU baselines: the oracle (reference arm / cpu_baseline, bounded sample) and the
+# independent OpenMP bitset program (cpu_bitset, the full benched configuration)
 # ------------------------------------------------------------------------------------------
 
-def oracle_sample(name: str, seed: int):
+def oracle_sample(name: str, seed: int, n4: int = 2048):
     import inputs as I
     if name == "config4":
-        return I.config4_workload(seed=seed, n=2048), "config-4 generator at n=2048 (depth 10): full closure"
+        return I.config4_workload(seed=seed, n=n4), f"config-4 generator at n={n4} (depth 10): full closure"
     if name in ("config3", "config5"):
         return I.anbn_workload(2, 255), "a^n b^n p=2, q=255 (n=256, 1021 iterations): full closure"
     if name == "config2":
@@ -395,17 +395,32 @@ def oracle_sample(name: str, seed: int):
     return I.dense_stress_workload(320, 2, seed), "S->SS|a on G(320, 640): full closure"
 
 
-def time_oracle(name: str, seed: int, reps: int = 1):
+def sample_numerator(name: str, w):
+    """The work unit of `value` on a CPU sample, in the same definition as our arm: 2 x the
+    semi-naive (Δ entry, neighbour) pairs (counted by the independent bitset program, whose
+    expansion rules are the engine's: tests/test_gpu_units.py) — or, for the dense config S,
+    2 x the Jacobi AND-true triples (the oracle's own count)."""
+    if name == "configS":
+        return None
+    import cpu_baseline as CB
+    b = CB.BitsetBaseline(w)
+    k = b.run(w.edges)
+    _, cand = b.iteration_stats(k)
+    return 2 * int(cand.sum())
+
+
+def time_oracle(name: str, seed: int, reps: int = 1, n4: int = 2048):
     import oracle as O
-    w, sample = oracle_sample(name, seed)
+    w, sample = oracle_sample(name, seed, n4)
     lengths = name == "config5"
+    num = sample_numerator(name, w)
     ts, ops = [], 0
     for _ in range(reps):
         t0 = time.perf_counter()
         res = O.run(w, lengths=lengths)
         ts.append(time.perf_counter() - t0)
-        ops = 2 * int(res.stats()["jacobi_triples"].sum())
-    return ops, ts, sample
+        ops = num if num is not None else 2 * int(res.stats()["jacobi_triples"].sum())
+    return ops, ts, sample, w
 
 
 def run_reference(args):
@@ -413,24 +428,61 @@ def run_reference(args):
     if rank != 0:
         return 0
     _, desc = make_workload(args.workload, args.seed)
-    for _ in range(args.warmup):
+    _, _, sample, sw = time_oracle(args.workload, args.seed)   # warm the oracle build / sample
+    for _ in range(max(args.warmup - 1, 0)):
         time_oracle(args.workload, args.seed)
     ops, ts = 0, []
     for _ in range(args.steps):
-        o, t, sample = time_oracle(args.workload, args.seed)
+        o, t, sample, sw = time_oracle(args.workload, args.seed)
         ops += o
         ts += t
     total = sum(ts)
     value = ops / total / 1e9
     ms = 1e3 * total / len(ts)
+    sdesc = {"what": sample, "n_nodes": int(sw.n_nodes), "n_edges": int(len(sw.edges))}
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "set<int> cells (CPU)", "data": "synthetic",
-            "config": {**desc, "sample": sample},
+            "config": {**desc, "sample": sdesc, "same_config": False,
+                       "note": "each step closes the bounded sample (n_nodes/n_edges above), not the full "
+                               "workload; value is in the same unit as our arm (2 x semi-naive pairs of the "
+                               "instance / time), so the ratio compares rates on instances of different size"},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
+
+
+def host_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def cpu_bitset(name: str, w, r, n_nt: int, reps: int = 3):
+    """The independent OpenMP bitset program on the FULL benched instance (all host cores),
+    single-thread time beside it; its relations are checked against the GPU result's counts."""
+    if name == "configS":
+        return None
+    import cpu_baseline as CB
+    b = CB.BitsetBaseline(w)
+    cores = host_cores()
+    k = b.run(w.edges, threads=cores)
+    ts = []
+    for _ in range(reps):
+        b.run(w.edges, threads=cores)
+        ts.append(b.seconds)
+    _, cand = b.iteration_stats(k)
+    num = 2 * int(cand.sum())
+    same = k == r.iterations and all(b.count(A) == r.count(A) for A in range(n_nt))
+    b.run(w.edges, threads=1)
+    t1 = b.seconds
+    sec = statistics.median(ts)
+    return {"value": num / sec / 1e9, "unit": UNIT, "cores": cores, "kind": "bitset (uint64 rows, semi-naive, OpenMP)",
+            "sample": "the full benched instance", "seconds": sec, "single_thread_seconds": t1,
+            "single_thread_value": num / t1 / 1e9, "iterations": k, "same_relations_as_gpu": bool(same),
+            "source": "cpu_baseline/bitset_cfpq.cpp"}
 
 
 # ------------------------------------------------------------------------------------------
@@ -446,19 +498,20 @@ def main():
     ap.add_argument("--workload", default="config4", choices=["config4", "config3", "config5", "config2", "configS"])
     ap.add_argument("--tensor-format", type=int, default=0, choices=[0, 1, 2],
                     help="tensor engine operands: 0 auto (fp4), 1 int8 (kind::i8), 2 fp4 (kind::mxf4)")
+    ap.add_argument("--schedule", type=int, default=0, choices=[0, 3],
+                    help="0 Jacobi (Alg. 1 states), 3 Gauss-Seidel (in-place stages, same fixpoint)")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-supplementary", action="store_true")
     ap.add_argument("--solo", type=int, default=-1)
-    ap.add_argument("--sharded", action="store_true",
-                    help="N>1, config4: headline = ONE problem row-block sharded over the ranks (strong)")
+    ap.add_argument("--replicas", action="store_true",
+                    help="N>1, config4/configS: headline = N independent problems (weak) instead of ONE sharded problem")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
     args.warmup = max(args.warmup, 3)
 
-    import numpy as np
     import torch
     import torch.distributed as dist
 
@@ -473,9 +526,9 @@ def main():
     stream = torch.cuda.current_stream()
     dev_index = torch.cuda.current_device()
 
-    # config S / config 4 shard ONE problem by row blocks over NCCL (strong scaling); the
-    # other workloads close one independent seeded problem per GPU (weak scaling)
-    sharded = world > 1 and (args.workload == "configS" or (args.workload == "config4" and args.sharded))
+    # config 4 / config S: ONE problem row-block sharded over the ranks (strong scaling);
+    # the other workloads close one independent seeded problem per GPU (weak scaling)
+    sharded = world > 1 and args.workload in ("config4", "configS") and not args.replicas
     w, desc = make_workload(args.workload, args.seed + (0 if sharded else rank))
     shard_kw = {}
     if sharded:
@@ -488,12 +541,19 @@ def main():
     g = C.Grammar.from_workload(w)
     edges_dev = torch.from_numpy(w.edges).cuda()
     d = C.Graph(w.n_nodes, edges_dev, stream=stream)
-    ops = jacobi_ops(w, args.workload, g, d, C, stream)
-    if sharded:
-        ops = ops // world   # one problem split over the ranks: count its work once in total
     pol = policy_for(args.workload)
-    r = C.closure(g, d, stream=stream, semantics=int(lengths), solo_threshold=args.solo, path_policy=pol,
-                      tensor_format=args.tensor_format, **shard_kw)
+    kw = dict(stream=stream, semantics=int(lengths), solo_threshold=args.solo, path_policy=pol,
+              tensor_format=args.tensor_format, schedule=args.schedule)
+
+    # numerators (untimed): the executed semi-naive pairs of this instance on one GPU (the
+    # sparse engine's stats.candidates; the tensor engine executes Jacobi products) and the
+    # Jacobi-equivalent work of Alg. 1 line 9
+    jac = jacobi_ops(w, args.workload, g, d, C, stream)
+    r0 = C.closure(g, d, **kw)
+    useful = jac if pol == 2 else 2 * int(r0.stats()["candidates"])
+    del r0
+
+    r = C.closure(g, d, **kw, **shard_kw)
     iterations = r.iterations
     cells = r.stats()["cells"]
     cells_total = sum(r.count(A) for A in range(w.n_nt)) if pol == 2 else cells
@@ -504,9 +564,7 @@ def main():
     # L2 flush buffer (> 126 MB L2), written between timed steps, outside the events
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
     for _ in range(args.warmup):
-        C.closure_reuse(g, d, r, stream=stream, semantics=int(lengths), solo_threshold=args.solo, path_policy=pol,
-                      tensor_format=args.tensor_format,
-                            **shard_kw)
+        C.closure_reuse(g, d, r, **kw, **shard_kw)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -514,21 +572,20 @@ def main():
 
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
-    step_ms, loop_ns, seed_ns, launches = [], [], [], 0
+    step_ms, loop_ns, seed_ns, launches, cands = [], [], [], 0, []
     stats = None
     with ClockSampler(dev_index) as clk:
         for _ in range(args.steps):
             flush.fill_(1)
             ev0.record(stream)
-            C.closure_reuse(g, d, r, stream=stream, semantics=int(lengths), solo_threshold=args.solo, path_policy=pol,
-                      tensor_format=args.tensor_format,
-                            **shard_kw)
+            C.closure_reuse(g, d, r, **kw, **shard_kw)
             ev1.record(stream)
             ev1.synchronize()
             step_ms.append(ev0.elapsed_time(ev1))
             stats = r.stats()
             loop_ns.append(stats["loop_ns"])
             seed_ns.append(stats["seed_ns"])
+            cands.append(stats["candidates"])
             launches += stats["launches"]
     torch.cuda.synchronize()
     if world > 1:
@@ -536,24 +593,26 @@ def main():
     torch.cuda.synchronize()
     assert r.iterations == iterations and r.stats()["cells"] == cells
 
+    # whole-job work per step: one sharded problem counts once; replicas add up
     total_ms = float(sum(step_ms))
-    my = torch.tensor([total_ms, float(ops) * args.steps], dtype=torch.float64, device="cuda")
+    my = torch.tensor([total_ms, float(useful), float(jac)], dtype=torch.float64, device="cuda")
     if world > 1:
         t_max = my[0:1].clone()
         dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
-        o_sum = my[1:2].clone()
-        dist.all_reduce(o_sum, op=dist.ReduceOp.SUM)
-        total_ms_max, ops_all = float(t_max.item()), float(o_sum.item())
+        o_sum = my[1:3].clone()
+        if not sharded:
+            dist.all_reduce(o_sum, op=dist.ReduceOp.SUM)
+        total_ms_max, useful_job, jac_job = float(t_max.item()), float(o_sum[0].item()), float(o_sum[1].item())
     else:
-        total_ms_max, ops_all = total_ms, float(ops) * args.steps
-    value = ops_all / (total_ms_max * 1e-3) / 1e9
+        total_ms_max, useful_job, jac_job = total_ms, float(useful), float(jac)
+    value = useful_job * args.steps / (total_ms_max * 1e-3) / 1e9
     ms_per_step = total_ms_max / args.steps
 
     # ---- roofline of the dominant kernel (the persistent closure kernel) ----
-    # algorithmic bytes per launch: 8 B per Δ entry read, 8 B per
-    # (entry, rule) expansion (two adjacency offsets), 12 B per candidate (4 B adjacency
-    # index + 4 B read + 4 B write of its bit-matrix word), 8 B per appended cell;
-    # single-path adds 16 B per candidate (key read+write) and 8 B per entry (own key).
+    # algorithmic bytes per launch: 8 B per Δ entry read, 8 B per (entry, rule)
+    # expansion (two adjacency offsets), 12 B per candidate (4 B adjacency index + 4 B read +
+    # 4 B write of its bit-matrix word), 8 B per appended cell; single-path adds 16 B per
+    # candidate (key read+write) and 8 B per entry (own key).
     peak, peak_src = hbm_peak()
     if pol == 2:
         roofline = tensor_roofline(stats, total_ms / args.steps, 1 if args.tensor_format == 1 else 2)
@@ -589,9 +648,7 @@ def main():
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             d.set_edges(pinned, stream=stream)
-            C.closure_reuse(g, d, r, stream=stream, semantics=int(lengths), solo_threshold=args.solo, path_policy=pol,
-                      tensor_format=args.tensor_format,
-                            **shard_kw)
+            C.closure_reuse(g, d, r, **kw, **shard_kw)
             pairs = r.pairs(w.start, out=out_pairs)
             t1 = time.perf_counter()
             if it >= args.warmup:
@@ -600,15 +657,16 @@ def main():
         e_total = torch.tensor([sum(ts)], dtype=torch.float64, device="cuda")
         if world > 1:
             dist.all_reduce(e_total, op=dist.ReduceOp.MAX)
-        e2e = {"value": ops_all / float(e_total.item()) / 1e9, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
-               "d2h_bytes_per_step": int(d2h), "ms_per_step": 1e3 * float(e_total.item()) / len(ts)}
+        e2e = {"value": useful_job * len(ts) / float(e_total.item()) / 1e9, "unit": UNIT,
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "ms_per_step": 1e3 * float(e_total.item()) / len(ts)}
 
     supp = None
-    if world > 1 and args.workload == "config4" and not sharded and not args.no_supplementary:
-        # ONE config-4 problem row-block sharded over all ranks (every rank takes part)
-        rs = supplementary_row_sharded(C, args, rank, world, stream, dist)
-        if rank == 0:
-            supp = {"row_sharded": rs}
+    if world > 1 and args.workload == "config4" and not args.no_supplementary:
+        supp = {}
+        if sharded:
+            rs = supplementary_replicas(C, args, rank, world, stream, dist)
+            supp["replicas"] = rs
     if rank == 0 and world == 1 and args.workload == "config4" and not args.no_supplementary:
         supp = {}
         try:
@@ -624,11 +682,15 @@ def main():
         except Exception as ex:
             supp["paper_faithful_rows_error"] = repr(ex)
 
-    cpu = None
+    cpu = bits = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        o, t, sample = time_oracle(args.workload, args.seed)
+        o, t, sample, sw = time_oracle(args.workload, args.seed, n4=4096)
         cpu = {"value": o / sum(t) / 1e9, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample,
-               "seconds": sum(t)}
+               "sample_n_nodes": int(sw.n_nodes), "sample_n_edges": int(len(sw.edges)), "seconds": sum(t)}
+        try:
+            bits = cpu_bitset(args.workload, w, r, w.n_nt)
+        except Exception as ex:
+            bits = {"error": repr(ex)}
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -639,15 +701,27 @@ def main():
                           if pol == 2 else "u32 bit-words (boolean)"),
                 "data": "synthetic",
                 "config": {**desc, "iterations": iterations, "cells": int(cells_total),
-                           "results_start_nt": int(results_start), "useful_ops_per_step": int(ops),
+                           "results_start_nt": int(results_start),
+                           "ops_per_step": int(useful_job),
+                           "ops_definition": ("2 x Jacobi AND-true triples (the tensor engine executes full products)"
+                                              if pol == 2 else "2 x executed semi-naive (Δ entry, neighbour) pairs "
+                                              "= 2 x stats.candidates"),
+                           "candidates_per_step": int(statistics.median(cands)) if cands else None,
+                           "schedule": {0: "jacobi", 3: "gauss-seidel"}[args.schedule],
                            "l2": "flushed between steps (512 MiB write outside the timed events)",
-                           "parallelism": (f"row-block sharded over {world} GPUs (NCCL all-gather per iteration"
-                                           + (": Δ index lists)" if pol != 2 else ": dense row blocks)")
+                           "parallelism": (f"ONE problem row-block sharded over {world} GPUs (NCCL all-gather per "
+                                           "iteration" + (": Δ index lists)" if pol != 2 else ": dense row blocks)")
                                            if sharded else f"{world} independent replicas (seed+rank)")
                            if world > 1 else "1 GPU",
-                           "engine": ("dense tcgen05 int8 (kind::i8)" if args.tensor_format == 1 else "dense tcgen05 fp4 (kind::mxf4)") + ", CTA pairs" if pol == 2 else "sparse semi-naive persistent kernel",
+                           "engine": ("dense tcgen05 int8 (kind::i8)" if args.tensor_format == 1 else
+                                      "dense tcgen05 fp4 (kind::mxf4)") + ", CTA pairs" if pol == 2 else
+                                     "sparse semi-naive persistent kernel",
                            "seed_phase_ms": statistics.mean(seed_ns) * 1e-6},
-                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+                "jacobi_equivalent": {"value": jac_job * args.steps / (total_ms_max * 1e-3) / 1e9, "unit": UNIT,
+                                      "ops_per_step": int(jac_job),
+                                      "definition": "2 x AND-true triples of T_{k-1} x T_{k-1} over all iterations "
+                                                    "(Alg. 1 line 9 on sparse operands), same closure time"},
+                "roofline": roofline, "cpu_baseline": cpu, "cpu_bitset": bits, "e2e": e2e,
                 "gpu_launches": int(launches), "clocks": clk.summary(), "supplementary": supp}
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -145,6 +145,7 @@ struct cfpq_result {
     std::vector<int64_t> dense_new;           // new cells per iteration
     std::vector<int64_t> dense_jac;           // Jacobi AND-true triples per iteration (account_work)
     unsigned long long dense_kb = 0;          // issued 128x256x128 int8 MMA k-blocks
+    int32_t n_stages = 0;                     // distinct LHS NTs (Gauss-Seidel stages, schedule 3)
     int32_t n_ranks = 1;                      // row-block shards (NCCL ranks or emulated)
     int32_t my_rank = 0;
     bool emulated = false;
@@ -223,7 +224,8 @@ struct cfpq_result {
         p.has_snapshots = has_snapshots;
         p.nblocks = grid;
         p.profile = opts.record_times;
-        p.switch_cells = switch_cells;
+        p.gs_stages = opts.schedule == 3 ? n_stages : 0;
+        p.switch_cells = opts.schedule == 3 ? 0 : switch_cells;   // Gauss-Seidel stays sparse
         // read a candidate's bit before its atomicOr (skips the RMW on already-set words;
         // config 4: 0.611 vs 0.623 ms per step); flags bit 0 disables (diagnostics)
         p.precheck = (opts.reserved[0] & 1) ? 0 : 1;
@@ -298,6 +300,9 @@ static cfpq_status upload_edges(cfpq_graph* g, const int32_t* edges, int64_t n_e
     if (n_edges > 0)
         CFPQ_CUDA_TRY(cudaMemcpyAsync(g->d_edges, edges, (size_t)n_edges * 3 * sizeof(int32_t),
                                       on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
+    // the caller may free or reuse `edges` as soon as this returns (pinned host memory and
+    // device input are copied asynchronously): wait for the copy
+    if (n_edges > 0) CFPQ_CUDA_TRY(cudaStreamSynchronize(s));
     g->n_edges = n_edges;
     return CFPQ_OK;
 }
@@ -433,16 +438,38 @@ static bool make_spare(cfpq_result* r) {
 // ------------------------------------------------------------------------------------------
 // planning: per-NT tables, expansions, buffers
 // ------------------------------------------------------------------------------------------
+// Theorem 3: |V|^2 |N| changes at most -> |V|^2|N| + 1 loop bodies (max_iterations 0)
+static long long theorem3_cap(int64_t n, int32_t n_nt) {
+    double cap = (double)n * (double)n * (double)n_nt + 1.0;
+    return cap > 4e18 ? (long long)4e18 : (long long)cap;
+}
+
+// Per-iteration buffers (offsets, timestamps, phases, Jacobi work) sized for the current
+// cap (at most 2^22 recorded iterations); grown when a reuse raises the cap.
+static cfpq_status size_iteration_buffers(cfpq_result* r) {
+    const long long want = std::min<long long>(r->opts.max_iterations + 2, 1ll << 22);
+    if (want <= r->iter_off_cap && r->d_iter_off && (!r->opts.account_work || r->d_jac)) return CFPQ_OK;
+    const long long cap = std::max(want, r->iter_off_cap);
+    dfree(r->d_iter_off);
+    dfree(r->d_iter_time);
+    dfree(r->d_phase);
+    dfree(r->d_jac);
+    r->iter_off_cap = 0;
+    cfpq_status st;
+    if ((st = dalloc(&r->d_iter_off, (size_t)cap, "iteration offsets")) != CFPQ_OK) return st;
+    if ((st = dalloc(&r->d_iter_time, (size_t)cap, "iteration timestamps")) != CFPQ_OK) return st;
+    if ((st = dalloc(&r->d_phase, (size_t)cap * 4, "iteration phases")) != CFPQ_OK) return st;
+    if (r->opts.account_work && (st = dalloc(&r->d_jac, (size_t)cap, "work counts")) != CFPQ_OK) return st;
+    r->iter_off_cap = cap;
+    return CFPQ_OK;
+}
+
 static cfpq_status plan(cfpq_result* r, const cfpq_grammar* g, const cfpq_graph* d, const cfpq_options* o) {
     r->n = d->n_nodes;
     r->n_nt = g->n_nt;
     r->n_labels = g->n_labels;
     r->opts = *o;
-    if (r->opts.max_iterations <= 0) {
-        // Theorem 3: |V|^2 |N| changes at most -> |V|^2|N| + 1 loop bodies
-        double cap = (double)r->n * (double)r->n * (double)r->n_nt + 1.0;
-        r->opts.max_iterations = cap > 4e18 ? (long long)4e18 : (long long)cap;
-    }
+    if (r->opts.max_iterations <= 0) r->opts.max_iterations = theorem3_cap(r->n, r->n_nt);
     if (r->opts.solo_threshold < 0) r->opts.solo_threshold = 1024;
     r->stream = (cudaStream_t)o->cuda_stream;
     r->rules = g->rules;
@@ -476,6 +503,13 @@ static cfpq_status plan(cfpq_result* r, const cfpq_grammar* g, const cfpq_graph*
         // the bit-row path gathers rows i of a preterminal left operand from its CSR
         if (o->path_policy == 3 && bc) need_csr[rl.B] = 1;
     }
+    // Gauss-Seidel stages: the LHS NTs in id order (DESIGN reading c17)
+    std::vector<int32_t> stage_of(g->n_nt, -1);
+    r->n_stages = 0;
+    for (int A = 0; A < g->n_nt; ++A)
+        if (!g->is_const[A]) stage_of[A] = r->n_stages++;
+    for (auto& v : ex)
+        for (auto& e : v) e.stage = stage_of[e.A];
     std::vector<Expansion> exps;
     r->h_nt.assign(g->n_nt, NTInfo{});
     for (int A = 0; A < g->n_nt; ++A) {
@@ -604,12 +638,8 @@ static cfpq_status plan(cfpq_result* r, const cfpq_grammar* g, const cfpq_graph*
         CFPQ_CUDA_TRY(cudaMemcpyAsync(r->d_lab_nt, lab_nt.data(), lab_nt.size() * 4, cudaMemcpyHostToDevice, r->stream));
 
     if ((st = dalloc(&r->d_st, 1, "state")) != CFPQ_OK) return st;
-    r->iter_off_cap = std::min<long long>(r->opts.max_iterations + 2, 1ll << 22);
-    if ((st = dalloc(&r->d_iter_off, (size_t)r->iter_off_cap, "iteration offsets")) != CFPQ_OK) return st;
-    if ((st = dalloc(&r->d_iter_time, (size_t)r->iter_off_cap, "iteration timestamps")) != CFPQ_OK) return st;
-    if ((st = dalloc(&r->d_phase, (size_t)r->iter_off_cap * 4, "iteration phases")) != CFPQ_OK) return st;
+    if ((st = size_iteration_buffers(r)) != CFPQ_OK) return st;
     if (o->account_work) {
-        if ((st = dalloc(&r->d_jac, (size_t)r->iter_off_cap, "work counts")) != CFPQ_OK) return st;
         if ((st = dalloc(&r->d_rowc, (size_t)g->n_nt * n, "row counts")) != CFPQ_OK) return st;
         if ((st = dalloc(&r->d_colc, (size_t)g->n_nt * n, "col counts")) != CFPQ_OK) return st;
         CFPQ_CUDA_TRY(cudaMemsetAsync(r->d_rowc, 0, (size_t)g->n_nt * n * 4, r->stream));
@@ -1072,6 +1102,11 @@ static cfpq_status run(cfpq_result* r, const cfpq_graph* d) {
             for (auto& t : r->h_nt) n_snap += (t.S ? 1 : 0) + (t.ST ? 1 : 0);
             CFPQ_CUDA_TRY(cudaMemsetAsync(r->d_snap, 0, mw * n_snap * 4, s));
         }
+        if (r->d_rowc) {
+            // the sparse iterations before an auto switch counted their cells here
+            CFPQ_CUDA_TRY(cudaMemsetAsync(r->d_rowc, 0, (size_t)r->n_nt * r->n * 4, s));
+            CFPQ_CUDA_TRY(cudaMemsetAsync(r->d_colc, 0, (size_t)r->n_nt * r->n * 4, s));
+        }
         r->n_cells = 0;
         p = r->params();
     }
@@ -1235,7 +1270,8 @@ static cfpq_status run(cfpq_result* r, const cfpq_graph* d) {
         }
         break;
     }
-    r->iterations = r->h_st.iter;
+    // Gauss-Seidel: the kernel counts steps; an iteration is a round of n_stages steps
+    r->iterations = r->opts.schedule == 3 && r->n_stages > 0 ? r->h_st.iter / r->n_stages : r->h_st.iter;
     r->n_cells = std::min<unsigned long long>(r->h_st.log_size, r->log_cap);
     r->t_clean = r->self_clear_ok() && (r->h_st.status == ST_DONE || r->h_st.status == ST_CAP);
     if (r->h_st.status == ST_SWITCH) {
@@ -1266,7 +1302,17 @@ static cfpq_status run(cfpq_result* r, const cfpq_graph* d) {
 static cfpq_status check_inputs(const cfpq_grammar* g, const cfpq_graph* d, const cfpq_options* o) {
     CFPQ_CHECK_ARG(g != nullptr && d != nullptr && o != nullptr, "cfpq_closure: NULL grammar/graph/options");
     CFPQ_CHECK_ARG(o->semantics == 0 || o->semantics == 1, "cfpq_closure: semantics must be 0 or 1");
-    CFPQ_CHECK_ARG(o->schedule >= 0 && o->schedule <= 2, "cfpq_closure: schedule must be 0, 1 or 2");
+    CFPQ_CHECK_ARG(o->schedule >= 0 && o->schedule <= 3, "cfpq_closure: schedule must be 0, 1, 2 or 3");
+    if (o->schedule == 3) {
+        int lhs = 0;
+        for (int A = 0; A < g->n_nt; ++A) lhs += g->is_const[A] ? 0 : 1;
+        if (o->semantics != 0 || o->path_policy > 1 || o->world_size > 1 || o->reserved_emulate > 1 ||
+            o->account_work || lhs > kMaxStages) {
+            set_error("cfpq_closure: schedule 3 (Gauss-Seidel) is relational, sparse-engine, one GPU, no work "
+                      "accounting, at most 64 LHS nonterminals");
+            return CFPQ_E_UNSUPPORTED;
+        }
+    }
     if (o->schedule == 2 && (o->semantics != 0 || o->path_policy > 1 || g->n_nt > 512)) {
         set_error("cfpq_closure: schedule 2 (asynchronous) is relational, sparse-engine only, |N| <= 512");
         return CFPQ_E_UNSUPPORTED;
@@ -1339,8 +1385,14 @@ extern "C" cfpq_status cfpq_closure_reuse(const cfpq_grammar* g, const cfpq_grap
     CFPQ_CHECK_ARG(g->term == r->term, "cfpq_closure_reuse: terminal rules differ from the result's plan");
     r->stream = (cudaStream_t)o->cuda_stream;
     r->opts.cuda_stream = o->cuda_stream;
-    if (o->max_iterations > 0) r->opts.max_iterations = o->max_iterations;
-    if (o->solo_threshold >= 0) r->opts.solo_threshold = o->solo_threshold;
+    // every option of this call applies to the re-run: max_iterations 0 restores the Theorem 3
+    // default, and the per-iteration buffers grow with a larger cap
+    r->opts.max_iterations = o->max_iterations > 0 ? o->max_iterations : theorem3_cap(r->n, r->n_nt);
+    {
+        cfpq_status sb = size_iteration_buffers(r);
+        if (sb != CFPQ_OK) return sb;
+    }
+    r->opts.solo_threshold = o->solo_threshold >= 0 ? o->solo_threshold : 1024;
     r->opts.record_times = o->record_times;
     if (o->schedule == 2 && (r->opts.semantics != 0 || r->n_nt > 512)) {
         set_error("cfpq_closure_reuse: schedule 2 is relational with |N| <= 512");
@@ -1572,8 +1624,12 @@ extern "C" cfpq_status cfpq_result_matrix(cfpq_result* r, int32_t nt, uint32_t* 
     const int64_t wn = (r->n + 31) / 32;
     CFPQ_CHECK_ARG(row_stride_words >= wn, "cfpq_result_matrix: row_stride_words < ceil(n/32)");
     if (r->n == 0) return CFPQ_OK;
-    if (r->hashed || r->t_clean) {
-        // no bit matrices: scatter A's cells from the log
+    // the log holds every cell when there are no bit matrices (hashed set), when the kernel
+    // reset them at the fixpoint (t_clean), or when NCCL row shards derived only their own
+    // rows into T (the log has every rank's cells after the exchange)
+    const bool sparse_sharded = r->comm != nullptr && !r->dense_mode;
+    if (r->hashed || r->t_clean || sparse_sharded) {
+        // no (complete) bit matrices: scatter A's cells from the log
         cudaStream_t s = r->stream;
         uint32_t* d = dst;
         int64_t stride = row_stride_words;

@@ -53,8 +53,10 @@ struct Expansion {
     int32_t kind;
     int32_t A;      // LHS
     int32_t other;  // the other operand NT (C for L kinds, B for R kinds)
-    int32_t pad;
+    int32_t stage;  // Gauss-Seidel schedule: the stage of the LHS A (LHS NTs in id order)
 };
+
+constexpr int kMaxStages = 64;   // Gauss-Seidel stages (distinct LHS NTs) supported
 
 // Per-NT device table (read through the read-only path).
 struct NTInfo {
@@ -92,6 +94,9 @@ struct EngineState {
     int snap_flags[2];             // bit 0 overflow, bit 1 length overflow (slot k&1)
     unsigned pad1[20];
     unsigned long long clr_cursor; // in-kernel clear of the other bank: next cell to claim
+    // Gauss-Seidel schedule: gs_ring[t mod (S+1)] = L_t, the log size when step t starts
+    // (L_1 = |Δ_0|); step t expands log[L_{t-S}, L_t) through the rules of stage (t-1) mod S
+    unsigned long long gs_ring[kMaxStages + 1];
 };
 
 enum : int { ST_RUNNING = 0, ST_DONE = 1, ST_OVERFLOW = 2, ST_CAP = 3, ST_LEN_OVERFLOW = 4, ST_SWITCH = 5 };
@@ -143,6 +148,7 @@ struct EngineParams {
     uint32_t* clr_rowc;
     uint32_t* clr_colc;
     unsigned long long async_init; // asynchronous schedule: log entries < this are valid unflagged
+    int32_t gs_stages;             // > 0: Gauss-Seidel schedule with that many stages (0: Jacobi)
 };
 
 // ------------------------------------------------------------------------------------------

@@ -355,6 +355,7 @@ __global__ void adj_count_kernel(EngineParams p, const int32_t* __restrict__ slo
         if (p.iter_off_cap > 0) p.iter_off[0] = 0;
         if (p.iter_off_cap > 1) p.iter_off[1] = n_seed;
         if (p.iter_time) p.iter_time[0] = globaltimer();
+        p.st->gs_ring[1] = n_seed;   // L_1 (Gauss-Seidel windows)
     }
     for (unsigned long long e = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; e < n_seed;
          e += (unsigned long long)gridDim.x * blockDim.x) {
@@ -432,6 +433,11 @@ __device__ __forceinline__ void cand_coords(uint32_t fx, int32_t nb, uint32_t& i
         i = fx;
         j = (uint32_t)nb;
     }
+}
+
+// Gauss-Seidel schedule: step k applies only the rules of stage (k-1) mod S.
+__device__ __forceinline__ bool stage_ok(const EngineParams& p, const Expansion& ex, long long k) {
+    return p.gs_stages == 0 || ex.stage == (int)((k - 1) % p.gs_stages);
 }
 
 // Neighbours beyond the ELL head (deg > 2): warp-wide exclusive scan of the tail
@@ -516,6 +522,7 @@ __device__ __forceinline__ void expand_chunk(const EngineParams& p, const NTInfo
         efx[x] = 0;
         if (x < nexp) {
             Expansion ex = exps[eb + x];
+            if (!stage_ok(p, ex, k)) continue;
             if (ex.kind == EXP_L_CONST || ex.kind == EXP_R_CONST) el[x] = load_head(nt, ex, ci, cj, eA[x], efx[x]);
             else var_mask |= 1u << x;
         }
@@ -576,8 +583,12 @@ __device__ __forceinline__ void expand_chunk(const EngineParams& p, const NTInfo
         uint32_t A = 0, fx = 0;
         if (x < nexp) {
             Expansion ex = exps[eb + x];
-            if (ex.kind == EXP_L_CONST || ex.kind == EXP_R_CONST) h = load_head(nt, ex, ci, cj, A, fx);
-            else if (x < 32) var_mask |= 1u << x;
+            if (!stage_ok(p, ex, k)) {
+            } else if (ex.kind == EXP_L_CONST || ex.kind == EXP_R_CONST) {
+                h = load_head(nt, ex, ci, cj, A, fx);
+            } else if (x < 32) {
+                var_mask |= 1u << x;
+            }
         }
         uint32_t a0, b0, a1, b1;
         cand_coords(fx, h.z, a0, b0);
@@ -775,6 +786,30 @@ __device__ __forceinline__ void close_iteration(const EngineParams& p, long long
     }
     if (flags & 1) {
         s.status = ST_OVERFLOW;   // keep lo/hi/iter: the host grows the log and re-runs k
+        return;
+    }
+    if (p.gs_stages > 0) {
+        // Gauss-Seidel: step k+1 expands log[L_{k+1-S}, L_{k+1}) (everything derived since its
+        // stage last ran); the fixpoint test and the records are per round of S steps
+        const int S = p.gs_stages, R = S + 1;
+        const long long t = k + 1 - S;
+        unsigned long long* ring = p.st->gs_ring;
+        const unsigned long long lo = t >= 1 ? *(volatile unsigned long long*)&ring[t % R] : 0ull;
+        if (record) ring[(k + 1) % R] = ls;   // read S steps later; never the slot read above
+        s.lo = lo;
+        s.hi = ls;
+        s.iter = k;
+        if (k % S != 0) return;
+        const long long rd = k / S;
+        if (record) {
+            if (rd < p.iter_off_cap) {
+                p.iter_off[rd] = lo;
+                if (p.iter_time) p.iter_time[rd] = globaltimer();
+            }
+            if (rd + 1 < p.iter_off_cap) p.iter_off[rd + 1] = ls;
+        }
+        if (ls == lo) s.status = ST_DONE;                // a whole round added nothing
+        else if (rd >= p.max_iter) s.status = ST_CAP;
         return;
     }
     s.lo = s.hi;
@@ -1056,6 +1091,7 @@ __device__ void warp_solo(const EngineParams& p, const NTInfo* nt, const Expansi
             const uint64_t len_e = (p.lengths && ee > eb) ? cell_len(p, nt, X, ci, cj) : 0;
             for (int x = eb; x < ee; ++x) {
                 const Expansion ex = exps[x];
+                if (!stage_ok(p, ex, k)) continue;
                 if (ex.kind == EXP_L_CONST || ex.kind == EXP_R_CONST) {
                     uint32_t A, fx;
                     const int4 h = load_head(nt, ex, ci, cj, A, fx);
@@ -1107,7 +1143,7 @@ __device__ void warp_solo(const EngineParams& p, const NTInfo* nt, const Expansi
         if (s.status != ST_RUNNING) break;
         if (p.has_snapshots) {
             for (int q = lane; q < total; q += 32) {
-                const uint64_t c = q < 32 ? w.nxt[q] : ldcg64(p.log + s.lo + q);
+                const uint64_t c = q < 32 ? w.nxt[q] : ldcg64(p.log + base + q);
                 const uint32_t A = cell_nt(c), i = cell_i(c), j = cell_j(c);
                 if (nt[A].S) atomicOr(nt[A].S + (size_t)i * p.Wp + (j >> 5), 1u << (j & 31));
                 if (nt[A].ST) atomicOr(nt[A].ST + (size_t)j * p.Wp + (i >> 5), 1u << (i & 31));
@@ -1115,9 +1151,12 @@ __device__ void warp_solo(const EngineParams& p, const NTInfo* nt, const Expansi
             __syncwarp();
         }
         ++k;
-        if (total > 32 || total > p.solo_max) break;   // hand over to the CTA or grid paths
-        m = total;
-        cell = lane < m ? w.nxt[lane] : 0ull;
+        const long long mw = (long long)(s.hi - s.lo);   // the next step's entries (Jacobi: = total)
+        if (mw > 32 || mw > p.solo_max) break;           // hand over to the CTA or grid paths
+        m = (int)mw;
+        __syncwarp();
+        // Gauss-Seidel windows span several steps: read them from the log
+        cell = lane < m ? (p.gs_stages ? ldcg64(p.log + s.lo + lane) : w.nxt[lane]) : 0ull;
         __syncwarp();
     }
 }
@@ -1149,6 +1188,7 @@ __device__ void solo_expand(const EngineParams& p, const NTInfo* nt, const Expan
         uint64_t len_e = (p.lengths && ee > eb) ? cell_len(p, nt, X, ci, cj) : 0;
         for (int x = eb; x < ee; ++x) {
             Expansion ex = exps[x];
+            if (!stage_ok(p, ex, k)) continue;
             if (ex.kind == EXP_L_CONST || ex.kind == EXP_R_CONST) {
                 uint32_t A, fx;
                 int4 h = load_head(nt, ex, ci, cj, A, fx);
@@ -1310,7 +1350,8 @@ __global__ void __launch_bounds__(kBlock, 1) closure_kernel(EngineParams p) {
                         pacc[0] += t - tp;   // loop overhead
                         tp = t;
                     }
-                    const uint64_t* src = (s.hi - s.lo <= (unsigned long long)kSoloMax) ? so.delta[cur] : nullptr;
+                    const uint64_t* src =
+                        (s.hi - s.lo <= (unsigned long long)kSoloMax && !p.gs_stages) ? so.delta[cur] : nullptr;
                     solo_expand(p, nt, exps, so, src, s.lo, s.hi, k, slot, so.delta[cur ^ 1], dcand, dexp,
                                 prof ? pacc : nullptr);
                     if (threadIdx.x == 0) {
@@ -1331,6 +1372,7 @@ __global__ void __launch_bounds__(kBlock, 1) closure_kernel(EngineParams p) {
                         tp = t;
                     }
                     const unsigned long long ls = s.hi + so.cnt[slot];
+                    const unsigned long long old_hi = s.hi;
                     const int f = (so.ov[slot] ? 1 : 0) | (so.lov[slot] ? 2 : 0);
                     last_ls = ls;
                     close_iteration(p, k, s, ls, f, threadIdx.x == 0);
@@ -1342,8 +1384,12 @@ __global__ void __launch_bounds__(kBlock, 1) closure_kernel(EngineParams p) {
                     if (s.status != ST_RUNNING) break;
                     cur ^= 1;
                     if (p.has_snapshots) {
-                        const uint64_t* sn = (s.hi - s.lo <= (unsigned long long)kSoloMax) ? so.delta[cur] : nullptr;
-                        apply_snapshots(p, nt, sn, s.lo, s.hi, threadIdx.x, kBlock);
+                        if (p.gs_stages) {   // this step's cells only (the window spans S steps)
+                            apply_snapshots(p, nt, nullptr, old_hi, s.hi, threadIdx.x, kBlock);
+                        } else {
+                            const uint64_t* sn = (s.hi - s.lo <= (unsigned long long)kSoloMax) ? so.delta[cur] : nullptr;
+                            apply_snapshots(p, nt, sn, s.lo, s.hi, threadIdx.x, kBlock);
+                        }
                         __syncthreads();
                     }
                     ++k;
@@ -1429,7 +1475,7 @@ __global__ void __launch_bounds__(kBlock, 1) closure_kernel(EngineParams p) {
             s.iter = prev.iter;
         }
         if (p.has_snapshots && s.status == ST_RUNNING) {
-            apply_snapshots(p, nt, nullptr, s.lo, s.hi, gtid, gthreads);
+            apply_snapshots(p, nt, nullptr, p.gs_stages ? prev.hi : s.lo, s.hi, gtid, gthreads);
             if (!grid_barrier(p, -1)) {
                 aborted = true;
                 break;
@@ -1599,6 +1645,7 @@ __global__ void begin_kernel(EngineParams p) {
     if (p.iter_off_cap > 0) p.iter_off[0] = 0;
     if (p.iter_off_cap > 1) p.iter_off[1] = n0;
     if (p.iter_time) p.iter_time[0] = globaltimer();
+    st->gs_ring[1] = n0;   // L_1 (Gauss-Seidel windows)
 }
 
 // Δ_0 into the snapshots (one launch after seeding).

@@ -1,0 +1,165 @@
+"""Edge sizes and degenerate inputs for EVERY engine against the oracle or a closed form
+(SURVEY §4 test layer 2: n ∈ {1, 31, 32, 33, 127, 128, 129, 255, 256, 257, 1025} around the
+32-bit word, 128-row tile and 256-column tile boundaries; all-zero, all-one and identity
+inputs), plus reuse of a result after a capped run.
+
+Engines: sparse semi-naive (bit matrices / hashed cell set), tcgen05 tensor (fp4, int8),
+bit-row full-operand, asynchronous schedule, Gauss-Seidel stages, emulated row shards.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import inputs as I
+import oracle as O
+from tests.gpu_util import cuda_ok
+
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not cuda_ok(), reason="needs a CUDA device")]
+
+SIZES = [1, 31, 32, 33, 127, 128, 129, 255, 256, 257, 1025]
+
+# name -> (options, per-iteration Jacobi states?, allows a rule whose two operands change?)
+ENGINES = {
+    "sparse": (dict(path_policy=1, cell_set=1), True, True),
+    "hashed": (dict(path_policy=1, cell_set=2), True, False),
+    "tensor_fp4": (dict(path_policy=2, tensor_format=2), True, True),
+    "tensor_int8": (dict(path_policy=2, tensor_format=1), True, True),
+    "rows": (dict(path_policy=3), True, True),
+    "async": (dict(schedule=2), False, True),
+    "gauss_seidel": (dict(schedule=3), False, True),
+    "shards3": (dict(emulate_ranks=3), True, False),
+    "tensor_shards3": (dict(path_policy=2, emulate_ranks=3), True, True),
+}
+
+
+def _varvar(w):
+    lhs = set(np.asarray(w.bin).reshape(-1, 3)[:, 0].tolist())
+    return any(b in lhs and c in lhs for _, b, c in np.asarray(w.bin).reshape(-1, 3).tolist())
+
+
+def _run(w, name):
+    from paper_1707_01007_b200 import cfpq as C
+    opts, jacobi, vv = ENGINES[name]
+    if _varvar(w) and not vv:
+        pytest.skip(f"{name} needs a preterminal operand in every rule")
+    r = C.closure(C.Grammar.from_workload(w), C.Graph(w.n_nodes, w.edges), **opts)
+    return r, jacobi
+
+
+def _compare(w, r, jacobi, exp_rel, exp_iters=None, exp_new=None):
+    for A in range(w.n_nt):
+        got = set(map(tuple, r.pairs(A).tolist()))
+        assert got == exp_rel[A], (w.name, w.nt_names[A], len(got), len(exp_rel[A]))
+    if jacobi and exp_iters is not None:
+        assert r.iterations == exp_iters, (w.name, r.iterations, exp_iters)
+    if jacobi and exp_new is not None:
+        nc, _ = r.iteration_stats()
+        assert nc.tolist() == list(exp_new), w.name
+
+
+_ORACLE = {}
+
+
+def _oracle(w):
+    if w.name not in _ORACLE:
+        o = O.run(w)
+        _ORACLE[w.name] = (o.relation_sets(), o.iterations, o.stats()["new_bits"].tolist())
+    return _ORACLE[w.name]
+
+
+def _random_instance(n, seed):
+    rng = np.random.default_rng(1000 * n + seed)
+    g = I.random_grammar(rng, 3, 5, 3, 2)
+    e = I.random_labeled_edges(rng, n, 2 * n, ["l0", "l1"])
+    return I.bind(f"rand_n{n}_s{seed}", g, n, e, "N0", extra_labels=["l0", "l1"])
+
+
+def _anbn_for(n):
+    """a^n b^n on two coprime cycles with p + q - 1 = n nodes (Lemma 3 + CRT pin)."""
+    for p in range(2, n + 1):
+        q = n + 1 - p
+        if q >= 1 and math.gcd(p, q) == 1:
+            return I.anbn_workload(p, q), p, q
+    return None, 0, 0
+
+
+@pytest.mark.parametrize("engine", list(ENGINES))
+@pytest.mark.parametrize("n", SIZES)
+def test_random_grammar_vs_oracle(n, engine):
+    if n > 257:
+        w = I.config4_workload(n=n, seed=3)      # ontology shape, union grammar
+    else:
+        w = _random_instance(n, 0)
+    rel, it, new = _oracle(w)
+    r, jac = _run(w, engine)
+    _compare(w, r, jac, rel, it, new)
+
+
+@pytest.mark.parametrize("engine", list(ENGINES))
+@pytest.mark.parametrize("n", SIZES)
+def test_anbn_closed_form(n, engine):
+    w, p, q = _anbn_for(n)
+    if w is None:
+        pytest.skip("no coprime two-cycle graph with one node")
+    S, S1 = w.nt_names.index("S"), w.nt_names.index("S1")
+    va = set(range(p))
+    vb = {0} | set(range(p, p + q - 1))
+    rel = {A: set() for A in range(w.n_nt)}
+    rel[S] = rel[S1] = {(i, j) for i in va for j in vb}
+    rel[w.nt_names.index("A")] = {(i, (i + 1) % p) for i in range(p)}
+    bn = [0] + list(range(p, p + q - 1))
+    rel[w.nt_names.index("B")] = {(bn[t], bn[(t + 1) % q]) for t in range(q)}
+    if engine == "tensor_int8" and 2 * p * q + 1 > 4000:
+        pytest.skip("covered by tensor_fp4 (same kernel template); keeps the suite short")
+    r, jac = _run(w, engine)
+    # 2pq + 1 Jacobi loop bodies, exactly one new cell in each but the last (SURVEY V-2)
+    _compare(w, r, jac, rel, 2 * p * q + 1, [1] * (2 * p * q) + [0])
+
+
+def _dense_grammar_on(n, edges, name):
+    return I.bind(name, I.dense_stress_grammar(), n, edges, "S", extra_labels=["a"])
+
+
+@pytest.mark.parametrize("engine", list(ENGINES))
+@pytest.mark.parametrize("n", SIZES)
+def test_all_zero_identity_all_one(n, engine):
+    # all-zero: no edges -> every R_A empty, one loop body
+    w = I.bind(f"zero_n{n}", I.union_grammar(), n, [], "S_Q1")
+    r, jac = _run(w, engine)
+    _compare(w, r, jac, {A: set() for A in range(w.n_nt)}, 1, [0])
+    # identity: a self-loop on every node, S -> S S | a -> R_S = {(i,i)}, nothing new
+    w = _dense_grammar_on(n, [(i, "a", i) for i in range(n)], f"identity_n{n}")
+    r, jac = _run(w, engine)
+    _compare(w, r, jac, {0: {(i, i) for i in range(n)}}, 1, [0])
+    # all-one: every (i,j) an a-edge -> R_S = V x V already at T_0
+    w = _dense_grammar_on(n, [(i, "a", j) for i in range(n) for j in range(n)], f"allone_n{n}")
+    r, jac = _run(w, engine)
+    _compare(w, r, jac, {0: {(i, j) for i in range(n) for j in range(n)}}, 1, [0])
+    # a single directed path 0 -> 1 -> ... -> n-1: R_S = {(i,j) : i < j}, ceil(log2(n-1))+1 bodies
+    if n >= 2:
+        w = _dense_grammar_on(n, [(i, "a", i + 1) for i in range(n - 1)], f"path_n{n}")
+        r, jac = _run(w, engine)
+        it = (math.ceil(math.log2(n - 1)) if n > 2 else 0) + 1
+        _compare(w, r, jac, {0: {(i, j) for i in range(n) for j in range(i + 1, n)}}, it)
+
+
+@pytest.mark.parametrize("opts", [dict(path_policy=1), dict(path_policy=2), dict(path_policy=3)])
+def test_reuse_after_a_capped_run(opts):
+    """A capped run returns NOT_CONVERGED with 7 bodies; a reuse with max_iterations = 0
+    restores the Theorem 3 cap, converges, and records every iteration."""
+    from paper_1707_01007_b200 import cfpq as C
+    w = I.anbn_workload(3, 5)    # 2pq+1 = 31 bodies
+    g, d = C.Grammar.from_workload(w), C.Graph(w.n_nodes, w.edges)
+    r = C.closure(g, d, max_iterations=7, **opts)
+    assert r.status == C.CFPQ_E_NOT_CONVERGED and r.iterations == 7
+    C.closure_reuse(g, d, r, max_iterations=0, **opts)
+    assert r.status == C.CFPQ_OK and r.iterations == 31
+    nc, _ = r.iteration_stats()
+    assert nc.tolist() == [1] * 30 + [0]
+    o = O.run(w)
+    for A in range(w.n_nt):
+        assert np.array_equal(r.pairs(A), o.pairs(A))
+    # and a larger explicit cap after the default one
+    C.closure_reuse(g, d, r, max_iterations=1000, **opts)
+    assert r.iterations == 31

@@ -1,0 +1,108 @@
+"""Full-size GPU parity against the ORACLE (not engine against engine): config 4 — the
+benched workload, n = 65,536 — and n = 16,384, where the bit-row R form takes 2 row slices
+and the 64k run takes 8.
+
+The expected values are the committed digests tests/golden/config4_n*_s0.json, written by
+scripts/golden_oracle_digest.py from oracle/ alone (Alg. 1, std::set Jacobi loop;
+~25 min single-threaded at 64k): loop bodies, per-iteration |T_k minus T_{k-1}| (the
+Jacobi states of P:222), |R_A| and the SHA-256 of every R_A's ascending (i, j) pairs
+(Theorem 2).  Every engine runs in the launch configuration bench.py times (the
+library stream = torch's current stream, cfpq_closure then cfpq_closure_reuse on the same
+result) and is compared after the reuse.
+"""
+import hashlib
+import json
+import os
+
+import numpy as np
+import pytest
+
+import inputs as I
+from tests.gpu_util import cuda_ok
+
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not cuda_ok(), reason="needs a CUDA device")]
+
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+SIZES = [16384, 65536]
+
+_cache = {}
+
+
+def _setup(n):
+    if n not in _cache:
+        import torch
+
+        from paper_1707_01007_b200 import cfpq as C
+        path = os.path.join(GOLDEN, f"config4_n{n}_s0.json")
+        if not os.path.exists(path):
+            pytest.skip(f"{path} not generated (scripts/golden_oracle_digest.py)")
+        with open(path) as f:
+            gd = json.load(f)
+        w = I.config4_workload(seed=0, n=n)
+        assert w.name == gd["workload"] and len(w.edges) == gd["n_edges"]
+        g = C.Grammar.from_workload(w)
+        d = C.Graph(w.n_nodes, torch.from_numpy(w.edges).cuda(), stream=torch.cuda.current_stream())
+        _cache[n] = (gd, w, g, d)
+    return _cache[n]
+
+
+def _check(gd, w, r, per_iteration=True, iterations=True):
+    if iterations:
+        assert r.iterations == gd["iterations"], (r.iterations, gd["iterations"])
+    if per_iteration:
+        nc, _ = r.iteration_stats()
+        assert nc.tolist() == gd["new_cells"]
+    for A in range(w.n_nt):
+        p = np.ascontiguousarray(r.pairs(A).astype("<i4"))
+        assert len(p) == gd["count"][A], (w.nt_names[A], len(p), gd["count"][A])
+        assert hashlib.sha256(p.tobytes()).hexdigest() == gd["sha256"][A], w.nt_names[A]
+
+
+def _run(n, **kw):
+    import torch
+
+    from paper_1707_01007_b200 import cfpq as C
+    gd, w, g, d = _setup(n)
+    s = torch.cuda.current_stream()
+    r = C.closure(g, d, stream=s, **kw)
+    C.closure_reuse(g, d, r, stream=s, **kw)
+    return gd, w, r
+
+
+@pytest.mark.parametrize("n", SIZES)
+def test_sparse_engine_bit_matrices(n):
+    gd, w, r = _run(n, cell_set=1)
+    _check(gd, w, r)
+    # the executed semi-naive pairs (bench.py's work unit) equal the independent bitset
+    # program's count on the same instance
+    import cpu_baseline as CB
+    b = CB.BitsetBaseline(w)
+    k = b.run(w.edges)
+    _, cand = b.iteration_stats(k)
+    assert r.stats()["candidates"] == int(cand.sum())
+
+
+@pytest.mark.parametrize("n", SIZES)
+def test_sparse_engine_hashed_cell_set(n):
+    gd, w, r = _run(n, cell_set=2)
+    assert r.stats()["hashed"] == 1
+    _check(gd, w, r)
+
+
+@pytest.mark.parametrize("n", SIZES)
+def test_bit_row_engine(n):
+    gd, w, r = _run(n, path_policy=3)
+    _check(gd, w, r)
+
+
+@pytest.mark.parametrize("n", SIZES)
+def test_asynchronous_schedule(n):
+    gd, w, r = _run(n, schedule=2)
+    _check(gd, w, r, per_iteration=False, iterations=False)
+
+
+@pytest.mark.parametrize("n", SIZES)
+@pytest.mark.parametrize("ranks", [2, 8])
+def test_emulated_row_shards(n, ranks):
+    gd, w, r = _run(n, emulate_ranks=ranks)
+    _check(gd, w, r)
