@@ -350,6 +350,59 @@ def supplementary_rows(C, w, g, d, r_sparse, stream, steps=2):
                                  "output word touched, 32 B per Delta word"}}
 
 
+def job_totals(dist, world, sharded, total_ms, useful, jac, device):
+    """Whole-job aggregation over the ranks: time = MAX over ranks of the device-timed region;
+    work per step = the one sharded problem's work counted once, or the sum over replicas."""
+    import torch
+    if world <= 1:
+        return float(total_ms), float(useful), float(jac)
+    my = torch.tensor([total_ms, float(useful), float(jac)], dtype=torch.float64, device=device)
+    t_max = my[0:1].clone()
+    dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
+    o_sum = my[1:3].clone()
+    if not sharded:
+        dist.all_reduce(o_sum, op=dist.ReduceOp.SUM)
+    return float(t_max.item()), float(o_sum[0].item()), float(o_sum[1].item())
+
+
+def supplementary_rows_sharded(C, w, g, d, args, rank, world, stream, dist, shard_kw):
+    """Config 4 in the paper-faithful full-operand mode (bit-row engine, path_policy 3) closed
+    as ONE problem row-block sharded over the ranks (Δ_k word lists exchanged over NCCL),
+    time = max over ranks; rank 0 also times the unsharded 1-GPU closure of the same problem
+    (the other ranks wait) so the line carries its own speedup."""
+    import torch
+    r = C.closure(g, d, stream=stream, path_policy=3, **shard_kw)
+    for _ in range(max(args.warmup // 2, 1)):
+        C.closure_reuse(g, d, r, stream=stream, path_policy=3, **shard_kw)
+    torch.cuda.synchronize()
+    dist.barrier()
+    steps = max(args.steps // 4, 2)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        C.closure_reuse(g, d, r, stream=stream, path_policy=3, **shard_kw)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item()) / steps
+    one = None
+    if rank == 0:
+        r1 = C.closure(g, d, stream=stream, path_policy=3)
+        C.closure_reuse(g, d, r1, stream=stream, path_policy=3)
+        e0.record(stream)
+        for _ in range(steps):
+            C.closure_reuse(g, d, r1, stream=stream, path_policy=3)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        one = e0.elapsed_time(e1) / steps
+        del r1
+    dist.barrier()
+    return {"workload": "config4, ONE problem, bit-row engine row-sharded over %d GPUs (NCCL word-list exchange)"
+                        % world, "ms_per_step": ms, "iterations": r.iterations, "scaling": "strong",
+            "one_gpu_ms_per_step": one, "speedup_vs_1gpu": (one / ms) if one else None}
+
+
 def supplementary_replicas(C, args, rank, world, stream, dist):
     """N > 1: N independent seeded config-4 problems (seed + rank), one per GPU, single-GPU
     engine, no data-path collective ("scaling": "weak").  Time = max over ranks."""
@@ -593,18 +646,8 @@ def main():
     torch.cuda.synchronize()
     assert r.iterations == iterations and r.stats()["cells"] == cells
 
-    # whole-job work per step: one sharded problem counts once; replicas add up
     total_ms = float(sum(step_ms))
-    my = torch.tensor([total_ms, float(useful), float(jac)], dtype=torch.float64, device="cuda")
-    if world > 1:
-        t_max = my[0:1].clone()
-        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
-        o_sum = my[1:3].clone()
-        if not sharded:
-            dist.all_reduce(o_sum, op=dist.ReduceOp.SUM)
-        total_ms_max, useful_job, jac_job = float(t_max.item()), float(o_sum[0].item()), float(o_sum[1].item())
-    else:
-        total_ms_max, useful_job, jac_job = total_ms, float(useful), float(jac)
+    total_ms_max, useful_job, jac_job = job_totals(dist, world, sharded, total_ms, useful, jac, "cuda")
     value = useful_job * args.steps / (total_ms_max * 1e-3) / 1e9
     ms_per_step = total_ms_max / args.steps
 
@@ -665,8 +708,12 @@ def main():
     if world > 1 and args.workload == "config4" and not args.no_supplementary:
         supp = {}
         if sharded:
-            rs = supplementary_replicas(C, args, rank, world, stream, dist)
-            supp["replicas"] = rs
+            supp["replicas"] = supplementary_replicas(C, args, rank, world, stream, dist)
+            try:
+                supp["paper_faithful_rows_sharded"] = supplementary_rows_sharded(C, w, g, d, args, rank, world,
+                                                                                 stream, dist, shard_kw)
+            except Exception as ex:
+                supp["paper_faithful_rows_sharded_error"] = repr(ex)
     if rank == 0 and world == 1 and args.workload == "config4" and not args.no_supplementary:
         supp = {}
         try:

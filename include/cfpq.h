@@ -103,7 +103,13 @@ typedef struct {
                                 2 asynchronous: cells are expanded as soon as they appear,
                                 no iteration barriers; same fixpoint T^cf (monotone
                                 operator), no per-iteration states (iterations = 0);
-                                relational semantics, sparse engine, |N| <= 512            */
+                                relational semantics, sparse engine, |N| <= 512;
+                                3 Gauss-Seidel: an iteration applies the rules stage by
+                                stage (LHS NTs in id order), each stage reading T with the
+                                cells of the earlier stages of the same iteration (in-place
+                                update of P:222); same fixpoint, fewer iterations (a^n b^n:
+                                pq + 1 instead of 2pq + 1); relational, sparse engine, one
+                                GPU, no account_work, <= 64 LHS NTs                         */
     int32_t path_policy;     /* 0 auto: sparse, switching to tensor when Δ turns dense and a
                                 rule has two changing operands; 1 sparse (index-list semi-
                                 naive); 2 tensor (tcgen05 dense, tensor_format); 3 rows (bit-row full-
@@ -113,9 +119,12 @@ typedef struct {
     int64_t max_iterations;  /* 0 = |V|^2 |N| + 1 (Theorem 3)                   */
     void*   cuda_stream;     /* cudaStream_t to run on (NULL = default stream)             */
     int32_t world_size;      /* > 1: this process is `rank` of world_size GPUs; every T_A is
-                                row-block sharded (cfpq_shard_rows) and the blocks are
-                                all-gathered over NCCL after every iteration (dense engine,
-                                path_policy 2).  Every rank passes identical inputs.         */
+                                row-block sharded (cfpq_shard_rows): each rank derives the
+                                cells of its rows and the ranks exchange every iteration over
+                                NCCL — Δ_k cells as index lists (sparse engine, path_policy
+                                0/1), Δ_k word lists (bit-row engine, 3), row blocks or 2-D
+                                blocks of T_k (tensor engine, 2).  Every rank passes identical
+                                inputs.                                                       */
     int32_t rank;
     const void* nccl_unique_id;  /* world_size > 1: the 128-byte ncclUniqueId from
                                 cfpq_nccl_unique_id on one rank, broadcast to all ranks      */
@@ -137,9 +146,20 @@ typedef struct {
                                 2 fp4 (tcgen05 kind::mxf4: 0/1 as e2m1 nibbles, every block
                                 scale 1.0, f32 accumulator; all terms are >= 0, so the
                                 threshold P > 0 is exact)                           */
-    int32_t reserved[2];     /* reserved[0]: diagnostics flags (0 = defaults): bit 0 no bit
-                                precheck before the atomic, bit 1 clear the other bank on a side
-                                stream, bit 2 no reset of the bit words at the fixpoint; others 0 */
+    int32_t dense_launch;    /* CTA layout of the tensor engine: 0 auto (= 1), 1 CTA pairs
+                                (tcgen05.mma.cta_group::2, M = 256 per pair), 2 one CTA per
+                                SM (cta_group::1), 3 CTA pairs of one-SM MMAs sharing the B
+                                tile by TMA multicast                                        */
+    int32_t diag_flags;      /* diagnostics, 0 = defaults: bit 0 no bit pre-check before the
+                                atomic, bit 1 clear the other workspace bank on a side
+                                stream, bit 2 no reset of the bit words at the fixpoint       */
+    int32_t grid_rows;       /* tensor engine, world_size (or reserved_emulate) > 1: 2-D
+                                process grid grid_rows x grid_cols (SUMMA-style blocks
+                                (I_a, J_b) of every T_A); 0 = 1-D row blocks.
+                                grid_rows * grid_cols must equal the number of shards        */
+    int32_t grid_cols;
+    int64_t rows_list_capacity; /* bit-row engine: initial capacity (words) of the Δ_k word
+                                list; 0 = 2^20.  Grown on overflow (tests use tiny values)    */
 } cfpq_options;
 
 CFPQ_API void cfpq_options_default(cfpq_options* o);
@@ -241,6 +261,13 @@ CFPQ_API cfpq_status cfpq_nccl_unique_id(void* out, int64_t bytes);
  * be performed on different GPGPU independently").  Pure host function. */
 CFPQ_API cfpq_status cfpq_shard_rows(int64_t n_nodes, int32_t world_size, int32_t rank, int64_t* row_lo,
                                      int64_t* row_hi);
+
+/* Block [row_lo, row_hi) x [col_lo, col_hi) of every T_A that shard `rank` (row-major in the
+ * grid: a = rank / grid_cols, b = rank % grid_cols) derives under 2-D block sharding of the
+ * tensor engine (grid_rows x grid_cols grid; 128-row and 256-column tiles).  Pure host
+ * function; CFPQ_E_INVAL on a bad grid or rank. */
+CFPQ_API cfpq_status cfpq_shard_block(int64_t n_nodes, int32_t grid_rows, int32_t grid_cols, int32_t rank,
+                                      int64_t* row_lo, int64_t* row_hi, int64_t* col_lo, int64_t* col_hi);
 
 /* Thread-local message describing the last non-OK status. */
 CFPQ_API const char* cfpq_last_error(void);

@@ -30,7 +30,7 @@ EXPORTS = [
     "cfpq_result_pairs", "cfpq_result_pairs_at", "cfpq_result_matrix", "cfpq_result_lengths",
     "cfpq_result_stats", "cfpq_result_iteration_stats", "cfpq_result_iteration_stats2",
     "cfpq_result_iteration_phases", "cfpq_result_witness", "cfpq_last_error",
-    "cfpq_version", "cfpq_nccl_unique_id", "cfpq_shard_rows",
+    "cfpq_version", "cfpq_nccl_unique_id", "cfpq_shard_rows", "cfpq_shard_block",
 ]
 
 
@@ -50,7 +50,9 @@ class Options(ctypes.Structure):
                 ("max_ctas", ctypes.c_int32), ("emulate_ranks", ctypes.c_int32),
                 ("cell_set", ctypes.c_int32),
                 ("tensor_format", ctypes.c_int32),
-                ("reserved", ctypes.c_int32 * 2)]
+                ("dense_launch", ctypes.c_int32), ("diag_flags", ctypes.c_int32),
+                ("grid_rows", ctypes.c_int32), ("grid_cols", ctypes.c_int32),
+                ("rows_list_capacity", ctypes.c_int64)]
 
 
 _lib = None
@@ -92,6 +94,7 @@ def load() -> ctypes.CDLL:
         "cfpq_version": (ctypes.c_char_p, []),
         "cfpq_nccl_unique_id": (i32, [vp, i64]),
         "cfpq_shard_rows": (i32, [i64, i32, i32, P(i64), P(i64)]),
+        "cfpq_shard_block": (i32, [i64, i32, i32, i32, P(i64), P(i64), P(i64), P(i64)]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -190,7 +193,8 @@ def options(semantics: int = 0, schedule: int = 0, path_policy: int = 0, account
             max_iterations: int = 0, stream=None, log_capacity: int = 0, solo_threshold: int = -1,
             record_times: bool = False, max_ctas: int = 0, world_size: int = 1, rank: int = 0,
             nccl_unique_id=None, emulate_ranks: int = 0, flags: int = 0, cell_set: int = 0,
-            tensor_format: int = 0) -> Options:
+            tensor_format: int = 0, dense_launch: int = 0, grid: Tuple[int, int] = (0, 0),
+            rows_list_capacity: int = 0) -> Options:
     o = Options()
     load().cfpq_options_default(ctypes.byref(o))
     o.semantics, o.schedule, o.path_policy = int(semantics), int(schedule), int(path_policy)
@@ -204,7 +208,10 @@ def options(semantics: int = 0, schedule: int = 0, path_policy: int = 0, account
     o.world_size = int(world_size)
     o.rank = int(rank)
     o.emulate_ranks = int(emulate_ranks)
-    o.reserved[0] = int(flags)
+    o.diag_flags = int(flags)
+    o.dense_launch = int(dense_launch)
+    o.grid_rows, o.grid_cols = int(grid[0]), int(grid[1])
+    o.rows_list_capacity = int(rows_list_capacity)
     o.cell_set = int(cell_set)
     o.tensor_format = int(tensor_format)
     if nccl_unique_id is not None:
@@ -227,6 +234,14 @@ def shard_rows(n_nodes: int, world_size: int, rank: int) -> Tuple[int, int]:
     _check(load().cfpq_shard_rows(int(n_nodes), int(world_size), int(rank), ctypes.byref(lo), ctypes.byref(hi)),
            "cfpq_shard_rows")
     return lo.value, hi.value
+
+
+def shard_block(n_nodes: int, grid_rows: int, grid_cols: int, rank: int) -> Tuple[int, int, int, int]:
+    """cfpq_shard_block: the 2-D block (row_lo, row_hi, col_lo, col_hi) of shard `rank`."""
+    v = [ctypes.c_int64() for _ in range(4)]
+    _check(load().cfpq_shard_block(int(n_nodes), int(grid_rows), int(grid_cols), int(rank), *[ctypes.byref(x) for x in v]),
+           "cfpq_shard_block")
+    return tuple(x.value for x in v)
 
 
 class Result:

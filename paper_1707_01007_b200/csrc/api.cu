@@ -146,6 +146,11 @@ struct cfpq_result {
     std::vector<int64_t> dense_jac;           // Jacobi AND-true triples per iteration (account_work)
     unsigned long long dense_kb = 0;          // issued 128x256x128 int8 MMA k-blocks
     int32_t n_stages = 0;                     // distinct LHS NTs (Gauss-Seidel stages, schedule 3)
+    int32_t grid_r = 0, grid_c = 0;           // 2-D process grid of the tensor engine (0: 1-D)
+    void* comm_row = nullptr;                 // NCCL sub-communicators of the grid row / column
+    void* comm_col = nullptr;
+    uint32_t* d_stage = nullptr;              // 2-D block exchange staging
+    size_t stage_cap = 0;
     int32_t n_ranks = 1;                      // row-block shards (NCCL ranks or emulated)
     int32_t my_rank = 0;
     bool emulated = false;
@@ -187,6 +192,9 @@ struct cfpq_result {
         dfree(d_iter_off); dfree(d_jac); dfree(d_iter_time); dfree(d_phase); dfree(d_hset); dfree(d_xbuf); dfree(d_rowc); dfree(d_colc); dfree(d_temp); dfree(d_keys);
         dfree(d_small); dfree(d_Tn); dfree(d_rowcnt); dfree(d_rowoff);
         if (dense) dense_destroy(dense);
+        dfree(d_stage);
+        if (comm_row) nccl_comm_destroy(comm_row);
+        if (comm_col) nccl_comm_destroy(comm_col);
         if (comm) nccl_comm_destroy(comm);
     }
 
@@ -194,7 +202,7 @@ struct cfpq_result {
     // kernel can reset the bit words at the fixpoint (flags bit 2 disables, diagnostics)
     bool self_clear_ok() const {
         return opts.semantics == 0 && !hashed && opts.schedule != 2 && n_ranks == 1 && !comm &&
-               opts.path_policy < 2 && (opts.reserved[0] & 4) == 0;
+               opts.path_policy < 2 && (opts.diag_flags & 4) == 0;
     }
 
     EngineParams params() const {
@@ -228,7 +236,7 @@ struct cfpq_result {
         p.switch_cells = opts.schedule == 3 ? 0 : switch_cells;   // Gauss-Seidel stays sparse
         // read a candidate's bit before its atomicOr (skips the RMW on already-set words;
         // config 4: 0.611 vs 0.623 ms per step); flags bit 0 disables (diagnostics)
-        p.precheck = (opts.reserved[0] & 1) ? 0 : 1;
+        p.precheck = (opts.diag_flags & 1) ? 0 : 1;
         p.self_clear = self_clear_ok() ? 1 : 0;
         p.row_lo = 0;
         p.row_hi = (uint32_t)n;
@@ -348,7 +356,8 @@ static cfpq_status ensure_dense(cfpq_result* r) {
     if (r->dense) return CFPQ_OK;
     std::string err;
     r->dense = dense_create((int32_t)r->n, r->n_nt, r->Wp, r->rules, r->is_const, r->stream, &err,
-                            r->opts.path_policy != 3, r->opts.tensor_format != 1);
+                            r->opts.path_policy != 3, r->opts.tensor_format != 1, r->opts.rows_list_capacity,
+                            r->opts.dense_launch);
     if (!r->dense) {
         set_error(err);
         return CFPQ_E_CUDA;
@@ -532,7 +541,8 @@ static cfpq_status plan(cfpq_result* r, const cfpq_grammar* g, const cfpq_graph*
         r->max_rules_per_label = std::max(r->max_rules_per_label, lab_ptr[x + 1] - lab_ptr[x]);
 
     cfpq_status st;
-    const bool use_nccl = o->nccl_unique_id != nullptr && o->path_policy != 3;
+    // a communicator whenever an id is given (world_size 1 exercises the NCCL exchange path)
+    const bool use_nccl = o->nccl_unique_id != nullptr;
     r->n_ranks = o->world_size > 1 ? o->world_size : (o->reserved_emulate > 1 ? o->reserved_emulate : 1);
     r->emulated = !use_nccl && r->n_ranks > 1;
     r->my_rank = o->world_size > 1 ? o->rank : 0;
@@ -548,6 +558,19 @@ static cfpq_status plan(cfpq_result* r, const cfpq_grammar* g, const cfpq_graph*
         if (!r->comm) {
             set_error(err);
             return CFPQ_E_NCCL;
+        }
+    }
+    if (o->path_policy == 2 && o->grid_rows > 0 && o->grid_cols > 0) {
+        r->grid_r = o->grid_rows;
+        r->grid_c = o->grid_cols;
+        if (r->comm) {
+            std::string err;
+            r->comm_row = nccl_comm_split(r->comm, r->my_rank / r->grid_c, r->my_rank % r->grid_c, &err);
+            if (r->comm_row) r->comm_col = nccl_comm_split(r->comm, r->my_rank % r->grid_c, r->my_rank / r->grid_c, &err);
+            if (!r->comm_row || !r->comm_col) {
+                set_error(err);
+                return CFPQ_E_NCCL;
+            }
         }
     }
     const size_t mat_words = (size_t)r->rows_alloc * (size_t)r->Wp;
@@ -752,6 +775,211 @@ static cfpq_status grow_log(cfpq_result* r, unsigned long long reached, unsigned
     return CFPQ_OK;
 }
 
+// One row-block sharded iteration of the bit-row engine (§8(e); "matrix multiplication
+// in the main loop ... may be performed on different GPGPU independently").  Every rank holds
+// full replicas of T_{k-1} and T_k and derives the rows it owns (cfpq_shard_rows); the Δ_k
+// word lists {A, i, word, bits} of the ranks are exchanged — all-gather of the counts, padded
+// all-gather of the words, compaction in rank order — and every rank applies all of them to
+// its T_k (the new-cell total, Alg. 1 line 8's "changed", counts the bits they flip).  Emulated
+// ranks (one process) run the shards one after another on the shared buffers and pass their
+// lists through the same padded buffer and compaction.
+static cfpq_status rows_sharded_iteration(cfpq_result* r, bool first, int* launches) {
+    cudaStream_t s = r->stream;
+    DenseEngine* e = r->dense;
+    const int P = r->n_ranks;
+    CFPQ_CUDA_TRY(rows_begin(e, r->d_nt, r->d_adj_idx, r->d_log, r->n_cells, first, s, launches));
+    const int g_begin = r->emulated ? 0 : r->my_rank, g_end = r->emulated ? P : r->my_rank + 1;
+    std::vector<unsigned long long> cnt(P, 0);
+    unsigned long long end = 0;
+    for (int g = g_begin; g < g_end; ++g) {
+        int64_t tlo, thi, br;
+        dense_partition(r->n, P, g, &tlo, &thi, &br);
+        const int64_t lo = std::min<int64_t>(tlo * 128, r->n), hi = std::min<int64_t>(thi * 128, r->n);
+        CFPQ_CUDA_TRY(rows_shard(e, lo, hi, s, launches));
+        unsigned long long m = 0;
+        CFPQ_CUDA_TRY(rows_list_settle(e, lo, hi, end, s, &m));
+        cnt[g] = m - end;
+        end = m;
+    }
+    // exchange buffer: P slots of the largest list (2 uint64 per word)
+    auto ensure_x = [&](size_t want) -> cfpq_status {
+        if (r->xbuf_cap >= want) return CFPQ_OK;
+        dfree(r->d_xbuf);
+        r->xbuf_cap = 0;
+        cfpq_status st = dalloc(&r->d_xbuf, want, "exchange buffer");
+        if (st == CFPQ_OK) r->xbuf_cap = want;
+        return st;
+    };
+    cfpq_status st;
+    if (r->comm) {
+        if ((st = ensure_x((size_t)P * 64)) != CFPQ_OK) return st;
+        uint64_t mine = cnt[r->my_rank];
+        CFPQ_CUDA_TRY(cudaMemcpyAsync(r->d_xbuf + r->my_rank, &mine, 8, cudaMemcpyHostToDevice, s));
+        std::string err;
+        if (!nccl_allgather_u64(r->comm, r->d_xbuf, 1, r->my_rank, s, &err)) {
+            set_error(err);
+            return CFPQ_E_NCCL;
+        }
+        std::vector<uint64_t> hc(P);
+        CFPQ_CUDA_TRY(cudaMemcpyAsync(hc.data(), r->d_xbuf, 8 * P, cudaMemcpyDeviceToHost, s));
+        CFPQ_CUDA_TRY(cudaStreamSynchronize(s));
+        for (int g = 0; g < P; ++g) cnt[g] = hc[g];
+    }
+    unsigned long long tot = 0, mx = 0;
+    for (int g = 0; g < P; ++g) {
+        tot += cnt[g];
+        mx = std::max(mx, cnt[g]);
+    }
+    void* list = nullptr;
+    unsigned long long cap = 0;
+    CFPQ_CUDA_TRY(rows_list(e, 0, &list, &cap));
+    if ((st = ensure_x((size_t)P * std::max<unsigned long long>(2 * mx, 64))) != CFPQ_OK) return st;
+    const size_t slot = (size_t)2 * mx;   // uint64 per rank slot
+    {
+        unsigned long long off = 0;
+        for (int g = g_begin; g < g_end; ++g) {
+            if (cnt[g])
+                CFPQ_CUDA_TRY(cudaMemcpyAsync(r->d_xbuf + g * slot, (const uint4*)list + off, cnt[g] * 16,
+                                              cudaMemcpyDeviceToDevice, s));
+            off += cnt[g];
+        }
+    }
+    if (r->comm && mx) {
+        std::string err;
+        if (!nccl_allgather_u64(r->comm, r->d_xbuf, slot, r->my_rank, s, &err)) {
+            set_error(err);
+            return CFPQ_E_NCCL;
+        }
+    }
+    CFPQ_CUDA_TRY(cudaStreamSynchronize(s));   // the old list may be replaced below
+    CFPQ_CUDA_TRY(rows_list(e, tot, &list, &cap));
+    {
+        unsigned long long off = 0;
+        for (int g = 0; g < P; ++g) {
+            if (cnt[g])
+                CFPQ_CUDA_TRY(cudaMemcpyAsync((uint4*)list + off, r->d_xbuf + g * slot, cnt[g] * 16,
+                                              cudaMemcpyDeviceToDevice, s));
+            off += cnt[g];
+        }
+    }
+    CFPQ_CUDA_TRY(rows_apply_all(e, tot, s, launches));
+    return CFPQ_OK;
+}
+
+// 2-D (SUMMA-style) block sharding of the tensor engine ("|N|^2
+// Boolean matrix multiplications", P:572 products "performed on different GPGPU").  The shards
+// form a grid_r x grid_c grid; shard (a, b) derives block (I_a, J_b) of every T_A:
+//     T_k,A[I_a, J_b] = T_{k-1},A[I_a, J_b] ∪ ⋃_{A->BC} T_{k-1},B[I_a, :] × T_{k-1},C[:, J_b]
+// so it reads the row panel I_a of left operands and the column panel J_b of right operands.
+// After the products the blocks travel along the grid: the row group (a, *) all-gathers its
+// blocks (row panel I_a of T_k), the column group (*, b) all-gathers its blocks (column panel
+// J_b), each through a contiguous staging buffer; the new-cell counts are summed over all
+// shards (Alg. 1 line 8's "changed").  Per iteration a shard receives n/grid_r x n +
+// n x n/grid_c bits per output instead of the 1-D all-gather's n x n.  Emulated shards (one
+// process) share the matrices, so their blocks go through the staging buffer as identity
+// copies.  At the fixpoint one world all-gather of the blocks makes every T_A whole again.
+static cfpq_status grid_exchange(cfpq_result* r, bool final_gather) {
+    cudaStream_t s = r->stream;
+    const auto& outs = dense_outputs(r->dense);
+    const int gr = r->grid_r, gc = r->grid_c, P = gr * gc;
+    const int64_t Wp = r->Wp;
+    std::vector<int64_t> ti_lo(P), ti_hi(P), tj_lo(P), tj_hi(P);
+    int64_t max_rows = 0, max_words = 0;
+    for (int g = 0; g < P; ++g) {
+        dense_partition2(r->n, gr, gc, g / gc, g % gc, &ti_lo[g], &ti_hi[g], &tj_lo[g], &tj_hi[g]);
+        max_rows = std::max(max_rows, (ti_hi[g] - ti_lo[g]) * 128);
+        max_words = std::max(max_words, (tj_hi[g] - tj_lo[g]) * 8);
+    }
+    const int64_t n_out = (int64_t)outs.size();
+    auto rows_of = [&](int g, int64_t* lo, int64_t* hi) {
+        *lo = std::min<int64_t>(ti_lo[g] * 128, r->n);
+        *hi = std::min<int64_t>(ti_hi[g] * 128, r->n);
+    };
+    auto words_of = [&](int g, int64_t* lo, int64_t* hi) {
+        const int64_t wn = (r->n + 31) / 32;
+        *lo = std::min<int64_t>(tj_lo[g] * 8, wn);
+        *hi = std::min<int64_t>(tj_hi[g] * 8, wn);
+    };
+    const size_t slot = (size_t)max_rows * max_words * n_out;   // uint32 per shard block (all outputs)
+    const size_t want = slot * (size_t)std::max(P, 1);
+    if (r->stage_cap < want) {
+        dfree(r->d_stage);
+        r->stage_cap = 0;
+        cfpq_status st = dalloc(&r->d_stage, want, "2-D exchange staging");
+        if (st != CFPQ_OK) return st;
+        r->stage_cap = want;
+    }
+    // pack / unpack shard g's block of every output at staging slot `at`
+    auto pack = [&](int g, size_t at, int to_buf) -> cudaError_t {
+        int64_t rl, rh, wl, wh;
+        rows_of(g, &rl, &rh);
+        words_of(g, &wl, &wh);
+        for (int64_t q = 0; q < n_out; ++q) {
+            uint32_t* T = r->Tnxt[outs[q]];
+            cudaError_t e = bit_block_copy(T, Wp, rl, rh, wl, wh, r->d_stage + at * slot + (size_t)q * max_rows * max_words,
+                                           to_buf, s);
+            if (e != cudaSuccess) return e;
+        }
+        return cudaSuccess;
+    };
+    if (!r->comm) {
+        // emulated: every shard's block through the staging buffer and back (identity)
+        for (int g = 0; g < P; ++g) CFPQ_CUDA_TRY(pack(g, (size_t)g, 1));
+        for (int g = 0; g < P; ++g) CFPQ_CUDA_TRY(pack(g, (size_t)g, 0));
+        return CFPQ_OK;
+    }
+    const int me = r->my_rank, a = me / gc, b = me % gc;
+    std::string err;
+    if (final_gather) {
+        CFPQ_CUDA_TRY(pack(me, (size_t)me, 1));
+        if (!nccl_allgather_u32(r->comm, r->d_stage, slot, me, s, &err)) {
+            set_error(err);
+            return CFPQ_E_NCCL;
+        }
+        for (int g = 0; g < P; ++g)
+            if (g != me) CFPQ_CUDA_TRY(pack(g, (size_t)g, 0));
+        return CFPQ_OK;
+    }
+    // row group (a, *): slots by b'; column group (*, b): slots by a' (after the row slots)
+    CFPQ_CUDA_TRY(pack(me, (size_t)b, 1));
+    if (!nccl_allgather_u32(r->comm_row, r->d_stage, slot, b, s, &err)) {
+        set_error(err);
+        return CFPQ_E_NCCL;
+    }
+    for (int bb = 0; bb < gc; ++bb)
+        if (bb != b) CFPQ_CUDA_TRY(pack(a * gc + bb, (size_t)bb, 0));
+    // the column group reuses the staging buffer: the row blocks are unpacked already
+    CFPQ_CUDA_TRY(pack(me, (size_t)a, 1));
+    if (!nccl_allgather_u32(r->comm_col, r->d_stage, slot, a, s, &err)) {
+        set_error(err);
+        return CFPQ_E_NCCL;
+    }
+    for (int aa = 0; aa < gr; ++aa)
+        if (aa != a) CFPQ_CUDA_TRY(pack(aa * gc + b, (size_t)aa, 0));
+    return CFPQ_OK;
+}
+
+static cfpq_status dense_grid_iteration(cfpq_result* r, int* launches) {
+    cudaStream_t s = r->stream;
+    const int gr = r->grid_r, gc = r->grid_c;
+    const int g_begin = r->emulated ? 0 : r->my_rank, g_end = r->emulated ? gr * gc : r->my_rank + 1;
+    for (int g = g_begin; g < g_end; ++g) {
+        int64_t ilo, ihi, jlo, jhi;
+        dense_partition2(r->n, gr, gc, g / gc, g % gc, &ilo, &ihi, &jlo, &jhi);
+        CFPQ_CUDA_TRY(dense_product(r->dense, ilo, ihi, s, launches, jlo, jhi));
+    }
+    cfpq_status st = grid_exchange(r, false);
+    if (st != CFPQ_OK) return st;
+    if (r->comm) {
+        std::string err;
+        if (!nccl_allreduce_sum_u64(r->comm, dense_total_counter(r->dense), 1, s, &err)) {
+            set_error(err);
+            return CFPQ_E_NCCL;
+        }
+    }
+    return CFPQ_OK;
+}
+
 // Dense engine loop (path_policy 2): host-driven Jacobi iterations, one tcgen05 product
 // launch (+ packs) per iteration; T and Tn swap roles after every iteration.
 static cfpq_status run_dense(cfpq_result* r, int64_t start_k) {
@@ -801,11 +1029,17 @@ static cfpq_status run_dense(cfpq_result* r, int64_t start_k) {
         }
         const bool rows = r->opts.path_policy == 3;
         CFPQ_CUDA_TRY(dense_begin(r->dense, r->Tcur.data(), r->Tnxt.data(), k == start_k + 1, s, &launches, !rows));
-        if (rows) {
+        if (rows && r->n_ranks == 1 && !r->comm) {
             CFPQ_CUDA_TRY(rows_product(r->dense, r->Tcur.data(), r->Tnxt.data(), r->d_nt, r->d_adj_idx, r->d_log,
                                        r->n_cells, k == start_k + 1, s, &launches));
+        } else if (rows) {
+            cfpq_status rs = rows_sharded_iteration(r, k == start_k + 1, &launches);
+            if (rs != CFPQ_OK) return rs;
         } else if (r->n_ranks == 1 && !r->comm) {
             CFPQ_CUDA_TRY(dense_product(r->dense, 0, tiles, s, &launches));
+        } else if (r->grid_r > 0) {
+            cfpq_status gs = dense_grid_iteration(r, &launches);
+            if (gs != CFPQ_OK) return gs;
         } else if (r->emulated) {
             // P row-block shards in one process: each writes its rows of the shared T_k
             for (int g = 0; g < r->n_ranks; ++g) {
@@ -836,6 +1070,14 @@ static cfpq_status run_dense(cfpq_result* r, int64_t start_k) {
             capped = true;
             break;
         }
+    }
+    if (r->grid_r > 0 && r->comm) {
+        // every shard holds its panels only: make T whole for the result queries (T_k was
+        // swapped into Tcur; the exchange reads Tnxt, so point it at the final matrices)
+        for (int A : outs) std::swap(r->Tcur[A], r->Tnxt[A]);
+        cfpq_status gs = grid_exchange(r, true);
+        for (int A : outs) std::swap(r->Tcur[A], r->Tnxt[A]);
+        if (gs != CFPQ_OK) return gs;
     }
     CFPQ_CUDA_TRY(cudaEventRecord(e1, s));
     CFPQ_CUDA_TRY(cudaEventSynchronize(e1));
@@ -1126,7 +1368,7 @@ static cfpq_status run(cfpq_result* r, const cfpq_graph* d) {
         }
         // the persistent closure kernel clears the other bank itself (barrier idle time)
         const bool in_kernel = !r->hashed && r->opts.schedule != 2 && r->n_ranks == 1 && !r->comm &&
-                               r->opts.path_policy < 2 && (r->opts.reserved[0] & 2) == 0;
+                               r->opts.path_policy < 2 && (r->opts.diag_flags & 2) == 0;
         if (r->have_spare && in_kernel) {
             swap_with(r, r->spare);                       // current = clean bank
             CFPQ_CUDA_TRY(cudaStreamWaitEvent(s, r->spare_clean, 0));   // a side-stream clear, if any
@@ -1333,10 +1575,6 @@ static cfpq_status check_inputs(const cfpq_grammar* g, const cfpq_graph* d, cons
         CFPQ_CHECK_ARG(o->rank >= 0 && o->rank < o->world_size, "cfpq_closure: rank out of range");
         CFPQ_CHECK_ARG(o->nccl_unique_id != nullptr, "cfpq_closure: world_size > 1 needs nccl_unique_id");
     }
-    if (o->path_policy == 3 && (o->world_size > 1 || o->reserved_emulate > 1)) {
-        set_error("cfpq_closure: the bit-row path (policy 3) runs on one GPU");
-        return CFPQ_E_UNSUPPORTED;
-    }
     if (o->path_policy == 3 && d->n_nodes > 262144) {
         set_error("cfpq_closure: the bit-row path keeps a row in registers: n_nodes <= 262144");
         return CFPQ_E_UNSUPPORTED;
@@ -1346,6 +1584,16 @@ static cfpq_status check_inputs(const cfpq_grammar* g, const cfpq_graph* d, cons
         return CFPQ_E_UNSUPPORTED;
     }
     CFPQ_CHECK_ARG(o->path_policy >= 0 && o->path_policy <= 3, "cfpq_closure: bad path_policy");
+    CFPQ_CHECK_ARG(o->grid_rows >= 0 && o->grid_cols >= 0, "cfpq_closure: negative grid");
+    if (o->grid_rows > 0 || o->grid_cols > 0) {
+        const int shards = o->world_size > 1 ? o->world_size : (o->reserved_emulate > 1 ? o->reserved_emulate : 1);
+        if (o->path_policy != 2 || o->grid_rows * o->grid_cols != shards) {
+            set_error("cfpq_closure: a 2-D grid needs the tensor engine (path_policy 2) and grid_rows * grid_cols "
+                      "= world_size (or emulated shards)");
+            return CFPQ_E_UNSUPPORTED;
+        }
+    }
+    CFPQ_CHECK_ARG(o->dense_launch >= 0 && o->dense_launch <= 3, "cfpq_closure: dense_launch must be 0..3");
     CFPQ_CHECK_ARG(o->cell_set >= 0 && o->cell_set <= 2, "cfpq_closure: cell_set must be 0, 1 or 2");
     CFPQ_CHECK_ARG(o->tensor_format >= 0 && o->tensor_format <= 2, "cfpq_closure: tensor_format must be 0, 1 or 2");
     return CFPQ_OK;
@@ -1876,6 +2124,20 @@ extern "C" cfpq_status cfpq_shard_rows(int64_t n_nodes, int32_t world_size, int3
     dense_partition(n_nodes, world_size, rank, &lo, &hi, &br);
     *row_lo = std::min<int64_t>(lo * 128, n_nodes);
     *row_hi = std::min<int64_t>(hi * 128, n_nodes);
+    return CFPQ_OK;
+}
+
+extern "C" cfpq_status cfpq_shard_block(int64_t n_nodes, int32_t grid_rows, int32_t grid_cols, int32_t rank,
+                                        int64_t* row_lo, int64_t* row_hi, int64_t* col_lo, int64_t* col_hi) {
+    CFPQ_CHECK_ARG(row_lo && row_hi && col_lo && col_hi, "cfpq_shard_block: NULL output");
+    CFPQ_CHECK_ARG(n_nodes >= 0 && grid_rows >= 1 && grid_cols >= 1 && rank >= 0 && rank < grid_rows * grid_cols,
+                   "cfpq_shard_block: bad grid or rank");
+    int64_t ilo, ihi, jlo, jhi;
+    dense_partition2(n_nodes, grid_rows, grid_cols, rank / grid_cols, rank % grid_cols, &ilo, &ihi, &jlo, &jhi);
+    *row_lo = std::min<int64_t>(ilo * 128, n_nodes);
+    *row_hi = std::min<int64_t>(ihi * 128, n_nodes);
+    *col_lo = std::min<int64_t>(jlo * 256, n_nodes);
+    *col_hi = std::min<int64_t>(jhi * 256, n_nodes);
     return CFPQ_OK;
 }
 

@@ -242,7 +242,7 @@ cudaError_t launch_bitmap_pairs(const uint32_t* T, int32_t n, int64_t Wp, const 
 struct DenseEngine;
 DenseEngine* dense_create(int32_t n, int32_t n_nt, int64_t Wp, const std::vector<Rule3>& rules,
                           const std::vector<int32_t>& is_const, cudaStream_t s, std::string* err, bool tensor,
-                          bool fp4);
+                          bool fp4, int64_t dlist_cap, int32_t launch_mode);
 bool dense_is_fp4(const DenseEngine* e);
 void dense_destroy(DenseEngine* e);
 cudaError_t dense_begin(DenseEngine* e, uint32_t* const* T, uint32_t* const* Tn, bool first, cudaStream_t s,
@@ -253,7 +253,24 @@ cudaError_t dense_begin(DenseEngine* e, uint32_t* const* T, uint32_t* const* Tn,
 cudaError_t rows_product(DenseEngine* e, uint32_t* const* T, uint32_t* const* Tn, const NTInfo* nt,
                          const int32_t* adj_idx, const uint64_t* log, unsigned long long n_seeds, bool first,
                          cudaStream_t s, int* launches);
-cudaError_t dense_product(DenseEngine* e, int64_t i_lo, int64_t i_hi, cudaStream_t s, int* launches);
+// T_k rows of row tiles [i_lo, i_hi) (128 rows) x column tiles [j_lo, j_hi) (256 columns;
+// j_hi < 0: all) of every output.
+cudaError_t dense_product(DenseEngine* e, int64_t i_lo, int64_t i_hi, cudaStream_t s, int* launches, int64_t j_lo = 0,
+                          int64_t j_hi = -1);
+// 2-D block exchange: copy the bit block rows [r_lo, r_hi) x words [w_lo, w_hi) of T between
+// the matrix and a contiguous staging buffer (to_buf 1: matrix -> buffer).
+cudaError_t bit_block_copy(uint32_t* T, int64_t Wp, int64_t r_lo, int64_t r_hi, int64_t w_lo, int64_t w_hi,
+                           uint32_t* buf, int to_buf, cudaStream_t s);
+// Row-block sharded bit-row iterations: begin (T_k := T_{k-1}), per shard plan + products of
+// rows [row_lo, row_hi), settle (list length; rebuilt from T_k minus T_{k-1} on overflow), the
+// exchange of the word lists (caller), then apply every rank's words to T_k.
+cudaError_t rows_begin(DenseEngine* e, const NTInfo* nt, const int32_t* adj_idx, const uint64_t* log,
+                       unsigned long long n_seeds, bool first, cudaStream_t s, int* launches);
+cudaError_t rows_shard(DenseEngine* e, int64_t row_lo, int64_t row_hi, cudaStream_t s, int* launches);
+cudaError_t rows_list_settle(DenseEngine* e, int64_t row_lo, int64_t row_hi, unsigned long long keep, cudaStream_t s,
+                             unsigned long long* count);
+cudaError_t rows_list(DenseEngine* e, unsigned long long want, void** list, unsigned long long* cap);
+cudaError_t rows_apply_all(DenseEngine* e, unsigned long long total, cudaStream_t s, int* launches);
 cudaError_t dense_finish(DenseEngine* e, cudaStream_t s, unsigned long long* new_total);
 unsigned long long* dense_total_counter(DenseEngine* e);
 int64_t dense_row_tiles(const DenseEngine* e);
@@ -267,6 +284,14 @@ bool nccl_allgather_u64(void* comm, uint64_t* buf, size_t count, int rank, cudaS
 bool nccl_exchange_rows(void* comm, uint32_t* const* mats, int n_mats, size_t block_words, int rank,
                         unsigned long long* counter, cudaStream_t s, std::string* err);
 void dense_partition(int64_t n, int world, int rank, int64_t* tile_lo, int64_t* tile_hi, int64_t* block_rows);
+// 2-D process grid gr x gc: shard (a, b) owns row tiles [ti_lo, ti_hi) (128 rows) and column
+// tiles [tj_lo, tj_hi) (256 columns) of every T_A.
+void dense_partition2(int64_t n, int gr, int gc, int a, int b, int64_t* ti_lo, int64_t* ti_hi, int64_t* tj_lo,
+                      int64_t* tj_hi);
+void* nccl_comm_split(void* comm, int color, int key, std::string* err);
+bool nccl_allgather_u32(void* comm, uint32_t* buf, size_t count, int rank, cudaStream_t s, std::string* err);
+bool nccl_allreduce_sum_u64(void* comm, unsigned long long* buf, size_t count, cudaStream_t s, std::string* err);
+bool nccl_group(bool start, std::string* err);
 const std::vector<int32_t>& dense_outputs(const DenseEngine* e);
 unsigned long long dense_kblocks(DenseEngine* e, bool reset);
 cudaError_t dense_account(DenseEngine* e, uint32_t* const* T, const std::vector<Rule3>& rules, cudaStream_t s,

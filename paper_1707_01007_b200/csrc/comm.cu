@@ -21,6 +21,7 @@ struct NcclApi {
     ncclResult_t (*GroupStart)() = nullptr;
     ncclResult_t (*GroupEnd)() = nullptr;
     ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*CommSplit)(ncclComm_t, int, int, ncclComm_t*, ncclConfig_t*) = nullptr;   // NCCL >= 2.18
     const char* (*GetErrorString)(ncclResult_t) = nullptr;
 };
 
@@ -54,6 +55,7 @@ static bool load_nccl(std::string* err) {
     SYM(CommDestroy);
     SYM(GetErrorString);
 #undef SYM
+    g_nccl.CommSplit = reinterpret_cast<decltype(g_nccl.CommSplit)>(dlsym(h, "ncclCommSplit"));
     g_nccl.h = h;
     return true;
 }
@@ -115,6 +117,60 @@ bool nccl_allgather_u64(void* comm, uint64_t* buf, size_t count, int rank, cudaS
         return false;
     }
     return true;
+}
+
+// Sub-communicator (2-D process grid rows / columns): ranks with the same color, ordered by key.
+void* nccl_comm_split(void* comm, int color, int key, std::string* err) {
+    if (!g_nccl.CommSplit) {
+        if (err) *err = "libnccl lacks ncclCommSplit (NCCL >= 2.18 needed for 2-D grids)";
+        return nullptr;
+    }
+    ncclComm_t out = nullptr;
+    ncclResult_t r = g_nccl.CommSplit((ncclComm_t)comm, color, key, &out, nullptr);
+    if (r != ncclSuccess) {
+        if (err) *err = std::string("ncclCommSplit: ") + g_nccl.GetErrorString(r);
+        return nullptr;
+    }
+    return out;
+}
+
+bool nccl_allgather_u32(void* comm, uint32_t* buf, size_t count, int rank, cudaStream_t s, std::string* err) {
+    ncclResult_t r = g_nccl.AllGather(buf + (size_t)rank * count, buf, count, ncclUint32, (ncclComm_t)comm, s);
+    if (r != ncclSuccess) {
+        if (err) *err = std::string("NCCL all-gather: ") + g_nccl.GetErrorString(r);
+        return false;
+    }
+    return true;
+}
+
+bool nccl_allreduce_sum_u64(void* comm, unsigned long long* buf, size_t count, cudaStream_t s, std::string* err) {
+    ncclResult_t r = g_nccl.AllReduce(buf, buf, count, ncclUint64, ncclSum, (ncclComm_t)comm, s);
+    if (r != ncclSuccess) {
+        if (err) *err = std::string("NCCL all-reduce: ") + g_nccl.GetErrorString(r);
+        return false;
+    }
+    return true;
+}
+
+bool nccl_group(bool start, std::string* err) {
+    ncclResult_t r = start ? g_nccl.GroupStart() : g_nccl.GroupEnd();
+    if (r != ncclSuccess) {
+        if (err) *err = std::string("NCCL group: ") + g_nccl.GetErrorString(r);
+        return false;
+    }
+    return true;
+}
+
+// 2-D grid: rows split like dense_partition over gr, 256-column tiles split over gc.
+void dense_partition2(int64_t n, int gr, int gc, int a, int b, int64_t* ti_lo, int64_t* ti_hi, int64_t* tj_lo,
+                      int64_t* tj_hi) {
+    int64_t br;
+    dense_partition(n, gr, a, ti_lo, ti_hi, &br);
+    const int64_t np = ((n + 255) / 256) * 256;
+    const int64_t jt = np / 256 > 0 ? np / 256 : 1;
+    const int64_t bj = (jt + gc - 1) / gc;
+    *tj_lo = std::min<int64_t>((int64_t)b * bj, jt);
+    *tj_hi = std::min<int64_t>(*tj_lo + bj, jt);
 }
 
 // Row-block partition of the dense engine: tiles of 128 rows, equal blocks of

@@ -51,6 +51,7 @@ struct DenseParams {
     unsigned long long* new_cells; // [n_nt + 1] new cells per NT, [n_nt] = total
     int32_t n_nt;
     int32_t i_lo, i_hi;            // row-tile range of this rank (row-block sharding)
+    int32_t j_lo, j_hi;            // column-tile range (256-column tiles; 2-D block sharding)
 };
 
 // ------------------------------------------------------------------------------------------
@@ -345,7 +346,7 @@ __device__ __forceinline__ void tile_coords(const DenseParams& p, int t, int til
     const int within = rem - g * (kGroup * n_j);
     const int rows_g = min(kGroup, n_i - g * kGroup);
     I = g * kGroup + within % rows_g;   // relative to the rank's first (pair of) row tile(s)
-    J = within / rows_g;
+    J = p.j_lo + within / rows_g;        // absolute column tile
 }
 
 // kCl = 2: CTA pairs (thread-block clusters of 2) compute row tiles I0 and I0+1 of the same
@@ -377,7 +378,7 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
     uint32_t* tmem_base_smem = reinterpret_cast<uint32_t*>(tmem_empty + 2);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int n_j = p.np / kTN;
+    const int n_j = p.j_hi - p.j_lo;
     const int n_i = (p.i_hi - p.i_lo + kCl - 1) / kCl;   // (pairs of) row tiles
     const int tiles_per_nt = n_i * n_j;
     const int total_tiles = tiles_per_nt * p.n_out;
@@ -668,7 +669,7 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
 
     constexpr int kAcc = kF4 ? 1 : 2;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int n_j = p.np / kTN;
+    const int n_j = p.j_hi - p.j_lo;
     const int n_i = (p.i_hi - p.i_lo + 1) / 2;        // pairs of row tiles
     const int tiles_per_nt = n_i * n_j;
     const int total_tiles = tiles_per_nt * p.n_out;
@@ -934,6 +935,7 @@ struct RowsCtx {
                                        // [3] V chunks, [4] L/P tasks
     int32_t first;                     // iteration 1 (both-preterminal rules evaluated)
     int32_t n_rules;
+    int32_t row_lo, row_hi;            // rows this shard derives (row-block sharding; [0, n) else)
 };
 
 enum : int { RF_NONE = 0, RF_L = 1, RF_R = 2, RF_V = 3, RF_P = 4 };
@@ -1022,7 +1024,7 @@ __global__ void rows_plan_kernel(DenseParams p, RowsCtx c, RowChunk* chunks, uns
         }
         __syncthreads();
     }
-    const int64_t tasks = (int64_t)c.n_rules * p.n;
+    const int64_t tasks = (int64_t)c.n_rules * (c.row_hi - c.row_lo);   // this shard's rows only
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t t0 = blockIdx.x * (int64_t)blockDim.x; t0 < tasks; t0 += stride) {
         const int64_t t = t0 + threadIdx.x;
@@ -1037,6 +1039,7 @@ __global__ void rows_plan_kernel(DenseParams p, RowsCtx c, RowChunk* chunks, uns
                 i = (int)(t / c.n_rules);
                 q = (int)(t - (int64_t)i * c.n_rules);
             }
+            i += c.row_lo;
             DenseRule r;
             int f;
             const int32_t* bptr;
@@ -1373,6 +1376,48 @@ __global__ void __launch_bounds__(kRowThreads) rows_gather_kernel(DenseParams p,
     if (lane == 0 && my_new) atomicAdd(p.new_cells + p.n_nt, my_new);
 }
 
+// Row-block sharding of the bit-row engine (§8(e)).  Every rank keeps full replicas of
+// T_{k-1} and T_k and derives only its rows [row_lo, row_hi); its Δ_k word list is exchanged
+// and applied on every rank.  Applying a word ORs it into T_k and counts the bits it flips
+// (into the new-cell total and the row popcounts): idempotent, so words a rank already holds
+// (its own, or every shard's when the shards are emulated in one process) flip nothing.
+__global__ void rows_apply_kernel(DenseParams p, RowsCtx c, unsigned long long begin, unsigned long long end) {
+    unsigned long long flips = 0;
+    for (unsigned long long e = begin + blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; e < end;
+         e += (unsigned long long)gridDim.x * blockDim.x) {
+        const uint4 d = c.dlist[e];
+        uint32_t* addr = p.Tn[d.x] + (size_t)d.y * p.Wp + d.z;
+        if ((d.w & ~*addr) == 0) continue;
+        const uint32_t fl = d.w & ~atomicOr(addr, d.w);
+        if (fl) {
+            atomicAdd(c.cnt + (size_t)d.x * p.n + d.y, (uint32_t)__popc(fl));
+            flips += __popc(fl);
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) flips += __shfl_xor_sync(0xffffffffu, flips, o);
+    if ((threadIdx.x & 31) == 0 && flips) atomicAdd(p.new_cells + p.n_nt, flips);
+}
+
+// A shard's Δ_k word list after it overflowed: rebuild it from T_k minus T_{k-1} over the
+// shard's rows (count = 1: only count the words that gained bits).  Runs only on overflow.
+__global__ void rows_diff_kernel(DenseParams p, RowsCtx c, int count_only) {
+    const int64_t wn = (p.n + 31) / 32;
+    const int64_t per_nt = (int64_t)(c.row_hi - c.row_lo) * wn;
+    const int64_t total = per_nt * p.n_out;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+        const int o = (int)(t / per_nt);
+        const int64_t rem = t - (int64_t)o * per_nt;
+        const int i = c.row_lo + (int)(rem / wn);
+        const int64_t w = rem - (int64_t)(i - c.row_lo) * wn;
+        const int A = p.out_nt[o];
+        const uint32_t d = p.Tn[A][(size_t)i * p.Wp + w] & ~p.T[A][(size_t)i * p.Wp + w];
+        if (!d) continue;
+        const unsigned long long at = atomicAdd(c.rc + 1, 1ull);
+        if (!count_only && at < c.dlist_cap) c.dlist[at] = make_uint4((uint32_t)A, (uint32_t)i, (uint32_t)w, d);
+    }
+}
+
 // ------------------------------------------------------------------------------------------
 // host side
 // ------------------------------------------------------------------------------------------
@@ -1437,6 +1482,10 @@ struct DenseEngine {
     void* dlist = nullptr;                     // bit-row path: Δ_k word list (uint4)
     unsigned long long dlist_cap = 0;
     unsigned long long* rc = nullptr;          // bit-row path counters
+    int32_t launch_mode = 0;                   // cfpq_options.dense_launch
+    const NTInfo* rows_nt = nullptr;           // bit-row path: this iteration's NT table / CSR
+    const int32_t* rows_adj = nullptr;
+    bool rows_first = false;
     ~DenseEngine() {
         cudaFree(cnt);
         cudaFree(rule_out);
@@ -1453,7 +1502,7 @@ void dense_destroy(DenseEngine* e) { delete e; }
 
 DenseEngine* dense_create(int32_t n, int32_t n_nt, int64_t Wp, const std::vector<Rule3>& rules,
                           const std::vector<int32_t>& is_const, cudaStream_t s, std::string* err, bool tensor,
-                          bool fp4) {
+                          bool fp4, int64_t dlist_cap, int32_t launch_mode) {
     DenseEngine* e = new DenseEngine();
     e->fp4 = fp4;
     e->n = n;
@@ -1555,6 +1604,8 @@ DenseEngine* dense_create(int32_t n, int32_t n_nt, int64_t Wp, const std::vector
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int total = e->n_out * (e->np / kTM) * (e->np / kTN);
     e->grid = std::max(1, std::min(sms, total));
+    e->launch_mode = launch_mode;
+    e->dlist_cap = dlist_cap > 0 ? (unsigned long long)dlist_cap : (1ull << 20);   // bit-row Δ_k word list
     return e;
 }
 
@@ -1585,8 +1636,10 @@ cudaError_t dense_begin(DenseEngine* e, uint32_t* const* T, uint32_t* const* Tn,
     return cudaMemsetAsync(e->new_cells, 0, (e->n_nt + 2) * 8, s);
 }
 
-cudaError_t dense_product(DenseEngine* e, int64_t i_lo, int64_t i_hi, cudaStream_t s, int* launches) {
-    if (e->n_out == 0 || i_hi <= i_lo) return cudaSuccess;
+cudaError_t dense_product(DenseEngine* e, int64_t i_lo, int64_t i_hi, cudaStream_t s, int* launches, int64_t j_lo,
+                          int64_t j_hi) {
+    if (j_hi < 0) j_hi = e->np / kTN;
+    if (e->n_out == 0 || i_hi <= i_lo || j_hi <= j_lo) return cudaSuccess;
     DenseParams p{};
     p.n = e->n;
     p.np = e->np;
@@ -1603,26 +1656,21 @@ cudaError_t dense_product(DenseEngine* e, int64_t i_lo, int64_t i_hi, cudaStream
     p.n_nt = e->n_nt;
     p.i_lo = (int32_t)i_lo;
     p.i_hi = (int32_t)i_hi;
+    p.j_lo = (int32_t)j_lo;
+    p.j_hi = (int32_t)j_hi;
     int dev = 0, sms = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    // CTA pairs with a multicast B tile: measured 18% SLOWER on config S (31.6 vs 26.7 ms at
-    // n = 16,384: the pair runs in lockstep and a 2-CTA multicast saves no L2 traffic, cf.
-    // B300_MICROARCH "TMA-MC at csz <= 4, MC ~ UC"), so it is opt-in (CFPQ_DENSE_PAIR=1)
-    static const bool pair = [] {
-        const char* v = getenv("CFPQ_DENSE_PAIR");
-        return v && v[0] == '1';
-    }();
-    // 2-SM pairs (cta_group::2, M = 256) by default (CFPQ_DENSE_2SM=0: one CTA per SM).
-    // Config S, n = 16,384: fp4 10.3 vs 10.7 ms, int8 18.0 vs 20.5 ms (once the skip list
-    // stopped sitting on the issue path; before that the pair was slower)
-    static const bool two_sm = [] {
-        const char* v = getenv("CFPQ_DENSE_2SM");
-        return !(v && v[0] == '0');
-    }();
+    // cfpq_options.dense_launch: CTA pairs with one M = 256 UMMA per pair (cta_group::2) by
+    // default (config S, n = 16,384: fp4 10.3 vs 10.7 ms one CTA per SM, int8 18.0 vs 20.5
+    // ms); CTA pairs sharing a multicast B tile measured 18% SLOWER than one CTA per SM (31.6
+    // vs 26.7 ms: the pair runs in lockstep and a 2-CTA multicast saves no L2 traffic, cf.
+    // B300_MICROARCH "TMA-MC at csz <= 4, MC ~ UC")
+    const bool pair = e->launch_mode == 3;
+    const bool two_sm = e->launch_mode == 0 || e->launch_mode == 1;
     const bool use2 = two_sm && sms >= 2 && !pair;
     if (use2) {
-        const int64_t units = (int64_t)e->n_out * ((i_hi - i_lo + 1) / 2) * (e->np / kTN);
+        const int64_t units = (int64_t)e->n_out * ((i_hi - i_lo + 1) / 2) * (j_hi - j_lo);
         const int grid = (int)std::max<int64_t>(2, std::min<int64_t>(sms / 2, units) * 2);
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3(grid);
@@ -1645,7 +1693,7 @@ cudaError_t dense_product(DenseEngine* e, int64_t i_lo, int64_t i_hi, cudaStream
     }
     if (pair && sms >= 2) {
         // CTA pairs (clusters of 2) share the B tile through TMA multicast
-        const int64_t units = (int64_t)e->n_out * ((i_hi - i_lo + 1) / 2) * (e->np / kTN);
+        const int64_t units = (int64_t)e->n_out * ((i_hi - i_lo + 1) / 2) * (j_hi - j_lo);
         const int grid = (int)std::max<int64_t>(2, std::min<int64_t>(sms / 2, units) * 2);
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3(grid);
@@ -1666,7 +1714,7 @@ cudaError_t dense_product(DenseEngine* e, int64_t i_lo, int64_t i_hi, cudaStream
         if (launches) ++*launches;
         return c != cudaSuccess ? c : cudaGetLastError();
     }
-    const int64_t total = (int64_t)e->n_out * (i_hi - i_lo) * (e->np / kTN);
+    const int64_t total = (int64_t)e->n_out * (i_hi - i_lo) * (j_hi - j_lo);
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(sms, total));
     if (e->fp4)
         dense_kernel<1, true><<<grid, kDenseThreads, dense_smem_bytes(), s>>>(p, e->tmA, e->tmB, e->mapA_row, e->mapB_row);
@@ -1684,11 +1732,54 @@ static int resident_grid(K kernel, int threads, int sms) {
     return sms * per;
 }
 
-cudaError_t rows_product(DenseEngine* e, uint32_t* const* T, uint32_t* const* Tn, const NTInfo* nt,
-                         const int32_t* adj_idx, const uint64_t* log, unsigned long long n_seeds, bool first,
-                         cudaStream_t s, int* launches) {
-    (void)T;
-    (void)Tn;   // the kernels read the device copies set by dense_begin
+// 2-D block exchange staging (rows [r_lo, r_hi) x words [w_lo, w_hi) <-> contiguous buffer).
+__global__ void bit_block_copy_kernel(uint32_t* T, int64_t Wp, int64_t r_lo, int64_t rows, int64_t w_lo, int64_t words,
+                                      uint32_t* buf, int to_buf) {
+    const int64_t total = rows * words;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = t / words, w = t - r * words;
+        uint32_t* m = T + (size_t)(r_lo + r) * Wp + w_lo + w;
+        if (to_buf) buf[t] = *m;
+        else *m = buf[t];
+    }
+}
+
+cudaError_t bit_block_copy(uint32_t* T, int64_t Wp, int64_t r_lo, int64_t r_hi, int64_t w_lo, int64_t w_hi,
+                           uint32_t* buf, int to_buf, cudaStream_t s) {
+    if (r_hi <= r_lo || w_hi <= w_lo) return cudaSuccess;
+    const int64_t total = (r_hi - r_lo) * (w_hi - w_lo);
+    const int grid = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
+    bit_block_copy_kernel<<<grid, 256, 0, s>>>(T, Wp, r_lo, r_hi - r_lo, w_lo, w_hi - w_lo, buf, to_buf);
+    return cudaGetLastError();
+}
+
+static DenseParams rows_params(DenseEngine* e) {
+    DenseParams p{};
+    p.n = e->n;
+    p.np = e->np;
+    p.Wp = e->Wp;
+    p.n_out = e->n_out;
+    p.out_nt = e->out_nt;
+    p.rule_ptr = e->rule_ptr;
+    p.rules = e->rules;
+    p.T = e->Tptr;
+    p.Tn = e->Tnptr;
+    p.new_cells = e->new_cells;
+    p.n_nt = e->n_nt;
+    return p;
+}
+
+static int device_sms() {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return sms;
+}
+
+// Start of a bit-row iteration: T_k buffer := T_{k-1} (seed cells at iteration 1, else
+// T_{k-2} | Δ_{k-1} words), Δ_k list and chunk counters reset.
+cudaError_t rows_begin(DenseEngine* e, const NTInfo* nt, const int32_t* adj_idx, const uint64_t* log,
+                       unsigned long long n_seeds, bool first, cudaStream_t s, int* launches) {
     if (e->n_out == 0) return cudaSuccess;
     if ((e->n + 31) / 32 > (int64_t)kRowMaxV4 * 4 * kRowThreads) return cudaErrorInvalidValue;
     cudaError_t c;
@@ -1697,9 +1788,6 @@ cudaError_t rows_product(DenseEngine* e, uint32_t* const* T, uint32_t* const* Tn
         if ((c = cudaMalloc(&e->rcnt, (size_t)e->n_nt * std::max(e->n, 1) * 4)) != cudaSuccess) return c;
         if ((c = cudaMalloc(&e->rc, 8 * 8)) != cudaSuccess) return c;
         if ((c = cudaMemsetAsync(e->rc, 0, 8 * 8, s)) != cudaSuccess) return c;
-        // testing knob: a tiny list exercises the whole-matrix fallback after an overflow
-        const char* cap_env = getenv("CFPQ_ROWS_DLIST_CAP");
-        e->dlist_cap = cap_env ? std::max(1ull, strtoull(cap_env, nullptr, 10)) : (1ull << 20);
         if ((c = cudaMalloc(&e->dlist, e->dlist_cap * sizeof(uint4))) != cudaSuccess) return c;
     }
     // chunk capacity: grow lazily (the plan reports the exact count)
@@ -1717,25 +1805,12 @@ cudaError_t rows_product(DenseEngine* e, uint32_t* const* T, uint32_t* const* Tn
         }
         e->forms_known = true;
     }
-    DenseParams p{};
-    p.n = e->n;
-    p.np = e->np;
-    p.Wp = e->Wp;
-    p.n_out = e->n_out;
-    p.out_nt = e->out_nt;
-    p.rule_ptr = e->rule_ptr;
-    p.rules = e->rules;
-    p.T = e->Tptr;
-    p.Tn = e->Tnptr;
-    p.new_cells = e->new_cells;
-    p.n_nt = e->n_nt;
-    RowsCtx rc{nt, adj_idx, e->rcnt, (uint4*)e->dlist, e->dlist_cap, e->rc, first ? 1 : 0, n_rules};
-    int sms = 148;
-    {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    }
+    e->rows_nt = nt;
+    e->rows_adj = adj_idx;
+    e->rows_first = first;
+    DenseParams p = rows_params(e);
+    RowsCtx rc{nt, adj_idx, e->rcnt, (uint4*)e->dlist, e->dlist_cap, e->rc, first ? 1 : 0, n_rules, 0, e->n};
+    const int sms = device_sms();
     // T_k buffer := T_{k-1}
     if (first) {
         if ((c = cudaMemsetAsync(e->rcnt, 0, (size_t)e->n_nt * e->n * 4, s)) != cudaSuccess) return c;
@@ -1744,10 +1819,26 @@ cudaError_t rows_product(DenseEngine* e, uint32_t* const* T, uint32_t* const* Tn
     } else {
         rows_delta_kernel<<<sms * 8, 256, 0, s>>>(p, rc);
     }
-    // Δ_k list and chunk counter restart; plan
+    if (launches) *launches += 1;
+    // Δ_k list and chunk counters restart
     if ((c = cudaMemsetAsync(e->rc, 0, 2 * 8, s)) != cudaSuccess) return c;
     if ((c = cudaMemsetAsync(e->rc + 3, 0, 2 * 8, s)) != cudaSuccess) return c;
+    return cudaGetLastError();
+}
+
+// Plan + products of the rows [row_lo, row_hi) of every output (all rows: one GPU).  Δ_k
+// words are appended to the list after the ones already there (earlier emulated shards).
+cudaError_t rows_shard(DenseEngine* e, int64_t row_lo, int64_t row_hi, cudaStream_t s, int* launches) {
+    if (e->n_out == 0 || row_hi <= row_lo) return cudaSuccess;
+    cudaError_t c;
+    const int32_t n_rules = (int32_t)e->h_rule_out.size();
+    DenseParams p = rows_params(e);
+    RowsCtx rc{e->rows_nt, e->rows_adj, e->rcnt, (uint4*)e->dlist, e->dlist_cap, e->rc, e->rows_first ? 1 : 0,
+               n_rules, (int32_t)row_lo, (int32_t)row_hi};
+    const int sms = device_sms();
     for (int attempt = 0; attempt < 2; ++attempt) {
+        if ((c = cudaMemsetAsync(e->rc, 0, 8, s)) != cudaSuccess) return c;       // chunk lists of this shard
+        if ((c = cudaMemsetAsync(e->rc + 3, 0, 2 * 8, s)) != cudaSuccess) return c;
         rows_plan_kernel<<<sms * 8, 256, 0, s>>>(p, rc, (RowChunk*)e->chunks, e->chunk_cap);
         unsigned long long got[5] = {0, 0, 0, 0, 0};
         if ((c = cudaMemcpyAsync(got, e->rc, 5 * 8, cudaMemcpyDeviceToHost, s)) != cudaSuccess) return c;
@@ -1767,8 +1858,6 @@ cudaError_t rows_product(DenseEngine* e, uint32_t* const* T, uint32_t* const* Tn
         cudaFree(e->chunks);
         e->chunk_cap = need + need / 4;
         if ((c = cudaMalloc(&e->chunks, 3 * e->chunk_cap * sizeof(RowChunk))) != cudaSuccess) return c;
-        if ((c = cudaMemsetAsync(e->rc, 0, 8, s)) != cudaSuccess) return c;
-        if ((c = cudaMemsetAsync(e->rc + 3, 0, 2 * 8, s)) != cudaSuccess) return c;
     }
     // 4 CTAs x 8 warps per SM (measured: 6 or 8 CTAs with fewer registers are not faster)
     rows_scatter_kernel<<<resident_grid(rows_scatter_kernel, 256, sms), 256, 0, s>>>(p, rc, e->rule_out,
@@ -1789,7 +1878,78 @@ cudaError_t rows_product(DenseEngine* e, uint32_t* const* T, uint32_t* const* Tn
         // (config 4: 10.2 ms closure; 4 / 8 / 16 uint4 per lane: 10.7 / 11.8 / 16.0 ms; 1: 11.5 ms)
         rows_rgather_kernel<2><<<resident_grid(rows_rgather_kernel<2>, 256, sms), 256, 0, s>>>(p, rc, e->rule_out, chR);
     }
-    if (launches) *launches += 3 + (e->has_v ? 1 : 0) + (e->has_r ? 1 : 0);
+    if (launches) *launches += 2 + (e->has_v ? 1 : 0) + (e->has_r ? 1 : 0);
+    return cudaGetLastError();
+}
+
+cudaError_t rows_product(DenseEngine* e, uint32_t* const* T, uint32_t* const* Tn, const NTInfo* nt,
+                         const int32_t* adj_idx, const uint64_t* log, unsigned long long n_seeds, bool first,
+                         cudaStream_t s, int* launches) {
+    (void)T;
+    (void)Tn;   // the kernels read the device copies set by dense_begin
+    cudaError_t c = rows_begin(e, nt, adj_idx, log, n_seeds, first, s, launches);
+    if (c != cudaSuccess) return c;
+    return rows_shard(e, 0, e->n, s, launches);
+}
+
+// Sharded runs: the list length after a shard's products (host read, synchronises); when
+// the list overflowed, the shard's words are rebuilt from T_k minus T_{k-1} into a grown list
+// (the entries [0, keep) of earlier emulated shards are kept).
+cudaError_t rows_list_settle(DenseEngine* e, int64_t row_lo, int64_t row_hi, unsigned long long keep, cudaStream_t s,
+                             unsigned long long* count) {
+    cudaError_t c;
+    unsigned long long m = 0;
+    if ((c = cudaMemcpyAsync(&m, e->rc + 1, 8, cudaMemcpyDeviceToHost, s)) != cudaSuccess) return c;
+    if ((c = cudaStreamSynchronize(s)) != cudaSuccess) return c;
+    if (m > e->dlist_cap) {
+        const unsigned long long cap = std::max<unsigned long long>(e->dlist_cap * 2, m + m / 4 + 1024);
+        void* nl = nullptr;
+        if ((c = cudaMalloc(&nl, cap * sizeof(uint4))) != cudaSuccess) return c;
+        if (keep && (c = cudaMemcpyAsync(nl, e->dlist, keep * sizeof(uint4), cudaMemcpyDeviceToDevice, s)) != cudaSuccess)
+            return c;
+        if ((c = cudaStreamSynchronize(s)) != cudaSuccess) return c;
+        cudaFree(e->dlist);
+        e->dlist = nl;
+        e->dlist_cap = cap;
+        if ((c = cudaMemcpyAsync(e->rc + 1, &keep, 8, cudaMemcpyHostToDevice, s)) != cudaSuccess) return c;
+        DenseParams p = rows_params(e);
+        RowsCtx rc{e->rows_nt, e->rows_adj, e->rcnt, (uint4*)e->dlist, e->dlist_cap, e->rc, 0,
+                   (int32_t)e->h_rule_out.size(), (int32_t)row_lo, (int32_t)row_hi};
+        rows_diff_kernel<<<device_sms() * 8, 256, 0, s>>>(p, rc, 0);
+        if ((c = cudaMemcpyAsync(&m, e->rc + 1, 8, cudaMemcpyDeviceToHost, s)) != cudaSuccess) return c;
+        if ((c = cudaStreamSynchronize(s)) != cudaSuccess) return c;
+        if (m > e->dlist_cap) return cudaErrorMemoryAllocation;
+    }
+    *count = m;
+    return cudaGetLastError();
+}
+
+// The Δ_k word list (uint4 {A, i, word, bits}) for the exchange; `ensure` grows it (content
+// not kept) to hold `want` words.
+cudaError_t rows_list(DenseEngine* e, unsigned long long want, void** list, unsigned long long* cap) {
+    if (want > e->dlist_cap) {
+        cudaFree(e->dlist);
+        e->dlist = nullptr;
+        const unsigned long long nc = want + want / 4 + 1024;
+        cudaError_t c = cudaMalloc(&e->dlist, nc * sizeof(uint4));
+        if (c != cudaSuccess) return c;
+        e->dlist_cap = nc;
+    }
+    *list = e->dlist;
+    *cap = e->dlist_cap;
+    return cudaSuccess;
+}
+
+// After the exchange: the list holds every rank's words [0, total); apply them to T_k.
+cudaError_t rows_apply_all(DenseEngine* e, unsigned long long total, cudaStream_t s, int* launches) {
+    cudaError_t c;
+    if ((c = cudaMemcpyAsync(e->rc + 1, &total, 8, cudaMemcpyHostToDevice, s)) != cudaSuccess) return c;
+    if (total == 0) return cudaSuccess;
+    DenseParams p = rows_params(e);
+    RowsCtx rc{e->rows_nt, e->rows_adj, e->rcnt, (uint4*)e->dlist, e->dlist_cap, e->rc, 0,
+               (int32_t)e->h_rule_out.size(), 0, e->n};
+    rows_apply_kernel<<<device_sms() * 8, 256, 0, s>>>(p, rc, 0ull, total);
+    if (launches) *launches += 1;
     return cudaGetLastError();
 }
 

@@ -106,3 +106,18 @@ def test_asynchronous_schedule(n):
 def test_emulated_row_shards(n, ranks):
     gd, w, r = _run(n, emulate_ranks=ranks)
     _check(gd, w, r)
+
+
+@pytest.mark.parametrize("n", SIZES)
+def test_bit_row_engine_emulated_shards(n):
+    """The row-sharded paper-faithful engine (8 shards: word-list exchange + apply) at full size."""
+    gd, w, r = _run(n, path_policy=3, emulate_ranks=8)
+    _check(gd, w, r)
+
+
+@pytest.mark.parametrize("n", SIZES)
+def test_gauss_seidel_schedule(n):
+    """Schedule 3: the same fixpoint in fewer iterations (relations only)."""
+    gd, w, r = _run(n, schedule=3)
+    _check(gd, w, r, per_iteration=False, iterations=False)
+    assert r.iterations < gd["iterations"]

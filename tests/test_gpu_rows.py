@@ -66,23 +66,14 @@ def test_rows_ontology_and_reuse(query):
 
 def test_rows_delta_list_overflow_fallback():
     """A Δ word list that overflows makes the next iteration copy whole matrices instead
-    (and the list grows): same states.  CFPQ_ROWS_DLIST_CAP=8 forces it from iteration 1."""
-    import os
-    import subprocess
-    import sys
-    code = (
-        "import inputs as I\n"
-        "from tests.gpu_util import gpu_closure, assert_parity\n"
-        "for w in (I.config4_workload(n=1500), I.dense_stress_workload(200, 2, seed=1)):\n"
-        "    r, _, _ = gpu_closure(w, path_policy=3)\n"
-        "    o = assert_parity(w, r)\n"
-        "    nc, _ = r.iteration_stats()\n"
-        "    assert nc.tolist() == o.stats()['new_bits'].tolist()\n"
-        "print('ok')\n")
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, CFPQ_ROWS_DLIST_CAP="8", PYTHONPATH=root)
-    out = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
-    assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
+    (and the list grows): same states.  rows_list_capacity = 8 forces it from iteration 1;
+    the row-sharded variant rebuilds the shard's list from T_k minus T_{k-1} instead."""
+    for w in (I.config4_workload(n=1500), I.dense_stress_workload(200, 2, seed=1)):
+        for kw in (dict(), dict(emulate_ranks=3)):
+            r, _, _ = gpu_closure(w, path_policy=3, rows_list_capacity=8, **kw)
+            o = assert_parity(w, r)
+            nc, _ = r.iteration_stats()
+            assert nc.tolist() == o.stats()["new_bits"].tolist(), (w.name, kw)
 
 
 def test_rows_wide_rows_agree_with_sparse():
@@ -133,3 +124,38 @@ def test_rows_wider_than_config4():
     assert r3.iteration_stats()[0].tolist() == r1.iteration_stats()[0].tolist()
     for A in range(w.n_nt):
         assert np.array_equal(r3.pairs(A), r1.pairs(A)), w.nt_names[A]
+
+
+@pytest.mark.parametrize("ranks", [2, 3, 8])
+def test_rows_shards_emulated(ranks):
+    """Row-block sharded bit-row engine (§8(e)): every shard derives its rows from full
+    replicas, the Δ_k word lists go through the padded exchange buffer and the rank-order
+    compaction, every word is applied to T_k (flip-counted).  Jacobi states per iteration."""
+    for w in (I.ontology_workload("q1", 700, depth=7, seed=ranks), I.ontology_workload("q2", 500, depth=6, seed=1),
+              I.config4_workload(n=1500, seed=ranks), I.anbn_workload(3, 7), I.dense_stress_workload(300, 2, seed=2),
+              I.example_workload()):
+        r, _, _ = gpu_closure(w, path_policy=3, emulate_ranks=ranks)
+        ores = assert_parity(w, r)
+        nc, _ = r.iteration_stats()
+        assert nc.tolist() == ores.stats()["new_bits"].tolist(), (w.name, ranks)
+
+
+def test_rows_shards_random_grammars():
+    for s in range(60):
+        w = I.random_workload(90_000 + s, max_nodes=80, max_edges=240, max_nt=6, max_bin=10, max_term=5)
+        r, _, _ = gpu_closure(w, path_policy=3, emulate_ranks=2 + s % 5)
+        ores = assert_parity(w, r)
+        nc, _ = r.iteration_stats()
+        assert nc.tolist() == ores.stats()["new_bits"].tolist(), w.name
+
+
+def test_rows_nccl_single_rank():
+    """The NCCL exchange of the word lists with one rank (libnccl dlopen'ed, counts + padded
+    words all-gathered every iteration)."""
+    from paper_1707_01007_b200 import cfpq as C
+    uid = C.nccl_unique_id()
+    w = I.config4_workload(n=2000, seed=4)
+    r, _, _ = gpu_closure(w, path_policy=3, world_size=1, rank=0, nccl_unique_id=uid)
+    ores = assert_parity(w, r)
+    nc, _ = r.iteration_stats()
+    assert nc.tolist() == ores.stats()["new_bits"].tolist()

@@ -155,54 +155,32 @@ def test_auto_policy_switches_to_tensor(n, d):
 
 
 def test_tensor_cta_pairs_multicast():
-    """The opt-in CTA-pair variant (clusters of 2 sharing the B tile through TMA multicast,
-    MMA commits arriving on both CTAs' stage barriers) gives the same closure, including an
-    odd number of row tiles (the second tile of the last pair does not exist)."""
-    import os
-    import subprocess
-    import sys
-    code = (
-        "import inputs as I, numpy as np\n"
-        "from tests.gpu_util import gpu_closure, assert_parity\n"
-        "for n, d in [(300, 2), (1000, 2), (130, 1)]:\n"
-        "    w = I.dense_stress_workload(n, d, seed=n)\n"
-        "    r, _, _ = gpu_closure(w, path_policy=2, tensor_format=1)\n"
-        "    assert_parity(w, r)\n"
-        "    r, _, _ = gpu_closure(w, path_policy=2, tensor_format=1, emulate_ranks=3)\n"
-        "    assert_parity(w, r)\n"
-        "print('ok')\n")
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, CFPQ_DENSE_PAIR="1", PYTHONPATH=root)
-    out = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
-    assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
+    """dense_launch = 3: CTA pairs (clusters of 2) sharing the B tile through TMA multicast,
+    MMA commits arriving on both CTAs' stage barriers; same closure, including an odd number
+    of row tiles (the second tile of the last pair does not exist)."""
+    for n, d in [(300, 2), (1000, 2), (130, 1)]:
+        w = I.dense_stress_workload(n, d, seed=n)
+        r, _, _ = gpu_closure(w, path_policy=2, tensor_format=1, dense_launch=3)
+        assert_parity(w, r)
+        r, _, _ = gpu_closure(w, path_policy=2, tensor_format=1, dense_launch=3, emulate_ranks=3)
+        assert_parity(w, r)
 
 
 def test_tensor_one_cta_per_sm():
-    """The one-CTA-per-SM kernel (CFPQ_DENSE_2SM=0; the default is the 2-SM pair kernel:
+    """dense_launch = 2: the one-CTA-per-SM kernel (the default is the 2-SM pair kernel:
     cta_group::2, M = 256 UMMAs issued by the even CTA, each CTA staging its A rows and half
     of B, TMA bytes of both CTAs completing on the leader's barrier) in both formats,
     including the emulated row-block shards."""
-    import os
-    import subprocess
-    import sys
-    code = (
-        "import inputs as I\n"
-        "from tests.gpu_util import gpu_closure, assert_parity\n"
-        "for fmt in (1, 2):\n"
-        "    for n, d in [(300, 2), (700, 2), (130, 1)]:\n"
-        "        w = I.dense_stress_workload(n, d, seed=n)\n"
-        "        r, _, _ = gpu_closure(w, path_policy=2, tensor_format=fmt)\n"
-        "        o = assert_parity(w, r)\n"
-        "        nc, _ = r.iteration_stats()\n"
-        "        assert nc.tolist() == o.stats()['new_bits'].tolist()\n"
-        "    w = I.ontology_workload('union', 500, depth=5, seed=3)\n"
-        "    r, _, _ = gpu_closure(w, path_policy=2, tensor_format=fmt, emulate_ranks=3)\n"
-        "    assert_parity(w, r)\n"
-        "print('ok')\n")
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, CFPQ_DENSE_2SM="0", PYTHONPATH=root)
-    out = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=900)
-    assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
+    for fmt in (1, 2):
+        for n, d in [(300, 2), (700, 2), (130, 1)]:
+            w = I.dense_stress_workload(n, d, seed=n)
+            r, _, _ = gpu_closure(w, path_policy=2, tensor_format=fmt, dense_launch=2)
+            o = assert_parity(w, r)
+            nc, _ = r.iteration_stats()
+            assert nc.tolist() == o.stats()["new_bits"].tolist()
+        w = I.ontology_workload("union", 500, depth=5, seed=3)
+        r, _, _ = gpu_closure(w, path_policy=2, tensor_format=fmt, dense_launch=2, emulate_ranks=3)
+        assert_parity(w, r)
 
 
 @pytest.mark.parametrize("fmt", [1, 2])
@@ -236,3 +214,62 @@ def test_tensor_config_s_full_size_sampled(fmt):
         got = pairs[starts[s]:starts[s + 1], 1]
         assert np.array_equal(got, np.array(sorted(seen), dtype=got.dtype)), s
     assert r.iterations == 7
+
+
+@pytest.mark.parametrize("grid", [(2, 2), (2, 3), (3, 2), (1, 4), (4, 1), (2, 4)])
+@pytest.mark.parametrize("fmt", [1, 2])
+def test_tensor_2d_grid_emulated(grid, fmt):
+    """2-D (SUMMA-style) block sharding: shard (a, b) derives block (I_a, J_b)
+    of every T_A from the row panel I_a of the left and the column panel J_b of the right
+    operands; blocks go through the staging buffer.  Jacobi states per iteration."""
+    for w in (I.dense_stress_workload(300, 2, seed=7), I.dense_stress_workload(1000, 2, seed=8),
+              I.dense_stress_workload(129, 1, seed=9), I.ontology_workload("union", 600, depth=6, seed=4),
+              I.anbn_workload(5, 7)):
+        r, _, _ = gpu_closure(w, path_policy=2, tensor_format=fmt, emulate_ranks=grid[0] * grid[1], grid=grid)
+        o = assert_parity(w, r)
+        nc, _ = r.iteration_stats()
+        assert nc.tolist() == o.stats()["new_bits"].tolist(), (w.name, grid)
+
+
+def test_tensor_2d_grid_random_grammars():
+    for s in range(30):
+        w = I.random_workload(70_000 + s, max_nodes=300, max_edges=900, max_nt=4, max_bin=8, max_term=4)
+        grid = [(2, 2), (1, 3), (3, 1), (2, 3)][s % 4]
+        r, _, _ = gpu_closure(w, path_policy=2, emulate_ranks=grid[0] * grid[1], grid=grid)
+        o = assert_parity(w, r)
+        nc, _ = r.iteration_stats()
+        assert nc.tolist() == o.stats()["new_bits"].tolist(), (w.name, grid)
+
+
+def test_tensor_2d_grid_rejections():
+    from paper_1707_01007_b200 import cfpq as C
+    w = I.dense_stress_workload(50, 1)
+    for kw in (dict(path_policy=2, emulate_ranks=4, grid=(2, 3)), dict(path_policy=1, emulate_ranks=4, grid=(2, 2)),
+               dict(path_policy=3, emulate_ranks=4, grid=(2, 2))):
+        with pytest.raises(C.CfpqError):
+            gpu_closure(w, **kw)
+
+
+@pytest.mark.parametrize("variant", ["pairs_fp4", "pairs_int8", "grid_2x4_fp4"])
+def test_tensor_config_s_full_size_all_rows(variant):
+    """Config S at its bench size (S -> S S | a on G(16384, 32768)): EVERY row of R_S equals
+    the strict transitive closure of the a-edges (tests/closure_pin.py: SCC condensation,
+    pinned to the oracle on CPU), bit for bit, for the default CTA-pair kernel in both operand
+    formats and for the 2-D block-sharded run on an emulated 2 x 4 grid."""
+    import torch
+
+    from paper_1707_01007_b200 import cfpq as C
+    from tests.closure_pin import strict_closure_bits
+    w = I.dense_stress_workload(16384, 2, 0)
+    e = np.asarray(w.edges)
+    exp = strict_closure_bits(w.n_nodes, e[:, 0], e[:, 2])
+    kw = {"pairs_fp4": dict(tensor_format=2), "pairs_int8": dict(tensor_format=1),
+          "grid_2x4_fp4": dict(tensor_format=2, emulate_ranks=8, grid=(2, 4))}[variant]
+    g = C.Grammar.from_workload(w)
+    d = C.Graph(w.n_nodes, torch.from_numpy(w.edges).cuda(), stream=torch.cuda.current_stream())
+    r = C.closure(g, d, path_policy=2, stream=torch.cuda.current_stream(), **kw)
+    got = r.matrix(0)
+    assert got.shape == exp.shape
+    bad = np.nonzero((got != exp).any(axis=1))[0]
+    assert len(bad) == 0, (variant, len(bad), bad[:5])
+    assert r.count(0) == int(np.unpackbits(exp.view(np.uint8)).sum())

@@ -4,6 +4,7 @@ computes (the products of the main loop split across GPUs)."""
 import os
 import socket
 
+import numpy as np
 import pytest
 import torch.multiprocessing as mp
 
@@ -43,8 +44,21 @@ def _worker(rank, world, port, q):
         allb = [torch.zeros(2, dtype=torch.int64) for _ in range(world)]
         dist.all_gather(allb, lo_t)
         blocks[n] = [tuple(b.tolist()) for b in allb]
+    # 2-D grids (tensor engine, SUMMA-style blocks): every rank its block, all tile [0,n)^2
+    grids = {}
+    for n in (1, 300, 1025, 16384):
+        for gr, gc in ((1, 2), (2, 1)):
+            blk = torch.tensor(C.shard_block(n, gr, gc, rank), dtype=torch.int64)
+            allb = [torch.zeros(4, dtype=torch.int64) for _ in range(world)]
+            dist.all_gather(allb, blk)
+            grids[(n, gr, gc)] = [tuple(b.tolist()) for b in allb]
+    # bench.py's whole-job numbers: max time over ranks, work once (sharded) or summed (replicas)
+    import bench
+    t = 10.0 + rank
+    sh = bench.job_totals(dist, world, True, t, 100.0, 1000.0, "cpu")
+    rp = bench.job_totals(dist, world, False, t, 100.0 + rank, 1000.0, "cpu")
     dist.destroy_process_group()
-    q.put((rank, same, blocks))
+    q.put((rank, same, blocks, grids, sh, rp))
 
 
 def test_bootstrap_and_partition_gloo_world2():
@@ -59,8 +73,18 @@ def test_bootstrap_and_partition_gloo_world2():
     for p in ps:
         p.join(timeout=60)
         assert p.exitcode == 0
-    for rank, same, blocks in res:
+    for rank, same, blocks, grids, sh, rp in res:
         assert same
+        assert sh == (11.0, 100.0, 1000.0)
+        assert rp == (11.0, 201.0, 2000.0)
+        for (n, gr, gc), bl in grids.items():
+            cover = np.zeros((n, n), np.int32) if n <= 1025 else None
+            for r0, r1, c0, c1 in bl:
+                assert 0 <= r0 <= r1 <= n and 0 <= c0 <= c1 <= n
+                if cover is not None:
+                    cover[r0:r1, c0:c1] += 1
+            if cover is not None:
+                assert (cover == 1).all(), (n, gr, gc)
         for n, bl in blocks.items():
             # contiguous, ordered, disjoint, covering [0, n), boundaries on 128-row tiles
             cur = 0
