@@ -20,9 +20,13 @@
  *   - Handles are opaque, created and destroyed by the library; the caller owns them
  *     and must destroy them (destroy(NULL) is a no-op).  Handles are not thread-safe:
  *     use one handle from one thread at a time.
- *   - Input arrays are copied (host or device memory as flagged); the caller may free
- *     them as soon as the call returns.  Output buffers are caller-allocated; query
- *     sizes first (two-call pattern via cfpq_result_count).
+ *   - Input arrays are copied (host or device memory as flagged).  Grammar arrays may be
+ *     freed as soon as the call returns.  Edge arrays (cfpq_graph_create/set_edges) are
+ *     copied on cuda_stream: pageable host memory may be freed on return; device memory
+ *     and page-locked host memory are copied asynchronously and must stay valid and
+ *     unmodified until the stream has passed the copy (cfpq_closure synchronises the
+ *     stream before it returns).  Output buffers are caller-allocated; query sizes first
+ *     (two-call pattern via cfpq_result_count).
  *   - Node ids are dense 0..n_nodes-1 ("We enumerate the nodes ... from 0 to
  *     (|V|-1)"); NT ids dense 0..n_nt-1; label ids dense 0..n_labels-1.
  *   - Limits: n_nodes < 2^27, n_nt <= 1024.

@@ -308,9 +308,9 @@ static cfpq_status upload_edges(cfpq_graph* g, const int32_t* edges, int64_t n_e
     if (n_edges > 0)
         CFPQ_CUDA_TRY(cudaMemcpyAsync(g->d_edges, edges, (size_t)n_edges * 3 * sizeof(int32_t),
                                       on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
-    // the caller may free or reuse `edges` as soon as this returns (pinned host memory and
-    // device input are copied asynchronously): wait for the copy
-    if (n_edges > 0) CFPQ_CUDA_TRY(cudaStreamSynchronize(s));
+    // asynchronous on `s` for device and page-locked host input (cfpq.h: the caller keeps the
+    // buffer until the stream passes the copy; cfpq_closure synchronises it); pageable host
+    // memory is staged by the runtime before cudaMemcpyAsync returns
     g->n_edges = n_edges;
     return CFPQ_OK;
 }

@@ -779,7 +779,7 @@ __device__ __forceinline__ void fence_acq_rel() { asm volatile("fence.acq_rel.gp
 // Close iteration k from the log size `ls` and the error flags: Δ_k = log[hi, ls).
 // Every CTA runs this on identical inputs and reaches the identical state.
 __device__ __forceinline__ void close_iteration(const EngineParams& p, long long k, LoopState& s, unsigned long long ls,
-                                                int flags, bool record) {
+                                                int flags, bool record, unsigned long long* gs_ring = nullptr) {
     if (flags & 2) {
         s.status = ST_LEN_OVERFLOW;
         return;
@@ -793,7 +793,7 @@ __device__ __forceinline__ void close_iteration(const EngineParams& p, long long
         // stage last ran); the fixpoint test and the records are per round of S steps
         const int S = p.gs_stages, R = S + 1;
         const long long t = k + 1 - S;
-        unsigned long long* ring = p.st->gs_ring;
+        unsigned long long* ring = gs_ring ? gs_ring : p.st->gs_ring;   // warp-solo: a shared copy
         const unsigned long long lo = t >= 1 ? *(volatile unsigned long long*)&ring[t % R] : 0ull;
         if (record) ring[(k + 1) % R] = ls;   // read S steps later; never the slot read above
         s.lo = lo;
@@ -1017,6 +1017,20 @@ __device__ __forceinline__ bool solo_try(const EngineParams& p, const NTInfo* nt
     return !(atomicOr(nt[A].T + (size_t)i * (size_t)p.Wp + (j >> 5), bit) & bit);
 }
 
+// Prefetch into L1 the ELL head that the next iteration reads for candidate (A,i,j)
+// if it becomes new (its first two rule occurrences); overlaps with the bit atomic.
+__device__ __forceinline__ void prefetch_next(const NTInfo* nt, const Expansion* exps, uint32_t A, uint32_t i,
+                                              uint32_t j) {
+    int eb = nt[A].exp_begin, ee = nt[A].exp_end;
+    for (int x = eb; x < ee && x < eb + 2; ++x) {
+        Expansion ex = exps[x];
+        const int4* a = nullptr;
+        if (ex.kind == EXP_L_CONST) a = nt[ex.other].csr_ell + j;
+        else if (ex.kind == EXP_R_CONST) a = nt[ex.other].csc_ell + i;
+        if (a) asm volatile("prefetch.global.L1 [%0];" ::"l"(a));
+    }
+}
+
 // ------------------------------------------------------------------------------------------
 // Warp-solo iterations (|Δ| <= 32): warp 0 of CTA 0 alone, one Δ entry per lane, no CTA
 // barrier (__syncwarp only), appends positioned by a shared counter of this warp only.
@@ -1024,6 +1038,8 @@ __device__ __forceinline__ bool solo_try(const EngineParams& p, const NTInfo* nt
 // ------------------------------------------------------------------------------------------
 struct WarpSoloShared {
     uint64_t nxt[32];
+    uint64_t win[64];                        // Gauss-Seidel: log entries by position mod 64
+    unsigned long long ring[kMaxStages + 1]; // Gauss-Seidel: shared copy of EngineState::gs_ring
     int cnt;
     int ov, lov;
 };
@@ -1057,6 +1073,7 @@ __device__ __forceinline__ void ws_append(const EngineParams& p, const NTInfo* n
     if (idx < p.log_cap) {
         p.log[idx] = c;
         if (pos < 32) w.nxt[pos] = c;
+        if (p.gs_stages) w.win[idx & 63] = c;
         if (K != nullptr) atomicOr(word, bit);
         if (p.rowc != nullptr) {
             atomicAdd(p.rowc + (size_t)A * p.n + i, 1u);
@@ -1076,6 +1093,15 @@ __device__ void warp_solo(const EngineParams& p, const NTInfo* nt, const Expansi
     long long k = s.iter + 1;
     int m = (int)(s.hi - s.lo);
     uint64_t cell = lane < m ? ldcg64(p.log + s.lo + lane) : 0ull;
+    unsigned long long* ring = nullptr;
+    if (p.gs_stages) {
+        // Gauss-Seidel windows span S steps: keep the ring and the latest 64 log entries in
+        // shared memory (a window of <= 32 entries lies inside them)
+        for (int q = lane; q <= p.gs_stages; q += 32) w.ring[q] = ld_volatile_u64(&p.st->gs_ring[q]);
+        if (lane < m) w.win[(s.lo + lane) & 63] = cell;
+        ring = w.ring;
+        __syncwarp();
+    }
     for (;;) {
         if (lane == 0) {
             w.cnt = 0;
@@ -1099,6 +1125,11 @@ __device__ void warp_solo(const EngineParams& p, const NTInfo* nt, const Expansi
                     uint32_t a0, b0, a1, b1;
                     cand_coords(fx, h.z, a0, b0);
                     cand_coords(fx, h.w, a1, b1);
+                    // the ELL heads the next step reads if a candidate is new: fetched into
+                    // L1 while its membership atomic is in flight (the dependent chain of
+                    // one new cell per step, a^n b^n, loses one memory round trip)
+                    if (h.y > 0) prefetch_next(nt, exps, A, a0, b0);
+                    if (h.y > 1) prefetch_next(nt, exps, A, a1, b1);
                     bool n0, n1;
                     if (p.hset) {
                         hash_pair(p, h.y > 0, pack_cell(A, a0, b0), h.y > 1, pack_cell(A, a1, b1), n0, n1, &w.ov);
@@ -1138,7 +1169,7 @@ __device__ void warp_solo(const EngineParams& p, const NTInfo* nt, const Expansi
         __syncwarp();
         const int total = *(volatile int*)&w.cnt;
         const int f = (*(volatile int*)&w.ov ? 1 : 0) | (*(volatile int*)&w.lov ? 2 : 0);
-        close_iteration(p, k, s, base + (unsigned long long)total, f, lane == 0);
+        close_iteration(p, k, s, base + (unsigned long long)total, f, lane == 0, ring);
         ++iters;
         if (s.status != ST_RUNNING) break;
         if (p.has_snapshots) {
@@ -1155,23 +1186,14 @@ __device__ void warp_solo(const EngineParams& p, const NTInfo* nt, const Expansi
         if (mw > 32 || mw > p.solo_max) break;           // hand over to the CTA or grid paths
         m = (int)mw;
         __syncwarp();
-        // Gauss-Seidel windows span several steps: read them from the log
-        cell = lane < m ? (p.gs_stages ? ldcg64(p.log + s.lo + lane) : w.nxt[lane]) : 0ull;
+        // Gauss-Seidel windows span several steps: read them from the shared log mirror
+        cell = lane < m ? (p.gs_stages ? w.win[(s.lo + lane) & 63] : w.nxt[lane]) : 0ull;
         __syncwarp();
     }
-}
-
-// Prefetch into L1 the ELL head that the next iteration reads for candidate (A,i,j)
-// if it becomes new (its first two rule occurrences); overlaps with the bit atomic.
-__device__ __forceinline__ void prefetch_next(const NTInfo* nt, const Expansion* exps, uint32_t A, uint32_t i,
-                                              uint32_t j) {
-    int eb = nt[A].exp_begin, ee = nt[A].exp_end;
-    for (int x = eb; x < ee && x < eb + 2; ++x) {
-        Expansion ex = exps[x];
-        const int4* a = nullptr;
-        if (ex.kind == EXP_L_CONST) a = nt[ex.other].csr_ell + j;
-        else if (ex.kind == EXP_R_CONST) a = nt[ex.other].csc_ell + i;
-        if (a) asm volatile("prefetch.global.L1 [%0];" ::"l"(a));
+    if (p.gs_stages) {
+        __syncwarp();
+        for (int q = lane; q <= p.gs_stages; q += 32) p.st->gs_ring[q] = w.ring[q];
+        __syncwarp();
     }
 }
 
