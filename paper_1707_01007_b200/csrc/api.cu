@@ -555,6 +555,7 @@ static cfpq_status plan(cfpq_result* r, const cfpq_grammar* g, const cfpq_graph*
     if (use_nccl) {
         std::string err;
         r->comm = nccl_comm_create(o->nccl_unique_id, r->n_ranks, r->my_rank, &err);
+        (void)cudaGetLastError();   // NCCL's device probing may leave a non-sticky error behind
         if (!r->comm) {
             set_error(err);
             return CFPQ_E_NCCL;

@@ -182,6 +182,7 @@ void set_error(const std::string& msg);
     do {                                                                                  \
         cudaError_t _e = (expr);                                                          \
         if (_e != cudaSuccess) {                                                          \
+            (void)cudaGetLastError(); /* a non-sticky error must not leak into later calls */ \
             ::cfpq::set_error(std::string(#expr) + ": " + cudaGetErrorString(_e));        \
             return CFPQ_E_CUDA;                                                           \
         }                                                                                 \

@@ -1899,6 +1899,8 @@ cudaError_t rows_list_settle(DenseEngine* e, int64_t row_lo, int64_t row_hi, uns
                              unsigned long long* count) {
     cudaError_t c;
     unsigned long long m = 0;
+    *count = keep;
+    if (e->n_out == 0 || !e->rc) return cudaSuccess;   // no binary rule: nothing derived
     if ((c = cudaMemcpyAsync(&m, e->rc + 1, 8, cudaMemcpyDeviceToHost, s)) != cudaSuccess) return c;
     if ((c = cudaStreamSynchronize(s)) != cudaSuccess) return c;
     if (m > e->dlist_cap) {
@@ -1927,7 +1929,7 @@ cudaError_t rows_list_settle(DenseEngine* e, int64_t row_lo, int64_t row_hi, uns
 // The Δ_k word list (uint4 {A, i, word, bits}) for the exchange; `ensure` grows it (content
 // not kept) to hold `want` words.
 cudaError_t rows_list(DenseEngine* e, unsigned long long want, void** list, unsigned long long* cap) {
-    if (want > e->dlist_cap) {
+    if (want > e->dlist_cap || !e->dlist) {
         cudaFree(e->dlist);
         e->dlist = nullptr;
         const unsigned long long nc = want + want / 4 + 1024;
@@ -1943,6 +1945,7 @@ cudaError_t rows_list(DenseEngine* e, unsigned long long want, void** list, unsi
 // After the exchange: the list holds every rank's words [0, total); apply them to T_k.
 cudaError_t rows_apply_all(DenseEngine* e, unsigned long long total, cudaStream_t s, int* launches) {
     cudaError_t c;
+    if (e->n_out == 0 || !e->rc) return cudaSuccess;
     if ((c = cudaMemcpyAsync(e->rc + 1, &total, 8, cudaMemcpyHostToDevice, s)) != cudaSuccess) return c;
     if (total == 0) return cudaSuccess;
     DenseParams p = rows_params(e);

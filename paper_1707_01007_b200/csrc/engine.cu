@@ -1125,11 +1125,6 @@ __device__ void warp_solo(const EngineParams& p, const NTInfo* nt, const Expansi
                     uint32_t a0, b0, a1, b1;
                     cand_coords(fx, h.z, a0, b0);
                     cand_coords(fx, h.w, a1, b1);
-                    // the ELL heads the next step reads if a candidate is new: fetched into
-                    // L1 while its membership atomic is in flight (the dependent chain of
-                    // one new cell per step, a^n b^n, loses one memory round trip)
-                    if (h.y > 0) prefetch_next(nt, exps, A, a0, b0);
-                    if (h.y > 1) prefetch_next(nt, exps, A, a1, b1);
                     bool n0, n1;
                     if (p.hset) {
                         hash_pair(p, h.y > 0, pack_cell(A, a0, b0), h.y > 1, pack_cell(A, a1, b1), n0, n1, &w.ov);

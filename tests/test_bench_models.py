@@ -55,3 +55,56 @@ def test_tensor_roofline_accounting():
     assert abs(r8["achieved"] - ops / 1e-3 / 1e12) < 1e-6
     assert abs(r4["peak"] - 2 * r8["peak"]) < 1e-6
     assert abs(r4["frac_of_nominal"] * 9000.0 - r8["frac_of_nominal"] * 4500.0) < 1e-6
+
+
+def _rows_bytes_by_definition(w, snaps):
+    """DESIGN §5's bit-row byte model written out with plain loops over the oracle's T_k
+    (an independent count of what bench.rows_alg_bytes computes with scipy)."""
+    n = w.n_nodes
+    W = (n + 31) // 32
+    rules = sorted(set(map(tuple, np.asarray(w.bin).reshape(-1, 3).tolist())))
+    lhs = {a for a, _, _ in rules}
+    K = len(snaps) - 1
+    total = 8 * sum(len(snaps[0][A]) for A in range(w.n_nt))
+    for k in range(1, K + 1):
+        T = snaps[k - 1]
+        for A, B, C in rules:
+            tb, tc = T[B], T[C]
+            pb, pc = B not in lhs, C not in lhs
+            rows_b = {i for i, _ in tb}
+            if not tb or not tc:
+                if not pb and tb:
+                    total += 4 * W * len(rows_b)
+                continue
+            row_c = {}
+            for r, j in tc:
+                row_c.setdefault(r, set()).add(j)
+            if not pb and pc:
+                total += 4 * W * len(rows_b) + 8 * len(tb) + 4 * sum(len(row_c.get(r, ())) for _, r in tb)
+            elif pb and not pc:
+                refs = {r for _, r in tb}
+                total += 8 * len(rows_b) + 4 * len(tb) + 4 * W * sum(1 for r in refs if r in row_c)
+            elif not pb and not pc:
+                refs = {r for _, r in tb}
+                total += 4 * W * len(rows_b) + 4 * W * sum(1 for r in refs if r in row_c)
+            else:
+                if k > 1:
+                    continue
+                total += 8 * len(rows_b) + 12 * len(tb) + 4 * sum(len(row_c.get(r, ())) for _, r in tb)
+            words = {(i, j // 32) for i, r in tb for j in row_c.get(r, ())}
+            total += 8 * len(words)
+        for A in lhs:
+            new = snaps[k][A] - snaps[k - 1][A]
+            total += 32 * len({(i, j // 32) for i, j in new})
+    return total
+
+
+def test_rows_alg_bytes_equals_the_definition_counted_by_hand():
+    """bench.rows_alg_bytes (scipy) == the same model counted cell by cell, on the paper's
+    example (n = 3: W = 1 word per row) and on small union-grammar / random instances."""
+    for w in (I.example_workload(), I.config4_workload(n=300, seed=2), I.random_workload(31),
+              I.ontology_workload("q2", 200, depth=5, seed=1)):
+        s = _Snapshots(w)
+        snaps = [{A: set(map(tuple, s.pairs_at(A, k).tolist())) for A in range(w.n_nt)}
+                 for k in range(s.iterations + 1)]
+        assert bench.rows_alg_bytes(w, s) == _rows_bytes_by_definition(w, snaps), w.name
