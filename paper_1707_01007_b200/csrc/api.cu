@@ -201,8 +201,8 @@ struct cfpq_result {
     // relational sparse runs on one GPU keep their results in the log only, so the closure
     // kernel can reset the bit words at the fixpoint (flags bit 2 disables, diagnostics)
     bool self_clear_ok() const {
-        return opts.semantics == 0 && !hashed && opts.schedule != 2 && n_ranks == 1 && !comm &&
-               opts.path_policy < 2 && (opts.diag_flags & 4) == 0;
+        return opts.semantics == 0 && !hashed && n_ranks == 1 && !comm && opts.path_policy < 2 &&
+               (opts.diag_flags & 4) == 0;
     }
 
     EngineParams params() const {
@@ -410,7 +410,7 @@ static bool make_spare(cfpq_result* r) {
     if (good && n_key)
         good = ok(cudaMalloc(&b.d_K, (size_t)r->n * r->n * n_key * 8)) &&
                ok(cudaMemsetAsync(b.d_K, 0xff, (size_t)r->n * r->n * n_key * 8, s));
-    if (good) good = ok(cudaMalloc(&b.d_log, r->log_cap * 8));
+    if (good) good = ok(cudaMalloc(&b.d_log, r->log_cap * 8)) && ok(cudaMemsetAsync(b.d_log, 0, r->log_cap * 8, s));
     if (good && r->d_rowc)
         good = ok(cudaMalloc(&b.d_rowc, (size_t)r->n_nt * r->n * 4)) && ok(cudaMalloc(&b.d_colc, (size_t)r->n_nt * r->n * 4)) &&
                ok(cudaMemsetAsync(b.d_rowc, 0, (size_t)r->n_nt * r->n * 4, s)) &&
@@ -729,6 +729,7 @@ static cfpq_status size_for_graph(cfpq_result* r, const cfpq_graph* d) {
         uint64_t* nl = nullptr;
         cfpq_status st = dalloc(&nl, want, "cell log");
         if (st != CFPQ_OK) return st;
+        CFPQ_CUDA_TRY(cudaMemsetAsync(nl, 0, want * 8, r->stream));   // no stale async flags
         if (r->d_log && r->n_cells)
             CFPQ_CUDA_TRY(cudaMemcpyAsync(nl, r->d_log, r->n_cells * 8, cudaMemcpyDeviceToDevice, r->stream));
         dfree(r->d_log);
@@ -756,6 +757,7 @@ static cfpq_status grow_log(cfpq_result* r, unsigned long long reached, unsigned
     cfpq_status st = dalloc(&nl, want, "cell log (grow)");
     if (st != CFPQ_OK) return st;
     CFPQ_CUDA_TRY(cudaMemcpyAsync(nl, r->d_log, r->log_cap * 8, cudaMemcpyDeviceToDevice, r->stream));
+    CFPQ_CUDA_TRY(cudaMemsetAsync(nl + r->log_cap, 0, (want - r->log_cap) * 8, r->stream));
     CFPQ_CUDA_TRY(cudaStreamSynchronize(r->stream));
     const unsigned long long old_cap = r->log_cap;
     dfree(r->d_log);
@@ -1139,7 +1141,11 @@ static cfpq_status run_async(cfpq_result* r, unsigned long long seeds_upper) {
         CFPQ_CUDA_TRY(cudaMemcpyAsync(r->d_st, &fix, sizeof(EngineState), cudaMemcpyHostToDevice, s));
     }
     r->n_cells = std::min<unsigned long long>(r->h_st.log_size, r->log_cap);
-    CFPQ_CUDA_TRY(launch_strip_flags(r->d_log, 0, r->n_cells, s));
+    if (r->self_clear_ok()) {
+        r->t_clean = true;   // the kernel stripped the flags and reset the bit words at quiescence
+    } else {
+        CFPQ_CUDA_TRY(launch_strip_flags(r->d_log, 0, r->n_cells, s));
+    }
     {
         float ms = 0;
         CFPQ_CUDA_TRY(cudaEventElapsedTime(&ms, r->ev[0], r->ev[1]));
@@ -1385,6 +1391,7 @@ static cfpq_status run(cfpq_result* r, const cfpq_graph* d) {
             if (r->log_cap < r->spare.log_cap) {
                 uint64_t* nl = nullptr;
                 if ((st = dalloc(&nl, r->spare.log_cap, "cell log")) != CFPQ_OK) return st;
+                CFPQ_CUDA_TRY(cudaMemsetAsync(nl, 0, r->spare.log_cap * 8, s));
                 dfree(r->d_log);
                 r->d_log = nl;
                 r->log_cap = r->spare.log_cap;
@@ -1410,6 +1417,7 @@ static cfpq_status run(cfpq_result* r, const cfpq_graph* d) {
             if (r->log_cap < r->spare.log_cap) {          // the other bank's log grew last run
                 uint64_t* nl = nullptr;
                 if ((st = dalloc(&nl, r->spare.log_cap, "cell log")) != CFPQ_OK) return st;
+                CFPQ_CUDA_TRY(cudaMemsetAsync(nl, 0, r->spare.log_cap * 8, s));
                 dfree(r->d_log);
                 r->d_log = nl;
                 r->log_cap = r->spare.log_cap;
@@ -1429,7 +1437,8 @@ static cfpq_status run(cfpq_result* r, const cfpq_graph* d) {
     if (r->opts.account_work) CFPQ_CUDA_TRY(cudaMemsetAsync(r->d_jac, 0, r->iter_off_cap * 8, s));
     CFPQ_CUDA_TRY(cudaMemsetAsync(r->d_st, 0, sizeof(EngineState), s));
     const bool async = r->opts.schedule == 2;
-    if (async) CFPQ_CUDA_TRY(cudaMemsetAsync(r->d_log, 0, r->log_cap * 8, s));   // valid flags start clear
+    // async valid flags (bit 63): every log buffer is zeroed when allocated, no other schedule
+    // sets bit 63 (A < 512), and every async run strips its flags, so no per-run clear
     if (r->opts.record_times) CFPQ_CUDA_TRY(cudaMemsetAsync(r->d_phase, 0, r->iter_off_cap * 32, s));
     if (!r->ev[0])
         for (auto& e : r->ev) CFPQ_CUDA_TRY(cudaEventCreate(&e));
@@ -1505,7 +1514,7 @@ static cfpq_status run(cfpq_result* r, const cfpq_graph* d) {
             fix.status = ST_RUNNING;
             fix.overflow = 0;
             fix.bar_count = 0;
-            fix.bar_gen = 0;
+            fix.bar_word = 0;
             if (r->opts.account_work && fix.iter + 1 < r->iter_off_cap)
                 CFPQ_CUDA_TRY(cudaMemsetAsync(r->d_jac + fix.iter + 1, 0, 8, s));
             CFPQ_CUDA_TRY(cudaMemcpyAsync(r->d_st, &fix, sizeof(EngineState), cudaMemcpyHostToDevice, s));

@@ -89,9 +89,12 @@ struct EngineState {
     unsigned long long async_head; // asynchronous schedule: next log slot to claim
     unsigned long long async_done; // asynchronous schedule: log entries fully expanded
     unsigned bar_count;            // grid-barrier words, on their own 128-byte line
-    unsigned bar_gen;
-    unsigned long long snap_ls[2]; // log size when iteration k closed (slot k&1)
-    int snap_flags[2];             // bit 0 overflow, bit 1 length overflow (slot k&1)
+    unsigned bar_pad;
+    // released by the last CTA to arrive: generation (bits 63-40) | error flags of the
+    // iteration it closes (bits 39-38: overflow, length overflow) | log size (bits 37-0), so
+    // a waiting CTA gets the iteration's outcome with the same load that releases it
+    unsigned long long bar_word;
+    unsigned long long pad_snap[2];
     unsigned pad1[20];
     unsigned long long clr_cursor; // in-kernel clear of the other bank: next cell to claim
     // Gauss-Seidel schedule: gs_ring[t mod (S+1)] = L_t, the log size when step t starts

@@ -775,6 +775,25 @@ __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
     return v;
 }
 __device__ __forceinline__ void fence_acq_rel() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+__device__ __forceinline__ unsigned long long ld_acquire_word(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_word(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+constexpr int kBarGenShift = 40;
+constexpr unsigned long long kBarLsMask = (1ull << 38) - 1;
+// The released barrier word of the last arriver: next generation | flags | log size.
+__device__ __forceinline__ unsigned long long bar_release_word(EngineState* st, unsigned long long gen, long long k) {
+    unsigned long long f = 0, ls = 0;
+    if (k >= 0) {
+        f = (*(volatile int*)&st->overflow ? 1ull : 0ull) | (*(volatile int*)&st->len_overflow ? 2ull : 0ull);
+        ls = ld_volatile_u64(&st->log_size) & kBarLsMask;
+    }
+    return (((gen + 1) & 0xFFFFFFull) << kBarGenShift) | (f << 38) | ls;
+}
 
 // Close iteration k from the log size `ls` and the error flags: Δ_k = log[hi, ls).
 // Every CTA runs this on identical inputs and reaches the identical state.
@@ -836,9 +855,6 @@ __device__ void publish(const EngineParams& p, const LoopState& s) {
     fence_acq_rel();
 }
 
-// Grid barrier (generation counter, release/acquire).  If k >= 0 the last CTA to
-// arrive snapshots the log size and error flags of iteration k into slot k&1 before
-// releasing, so every CTA can close the iteration locally afterwards.
 // ---- clearing the other bank's cells with otherwise idle barrier time ----
 constexpr unsigned long long kClrChunk = 2048;
 
@@ -873,29 +889,30 @@ __device__ void clear_drain(const EngineParams& p) {
     }
 }
 
-__device__ bool grid_barrier(const EngineParams& p, long long k) {
+// Grid barrier (generation counter, release/acquire).  If k >= 0 the last CTA to arrive
+// publishes the log size and error flags of iteration k in the released word; every CTA
+// closes the iteration from it (`word`, valid in thread 0 after the barrier).
+__device__ bool grid_barrier(const EngineParams& p, long long k, unsigned long long* word = nullptr) {
     __shared__ int s_timeout;
+    __shared__ unsigned long long s_word;
     if (p.clr_n) {
         // CTAs that are not the last to arrive clear chunks of the other bank while they
         // wait; the release is checked between chunks
         __shared__ int s_go;
-        __shared__ unsigned s_my;
+        __shared__ unsigned long long s_my;
         __shared__ unsigned long long s_base;
         __syncthreads();
         if (threadIdx.x == 0) {
             s_timeout = 0;
             s_go = 0;
             EngineState* st = p.st;
-            s_my = *(volatile unsigned*)&st->bar_gen;
+            s_my = ld_volatile_u64(&st->bar_word) >> kBarGenShift;
             unsigned arrived = atom_add_acq_rel(&st->bar_count, 1u);
             if (arrived == (unsigned)p.nblocks - 1u) {
-                if (k >= 0) {
-                    int f = (*(volatile int*)&st->overflow ? 1 : 0) | (*(volatile int*)&st->len_overflow ? 2 : 0);
-                    st->snap_ls[k & 1] = ld_volatile_u64(&st->log_size);
-                    st->snap_flags[k & 1] = f;
-                }
+                const unsigned long long w = bar_release_word(st, s_my, k);
                 st->bar_count = 0u;
-                red_add_release(&st->bar_gen, 1u);
+                st_release_word(&st->bar_word, w);
+                s_word = w;
                 s_go = 1;
             }
         }
@@ -908,13 +925,15 @@ __device__ bool grid_barrier(const EngineParams& p, long long k) {
             const bool work = s_base < p.clr_n;
             if (work) clear_chunk(p, s_base);
             if (threadIdx.x == 0) {
-                if (ld_acquire_u32(&p.st->bar_gen) != s_my) {
+                unsigned long long w = ld_acquire_word(&p.st->bar_word);
+                if ((w >> kBarGenShift) != s_my) {
+                    s_word = w;
                     s_go = 1;
                 } else if (!work) {
                     // nothing left to clear: plain wait
                     long long t0 = clock64();
                     unsigned ns = 0;
-                    while (ld_acquire_u32(&p.st->bar_gen) == s_my) {
+                    while (((w = ld_acquire_word(&p.st->bar_word)) >> kBarGenShift) == s_my) {
                         if (ns) __nanosleep(ns);
                         if (clock64() - t0 > 40000) ns = ns ? (ns < 2048u ? ns * 2u : 2048u) : 64u;
                         if (clock64() - t0 > 60000000000ll) {
@@ -922,31 +941,30 @@ __device__ bool grid_barrier(const EngineParams& p, long long k) {
                             break;
                         }
                     }
+                    s_word = w;
                     s_go = 1;
                 }
             }
             __syncthreads();
         }
+        if (word && threadIdx.x == 0) *word = s_word;
         return s_timeout == 0;
     }
     __syncthreads();
     if (threadIdx.x == 0) {
         s_timeout = 0;
         EngineState* st = p.st;
-        unsigned my = *(volatile unsigned*)&st->bar_gen;
+        const unsigned long long my = ld_volatile_u64(&st->bar_word) >> kBarGenShift;
         unsigned arrived = atom_add_acq_rel(&st->bar_count, 1u);
+        unsigned long long w;
         if (arrived == (unsigned)p.nblocks - 1u) {
-            if (k >= 0) {
-                int f = (*(volatile int*)&st->overflow ? 1 : 0) | (*(volatile int*)&st->len_overflow ? 2 : 0);
-                st->snap_ls[k & 1] = ld_volatile_u64(&st->log_size);
-                st->snap_flags[k & 1] = f;
-            }
+            w = bar_release_word(st, my, k);
             st->bar_count = 0u;
-            red_add_release(&st->bar_gen, 1u);
+            st_release_word(&st->bar_word, w);
         } else {
             long long t0 = clock64();
             unsigned ns = 0;
-            while (ld_acquire_u32(&st->bar_gen) == my) {
+            while (((w = ld_acquire_word(&st->bar_word)) >> kBarGenShift) == my) {
                 // poll at L2 latency for ~20 µs (grid iterations), then back off (a
                 // single-CTA phase can park the other CTAs for a long time)
                 if (ns) __nanosleep(ns);
@@ -957,6 +975,7 @@ __device__ bool grid_barrier(const EngineParams& p, long long k) {
                 }
             }
         }
+        if (word) *word = w;
     }
     __syncthreads();
     return s_timeout == 0;
@@ -1463,15 +1482,15 @@ __global__ void __launch_bounds__(kBlock, 1) closure_kernel(EngineParams p) {
         }
         cta_flush(p, nt, gsink, S.ws, wib, lane, &S.flush_base, S.flush_prefix);
         if (ph) c2 = clock64();
-        if (!grid_barrier(p, k)) {
+        unsigned long long bw = 0;
+        if (!grid_barrier(p, k, &bw)) {
             aborted = true;
             break;
         }
         if (ph) c3 = clock64();
         if (threadIdx.x == 0) {
             LoopState t = s;
-            close_iteration(p, k, t, ld_volatile_u64(&st->snap_ls[k & 1]), *(volatile int*)&st->snap_flags[k & 1],
-                            blockIdx.x == 0);
+            close_iteration(p, k, t, bw & kBarLsMask, (int)((bw >> 38) & 3ull), blockIdx.x == 0);
             S.state = t;
         }
         __syncthreads();
@@ -1624,6 +1643,26 @@ __global__ void __launch_bounds__(kBlock, 1) async_kernel(EngineParams p) {
     if (lane == 0) {
         if (dcand) atomicAdd(&st->candidates, dcand);
         if (dexp) atomicAdd(&st->expansions, dexp);
+    }
+    if (p.self_clear) {
+        // quiescence is global and stable (done == appended): every CTA passes one grid
+        // barrier, then one pass over the log strips the valid flags and resets the bit
+        // words of every cell while they are hot in L2 (the relations stay in the log; the
+        // next run starts on clean matrices).  After an overflow the host re-runs instead.
+        __syncthreads();
+        if (!grid_barrier(p, -1)) return;
+        if (*(volatile int*)&st->overflow || *(volatile int*)&st->bad_edge) return;
+        const unsigned long long n_cells = ld_volatile_u64(&st->log_size);
+        for (unsigned long long e = (unsigned long long)blockIdx.x * kBlock + threadIdx.x; e < n_cells;
+             e += (unsigned long long)gridDim.x * kBlock) {
+            const uint64_t c = ldcg64(p.log + e) & ~kValid;
+            p.log[e] = c;
+            const uint32_t A = cell_nt(c), i = cell_i(c), j = cell_j(c);
+            const NTInfo& t = nt[A];
+            t.T[(size_t)i * p.Wp + (j >> 5)] = 0u;
+            if (t.S) t.S[(size_t)i * p.Wp + (j >> 5)] = 0u;
+            if (t.ST) t.ST[(size_t)j * p.Wp + (i >> 5)] = 0u;
+        }
     }
 }
 
