@@ -184,20 +184,61 @@ def ncu_traffic(workload: str):
         return None
 
 
+_INT8_PROBE = {}
+
+
+def probe_int8_tops():
+    """Dense int8 tensor throughput measured on this GPU: torch._int_mm (cuBLASLt) on
+    8192^3 int8 -> int32, best of 10 (the same method as MEASURED_PEAKS' bf16 probe).
+    Cached per process; None if the probe is unavailable."""
+    if "tops" in _INT8_PROBE:
+        return _INT8_PROBE["tops"]
+    tops = None
+    try:
+        import torch
+        n = 8192
+        a = torch.randint(-4, 4, (n, n), dtype=torch.int8, device="cuda")
+        b = torch.randint(-4, 4, (n, n), dtype=torch.int8, device="cuda")
+        for _ in range(3):
+            torch._int_mm(a, b)
+        best = None
+        for _ in range(10):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            torch._int_mm(a, b)
+            e1.record()
+            e1.synchronize()
+            ms = e0.elapsed_time(e1)
+            best = ms if best is None else min(best, ms)
+        tops = 2.0 * n ** 3 / (best * 1e-3) / 1e12
+        del a, b
+    except Exception:
+        tops = None
+    _INT8_PROBE["tops"] = tops
+    return tops
+
+
 def int8_peak():
-    """Dense int8 tensor peak = measured bf16 (MEASURED_PEAKS.json) x the nominal int8/bf16 ratio (2)."""
+    """Dense int8 tensor peak: the torch._int_mm probe on this GPU when available, else the
+    measured bf16 (MEASURED_PEAKS.json) x the nominal int8/bf16 ratio (2)."""
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             d = json.load(f)
-        return 2.0 * float(d["bf16_tflops"]), 2.0 * float(d["bf16_tflops_sustained"]), "measured bf16 x 2 (nominal int8/bf16)"
+        derived = 2.0 * float(d["bf16_tflops"]), 2.0 * float(d["bf16_tflops_sustained"]), \
+            "measured bf16 x 2 (nominal int8/bf16)"
     except Exception:
-        return 2.0 * 1590.0, 2.0 * 1400.0, "fallback bf16 x 2 (B200_PROFILING.md)"
+        derived = 2.0 * 1590.0, 2.0 * 1400.0, "fallback bf16 x 2 (B200_PROFILING.md)"
+    probed = probe_int8_tops()
+    if probed:
+        return probed, probed * derived[1] / derived[0], "measured: torch._int_mm 8192^3 int8, best of 10 (this run)"
+    return derived
 
 
 def fp4_peak():
-    """Dense FP4 (kind::mxf4) tensor peak = measured bf16 x the nominal fp4/bf16 ratio (9 / 2.25 = 4)."""
+    """Dense FP4 (kind::mxf4) tensor peak = the int8 peak x the nominal fp4/int8 ratio
+    (9 / 4.5 = 2; no fp4 library GEMM to probe)."""
     b, s, src = int8_peak()
-    return 2.0 * b, 2.0 * s, src.replace("x 2 (nominal int8/bf16)", "x 4 (nominal fp4/bf16)")
+    return 2.0 * b, 2.0 * s, src + " x 2 (nominal fp4/int8)"
 
 
 TENSOR_FORMATS = {1: "int8", 2: "fp4"}
@@ -216,6 +257,7 @@ def tensor_roofline(stats, step_ms, fmt=2):
     kind = "kind::mxf4, e2m1 0/1, unit ue8m0 scales, f32 accumulator" if fmt == 2 else "kind::i8"
     nominal = 9000.0 if fmt == 2 else 4500.0   # dense fp4 / int8 datasheet figures (context only)
     return {"bound": "tensor", "achieved": achieved, "peak": burst, "unit": "TFLOP/s", "frac": achieved / burst,
+            "int8_probe_tops": probe_int8_tops(),
             "frac_of_sustained": achieved / sustained, "frac_of_nominal": achieved / nominal, "traffic": ncu_traffic("configS" if fmt == 2 else "configS_int8"),
             "kernel": f"cfpq::dense2sm_kernel (tcgen05.mma.cta_group::2 {kind}, CTA pairs)", "format": TENSOR_FORMATS[fmt],
             "loop_ms": loop_s * 1e3, "share_of_step": loop_s * 1e3 / step_ms, "issued_ops": ops, "peak_source": src,

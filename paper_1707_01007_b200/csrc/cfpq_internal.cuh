@@ -100,6 +100,9 @@ struct EngineState {
     // Gauss-Seidel schedule: gs_ring[t mod (S+1)] = L_t, the log size when step t starts
     // (L_1 = |Δ_0|); step t expands log[L_{t-S}, L_t) through the rules of stage (t-1) mod S
     unsigned long long gs_ring[kMaxStages + 1];
+    int gs_stage;                  // stage of the next step ((k) mod S after step k closed)
+    int gs_slot;                   // ring slot of L_{k+1} ((k+1) mod (S+1))
+    long long gs_round;            // rounds completed (k / S)
 };
 
 enum : int { ST_RUNNING = 0, ST_DONE = 1, ST_OVERFLOW = 2, ST_CAP = 3, ST_LEN_OVERFLOW = 4, ST_SWITCH = 5 };

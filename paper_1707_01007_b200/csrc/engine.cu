@@ -356,6 +356,9 @@ __global__ void adj_count_kernel(EngineParams p, const int32_t* __restrict__ slo
         if (p.iter_off_cap > 1) p.iter_off[1] = n_seed;
         if (p.iter_time) p.iter_time[0] = globaltimer();
         p.st->gs_ring[1] = n_seed;   // L_1 (Gauss-Seidel windows)
+        p.st->gs_slot = 1;
+        p.st->gs_stage = 0;
+        p.st->gs_round = 0;
     }
     for (unsigned long long e = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; e < n_seed;
          e += (unsigned long long)gridDim.x * blockDim.x) {
@@ -403,6 +406,15 @@ __global__ void adj_fill_kernel(EngineParams p, const int32_t* __restrict__ slot
     }
 }
 
+// Reset the bit word of a cell by zeroing its whole aligned 32-byte sector: every bit of the
+// matrices is being reset (all of them belong to logged cells), and a full-sector store needs
+// no DRAM read-modify-write of a partial sector.
+__device__ __forceinline__ void zero_sector(uint32_t* w) {
+    uint4* sct = reinterpret_cast<uint4*>(reinterpret_cast<uintptr_t>(w) & ~uintptr_t(31));
+    sct[0] = make_uint4(0u, 0u, 0u, 0u);
+    sct[1] = make_uint4(0u, 0u, 0u, 0u);
+}
+
 // Clear the cells of a previous run (bitmaps, snapshots, keys, counters) in O(|log|).
 __global__ void clear_log_kernel(EngineParams p, unsigned long long n_cells) {
     for (unsigned long long e = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; e < n_cells;
@@ -410,9 +422,9 @@ __global__ void clear_log_kernel(EngineParams p, unsigned long long n_cells) {
         uint64_t c = p.log[e];
         uint32_t A = cell_nt(c), i = cell_i(c), j = cell_j(c);
         const NTInfo& nt = p.nt[A];
-        if (nt.T) nt.T[(size_t)i * p.Wp + (j >> 5)] = 0u;
-        if (nt.S) nt.S[(size_t)i * p.Wp + (j >> 5)] = 0u;
-        if (nt.ST) nt.ST[(size_t)j * p.Wp + (i >> 5)] = 0u;
+        if (nt.T) zero_sector(nt.T + (size_t)i * p.Wp + (j >> 5));
+        if (nt.S) zero_sector(nt.S + (size_t)i * p.Wp + (j >> 5));
+        if (nt.ST) zero_sector(nt.ST + (size_t)j * p.Wp + (i >> 5));
         if (nt.K) nt.K[(size_t)i * p.n + j] = kEmptyKey;
         if (p.rowc) {
             p.rowc[(size_t)A * p.n + i] = 0u;
@@ -436,8 +448,8 @@ __device__ __forceinline__ void cand_coords(uint32_t fx, int32_t nb, uint32_t& i
 }
 
 // Gauss-Seidel schedule: step k applies only the rules of stage (k-1) mod S.
-__device__ __forceinline__ bool stage_ok(const EngineParams& p, const Expansion& ex, long long k) {
-    return p.gs_stages == 0 || ex.stage == (int)((k - 1) % p.gs_stages);
+__device__ __forceinline__ bool stage_ok(const EngineParams& p, const Expansion& ex, int stage) {
+    return p.gs_stages == 0 || ex.stage == stage;
 }
 
 // Neighbours beyond the ELL head (deg > 2): warp-wide exclusive scan of the tail
@@ -495,7 +507,7 @@ __device__ __forceinline__ int4 load_head(const NTInfo* nt, const Expansion& ex,
 
 // Expand one 32-entry chunk (one entry per lane, `valid` lanes only) of iteration k.
 __device__ __forceinline__ void expand_chunk(const EngineParams& p, const NTInfo* nt, const Expansion* exps,
-                                             const Sink& sk, uint64_t cell, bool valid, long long k, int lane,
+                                             const Sink& sk, uint64_t cell, bool valid, long long k, int gstage, int lane,
                                              WarpScratch* ws, unsigned long long& dcand, unsigned long long& dexp) {
     uint32_t X = cell_nt(cell), ci = cell_i(cell), cj = cell_j(cell);
     int eb = 0, nexp = 0;
@@ -522,7 +534,7 @@ __device__ __forceinline__ void expand_chunk(const EngineParams& p, const NTInfo
         efx[x] = 0;
         if (x < nexp) {
             Expansion ex = exps[eb + x];
-            if (!stage_ok(p, ex, k)) continue;
+            if (!stage_ok(p, ex, gstage)) continue;
             if (ex.kind == EXP_L_CONST || ex.kind == EXP_R_CONST) el[x] = load_head(nt, ex, ci, cj, eA[x], efx[x]);
             else var_mask |= 1u << x;
         }
@@ -583,7 +595,7 @@ __device__ __forceinline__ void expand_chunk(const EngineParams& p, const NTInfo
         uint32_t A = 0, fx = 0;
         if (x < nexp) {
             Expansion ex = exps[eb + x];
-            if (!stage_ok(p, ex, k)) {
+            if (!stage_ok(p, ex, gstage)) {
             } else if (ex.kind == EXP_L_CONST || ex.kind == EXP_R_CONST) {
                 h = load_head(nt, ex, ci, cj, A, fx);
             } else if (x < 32) {
@@ -660,7 +672,7 @@ __device__ __forceinline__ void expand_chunk(const EngineParams& p, const NTInfo
 // consecutive entries per warp; warps [warp, warp+nwarps) stride over chunks.
 // `src` = shared-memory copy of log[lo,hi) (single-CTA path) or null (read the log).
 __device__ void expand(const EngineParams& p, const NTInfo* nt, const Expansion* exps, const Sink& sk,
-                       const uint64_t* src, unsigned long long lo, unsigned long long hi, long long k, int warp,
+                       const uint64_t* src, unsigned long long lo, unsigned long long hi, long long k, int gstage, int warp,
                        int nwarps, int lane, WarpScratch* ws, unsigned long long& dcand, unsigned long long& dexp,
                        bool final_flush = true) {
     for (unsigned long long cbase = lo + (unsigned long long)warp * 32ull; cbase < hi;
@@ -669,7 +681,7 @@ __device__ void expand(const EngineParams& p, const NTInfo* nt, const Expansion*
         bool valid = e < hi;
         uint64_t cell = 0ull;
         if (valid) cell = src ? src[e - lo] : ldcg64(p.log + e);
-        expand_chunk(p, nt, exps, sk, cell, valid, k, lane, ws, dcand, dexp);
+        expand_chunk(p, nt, exps, sk, cell, valid, k, gstage, lane, ws, dcand, dexp);
     }
     if (final_flush) flush(p, nt, sk, ws, lane);
 }
@@ -758,6 +770,8 @@ struct LoopState {
     unsigned long long lo, hi;
     long long iter;
     int status;
+    int gs_stage, gs_slot;   // Gauss-Seidel: stage of the next step, ring slot of its L (EngineState)
+    long long gs_round;
 };
 
 // ---- memory-model primitives for the grid barrier (release/acquire at gpu scope) ----
@@ -809,17 +823,21 @@ __device__ __forceinline__ void close_iteration(const EngineParams& p, long long
     }
     if (p.gs_stages > 0) {
         // Gauss-Seidel: step k+1 expands log[L_{k+1-S}, L_{k+1}) (everything derived since its
-        // stage last ran); the fixpoint test and the records are per round of S steps
+        // stage last ran); slots and stages advance incrementally (R = S+1, so the slot of
+        // L_{k+1-S} is the one after L_{k+1}'s); fixpoint test and records per round of S steps
         const int S = p.gs_stages, R = S + 1;
-        const long long t = k + 1 - S;
         unsigned long long* ring = gs_ring ? gs_ring : p.st->gs_ring;   // warp-solo: a shared copy
-        const unsigned long long lo = t >= 1 ? *(volatile unsigned long long*)&ring[t % R] : 0ull;
-        if (record) ring[(k + 1) % R] = ls;   // read S steps later; never the slot read above
+        const int slot = s.gs_slot + 1 == R ? 0 : s.gs_slot + 1;        // (k+1) mod R
+        const int lo_slot = slot + 1 == R ? 0 : slot + 1;               // (k+1-S) mod R
+        const unsigned long long lo = k + 1 - S >= 1 ? *(volatile unsigned long long*)&ring[lo_slot] : 0ull;
+        if (record) ring[slot] = ls;   // read S steps later; never the slot read above
         s.lo = lo;
         s.hi = ls;
         s.iter = k;
-        if (k % S != 0) return;
-        const long long rd = k / S;
+        s.gs_slot = slot;
+        s.gs_stage = s.gs_stage + 1 == S ? 0 : s.gs_stage + 1;
+        if (s.gs_stage != 0) return;   // a round ends when the next step is stage 0 again
+        const long long rd = ++s.gs_round;
         if (record) {
             if (rd < p.iter_off_cap) {
                 p.iter_off[rd] = lo;
@@ -852,6 +870,9 @@ __device__ void publish(const EngineParams& p, const LoopState& s) {
     st->hi = s.hi;
     st->iter = s.iter;
     st->status = s.status;
+    st->gs_stage = s.gs_stage;
+    st->gs_slot = s.gs_slot;
+    st->gs_round = s.gs_round;
     fence_acq_rel();
 }
 
@@ -865,9 +886,9 @@ __device__ __forceinline__ void clear_chunk(const EngineParams& p, unsigned long
         const uint64_t c = ldcg64(p.clr_log + e);
         const uint32_t A = cell_nt(c), i = cell_i(c), j = cell_j(c);
         const NTInfo& t = p.clr_nt[A];
-        if (t.T) t.T[(size_t)i * p.Wp + (j >> 5)] = 0u;
-        if (t.S) t.S[(size_t)i * p.Wp + (j >> 5)] = 0u;
-        if (t.ST) t.ST[(size_t)j * p.Wp + (i >> 5)] = 0u;
+        if (t.T) zero_sector(t.T + (size_t)i * p.Wp + (j >> 5));
+        if (t.S) zero_sector(t.S + (size_t)i * p.Wp + (j >> 5));
+        if (t.ST) zero_sector(t.ST + (size_t)j * p.Wp + (i >> 5));
         if (t.K) t.K[(size_t)i * p.n + j] = kEmptyKey;
         if (p.clr_rowc) {
             p.clr_rowc[(size_t)A * p.n + i] = 0u;
@@ -1136,7 +1157,7 @@ __device__ void warp_solo(const EngineParams& p, const NTInfo* nt, const Expansi
             const uint64_t len_e = (p.lengths && ee > eb) ? cell_len(p, nt, X, ci, cj) : 0;
             for (int x = eb; x < ee; ++x) {
                 const Expansion ex = exps[x];
-                if (!stage_ok(p, ex, k)) continue;
+                if (!stage_ok(p, ex, s.gs_stage)) continue;
                 if (ex.kind == EXP_L_CONST || ex.kind == EXP_R_CONST) {
                     uint32_t A, fx;
                     const int4 h = load_head(nt, ex, ci, cj, A, fx);
@@ -1212,7 +1233,8 @@ __device__ void warp_solo(const EngineParams& p, const NTInfo* nt, const Expansi
 }
 
 __device__ void solo_expand(const EngineParams& p, const NTInfo* nt, const Expansion* exps, SoloShared& so,
-                            const uint64_t* src, unsigned long long lo, unsigned long long hi, long long k, int slot,
+                            const uint64_t* src, unsigned long long lo, unsigned long long hi, long long k, int gstage,
+                            int slot,
                             uint64_t* mirror, unsigned long long& dcand, unsigned long long& dexp,
                             long long* pacc = nullptr) {
     long long t0 = pacc ? clock64() : 0;
@@ -1224,7 +1246,7 @@ __device__ void solo_expand(const EngineParams& p, const NTInfo* nt, const Expan
         uint64_t len_e = (p.lengths && ee > eb) ? cell_len(p, nt, X, ci, cj) : 0;
         for (int x = eb; x < ee; ++x) {
             Expansion ex = exps[x];
-            if (!stage_ok(p, ex, k)) continue;
+            if (!stage_ok(p, ex, gstage)) continue;
             if (ex.kind == EXP_L_CONST || ex.kind == EXP_R_CONST) {
                 uint32_t A, fx;
                 int4 h = load_head(nt, ex, ci, cj, A, fx);
@@ -1316,6 +1338,9 @@ __global__ void __launch_bounds__(kBlock, 1) closure_kernel(EngineParams p) {
         S.state.hi = ld_volatile_u64(&st->hi);
         S.state.iter = *(volatile long long*)&st->iter;
         S.state.status = *(volatile int*)&st->status;
+        S.state.gs_stage = *(volatile int*)&st->gs_stage;
+        S.state.gs_slot = *(volatile int*)&st->gs_slot;
+        S.state.gs_round = *(volatile long long*)&st->gs_round;
     }
     __syncthreads();
     LoopState s = S.state;   // identical in every CTA
@@ -1388,7 +1413,7 @@ __global__ void __launch_bounds__(kBlock, 1) closure_kernel(EngineParams p) {
                     }
                     const uint64_t* src =
                         (s.hi - s.lo <= (unsigned long long)kSoloMax && !p.gs_stages) ? so.delta[cur] : nullptr;
-                    solo_expand(p, nt, exps, so, src, s.lo, s.hi, k, slot, so.delta[cur ^ 1], dcand, dexp,
+                    solo_expand(p, nt, exps, so, src, s.lo, s.hi, k, s.gs_stage, slot, so.delta[cur ^ 1], dcand, dexp,
                                 prof ? pacc : nullptr);
                     if (threadIdx.x == 0) {
                         so.cnt[nx] = 0u;
@@ -1454,6 +1479,9 @@ __global__ void __launch_bounds__(kBlock, 1) closure_kernel(EngineParams p) {
                 S.state.hi = ld_volatile_u64(&st->hi);
                 S.state.iter = *(volatile long long*)&st->iter;
                 S.state.status = *(volatile int*)&st->status;
+        S.state.gs_stage = *(volatile int*)&st->gs_stage;
+        S.state.gs_slot = *(volatile int*)&st->gs_slot;
+        S.state.gs_round = *(volatile long long*)&st->gs_round;
             }
             __syncthreads();
             s = S.state;
@@ -1474,7 +1502,7 @@ __global__ void __launch_bounds__(kBlock, 1) closure_kernel(EngineParams p) {
         // [3] close; [2] = ~(min over CTAs of the barrier wait) = the last arriver's release
         const bool ph = p.phase != nullptr && k < p.iter_off_cap;
         long long c0 = ph ? clock64() : 0, c1 = 0, c2 = 0, c3 = 0;
-        expand(p, nt, exps, gsink, nullptr, s.lo, s.hi, k, blockIdx.x * kWarps + wib, gridDim.x * kWarps, lane,
+        expand(p, nt, exps, gsink, nullptr, s.lo, s.hi, k, s.gs_stage, blockIdx.x * kWarps + wib, gridDim.x * kWarps, lane,
                &S.ws[wib], dcand, dexp, false);
         if (ph) {
             __syncthreads();
@@ -1530,9 +1558,9 @@ __global__ void __launch_bounds__(kBlock, 1) closure_kernel(EngineParams p) {
             const uint64_t c = ldcg64(p.log + e);
             const uint32_t A = cell_nt(c), i = cell_i(c), j = cell_j(c);
             const NTInfo& t = nt[A];
-            t.T[(size_t)i * p.Wp + (j >> 5)] = 0u;
-            if (t.S) t.S[(size_t)i * p.Wp + (j >> 5)] = 0u;
-            if (t.ST) t.ST[(size_t)j * p.Wp + (i >> 5)] = 0u;
+            zero_sector(t.T + (size_t)i * p.Wp + (j >> 5));
+            if (t.S) zero_sector(t.S + (size_t)i * p.Wp + (j >> 5));
+            if (t.ST) zero_sector(t.ST + (size_t)j * p.Wp + (i >> 5));
             if (p.rowc) {
                 p.rowc[(size_t)A * p.n + i] = 0u;
                 p.colc[(size_t)A * p.n + j] = 0u;
@@ -1610,7 +1638,7 @@ __global__ void __launch_bounds__(kBlock, 1) async_kernel(EngineParams p) {
             }
             const unsigned okm = __ballot_sync(kFull, ok);
             if (okm) {
-                expand_chunk(p, nt, exps, sk, cell, ok, 0, lane, ws, dcand, dexp);
+                expand_chunk(p, nt, exps, sk, cell, ok, 0, 0, lane, ws, dcand, dexp);
                 flush(p, nt, sk, ws, lane);   // produced cells are appended before ours count as done
                 if (lane == 0) {
                     __threadfence();
@@ -1659,9 +1687,9 @@ __global__ void __launch_bounds__(kBlock, 1) async_kernel(EngineParams p) {
             p.log[e] = c;
             const uint32_t A = cell_nt(c), i = cell_i(c), j = cell_j(c);
             const NTInfo& t = nt[A];
-            t.T[(size_t)i * p.Wp + (j >> 5)] = 0u;
-            if (t.S) t.S[(size_t)i * p.Wp + (j >> 5)] = 0u;
-            if (t.ST) t.ST[(size_t)j * p.Wp + (i >> 5)] = 0u;
+            zero_sector(t.T + (size_t)i * p.Wp + (j >> 5));
+            if (t.S) zero_sector(t.S + (size_t)i * p.Wp + (j >> 5));
+            if (t.ST) zero_sector(t.ST + (size_t)j * p.Wp + (i >> 5));
         }
     }
 }
@@ -1702,6 +1730,9 @@ __global__ void begin_kernel(EngineParams p) {
     if (p.iter_off_cap > 1) p.iter_off[1] = n0;
     if (p.iter_time) p.iter_time[0] = globaltimer();
     st->gs_ring[1] = n0;   // L_1 (Gauss-Seidel windows)
+    st->gs_slot = 1;
+    st->gs_stage = 0;
+    st->gs_round = 0;
 }
 
 // Δ_0 into the snapshots (one launch after seeding).
