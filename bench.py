@@ -602,6 +602,9 @@ def main():
     ap.add_argument("--solo", type=int, default=-1)
     ap.add_argument("--replicas", action="store_true",
                     help="N>1, config4/configS: headline = N independent problems (weak) instead of ONE sharded problem")
+    ap.add_argument("--force-sharded", action="store_true",
+                    help="testing: take the N>1 code path (NCCL communicator, sharded engines, supplements) "
+                         "even with one process")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -616,14 +619,18 @@ def main():
 
     rank, world, local = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
     torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    multi = world > 1 or args.force_sharded
+    if multi:
+        if not dist.is_initialized():
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", str(29500 + os.getpid() % 1000))
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local), rank=rank, world_size=world)
     stream = torch.cuda.current_stream()
     dev_index = torch.cuda.current_device()
 
     # config 4 / config S: ONE problem row-block sharded over the ranks (strong scaling);
     # the other workloads close one independent seeded problem per GPU (weak scaling)
-    sharded = world > 1 and args.workload in ("config4", "configS") and not args.replicas
+    sharded = multi and args.workload in ("config4", "configS") and not args.replicas
     w, desc = make_workload(args.workload, args.seed + (0 if sharded else rank))
     shard_kw = {}
     if sharded:
@@ -747,7 +754,7 @@ def main():
                "ms_per_step": 1e3 * float(e_total.item()) / len(ts)}
 
     supp = None
-    if world > 1 and args.workload == "config4" and not args.no_supplementary:
+    if multi and args.workload == "config4" and not args.no_supplementary:
         supp = {}
         if sharded:
             supp["replicas"] = supplementary_replicas(C, args, rank, world, stream, dist)
@@ -756,7 +763,7 @@ def main():
                                                                                  stream, dist, shard_kw)
             except Exception as ex:
                 supp["paper_faithful_rows_sharded_error"] = repr(ex)
-    if rank == 0 and world == 1 and args.workload == "config4" and not args.no_supplementary:
+    if rank == 0 and not multi and args.workload == "config4" and not args.no_supplementary:
         supp = {}
         try:
             supp["tensor_path"] = supplementary_tensor(C, stream, fmt=2)
@@ -813,7 +820,7 @@ def main():
                 "roofline": roofline, "cpu_baseline": cpu, "cpu_bitset": bits, "e2e": e2e,
                 "gpu_launches": int(launches), "clocks": clk.summary(), "supplementary": supp}
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if multi:
         dist.destroy_process_group()
     return 0
 

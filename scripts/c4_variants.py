@@ -25,6 +25,9 @@ variants = {
     "gauss_seidel_hashed": dict(cell_set=2, schedule=3),
     "async": dict(schedule=2),
     "rows": dict(path_policy=3),
+    "ctas111": dict(cell_set=1, max_ctas=111),
+    "ctas74": dict(cell_set=1, max_ctas=74),
+    "ctas37": dict(cell_set=1, max_ctas=37),
 }
 for name, kw in variants.items():
     r = C.closure(g, d, stream=s, **kw)
