@@ -300,6 +300,62 @@ __device__ __forceinline__ Sink global_sink(const EngineParams& p) {
     return sk;
 }
 
+// End of a grid-wide expansion: the CTA appends all warps' staged cells with ONE global
+// atomic (thousands of warps ending the iteration together would otherwise serialise on
+// the log counter).
+template <int NW>
+__device__ void cta_flush_n(const EngineParams& p, const NTInfo* nt, const Sink& sk, WarpScratch* ws_all, int wib,
+                            int lane, unsigned long long* s_base, int32_t* s_prefix) {
+    __syncthreads();
+    if (wib == 0) {
+        int nb = lane < NW ? ws_all[lane].nbuf : 0;
+        int incl = nb;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            int v = __shfl_up_sync(kFull, incl, o);
+            if (lane >= o) incl += v;
+        }
+        if (lane < NW) s_prefix[lane] = incl - nb;
+        int tot = __shfl_sync(kFull, incl, 31);
+        unsigned long long b = 0;
+        if (lane == 0 && tot) b = atomicAdd(sk.counter, (unsigned long long)tot);
+        if (lane == 0) *s_base = b;
+    }
+    __syncthreads();
+    WarpScratch* ws = &ws_all[wib];
+    const int nb = ws->nbuf;
+    const unsigned long long base = *s_base + (unsigned long long)s_prefix[wib];
+    for (int t = lane; t < nb; t += 32) {
+        uint64_t c = ws->buf[t];
+        unsigned long long idx = base + (unsigned long long)t;
+        uint32_t A = cell_nt(c), i = cell_i(c), j = cell_j(c);
+        uint64_t* K = p.lengths ? nt[A].K : nullptr;
+        uint32_t* word = nt[A].T + (size_t)i * (size_t)p.Wp + (j >> 5);
+        uint32_t bit = 1u << (j & 31);
+        if (idx < p.log_cap) {
+            p.log[idx] = c;
+            if (K != nullptr) atomicOr(word, bit);
+            if (p.rowc != nullptr) {
+                atomicAdd(p.rowc + (size_t)A * p.n + i, 1u);
+                atomicAdd(p.colc + (size_t)A * p.n + j, 1u);
+            }
+        } else {
+            if (K != nullptr) atomicExch((unsigned long long*)(K + (size_t)i * (size_t)p.n + j),
+                                         (unsigned long long)kEmptyKey);
+            else if (!p.hset) atomicAnd(word, ~bit);
+            *(volatile int*)sk.overflow = 1;
+        }
+    }
+    __syncwarp();
+    if (lane == 0) ws->nbuf = 0;
+    __syncwarp();
+}
+
+__device__ __forceinline__ void cta_flush(const EngineParams& p, const NTInfo* nt, const Sink& sk, WarpScratch* ws_all,
+                                          int wib, int lane, unsigned long long* s_base, int32_t* s_prefix) {
+    cta_flush_n<kWarps>(p, nt, sk, ws_all, wib, lane, s_base, s_prefix);
+}
+
 // ------------------------------------------------------------------------------------------
 // Seeding (Alg. 1 lines 6-7): T_ij ∪= {A | A -> x} for every (i,x,j) ∈ E.
 // Parallel edges accumulate; duplicate edges dedupe through the bit test.
@@ -337,7 +393,10 @@ __global__ void __launch_bounds__(kSeedBlock) seed_kernel(EngineParams p, const 
             emit(p, p.nt, sk, ws, lane, has, A, (uint32_t)s, (uint32_t)d, 1, 0);
         }
     }
-    flush(p, p.nt, sk, ws, lane);
+    // one log atomic per CTA (thousands of warps ending together would serialise on it)
+    __shared__ unsigned long long s_base;
+    __shared__ int32_t s_prefix[kSeedBlock / 32];
+    cta_flush_n<kSeedBlock / 32>(p, p.nt, sk, wsa, threadIdx.x >> 5, lane, &s_base, s_prefix);
 }
 
 // CSR / CSC of preterminals from the seed cells Δ_0 = log[0, n_seed).
@@ -684,56 +743,6 @@ __device__ void expand(const EngineParams& p, const NTInfo* nt, const Expansion*
         expand_chunk(p, nt, exps, sk, cell, valid, k, gstage, lane, ws, dcand, dexp);
     }
     if (final_flush) flush(p, nt, sk, ws, lane);
-}
-
-// End of a grid-wide expansion: the CTA appends all warps' staged cells with ONE global
-// atomic (thousands of warps ending the iteration together would otherwise serialise on
-// the log counter).
-__device__ void cta_flush(const EngineParams& p, const NTInfo* nt, const Sink& sk, WarpScratch* ws_all, int wib,
-                          int lane, unsigned long long* s_base, int32_t* s_prefix) {
-    __syncthreads();
-    if (wib == 0) {
-        int nb = lane < kWarps ? ws_all[lane].nbuf : 0;
-        int incl = nb;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            int v = __shfl_up_sync(kFull, incl, o);
-            if (lane >= o) incl += v;
-        }
-        if (lane < kWarps) s_prefix[lane] = incl - nb;
-        int tot = __shfl_sync(kFull, incl, 31);
-        unsigned long long b = 0;
-        if (lane == 0 && tot) b = atomicAdd(sk.counter, (unsigned long long)tot);
-        if (lane == 0) *s_base = b;
-    }
-    __syncthreads();
-    WarpScratch* ws = &ws_all[wib];
-    const int nb = ws->nbuf;
-    const unsigned long long base = *s_base + (unsigned long long)s_prefix[wib];
-    for (int t = lane; t < nb; t += 32) {
-        uint64_t c = ws->buf[t];
-        unsigned long long idx = base + (unsigned long long)t;
-        uint32_t A = cell_nt(c), i = cell_i(c), j = cell_j(c);
-        uint64_t* K = p.lengths ? nt[A].K : nullptr;
-        uint32_t* word = nt[A].T + (size_t)i * (size_t)p.Wp + (j >> 5);
-        uint32_t bit = 1u << (j & 31);
-        if (idx < p.log_cap) {
-            p.log[idx] = c;
-            if (K != nullptr) atomicOr(word, bit);
-            if (p.rowc != nullptr) {
-                atomicAdd(p.rowc + (size_t)A * p.n + i, 1u);
-                atomicAdd(p.colc + (size_t)A * p.n + j, 1u);
-            }
-        } else {
-            if (K != nullptr) atomicExch((unsigned long long*)(K + (size_t)i * (size_t)p.n + j),
-                                         (unsigned long long)kEmptyKey);
-            else if (!p.hset) atomicAnd(word, ~bit);
-            *(volatile int*)sk.overflow = 1;
-        }
-    }
-    __syncwarp();
-    if (lane == 0) ws->nbuf = 0;
-    __syncwarp();
 }
 
 // Fold Δ_k = log[lo,hi) into the snapshots S (row) and ST (transposed).
@@ -1503,12 +1512,12 @@ __global__ void __launch_bounds__(kBlock, 1) closure_kernel(EngineParams p) {
         const bool ph = p.phase != nullptr && k < p.iter_off_cap;
         long long c0 = ph ? clock64() : 0, c1 = 0, c2 = 0, c3 = 0;
         expand(p, nt, exps, gsink, nullptr, s.lo, s.hi, k, s.gs_stage, blockIdx.x * kWarps + wib, gridDim.x * kWarps, lane,
-               &S.ws[wib], dcand, dexp, false);
+               &S.ws[wib], dcand, dexp, p.warp_flush != 0);
         if (ph) {
             __syncthreads();
             c1 = clock64();
         }
-        cta_flush(p, nt, gsink, S.ws, wib, lane, &S.flush_base, S.flush_prefix);
+        if (!p.warp_flush) cta_flush(p, nt, gsink, S.ws, wib, lane, &S.flush_base, S.flush_prefix);
         if (ph) c2 = clock64();
         unsigned long long bw = 0;
         if (!grid_barrier(p, k, &bw)) {
@@ -1756,7 +1765,7 @@ cudaError_t launch_seed(const int32_t* edges, int64_t n_edges, int32_t n_nodes, 
                         const EngineParams& p, cudaStream_t s) {
     (void)n_nodes;
     if (n_edges > 0 && max_rules_per_label > 0)
-        seed_kernel<<<grid_for(n_edges, kSeedBlock), kSeedBlock, 0, s>>>(p, edges, n_edges, lab_ptr, lab_nt, n_labels,
+        seed_kernel<<<std::min(grid_for(n_edges, kSeedBlock), 148 * 8), kSeedBlock, 0, s>>>(p, edges, n_edges, lab_ptr, lab_nt, n_labels,
                                                                           max_rules_per_label);
     return cudaGetLastError();
 }

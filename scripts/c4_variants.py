@@ -25,6 +25,7 @@ variants = {
     "gauss_seidel_hashed": dict(cell_set=2, schedule=3),
     "async": dict(schedule=2),
     "rows": dict(path_policy=3),
+    "warp_flush": dict(cell_set=1, flags=8),
     "ctas111": dict(cell_set=1, max_ctas=111),
     "ctas74": dict(cell_set=1, max_ctas=74),
     "ctas37": dict(cell_set=1, max_ctas=37),
