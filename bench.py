@@ -295,7 +295,8 @@ def rows_alg_bytes(w, r_sparse):
     """Algorithmic bytes of the bit-row path (path_policy 3): the full Jacobi product
     T_{k-1} x T_{k-1} of every rule at every iteration k, in the form the kernels evaluate it
     (DESIGN §3.3), each distinct row / index entry read once per rule and iteration:
-      L (B changes, C preterminal): 4W per non-empty row of T_B (bit-row scan) + 8 B per set
+      L (B changes, C preterminal): 4W per non-empty row of T_B (bit-row scan, once per B for
+        all L rules sharing it) + 8 B per set
         bit (its CSR_C row pointers) + 4 B per CSR_C entry reached (candidate index)
       R (B preterminal, C changes): 8 B per row of CSR_B + 4 B per CSR_B entry + 4W per
         distinct non-empty row of T_C referenced
@@ -331,17 +332,23 @@ def rows_alg_bytes(w, r_sparse):
 
     total = 8 * sum(len(at(X, 0)) for X in range(w.n_nt))
     for k in range(1, K + 1):
+        scanned = set()   # L-form rules with the same B share one scan of each row of T_B
         for A, B, C in rules:
             pb, pc = at(B, k - 1), at(C, k - 1)
+            lform = not pre[B] and pre[C]
+            scan = 4 * W * len(np.unique(pb[:, 0])) if len(pb) else 0
+            if lform:
+                scan = 0 if B in scanned else scan
+                scanned.add(B)
             if len(pb) == 0 or len(pc) == 0:
                 if not pre[B] and len(pb):
-                    total += 4 * W * len(np.unique(pb[:, 0]))   # the row is still scanned
+                    total += scan   # the row is still scanned
                 continue
             MB, MC = mat(pb), mat(pc)
             degC = np.diff(MC.indptr)
             P = (MB.astype(np.int32) @ MC.astype(np.int32))
-            if not pre[B] and pre[C]:
-                total += 4 * W * len(np.unique(pb[:, 0])) + 8 * len(pb) + 4 * int(degC[pb[:, 1]].sum())
+            if lform:
+                total += scan + 8 * len(pb) + 4 * int(degC[pb[:, 1]].sum())
             elif pre[B] and not pre[C]:
                 ref = np.unique(pb[:, 1])
                 total += 8 * len(np.unique(pb[:, 0])) + 4 * len(pb) + 4 * W * int((degC[ref] > 0).sum())

@@ -799,9 +799,12 @@ static cfpq_status rows_sharded_iteration(cfpq_result* r, bool first, int* launc
         int64_t tlo, thi, br;
         dense_partition(r->n, P, g, &tlo, &thi, &br);
         const int64_t lo = std::min<int64_t>(tlo * 128, r->n), hi = std::min<int64_t>(thi * 128, r->n);
-        CFPQ_CUDA_TRY(rows_shard(e, lo, hi, s, launches));
         unsigned long long m = 0;
-        CFPQ_CUDA_TRY(rows_list_settle(e, lo, hi, end, s, &m));
+        for (bool redo = true; redo;) {   // a chunk-list overflow re-runs the shard (grown lists)
+            CFPQ_CUDA_TRY(rows_shard(e, lo, hi, s, launches));
+            CFPQ_CUDA_TRY(rows_list_settle(e, lo, hi, end, s, &m));
+            CFPQ_CUDA_TRY(rows_shard_check(e, s, &redo));
+        }
         cnt[g] = m - end;
         end = m;
     }
@@ -1066,6 +1069,17 @@ static cfpq_status run_dense(cfpq_result* r, int64_t start_k) {
             }
         }
         CFPQ_CUDA_TRY(dense_finish(r->dense, s, &nw));
+        if (rows && r->n_ranks == 1 && !r->comm) {
+            // the plan ran without a host round trip: a chunk-list overflow re-runs the
+            // products of this iteration with grown lists (the counter keeps accumulating)
+            for (bool redo = true; redo;) {
+                CFPQ_CUDA_TRY(rows_shard_check(r->dense, s, &redo));
+                if (redo) {
+                    CFPQ_CUDA_TRY(rows_shard(r->dense, 0, r->n, s, &launches));
+                    CFPQ_CUDA_TRY(dense_finish(r->dense, s, &nw));
+                }
+            }
+        }
         r->launches += launches;
         r->dense_new.push_back((int64_t)nw);
         for (int A : outs) std::swap(r->Tcur[A], r->Tnxt[A]);

@@ -936,9 +936,16 @@ struct RowsCtx {
     int32_t first;                     // iteration 1 (both-preterminal rules evaluated)
     int32_t n_rules;
     int32_t row_lo, row_hi;            // rows this shard derives (row-block sharding; [0, n) else)
+    const int32_t* l_next;             // L-form rules sharing B: next rule of the group (-1 = last);
+                                       // l_next[q] = -2 marks a rule that is not a group leader
+    unsigned long long chunk_cap;      // capacity of each chunk list (the products clamp to it;
+                                       // the host re-runs the shard when a list overflowed)
 };
 
 enum : int { RF_NONE = 0, RF_L = 1, RF_R = 2, RF_V = 3, RF_P = 4 };
+
+// Next rule of an L-form group from RowsCtx::l_next (-1: none).
+__device__ __forceinline__ int rows_l_follow(int v) { return v >= 0 ? v : (v <= -3 ? -(v + 3) : -1); }
 
 __device__ __forceinline__ int row_form(const RowsCtx& c, const DenseRule& r) {
     const bool bc = c.nt[r.B].is_const, cc = c.nt[r.C].is_const;
@@ -1061,9 +1068,12 @@ __global__ void rows_plan_kernel(DenseParams p, RowsCtx c, RowChunk* chunks, uns
                 per = kChunk;
                 isv = 1;
             } else if (f == RF_L) {
-                // chunks of <= kChunkL set bits of T_B[i] (hub rows over many warps)
-                lp = (int)((c.cnt[(size_t)r.B * p.n + i] + kChunkL - 1) / kChunkL);
-                lpl = (int)c.cnt[(size_t)r.B * p.n + i];
+                // chunks of <= kChunkL set bits of T_B[i] (hub rows over many warps); one task
+                // per group of L rules with the same B (the leader scans the row once for all)
+                if (c.l_next[q] >= -1) {   // a group leader
+                    lp = (int)((c.cnt[(size_t)r.B * p.n + i] + kChunkL - 1) / kChunkL);
+                    lpl = (int)c.cnt[(size_t)r.B * p.n + i];
+                }
             } else if (f == RF_P) {
                 const int32_t* ptr = bptr;
                 lp = __ldg(ptr + i + 1) > __ldg(ptr + i);
@@ -1121,7 +1131,7 @@ __global__ void __launch_bounds__(256, NVW <= 2 ? 8 : 3) rows_rgather_kernel(Den
     const int lane = threadIdx.x & 31;
     const int64_t nv4 = ((p.n + 31) / 32 + 3) / 4;
     const int parts = (int)((nv4 + 32 * NVW - 1) / (32 * NVW));   // row slices of 32*NVW uint4
-    const unsigned long long m = c.rc[0] * (unsigned long long)parts;
+    const unsigned long long m = min(c.rc[0], c.chunk_cap) * (unsigned long long)parts;
     unsigned long long my_new = 0;
     for (unsigned long long ti = (blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x) >> 5; ti < m;
          ti += ((unsigned long long)gridDim.x * blockDim.x) >> 5) {
@@ -1181,7 +1191,7 @@ __global__ void __launch_bounds__(256, 4) rows_scatter_kernel(DenseParams p, Row
     __shared__ int32_t wlist[8][kChunkL];   // per warp: the chunk's selected set bits
     const int lane = threadIdx.x & 31;
     const int64_t wn = (p.n + 31) / 32;
-    const unsigned long long m = c.rc[4];
+    const unsigned long long m = min(c.rc[4], c.chunk_cap);
     unsigned long long my_new = 0;
     for (unsigned long long t = (blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x) >> 5; t < m;
          t += ((unsigned long long)gridDim.x * blockDim.x) >> 5) {
@@ -1233,12 +1243,17 @@ __global__ void __launch_bounds__(256, 4) rows_scatter_kernel(DenseParams p, Row
                 }
             }
             __syncwarp();
-            for (int e = lane; e < tk.count; e += 32) {
-                const int rr = lst[e];
-                const int e1 = __ldg(cptr + rr + 1);
-                for (int f2 = __ldg(cptr + rr); f2 < e1; ++f2) {
-                    const int j = __ldg(c.adj_idx + f2);
-                    rows_merge(p, c, A, i, j >> 5, 1u << (j & 31), my_new);
+            // every L rule of the group (same B, so the same listed bits): A -> B C_g
+            for (int qq = q; qq >= 0; qq = rows_l_follow(c.l_next[qq])) {
+                const int Ag = rule_out[qq];
+                const int32_t* cp = c.nt[p.rules[qq].C].csr_ptr;
+                for (int e = lane; e < tk.count; e += 32) {
+                    const int rr = lst[e];
+                    const int e1 = __ldg(cp + rr + 1);
+                    for (int f2 = __ldg(cp + rr); f2 < e1; ++f2) {
+                        const int j = __ldg(c.adj_idx + f2);
+                        rows_merge(p, c, Ag, i, j >> 5, 1u << (j & 31), my_new);
+                    }
                 }
             }
             __syncwarp();
@@ -1273,7 +1288,7 @@ __global__ void __launch_bounds__(kRowThreads) rows_gather_kernel(DenseParams p,
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t wn = (p.n + 31) / 32;
     const int64_t nv4 = (wn + 3) / 4;
-    const unsigned long long m = c.rc[counter];
+    const unsigned long long m = min(c.rc[counter], c.chunk_cap);
     unsigned long long my_new = 0;
     for (unsigned long long ci = blockIdx.x; ci < m; ci += gridDim.x) {
         const RowChunk ch = chunks[ci];
@@ -1473,7 +1488,9 @@ struct DenseEngine {
     unsigned long long kblocks_total = 0;
     uint32_t* cnt = nullptr;   // accounting scratch
     int32_t* rule_out = nullptr;               // [rules] output NT of each rule (bit-row path)
+    int32_t* l_next = nullptr;                 // [rules] L-form groups by B (RowsCtx::l_next)
     std::vector<int32_t> h_rule_out;
+    std::vector<int32_t> h_l_plan;
     void* chunks = nullptr;                    // bit-row path work list
     unsigned long long chunk_cap = 0;
     uint32_t* rcnt = nullptr;                  // bit-row path: per NT row popcounts
@@ -1483,12 +1500,15 @@ struct DenseEngine {
     unsigned long long dlist_cap = 0;
     unsigned long long* rc = nullptr;          // bit-row path counters
     int32_t launch_mode = 0;                   // cfpq_options.dense_launch
+    unsigned long long* h_rc = nullptr;        // bit-row path counters, pinned host copy
     const NTInfo* rows_nt = nullptr;           // bit-row path: this iteration's NT table / CSR
     const int32_t* rows_adj = nullptr;
     bool rows_first = false;
     ~DenseEngine() {
         cudaFree(cnt);
         cudaFree(rule_out);
+        cudaFree(l_next);
+        if (h_rc) cudaFreeHost(h_rc);
         cudaFree(chunks);
         cudaFree(rcnt);
         cudaFree(dlist);
@@ -1570,6 +1590,24 @@ DenseEngine* dense_create(int32_t n, int32_t n_nt, int64_t Wp, const std::vector
     if ((c = cudaMalloc(&e->rule_out, std::max<size_t>(1, rl.size()) * 4)) != cudaSuccess) return fail("tables", c);
     if (!rl.empty())
         cudaMemcpyAsync(e->rule_out, e->h_rule_out.data(), rl.size() * 4, cudaMemcpyHostToDevice, s);
+    {
+        // L-form rules (B changes, C preterminal) grouped by B, in rule order: the leader owns
+        // the row scan and links to the next member (>= 0, or -1 if alone); member q links
+        // to the next one as -(next + 3), or -2 if last (RowsCtx::l_next, rows_l_follow)
+        std::vector<std::vector<int32_t>> groups(n_nt);
+        for (size_t q = 0; q < rl.size(); ++q)
+            if (!is_const[rl[q].B] && is_const[rl[q].C]) groups[rl[q].B].push_back((int32_t)q);
+        e->h_l_plan.assign(rl.size(), -1);
+        for (auto& gq : groups)
+            for (size_t t = 0; t < gq.size(); ++t) {
+                const bool has_next = t + 1 < gq.size();
+                if (t == 0) e->h_l_plan[gq[t]] = has_next ? gq[t + 1] : -1;
+                else e->h_l_plan[gq[t]] = has_next ? -(gq[t + 1] + 3) : -2;
+            }
+    }
+    if ((c = cudaMalloc(&e->l_next, std::max<size_t>(1, rl.size()) * 4)) != cudaSuccess) return fail("tables", c);
+    if (!rl.empty())
+        cudaMemcpyAsync(e->l_next, e->h_l_plan.data(), rl.size() * 4, cudaMemcpyHostToDevice, s);
     const int64_t row_bytes = fp4 ? e->np / 2 : e->np;   // nibble packs: half the bytes per row
     if (!make_map(&e->tmA, e->T8, (int64_t)std::max(na, 1) * e->np, row_bytes, kTM) ||
         !make_map(&e->tmB, e->T8T, (int64_t)std::max(nb, 1) * e->np, row_bytes, kTN) ||
@@ -1789,6 +1827,8 @@ cudaError_t rows_begin(DenseEngine* e, const NTInfo* nt, const int32_t* adj_idx,
         if ((c = cudaMalloc(&e->rc, 8 * 8)) != cudaSuccess) return c;
         if ((c = cudaMemsetAsync(e->rc, 0, 8 * 8, s)) != cudaSuccess) return c;
         if ((c = cudaMalloc(&e->dlist, e->dlist_cap * sizeof(uint4))) != cudaSuccess) return c;
+        if ((c = cudaMallocHost(&e->h_rc, 8 * 8)) != cudaSuccess) return c;
+        memset(e->h_rc, 0, 8 * 8);
     }
     // chunk capacity: grow lazily (the plan reports the exact count)
     const unsigned long long want = std::max<unsigned long long>(e->chunk_cap, (unsigned long long)n_rules * e->n + 1024);
@@ -1809,7 +1849,7 @@ cudaError_t rows_begin(DenseEngine* e, const NTInfo* nt, const int32_t* adj_idx,
     e->rows_adj = adj_idx;
     e->rows_first = first;
     DenseParams p = rows_params(e);
-    RowsCtx rc{nt, adj_idx, e->rcnt, (uint4*)e->dlist, e->dlist_cap, e->rc, first ? 1 : 0, n_rules, 0, e->n};
+    RowsCtx rc{nt, adj_idx, e->rcnt, (uint4*)e->dlist, e->dlist_cap, e->rc, first ? 1 : 0, n_rules, 0, e->n, e->l_next, e->chunk_cap};
     const int sms = device_sms();
     // T_k buffer := T_{k-1}
     if (first) {
@@ -1834,31 +1874,15 @@ cudaError_t rows_shard(DenseEngine* e, int64_t row_lo, int64_t row_hi, cudaStrea
     const int32_t n_rules = (int32_t)e->h_rule_out.size();
     DenseParams p = rows_params(e);
     RowsCtx rc{e->rows_nt, e->rows_adj, e->rcnt, (uint4*)e->dlist, e->dlist_cap, e->rc, e->rows_first ? 1 : 0,
-               n_rules, (int32_t)row_lo, (int32_t)row_hi};
+               n_rules, (int32_t)row_lo, (int32_t)row_hi, e->l_next, e->chunk_cap};
     const int sms = device_sms();
-    for (int attempt = 0; attempt < 2; ++attempt) {
-        if ((c = cudaMemsetAsync(e->rc, 0, 8, s)) != cudaSuccess) return c;       // chunk lists of this shard
-        if ((c = cudaMemsetAsync(e->rc + 3, 0, 2 * 8, s)) != cudaSuccess) return c;
-        rows_plan_kernel<<<sms * 8, 256, 0, s>>>(p, rc, (RowChunk*)e->chunks, e->chunk_cap);
-        unsigned long long got[5] = {0, 0, 0, 0, 0};
-        if ((c = cudaMemcpyAsync(got, e->rc, 5 * 8, cudaMemcpyDeviceToHost, s)) != cudaSuccess) return c;
-        if ((c = cudaStreamSynchronize(s)) != cudaSuccess) return c;
-        if (got[2]) {
-            // the previous iteration's list overflowed (the delta kernel copied whole
-            // matrices instead): grow it for the next iterations
-            cudaFree(e->dlist);
-            e->dlist_cap *= 4;
-            if ((c = cudaMalloc(&e->dlist, e->dlist_cap * sizeof(uint4))) != cudaSuccess) return c;
-            rc.dlist = (uint4*)e->dlist;
-            rc.dlist_cap = e->dlist_cap;
-            if ((c = cudaMemsetAsync(e->rc + 2, 0, 8, s)) != cudaSuccess) return c;
-        }
-        const unsigned long long need = std::max(got[0], std::max(got[3], got[4]));
-        if (need <= e->chunk_cap) break;
-        cudaFree(e->chunks);
-        e->chunk_cap = need + need / 4;
-        if ((c = cudaMalloc(&e->chunks, 3 * e->chunk_cap * sizeof(RowChunk))) != cudaSuccess) return c;
-    }
+    // plan and products back to back, no host round trip: the products clamp every list to
+    // its capacity and the counters are copied to pinned host memory behind them; the host
+    // checks them after the iteration's synchronisation (rows_shard_check) and re-runs the
+    // shard if a list overflowed (products are idempotent ORs; Δ_k records only new flips)
+    if ((c = cudaMemsetAsync(e->rc, 0, 8, s)) != cudaSuccess) return c;       // chunk lists of this shard
+    if ((c = cudaMemsetAsync(e->rc + 3, 0, 2 * 8, s)) != cudaSuccess) return c;
+    rows_plan_kernel<<<sms * 8, 256, 0, s>>>(p, rc, (RowChunk*)e->chunks, e->chunk_cap);
     // 4 CTAs x 8 warps per SM (measured: 6 or 8 CTAs with fewer registers are not faster)
     rows_scatter_kernel<<<resident_grid(rows_scatter_kernel, 256, sms), 256, 0, s>>>(p, rc, e->rule_out,
                                                                                  (const RowChunk*)e->chunks + 2 * e->chunk_cap);
@@ -1879,7 +1903,33 @@ cudaError_t rows_shard(DenseEngine* e, int64_t row_lo, int64_t row_hi, cudaStrea
         rows_rgather_kernel<2><<<resident_grid(rows_rgather_kernel<2>, 256, sms), 256, 0, s>>>(p, rc, e->rule_out, chR);
     }
     if (launches) *launches += 2 + (e->has_v ? 1 : 0) + (e->has_r ? 1 : 0);
+    if ((c = cudaMemcpyAsync(e->h_rc, e->rc, 5 * 8, cudaMemcpyDeviceToHost, s)) != cudaSuccess) return c;
     return cudaGetLastError();
+}
+
+// After the stream passed rows_shard: grow what overflowed.  *redo = a chunk list did not
+// fit (the shard must run again for the same rows); a Δ_k word list overflow of the previous
+// iteration (the delta kernel copied whole matrices instead) only grows the list.
+cudaError_t rows_shard_check(DenseEngine* e, cudaStream_t s, bool* redo) {
+    cudaError_t c;
+    *redo = false;
+    if (e->n_out == 0 || !e->rc) return cudaSuccess;
+    const unsigned long long* got = e->h_rc;
+    if (got[2]) {
+        cudaFree(e->dlist);
+        e->dlist_cap *= 4;
+        if ((c = cudaMalloc(&e->dlist, e->dlist_cap * sizeof(uint4))) != cudaSuccess) return c;
+        if ((c = cudaMemsetAsync(e->rc + 2, 0, 8, s)) != cudaSuccess) return c;
+        e->h_rc[2] = 0;
+    }
+    const unsigned long long need = std::max(got[0], std::max(got[3], got[4]));
+    if (need > e->chunk_cap) {
+        cudaFree(e->chunks);
+        e->chunk_cap = need + need / 4;
+        if ((c = cudaMalloc(&e->chunks, 3 * e->chunk_cap * sizeof(RowChunk))) != cudaSuccess) return c;
+        *redo = true;
+    }
+    return cudaSuccess;
 }
 
 cudaError_t rows_product(DenseEngine* e, uint32_t* const* T, uint32_t* const* Tn, const NTInfo* nt,
@@ -1916,7 +1966,7 @@ cudaError_t rows_list_settle(DenseEngine* e, int64_t row_lo, int64_t row_hi, uns
         if ((c = cudaMemcpyAsync(e->rc + 1, &keep, 8, cudaMemcpyHostToDevice, s)) != cudaSuccess) return c;
         DenseParams p = rows_params(e);
         RowsCtx rc{e->rows_nt, e->rows_adj, e->rcnt, (uint4*)e->dlist, e->dlist_cap, e->rc, 0,
-                   (int32_t)e->h_rule_out.size(), (int32_t)row_lo, (int32_t)row_hi};
+                   (int32_t)e->h_rule_out.size(), (int32_t)row_lo, (int32_t)row_hi, e->l_next, e->chunk_cap};
         rows_diff_kernel<<<device_sms() * 8, 256, 0, s>>>(p, rc, 0);
         if ((c = cudaMemcpyAsync(&m, e->rc + 1, 8, cudaMemcpyDeviceToHost, s)) != cudaSuccess) return c;
         if ((c = cudaStreamSynchronize(s)) != cudaSuccess) return c;
@@ -1950,7 +2000,7 @@ cudaError_t rows_apply_all(DenseEngine* e, unsigned long long total, cudaStream_
     if (total == 0) return cudaSuccess;
     DenseParams p = rows_params(e);
     RowsCtx rc{e->rows_nt, e->rows_adj, e->rcnt, (uint4*)e->dlist, e->dlist_cap, e->rc, 0,
-               (int32_t)e->h_rule_out.size(), 0, e->n};
+               (int32_t)e->h_rule_out.size(), 0, e->n, e->l_next, e->chunk_cap};
     rows_apply_kernel<<<device_sms() * 8, 256, 0, s>>>(p, rc, 0ull, total);
     if (launches) *launches += 1;
     return cudaGetLastError();

@@ -68,19 +68,25 @@ def _rows_bytes_by_definition(w, snaps):
     total = 8 * sum(len(snaps[0][A]) for A in range(w.n_nt))
     for k in range(1, K + 1):
         T = snaps[k - 1]
+        scanned = set()
         for A, B, C in rules:
             tb, tc = T[B], T[C]
             pb, pc = B not in lhs, C not in lhs
             rows_b = {i for i, _ in tb}
+            scan = 4 * W * len(rows_b)
+            if not pb and pc:           # L rules sharing B scan each row of T_B once
+                if B in scanned:
+                    scan = 0
+                scanned.add(B)
             if not tb or not tc:
                 if not pb and tb:
-                    total += 4 * W * len(rows_b)
+                    total += scan
                 continue
             row_c = {}
             for r, j in tc:
                 row_c.setdefault(r, set()).add(j)
             if not pb and pc:
-                total += 4 * W * len(rows_b) + 8 * len(tb) + 4 * sum(len(row_c.get(r, ())) for _, r in tb)
+                total += scan + 8 * len(tb) + 4 * sum(len(row_c.get(r, ())) for _, r in tb)
             elif pb and not pc:
                 refs = {r for _, r in tb}
                 total += 8 * len(rows_b) + 4 * len(tb) + 4 * W * sum(1 for r in refs if r in row_c)
