@@ -157,7 +157,8 @@ typedef struct {
     int32_t diag_flags;      /* diagnostics, 0 = defaults: bit 0 no bit pre-check before the
                                 atomic, bit 1 clear the other workspace bank on a side
                                 stream, bit 2 no reset of the bit words at the fixpoint,
-                                bit 3 per-warp log appends instead of the CTA-level flush    */
+                                bit 3 per-warp log appends instead of the CTA-level flush,
+                                bits 4-6 bit-row R-form kernel variant (0 = default)          */
     int32_t grid_rows;       /* tensor engine, world_size (or reserved_emulate) > 1: 2-D
                                 process grid grid_rows x grid_cols (SUMMA-style blocks
                                 (I_a, J_b) of every T_A); 0 = 1-D row blocks.

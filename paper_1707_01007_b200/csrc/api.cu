@@ -363,6 +363,7 @@ static cfpq_status ensure_dense(cfpq_result* r) {
         set_error(err);
         return CFPQ_E_CUDA;
     }
+    dense_set_rgather_variant(r->dense, (r->opts.diag_flags >> 4) & 7);
     const size_t mat_words = (size_t)r->rows_alloc * (size_t)r->Wp;
     int n_out = (int)dense_outputs(r->dense).size();
     cfpq_status st = dalloc(&r->d_Tn, mat_words * std::max(n_out, 1), "dense next bit matrices");

@@ -254,6 +254,7 @@ DenseEngine* dense_create(int32_t n, int32_t n_nt, int64_t Wp, const std::vector
                           bool fp4, int64_t dlist_cap, int32_t launch_mode);
 bool dense_is_fp4(const DenseEngine* e);
 void dense_destroy(DenseEngine* e);
+void dense_set_rgather_variant(DenseEngine* e, int v);   // diagnostics (diag_flags bits 4-6)
 cudaError_t dense_begin(DenseEngine* e, uint32_t* const* T, uint32_t* const* Tn, bool first, cudaStream_t s,
                         int* launches, bool pack_operands);
 // Bit-row (full-operand Jacobi) iteration: nt = the device NT table (is_const, CSR rows of

@@ -1125,9 +1125,11 @@ __global__ void rows_plan_kernel(DenseParams p, RowsCtx c, RowChunk* chunks, uns
 // Form R, one warp per (chunk, row slice of 32 * NVW uint4): lane e holds CSR_B(i) entry
 // e, the non-empty rows T_C[r] are ORed one after another with NVW 128-bit loads per lane
 // in flight, then the non-zero words of the slice are merged.  No CTA barriers.
-template <int NVW>
-__global__ void __launch_bounds__(256, NVW <= 2 ? 8 : 3) rows_rgather_kernel(DenseParams p, RowsCtx c, const int32_t* __restrict__ rule_out,
-                                                           const RowChunk* __restrict__ chunks) {
+template <int NVW, int RU, int MINB>
+__global__ void __launch_bounds__(256, MINB) rows_rgather_kernel(DenseParams p, RowsCtx c, const int32_t* __restrict__ rule_out,
+                                                                 const RowChunk* __restrict__ chunks) {
+    // RU rows of T_C in flight per step (RU x NVW 128-bit loads per lane issued before the
+    // ORs): the R form is latency-bound on the load -> OR dependence of one row at a time
     const int lane = threadIdx.x & 31;
     const int64_t nv4 = ((p.n + 31) / 32 + 3) / 4;
     const int parts = (int)((nv4 + 32 * NVW - 1) / (32 * NVW));   // row slices of 32*NVW uint4
@@ -1153,21 +1155,32 @@ __global__ void __launch_bounds__(256, NVW <= 2 ? 8 : 3) rows_rgather_kernel(Den
         const uint4* TC = reinterpret_cast<const uint4*>(p.T[r.C]);
         const int64_t wp4 = p.Wp / 4;
         while (todo) {
-            const int src_lane = __ffs(todo) - 1;
-            todo &= todo - 1u;
-            const int row = __shfl_sync(0xffffffffu, rr, src_lane);
-            const uint4* rowC = TC + (size_t)row * wp4;
+            int rows_u[RU];
+            bool have[RU];
 #pragma unroll
-            for (int b = 0; b < NVW; ++b) {
-                const int64_t v = vbase + (int64_t)b * 32 + lane;
-                if (v < nv4) {
-                    const uint4 x = __ldg(rowC + v);
-                    acc[b].x |= x.x;
-                    acc[b].y |= x.y;
-                    acc[b].z |= x.z;
-                    acc[b].w |= x.w;
-                }
+            for (int u = 0; u < RU; ++u) {
+                have[u] = todo != 0u;   // warp-uniform
+                const int src_lane = have[u] ? __ffs(todo) - 1 : 0;
+                if (have[u]) todo &= todo - 1u;
+                rows_u[u] = __shfl_sync(0xffffffffu, rr, src_lane);
             }
+            uint4 x[RU][NVW];
+#pragma unroll
+            for (int u = 0; u < RU; ++u)
+#pragma unroll
+                for (int b = 0; b < NVW; ++b) {
+                    const int64_t v = vbase + (int64_t)b * 32 + lane;
+                    x[u][b] = have[u] && v < nv4 ? __ldg(TC + (size_t)rows_u[u] * wp4 + v) : make_uint4(0, 0, 0, 0);
+                }
+#pragma unroll
+            for (int u = 0; u < RU; ++u)
+#pragma unroll
+                for (int b = 0; b < NVW; ++b) {
+                    acc[b].x |= x[u][b].x;
+                    acc[b].y |= x[u][b].y;
+                    acc[b].z |= x[u][b].z;
+                    acc[b].w |= x[u][b].w;
+                }
         }
         const int A = rule_out[ch.rule];
 #pragma unroll
@@ -1500,6 +1513,7 @@ struct DenseEngine {
     unsigned long long dlist_cap = 0;
     unsigned long long* rc = nullptr;          // bit-row path counters
     int32_t launch_mode = 0;                   // cfpq_options.dense_launch
+    int32_t rgather_variant = 0;               // diagnostics (diag_flags bits 4-6): R-form kernel shape
     unsigned long long* h_rc = nullptr;        // bit-row path counters, pinned host copy
     const NTInfo* rows_nt = nullptr;           // bit-row path: this iteration's NT table / CSR
     const int32_t* rows_adj = nullptr;
@@ -1519,6 +1533,7 @@ struct DenseEngine {
 };
 
 void dense_destroy(DenseEngine* e) { delete e; }
+void dense_set_rgather_variant(DenseEngine* e, int v) { e->rgather_variant = v; }
 
 DenseEngine* dense_create(int32_t n, int32_t n_nt, int64_t Wp, const std::vector<Rule3>& rules,
                           const std::vector<int32_t>& is_const, cudaStream_t s, std::string* err, bool tensor,
@@ -1898,9 +1913,19 @@ cudaError_t rows_shard(DenseEngine* e, int64_t row_lo, int64_t row_hi, cudaStrea
     };
     if (e->has_v) cta_gather(chV, 3);
     if (e->has_r) {
-        // R chunks: a warp per (chunk, row slice of 32 x 2 uint4 = 1 KiB): many light warps
-        // (config 4: 10.2 ms closure; 4 / 8 / 16 uint4 per lane: 10.7 / 11.8 / 16.0 ms; 1: 11.5 ms)
-        rows_rgather_kernel<2><<<resident_grid(rows_rgather_kernel<2>, 256, sms), 256, 0, s>>>(p, rc, e->rule_out, chR);
+        // R chunks: a warp per (chunk, row slice of 32 x NVW uint4): many light warps
+        // (config 4, one row in flight: 2 uint4 per lane 10.2 ms closure; 4 / 8 / 16: 10.7 /
+        // 11.8 / 16.0 ms; 1: 11.5 ms); variants with RU rows in flight (rgather_variant)
+        auto rg = [&](auto kern) {
+            kern<<<resident_grid(kern, 256, sms), 256, 0, s>>>(p, rc, e->rule_out, chR);
+        };
+        switch (e->rgather_variant) {
+            case 1: rg(rows_rgather_kernel<1, 4, 6>); break;
+            case 2: rg(rows_rgather_kernel<2, 2, 6>); break;
+            case 3: rg(rows_rgather_kernel<2, 4, 4>); break;
+            case 4: rg(rows_rgather_kernel<1, 8, 4>); break;
+            default: rg(rows_rgather_kernel<2, 1, 8>); break;
+        }
     }
     if (launches) *launches += 2 + (e->has_v ? 1 : 0) + (e->has_r ? 1 : 0);
     if ((c = cudaMemcpyAsync(e->h_rc, e->rc, 5 * 8, cudaMemcpyDeviceToHost, s)) != cudaSuccess) return c;

@@ -25,6 +25,10 @@ variants = {
     "gauss_seidel_hashed": dict(cell_set=2, schedule=3),
     "async": dict(schedule=2),
     "rows": dict(path_policy=3),
+    "rows_rg1": dict(path_policy=3, flags=1 << 4),
+    "rows_rg2": dict(path_policy=3, flags=2 << 4),
+    "rows_rg3": dict(path_policy=3, flags=3 << 4),
+    "rows_rg4": dict(path_policy=3, flags=4 << 4),
     "warp_flush": dict(cell_set=1, flags=8),
     "ctas111": dict(cell_set=1, max_ctas=111),
     "ctas74": dict(cell_set=1, max_ctas=74),
