@@ -804,7 +804,7 @@ static cfpq_status rows_sharded_iteration(cfpq_result* r, bool first, int* launc
         for (bool redo = true; redo;) {   // a chunk-list overflow re-runs the shard (grown lists)
             CFPQ_CUDA_TRY(rows_shard(e, lo, hi, s, launches));
             CFPQ_CUDA_TRY(rows_list_settle(e, lo, hi, end, s, &m));
-            CFPQ_CUDA_TRY(rows_shard_check(e, s, &redo));
+            CFPQ_CUDA_TRY(rows_shard_check(e, s, &redo, false));
         }
         cnt[g] = m - end;
         end = m;
@@ -1074,7 +1074,7 @@ static cfpq_status run_dense(cfpq_result* r, int64_t start_k) {
             // the plan ran without a host round trip: a chunk-list overflow re-runs the
             // products of this iteration with grown lists (the counter keeps accumulating)
             for (bool redo = true; redo;) {
-                CFPQ_CUDA_TRY(rows_shard_check(r->dense, s, &redo));
+                CFPQ_CUDA_TRY(rows_shard_check(r->dense, s, &redo, true));
                 if (redo) {
                     CFPQ_CUDA_TRY(rows_shard(r->dense, 0, r->n, s, &launches));
                     CFPQ_CUDA_TRY(dense_finish(r->dense, s, &nw));

@@ -277,7 +277,9 @@ cudaError_t bit_block_copy(uint32_t* T, int64_t Wp, int64_t r_lo, int64_t r_hi, 
 cudaError_t rows_begin(DenseEngine* e, const NTInfo* nt, const int32_t* adj_idx, const uint64_t* log,
                        unsigned long long n_seeds, bool first, cudaStream_t s, int* launches);
 cudaError_t rows_shard(DenseEngine* e, int64_t row_lo, int64_t row_hi, cudaStream_t s, int* launches);
-cudaError_t rows_shard_check(DenseEngine* e, cudaStream_t s, bool* redo);   // after a sync
+// After a sync: grow what overflowed; *redo = re-run the shard (chunk lists); check_list:
+// also handle a Δ word-list overflow (unsharded runs; sharded runs rebuild the list instead)
+cudaError_t rows_shard_check(DenseEngine* e, cudaStream_t s, bool* redo, bool check_list);
 cudaError_t rows_list_settle(DenseEngine* e, int64_t row_lo, int64_t row_hi, unsigned long long keep, cudaStream_t s,
                              unsigned long long* count);
 cudaError_t rows_list(DenseEngine* e, unsigned long long want, void** list, unsigned long long* cap);

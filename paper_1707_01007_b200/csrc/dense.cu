@@ -989,18 +989,17 @@ __global__ void rows_seed_kernel(DenseParams p, RowsCtx c, const uint64_t* __res
 
 // Iteration k > 1: T_k buffer (holding T_{k-2}) |= Δ_{k-1} words; after an overflowed list,
 // copy T_{k-1} whole (and flag it for the host to grow the list).
-__global__ void rows_delta_kernel(DenseParams p, RowsCtx c) {
+__global__ void rows_delta_kernel(DenseParams p, RowsCtx c, int copy_whole) {
     const unsigned long long m = c.rc[1];
     const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
     const unsigned long long t0 = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x;
-    if (m <= c.dlist_cap) {
+    if (!copy_whole) {   // the host knows the list of Δ_{k-1} is complete
         for (unsigned long long e = t0; e < m; e += stride) {
             const uint4 d = c.dlist[e];
             atomicOr(p.Tn[d.x] + (size_t)d.y * p.Wp + d.z, d.w);
         }
         return;
     }
-    if (t0 == 0) c.rc[2] = 1;
     const unsigned long long words4 = (unsigned long long)p.n * p.Wp / 4;
     for (int o = 0; o < p.n_out; ++o) {
         const int A = p.out_nt[o];
@@ -1515,6 +1514,7 @@ struct DenseEngine {
     int32_t launch_mode = 0;                   // cfpq_options.dense_launch
     int32_t rgather_variant = 0;               // diagnostics (diag_flags bits 4-6): R-form kernel shape
     unsigned long long* h_rc = nullptr;        // bit-row path counters, pinned host copy
+    bool list_complete = true;                 // the Δ word list of the last iteration holds every word
     const NTInfo* rows_nt = nullptr;           // bit-row path: this iteration's NT table / CSR
     const int32_t* rows_adj = nullptr;
     bool rows_first = false;
@@ -1871,8 +1871,10 @@ cudaError_t rows_begin(DenseEngine* e, const NTInfo* nt, const int32_t* adj_idx,
         if ((c = cudaMemsetAsync(e->rcnt, 0, (size_t)e->n_nt * e->n * 4, s)) != cudaSuccess) return c;
         if ((c = cudaMemsetAsync(e->rc, 0, 8 * 8, s)) != cudaSuccess) return c;
         if (n_seeds) rows_seed_kernel<<<sms * 8, 256, 0, s>>>(p, rc, log, n_seeds);
+        e->list_complete = true;
     } else {
-        rows_delta_kernel<<<sms * 8, 256, 0, s>>>(p, rc);
+        rows_delta_kernel<<<sms * 8, 256, 0, s>>>(p, rc, e->list_complete ? 0 : 1);
+        e->list_complete = true;
     }
     if (launches) *launches += 1;
     // Δ_k list and chunk counters restart
@@ -1935,17 +1937,20 @@ cudaError_t rows_shard(DenseEngine* e, int64_t row_lo, int64_t row_hi, cudaStrea
 // After the stream passed rows_shard: grow what overflowed.  *redo = a chunk list did not
 // fit (the shard must run again for the same rows); a Δ_k word list overflow of the previous
 // iteration (the delta kernel copied whole matrices instead) only grows the list.
-cudaError_t rows_shard_check(DenseEngine* e, cudaStream_t s, bool* redo) {
+cudaError_t rows_shard_check(DenseEngine* e, cudaStream_t s, bool* redo, bool check_list) {
     cudaError_t c;
+    (void)s;
     *redo = false;
     if (e->n_out == 0 || !e->rc) return cudaSuccess;
     const unsigned long long* got = e->h_rc;
-    if (got[2]) {
+    if (check_list && got[1] > e->dlist_cap) {
+        // the Δ_k word list overflowed (words lost): the next iteration builds T_{k+1}'s buffer
+        // by a whole-matrix copy, and the list grows for the iterations after
         cudaFree(e->dlist);
-        e->dlist_cap *= 4;
+        e->dlist = nullptr;
+        e->dlist_cap = std::max<unsigned long long>(e->dlist_cap * 4, got[1] + got[1] / 4);
         if ((c = cudaMalloc(&e->dlist, e->dlist_cap * sizeof(uint4))) != cudaSuccess) return c;
-        if ((c = cudaMemsetAsync(e->rc + 2, 0, 8, s)) != cudaSuccess) return c;
-        e->h_rc[2] = 0;
+        e->list_complete = false;
     }
     const unsigned long long need = std::max(got[0], std::max(got[3], got[4]));
     if (need > e->chunk_cap) {
