@@ -1255,11 +1255,14 @@ __global__ void __launch_bounds__(256, 4) rows_scatter_kernel(DenseParams p, Row
                 }
             }
             __syncwarp();
+            // the plan sized the chunk from cnt[B][i], which a re-run of the shard (chunk-list
+            // overflow) reads after this iteration's merges grew it: list only the bits found
+            const int found = min(tk.count, max(0, base - tk.first));
             // every L rule of the group (same B, so the same listed bits): A -> B C_g
             for (int qq = q; qq >= 0; qq = rows_l_follow(c.l_next[qq])) {
                 const int Ag = rule_out[qq];
                 const int32_t* cp = c.nt[p.rules[qq].C].csr_ptr;
-                for (int e = lane; e < tk.count; e += 32) {
+                for (int e = lane; e < found; e += 32) {
                     const int rr = lst[e];
                     const int e1 = __ldg(cp + rr + 1);
                     for (int f2 = __ldg(cp + rr); f2 < e1; ++f2) {
@@ -1340,7 +1343,8 @@ __global__ void __launch_bounds__(kRowThreads) rows_gather_kernel(DenseParams p,
                 base += total;
                 __syncthreads();
             }
-            if (threadIdx.x == 0) n_list = ch.count;
+            // bits found (a re-run of the shard may have sized the chunk from a grown count)
+            if (threadIdx.x == 0) n_list = min(ch.count, max(0, base - ch.first));
         } else {
             // R: CSR_B(i) entries [first, first+count), rows of T_C that are empty skipped
             if (threadIdx.x < ch.count) {

@@ -2,6 +2,6 @@
 cd "$GRAFT_REPO_ROOT" 2>/dev/null || cd /root/repo
 mkdir -p gpurun_out
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build_g.txt 2>&1
-timeout 1800 python -m pytest tests/test_gpu_rows.py tests/test_gpu_fullsize.py tests/test_gpu_edges.py -k "rows or bit_row" -m gpu -x -q -p no:cacheprovider --timeout 900 -rf > gpurun_out/pytest_g.txt 2>&1
+timeout 1800 python -m pytest tests/test_gpu_rows.py tests/test_gpu_fullsize.py tests/test_gpu_edges.py -k "rows or bit_row" -m gpu -q -p no:cacheprovider --timeout 900 -rf > gpurun_out/pytest_g.txt 2>&1
 timeout 900 python scripts/c4_variants.py > gpurun_out/c4_variants_g.txt 2>&1
 tail -n 3 gpurun_out/pytest_g.txt
