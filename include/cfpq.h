@@ -166,6 +166,13 @@ typedef struct {
     int32_t grid_cols;
     int64_t rows_list_capacity; /* bit-row engine: initial capacity (words) of the Δ_k word
                                 list; 0 = 2^20.  Grown on overflow (tests use tiny values)    */
+    int32_t exchange;        /* row-sharded sparse engine (world_size or reserved_emulate > 1):
+                                0 NCCL, host-driven iterations (all-gather of counts + padded
+                                cells per iteration); 1 peer memory, device-resident: one
+                                persistent kernel per GPU appends every new cell to every
+                                rank's log over NVLink (CUDA IPC mappings) and meets the other
+                                ranks at a cross-GPU barrier each iteration (emulated shards:
+                                virtual ranks = CTA groups of one launch)                    */
 } cfpq_options;
 
 CFPQ_API void cfpq_options_default(cfpq_options* o);

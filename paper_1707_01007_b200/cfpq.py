@@ -52,7 +52,7 @@ class Options(ctypes.Structure):
                 ("tensor_format", ctypes.c_int32),
                 ("dense_launch", ctypes.c_int32), ("diag_flags", ctypes.c_int32),
                 ("grid_rows", ctypes.c_int32), ("grid_cols", ctypes.c_int32),
-                ("rows_list_capacity", ctypes.c_int64)]
+                ("rows_list_capacity", ctypes.c_int64), ("exchange", ctypes.c_int32)]
 
 
 _lib = None
@@ -194,7 +194,7 @@ def options(semantics: int = 0, schedule: int = 0, path_policy: int = 0, account
             record_times: bool = False, max_ctas: int = 0, world_size: int = 1, rank: int = 0,
             nccl_unique_id=None, emulate_ranks: int = 0, flags: int = 0, cell_set: int = 0,
             tensor_format: int = 0, dense_launch: int = 0, grid: Tuple[int, int] = (0, 0),
-            rows_list_capacity: int = 0) -> Options:
+            rows_list_capacity: int = 0, exchange: int = 0) -> Options:
     o = Options()
     load().cfpq_options_default(ctypes.byref(o))
     o.semantics, o.schedule, o.path_policy = int(semantics), int(schedule), int(path_policy)
@@ -212,6 +212,7 @@ def options(semantics: int = 0, schedule: int = 0, path_policy: int = 0, account
     o.dense_launch = int(dense_launch)
     o.grid_rows, o.grid_cols = int(grid[0]), int(grid[1])
     o.rows_list_capacity = int(rows_list_capacity)
+    o.exchange = int(exchange)
     o.cell_set = int(cell_set)
     o.tensor_format = int(tensor_format)
     if nccl_unique_id is not None:

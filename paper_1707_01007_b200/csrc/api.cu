@@ -147,6 +147,18 @@ struct cfpq_result {
     unsigned long long dense_kb = 0;          // issued 128x256x128 int8 MMA k-blocks
     int32_t n_stages = 0;                     // distinct LHS NTs (Gauss-Seidel stages, schedule 3)
     int32_t grid_r = 0, grid_c = 0;           // 2-D process grid of the tensor engine (0: 1-D)
+    // peer-memory exchange of the row-sharded sparse engine (exchange = 1, XrParams)
+    bool xr = false;
+    std::vector<EngineState*> xr_st;          // [P] state of every rank (own / peer mapped / virtual)
+    std::vector<uint64_t*> xr_log;            // [P]
+    std::vector<void*> xr_owned;              // emulated: the virtual ranks' buffers (freed here)
+    std::vector<void*> xr_opened;             // real GPUs: IPC mappings of peers (closed here)
+    EngineState** d_xr_st = nullptr;
+    uint64_t** d_xr_log = nullptr;
+    uint32_t* d_xr_rows = nullptr;            // [2P] row_lo | row_hi
+    uint64_t* xr_log_of = nullptr;            // own log the peers were given (re-exchange on change)
+    unsigned long long xr_cap = 0;
+    int xr_depth = 0;
     void* comm_row = nullptr;                 // NCCL sub-communicators of the grid row / column
     void* comm_col = nullptr;
     uint32_t* d_stage = nullptr;              // 2-D block exchange staging
@@ -193,6 +205,9 @@ struct cfpq_result {
         dfree(d_small); dfree(d_Tn); dfree(d_rowcnt); dfree(d_rowoff);
         if (dense) dense_destroy(dense);
         dfree(d_stage);
+        for (void* q : xr_opened) cudaIpcCloseMemHandle(q);
+        for (void* q : xr_owned) cudaFree(q);
+        dfree(d_xr_st); dfree(d_xr_log); dfree(d_xr_rows);
         if (comm_row) nccl_comm_destroy(comm_row);
         if (comm_col) nccl_comm_destroy(comm_col);
         if (comm) nccl_comm_destroy(comm);
@@ -201,7 +216,7 @@ struct cfpq_result {
     // relational sparse runs on one GPU keep their results in the log only, so the closure
     // kernel can reset the bit words at the fixpoint (flags bit 2 disables, diagnostics)
     bool self_clear_ok() const {
-        return opts.semantics == 0 && !hashed && n_ranks == 1 && !comm && opts.path_policy < 2 &&
+        return opts.semantics == 0 && !hashed && ((n_ranks == 1 && !comm) || xr) && opts.path_policy < 2 &&
                (opts.diag_flags & 4) == 0;
     }
 
@@ -576,6 +591,11 @@ static cfpq_status plan(cfpq_result* r, const cfpq_grammar* g, const cfpq_graph*
             }
         }
     }
+    r->xr = o->exchange == 1 && r->n_ranks > 1 && o->path_policy < 2;
+    if (r->xr && r->n_ranks > kMaxXrRanks) {
+        set_error("cfpq_closure: the peer-memory exchange supports at most 32 ranks");
+        return CFPQ_E_UNSUPPORTED;
+    }
     const size_t mat_words = (size_t)r->rows_alloc * (size_t)r->Wp;
     int n_snap = 0;
     for (int A = 0; A < g->n_nt; ++A) n_snap += need_S[A] + need_ST[A];
@@ -597,7 +617,7 @@ static cfpq_status plan(cfpq_result* r, const cfpq_grammar* g, const cfpq_graph*
         CFPQ_CUDA_TRY(cudaMemGetInfo(&free_b, &total_b));
         want_hash = (double)mat_words * 4.0 * g->n_nt > 0.25 * (double)free_b;
     }
-    r->hashed = hash_ok && want_hash;
+    r->hashed = hash_ok && want_hash && !r->xr;
     if (!r->hashed) {
         if ((st = dalloc(&r->d_T, mat_words * g->n_nt, "T bit matrices")) != CFPQ_OK) return st;
         CFPQ_CUDA_TRY(cudaMemsetAsync(r->d_T, 0, mat_words * g->n_nt * 4, r->stream));
@@ -1346,6 +1366,196 @@ static cfpq_status run_sharded(cfpq_result* r) {
     return CFPQ_OK;
 }
 
+static cfpq_status run(cfpq_result* r, const cfpq_graph* d);
+
+// Peer pointers of every rank's log and state.  Emulated shards: the virtual ranks 1..P-1 get
+// their own logs and states here.  Real GPUs: the own log / state are exported as CUDA IPC
+// handles, all-gathered over NCCL, and the peers' mapped (NVLink peer access).
+static cfpq_status xr_setup(cfpq_result* r) {
+    const int P = r->n_ranks;
+    if (r->xr_log.size() == (size_t)P && r->xr_cap == r->log_cap && r->xr_log_of == r->d_log) return CFPQ_OK;
+    cudaStream_t s = r->stream;
+    CFPQ_CUDA_TRY(cudaStreamSynchronize(s));
+    for (void* q : r->xr_opened) cudaIpcCloseMemHandle(q);
+    for (void* q : r->xr_owned) cudaFree(q);
+    r->xr_opened.clear();
+    r->xr_owned.clear();
+    r->xr_st.assign(P, nullptr);
+    r->xr_log.assign(P, nullptr);
+    if (r->emulated) {
+        r->xr_st[0] = r->d_st;
+        r->xr_log[0] = r->d_log;
+        for (int q = 1; q < P; ++q) {
+            EngineState* sq = nullptr;
+            uint64_t* lq = nullptr;
+            cfpq_status st;
+            if ((st = dalloc(&sq, 1, "virtual rank state")) != CFPQ_OK) return st;
+            r->xr_owned.push_back(sq);
+            if ((st = dalloc(&lq, r->log_cap, "virtual rank log")) != CFPQ_OK) return st;
+            r->xr_owned.push_back(lq);
+            r->xr_st[q] = sq;
+            r->xr_log[q] = lq;
+        }
+    } else {
+        const int me = r->my_rank;
+        r->xr_st[me] = r->d_st;
+        r->xr_log[me] = r->d_log;
+        cudaIpcMemHandle_t hl, hs;
+        CFPQ_CUDA_TRY(cudaIpcGetMemHandle(&hl, r->d_log));
+        CFPQ_CUDA_TRY(cudaIpcGetMemHandle(&hs, r->d_st));
+        const size_t per = 2 * sizeof(cudaIpcMemHandle_t);   // 128 bytes = 16 uint64 per rank
+        const size_t slot = (per + 7) / 8;
+        if (r->xbuf_cap < (size_t)P * slot) {
+            dfree(r->d_xbuf);
+            r->xbuf_cap = 0;
+            cfpq_status st = dalloc(&r->d_xbuf, (size_t)P * slot, "handle exchange");
+            if (st != CFPQ_OK) return st;
+            r->xbuf_cap = (size_t)P * slot;
+        }
+        std::vector<unsigned char> mine(slot * 8, 0);
+        memcpy(mine.data(), &hl, sizeof(hl));
+        memcpy(mine.data() + sizeof(hl), &hs, sizeof(hs));
+        CFPQ_CUDA_TRY(cudaMemcpy(r->d_xbuf + (size_t)me * slot, mine.data(), slot * 8, cudaMemcpyHostToDevice));
+        std::string err;
+        if (!nccl_allgather_u64(r->comm, r->d_xbuf, slot, me, s, &err)) {
+            set_error(err);
+            return CFPQ_E_NCCL;
+        }
+        std::vector<unsigned char> all((size_t)P * slot * 8);
+        CFPQ_CUDA_TRY(cudaMemcpyAsync(all.data(), r->d_xbuf, all.size(), cudaMemcpyDeviceToHost, s));
+        CFPQ_CUDA_TRY(cudaStreamSynchronize(s));
+        for (int q = 0; q < P; ++q) {
+            if (q == me) continue;
+            cudaIpcMemHandle_t ql, qs;
+            memcpy(&ql, all.data() + (size_t)q * slot * 8, sizeof(ql));
+            memcpy(&qs, all.data() + (size_t)q * slot * 8 + sizeof(ql), sizeof(qs));
+            void *pl = nullptr, *ps = nullptr;
+            CFPQ_CUDA_TRY(cudaIpcOpenMemHandle(&pl, ql, cudaIpcMemLazyEnablePeerAccess));
+            r->xr_opened.push_back(pl);
+            CFPQ_CUDA_TRY(cudaIpcOpenMemHandle(&ps, qs, cudaIpcMemLazyEnablePeerAccess));
+            r->xr_opened.push_back(ps);
+            r->xr_log[q] = (uint64_t*)pl;
+            r->xr_st[q] = (EngineState*)ps;
+        }
+    }
+    if (!r->d_xr_st) {
+        cfpq_status st;
+        if ((st = dalloc(&r->d_xr_st, (size_t)P, "peer states")) != CFPQ_OK) return st;
+        if ((st = dalloc(&r->d_xr_log, (size_t)P, "peer logs")) != CFPQ_OK) return st;
+        if ((st = dalloc(&r->d_xr_rows, (size_t)2 * P, "rank rows")) != CFPQ_OK) return st;
+        std::vector<uint32_t> rows(2 * P);
+        for (int g = 0; g < P; ++g) {
+            int64_t tlo, thi, br;
+            dense_partition(r->n, P, g, &tlo, &thi, &br);
+            rows[g] = (uint32_t)std::min<int64_t>(tlo * 128, r->n);
+            rows[P + g] = (uint32_t)std::min<int64_t>(thi * 128, r->n);
+        }
+        CFPQ_CUDA_TRY(cudaMemcpy(r->d_xr_rows, rows.data(), rows.size() * 4, cudaMemcpyHostToDevice));
+    }
+    CFPQ_CUDA_TRY(cudaMemcpy(r->d_xr_st, r->xr_st.data(), P * sizeof(void*), cudaMemcpyHostToDevice));
+    CFPQ_CUDA_TRY(cudaMemcpy(r->d_xr_log, r->xr_log.data(), P * sizeof(void*), cudaMemcpyHostToDevice));
+    r->xr_cap = r->log_cap;
+    r->xr_log_of = r->d_log;
+    return CFPQ_OK;
+}
+
+// The row-sharded sparse engine with the device-resident peer-memory exchange (§3.5).
+static cfpq_status run_xr(cfpq_result* r, const cfpq_graph* d) {
+    cudaStream_t s = r->stream;
+    const int P = r->n_ranks;
+    CFPQ_CUDA_TRY(cudaMemcpyAsync(&r->h_st, r->d_st, sizeof(EngineState), cudaMemcpyDeviceToHost, s));
+    CFPQ_CUDA_TRY(cudaStreamSynchronize(s));
+    if (r->h_st.bad_edge) {
+        r->n_cells = std::min<unsigned long long>(r->h_st.log_size, r->log_cap);
+        set_error("graph has an edge with a node id >= n_nodes or a label id >= n_labels");
+        return CFPQ_E_INVAL;
+    }
+    cfpq_status st = xr_setup(r);
+    if (st != CFPQ_OK) return st;
+    const unsigned long long n_seed = r->h_st.log_size;
+    if (r->emulated) {
+        // every virtual rank starts from the same Δ_0 (every rank seeds every cell)
+        for (int q = 1; q < P; ++q) {
+            CFPQ_CUDA_TRY(cudaMemcpyAsync(r->xr_st[q], r->d_st, sizeof(EngineState), cudaMemcpyDeviceToDevice, s));
+            if (n_seed)
+                CFPQ_CUDA_TRY(cudaMemcpyAsync(r->xr_log[q], r->d_log, n_seed * 8, cudaMemcpyDeviceToDevice, s));
+        }
+    } else if (r->comm) {
+        // the peers must have seeded (and zeroed their barrier words) before anyone appends
+        std::string err;
+        if (!nccl_allreduce_sum_u64(r->comm, (unsigned long long*)r->d_xbuf, 1, s, &err)) {
+            set_error(err);
+            return CFPQ_E_NCCL;
+        }
+    }
+    XrParams x{};
+    x.P = P;
+    x.my_rank = r->emulated ? -1 : r->my_rank;
+    x.cpr = r->emulated ? std::max(1, r->grid / P) : r->grid;
+    x.st = r->d_xr_st;
+    x.log = r->d_xr_log;
+    x.row_lo = r->d_xr_rows;
+    x.row_hi = r->d_xr_rows + P;
+    EngineParams p = r->params();
+    p.self_clear = r->self_clear_ok() ? 1 : 0;
+    const int grid = r->emulated ? x.cpr * P : r->grid;
+    CFPQ_CUDA_TRY(launch_xr_closure(p, x, grid, s));
+    CFPQ_CUDA_TRY(cudaEventRecord(r->ev[3], s));
+    r->launches++;
+    CFPQ_CUDA_TRY(cudaMemcpyAsync(&r->h_st, r->d_st, sizeof(EngineState), cudaMemcpyDeviceToHost, s));
+    CFPQ_CUDA_TRY(cudaStreamSynchronize(s));
+    {
+        float ms = 0;
+        CFPQ_CUDA_TRY(cudaEventElapsedTime(&ms, r->ev[0], r->ev[1]));
+        r->seed_ns = ms * 1e6;
+        CFPQ_CUDA_TRY(cudaEventElapsedTime(&ms, r->ev[1], r->ev[3]));
+        r->loop_ns = ms * 1e6;
+    }
+    r->n_cells = std::min<unsigned long long>(r->h_st.log_size, r->log_cap);
+    if (r->h_st.status == ST_OVERFLOW) {
+        // some rank's log ran out: every rank saw it in the same iteration.  Grow every log,
+        // clear the matrices and run the closure again from the seeds.
+        if (r->xr_depth > 8) {
+            set_error("peer-memory exchange: the logs kept overflowing");
+            return CFPQ_E_NOMEM;
+        }
+        const unsigned long long want = std::max<unsigned long long>(2 * r->log_cap, r->h_st.log_size + 1024);
+        uint64_t* nl = nullptr;
+        if ((st = dalloc(&nl, want, "cell log (grow)")) != CFPQ_OK) return st;
+        CFPQ_CUDA_TRY(cudaMemsetAsync(nl, 0, want * 8, s));
+        dfree(r->d_log);
+        r->d_log = nl;
+        r->log_cap = want;
+        r->opts.log_capacity = (int64_t)want;
+        const size_t mw = (size_t)r->rows_alloc * (size_t)r->Wp;
+        CFPQ_CUDA_TRY(cudaMemsetAsync(r->d_T, 0, mw * r->n_nt * 4, s));
+        r->n_cells = 0;
+        r->t_clean = false;
+        r->ran = false;
+        r->regrows++;
+        ++r->xr_depth;
+        st = run(r, d);
+        --r->xr_depth;
+        return st;
+    }
+    if (r->h_st.status == ST_TIMEOUT) {
+        set_error("peer-memory exchange: a rank did not reach the iteration barrier (watchdog)");
+        return CFPQ_E_NCCL;
+    }
+    r->iterations = r->h_st.iter;
+    r->t_clean = r->self_clear_ok() && (r->h_st.status == ST_DONE || r->h_st.status == ST_CAP);
+    if (r->h_st.status == ST_CAP) {
+        set_error("max_iterations reached before the fixpoint");
+        return CFPQ_E_NOT_CONVERGED;
+    }
+    if (r->h_st.status != ST_DONE) {
+        set_error("peer-memory closure stopped without reaching the fixpoint (status " +
+                  std::to_string(r->h_st.status) + ")");
+        return CFPQ_E_CUDA;
+    }
+    return CFPQ_OK;
+}
+
 static cfpq_status run(cfpq_result* r, const cfpq_graph* d) {
     cudaStream_t s = r->stream;
     r->clr_active = false;
@@ -1487,6 +1697,7 @@ static cfpq_status run(cfpq_result* r, const cfpq_graph* d) {
     CFPQ_CUDA_TRY(cudaEventRecord(r->ev[1], s));
     if (r->opts.path_policy == 2 || r->opts.path_policy == 3) return run_dense(r, 0);
     if (async) return run_async(r, seeds_upper);
+    if (r->xr) return run_xr(r, d);
     if (r->n_ranks > 1 || r->comm) return run_sharded(r);
     // a2-a5: the fixpoint loop, device-resident
     bool first = true;
@@ -1620,6 +1831,7 @@ static cfpq_status check_inputs(const cfpq_grammar* g, const cfpq_graph* d, cons
         }
     }
     CFPQ_CHECK_ARG(o->dense_launch >= 0 && o->dense_launch <= 3, "cfpq_closure: dense_launch must be 0..3");
+    CFPQ_CHECK_ARG(o->exchange == 0 || o->exchange == 1, "cfpq_closure: exchange must be 0 or 1");
     CFPQ_CHECK_ARG(o->cell_set >= 0 && o->cell_set <= 2, "cfpq_closure: cell_set must be 0, 1 or 2");
     CFPQ_CHECK_ARG(o->tensor_format >= 0 && o->tensor_format <= 2, "cfpq_closure: tensor_format must be 0, 1 or 2");
     return CFPQ_OK;
@@ -1651,7 +1863,8 @@ extern "C" cfpq_status cfpq_closure_reuse(const cfpq_grammar* g, const cfpq_grap
     CFPQ_CHECK_ARG(d->n_nodes == r->n && g->n_nt == r->n_nt && g->n_labels == r->n_labels &&
                        g->rules.size() == r->rules.size() && o->semantics == r->opts.semantics &&
                        o->account_work == r->opts.account_work && o->path_policy == r->opts.path_policy &&
-                       o->cell_set == r->opts.cell_set && o->tensor_format == r->opts.tensor_format,
+                       o->cell_set == r->opts.cell_set && o->tensor_format == r->opts.tensor_format &&
+                       o->exchange == r->opts.exchange,
                    "cfpq_closure_reuse: grammar/graph/options differ from the result's plan");
     for (size_t k = 0; k < g->rules.size(); ++k)
         CFPQ_CHECK_ARG(g->rules[k].A == r->rules[k].A && g->rules[k].B == r->rules[k].B && g->rules[k].C == r->rules[k].C,

@@ -100,12 +100,28 @@ struct EngineState {
     // Gauss-Seidel schedule: gs_ring[t mod (S+1)] = L_t, the log size when step t starts
     // (L_1 = |Δ_0|); step t expands log[L_{t-S}, L_t) through the rules of stage (t-1) mod S
     unsigned long long gs_ring[kMaxStages + 1];
+    unsigned long long xbar;       // peer-memory exchange: arrivals of every rank's last CTA
     int gs_stage;                  // stage of the next step ((k) mod S after step k closed)
     int gs_slot;                   // ring slot of L_{k+1} ((k+1) mod (S+1))
     long long gs_round;            // rounds completed (k / S)
 };
 
-enum : int { ST_RUNNING = 0, ST_DONE = 1, ST_OVERFLOW = 2, ST_CAP = 3, ST_LEN_OVERFLOW = 4, ST_SWITCH = 5 };
+enum : int { ST_RUNNING = 0, ST_DONE = 1, ST_OVERFLOW = 2, ST_CAP = 3, ST_LEN_OVERFLOW = 4, ST_SWITCH = 5,
+              ST_TIMEOUT = 6 };
+
+// Peer-memory exchange of the row-sharded sparse engine (exchange = 1): every rank's engine
+// state and log, reachable from every rank (NVLink peer mappings on real GPUs; plain device
+// pointers of the virtual ranks of an emulated launch).
+constexpr int kMaxXrRanks = 32;
+struct XrParams {
+    int32_t P;                     // ranks
+    int32_t my_rank;               // >= 0: one launch per GPU; -1: emulated, rank = blockIdx.x / cpr
+    int32_t cpr;                   // CTAs per rank
+    EngineState* const* st;        // [P]
+    uint64_t* const* log;          // [P]
+    const uint32_t* row_lo;        // [P] rows each rank derives
+    const uint32_t* row_hi;
+};
 
 struct EngineParams {
     int32_t n;
@@ -219,6 +235,7 @@ cudaError_t launch_seed_snapshots(const EngineParams& p, unsigned long long n_se
 int closure_kernel_blocks_per_sm();
 int closure_kernel_block_size();
 cudaError_t launch_closure(const EngineParams& p, int grid, cudaStream_t s);
+cudaError_t launch_xr_closure(const EngineParams& p, const XrParams& x, int grid, cudaStream_t s);
 
 cudaError_t launch_nt_histogram(const uint64_t* log, unsigned long long n, unsigned long long* counts, int n_nt,
                                 cudaStream_t s);

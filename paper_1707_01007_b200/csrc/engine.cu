@@ -74,7 +74,20 @@ struct Sink {
     uint64_t* mirror;
     unsigned long long mirror_base;
     unsigned long long mirror_cap;
+    // peer-memory exchange (xr_P > 0): every append goes to every rank's log
+    int32_t xr_P;
+    EngineState* const* xr_st;
+    uint64_t* const* xr_log;
 };
+
+// Peer-memory exchange: reserve nb entries in rank q's log (system scope: q may be another GPU).
+__device__ __forceinline__ unsigned long long xr_reserve(const Sink& sk, int q, unsigned long long nb) {
+    return atomicAdd_system(&sk.xr_st[q]->log_size, nb);
+}
+// Every rank learns of an overflow (the run is restarted with larger logs).
+__device__ __forceinline__ void xr_flag_overflow(const Sink& sk) {
+    for (int q = 0; q < sk.xr_P; ++q) *(volatile int*)&sk.xr_st[q]->overflow = 1;
+}
 
 struct __align__(16) WarpScratch {
     uint64_t buf[kBuf];   // staged new cells
@@ -229,6 +242,24 @@ __device__ __forceinline__ void flush(const EngineParams& p, const NTInfo* nt, c
                                       int lane) {
     int nb = ws->nbuf;
     if (nb == 0) return;
+    if (sk.xr_P) {
+        // peer-memory exchange: the warp's cells into every rank's log (relational only)
+        for (int q = 0; q < sk.xr_P; ++q) {
+            unsigned long long base = 0;
+            if (lane == 0) base = xr_reserve(sk, q, (unsigned long long)nb);
+            base = __shfl_sync(kFull, base, 0);
+            uint64_t* lg = sk.xr_log[q];
+            for (int t = lane; t < nb; t += 32) {
+                const unsigned long long idx = base + (unsigned long long)t;
+                if (idx < p.log_cap) lg[idx] = ws->buf[t];
+                else xr_flag_overflow(sk);
+            }
+        }
+        __syncwarp();
+        if (lane == 0) ws->nbuf = 0;
+        __syncwarp();
+        return;
+    }
     unsigned long long base = 0;
     if (lane == 0) base = atomicAdd(sk.counter, (unsigned long long)nb);
     base = __shfl_sync(kFull, base, 0);
@@ -297,12 +328,50 @@ __device__ __forceinline__ Sink global_sink(const EngineParams& p) {
     sk.mirror = nullptr;
     sk.mirror_base = 0;
     sk.mirror_cap = 0;
+    sk.xr_P = 0;
+    sk.xr_st = nullptr;
+    sk.xr_log = nullptr;
     return sk;
 }
 
 // End of a grid-wide expansion: the CTA appends all warps' staged cells with ONE global
 // atomic (thousands of warps ending the iteration together would otherwise serialise on
 // the log counter).
+// Peer-memory exchange variant: one reservation per rank's log per CTA (warp 0, lane q),
+// then every warp writes its cells into every rank's log.
+template <int NW>
+__device__ void cta_flush_xr(const EngineParams& p, const Sink& sk, WarpScratch* ws_all, int wib, int lane,
+                             unsigned long long* s_bases, int32_t* s_prefix) {
+    __syncthreads();
+    if (wib == 0) {
+        int nb = lane < NW ? ws_all[lane].nbuf : 0;
+        int incl = nb;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            int v = __shfl_up_sync(kFull, incl, o);
+            if (lane >= o) incl += v;
+        }
+        if (lane < NW) s_prefix[lane] = incl - nb;
+        const int tot = __shfl_sync(kFull, incl, 31);
+        if (lane < sk.xr_P) s_bases[lane] = tot ? xr_reserve(sk, lane, (unsigned long long)tot) : 0ull;
+    }
+    __syncthreads();
+    WarpScratch* ws = &ws_all[wib];
+    const int nb = ws->nbuf;
+    for (int q = 0; q < sk.xr_P; ++q) {
+        const unsigned long long base = s_bases[q] + (unsigned long long)s_prefix[wib];
+        uint64_t* lg = sk.xr_log[q];
+        for (int t = lane; t < nb; t += 32) {
+            const unsigned long long idx = base + (unsigned long long)t;
+            if (idx < p.log_cap) lg[idx] = ws->buf[t];
+            else xr_flag_overflow(sk);
+        }
+    }
+    __syncwarp();
+    if (lane == 0) ws->nbuf = 0;
+    __syncwarp();
+}
+
 template <int NW>
 __device__ void cta_flush_n(const EngineParams& p, const NTInfo* nt, const Sink& sk, WarpScratch* ws_all, int wib,
                             int lane, unsigned long long* s_base, int32_t* s_prefix) {
@@ -594,6 +663,8 @@ __device__ __forceinline__ void expand_chunk(const EngineParams& p, const NTInfo
         if (x < nexp) {
             Expansion ex = exps[eb + x];
             if (!stage_ok(p, ex, gstage)) continue;
+            // row shards: an L expansion derives cells in the entry's row only
+            if (ex.kind == EXP_L_CONST && (ci < p.row_lo || ci >= p.row_hi)) continue;
             if (ex.kind == EXP_L_CONST || ex.kind == EXP_R_CONST) el[x] = load_head(nt, ex, ci, cj, eA[x], efx[x]);
             else var_mask |= 1u << x;
         }
@@ -654,7 +725,7 @@ __device__ __forceinline__ void expand_chunk(const EngineParams& p, const NTInfo
         uint32_t A = 0, fx = 0;
         if (x < nexp) {
             Expansion ex = exps[eb + x];
-            if (!stage_ok(p, ex, gstage)) {
+            if (!stage_ok(p, ex, gstage) || (ex.kind == EXP_L_CONST && (ci < p.row_lo || ci >= p.row_hi))) {
             } else if (ex.kind == EXP_L_CONST || ex.kind == EXP_R_CONST) {
                 h = load_head(nt, ex, ci, cj, A, fx);
             } else if (x < 32) {
@@ -1588,6 +1659,150 @@ __global__ void __launch_bounds__(kBlock, 1) closure_kernel(EngineParams p) {
     }
 }
 
+// ------------------------------------------------------------------------------------------
+// Row-sharded sparse engine with a device-resident peer-memory exchange (exchange = 1; §8(e),
+// P:572).  Each rank runs this persistent kernel over the whole fixpoint: it expands all of
+// Δ_{k-1} (its own copy in its own log), inserts only the cells of its rows, and appends every
+// new cell to EVERY rank's log (system-scope reservations and stores; NVLink peer mappings on
+// real GPUs), so the exchange overlaps the expansion instead of following it.  Iteration end:
+// the rank's CTAs meet at a rank-local barrier whose last CTA fences system-wide, arrives on
+// every rank's cross counter (xbar) and waits for all P arrivals of this iteration; after that
+// its own log holds Δ_k of every rank (the same set on every rank), and it releases its CTAs
+// with the log size.  An emulated launch runs P virtual ranks as CTA groups of one grid.
+// ------------------------------------------------------------------------------------------
+__device__ bool xr_barrier(const EngineParams& p, const XrParams& x, long long k, unsigned long long* word) {
+    __shared__ int s_timeout;
+    __threadfence_system();   // this CTA's appends to peer logs are visible system-wide first
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        s_timeout = 0;
+        EngineState* st = p.st;
+        const unsigned long long my = ld_volatile_u64(&st->bar_word) >> kBarGenShift;
+        const unsigned arrived = atom_add_acq_rel(&st->bar_count, 1u);
+        unsigned long long w;
+        if (arrived == (unsigned)p.nblocks - 1u) {
+            __threadfence_system();
+            for (int q = 0; q < x.P; ++q) atomicAdd_system(&x.st[q]->xbar, 1ull);
+            const unsigned long long want = (unsigned long long)x.P * (unsigned long long)k;
+            long long t0 = clock64();
+            unsigned ns = 0;
+            while (ld_volatile_u64(&st->xbar) < want) {
+                if (ns) __nanosleep(ns);
+                if (clock64() - t0 > 40000) ns = ns ? (ns < 1024u ? ns * 2u : 1024u) : 64u;
+                if (clock64() - t0 > 60000000000ll) {
+                    s_timeout = 1;
+                    break;
+                }
+            }
+            __threadfence_system();
+            w = bar_release_word(st, my, k);
+            st->bar_count = 0u;
+            st_release_word(&st->bar_word, w);
+        } else {
+            long long t0 = clock64();
+            unsigned ns = 0;
+            while (((w = ld_acquire_word(&st->bar_word)) >> kBarGenShift) == my) {
+                if (ns) __nanosleep(ns);
+                if (clock64() - t0 > 40000) ns = ns ? (ns < 2048u ? ns * 2u : 2048u) : 64u;
+                if (clock64() - t0 > 60000000000ll) {
+                    s_timeout = 1;
+                    break;
+                }
+            }
+        }
+        *word = w;
+    }
+    __syncthreads();
+    return s_timeout == 0;
+}
+
+__global__ void __launch_bounds__(kBlock, 1) xr_closure_kernel(EngineParams p0, XrParams x) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    ClosureShared& S = *reinterpret_cast<ClosureShared*>(smem_raw);
+    __shared__ unsigned long long s_bases[kMaxXrRanks];
+    const int lane = threadIdx.x & 31;
+    const int wib = threadIdx.x >> 5;
+    const int rank = x.my_rank >= 0 ? x.my_rank : (int)blockIdx.x / x.cpr;
+    const int lb = x.my_rank >= 0 ? (int)blockIdx.x : (int)blockIdx.x % x.cpr;
+    EngineParams p = p0;
+    p.st = x.st[rank];
+    p.log = x.log[rank];
+    p.row_lo = x.row_lo[rank];
+    p.row_hi = x.row_hi[rank];
+    p.nblocks = x.cpr;
+    EngineState* st = p.st;
+    const bool small = p.n_nt <= kSmemNT && p.n_exps <= kSmemExp;
+    if (small) {
+        for (int t = threadIdx.x; t < p.n_nt; t += kBlock) S.nt[t] = p.nt[t];
+        for (int t = threadIdx.x; t < p.n_exps; t += kBlock) S.exp[t] = p.exps[t];
+    }
+    const NTInfo* nt = small ? S.nt : p.nt;
+    const Expansion* exps = small ? S.exp : p.exps;
+    Sink sk = global_sink(p);
+    sk.xr_P = x.P;
+    sk.xr_st = x.st;
+    sk.xr_log = x.log;
+    if (lane == 0) S.ws[wib].nbuf = 0;
+    if (threadIdx.x == 0) {
+        S.state.lo = ld_volatile_u64(&st->lo);
+        S.state.hi = ld_volatile_u64(&st->hi);
+        S.state.iter = *(volatile long long*)&st->iter;
+        S.state.status = *(volatile int*)&st->status;
+        S.state.gs_stage = 0;
+        S.state.gs_slot = 1;
+        S.state.gs_round = 0;
+    }
+    __syncthreads();
+    LoopState s = S.state;
+    __syncthreads();
+    unsigned long long dcand = 0, dexp = 0;
+    bool aborted = false;
+    while (s.status == ST_RUNNING) {
+        const long long k = s.iter + 1;
+        expand(p, nt, exps, sk, nullptr, s.lo, s.hi, k, 0, lb * kWarps + wib, x.cpr * kWarps, lane, &S.ws[wib], dcand,
+               dexp, false);
+        cta_flush_xr<kWarps>(p, sk, S.ws, wib, lane, s_bases, S.flush_prefix);
+        unsigned long long bw = 0;
+        if (!xr_barrier(p, x, k, &bw)) {
+            aborted = true;
+            break;
+        }
+        if (threadIdx.x == 0) {
+            LoopState t = s;
+            close_iteration(p, k, t, bw & kBarLsMask, (int)((bw >> 38) & 3ull), lb == 0);
+            S.state = t;
+        }
+        __syncthreads();
+        s = S.state;
+        __syncthreads();
+    }
+    if (lb == 0 && threadIdx.x == 0) {
+        if (aborted) s.status = ST_TIMEOUT;
+        publish(p, s);
+    }
+    if (!aborted && p.self_clear && (s.status == ST_DONE || s.status == ST_CAP)) {
+        // reset the bit words of the cells of this rank's rows (the relations stay in the log)
+        __syncthreads();
+        const unsigned long long n_cells = s.hi;
+        for (unsigned long long e = (unsigned long long)lb * kBlock + threadIdx.x; e < n_cells;
+             e += (unsigned long long)x.cpr * kBlock) {
+            const uint64_t c = ldcg64(p.log + e);
+            const uint32_t i = cell_i(c);
+            if (i < p.row_lo || i >= p.row_hi) continue;
+            zero_sector(nt[cell_nt(c)].T + (size_t)i * p.Wp + (cell_j(c) >> 5));
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        dcand += __shfl_xor_sync(kFull, dcand, o);
+        dexp += __shfl_xor_sync(kFull, dexp, o);
+    }
+    if (lane == 0) {
+        if (dcand) atomicAdd(&st->candidates, dcand);
+        if (dexp) atomicAdd(&st->expansions, dexp);
+    }
+}
+
 static int grid_for(int64_t work, int block);
 size_t closure_kernel_smem() { return sizeof(ClosureShared); }
 
@@ -1824,6 +2039,14 @@ int closure_kernel_blocks_per_sm() {
         return 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, closure_kernel, kBlock, smem) != cudaSuccess) return 0;
     return nb;
+}
+
+cudaError_t launch_xr_closure(const EngineParams& p, const XrParams& x, int grid, cudaStream_t s) {
+    const size_t smem = sizeof(ClosureShared);
+    cudaError_t c = cudaFuncSetAttribute(xr_closure_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (c != cudaSuccess) return c;
+    void* args[] = {(void*)&p, (void*)&x};
+    return cudaLaunchCooperativeKernel((const void*)xr_closure_kernel, dim3(grid), dim3(kBlock), args, smem, s);
 }
 
 cudaError_t launch_closure(const EngineParams& p, int grid, cudaStream_t s) {

@@ -30,6 +30,9 @@ variants = {
     "rows_rg3": dict(path_policy=3, flags=3 << 4),
     "rows_rg4": dict(path_policy=3, flags=4 << 4),
     "warp_flush": dict(cell_set=1, flags=8),
+    "xr2_peer": dict(emulate_ranks=2, exchange=1),
+    "xr8_peer": dict(emulate_ranks=8, exchange=1),
+    "shard8_hostloop": dict(emulate_ranks=8),
     "ctas111": dict(cell_set=1, max_ctas=111),
     "ctas74": dict(cell_set=1, max_ctas=74),
     "ctas37": dict(cell_set=1, max_ctas=37),

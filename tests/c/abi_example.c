@@ -27,7 +27,7 @@ int main(int argc, char** argv) {
         FIELD(nccl_unique_id); FIELD(log_capacity); FIELD(solo_threshold); FIELD(record_times);
         FIELD(max_ctas); FIELD(reserved_emulate); FIELD(cell_set); FIELD(tensor_format);
         FIELD(dense_launch); FIELD(diag_flags); FIELD(grid_rows); FIELD(grid_cols);
-        FIELD(rows_list_capacity);
+        FIELD(rows_list_capacity); FIELD(exchange);
         return 0;
     }
     /* G': S=0, S1..S6 = 1..6; labels subClassOf_r=0, subClassOf=1, type_r=2, type=3 */

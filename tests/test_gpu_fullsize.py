@@ -121,3 +121,10 @@ def test_gauss_seidel_schedule(n):
     gd, w, r = _run(n, schedule=3)
     _check(gd, w, r, per_iteration=False, iterations=False)
     assert r.iterations < gd["iterations"]
+
+
+@pytest.mark.parametrize("n", SIZES)
+def test_sparse_peer_exchange_8_virtual_ranks(n):
+    """exchange = 1 (peer-memory exchange) with 8 virtual ranks at full size."""
+    gd, w, r = _run(n, emulate_ranks=8, exchange=1)
+    _check(gd, w, r)

@@ -78,3 +78,48 @@ def test_sparse_sharding_rejections():
     with pytest.raises(C.CfpqError) as e:
         gpu_closure(I.anbn_workload(2, 3), emulate_ranks=2, semantics=1)   # lengths
     assert e.value.status == C.CFPQ_E_UNSUPPORTED
+
+
+@pytest.mark.parametrize("ranks", [2, 3, 8])
+def test_sparse_peer_exchange_emulated(ranks):
+    """exchange = 1: the device-resident peer-memory exchange (one persistent kernel; every new
+    cell appended to every rank's log, a cross-rank barrier per iteration), emulated as CTA
+    groups of one launch with their own logs and states.  Jacobi states per iteration."""
+    for w in (I.ontology_workload("q1", 700, depth=7, seed=ranks), I.ontology_workload("q2", 500, depth=6, seed=1),
+              I.ontology_workload("union", 900, depth=6, seed=ranks + 10), I.anbn_workload(3, 7),
+              I.example_workload(), I.config4_workload(n=3000, seed=ranks)):
+        ores = O.run(w)
+        r, _, _ = gpu_closure(w, emulate_ranks=ranks, exchange=1)
+        _check(w, r, ores)
+
+
+def test_sparse_peer_exchange_overflow_and_reuse():
+    """A log overflow is seen by every rank in the same iteration; the logs grow and the closure
+    restarts from the seeds; a reuse runs again on the cleared matrices."""
+    from paper_1707_01007_b200 import cfpq as C
+    w = I.ontology_workload("union", 700, depth=6, seed=5)
+    ores = O.run(w)
+    r, _, _ = gpu_closure(w, emulate_ranks=4, exchange=1, log_capacity=64)
+    assert r.stats()["regrows"] > 0
+    _check(w, r, ores)
+    g, d = C.Grammar.from_workload(w), C.Graph(w.n_nodes, w.edges)
+    r = C.closure(g, d, emulate_ranks=4, exchange=1)
+    _check(w, r, ores)
+    w2 = I.ontology_workload("union", 700, depth=6, seed=6)
+    d.set_edges(w2.edges)
+    C.closure_reuse(g, d, r, emulate_ranks=4, exchange=1)
+    _check(w2, r, O.run(w2))
+
+
+def test_sparse_peer_exchange_random_grammars():
+    done = 0
+    for s in range(120):
+        w = I.random_workload(81_000 + s, max_nodes=80, max_edges=240, max_nt=6, max_bin=10, max_term=5)
+        try:
+            r, _, _ = gpu_closure(w, emulate_ranks=2 + s % 4, exchange=1)
+        except Exception as e:             # var x var rules need the dense engine
+            assert "sharding" in str(e)
+            continue
+        _check(w, r, O.run(w))
+        done += 1
+    assert done >= 20
