@@ -609,6 +609,8 @@ def main():
     ap.add_argument("--solo", type=int, default=-1)
     ap.add_argument("--replicas", action="store_true",
                     help="N>1, config4/configS: headline = N independent problems (weak) instead of ONE sharded problem")
+    ap.add_argument("--exchange", type=int, default=1, choices=[0, 1],
+                    help="sharded config4: 1 device-resident peer-memory exchange (default), 0 NCCL host loop")
     ap.add_argument("--force-sharded", action="store_true",
                     help="testing: take the N>1 code path (NCCL communicator, sharded engines, supplements) "
                          "even with one process")
@@ -646,6 +648,8 @@ def main():
             uid.copy_(torch.tensor(list(C.nccl_unique_id()), dtype=torch.uint8))
         dist.broadcast(uid, src=0)
         shard_kw = {"world_size": world, "rank": rank, "nccl_unique_id": bytes(uid.cpu().tolist())}
+        if args.workload == "config4":
+            shard_kw["exchange"] = args.exchange
     lengths = args.workload == "config5"
     g = C.Grammar.from_workload(w)
     edges_dev = torch.from_numpy(w.edges).cuda()
@@ -662,7 +666,22 @@ def main():
     useful = jac if pol == 2 else 2 * int(r0.stats()["candidates"])
     del r0
 
-    r = C.closure(g, d, **kw, **shard_kw)
+    exchange_note = None
+    try:
+        r = C.closure(g, d, **kw, **shard_kw)
+    except C.CfpqError as ex:
+        if shard_kw.get("exchange") != 1:
+            raise
+        # the peer-memory path could not map the peers (e.g. no CUDA IPC between these
+        # processes): fall back to the NCCL host loop, and say so in the line
+        exchange_note = "peer-memory exchange failed (%s); NCCL host loop used" % str(ex)[:200]
+        shard_kw["exchange"] = 0
+        uid = torch.zeros(128, dtype=torch.uint8, device="cuda")
+        if rank == 0:
+            uid.copy_(torch.tensor(list(C.nccl_unique_id()), dtype=torch.uint8))
+        dist.broadcast(uid, src=0)
+        shard_kw["nccl_unique_id"] = bytes(uid.cpu().tolist())
+        r = C.closure(g, d, **kw, **shard_kw)
     iterations = r.iterations
     cells = r.stats()["cells"]
     cells_total = sum(r.count(A) for A in range(w.n_nt)) if pol == 2 else cells
@@ -812,10 +831,15 @@ def main():
                            "candidates_per_step": int(statistics.median(cands)) if cands else None,
                            "schedule": {0: "jacobi", 3: "gauss-seidel"}[args.schedule],
                            "l2": "flushed between steps (512 MiB write outside the timed events)",
-                           "parallelism": (f"ONE problem row-block sharded over {world} GPUs (NCCL all-gather per "
-                                           "iteration" + (": Δ index lists)" if pol != 2 else ": dense row blocks)")
+                           "parallelism": (("ONE problem row-block sharded over %d GPUs: %s" % (world, (
+                                               "Δ cells appended to every rank's log over NVLink peer memory inside "
+                                               "one persistent kernel per GPU, cross-GPU barrier per iteration"
+                                               if shard_kw.get("exchange") == 1 else
+                                               "NCCL all-gather per iteration of "
+                                               + ("Δ index lists" if pol != 2 else "dense row blocks"))))
                                            if sharded else f"{world} independent replicas (seed+rank)")
                            if world > 1 else "1 GPU",
+                           "exchange_note": exchange_note,
                            "engine": ("dense tcgen05 int8 (kind::i8)" if args.tensor_format == 1 else
                                       "dense tcgen05 fp4 (kind::mxf4)") + ", CTA pairs" if pol == 2 else
                                      "sparse semi-naive persistent kernel",

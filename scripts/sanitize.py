@@ -1,6 +1,7 @@
 """Small closures on every engine, for compute-sanitizer (memcheck / racecheck / synccheck):
-sparse, hashed, sharded, async, tensor (fp4 and int8, 2-SM pairs by default; CFPQ_DENSE_2SM=0 /
-CFPQ_DENSE_PAIR=1 for the other variants), bit rows (forms L, R, V, P)."""
+sparse, hashed, sharded (NCCL-style host loop and peer-memory exchange), async, Gauss-Seidel,
+tensor (fp4 and int8; CTA pairs by default, dense_launch 2 / 3 for the other variants; 2-D
+grids), bit rows (forms L, R, V, P; row shards; list and chunk overflow)."""
 import sys, os
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
@@ -33,7 +34,18 @@ cases = [(I.example_workload(), dict()), (I.example_workload(), dict(semantics=1
          (I.ontology_workload("union", 300, depth=5, seed=2), dict(cell_set=2)),
          (I.ontology_workload("union", 300, depth=5, seed=2), dict(cell_set=2, log_capacity=64)),
          (I.ontology_workload("union", 300, depth=5, seed=3), dict(emulate_ranks=3)),
-         (I.ontology_workload("q1", 200, depth=5, seed=4), dict(schedule=2))]
+         (I.ontology_workload("q1", 200, depth=5, seed=4), dict(schedule=2)),
+         (I.ontology_workload("union", 300, depth=5, seed=8), dict(schedule=3)),
+         (I.anbn_workload(3, 5), dict(schedule=3)),
+         (I.dense_stress_workload(150, 2), dict(schedule=3)),
+         (I.ontology_workload("union", 300, depth=5, seed=9), dict(emulate_ranks=3, exchange=1)),
+         (I.ontology_workload("union", 300, depth=5, seed=9), dict(emulate_ranks=4, exchange=1, log_capacity=64)),
+         (I.ontology_workload("union", 300, depth=5, seed=10), dict(path_policy=3, emulate_ranks=3)),
+         (I.ontology_workload("union", 300, depth=5, seed=10), dict(path_policy=3, rows_list_capacity=8)),
+         (I.ontology_workload("union", 300, depth=5, seed=10), dict(path_policy=3, emulate_ranks=2, rows_list_capacity=8)),
+         (I.dense_stress_workload(150, 2), dict(path_policy=2, emulate_ranks=4, grid=(2, 2))),
+         (I.dense_stress_workload(150, 2), dict(path_policy=2, tensor_format=1, dense_launch=2)),
+         (I.dense_stress_workload(150, 2), dict(path_policy=2, tensor_format=1, dense_launch=3))]
 for w, kw in cases:
     run(w, **kw)
     print("ok", w.name, kw, flush=True)
