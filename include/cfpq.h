@@ -158,7 +158,10 @@ typedef struct {
                                 atomic, bit 1 clear the other workspace bank on a side
                                 stream, bit 2 no reset of the bit words at the fixpoint,
                                 bit 3 per-warp log appends instead of the CTA-level flush,
-                                bits 4-6 bit-row R-form kernel variant (0 = default)          */
+                                bits 4-6 bit-row R-form kernel variant (0 = default), bit 7
+                                reset the bit words at the fixpoint instead of rotating two
+                                workspace banks (the default clears the other bank inside
+                                the next closure, during its grid-barrier waits)              */
     int32_t grid_rows;       /* tensor engine, world_size (or reserved_emulate) > 1: 2-D
                                 process grid grid_rows x grid_cols (SUMMA-style blocks
                                 (I_a, J_b) of every T_A); 0 = 1-D row blocks.

@@ -215,9 +215,17 @@ struct cfpq_result {
 
     // relational sparse runs on one GPU keep their results in the log only, so the closure
     // kernel can reset the bit words at the fixpoint (flags bit 2 disables, diagnostics)
+    // Who clears a relational run's bit words for the next run.  One GPU: by default the next
+    // run switches to the other workspace bank and its closure kernel clears this bank's
+    // cells while its CTAs wait at grid barriers (config 4: 0.532 vs 0.564 ms per step with
+    // the reset at the fixpoint), so this run leaves its words; without a second bank (or
+    // with diag_flags bit 7) the kernel resets them at the fixpoint instead.  The peer-memory
+    // and asynchronous kernels always reset at the end (they have no bank rotation).
     bool self_clear_ok() const {
-        return opts.semantics == 0 && !hashed && ((n_ranks == 1 && !comm) || xr) && opts.path_policy < 2 &&
-               (opts.diag_flags & 4) == 0;
+        if (!(opts.semantics == 0 && !hashed && opts.path_policy < 2 && (opts.diag_flags & 4) == 0)) return false;
+        if (xr || opts.schedule == 2) return true;
+        if (n_ranks != 1 || comm) return false;
+        return spare_failed || (opts.diag_flags & 128) != 0;
     }
 
     EngineParams params() const {

@@ -19,6 +19,7 @@ variants = {
     "bitmaps": dict(cell_set=1),
     "bitmaps_noprecheck": dict(cell_set=1, flags=1),
     "bitmaps_noreset": dict(cell_set=1, flags=4),
+    "bitmaps_selfreset": dict(cell_set=1, flags=128),
     "hashed": dict(cell_set=2),
     "solo0": dict(cell_set=1, solo_threshold=0),
     "gauss_seidel": dict(cell_set=1, schedule=3),
