@@ -537,11 +537,31 @@ static cfpq_status plan(cfpq_result* r, const cfpq_grammar* g, const cfpq_graph*
         // the bit-row path gathers rows i of a preterminal left operand from its CSR
         if (o->path_policy == 3 && bc) need_csr[rl.B] = 1;
     }
-    // Gauss-Seidel stages: the LHS NTs in id order (DESIGN reading c17)
+    // Gauss-Seidel (DESIGN reading c17): the LHS NTs in id order, each reading T as the
+    // earlier LHS left it.  Consecutive LHS NTs that do not read each other's results share
+    // one barrier step (level): level(s) = max over earlier t of level(t) + 1 if s reads t's
+    // cells, and level(t) if t reads s's (so s still sees t's cells of this round and t does
+    // not see s's) — the states per round are exactly those of the one-by-one order.
     std::vector<int32_t> stage_of(g->n_nt, -1);
     r->n_stages = 0;
-    for (int A = 0; A < g->n_nt; ++A)
-        if (!g->is_const[A]) stage_of[A] = r->n_stages++;
+    {
+        std::vector<std::vector<char>> reads(g->n_nt, std::vector<char>(g->n_nt, 0));
+        for (auto& rl : g->rules) reads[rl.A][rl.B] = reads[rl.A][rl.C] = 1;
+        std::vector<int32_t> order;
+        for (int A = 0; A < g->n_nt; ++A)
+            if (!g->is_const[A]) order.push_back(A);
+        for (size_t a = 0; a < order.size(); ++a) {
+            const int sA = order[a];
+            int lv = 0;
+            for (size_t b = 0; b < a; ++b) {
+                const int tA = order[b];
+                if (reads[sA][tA]) lv = std::max(lv, stage_of[tA] + 1);
+                if (reads[tA][sA]) lv = std::max(lv, stage_of[tA]);
+            }
+            stage_of[sA] = lv;
+            r->n_stages = std::max(r->n_stages, lv + 1);
+        }
+    }
     for (auto& v : ex)
         for (auto& e : v) e.stage = stage_of[e.A];
     std::vector<Expansion> exps;
