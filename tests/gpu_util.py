@@ -25,10 +25,22 @@ def gpu_relations(r, n_nt):
     return {A: set(map(tuple, r.pairs(A).tolist())) for A in range(n_nt)}
 
 
+_ORACLE_CACHE = {}
+
+
+def oracle_run(w, lengths=False):
+    """O.run, memoised per workload (the workload names encode generator, size and seed):
+    parametrised GPU tests (formats, grids, launch variants) share one oracle closure."""
+    key = (w.name, int(w.n_nodes), len(w.edges), bool(lengths))
+    if key not in _ORACLE_CACHE:
+        _ORACLE_CACHE[key] = O.run(w, lengths=lengths)
+    return _ORACLE_CACHE[key]
+
+
 def assert_parity(w, r, ores=None, lengths=False, check_iterations=True):
     """Bit-exact comparison of every R_A (and lengths) with the oracle."""
     if ores is None:
-        ores = O.run(w, lengths=lengths)
+        ores = oracle_run(w, lengths=lengths)
         assert ores.status == 0
     for A in range(w.n_nt):
         exp = ores.pairs(A)

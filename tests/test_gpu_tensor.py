@@ -158,7 +158,7 @@ def test_tensor_cta_pairs_multicast():
     """dense_launch = 3: CTA pairs (clusters of 2) sharing the B tile through TMA multicast,
     MMA commits arriving on both CTAs' stage barriers; same closure, including an odd number
     of row tiles (the second tile of the last pair does not exist)."""
-    for n, d in [(300, 2), (1000, 2), (130, 1)]:
+    for n, d in [(300, 2), (700, 2), (130, 1)]:
         w = I.dense_stress_workload(n, d, seed=n)
         r, _, _ = gpu_closure(w, path_policy=2, tensor_format=1, dense_launch=3)
         assert_parity(w, r)
@@ -222,7 +222,7 @@ def test_tensor_2d_grid_emulated(grid, fmt):
     """2-D (SUMMA-style) block sharding: shard (a, b) derives block (I_a, J_b)
     of every T_A from the row panel I_a of the left and the column panel J_b of the right
     operands; blocks go through the staging buffer.  Jacobi states per iteration."""
-    for w in (I.dense_stress_workload(300, 2, seed=7), I.dense_stress_workload(1000, 2, seed=8),
+    for w in (I.dense_stress_workload(300, 2, seed=7), I.dense_stress_workload(700, 2, seed=8),
               I.dense_stress_workload(129, 1, seed=9), I.ontology_workload("union", 600, depth=6, seed=4),
               I.anbn_workload(5, 7)):
         r, _, _ = gpu_closure(w, path_policy=2, tensor_format=fmt, emulate_ranks=grid[0] * grid[1], grid=grid)
