@@ -1582,7 +1582,10 @@ __global__ void __launch_bounds__(kBlock, 1) closure_kernel(EngineParams p) {
         // [3] close; [2] = ~(min over CTAs of the barrier wait) = the last arriver's release
         const bool ph = p.phase != nullptr && k < p.iter_off_cap;
         long long c0 = ph ? clock64() : 0, c1 = 0, c2 = 0, c3 = 0;
-        expand(p, nt, exps, gsink, nullptr, s.lo, s.hi, k, s.gs_stage, blockIdx.x * kWarps + wib, gridDim.x * kWarps, lane,
+        // chunk c -> CTA c mod grid (interleaved): a Δ of ~3k chunks spreads over every SM
+        // instead of filling the first ~100 CTAs (diag_flags bit 8: CTA-major, round 1)
+        const int vwarp = p.cta_major ? (int)blockIdx.x * kWarps + wib : wib * (int)gridDim.x + (int)blockIdx.x;
+        expand(p, nt, exps, gsink, nullptr, s.lo, s.hi, k, s.gs_stage, vwarp, gridDim.x * kWarps, lane,
                &S.ws[wib], dcand, dexp, p.warp_flush != 0);
         if (ph) {
             __syncthreads();
@@ -1759,7 +1762,7 @@ __global__ void __launch_bounds__(kBlock, 1) xr_closure_kernel(EngineParams p0, 
     bool aborted = false;
     while (s.status == ST_RUNNING) {
         const long long k = s.iter + 1;
-        expand(p, nt, exps, sk, nullptr, s.lo, s.hi, k, 0, lb * kWarps + wib, x.cpr * kWarps, lane, &S.ws[wib], dcand,
+        expand(p, nt, exps, sk, nullptr, s.lo, s.hi, k, 0, wib * x.cpr + lb, x.cpr * kWarps, lane, &S.ws[wib], dcand,
                dexp, false);
         cta_flush_xr<kWarps>(p, sk, S.ws, wib, lane, s_bases, S.flush_prefix);
         unsigned long long bw = 0;

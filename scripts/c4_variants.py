@@ -20,6 +20,7 @@ variants = {
     "bitmaps_noprecheck": dict(cell_set=1, flags=1),
     "bitmaps_noreset": dict(cell_set=1, flags=4),
     "bitmaps_selfreset": dict(cell_set=1, flags=128),
+    "bitmaps_ctamajor": dict(cell_set=1, flags=256),
     "hashed": dict(cell_set=2),
     "solo0": dict(cell_set=1, solo_threshold=0),
     "gauss_seidel": dict(cell_set=1, schedule=3),
