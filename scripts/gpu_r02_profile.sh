@@ -33,6 +33,14 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:clos
    -o $O/prof_config4 python bench.py --workload config4 --steps 1 --warmup 3 --no-e2e --no-cpu-baseline --no-supplementary > $O/ncu_c4.txt 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:dense2sm_kernel -s 20 -c 1 \
    -o $O/prof_configS python bench.py --workload configS --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > $O/ncu_cS.txt 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:rows_scatter_kernel -s 6 -c 1 -o $O/prof_rows_scatter \
+   python -c "
+import sys; sys.path.insert(0,'.')
+import torch, inputs as I
+from paper_1707_01007_b200 import cfpq as C
+w=I.config4_workload(); g=C.Grammar.from_workload(w); d=C.Graph(w.n_nodes, torch.from_numpy(w.edges).cuda())
+r=C.closure(g,d,path_policy=3)
+" > $O/ncu_rows_scatter.txt 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:rows_rgather_kernel -s 6 -c 1 -o $O/prof_rows_rgather \
    python -c "
 import sys; sys.path.insert(0,'.')
@@ -42,4 +50,6 @@ w=I.config4_workload(); g=C.Grammar.from_workload(w); d=C.Graph(w.n_nodes, torch
 r=C.closure(g,d,path_policy=3)
 " > $O/ncu_rows.txt 2>&1
 python scripts/phase_profile.py config4 > $O/phase_config4.txt 2>&1
+python scripts/c4_variants.py > $O/c4_variants.txt 2>&1
+python scripts/e2e_breakdown.py > $O/e2e_config4.txt 2>&1
 ls -la $O
