@@ -1925,12 +1925,14 @@ cudaError_t rows_shard(DenseEngine* e, int64_t row_lo, int64_t row_hi, cudaStrea
         auto rg = [&](auto kern) {
             kern<<<resident_grid(kern, 256, sms), 256, 0, s>>>(p, rc, e->rule_out, chR);
         };
+        // default: 2 uint4 per lane, 2 rows in flight, 6 CTAs/SM (config 4: 9.03-9.08 ms loop in
+        // four runs vs 9.27-9.28 with one row in flight; 4 or 8 rows in flight lose occupancy)
         switch (e->rgather_variant) {
             case 1: rg(rows_rgather_kernel<1, 4, 6>); break;
-            case 2: rg(rows_rgather_kernel<2, 2, 6>); break;
+            case 2: rg(rows_rgather_kernel<2, 1, 8>); break;
             case 3: rg(rows_rgather_kernel<2, 4, 4>); break;
             case 4: rg(rows_rgather_kernel<1, 8, 4>); break;
-            default: rg(rows_rgather_kernel<2, 1, 8>); break;
+            default: rg(rows_rgather_kernel<2, 2, 6>); break;
         }
     }
     if (launches) *launches += 2 + (e->has_v ? 1 : 0) + (e->has_r ? 1 : 0);
