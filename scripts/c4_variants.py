@@ -27,10 +27,10 @@ variants = {
     "gauss_seidel_hashed": dict(cell_set=2, schedule=3),
     "async": dict(schedule=2),
     "rows": dict(path_policy=3),
-    "rows_rg1": dict(path_policy=3, flags=1 << 4),
-    "rows_rg2": dict(path_policy=3, flags=2 << 4),
-    "rows_rg3": dict(path_policy=3, flags=3 << 4),
-    "rows_rg4": dict(path_policy=3, flags=4 << 4),
+    "rows_R_1x4rows": dict(path_policy=3, flags=1 << 4),
+    "rows_R_2x1row": dict(path_policy=3, flags=2 << 4),
+    "rows_R_2x4rows": dict(path_policy=3, flags=3 << 4),
+    "rows_R_1x8rows": dict(path_policy=3, flags=4 << 4),
     "warp_flush": dict(cell_set=1, flags=8),
     "xr2_peer": dict(emulate_ranks=2, exchange=1),
     "xr8_peer": dict(emulate_ranks=8, exchange=1),
