@@ -97,7 +97,6 @@ struct __align__(16) WarpScratch {
     uint32_t fixed[32];   // bit 31 set: the fixed coordinate is j (R kinds), else i (L kinds)
     uint32_t len[32];
     int32_t nbuf;
-    int32_t nprev;        // cells of the last CTA flush still in buf (next-iteration prefetch)
 };
 
 // Length of an existing cell (X,i,j): preterminal cells have length 1 (P:393 seed),
@@ -395,7 +394,6 @@ __device__ void cta_flush_n(const EngineParams& p, const NTInfo* nt, const Sink&
     WarpScratch* ws = &ws_all[wib];
     const int nb = ws->nbuf;
     const unsigned long long base = *s_base + (unsigned long long)s_prefix[wib];
-    if (lane == 0) ws->nprev = nb;
     for (int t = lane; t < nb; t += 32) {
         uint64_t c = ws->buf[t];
         unsigned long long idx = base + (unsigned long long)t;
@@ -992,44 +990,10 @@ __device__ void clear_drain(const EngineParams& p) {
     }
 }
 
-// Next-iteration prefetch: a cell (A,i,j) new in iteration k is expanded in iteration k+1,
-// where its candidates' membership words are read first (a random DRAM access, the longest
-// link of the dependent chain).  While a CTA waits at the grid barrier its warps load the
-// adjacency heads of their flushed cells' first two expansions and prefetch those words into
-// L2, so iteration k+1 finds them there.  Off the critical path of the slowest CTA (its
-// thread 0 arrives first); heads of degree > 2 prefetch only their first two neighbours.
-__device__ __forceinline__ void prefetch_l2(const void* a) { asm volatile("prefetch.global.L2 [%0];" ::"l"(a)); }
-
-__device__ void prefetch_targets(const EngineParams& p, const NTInfo* nt, const Expansion* exps, const WarpScratch* ws,
-                                 int lane) {
-    const int nb = min(ws->nprev, kBuf);
-    for (int t = lane; t < nb; t += 32) {
-        const uint64_t c = ws->buf[t];
-        const uint32_t A = cell_nt(c), i = cell_i(c), j = cell_j(c);
-        const int eb = nt[A].exp_begin, ee = min(nt[A].exp_end, nt[A].exp_begin + 2);
-        for (int x = eb; x < ee; ++x) {
-            const Expansion ex = exps[x];
-            if (ex.kind == EXP_L_CONST) {
-                const int4 h = __ldg(nt[ex.other].csr_ell + j);
-                const uint32_t* row = nt[ex.A].T + (size_t)i * p.Wp;
-                if (h.y > 0) prefetch_l2(row + ((uint32_t)h.z >> 5));
-                if (h.y > 1) prefetch_l2(row + ((uint32_t)h.w >> 5));
-            } else if (ex.kind == EXP_R_CONST) {
-                const int4 h = __ldg(nt[ex.other].csc_ell + i);
-                if (h.y > 0) prefetch_l2(nt[ex.A].T + (size_t)h.z * p.Wp + (j >> 5));
-                if (h.y > 1) prefetch_l2(nt[ex.A].T + (size_t)h.w * p.Wp + (j >> 5));
-            }
-        }
-    }
-}
-
 // Grid barrier (generation counter, release/acquire).  If k >= 0 the last CTA to arrive
 // publishes the log size and error flags of iteration k in the released word; every CTA
-// closes the iteration from it (`word`, valid in thread 0 after the barrier).  With
-// `pf_ws`, warps 1..31 run the next-iteration prefetch while thread 0 arrives and waits.
-__device__ bool grid_barrier(const EngineParams& p, long long k, unsigned long long* word = nullptr,
-                             const WarpScratch* pf_ws = nullptr, const NTInfo* pf_nt = nullptr,
-                             const Expansion* pf_exps = nullptr) {
+// closes the iteration from it (`word`, valid in thread 0 after the barrier).
+__device__ bool grid_barrier(const EngineParams& p, long long k, unsigned long long* word = nullptr) {
     __shared__ int s_timeout;
     __shared__ unsigned long long s_word;
     if (p.clr_n) {
@@ -1052,8 +1016,6 @@ __device__ bool grid_barrier(const EngineParams& p, long long k, unsigned long l
                 s_word = w;
                 s_go = 1;
             }
-        } else if (pf_ws && threadIdx.x >= 32) {
-            prefetch_targets(p, pf_nt, pf_exps, &pf_ws[threadIdx.x >> 5], threadIdx.x & 31);
         }
         __syncthreads();
         while (!s_go) {
@@ -1115,8 +1077,6 @@ __device__ bool grid_barrier(const EngineParams& p, long long k, unsigned long l
             }
         }
         if (word) *word = w;
-    } else if (pf_ws && threadIdx.x >= 32) {
-        prefetch_targets(p, pf_nt, pf_exps, &pf_ws[threadIdx.x >> 5], threadIdx.x & 31);
     }
     __syncthreads();
     return s_timeout == 0;
@@ -1451,10 +1411,7 @@ __global__ void __launch_bounds__(kBlock, 1) closure_kernel(EngineParams p) {
     const NTInfo* nt = small ? S.nt : p.nt;
     const Expansion* exps = small ? S.exp : p.exps;
     const Sink gsink = global_sink(p);
-    if (lane == 0) {
-        S.ws[wib].nbuf = 0;
-        S.ws[wib].nprev = 0;
-    }
+    if (lane == 0) S.ws[wib].nbuf = 0;
     if (threadIdx.x == 0) {
         S.solo.solo = 0;
         S.state.lo = ld_volatile_u64(&st->lo);
@@ -1637,7 +1594,7 @@ __global__ void __launch_bounds__(kBlock, 1) closure_kernel(EngineParams p) {
         if (!p.warp_flush) cta_flush(p, nt, gsink, S.ws, wib, lane, &S.flush_base, S.flush_prefix);
         if (ph) c2 = clock64();
         unsigned long long bw = 0;
-        if (!grid_barrier(p, k, &bw, p.prefetch && !p.hset ? S.ws : nullptr, nt, exps)) {
+        if (!grid_barrier(p, k, &bw)) {
             aborted = true;
             break;
         }
@@ -1788,10 +1745,7 @@ __global__ void __launch_bounds__(kBlock, 1) xr_closure_kernel(EngineParams p0, 
     sk.xr_P = x.P;
     sk.xr_st = x.st;
     sk.xr_log = x.log;
-    if (lane == 0) {
-        S.ws[wib].nbuf = 0;
-        S.ws[wib].nprev = 0;
-    }
+    if (lane == 0) S.ws[wib].nbuf = 0;
     if (threadIdx.x == 0) {
         S.state.lo = ld_volatile_u64(&st->lo);
         S.state.hi = ld_volatile_u64(&st->hi);
