@@ -162,7 +162,9 @@ typedef struct {
                                 reset the bit words at the fixpoint instead of rotating two
                                 workspace banks (the default clears the other bank inside
                                 the next closure, during its grid-barrier waits), bit 8
-                                map Δ chunks to warps CTA-major instead of interleaved        */
+                                map Δ chunks to warps CTA-major instead of interleaved, bit 9
+                                seed with separate kernels instead of inside the closure
+                                kernel                                                       */
     int32_t grid_rows;       /* tensor engine, world_size (or reserved_emulate) > 1: 2-D
                                 process grid grid_rows x grid_cols (SUMMA-style blocks
                                 (I_a, J_b) of every T_A); 0 = 1-D row blocks.

@@ -162,6 +162,7 @@ struct cfpq_result {
     void* comm_row = nullptr;                 // NCCL sub-communicators of the grid row / column
     void* comm_col = nullptr;
     uint32_t* d_stage = nullptr;              // 2-D block exchange staging
+    unsigned long long* d_scan_tot = nullptr; // fused seeding: per-CTA totals of the adjacency scan
     size_t stage_cap = 0;
     int32_t n_ranks = 1;                      // row-block shards (NCCL ranks or emulated)
     int32_t my_rank = 0;
@@ -205,6 +206,7 @@ struct cfpq_result {
         dfree(d_small); dfree(d_Tn); dfree(d_rowcnt); dfree(d_rowoff);
         if (dense) dense_destroy(dense);
         dfree(d_stage);
+        dfree(d_scan_tot);
         for (void* q : xr_opened) cudaIpcCloseMemHandle(q);
         for (void* q : xr_owned) cudaFree(q);
         dfree(d_xr_st); dfree(d_xr_log); dfree(d_xr_rows);
@@ -1585,6 +1587,104 @@ static cfpq_status run_xr(cfpq_result* r, const cfpq_graph* d) {
     return CFPQ_OK;
 }
 
+// The device-resident fixpoint loop of the one-GPU sparse engine (a2-a5): one persistent
+// cooperative launch, re-launched only after a log overflow.  fused_seed: the first launch
+// also seeds T_0 and builds the preterminal adjacency (fused_seed_phase).
+static cfpq_status run_sparse_loop(cfpq_result* r, const cfpq_graph* d, bool fused_seed) {
+    cudaStream_t s = r->stream;
+    cfpq_status st;
+    EngineParams p;
+    bool first = true;
+    for (;;) {
+        p = r->params();
+        if (fused_seed && first) {
+            p.fused_seed = 1;
+            p.edges = d->d_edges;
+            p.n_edges = d->n_edges;
+            p.lab_ptr = r->d_lab_ptr;
+            p.lab_nt = r->d_lab_nt;
+            p.n_labels = r->n_labels;
+            p.max_rules = r->max_rules_per_label;
+            p.slot_row = r->d_slot_row;
+            p.slot_col = r->d_slot_col;
+            p.n_slots = r->n_adj_slots;
+            p.adj_cursor = r->d_adj_cnt;
+            p.adj_idx_w = r->d_adj_idx;
+            p.ell = r->d_adj_ell;
+            p.scan_tot = r->d_scan_tot;
+        }
+        if (!first) CFPQ_CUDA_TRY(cudaEventRecord(r->ev[2], s));
+        CFPQ_CUDA_TRY(launch_closure(p, r->grid, s));
+        CFPQ_CUDA_TRY(cudaEventRecord(r->ev[3], s));
+        r->launches++;
+        CFPQ_CUDA_TRY(cudaMemcpyAsync(&r->h_st, r->d_st, sizeof(EngineState), cudaMemcpyDeviceToHost, s));
+        CFPQ_CUDA_TRY(cudaStreamSynchronize(s));
+        if (r->clr_active && r->h_st.clr_cursor >= r->clr_n) {
+            r->spare.n_cells = 0;   // the other bank was cleared inside the kernel
+            r->clr_active = false;
+        }
+        {
+            float ms = 0;
+            if (first) {
+                CFPQ_CUDA_TRY(cudaEventElapsedTime(&ms, r->ev[0], r->ev[1]));
+                r->seed_ns = ms * 1e6;
+                CFPQ_CUDA_TRY(cudaEventElapsedTime(&ms, r->ev[1], r->ev[3]));
+            } else {
+                CFPQ_CUDA_TRY(cudaEventElapsedTime(&ms, r->ev[2], r->ev[3]));
+            }
+            r->loop_ns += ms * 1e6;
+            first = false;
+        }
+        if (r->h_st.bad_edge) {
+            r->n_cells = std::min<unsigned long long>(r->h_st.log_size, r->log_cap);
+            set_error("graph has an edge with a node id >= n_nodes or a label id >= n_labels");
+            return CFPQ_E_INVAL;
+        }
+        if (r->h_st.status == ST_OVERFLOW) {
+            // Δ_k did not fit: grow the log keeping its valid prefix (every slot below
+            // the old capacity was written) and re-run iteration k.
+            unsigned long long old_cap = r->log_cap;
+            st = grow_log(r, r->h_st.log_size);
+            if (st != CFPQ_OK) return st;
+            EngineState fix = r->h_st;
+            fix.log_size = std::min<unsigned long long>(r->h_st.log_size, old_cap);
+            fix.status = ST_RUNNING;
+            fix.overflow = 0;
+            fix.bar_count = 0;
+            fix.bar_word = 0;
+            if (r->opts.account_work && fix.iter + 1 < r->iter_off_cap)
+                CFPQ_CUDA_TRY(cudaMemsetAsync(r->d_jac + fix.iter + 1, 0, 8, s));
+            CFPQ_CUDA_TRY(cudaMemcpyAsync(r->d_st, &fix, sizeof(EngineState), cudaMemcpyHostToDevice, s));
+            continue;
+        }
+        break;
+    }
+    // Gauss-Seidel: the kernel counts steps; an iteration is a round of n_stages steps
+    r->iterations = r->opts.schedule == 3 && r->n_stages > 0 ? r->h_st.iter / r->n_stages : r->h_st.iter;
+    r->n_cells = std::min<unsigned long long>(r->h_st.log_size, r->log_cap);
+    r->t_clean = r->self_clear_ok() && (r->h_st.status == ST_DONE || r->h_st.status == ST_CAP);
+    if (r->h_st.status == ST_SWITCH) {
+        // Δ became dense: continue Alg. 1 from T_k on the tcgen05 engine (same states)
+        if ((st = ensure_dense(r)) != CFPQ_OK) return st;
+        r->switched++;
+        return run_dense(r, r->h_st.iter);
+    }
+    if (r->h_st.status == ST_CAP) {
+        set_error("max_iterations reached before the fixpoint");
+        return CFPQ_E_NOT_CONVERGED;
+    }
+    if (r->h_st.status == ST_LEN_OVERFLOW) {
+        set_error("a single-path length exceeded 2^32-1");
+        return CFPQ_E_OVERFLOW;
+    }
+    if (r->h_st.status != ST_DONE) {
+        set_error("closure kernel stopped without reaching the fixpoint (status " +
+                  std::to_string(r->h_st.status) + ", barrier watchdog?)");
+        return CFPQ_E_CUDA;
+    }
+    return CFPQ_OK;
+}
+
 static cfpq_status run(cfpq_result* r, const cfpq_graph* d) {
     cudaStream_t s = r->stream;
     r->clr_active = false;
@@ -1687,7 +1787,9 @@ static cfpq_status run(cfpq_result* r, const cfpq_graph* d) {
     }
     r->ran = true;
     r->n_cells = 0;
-    if (r->n_adj_slots)
+    const bool fused = r->opts.path_policy < 2 && r->n_ranks == 1 && !r->comm && !r->xr && r->opts.schedule != 2 &&
+                       (r->opts.diag_flags & 512) == 0;   // seeding inside the closure kernel
+    if (r->n_adj_slots && !fused)
         CFPQ_CUDA_TRY(cudaMemsetAsync(r->d_adj_cnt, 0, (size_t)r->n_adj_slots * (r->n + 1) * 4, s));
     if (r->opts.account_work) CFPQ_CUDA_TRY(cudaMemsetAsync(r->d_jac, 0, r->iter_off_cap * 8, s));
     CFPQ_CUDA_TRY(cudaMemsetAsync(r->d_st, 0, sizeof(EngineState), s));
@@ -1700,8 +1802,17 @@ static cfpq_status run(cfpq_result* r, const cfpq_graph* d) {
     r->seed_ns = r->loop_ns = 0;
     CFPQ_CUDA_TRY(cudaEventRecord(r->ev[0], s));
 
-    // a1: seed T_0; Δ_0 = the distinct seed cells
+    // a1: seed T_0; Δ_0 = the distinct seed cells.  One-GPU sparse runs seed
+    // inside the closure kernel (fused_seed_phase); the other engines run the seed kernels.
     const unsigned long long seeds_upper = (unsigned long long)d->n_edges * (unsigned long long)r->max_rules_per_label;
+    if (fused) {
+        if (!r->d_scan_tot) {
+            cfpq_status sa = dalloc(&r->d_scan_tot, (size_t)r->grid + 1, "scan totals");
+            if (sa != CFPQ_OK) return sa;
+        }
+        CFPQ_CUDA_TRY(cudaEventRecord(r->ev[1], s));
+        return run_sparse_loop(r, d, true);
+    }
     CFPQ_CUDA_TRY(launch_seed(d->d_edges, d->n_edges, (int32_t)r->n, r->d_lab_ptr, r->d_lab_nt, r->n_labels,
                               r->max_rules_per_label, p, s));
     r->launches += 1;
@@ -1728,80 +1839,7 @@ static cfpq_status run(cfpq_result* r, const cfpq_graph* d) {
     if (async) return run_async(r, seeds_upper);
     if (r->xr) return run_xr(r, d);
     if (r->n_ranks > 1 || r->comm) return run_sharded(r);
-    // a2-a5: the fixpoint loop, device-resident
-    bool first = true;
-    for (;;) {
-        p = r->params();
-        if (!first) CFPQ_CUDA_TRY(cudaEventRecord(r->ev[2], s));
-        CFPQ_CUDA_TRY(launch_closure(p, r->grid, s));
-        CFPQ_CUDA_TRY(cudaEventRecord(r->ev[3], s));
-        r->launches++;
-        CFPQ_CUDA_TRY(cudaMemcpyAsync(&r->h_st, r->d_st, sizeof(EngineState), cudaMemcpyDeviceToHost, s));
-        CFPQ_CUDA_TRY(cudaStreamSynchronize(s));
-        if (r->clr_active && r->h_st.clr_cursor >= r->clr_n) {
-            r->spare.n_cells = 0;   // the other bank was cleared inside the kernel
-            r->clr_active = false;
-        }
-        {
-            float ms = 0;
-            if (first) {
-                CFPQ_CUDA_TRY(cudaEventElapsedTime(&ms, r->ev[0], r->ev[1]));
-                r->seed_ns = ms * 1e6;
-                CFPQ_CUDA_TRY(cudaEventElapsedTime(&ms, r->ev[1], r->ev[3]));
-            } else {
-                CFPQ_CUDA_TRY(cudaEventElapsedTime(&ms, r->ev[2], r->ev[3]));
-            }
-            r->loop_ns += ms * 1e6;
-            first = false;
-        }
-        if (r->h_st.bad_edge) {
-            r->n_cells = std::min<unsigned long long>(r->h_st.log_size, r->log_cap);
-            set_error("graph has an edge with a node id >= n_nodes or a label id >= n_labels");
-            return CFPQ_E_INVAL;
-        }
-        if (r->h_st.status == ST_OVERFLOW) {
-            // Δ_k did not fit: grow the log keeping its valid prefix (every slot below
-            // the old capacity was written) and re-run iteration k.
-            unsigned long long old_cap = r->log_cap;
-            st = grow_log(r, r->h_st.log_size);
-            if (st != CFPQ_OK) return st;
-            EngineState fix = r->h_st;
-            fix.log_size = std::min<unsigned long long>(r->h_st.log_size, old_cap);
-            fix.status = ST_RUNNING;
-            fix.overflow = 0;
-            fix.bar_count = 0;
-            fix.bar_word = 0;
-            if (r->opts.account_work && fix.iter + 1 < r->iter_off_cap)
-                CFPQ_CUDA_TRY(cudaMemsetAsync(r->d_jac + fix.iter + 1, 0, 8, s));
-            CFPQ_CUDA_TRY(cudaMemcpyAsync(r->d_st, &fix, sizeof(EngineState), cudaMemcpyHostToDevice, s));
-            continue;
-        }
-        break;
-    }
-    // Gauss-Seidel: the kernel counts steps; an iteration is a round of n_stages steps
-    r->iterations = r->opts.schedule == 3 && r->n_stages > 0 ? r->h_st.iter / r->n_stages : r->h_st.iter;
-    r->n_cells = std::min<unsigned long long>(r->h_st.log_size, r->log_cap);
-    r->t_clean = r->self_clear_ok() && (r->h_st.status == ST_DONE || r->h_st.status == ST_CAP);
-    if (r->h_st.status == ST_SWITCH) {
-        // Δ became dense: continue Alg. 1 from T_k on the tcgen05 engine (same states)
-        if ((st = ensure_dense(r)) != CFPQ_OK) return st;
-        r->switched++;
-        return run_dense(r, r->h_st.iter);
-    }
-    if (r->h_st.status == ST_CAP) {
-        set_error("max_iterations reached before the fixpoint");
-        return CFPQ_E_NOT_CONVERGED;
-    }
-    if (r->h_st.status == ST_LEN_OVERFLOW) {
-        set_error("a single-path length exceeded 2^32-1");
-        return CFPQ_E_OVERFLOW;
-    }
-    if (r->h_st.status != ST_DONE) {
-        set_error("closure kernel stopped without reaching the fixpoint (status " +
-                  std::to_string(r->h_st.status) + ", barrier watchdog?)");
-        return CFPQ_E_CUDA;
-    }
-    return CFPQ_OK;
+    return run_sparse_loop(r, d, false);
 }
 
 // ------------------------------------------------------------------------------------------

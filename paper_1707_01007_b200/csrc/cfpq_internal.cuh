@@ -101,6 +101,7 @@ struct EngineState {
     // (L_1 = |Δ_0|); step t expands log[L_{t-S}, L_t) through the rules of stage (t-1) mod S
     unsigned long long gs_ring[kMaxStages + 1];
     unsigned long long xbar;       // peer-memory exchange: arrivals of every rank's last CTA
+    int adj_tail;                  // fused seeding: some adjacency row has > 2 entries
     int gs_stage;                  // stage of the next step ((k) mod S after step k closed)
     int gs_slot;                   // ring slot of L_{k+1} ((k+1) mod (S+1))
     long long gs_round;            // rounds completed (k / S)
@@ -174,6 +175,23 @@ struct EngineParams {
     uint32_t* clr_colc;
     unsigned long long async_init; // asynchronous schedule: log entries < this are valid unflagged
     int32_t gs_stages;             // > 0: Gauss-Seidel schedule with that many stages (0: Jacobi)
+    // seeding folded into the closure kernel (fused_seed = 1 on the first launch of a
+    // one-GPU sparse run): T_0 from the edges, the preterminal ELL heads counted on the fly,
+    // CSR tails (scan + fill) only when some adjacency row has more than two entries
+    int32_t fused_seed;
+    const int32_t* edges;
+    int64_t n_edges;
+    const int32_t* lab_ptr;
+    const int32_t* lab_nt;
+    int32_t n_labels;
+    int32_t max_rules;
+    const int32_t* slot_row;
+    const int32_t* slot_col;
+    int32_t n_slots;
+    int32_t* adj_cursor;           // [n_slots * n] CSR fill cursors (zeroed in the kernel)
+    int32_t* adj_idx_w;            // adj_idx, writable
+    int4* ell;                     // [n_slots * n] ELL heads {beg, deg, nb0, nb1}
+    unsigned long long* scan_tot;  // [grid + 1] per-CTA totals of the in-kernel scan
 };
 
 // ------------------------------------------------------------------------------------------

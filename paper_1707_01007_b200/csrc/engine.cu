@@ -1082,6 +1082,176 @@ __device__ bool grid_barrier(const EngineParams& p, long long k, unsigned long l
     return s_timeout == 0;
 }
 
+// ------------------------------------------------------------------------------------------
+// Seeding inside the closure kernel (fused_seed; one-GPU sparse runs).  Alg. 1 lines 6-7
+// as in seed_kernel, but a NEW seed cell of a preterminal also counts itself into
+// the ELL head of its row (CSR) / column (CSC) slot and claims the first two neighbour slots;
+// the CSR tails (exclusive scan of the degrees + fill) are built only when some head has
+// more than two entries.  Replaces 5-8 launches of the seed phase by grid barriers.
+// ------------------------------------------------------------------------------------------
+__device__ __forceinline__ void ell_add(const EngineParams& p, int sl, uint32_t row, int32_t nb) {
+    int* e = reinterpret_cast<int*>(p.ell + (size_t)sl * p.n + row);
+    const int old = atomicAdd(e + 1, 1);
+    if (old == 0) e[2] = nb;
+    else if (old == 1) e[3] = nb;
+    else if (old == 2) *(volatile int*)&p.st->adj_tail = 1;
+}
+
+__device__ __forceinline__ void ell_place(const EngineParams& p, int sl, uint32_t row, int32_t nb) {
+    const size_t x = (size_t)sl * p.n + row;
+    int* e = reinterpret_cast<int*>(p.ell + x);
+    const int k = atomicAdd(p.adj_cursor + x, 1);
+    p.adj_idx_w[e[0] + k] = nb;
+    if (k == 0) e[2] = nb;          // the ELL copies are the first two CSR entries
+    else if (k == 1) e[3] = nb;
+}
+
+// Block-wide exclusive scan of one value per thread (kBlock threads); returns the prefix,
+// *total = the block's sum.
+__device__ unsigned long long block_exclusive_scan(unsigned long long v, unsigned long long* total) {
+    __shared__ unsigned long long s_w[kWarps];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    unsigned long long incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long t = __shfl_up_sync(kFull, incl, o);
+        if (lane >= o) incl += t;
+    }
+    if (lane == 31) s_w[wib] = incl;
+    __syncthreads();
+    if (wib == 0) {
+        unsigned long long w = lane < kWarps ? s_w[lane] : 0ull;
+        unsigned long long wi = w;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned long long t = __shfl_up_sync(kFull, wi, o);
+            if (lane >= o) wi += t;
+        }
+        if (lane < kWarps) s_w[lane] = wi - w;
+        if (lane == kWarps - 1) *total = wi;
+    }
+    __syncthreads();
+    const unsigned long long r = s_w[wib] + incl - v;
+    __syncthreads();
+    return r;
+}
+
+__device__ bool fused_seed_phase(const EngineParams& p, const NTInfo* nt, WarpScratch* ws_all, int wib, int lane,
+                                 unsigned long long* s_base, int32_t* s_prefix, LoopState& s) {
+    __shared__ unsigned long long s_nseed, s_total, s_off;
+    __shared__ int s_tail;
+    const long long gtid = (long long)blockIdx.x * kBlock + threadIdx.x;
+    const long long gthreads = (long long)gridDim.x * kBlock;
+    const size_t ne = (size_t)p.n_slots * (size_t)p.n;
+    for (size_t t = (size_t)gtid; t < ne; t += (size_t)gthreads) {
+        p.ell[t] = make_int4(0, 0, 0, 0);
+        p.adj_cursor[t] = 0;
+    }
+    if (!grid_barrier(p, -1)) return false;
+    // ---- T_0 ----
+    const Sink sk = global_sink(p);
+    WarpScratch* ws = &ws_all[wib];
+    for (int64_t base = (int64_t)blockIdx.x * kBlock; base < p.n_edges; base += gthreads) {
+        const int64_t e = base + threadIdx.x;
+        bool valid = e < p.n_edges;
+        int32_t sv = 0, x = 0, dv = 0, rb = 0, re = 0;
+        if (valid) {
+            sv = __ldg(p.edges + 3 * e);
+            x = __ldg(p.edges + 3 * e + 1);
+            dv = __ldg(p.edges + 3 * e + 2);
+            if (sv < 0 || sv >= p.n || dv < 0 || dv >= p.n || x < 0 || x >= p.n_labels) {
+                p.st->bad_edge = 1;
+                valid = false;
+            } else {
+                rb = __ldg(p.lab_ptr + x);
+                re = __ldg(p.lab_ptr + x + 1);
+            }
+        }
+        for (int t = 0; t < p.max_rules; ++t) {
+            const bool has = valid && (rb + t < re);
+            const uint32_t A = has ? (uint32_t)__ldg(p.lab_nt + rb + t) : 0u;
+            uint64_t len = 1;
+            const bool keep = warp_dedup(p, sk, has, A, (uint32_t)sv, (uint32_t)dv, len, lane);
+            const bool nw = try_insert(p, nt, sk, keep, A, (uint32_t)sv, (uint32_t)dv, len, 0);
+            if (nw) {
+                const int sr = __ldg(p.slot_row + A), sc = __ldg(p.slot_col + A);
+                if (sr >= 0) ell_add(p, sr, (uint32_t)sv, dv);
+                if (sc >= 0) ell_add(p, sc, (uint32_t)dv, sv);
+            }
+            stage(p, nt, sk, ws, lane, nw, A, (uint32_t)sv, (uint32_t)dv);
+        }
+    }
+    cta_flush(p, nt, sk, ws_all, wib, lane, s_base, s_prefix);
+    unsigned long long bw = 0;
+    if (!grid_barrier(p, 0, &bw)) return false;
+    if (threadIdx.x == 0) {
+        s_nseed = bw & kBarLsMask;
+        s_tail = *(volatile int*)&p.st->adj_tail;
+    }
+    __syncthreads();
+    const unsigned long long n_seed = s_nseed;
+    if (s_tail) {
+        // ---- CSR tails: begins = exclusive scan of the degrees, then the fill ----
+        const size_t per = (ne + gridDim.x - 1) / gridDim.x;
+        const size_t lo = min(ne, (size_t)blockIdx.x * per), hi = min(ne, lo + per);
+        const size_t sub = (hi - lo + kBlock - 1) / kBlock;
+        const size_t a = min(hi, lo + (size_t)threadIdx.x * sub), b = min(hi, a + sub);
+        unsigned long long mine = 0;
+        for (size_t x = a; x < b; ++x) mine += (unsigned long long)p.ell[x].y;
+        const unsigned long long excl = block_exclusive_scan(mine, &s_total);
+        if (threadIdx.x == 0) p.scan_tot[blockIdx.x] = s_total;
+        if (!grid_barrier(p, -1)) return false;
+        if (wib == 0) {
+            unsigned long long acc = 0;
+            for (int q = lane; q < (int)blockIdx.x; q += 32) acc += ld_volatile_u64(&p.scan_tot[q]);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(kFull, acc, o);
+            if (lane == 0) s_off = acc;
+        }
+        __syncthreads();
+        unsigned long long run = s_off + excl;
+        for (size_t x = a; x < b; ++x) {
+            reinterpret_cast<int*>(p.ell + x)[0] = (int)run;
+            run += (unsigned long long)p.ell[x].y;
+        }
+        if (!grid_barrier(p, -1)) return false;
+        for (unsigned long long e = (unsigned long long)gtid; e < n_seed; e += (unsigned long long)gthreads) {
+            const uint64_t c = ldcg64(p.log + e);
+            const uint32_t X = cell_nt(c);
+            const int sr = __ldg(p.slot_row + X), sc = __ldg(p.slot_col + X);
+            if (sr >= 0) ell_place(p, sr, cell_i(c), (int32_t)cell_j(c));
+            if (sc >= 0) ell_place(p, sc, cell_j(c), (int32_t)cell_i(c));
+        }
+        if (!grid_barrier(p, -1)) return false;
+    }
+    // ---- open iteration 1: Δ_0 = log[0, n_seed) (T_0) ----
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        EngineState* st = p.st;
+        st->lo = 0;
+        st->hi = n_seed;
+        st->iter = 0;
+        if (p.iter_off_cap > 0) p.iter_off[0] = 0;
+        if (p.iter_off_cap > 1) p.iter_off[1] = n_seed;
+        if (p.iter_time) p.iter_time[0] = globaltimer();
+        st->gs_ring[1] = n_seed;
+        st->gs_slot = 1;
+        st->gs_stage = 0;
+        st->gs_round = 0;
+    }
+    s.lo = 0;
+    s.hi = n_seed;
+    s.iter = 0;
+    s.status = ST_RUNNING;
+    s.gs_stage = 0;
+    s.gs_slot = 1;
+    s.gs_round = 0;
+    if (p.has_snapshots) {
+        apply_snapshots(p, nt, nullptr, 0, n_seed, gtid, gthreads);
+        if (!grid_barrier(p, -1)) return false;
+    }
+    return true;
+}
+
 // Single-CTA iterations (|Δ| <= solo_max): one thread per Δ entry, Δ mirrored in
 // shared memory, appends counted in shared memory.  Counters and error flags rotate
 // over three slots (k mod 3) so that ONE __syncthreads() per iteration suffices: every
@@ -1427,7 +1597,8 @@ __global__ void __launch_bounds__(kBlock, 1) closure_kernel(EngineParams p) {
     __syncthreads();         // every thread holds it before warp-solo may rewrite S.state
     unsigned long long dcand = 0, dexp = 0;
     bool aborted = false;
-    while (s.status == ST_RUNNING) {
+    if (p.fused_seed && !fused_seed_phase(p, nt, S.ws, wib, lane, &S.flush_base, S.flush_prefix, s)) aborted = true;
+    while (!aborted && s.status == ST_RUNNING) {
         long long k = s.iter + 1;
         if ((long long)(s.hi - s.lo) <= (long long)p.solo_max) {
             // ------------- single-CTA iterations (see SoloShared) -------------

@@ -21,6 +21,7 @@ variants = {
     "bitmaps_noreset": dict(cell_set=1, flags=4),
     "bitmaps_selfreset": dict(cell_set=1, flags=128),
     "bitmaps_ctamajor": dict(cell_set=1, flags=256),
+    "bitmaps_seed_kernels": dict(cell_set=1, flags=512),
     "hashed": dict(cell_set=2),
     "solo0": dict(cell_set=1, solo_threshold=0),
     "gauss_seidel": dict(cell_set=1, schedule=3),

@@ -22,6 +22,7 @@ SIZES = [1, 31, 32, 33, 127, 128, 129, 255, 256, 257, 1025]
 # name -> (options, per-iteration Jacobi states?, allows a rule whose two operands change?)
 ENGINES = {
     "sparse": (dict(path_policy=1, cell_set=1), True, True),
+    "sparse_seed_kernels": (dict(path_policy=1, cell_set=1, flags=512), True, True),
     "hashed": (dict(path_policy=1, cell_set=2), True, False),
     "tensor_fp4": (dict(path_policy=2, tensor_format=2), True, True),
     "tensor_int8": (dict(path_policy=2, tensor_format=1), True, True),
