@@ -1597,7 +1597,12 @@ __global__ void __launch_bounds__(kBlock, 1) closure_kernel(EngineParams p) {
     __syncthreads();         // every thread holds it before warp-solo may rewrite S.state
     unsigned long long dcand = 0, dexp = 0;
     bool aborted = false;
-    if (p.fused_seed && !fused_seed_phase(p, nt, S.ws, wib, lane, &S.flush_base, S.flush_prefix, s)) aborted = true;
+    if (p.fused_seed) {
+        if (!fused_seed_phase(p, nt, S.ws, wib, lane, &S.flush_base, S.flush_prefix, s)) aborted = true;
+        __syncthreads();
+        if (threadIdx.x == 0) S.state = s;   // the solo paths re-read the loop state from here
+        __syncthreads();
+    }
     while (!aborted && s.status == ST_RUNNING) {
         long long k = s.iter + 1;
         if ((long long)(s.hi - s.lo) <= (long long)p.solo_max) {
