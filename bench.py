@@ -184,6 +184,38 @@ def ncu_traffic(workload: str):
         return None
 
 
+def probe_random_access(footprint_bytes: int, n_ops: int = 1 << 25):
+    """Random-access peaks over a buffer the size of the bit matrices, measured on this GPU
+    with library kernels (like the int8 peak): independent random 4-byte atomicAdds
+    (`index_add_`, the read-modify-write a bit insertion costs) and random 4-byte loads
+    (`take`), G ops/s, best of 3.  The closure kernel's unit of work is one random bit test
+    (+ set) per candidate into 5.4 GB of matrices, so these rates — not streaming bandwidth —
+    are what its memory system can deliver."""
+    words = max(1, footprint_bytes // 4)
+    try:
+        buf = torch.zeros(words, dtype=torch.int32, device="cuda")
+        idx = torch.randint(0, words, (n_ops,), dtype=torch.int64, device="cuda")
+        one = torch.ones(n_ops, dtype=torch.int32, device="cuda")
+        res = {}
+        for name, fn in (("atomic", lambda: buf.index_add_(0, idx, one)), ("load", lambda: torch.take(buf, idx))):
+            fn()
+            best = None
+            for _ in range(3):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                fn()
+                e1.record()
+                e1.synchronize()
+                ms = e0.elapsed_time(e1)
+                best = ms if best is None else min(best, ms)
+            res[name] = n_ops / (best * 1e-3) / 1e9
+        del buf, idx, one
+        torch.cuda.empty_cache()
+        return res
+    except Exception as ex:   # e.g. not enough free memory next to the closure's buffers
+        return {"error": str(ex)[:120]}
+
+
 _INT8_PROBE = {}
 
 
@@ -753,6 +785,19 @@ def main():
                     "note": ("latency-bound (SURVEY V-9): ~20 iterations of ~1e5 new cells, ~4 dependent memory "
                              "round trips each" if args.workload in ("config4", "config2") else
                              "latency-bound worst case: 2pq+1 iterations, one new cell each (SURVEY V-2)")}
+        if args.workload in ("config4", "config2") and not lengths:
+            # second roofline: candidates (one random bit test + set each) per second against the
+            # measured random 4-byte RMW rate over a buffer the size of the bit matrices
+            foot = int(w.n_nt) * int(w.n_nodes) * (((int(w.n_nodes) + 31) // 32 + 31) // 32 * 32) * 4
+            pr = probe_random_access(foot)
+            cand_rate = cand / loop_s / 1e9
+            roofline["random_access"] = {
+                "bound": "random 4-byte RMW into the bit matrices", "achieved": cand_rate,
+                "peak": pr.get("atomic"), "unit": "G candidates/s vs G random atomics/s",
+                "frac": (cand_rate / pr["atomic"]) if pr.get("atomic") else None,
+                "random_load_peak": pr.get("load"), "footprint_bytes": foot,
+                "peak_source": "measured in this run: torch index_add_ (int32 atomicAdd) / take, 2^25 uniform "
+                               "random indices over the footprint, best of 3" if "atomic" in pr else pr.get("error")}
 
     # ---- end to end through the public API with host buffers ----
     e2e = None
