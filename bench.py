@@ -191,6 +191,7 @@ def probe_random_access(footprint_bytes: int, n_ops: int = 1 << 25):
     (`take`), G ops/s, best of 3.  The closure kernel's unit of work is one random bit test
     (+ set) per candidate into 5.4 GB of matrices, so these rates — not streaming bandwidth —
     are what its memory system can deliver."""
+    import torch
     words = max(1, footprint_bytes // 4)
     try:
         buf = torch.zeros(words, dtype=torch.int32, device="cuda")
