@@ -786,7 +786,7 @@ def main():
                     "note": ("latency-bound (SURVEY V-9): ~20 iterations of ~1e5 new cells, ~4 dependent memory "
                              "round trips each" if args.workload in ("config4", "config2") else
                              "latency-bound worst case: 2pq+1 iterations, one new cell each (SURVEY V-2)")}
-        if args.workload in ("config4", "config2") and not lengths:
+        if args.workload in ("config4", "config2") and not lengths and not args.no_supplementary:
             # second roofline: candidates (one random bit test + set each) per second against the
             # measured random 4-byte RMW rate over a buffer the size of the bit matrices
             foot = int(w.n_nt) * int(w.n_nodes) * (((int(w.n_nodes) + 31) // 32 + 31) // 32 * 32) * 4
