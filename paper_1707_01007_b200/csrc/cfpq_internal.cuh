@@ -100,7 +100,11 @@ struct EngineState {
     // Gauss-Seidel schedule: gs_ring[t mod (S+1)] = L_t, the log size when step t starts
     // (L_1 = |Δ_0|); step t expands log[L_{t-S}, L_t) through the rules of stage (t-1) mod S
     unsigned long long gs_ring[kMaxStages + 1];
-    unsigned long long xbar;       // peer-memory exchange: arrivals of every rank's last CTA
+    // peer-memory exchange: xr_slot[k & 1] collects, on every rank, the iteration-k arrival of
+    // every rank's last CTA as (its new cells << 32) | (its overflow << 16) | 1; xr_new counts
+    // this rank's new cells of the current iteration (appended to every rank's log)
+    unsigned long long xr_slot[2];
+    unsigned long long xr_new;
     int adj_tail;                  // fused seeding: some adjacency row has > 2 entries
     int gs_stage;                  // stage of the next step ((k) mod S after step k closed)
     int gs_slot;                   // ring slot of L_{k+1} ((k+1) mod (S+1))

@@ -940,6 +940,7 @@ struct RowsCtx {
                                        // l_next[q] = -2 marks a rule that is not a group leader
     unsigned long long chunk_cap;      // capacity of each chunk list (the products clamp to it;
                                        // the host re-runs the shard when a list overflowed)
+    int32_t push;                      // form R by input row: chunks of CSC_B(r) (rows_rpush_kernel)
 };
 
 enum : int { RF_NONE = 0, RF_L = 1, RF_R = 2, RF_V = 3, RF_P = 4 };
@@ -1058,7 +1059,12 @@ __global__ void rows_plan_kernel(DenseParams p, RowsCtx c, RowChunk* chunks, uns
                 f = row_form(c, r);
                 bptr = c.nt[r.B].csr_ptr;
             }
-            if (f == RF_R) {
+            if (f == RF_R && c.push) {
+                // push form: task row = input row r of T_C (non-empty), chunks of CSC_B(r)
+                const int32_t* cp = c.nt[r.B].csc_ptr;
+                len = c.cnt[(size_t)p.rules[q].C * p.n + i] ? __ldg(cp + i + 1) - __ldg(cp + i) : 0;
+                per = kChunkR;
+            } else if (f == RF_R) {
                 const int32_t* ptr = bptr;
                 len = __ldg(ptr + i + 1) - __ldg(ptr + i);
                 per = kChunkR;
@@ -1189,6 +1195,56 @@ __global__ void __launch_bounds__(256, MINB) rows_rgather_kernel(DenseParams p, 
 #pragma unroll
             for (int q = 0; q < 4; ++q)
                 if (a[q]) rows_merge(p, c, A, ch.row, 4 * v + q, a[q], my_new);
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) my_new += __shfl_xor_sync(0xffffffffu, my_new, o);
+    if (lane == 0 && my_new) atomicAdd(p.new_cells + p.n_nt, my_new);
+}
+
+// Form R by input row (push; unsharded runs): T_k[i] |= T_{k-1},C[r] for every i in CSC_B(r)
+// — the same OR as the gather over CSR_B(i), but every non-empty row T_C[r] is streamed once
+// per rule and iteration.  One warp per (chunk of <= kChunkR CSC_B(r) entries, row slice of
+// 32 * NVW uint4): the slice and the chunk's output rows are loaded together, and the slice's
+// non-zero words are merged into each output row.
+template <int NVW, int MINB>
+__global__ void __launch_bounds__(256, MINB) rows_rpush_kernel(DenseParams p, RowsCtx c, const int32_t* __restrict__ rule_out,
+                                                               const RowChunk* __restrict__ chunks) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nv4 = ((p.n + 31) / 32 + 3) / 4;
+    const int parts = (int)((nv4 + 32 * NVW - 1) / (32 * NVW));
+    const unsigned long long m = min(c.rc[0], c.chunk_cap) * (unsigned long long)parts;
+    const int64_t wp4 = p.Wp / 4;
+    unsigned long long my_new = 0;
+    for (unsigned long long ti = (blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x) >> 5; ti < m;
+         ti += ((unsigned long long)gridDim.x * blockDim.x) >> 5) {
+        const unsigned long long ci = ti / parts;
+        const int64_t vbase = (int64_t)(ti - ci * parts) * 32 * NVW;
+        const RowChunk ch = chunks[ci];
+        const DenseRule r = p.rules[ch.rule];
+        const uint4* row = reinterpret_cast<const uint4*>(p.T[r.C]) + (size_t)ch.row * wp4;
+        uint4 x[NVW];
+#pragma unroll
+        for (int b = 0; b < NVW; ++b) {
+            const int64_t v = vbase + (int64_t)b * 32 + lane;
+            x[b] = v < nv4 ? __ldg(row + v) : make_uint4(0, 0, 0, 0);
+        }
+        const int ii = lane < ch.count ? __ldg(c.adj_idx + __ldg(c.nt[r.B].csc_ptr + ch.row) + ch.first + lane) : 0;
+        bool nz = false;
+#pragma unroll
+        for (int b = 0; b < NVW; ++b) nz |= (x[b].x | x[b].y | x[b].z | x[b].w) != 0u;
+        if (!__any_sync(0xffffffffu, nz)) continue;
+        const int A = rule_out[ch.rule];
+        for (int e = 0; e < ch.count; ++e) {
+            const int i = __shfl_sync(0xffffffffu, ii, e);
+#pragma unroll
+            for (int b = 0; b < NVW; ++b) {
+                const int64_t v = vbase + (int64_t)b * 32 + lane;
+                const uint32_t a[4] = {x[b].x, x[b].y, x[b].z, x[b].w};
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    if (a[q]) rows_merge(p, c, A, i, 4 * v + q, a[q], my_new);
+            }
         }
     }
 #pragma unroll
@@ -1894,8 +1950,12 @@ cudaError_t rows_shard(DenseEngine* e, int64_t row_lo, int64_t row_hi, cudaStrea
     cudaError_t c;
     const int32_t n_rules = (int32_t)e->h_rule_out.size();
     DenseParams p = rows_params(e);
+    // form R pushes input rows (each non-empty T_C row streamed once) on unsharded runs; row
+    // shards gather their own output rows (rgather variants 1-4 and 7 force the gather, A/B)
+    const bool push = row_lo == 0 && row_hi == e->n && (e->rgather_variant == 0 || e->rgather_variant == 5 ||
+                                                         e->rgather_variant == 6);
     RowsCtx rc{e->rows_nt, e->rows_adj, e->rcnt, (uint4*)e->dlist, e->dlist_cap, e->rc, e->rows_first ? 1 : 0,
-               n_rules, (int32_t)row_lo, (int32_t)row_hi, e->l_next, e->chunk_cap};
+               n_rules, (int32_t)row_lo, (int32_t)row_hi, e->l_next, e->chunk_cap, push ? 1 : 0};
     const int sms = device_sms();
     // plan and products back to back, no host round trip: the products clamp every list to
     // its capacity and the counters are copied to pinned host memory behind them; the host
@@ -1927,12 +1987,20 @@ cudaError_t rows_shard(DenseEngine* e, int64_t row_lo, int64_t row_hi, cudaStrea
         };
         // default: 2 uint4 per lane, 2 rows in flight, 6 CTAs/SM (config 4: 9.03-9.08 ms loop in
         // four runs vs 9.27-9.28 with one row in flight; 4 or 8 rows in flight lose occupancy)
-        switch (e->rgather_variant) {
-            case 1: rg(rows_rgather_kernel<1, 4, 6>); break;
-            case 2: rg(rows_rgather_kernel<2, 1, 8>); break;
-            case 3: rg(rows_rgather_kernel<2, 4, 4>); break;
-            case 4: rg(rows_rgather_kernel<1, 8, 4>); break;
-            default: rg(rows_rgather_kernel<2, 2, 6>); break;
+        if (push) {
+            switch (e->rgather_variant) {
+                case 5: rg(rows_rpush_kernel<1, 8>); break;
+                case 6: rg(rows_rpush_kernel<4, 4>); break;
+                default: rg(rows_rpush_kernel<2, 6>); break;
+            }
+        } else {
+            switch (e->rgather_variant) {
+                case 1: rg(rows_rgather_kernel<1, 4, 6>); break;
+                case 2: rg(rows_rgather_kernel<2, 1, 8>); break;
+                case 3: rg(rows_rgather_kernel<2, 4, 4>); break;
+                case 4: rg(rows_rgather_kernel<1, 8, 4>); break;
+                default: rg(rows_rgather_kernel<2, 2, 6>); break;
+            }
         }
     }
     if (launches) *launches += 2 + (e->has_v ? 1 : 0) + (e->has_r ? 1 : 0);

@@ -84,10 +84,9 @@ struct Sink {
 __device__ __forceinline__ unsigned long long xr_reserve(const Sink& sk, int q, unsigned long long nb) {
     return atomicAdd_system(&sk.xr_st[q]->log_size, nb);
 }
-// Every rank learns of an overflow (the run is restarted with larger logs).
-__device__ __forceinline__ void xr_flag_overflow(const Sink& sk) {
-    for (int q = 0; q < sk.xr_P; ++q) *(volatile int*)&sk.xr_st[q]->overflow = 1;
-}
+// An append that does not fit flags this rank only; the cross-rank barrier sums the flags of
+// every rank into the iteration's outcome (every rank then restarts with larger logs).
+__device__ __forceinline__ void xr_flag_overflow(const Sink& sk) { *(volatile int*)sk.overflow = 1; }
 
 struct __align__(16) WarpScratch {
     uint64_t buf[kBuf];   // staged new cells
@@ -255,6 +254,7 @@ __device__ __forceinline__ void flush(const EngineParams& p, const NTInfo* nt, c
                 else xr_flag_overflow(sk);
             }
         }
+        if (lane == 0) atomicAdd(&p.st->xr_new, (unsigned long long)nb);   // this rank's new cells
         __syncwarp();
         if (lane == 0) ws->nbuf = 0;
         __syncwarp();
@@ -354,6 +354,7 @@ __device__ void cta_flush_xr(const EngineParams& p, const Sink& sk, WarpScratch*
         if (lane < NW) s_prefix[lane] = incl - nb;
         const int tot = __shfl_sync(kFull, incl, 31);
         if (lane < sk.xr_P) s_bases[lane] = tot ? xr_reserve(sk, lane, (unsigned long long)tot) : 0ull;
+        if (lane == 0 && tot) atomicAdd(&p.st->xr_new, (unsigned long long)tot);   // this rank's new cells
     }
     __syncthreads();
     WarpScratch* ws = &ws_all[wib];
@@ -1844,12 +1845,13 @@ __global__ void __launch_bounds__(kBlock, 1) closure_kernel(EngineParams p) {
 // Δ_{k-1} (its own copy in its own log), inserts only the cells of its rows, and appends every
 // new cell to EVERY rank's log (system-scope reservations and stores; NVLink peer mappings on
 // real GPUs), so the exchange overlaps the expansion instead of following it.  Iteration end:
-// the rank's CTAs meet at a rank-local barrier whose last CTA fences system-wide, arrives on
-// every rank's cross counter (xbar) and waits for all P arrivals of this iteration; after that
-// its own log holds Δ_k of every rank (the same set on every rank), and it releases its CTAs
-// with the log size.  An emulated launch runs P virtual ranks as CTA groups of one grid.
+// the rank's CTAs meet at a rank-local barrier whose last CTA fences system-wide, adds its
+// rank's new-cell count and overflow flag to every rank's slot of this iteration (xr_slot) and
+// waits for all P arrivals; after that its own log holds Δ_k of every rank (the same set on
+// every rank) and it releases its CTAs with the log size hi + Σ counts.  An emulated launch runs P virtual ranks as CTA groups of one grid.
 // ------------------------------------------------------------------------------------------
-__device__ bool xr_barrier(const EngineParams& p, const XrParams& x, long long k, unsigned long long* word) {
+__device__ bool xr_barrier(const EngineParams& p, const XrParams& x, long long k, unsigned long long hi,
+                           unsigned long long* word) {
     __shared__ int s_timeout;
     __threadfence_system();   // this CTA's appends to peer logs are visible system-wide first
     __syncthreads();
@@ -1860,12 +1862,24 @@ __device__ bool xr_barrier(const EngineParams& p, const XrParams& x, long long k
         const unsigned arrived = atom_add_acq_rel(&st->bar_count, 1u);
         unsigned long long w;
         if (arrived == (unsigned)p.nblocks - 1u) {
+            // every CTA of this rank has appended (acq_rel chain): its iteration-k contribution
+            // is its new-cell count and its overflow flag, which no other rank writes
+            __threadfence();
+            const unsigned long long nk = ld_volatile_u64(&st->xr_new);
+            const unsigned long long ov = *(volatile int*)&st->overflow ? 1ull : 0ull;
+            st->xr_new = 0ull;
             __threadfence_system();
-            for (int q = 0; q < x.P; ++q) atomicAdd_system(&x.st[q]->xbar, 1ull);
-            const unsigned long long want = (unsigned long long)x.P * (unsigned long long)k;
+            const int sl = (int)(k & 1);
+            const unsigned long long add = (nk << 32) | (ov << 16) | 1ull;
+            for (int q = 0; q < x.P; ++q) atomicAdd_system(&x.st[q]->xr_slot[sl], add);
+            // Δ_k of THIS log = the sum of every rank's new cells, read from the slot once all P
+            // ranks arrived — not from the log counter, which a rank already released from
+            // iteration k may be advancing with its iteration-(k+1) appends.  The slot is next
+            // used at iteration k+2, whose arrivals need this rank's arrival at k+1 first.
             long long t0 = clock64();
             unsigned ns = 0;
-            while (ld_volatile_u64(&st->xbar) < want) {
+            unsigned long long v;
+            while (((v = ld_volatile_u64(&st->xr_slot[sl])) & 0xFFFFull) < (unsigned long long)x.P) {
                 if (ns) __nanosleep(ns);
                 if (clock64() - t0 > 40000) ns = ns ? (ns < 1024u ? ns * 2u : 1024u) : 64u;
                 if (clock64() - t0 > 60000000000ll) {
@@ -1874,7 +1888,9 @@ __device__ bool xr_barrier(const EngineParams& p, const XrParams& x, long long k
                 }
             }
             __threadfence_system();
-            w = bar_release_word(st, my, k);
+            st->xr_slot[sl] = 0ull;
+            const unsigned long long f = ((v >> 16) & 0xFFFFull) ? 1ull : 0ull;
+            w = (((my + 1) & 0xFFFFFFull) << kBarGenShift) | (f << 38) | ((hi + (v >> 32)) & kBarLsMask);
             st->bar_count = 0u;
             st_release_word(&st->bar_word, w);
         } else {
@@ -1942,7 +1958,7 @@ __global__ void __launch_bounds__(kBlock, 1) xr_closure_kernel(EngineParams p0, 
                dexp, false);
         cta_flush_xr<kWarps>(p, sk, S.ws, wib, lane, s_bases, S.flush_prefix);
         unsigned long long bw = 0;
-        if (!xr_barrier(p, x, k, &bw)) {
+        if (!xr_barrier(p, x, k, s.hi, &bw)) {
             aborted = true;
             break;
         }
