@@ -700,14 +700,25 @@ def main():
     del r0
 
     exchange_note = None
+    r, err = None, None
     try:
         r = C.closure(g, d, **kw, **shard_kw)
     except C.CfpqError as ex:
         if shard_kw.get("exchange") != 1:
             raise
+        err = ex
+    if shard_kw.get("exchange") == 1 and multi and dist.is_initialized():
+        # every rank takes the same path: one rank that could not map its peers sends all of
+        # them to the NCCL host loop
+        ok = torch.tensor([0 if err is not None else 1], dtype=torch.int32, device="cuda")
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        if int(ok.item()) == 0 and err is None:
+            err = RuntimeError("a peer rank could not use the peer-memory exchange")
+    if err is not None:
         # the peer-memory path could not map the peers (e.g. no CUDA IPC between these
         # processes): fall back to the NCCL host loop, and say so in the line
-        exchange_note = "peer-memory exchange failed (%s); NCCL host loop used" % str(ex)[:200]
+        exchange_note = "peer-memory exchange failed (%s); NCCL host loop used" % str(err)[:200]
+        r = None
         shard_kw["exchange"] = 0
         uid = torch.zeros(128, dtype=torch.uint8, device="cuda")
         if rank == 0:
