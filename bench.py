@@ -637,6 +637,8 @@ def main():
                     help="0 Jacobi (Alg. 1 states), 3 Gauss-Seidel (in-place stages, same fixpoint)")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-format", default="csr", choices=["csr", "pairs"],
+                    help="end-to-end result read back: CSR (default) or (i, j) pairs")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-supplementary", action="store_true")
     ap.add_argument("--solo", type=int, default=-1)
@@ -815,7 +817,12 @@ def main():
     e2e = None
     if not args.no_e2e:
         pinned = torch.from_numpy(w.edges.copy()).pin_memory()
-        out_pairs = torch.empty((max(results_start, 1), 2), dtype=torch.int32).pin_memory()
+        csr = args.e2e_format == "csr"
+        if csr:   # R_start as row pointers + columns (cfpq_result_csr): 4 B per pair + 8(n+1) B
+            out_ptr = torch.empty((w.n_nodes + 1,), dtype=torch.int64).pin_memory()
+            out_cols = torch.empty((max(results_start, 1),), dtype=torch.int32).pin_memory()
+        else:
+            out_pairs = torch.empty((max(results_start, 1), 2), dtype=torch.int32).pin_memory()
         h2d = pinned.numel() * 4
         d2h = 0
         ts = []
@@ -824,17 +831,22 @@ def main():
             t0 = time.perf_counter()
             d.set_edges(pinned, stream=stream)
             C.closure_reuse(g, d, r, **kw, **shard_kw)
-            pairs = r.pairs(w.start, out=out_pairs)
+            if csr:
+                rp, cols = r.csr(w.start, out_ptr, out_cols)
+            else:
+                pairs = r.pairs(w.start, out=out_pairs)
             t1 = time.perf_counter()
             if it >= args.warmup:
                 ts.append(t1 - t0)
-                d2h = pairs.numel() * 4
+                d2h = rp.numel() * 8 + cols.numel() * 4 if csr else pairs.numel() * 4
         e_total = torch.tensor([sum(ts)], dtype=torch.float64, device="cuda")
         if world > 1:
             dist.all_reduce(e_total, op=dist.ReduceOp.MAX)
         e2e = {"value": useful_job * len(ts) / float(e_total.item()) / 1e9, "unit": UNIT,
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-               "ms_per_step": 1e3 * float(e_total.item()) / len(ts)}
+               "ms_per_step": 1e3 * float(e_total.item()) / len(ts),
+               "result": ("R_start as CSR (cfpq_result_csr: int64 row pointers + int32 columns)" if csr else
+                          "R_start as sorted (i, j) int32 pairs (cfpq_result_pairs)") + " into pinned host memory"}
 
     supp = None
     if multi and args.workload == "config4" and not args.no_supplementary:

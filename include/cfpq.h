@@ -217,6 +217,14 @@ CFPQ_API cfpq_status cfpq_result_pairs(cfpq_result* r, int32_t nt, int32_t* dst_
 CFPQ_API cfpq_status cfpq_result_pairs_at(cfpq_result* r, int32_t nt, int64_t k, int32_t* dst_pairs,
                                  int64_t capacity, int32_t dst_is_device, int64_t* written);
 
+/* R_A in compressed-row form (Theorem 2): row_ptr[0..n] int64 with row i's columns in
+ * cols[row_ptr[i] .. row_ptr[i+1]) (int32, ascending: the order of cfpq_result_pairs), cols of
+ * capacity entries.  *written = |R_A|; CFPQ_E_INVAL if capacity < |R_A| (nothing written then).
+ * Both buffers on the host or both on the device (dst_is_device).  Half the bytes of the pair
+ * form (4 B per pair + 8(n+1) B) for reading a large relation back. */
+CFPQ_API cfpq_status cfpq_result_csr(cfpq_result* r, int32_t nt, int64_t* row_ptr, int32_t* cols, int64_t capacity,
+                                     int32_t dst_is_device, int64_t* written);
+
 /* The bit matrix of A: row i, bit j = word j>>5, bit j&31 (LSB first); dst rows are
  * row_stride_words uint32 apart (>= ceil(n/32)); n rows.  dst on host or device. */
 CFPQ_API cfpq_status cfpq_result_matrix(cfpq_result* r, int32_t nt, uint32_t* dst, int64_t row_stride_words,

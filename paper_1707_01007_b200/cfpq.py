@@ -16,7 +16,9 @@ from typing import Optional, Tuple
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libcfpq.so")
+# CFPQ_CHECKED=1 selects the checked build (device bounds assertions; diagnostics only,
+# `python paper_1707_01007_b200/build.py --checked`): the library itself reads no environment
+LIB_PATH = os.path.join(HERE, "libcfpq_checked.so" if os.environ.get("CFPQ_CHECKED") == "1" else "libcfpq.so")
 
 CFPQ_OK, CFPQ_E_INVAL, CFPQ_E_NOMEM, CFPQ_E_CUDA, CFPQ_E_NCCL = 0, -1, -2, -3, -4
 CFPQ_E_NOT_CONVERGED, CFPQ_E_OVERFLOW, CFPQ_E_UNSUPPORTED = -5, -6, -7
@@ -27,7 +29,7 @@ EXPORTS = [
     "cfpq_grammar_create", "cfpq_grammar_destroy", "cfpq_graph_create", "cfpq_graph_set_edges",
     "cfpq_graph_destroy", "cfpq_options_default", "cfpq_closure", "cfpq_closure_reuse",
     "cfpq_result_destroy", "cfpq_result_iterations", "cfpq_result_count", "cfpq_result_count_at",
-    "cfpq_result_pairs", "cfpq_result_pairs_at", "cfpq_result_matrix", "cfpq_result_lengths",
+    "cfpq_result_pairs", "cfpq_result_pairs_at", "cfpq_result_csr", "cfpq_result_matrix", "cfpq_result_lengths",
     "cfpq_result_stats", "cfpq_result_iteration_stats", "cfpq_result_iteration_stats2",
     "cfpq_result_iteration_phases", "cfpq_result_witness", "cfpq_last_error",
     "cfpq_version", "cfpq_nccl_unique_id", "cfpq_shard_rows", "cfpq_shard_block",
@@ -84,6 +86,7 @@ def load() -> ctypes.CDLL:
         "cfpq_result_pairs": (i32, [vp, i32, vp, i64, i32, P(i64)]),
         "cfpq_result_pairs_at": (i32, [vp, i32, i64, vp, i64, i32, P(i64)]),
         "cfpq_result_matrix": (i32, [vp, i32, vp, i64, i32]),
+        "cfpq_result_csr": (i32, [vp, i32, vp, vp, i64, i32, P(i64)]),
         "cfpq_result_lengths": (i32, [vp, i32, vp, i64, i32, P(i64)]),
         "cfpq_result_stats": (i32, [vp, P(i64), i32]),
         "cfpq_result_iteration_stats": (i32, [vp, vp, vp, i64]),
@@ -288,6 +291,21 @@ class Result:
         buf = np.zeros((m, 2), dtype=np.int32)
         _check(load().cfpq_result_pairs(self._h, int(A), _ptr(buf), m, 0, ctypes.byref(w)), "cfpq_result_pairs")
         return buf[: w.value]
+
+    def csr(self, A: int, row_ptr=None, cols=None):
+        """R_A in compressed-row form: (row_ptr int64 [n+1], cols int32 [|R_A|]), columns ascending
+        per row.  `row_ptr` / `cols` may be torch tensors (both on the device, or both in (pinned)
+        host memory); then they are written and (row_ptr, cols[:|R_A|]) is returned."""
+        w = ctypes.c_int64()
+        if row_ptr is not None:
+            _check(load().cfpq_result_csr(self._h, int(A), _ptr(row_ptr), _ptr(cols), int(cols.shape[0]),
+                                          int(_is_device(row_ptr)), ctypes.byref(w)), "cfpq_result_csr")
+            return row_ptr, cols[: w.value]
+        m = self.count(A)
+        rp = np.zeros(self.n_nodes + 1, dtype=np.int64)
+        cs = np.zeros(max(m, 1), dtype=np.int32)
+        _check(load().cfpq_result_csr(self._h, int(A), _ptr(rp), _ptr(cs), m, 0, ctypes.byref(w)), "cfpq_result_csr")
+        return rp, cs[: w.value]
 
     def pairs_at(self, A: int, k: int) -> np.ndarray:
         """Pairs of A in T_k (Alg. 1 state after k loop bodies)."""

@@ -175,6 +175,7 @@ struct cfpq_result {
     int64_t block_rows = 0;                   // rows per shard block (dense engine)
     int32_t* d_rowcnt = nullptr;              // bitmap extraction scratch [n+1]
     int32_t* d_rowoff = nullptr;
+    int64_t* d_csr_ptr = nullptr;             // CSR row pointers for a host destination [n+1]
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
     double seed_ns = 0, loop_ns = 0;
 
@@ -203,7 +204,7 @@ struct cfpq_result {
         dfree(d_lab_ptr); dfree(d_lab_nt); dfree(d_slot_row); dfree(d_slot_col); dfree(d_adj_cnt);
         dfree(d_adj_ptr); dfree(d_adj_cursor); dfree(d_adj_idx); dfree(d_adj_ell); dfree(d_log); dfree(d_st);
         dfree(d_iter_off); dfree(d_jac); dfree(d_iter_time); dfree(d_phase); dfree(d_hset); dfree(d_xbuf); dfree(d_rowc); dfree(d_colc); dfree(d_temp); dfree(d_keys);
-        dfree(d_small); dfree(d_Tn); dfree(d_rowcnt); dfree(d_rowoff);
+        dfree(d_small); dfree(d_Tn); dfree(d_rowcnt); dfree(d_rowoff); dfree(d_csr_ptr);
         if (dense) dense_destroy(dense);
         dfree(d_stage);
         dfree(d_scan_tot);
@@ -239,6 +240,7 @@ struct cfpq_result {
         p.exps = d_exps;
         p.n_exps = n_exps;
         p.adj_idx = d_adj_idx;
+        p.adj_cap = adj_idx_cap;
         p.log = d_log;
         p.log_cap = log_cap;
         p.st = d_st;
@@ -2163,6 +2165,68 @@ static cfpq_status pairs_impl(cfpq_result* r, int32_t nt, int64_t k, int32_t* ds
 extern "C" cfpq_status cfpq_result_pairs(cfpq_result* r, int32_t nt, int32_t* dst_pairs, int64_t capacity,
                                          int32_t dst_is_device, int64_t* written) {
     return pairs_impl(r, nt, -1, dst_pairs, capacity, dst_is_device, written);
+}
+
+// R_A in compressed-row form: the same sorted keys as cfpq_result_pairs (sparse engines) or the
+// bit-matrix rows (dense engine), written as row pointers + columns.
+extern "C" cfpq_status cfpq_result_csr(cfpq_result* r, int32_t nt, int64_t* row_ptr, int32_t* cols, int64_t capacity,
+                                       int32_t dst_is_device, int64_t* written) {
+    CFPQ_CHECK_ARG(r && written, "cfpq_result_csr: NULL argument");
+    CFPQ_CHECK_ARG(nt >= 0 && nt < r->n_nt, "cfpq_result_csr: NT id out of range");
+    CFPQ_CHECK_ARG(row_ptr != nullptr, "cfpq_result_csr: row_ptr is NULL");
+    cudaStream_t s = r->stream;
+    const int64_t n = r->n;
+    cfpq_status st;
+    int64_t* ptr_dev = row_ptr;
+    if (!dst_is_device) {
+        if (!r->d_csr_ptr && (st = dalloc(&r->d_csr_ptr, (size_t)n + 1, "CSR row pointers")) != CFPQ_OK) return st;
+        ptr_dev = r->d_csr_ptr;
+    }
+    unsigned long long m = 0;
+    int32_t* cols_dev = cols;
+    if (r->dense_mode) {
+        CFPQ_CUDA_TRY(cudaMemsetAsync(r->d_small, 0, 8, s));
+        CFPQ_CUDA_TRY(cudaMemsetAsync(r->d_rowcnt + n, 0, 4, s));
+        CFPQ_CUDA_TRY(launch_bitmap_rowcount(r->h_nt[nt].T, (int32_t)n, r->Wp, r->d_rowcnt, r->d_small, s));
+        CFPQ_CUDA_TRY(cudaMemcpyAsync(&m, r->d_small, 8, cudaMemcpyDeviceToHost, s));
+        CFPQ_CUDA_TRY(cudaStreamSynchronize(s));
+        *written = (int64_t)m;
+        CFPQ_CHECK_ARG((int64_t)m <= capacity, "cfpq_result_csr: capacity < |R_A|");
+        CFPQ_CHECK_ARG(m == 0 || cols != nullptr, "cfpq_result_csr: cols is NULL");
+        size_t need = 0;
+        CFPQ_CUDA_TRY(launch_scan(nullptr, nullptr, n + 1, nullptr, &need, s));
+        if (need > r->temp_bytes) {
+            dfree(r->d_temp);
+            if ((st = dalloc((uint8_t**)&r->d_temp, need, "scan temp")) != CFPQ_OK) return st;
+            r->temp_bytes = need;
+        }
+        CFPQ_CUDA_TRY(launch_scan(r->d_rowcnt, r->d_rowoff, n + 1, r->d_temp, &r->temp_bytes, s));
+        if (!dst_is_device && m) {
+            if ((m + 1) / 2 + 1 > r->keys_cap) {
+                dfree(r->d_keys);
+                if ((st = dalloc(&r->d_keys, (m + 1) / 2 + 1, "extraction scratch")) != CFPQ_OK) return st;
+                r->keys_cap = (m + 1) / 2 + 1;
+            }
+            cols_dev = (int32_t*)r->d_keys;
+        }
+        if (m) CFPQ_CUDA_TRY(launch_bitmap_pairs(r->h_nt[nt].T, (int32_t)n, r->Wp, r->d_rowoff, cols_dev, s, 1));
+        CFPQ_CUDA_TRY(launch_rowoff_to_ptr(r->d_rowoff, n, ptr_dev, s));
+    } else {
+        unsigned long long end = log_end(r, -1, &st);
+        if (st != CFPQ_OK) return st;
+        if ((st = sorted_keys(r, nt, end, &m)) != CFPQ_OK) return st;
+        *written = (int64_t)m;
+        CFPQ_CHECK_ARG((int64_t)m <= capacity, "cfpq_result_csr: capacity < |R_A|");
+        CFPQ_CHECK_ARG(m == 0 || cols != nullptr, "cfpq_result_csr: cols is NULL");
+        if (!dst_is_device) cols_dev = (int32_t*)(r->d_keys + m + 1);   // upper half of the key scratch
+        CFPQ_CUDA_TRY(launch_keys_to_csr(r->d_keys, m, key_bits(r), keys32(r), n, ptr_dev, cols_dev, s));
+    }
+    if (!dst_is_device) {
+        CFPQ_CUDA_TRY(cudaMemcpyAsync(row_ptr, ptr_dev, (size_t)(n + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+        if (m) CFPQ_CUDA_TRY(cudaMemcpyAsync(cols, cols_dev, m * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    }
+    CFPQ_CUDA_TRY(cudaStreamSynchronize(s));
+    return CFPQ_OK;
 }
 
 extern "C" cfpq_status cfpq_result_pairs_at(cfpq_result* r, int32_t nt, int64_t k, int32_t* dst_pairs,

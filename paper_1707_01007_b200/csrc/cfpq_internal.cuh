@@ -25,6 +25,24 @@
 
 #include "../../include/cfpq.h"
 
+// Checked build (libcfpq_checked.so, `build(checked=True)`): device-side bounds assertions on
+// the computed indices of the hot kernels (matrix words, log slots, adjacency entries); a
+// failed one prints its site and traps.  The product build compiles them out.
+#ifdef CFPQ_CHECKED
+#include <cstdio>
+#define CFPQ_DASSERT(c)                                                                    \
+    do {                                                                                   \
+        if (!(c)) {                                                                        \
+            printf("CFPQ_DASSERT failed %s:%d: %s\n", __FILE__, __LINE__, #c);           \
+            __trap();                                                                      \
+        }                                                                                  \
+    } while (0)
+#else
+#define CFPQ_DASSERT(c) \
+    do {                \
+    } while (0)
+#endif
+
 namespace cfpq {
 
 constexpr int kMaxNT = 1024;
@@ -136,6 +154,7 @@ struct EngineParams {
     const Expansion* exps;
     int32_t n_exps;
     const int32_t* adj_idx;        // concatenated CSR/CSC index array
+    long long adj_cap;             // its capacity (checked build)
     uint64_t* log;
     unsigned long long log_cap;
     EngineState* st;
@@ -285,7 +304,10 @@ size_t witness_frame_bytes();
 cudaError_t launch_bitmap_rowcount(const uint32_t* T, int32_t n, int64_t Wp, int32_t* rowcnt,
                                    unsigned long long* total, cudaStream_t s);
 cudaError_t launch_bitmap_pairs(const uint32_t* T, int32_t n, int64_t Wp, const int32_t* rowoff, int32_t* pairs,
-                                cudaStream_t s);
+                                cudaStream_t s, int cols_only = 0);
+cudaError_t launch_keys_to_csr(const void* keys, unsigned long long m, int bits, int k32, int64_t n, int64_t* row_ptr,
+                               int32_t* cols, cudaStream_t s);
+cudaError_t launch_rowoff_to_ptr(const int32_t* rowoff, int64_t n, int64_t* row_ptr, cudaStream_t s);
 
 // dense (tcgen05) engine, dense.cu
 struct DenseEngine;

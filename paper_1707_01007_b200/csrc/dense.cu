@@ -959,6 +959,7 @@ __device__ __forceinline__ int row_form(const RowsCtx& c, const DenseRule& r) {
 // OR `bits` into word w of row i of T_k,A; record what flips.  Warp-aggregated list append.
 __device__ __forceinline__ void rows_merge(const DenseParams& p, const RowsCtx& c, int A, int i, int64_t w,
                                            uint32_t bits, unsigned long long& my_new) {
+    CFPQ_DASSERT(A >= 0 && A < p.n_nt && i >= 0 && i < p.n && w >= 0 && w < p.Wp && p.Tn[A] != nullptr);
     uint32_t* addr = p.Tn[A] + (size_t)i * p.Wp + w;
     uint32_t fl = 0;
     if (bits & ~*addr) fl = bits & ~atomicOr(addr, bits);   // bits never clear: a stale load only costs the atomic
@@ -983,6 +984,7 @@ __global__ void rows_seed_kernel(DenseParams p, RowsCtx c, const uint64_t* __res
          e += (unsigned long long)gridDim.x * blockDim.x) {
         const uint64_t cell = log[e];
         const uint32_t A = cell_nt(cell), i = cell_i(cell), j = cell_j(cell);
+        CFPQ_DASSERT(A < (uint32_t)p.n_nt && i < (uint32_t)p.n && j < (uint32_t)p.n);
         atomicAdd(c.cnt + (size_t)A * p.n + i, 1u);
         if (p.Tn[A]) atomicOr(p.Tn[A] + (size_t)i * p.Wp + (j >> 5), 1u << (j & 31));
     }
@@ -997,6 +999,7 @@ __global__ void rows_delta_kernel(DenseParams p, RowsCtx c, int copy_whole) {
     if (!copy_whole) {   // the host knows the list of Δ_{k-1} is complete
         for (unsigned long long e = t0; e < m; e += stride) {
             const uint4 d = c.dlist[e];
+            CFPQ_DASSERT(e < c.dlist_cap && d.x < (uint32_t)p.n_nt && d.y < (uint32_t)p.n && d.z < (uint32_t)p.Wp);
             atomicOr(p.Tn[d.x] + (size_t)d.y * p.Wp + d.z, d.w);
         }
         return;
@@ -1229,6 +1232,7 @@ __global__ void __launch_bounds__(256, MINB) rows_rpush_kernel(DenseParams p, Ro
             const int64_t v = vbase + (int64_t)b * 32 + lane;
             x[b] = v < nv4 ? __ldg(row + v) : make_uint4(0, 0, 0, 0);
         }
+        CFPQ_DASSERT(ch.row >= 0 && ch.row < p.n && ch.count <= 32);
         const int ii = lane < ch.count ? __ldg(c.adj_idx + __ldg(c.nt[r.B].csc_ptr + ch.row) + ch.first + lane) : 0;
         bool nz = false;
 #pragma unroll
@@ -1301,8 +1305,10 @@ __global__ void __launch_bounds__(256, 4) rows_scatter_kernel(DenseParams p, Row
                             while (bits) {
                                 const int bit = __ffs(bits) - 1;
                                 bits &= bits - 1u;
-                                if (rank >= tk.first && rank < tk.first + tk.count)
+                                if (rank >= tk.first && rank < tk.first + tk.count) {
+                                    CFPQ_DASSERT(rank - tk.first < kChunkL);
                                     lst[rank - tk.first] = (int)((v * 4 + h) * 32) + bit;
+                                }
                                 ++rank;
                             }
                         }

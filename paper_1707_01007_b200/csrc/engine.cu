@@ -215,6 +215,7 @@ __global__ void log_to_bitmap_kernel(const uint64_t* __restrict__ log, unsigned 
 __device__ __forceinline__ bool try_insert(const EngineParams& p, const NTInfo* nt, const Sink& sk, bool has,
                                            uint32_t A, uint32_t i, uint32_t j, uint64_t len, long long k) {
     if (!has || i < p.row_lo || i >= p.row_hi) return false;   // rows owned by this shard only
+    CFPQ_DASSERT(A < (uint32_t)p.n_nt && i < (uint32_t)p.n && j < (uint32_t)p.n);
     uint64_t* K = nt[A].K;
     if (p.lengths && K != nullptr) {
         if (len > 0xffffffffull) {
@@ -612,6 +613,7 @@ __device__ void expand_tail(const EngineParams& p, const NTInfo* nt, const Sink&
 #pragma unroll
             for (int step = 16; step > 0; step >>= 1)
                 if (ws->off[l + step] <= t) l += step;
+            CFPQ_DASSERT((long long)ws->beg[l] + (t - ws->off[l]) < p.adj_cap);
             int32_t nbv = __ldg(p.adj_idx + ws->beg[l] + (t - ws->off[l]));
             cA = ws->A[l];
             cand_coords(ws->fixed[l], nbv, oi, oj);
@@ -626,6 +628,7 @@ __device__ void expand_tail(const EngineParams& p, const NTInfo* nt, const Sink&
 __device__ __forceinline__ int4 load_head(const NTInfo* nt, const Expansion& ex, uint32_t ci, uint32_t cj,
                                           uint32_t& A, uint32_t& fx) {
     A = (uint32_t)ex.A;
+    CFPQ_DASSERT(ci < 0x7fffffffu && cj < 0x7fffffffu && ex.other >= 0 && ex.A >= 0);
     if (ex.kind == EXP_L_CONST) {          // Δ_B entry (i, r=cj): row r of preterminal C
         fx = ci;
         return __ldg(nt[ex.other].csr_ell + cj);
@@ -966,6 +969,7 @@ __device__ __forceinline__ void clear_chunk(const EngineParams& p, unsigned long
     for (unsigned long long e = base + threadIdx.x; e < end; e += kBlock) {
         const uint64_t c = ldcg64(p.clr_log + e);
         const uint32_t A = cell_nt(c), i = cell_i(c), j = cell_j(c);
+        CFPQ_DASSERT(A < (uint32_t)p.n_nt && i < (uint32_t)p.n && j < (uint32_t)p.n);
         const NTInfo& t = p.clr_nt[A];
         if (t.T) zero_sector(t.T + (size_t)i * p.Wp + (j >> 5));
         if (t.S) zero_sector(t.S + (size_t)i * p.Wp + (j >> 5));
@@ -1102,6 +1106,7 @@ __device__ __forceinline__ void ell_place(const EngineParams& p, int sl, uint32_
     const size_t x = (size_t)sl * p.n + row;
     int* e = reinterpret_cast<int*>(p.ell + x);
     const int k = atomicAdd(p.adj_cursor + x, 1);
+    CFPQ_DASSERT((long long)e[0] + k < p.adj_cap && row < (uint32_t)p.n);
     p.adj_idx_w[e[0] + k] = nb;
     if (k == 0) e[2] = nb;          // the ELL copies are the first two CSR entries
     else if (k == 1) e[3] = nb;
@@ -1338,6 +1343,7 @@ struct WarpSoloShared {
 __device__ __forceinline__ bool ws_try(const EngineParams& p, const NTInfo* nt, uint32_t A, uint32_t i, uint32_t j,
                                        uint64_t len, long long k, int* lov, int* ovf) {
     if (i < p.row_lo || i >= p.row_hi) return false;
+    CFPQ_DASSERT(A < (uint32_t)p.n_nt && i < (uint32_t)p.n && j < (uint32_t)p.n);
     uint64_t* K = nt[A].K;
     if (p.lengths && K != nullptr) {
         if (len > 0xffffffffull) {
@@ -1427,7 +1433,9 @@ __device__ void warp_solo(const EngineParams& p, const NTInfo* nt, const Expansi
                     if (n1) ws_append(p, nt, w, base, A, a1, b1);
                     for (int t = 2; t < h.y; ++t) {
                         uint32_t a, b;
-                        cand_coords(fx, __ldg(p.adj_idx + h.x + t), a, b);
+                        CFPQ_DASSERT((long long)h.x + t < p.adj_cap);
+                        CFPQ_DASSERT((long long)h.x + t < p.adj_cap);
+                    cand_coords(fx, __ldg(p.adj_idx + h.x + t), a, b);
                         if (ws_try(p, nt, A, a, b, len_e + 1, k, &w.lov, &w.ov)) ws_append(p, nt, w, base, A, a, b);
                     }
                 } else {
@@ -1528,6 +1536,7 @@ __device__ void solo_expand(const EngineParams& p, const NTInfo* nt, const Expan
                 if (n1) solo_append(p, nt, so, slot, hi, mirror, A, a1, b1);
                 for (int t = 2; t < h.y; ++t) {
                     uint32_t a, b;
+                    CFPQ_DASSERT((long long)h.x + t < p.adj_cap);
                     cand_coords(fx, __ldg(p.adj_idx + h.x + t), a, b);
                     if (solo_try(p, nt, so, slot, A, a, b, len_e + 1, k)) solo_append(p, nt, so, slot, hi, mirror, A, a, b);
                 }

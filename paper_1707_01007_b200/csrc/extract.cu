@@ -117,8 +117,9 @@ __global__ void bitmap_rowcount_kernel(const uint32_t* __restrict__ T, int32_t n
 }
 
 // one warp per row: write (i,j) of the set bits of row i, ascending, from rowoff[i]
+// cols_only: write j into pairs[at] (the column array of the CSR form) instead of (i, j)
 __global__ void bitmap_pairs_kernel(const uint32_t* __restrict__ T, int32_t n, int64_t wn, int64_t Wp,
-                                    const int32_t* __restrict__ rowoff, int32_t* pairs) {
+                                    const int32_t* __restrict__ rowoff, int32_t* pairs, int cols_only) {
     const int lane = threadIdx.x & 31;
     for (int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; row < n;
          row += ((int64_t)gridDim.x * blockDim.x) >> 5) {
@@ -137,8 +138,12 @@ __global__ void bitmap_pairs_kernel(const uint32_t* __restrict__ T, int32_t n, i
             while (bits) {
                 int b = __ffs(bits) - 1;
                 bits &= bits - 1u;
-                pairs[2 * at] = (int32_t)row;
-                pairs[2 * at + 1] = (int32_t)(w * 32 + b);
+                if (cols_only) {
+                    pairs[at] = (int32_t)(w * 32 + b);
+                } else {
+                    pairs[2 * at] = (int32_t)row;
+                    pairs[2 * at + 1] = (int32_t)(w * 32 + b);
+                }
                 ++at;
             }
             base += __shfl_sync(0xffffffffu, incl, 31);
@@ -157,12 +162,51 @@ cudaError_t launch_bitmap_rowcount(const uint32_t* T, int32_t n, int64_t Wp, int
 }
 
 cudaError_t launch_bitmap_pairs(const uint32_t* T, int32_t n, int64_t Wp, const int32_t* rowoff, int32_t* pairs,
-                                cudaStream_t s) {
+                                cudaStream_t s, int cols_only) {
     if (n) {
         int64_t blocks = ((int64_t)n * 32 + 255) / 256;
         if (blocks > 148 * 16) blocks = 148 * 16;
-        bitmap_pairs_kernel<<<(int)blocks, 256, 0, s>>>(T, n, (n + 31) / 32, Wp, rowoff, pairs);
+        bitmap_pairs_kernel<<<(int)blocks, 256, 0, s>>>(T, n, (n + 31) / 32, Wp, rowoff, pairs, cols_only);
     }
+    return cudaGetLastError();
+}
+
+// CSR of sorted compact keys (i << bits | j): cols[t] = j; row_ptr[r] = first t with row >= r
+// (every row written exactly once: by the entry that opens it or, past the last entry, by it).
+__global__ void keys_to_csr_kernel(const void* __restrict__ keys, unsigned long long m, int bits, int k32, int64_t n,
+                                   int64_t* row_ptr, int32_t* cols) {
+    for (unsigned long long t = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; t < m;
+         t += (unsigned long long)gridDim.x * blockDim.x) {
+        auto key = [&](unsigned long long e) -> uint64_t {
+            return k32 ? (uint64_t)reinterpret_cast<const uint32_t*>(keys)[e] : reinterpret_cast<const uint64_t*>(keys)[e];
+        };
+        const uint64_t k = key(t);
+        const int64_t i = (int64_t)(k >> bits);
+        CFPQ_DASSERT(i < n);
+        cols[t] = (int32_t)(k & ((1ull << bits) - 1ull));
+        const int64_t prev = t ? (int64_t)(key(t - 1) >> bits) : -1;
+        for (int64_t r = prev + 1; r <= i; ++r) row_ptr[r] = (int64_t)t;
+        if (t == m - 1)
+            for (int64_t r = i + 1; r <= n; ++r) row_ptr[r] = (int64_t)m;
+    }
+}
+
+__global__ void rowoff_to_ptr_kernel(const int32_t* __restrict__ rowoff, int64_t n1, int64_t* row_ptr) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n1; t += (int64_t)gridDim.x * blockDim.x)
+        row_ptr[t] = rowoff[t];
+}
+
+static int grid_for(unsigned long long work);
+
+cudaError_t launch_keys_to_csr(const void* keys, unsigned long long m, int bits, int k32, int64_t n, int64_t* row_ptr,
+                               int32_t* cols, cudaStream_t s) {
+    if (m == 0) return cudaMemsetAsync(row_ptr, 0, (size_t)(n + 1) * sizeof(int64_t), s);
+    keys_to_csr_kernel<<<grid_for(m), 256, 0, s>>>(keys, m, bits, k32, n, row_ptr, cols);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_rowoff_to_ptr(const int32_t* rowoff, int64_t n, int64_t* row_ptr, cudaStream_t s) {
+    rowoff_to_ptr_kernel<<<grid_for((unsigned long long)n + 1), 256, 0, s>>>(rowoff, n + 1, row_ptr);
     return cudaGetLastError();
 }
 
