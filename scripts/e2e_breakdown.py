@@ -46,6 +46,21 @@ for it in range(25):
     if it >= 5:
         T["pairs_dev"].append(t5 - t4)
         T["count"].append(t6 - t5)
+# the same step reading R_start back as CSR (cfpq_result_csr) instead of pairs
+rp = torch.empty((w.n_nodes + 1,), dtype=torch.int64).pin_memory()
+cols = torch.empty((m,), dtype=torch.int32).pin_memory()
+T["csr_host"], T["total_csr"] = [], []
+for it in range(25):
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    d.set_edges(pinned, stream=stream)
+    C.closure_reuse(g, d, r, stream=stream)
+    t2 = time.perf_counter()
+    r.csr(w.start, rp, cols)
+    t3 = time.perf_counter()
+    if it >= 5:
+        T["csr_host"].append(t3 - t2)
+        T["total_csr"].append(t3 - t0)
 for k, v in T.items():
     print(f"{k:12s} {1e3 * np.median(v):8.3f} ms (median)  min {1e3 * min(v):8.3f}")
 st = r.stats()

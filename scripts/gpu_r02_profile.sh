@@ -41,7 +41,7 @@ from paper_1707_01007_b200 import cfpq as C
 w=I.config4_workload(); g=C.Grammar.from_workload(w); d=C.Graph(w.n_nodes, torch.from_numpy(w.edges).cuda())
 r=C.closure(g,d,path_policy=3)
 " > $O/ncu_rows_scatter.txt 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:rows_rgather_kernel -s 6 -c 1 -o $O/prof_rows_rgather \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:rows_rpush_kernel -s 6 -c 1 -o $O/prof_rows_rpush \
    python -c "
 import sys; sys.path.insert(0,'.')
 import torch, inputs as I
