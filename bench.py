@@ -825,12 +825,13 @@ def main():
             out_pairs = torch.empty((max(results_start, 1), 2), dtype=torch.int32).pin_memory()
         h2d = pinned.numel() * 4
         d2h = 0
-        ts = []
+        ts, t_run, t_read = [], [], []
         for it in range(args.warmup + args.steps):
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             d.set_edges(pinned, stream=stream)
             C.closure_reuse(g, d, r, **kw, **shard_kw)
+            ta = time.perf_counter()
             if csr:
                 rp, cols = r.csr(w.start, out_ptr, out_cols)
             else:
@@ -838,6 +839,8 @@ def main():
             t1 = time.perf_counter()
             if it >= args.warmup:
                 ts.append(t1 - t0)
+                t_run.append(ta - t0)
+                t_read.append(t1 - ta)
                 d2h = rp.numel() * 8 + cols.numel() * 4 if csr else pairs.numel() * 4
         e_total = torch.tensor([sum(ts)], dtype=torch.float64, device="cuda")
         if world > 1:
@@ -845,6 +848,8 @@ def main():
         e2e = {"value": useful_job * len(ts) / float(e_total.item()) / 1e9, "unit": UNIT,
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                "ms_per_step": 1e3 * float(e_total.item()) / len(ts),
+               "median_ms": {"upload_and_closure": 1e3 * statistics.median(t_run),
+                             "result_read": 1e3 * statistics.median(t_read)},
                "result": ("R_start as CSR (cfpq_result_csr: int64 row pointers + int32 columns)" if csr else
                           "R_start as sorted (i, j) int32 pairs (cfpq_result_pairs)") + " into pinned host memory"}
 
