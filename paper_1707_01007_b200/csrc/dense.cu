@@ -941,6 +941,12 @@ struct RowsCtx {
     unsigned long long chunk_cap;      // capacity of each chunk list (the products clamp to it;
                                        // the host re-runs the shard when a list overflowed)
     int32_t push;                      // form R by input row: chunks of CSC_B(r) (rows_rpush_kernel)
+    // compact mode (unsharded runs without V rules): the plan lists whole operand rows with an
+    // output offset; rows_compact_kernel streams them into entry lists (L: set bits of T_B[i],
+    // R: non-zero words of T_C[r]); rows_lmerge / rows_rmerge merge the entries
+    int32_t compact;
+    uint4* elist;                      // [2 * ecap]: L entries, then R entries
+    unsigned long long ecap;
 };
 
 enum : int { RF_NONE = 0, RF_L = 1, RF_R = 2, RF_V = 3, RF_P = 4 };
@@ -1021,8 +1027,8 @@ constexpr int kPlanRules = 64;   // rule forms cached in shared memory up to thi
 __global__ void rows_plan_kernel(DenseParams p, RowsCtx c, RowChunk* chunks, unsigned long long cap) {
     __shared__ int32_t s_form[kPlanRules], s_B[kPlanRules];
     __shared__ const int32_t* s_ptr[kPlanRules];
-    __shared__ int32_t s_wsum[3][32];
-    __shared__ unsigned long long s_base[3];
+    __shared__ int32_t s_wsum[5][32];
+    __shared__ unsigned long long s_base[5];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const bool cached = c.n_rules <= kPlanRules;
     if (cached) {
@@ -1062,7 +1068,30 @@ __global__ void rows_plan_kernel(DenseParams p, RowsCtx c, RowChunk* chunks, uns
                 f = row_form(c, r);
                 bptr = c.nt[r.B].csr_ptr;
             }
-            if (f == RF_R && c.push) {
+            if (f == RF_R && c.compact) {
+                // compact: one task per non-empty input row T_C[r] with output rows (CSC_B(r));
+                // its entries (<= cnt non-zero words) get slots [off, off + cnt) of the R list
+                const int32_t* cp = c.nt[r.B].csc_ptr;
+                const uint32_t cc = c.cnt[(size_t)p.rules[q].C * p.n + i];
+                if (cc && __ldg(cp + i + 1) > __ldg(cp + i)) {
+                    len = (int)cc;
+                    per = 1 << 30;   // one task
+                }
+            } else if (f == RF_L && c.compact) {
+                // compact: one task per non-empty T_B[i] per group of L rules sharing B; its set
+                // bits get slots [off, off + cnt) of the L list
+                if (c.l_next[q] >= -1) {
+                    len = (int)c.cnt[(size_t)r.B * p.n + i];
+                    per = 1 << 30;
+                    isv = 1;         // listed in the V slot (unused in compact mode)
+                }
+            } else if (f == RF_P && c.compact) {
+                // compact, iteration 1: both operands preterminal — the set bits of T_B[i] (= CSR_B(i),
+                // constant) listed like an L row; the merge applies this rule alone (not a group)
+                len = (int)c.cnt[(size_t)r.B * p.n + i];
+                per = 1 << 30;
+                isv = 1;
+            } else if (f == RF_R && c.push) {
                 // push form: task row = input row r of T_C (non-empty), chunks of CSC_B(r)
                 const int32_t* cp = c.nt[r.B].csc_ptr;
                 len = c.cnt[(size_t)p.rules[q].C * p.n + i] ? __ldg(cp + i + 1) - __ldg(cp + i) : 0;
@@ -1088,13 +1117,15 @@ __global__ void rows_plan_kernel(DenseParams p, RowsCtx c, RowChunk* chunks, uns
             }
             nch = (len + per - 1) / per;
         }
-        // three lists: 0 = R chunks (rc[0]), 1 = V chunks (rc[3]), 2 = L chunks / P tasks (rc[4]).
-        // Warp inclusive scans, then one atomic per list per CTA (not per warp: the three
+        // three lists: 0 = R chunks (rc[0]), 1 = V chunks (rc[3]), 2 = L chunks / P tasks (rc[4]);
+        // compact mode also sums the entry slots of its R tasks (rc[6]) and L tasks (rc[5]).
+        // Warp inclusive scans, then one atomic per list per CTA (not per warp: the
         // counters are hot), bases handed back through shared memory
-        const int cntv[3] = {isv ? 0 : nch, isv ? nch : 0, lp};
-        int incl[3];
+        const bool cpt = c.compact && nch == 1 && per == (1 << 30);
+        const int cntv[5] = {isv ? 0 : nch, isv ? nch : 0, lp, cpt && !isv ? len : 0, cpt && isv ? len : 0};
+        int incl[5];
 #pragma unroll
-        for (int l = 0; l < 3; ++l) {
+        for (int l = 0; l < 5; ++l) {
             incl[l] = cntv[l];
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
@@ -1104,13 +1135,21 @@ __global__ void rows_plan_kernel(DenseParams p, RowsCtx c, RowChunk* chunks, uns
             if (lane == 31) s_wsum[l][warp] = incl[l];
         }
         __syncthreads();
-        if (threadIdx.x < 3) {
+        if (threadIdx.x < 5) {
             const int l = threadIdx.x;
             unsigned long long tot = 0;
             for (int q2 = 0; q2 < (int)(blockDim.x >> 5); ++q2) tot += (unsigned long long)s_wsum[l][q2];
-            s_base[l] = tot ? atomicAdd(c.rc + (l == 0 ? 0 : (l == 1 ? 3 : 4)), tot) : 0ull;
+            const int ctr[5] = {0, 3, 4, 6, 5};
+            s_base[l] = tot ? atomicAdd(c.rc + ctr[l], tot) : 0ull;
         }
         __syncthreads();
+        unsigned long long ebase = 0;   // compact task: its first entry slot
+        if (cpt) {
+            const int l = isv ? 4 : 3;
+            ebase = s_base[l];
+            for (int q2 = 0; q2 < warp; ++q2) ebase += (unsigned long long)s_wsum[l][q2];
+            ebase += (unsigned long long)(incl[l] - cntv[l]);
+        }
 #pragma unroll
         for (int l = 0; l < 3; ++l) {
             unsigned long long at = s_base[l];
@@ -1118,6 +1157,11 @@ __global__ void rows_plan_kernel(DenseParams p, RowsCtx c, RowChunk* chunks, uns
             at += (unsigned long long)(incl[l] - cntv[l]);
             if (l < 2) {
                 RowChunk* out = chunks + (l ? cap : 0);
+                if (cpt) {
+                    // first = the entry slot (< 2^31: the host caps the entry lists below it)
+                    if (cntv[l] && at < cap) out[at] = RowChunk{q, i, (int32_t)ebase, len};
+                    continue;
+                }
                 for (int h = 0; h < cntv[l]; ++h, ++at)
                     if (at < cap) out[at] = RowChunk{q, i, h * per, min(per, len - h * per)};
             } else {
@@ -1254,6 +1298,133 @@ __global__ void __launch_bounds__(256, MINB) rows_rpush_kernel(DenseParams p, Ro
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) my_new += __shfl_xor_sync(0xffffffffu, my_new, o);
     if (lane == 0 && my_new) atomicAdd(p.new_cells + p.n_nt, my_new);
+}
+
+// ---- compact mode: stream whole operand rows into entry lists, then merge the entries ----
+// The streaming pass reads each listed row once (16-byte loads, kCompactB per lane in flight)
+// and is HBM-bound; the merges (adjacency lookups, pre-check, atomic) run as one thread per
+// entry over the whole GPU instead of inside the warp that scanned the row.
+constexpr int kCompactB = 4;
+
+// MODE 0 (L): tasks = (leader rule, row i of T_B, slot, count) -> entries {rule, i, r, 1} for
+// every set bit r of T_{k-1},B[i].  MODE 1 (R): tasks = (rule, row r of T_C, slot, count) ->
+// entries {rule, r, word, bits} for every non-zero word.  Slots past the row's entries are
+// written invalid (w = 0): count is the row's popcount in T_k, an upper bound.
+template <int MODE>
+__global__ void __launch_bounds__(256) rows_compact_kernel(DenseParams p, RowsCtx c, const RowChunk* __restrict__ tasks,
+                                                           int counter) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nv4 = ((p.n + 31) / 32 + 3) / 4;
+    const unsigned long long m = min(c.rc[counter], c.chunk_cap);
+    uint4* out = c.elist + (MODE ? c.ecap : 0);
+    for (unsigned long long t = (blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x) >> 5; t < m;
+         t += ((unsigned long long)gridDim.x * blockDim.x) >> 5) {
+        const RowChunk tk = tasks[t];
+        const DenseRule r = p.rules[tk.rule];
+        const int X = MODE ? r.C : r.B;
+        CFPQ_DASSERT(tk.row >= 0 && tk.row < p.n && tk.first >= 0);
+        const uint4* row = reinterpret_cast<const uint4*>(p.T[X] + (size_t)tk.row * p.Wp);
+        const unsigned long long base = (unsigned long long)(uint32_t)tk.first;
+        const unsigned long long lim = base + (unsigned long long)tk.count;
+        unsigned long long at0 = base;   // next slot (warp-uniform)
+        for (int64_t v0 = 0; v0 < nv4; v0 += 32 * kCompactB) {
+            uint4 x[kCompactB];
+#pragma unroll
+            for (int b = 0; b < kCompactB; ++b) {
+                const int64_t v = v0 + (int64_t)b * 32 + lane;
+                x[b] = v < nv4 ? __ldg(row + v) : make_uint4(0, 0, 0, 0);
+            }
+#pragma unroll
+            for (int b = 0; b < kCompactB; ++b) {
+                const uint32_t wd[4] = {x[b].x, x[b].y, x[b].z, x[b].w};
+                int cntl = 0;
+#pragma unroll
+                for (int q = 0; q < 4; ++q) cntl += MODE ? (wd[q] != 0u) : __popc(wd[q]);
+                int incl = cntl;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int v = __shfl_up_sync(0xffffffffu, incl, o);
+                    if (lane >= o) incl += v;
+                }
+                const int total = __shfl_sync(0xffffffffu, incl, 31);
+                if (cntl) {
+                    unsigned long long at = at0 + (unsigned long long)(incl - cntl);
+                    const int64_t v = v0 + (int64_t)b * 32 + lane;
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        uint32_t bits = wd[q];
+                        if (MODE) {
+                            if (bits) {
+                                if (at < lim && at < c.ecap)
+                                    out[at] = make_uint4((uint32_t)tk.rule, (uint32_t)tk.row, (uint32_t)(4 * v + q), bits);
+                                ++at;
+                            }
+                        } else {
+                            while (bits) {
+                                const int bt = __ffs(bits) - 1;
+                                bits &= bits - 1u;
+                                if (at < lim && at < c.ecap)
+                                    out[at] = make_uint4((uint32_t)tk.rule, (uint32_t)tk.row,
+                                                         (uint32_t)((4 * v + q) * 32 + bt), 1u);
+                                ++at;
+                            }
+                        }
+                    }
+                }
+                at0 += (unsigned long long)total;
+            }
+        }
+        for (unsigned long long e = at0 + lane; e < lim; e += 32)
+            if (e < c.ecap) out[e] = make_uint4(0, 0, 0, 0);
+    }
+}
+
+// L entries {leader rule, i, r}: every rule A -> B C_g of the group, j in CSR_C_g(r).
+__global__ void __launch_bounds__(256) rows_lmerge_kernel(DenseParams p, RowsCtx c, const int32_t* __restrict__ rule_out) {
+    const unsigned long long m = min(c.rc[5], c.ecap);
+    unsigned long long my_new = 0;
+    for (unsigned long long e = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; e < m;
+         e += (unsigned long long)gridDim.x * blockDim.x) {
+        const uint4 en = c.elist[e];
+        if (!en.w) continue;
+        const int i = (int)en.y, rr = (int)en.z;
+        CFPQ_DASSERT(i < p.n && rr < p.n);
+        for (int qq = (int)en.x; qq >= 0; qq = rows_l_follow(c.l_next[qq])) {
+            const int32_t* cp = c.nt[p.rules[qq].C].csr_ptr;
+            const int e1 = __ldg(cp + rr + 1);
+            const int A = rule_out[qq];
+            for (int f2 = __ldg(cp + rr); f2 < e1; ++f2) {
+                const int j = __ldg(c.adj_idx + f2);
+                rows_merge(p, c, A, i, j >> 5, 1u << (j & 31), my_new);
+            }
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) my_new += __shfl_xor_sync(0xffffffffu, my_new, o);
+    if ((threadIdx.x & 31) == 0 && my_new) atomicAdd(p.new_cells + p.n_nt, my_new);
+}
+
+// R entries {rule, r, word, bits}: OR bits into word `word` of every row i in CSC_B(r).
+__global__ void __launch_bounds__(256) rows_rmerge_kernel(DenseParams p, RowsCtx c, const int32_t* __restrict__ rule_out) {
+    const unsigned long long m = min(c.rc[6], c.ecap);
+    unsigned long long my_new = 0;
+    for (unsigned long long e = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; e < m;
+         e += (unsigned long long)gridDim.x * blockDim.x) {
+        const uint4 en = c.elist[c.ecap + e];
+        if (!en.w) continue;
+        const int q = (int)en.x, rr = (int)en.y;
+        CFPQ_DASSERT(rr < p.n && (int64_t)en.z < p.Wp);
+        const int32_t* cp = c.nt[p.rules[q].B].csc_ptr;
+        const int e1 = __ldg(cp + rr + 1);
+        const int A = rule_out[q];
+        for (int f2 = __ldg(cp + rr); f2 < e1; ++f2) {
+            const int i = __ldg(c.adj_idx + f2);
+            rows_merge(p, c, A, i, (int64_t)en.z, en.w, my_new);
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) my_new += __shfl_xor_sync(0xffffffffu, my_new, o);
+    if ((threadIdx.x & 31) == 0 && my_new) atomicAdd(p.new_cells + p.n_nt, my_new);
 }
 
 // Forms L and P: one warp per task of the plan's list: an L chunk (<= kChunkL set bits of one row of T_B)
@@ -1577,6 +1748,10 @@ struct DenseEngine {
     void* dlist = nullptr;                     // bit-row path: Δ_k word list (uint4)
     unsigned long long dlist_cap = 0;
     unsigned long long* rc = nullptr;          // bit-row path counters
+    uint4* elist = nullptr;                    // bit-row compact mode: L / R entry lists [2 * ecap]
+    unsigned long long ecap = 0;
+    cudaStream_t side = nullptr;               // compact mode: the R pipeline runs beside the L one
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     int32_t launch_mode = 0;                   // cfpq_options.dense_launch
     int32_t rgather_variant = 0;               // diagnostics (diag_flags bits 4-6): R-form kernel shape
     unsigned long long* h_rc = nullptr;        // bit-row path counters, pinned host copy
@@ -1592,6 +1767,10 @@ struct DenseEngine {
         cudaFree(chunks);
         cudaFree(rcnt);
         cudaFree(dlist);
+        cudaFree(elist);
+        if (ev_fork) cudaEventDestroy(ev_fork);
+        if (ev_join) cudaEventDestroy(ev_join);
+        if (side) cudaStreamDestroy(side);
         cudaFree(rc);
         cudaFree(T8); cudaFree(T8T); cudaFree(occ); cudaFree(mapA_row); cudaFree(mapB_row); cudaFree(out_nt);
         cudaFree(rule_ptr); cudaFree(rules); cudaFree(Tptr); cudaFree(Tnptr); cudaFree(new_cells);
@@ -1945,7 +2124,7 @@ cudaError_t rows_begin(DenseEngine* e, const NTInfo* nt, const int32_t* adj_idx,
     if (launches) *launches += 1;
     // Δ_k list and chunk counters restart
     if ((c = cudaMemsetAsync(e->rc, 0, 2 * 8, s)) != cudaSuccess) return c;
-    if ((c = cudaMemsetAsync(e->rc + 3, 0, 2 * 8, s)) != cudaSuccess) return c;
+    if ((c = cudaMemsetAsync(e->rc + 3, 0, 4 * 8, s)) != cudaSuccess) return c;   // + compact entry slots
     return cudaGetLastError();
 }
 
@@ -1960,15 +2139,28 @@ cudaError_t rows_shard(DenseEngine* e, int64_t row_lo, int64_t row_hi, cudaStrea
     // shards gather their own output rows (rgather variants 1-4 and 7 force the gather, A/B)
     const bool push = row_lo == 0 && row_hi == e->n && (e->rgather_variant == 0 || e->rgather_variant == 5 ||
                                                          e->rgather_variant == 6);
+    // compact mode (default on unsharded runs without rules whose two operands change): whole
+    // operand rows streamed into entry lists, entries merged by one thread each (variant 0)
+    const bool compact = push && !e->has_v && e->rgather_variant == 0;
+    if (compact && !e->elist) {
+        e->ecap = 1ull << 21;
+        if ((c = cudaMalloc(&e->elist, 2 * e->ecap * sizeof(uint4))) != cudaSuccess) return c;
+    }
+    if (compact && !e->side) {
+        if ((c = cudaStreamCreateWithFlags(&e->side, cudaStreamNonBlocking)) != cudaSuccess) return c;
+        if ((c = cudaEventCreateWithFlags(&e->ev_fork, cudaEventDisableTiming)) != cudaSuccess) return c;
+        if ((c = cudaEventCreateWithFlags(&e->ev_join, cudaEventDisableTiming)) != cudaSuccess) return c;
+    }
     RowsCtx rc{e->rows_nt, e->rows_adj, e->rcnt, (uint4*)e->dlist, e->dlist_cap, e->rc, e->rows_first ? 1 : 0,
-               n_rules, (int32_t)row_lo, (int32_t)row_hi, e->l_next, e->chunk_cap, push ? 1 : 0};
+               n_rules, (int32_t)row_lo, (int32_t)row_hi, e->l_next, e->chunk_cap, push ? 1 : 0,
+               compact ? 1 : 0, e->elist, compact ? e->ecap : 0};
     const int sms = device_sms();
     // plan and products back to back, no host round trip: the products clamp every list to
     // its capacity and the counters are copied to pinned host memory behind them; the host
     // checks them after the iteration's synchronisation (rows_shard_check) and re-runs the
     // shard if a list overflowed (products are idempotent ORs; Δ_k records only new flips)
     if ((c = cudaMemsetAsync(e->rc, 0, 8, s)) != cudaSuccess) return c;       // chunk lists of this shard
-    if ((c = cudaMemsetAsync(e->rc + 3, 0, 2 * 8, s)) != cudaSuccess) return c;
+    if ((c = cudaMemsetAsync(e->rc + 3, 0, 4 * 8, s)) != cudaSuccess) return c;   // + compact entry slots
     rows_plan_kernel<<<sms * 8, 256, 0, s>>>(p, rc, (RowChunk*)e->chunks, e->chunk_cap);
     // 4 CTAs x 8 warps per SM (measured: 6 or 8 CTAs with fewer registers are not faster)
     rows_scatter_kernel<<<resident_grid(rows_scatter_kernel, 256, sms), 256, 0, s>>>(p, rc, e->rule_out,
@@ -1983,8 +2175,25 @@ cudaError_t rows_shard(DenseEngine* e, int64_t row_lo, int64_t row_hi, cudaStrea
         else if (nv <= 4) rows_gather_kernel<4><<<sms * 8, kRowThreads, 0, s>>>(p, rc, e->rule_out, ch, counter);
         else rows_gather_kernel<8><<<sms * 8, kRowThreads, 0, s>>>(p, rc, e->rule_out, ch, counter);
     };
-    if (e->has_v) cta_gather(chV, 3);
-    if (e->has_r) {
+    if (compact) {
+        // L: tasks in the V slot (rc[3]) -> entries [0, rc[5]); R: tasks in the R slot (rc[0]) ->
+        // entries [ecap, ecap + rc[6]); then the merges.  The R pipeline runs on a side stream
+        // beside the L one: each is a bandwidth-bound stream followed by latency-bound merges,
+        // and the two overlap (they read T_{k-1} and OR into T_k with idempotent atomics)
+        if (e->has_r) {
+            if ((c = cudaEventRecord(e->ev_fork, s)) != cudaSuccess) return c;
+            if ((c = cudaStreamWaitEvent(e->side, e->ev_fork, 0)) != cudaSuccess) return c;
+            rows_compact_kernel<1><<<sms * 8, 256, 0, e->side>>>(p, rc, chR, 0);
+            rows_rmerge_kernel<<<sms * 16, 256, 0, e->side>>>(p, rc, e->rule_out);
+            if ((c = cudaEventRecord(e->ev_join, e->side)) != cudaSuccess) return c;
+        }
+        rows_compact_kernel<0><<<sms * 8, 256, 0, s>>>(p, rc, chV, 3);
+        rows_lmerge_kernel<<<sms * 16, 256, 0, s>>>(p, rc, e->rule_out);
+        if (e->has_r && (c = cudaStreamWaitEvent(s, e->ev_join, 0)) != cudaSuccess) return c;
+        if (launches) *launches += e->has_r ? 4 : 2;
+    }
+    if (e->has_v && !compact) cta_gather(chV, 3);
+    if (e->has_r && !compact) {
         // R chunks: a warp per (chunk, row slice of 32 x NVW uint4): many light warps
         // (config 4, one row in flight: 2 uint4 per lane 10.2 ms closure; 4 / 8 / 16: 10.7 /
         // 11.8 / 16.0 ms; 1: 11.5 ms); variants with RU rows in flight (rgather_variant)
@@ -2010,7 +2219,7 @@ cudaError_t rows_shard(DenseEngine* e, int64_t row_lo, int64_t row_hi, cudaStrea
         }
     }
     if (launches) *launches += 2 + (e->has_v ? 1 : 0) + (e->has_r ? 1 : 0);
-    if ((c = cudaMemcpyAsync(e->h_rc, e->rc, 5 * 8, cudaMemcpyDeviceToHost, s)) != cudaSuccess) return c;
+    if ((c = cudaMemcpyAsync(e->h_rc, e->rc, 7 * 8, cudaMemcpyDeviceToHost, s)) != cudaSuccess) return c;
     return cudaGetLastError();
 }
 
@@ -2037,6 +2246,16 @@ cudaError_t rows_shard_check(DenseEngine* e, cudaStream_t s, bool* redo, bool ch
         cudaFree(e->chunks);
         e->chunk_cap = need + need / 4;
         if ((c = cudaMalloc(&e->chunks, 3 * e->chunk_cap * sizeof(RowChunk))) != cudaSuccess) return c;
+        *redo = true;
+    }
+    // compact mode: an entry list that ran out (slots are task offsets: keep them < 2^31)
+    const unsigned long long eneed = std::max(got[5], got[6]);
+    if (e->elist && eneed > e->ecap) {
+        if (eneed >= (1ull << 31)) return cudaErrorInvalidValue;
+        cudaFree(e->elist);
+        e->elist = nullptr;
+        e->ecap = std::min<unsigned long long>(eneed + eneed / 4, (1ull << 31) - 1);
+        if ((c = cudaMalloc(&e->elist, 2 * e->ecap * sizeof(uint4))) != cudaSuccess) return c;
         *redo = true;
     }
     return cudaSuccess;
