@@ -983,6 +983,13 @@ __device__ __forceinline__ void rows_merge(const DenseParams& p, const RowsCtx& 
     my_new += __popc(fl);
 }
 
+// Per-shard counter reset in one launch: chunk list R (rc[0]), optionally the Δ list length
+// (rc[1]), lists V / L-P and the compact entry slots (rc[3..6]); rc[2] (sticky) is kept.
+__global__ void rows_reset_kernel(unsigned long long* rc, int with_list) {
+    const int t = threadIdx.x;
+    if (t == 0 || (t == 1 && with_list) || (t >= 3 && t <= 6)) rc[t] = 0ull;
+}
+
 // Iteration 1: the zeroed T_k buffers take T_0 (the seed cells of the outputs, from the
 // log) and cnt[X][i] = |row i of T_0,X| for every NT.
 __global__ void rows_seed_kernel(DenseParams p, RowsCtx c, const uint64_t* __restrict__ log, unsigned long long n_seeds) {
@@ -1755,6 +1762,7 @@ struct DenseEngine {
     int32_t launch_mode = 0;                   // cfpq_options.dense_launch
     int32_t rgather_variant = 0;               // diagnostics (diag_flags bits 4-6): R-form kernel shape
     unsigned long long* h_rc = nullptr;        // bit-row path counters, pinned host copy
+    unsigned long long* h_new = nullptr;       // new-cell counters, pinned host copy (dense_finish)
     bool list_complete = true;                 // the Δ word list of the last iteration holds every word
     const NTInfo* rows_nt = nullptr;           // bit-row path: this iteration's NT table / CSR
     const int32_t* rows_adj = nullptr;
@@ -1764,6 +1772,7 @@ struct DenseEngine {
         cudaFree(rule_out);
         cudaFree(l_next);
         if (h_rc) cudaFreeHost(h_rc);
+        if (h_new) cudaFreeHost(h_new);
         cudaFree(chunks);
         cudaFree(rcnt);
         cudaFree(dlist);
@@ -2123,8 +2132,7 @@ cudaError_t rows_begin(DenseEngine* e, const NTInfo* nt, const int32_t* adj_idx,
     }
     if (launches) *launches += 1;
     // Δ_k list and chunk counters restart
-    if ((c = cudaMemsetAsync(e->rc, 0, 2 * 8, s)) != cudaSuccess) return c;
-    if ((c = cudaMemsetAsync(e->rc + 3, 0, 4 * 8, s)) != cudaSuccess) return c;   // + compact entry slots
+    rows_reset_kernel<<<1, 32, 0, s>>>(e->rc, 1);
     return cudaGetLastError();
 }
 
@@ -2159,8 +2167,7 @@ cudaError_t rows_shard(DenseEngine* e, int64_t row_lo, int64_t row_hi, cudaStrea
     // its capacity and the counters are copied to pinned host memory behind them; the host
     // checks them after the iteration's synchronisation (rows_shard_check) and re-runs the
     // shard if a list overflowed (products are idempotent ORs; Δ_k records only new flips)
-    if ((c = cudaMemsetAsync(e->rc, 0, 8, s)) != cudaSuccess) return c;       // chunk lists of this shard
-    if ((c = cudaMemsetAsync(e->rc + 3, 0, 4 * 8, s)) != cudaSuccess) return c;   // + compact entry slots
+    rows_reset_kernel<<<1, 32, 0, s>>>(e->rc, 0);   // chunk lists of this shard, compact entry slots
     rows_plan_kernel<<<sms * 8, 256, 0, s>>>(p, rc, (RowChunk*)e->chunks, e->chunk_cap);
     // 4 CTAs x 8 warps per SM (measured: 6 or 8 CTAs with fewer registers are not faster)
     rows_scatter_kernel<<<resident_grid(rows_scatter_kernel, 256, sms), 256, 0, s>>>(p, rc, e->rule_out,
@@ -2336,13 +2343,13 @@ cudaError_t rows_apply_all(DenseEngine* e, unsigned long long total, cudaStream_
 }
 
 cudaError_t dense_finish(DenseEngine* e, cudaStream_t s, unsigned long long* new_total) {
-    std::vector<unsigned long long> h(e->n_nt + 2);
     cudaError_t c;
-    if ((c = cudaMemcpyAsync(h.data(), e->new_cells, (e->n_nt + 2) * 8, cudaMemcpyDeviceToHost, s)) != cudaSuccess)
+    if (!e->h_new && (c = cudaMallocHost(&e->h_new, (e->n_nt + 2) * 8)) != cudaSuccess) return c;
+    if ((c = cudaMemcpyAsync(e->h_new, e->new_cells, (e->n_nt + 2) * 8, cudaMemcpyDeviceToHost, s)) != cudaSuccess)
         return c;
     if ((c = cudaStreamSynchronize(s)) != cudaSuccess) return c;
-    *new_total = h[e->n_nt];
-    e->kblocks_total += h[e->n_nt + 1];
+    *new_total = e->h_new[e->n_nt];
+    e->kblocks_total += e->h_new[e->n_nt + 1];
     return cudaSuccess;
 }
 
