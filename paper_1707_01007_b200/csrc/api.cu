@@ -177,6 +177,7 @@ struct cfpq_result {
     int32_t* d_rowoff = nullptr;
     int64_t* d_csr_ptr = nullptr;             // CSR row pointers for a host destination [n+1]
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    cudaEvent_t pipe_ev[2] = {nullptr, nullptr};   // pipelined bit-row iterations
     double seed_ns = 0, loop_ns = 0;
 
     // second workspace bank (see Bank)
@@ -199,6 +200,8 @@ struct cfpq_result {
         if (spare_clean) cudaEventDestroy(spare_clean);
         if (main_done) cudaEventDestroy(main_done);
         for (auto& e : ev)
+            if (e) cudaEventDestroy(e);
+        for (auto& e : pipe_ev)
             if (e) cudaEventDestroy(e);
         dfree(d_T); dfree(d_snap); dfree(d_K); dfree(d_nt); dfree(d_exps); dfree(d_rules);
         dfree(d_lab_ptr); dfree(d_lab_nt); dfree(d_slot_row); dfree(d_slot_col); dfree(d_adj_cnt);
@@ -1043,6 +1046,90 @@ static cfpq_status dense_grid_iteration(cfpq_result* r, int* launches) {
 
 // Dense engine loop (path_policy 2): host-driven Jacobi iterations, one tcgen05 product
 // launch (+ packs) per iteration; T and Tn swap roles after every iteration.
+// Pipelined bit-row iterations (one GPU, compact mode): iteration k+1 is enqueued before the
+// host reads iteration k's outcome (rows_pipe_iteration), so the host round trip of every
+// iteration overlaps the next one's products; the device stop flag turns the speculative
+// iteration after the fixpoint / cap / a list overflow into a no-op.  A list that ran out at
+// iteration k is handled exactly as in the unpipelined loop (grow, redo k's products).
+static cfpq_status rows_pipelined_loop(cfpq_result* r, int64_t start_k, int64_t* k_out, bool* capped) {
+    cudaStream_t s = r->stream;
+    DenseEngine* e = r->dense;
+    const auto& outs = dense_outputs(e);
+    for (auto& ev : r->pipe_ev)
+        if (!ev) CFPQ_CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    CFPQ_CUDA_TRY(rows_pipe_begin(e, r->Tcur.data(), r->Tnxt.data(), s));
+    const long long cap = r->opts.max_iterations;
+    int64_t k = start_k + 1;
+    int slot = 0;
+    int launches = 0;
+    auto swap_tk = [&]() {
+        for (int A : outs) std::swap(r->Tcur[A], r->Tnxt[A]);
+    };
+    auto enqueue = [&](int64_t kk, int sl) -> cudaError_t {
+        cudaError_t c = rows_pipe_iteration(e, r->d_nt, r->d_adj_idx, r->d_log, r->n_cells, kk == start_k + 1, kk, cap,
+                                            sl, r->pipe_ev[sl], s, &launches);
+        swap_tk();
+        return c;
+    };
+    cfpq_status result = CFPQ_OK;
+    CFPQ_CUDA_TRY(enqueue(k, 0));
+    for (;;) {
+        CFPQ_CUDA_TRY(enqueue(k + 1, slot ^ 1));   // speculative: a no-op if k ends the loop
+        CFPQ_CUDA_TRY(cudaEventSynchronize(r->pipe_ev[slot]));
+        unsigned long long nw = 0, lw = 0;
+        int st = 0;
+        rows_pipe_result(e, slot, &nw, &st, &lw);
+        if (st == 2) {
+            // a chunk / entry list ran out at k: k+1 did nothing, and the pointers (swapped for k
+            // and k+1) are k's again; grow and redo k's products (the counter accumulates)
+            CFPQ_CUDA_TRY(cudaStreamSynchronize(s));
+            CFPQ_CUDA_TRY(rows_pipe_clear_stop(e, s));
+            CFPQ_CUDA_TRY(dense_set_tables(e, r->Tcur.data(), r->Tnxt.data(), s));
+            rows_set_first(e, k == start_k + 1);   // the speculative k+1 reset the flag of iteration 1
+            for (bool redo = true; redo;) {
+                CFPQ_CUDA_TRY(rows_shard_check(e, s, &redo, true));
+                if (redo) {
+                    CFPQ_CUDA_TRY(rows_shard(e, 0, r->n, s, &launches));
+                    CFPQ_CUDA_TRY(dense_finish(e, s, &nw));
+                }
+            }
+            r->dense_new.push_back((int64_t)nw);
+            swap_tk();
+            if (nw == 0) break;   // T_k = T_{k-1}
+            if (k >= cap) {
+                *capped = true;
+                break;
+            }
+            // restart the pipeline at k+1 from the host's view (tables, a fresh count)
+            CFPQ_CUDA_TRY(rows_pipe_begin(e, r->Tcur.data(), r->Tnxt.data(), s));
+            ++k;
+            slot = 0;
+            CFPQ_CUDA_TRY(enqueue(k, 0));
+            continue;
+        }
+        r->dense_new.push_back((int64_t)nw);
+        if (st == 1 || st == 3) {
+            // k+1 did nothing: undo its pointer swap (T_k stays where k put it)
+            CFPQ_CUDA_TRY(cudaStreamSynchronize(s));
+            swap_tk();
+            if (st == 3) *capped = true;
+            break;
+        }
+        if (lw > dense_list_capacity(e)) {
+            // Δ_k overflowed its list: k+1 copies T_k whole (device-side check); grow the list
+            // once k+1 is done with the old one
+            CFPQ_CUDA_TRY(cudaStreamSynchronize(s));
+            CFPQ_CUDA_TRY(rows_grow_list(e, lw));
+        }
+        ++k;
+        slot ^= 1;
+    }
+    rows_pipe_end(e);
+    r->launches += launches;
+    *k_out = k;
+    return result;
+}
+
 static cfpq_status run_dense(cfpq_result* r, int64_t start_k) {
     cudaStream_t s = r->stream;
     // seeding (and start_k sparse iterations) done; their cells are in the log
@@ -1079,7 +1166,13 @@ static cfpq_status run_dense(cfpq_result* r, int64_t start_k) {
     dense_kblocks(r->dense, true);
     cudaEvent_t e0 = r->ev[2], e1 = r->ev[3];
     CFPQ_CUDA_TRY(cudaEventRecord(e0, s));
-    for (;;) {
+    const bool pipelined = r->opts.path_policy == 3 && r->n_ranks == 1 && !r->comm && !r->opts.account_work &&
+                           (r->opts.diag_flags & (1 << 11)) == 0 && rows_pipe_eligible(r->dense);
+    if (pipelined) {
+        cfpq_status ps = rows_pipelined_loop(r, start_k, &k, &capped);
+        if (ps != CFPQ_OK) return ps;
+    }
+    for (; !pipelined;) {
         ++k;
         unsigned long long nw = 0;
         int launches = 0;

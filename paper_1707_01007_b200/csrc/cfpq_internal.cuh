@@ -347,6 +347,19 @@ cudaError_t rows_list_settle(DenseEngine* e, int64_t row_lo, int64_t row_hi, uns
 cudaError_t rows_list(DenseEngine* e, unsigned long long want, void** list, unsigned long long* cap);
 cudaError_t rows_apply_all(DenseEngine* e, unsigned long long total, cudaStream_t s, int* launches);
 cudaError_t dense_finish(DenseEngine* e, cudaStream_t s, unsigned long long* new_total);
+// pipelined bit-row iterations (unsharded compact mode; dense.cu)
+bool rows_pipe_eligible(DenseEngine* e);
+cudaError_t rows_pipe_begin(DenseEngine* e, uint32_t* const* T, uint32_t* const* Tn, cudaStream_t s);
+void rows_pipe_end(DenseEngine* e);
+void rows_set_first(DenseEngine* e, bool first);
+cudaError_t rows_pipe_clear_stop(DenseEngine* e, cudaStream_t s);
+cudaError_t dense_set_tables(DenseEngine* e, uint32_t* const* T, uint32_t* const* Tn, cudaStream_t s);
+cudaError_t rows_pipe_iteration(DenseEngine* e, const NTInfo* nt, const int32_t* adj_idx, const uint64_t* log,
+                                unsigned long long n_seeds, bool first, long long k, long long cap_iter, int slot,
+                                cudaEvent_t done, cudaStream_t s, int* launches);
+void rows_pipe_result(DenseEngine* e, int slot, unsigned long long* nw, int* stop, unsigned long long* list_words);
+cudaError_t rows_grow_list(DenseEngine* e, unsigned long long words);
+unsigned long long dense_list_capacity(const DenseEngine* e);
 unsigned long long* dense_total_counter(DenseEngine* e);
 int64_t dense_row_tiles(const DenseEngine* e);
 

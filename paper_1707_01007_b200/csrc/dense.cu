@@ -947,7 +947,15 @@ struct RowsCtx {
     int32_t compact;
     uint4* elist;                      // [2 * ecap]: L entries, then R entries
     unsigned long long ecap;
+    // pipelined iterations: a device flag set by rows_end_kernel (fixpoint, cap or a list that
+    // ran out); every kernel of a later, speculatively enqueued iteration then does nothing
+    const int* stop;
 };
+
+#define ROWS_GATE(c)                                                  \
+    do {                                                              \
+        if ((c).stop && *(volatile const int*)(c).stop) return;       \
+    } while (0)
 
 enum : int { RF_NONE = 0, RF_L = 1, RF_R = 2, RF_V = 3, RF_P = 4 };
 
@@ -985,7 +993,8 @@ __device__ __forceinline__ void rows_merge(const DenseParams& p, const RowsCtx& 
 
 // Per-shard counter reset in one launch: chunk list R (rc[0]), optionally the Δ list length
 // (rc[1]), lists V / L-P and the compact entry slots (rc[3..6]); rc[2] (sticky) is kept.
-__global__ void rows_reset_kernel(unsigned long long* rc, int with_list) {
+__global__ void rows_reset_kernel(unsigned long long* rc, int with_list, const int* stop) {
+    if (stop && *(volatile const int*)stop) return;
     const int t = threadIdx.x;
     if (t == 0 || (t == 1 && with_list) || (t >= 3 && t <= 6)) rc[t] = 0ull;
 }
@@ -993,6 +1002,7 @@ __global__ void rows_reset_kernel(unsigned long long* rc, int with_list) {
 // Iteration 1: the zeroed T_k buffers take T_0 (the seed cells of the outputs, from the
 // log) and cnt[X][i] = |row i of T_0,X| for every NT.
 __global__ void rows_seed_kernel(DenseParams p, RowsCtx c, const uint64_t* __restrict__ log, unsigned long long n_seeds) {
+    ROWS_GATE(c);
     for (unsigned long long e = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; e < n_seeds;
          e += (unsigned long long)gridDim.x * blockDim.x) {
         const uint64_t cell = log[e];
@@ -1006,10 +1016,11 @@ __global__ void rows_seed_kernel(DenseParams p, RowsCtx c, const uint64_t* __res
 // Iteration k > 1: T_k buffer (holding T_{k-2}) |= Δ_{k-1} words; after an overflowed list,
 // copy T_{k-1} whole (and flag it for the host to grow the list).
 __global__ void rows_delta_kernel(DenseParams p, RowsCtx c, int copy_whole) {
+    ROWS_GATE(c);
     const unsigned long long m = c.rc[1];
     const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
     const unsigned long long t0 = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x;
-    if (!copy_whole) {   // the host knows the list of Δ_{k-1} is complete
+    if (!copy_whole && m <= c.dlist_cap) {   // the list of Δ_{k-1} is complete
         for (unsigned long long e = t0; e < m; e += stride) {
             const uint4 d = c.dlist[e];
             CFPQ_DASSERT(e < c.dlist_cap && d.x < (uint32_t)p.n_nt && d.y < (uint32_t)p.n && d.z < (uint32_t)p.Wp);
@@ -1032,6 +1043,7 @@ __global__ void rows_delta_kernel(DenseParams p, RowsCtx c, int copy_whole) {
 constexpr int kPlanRules = 64;   // rule forms cached in shared memory up to this many rules
 
 __global__ void rows_plan_kernel(DenseParams p, RowsCtx c, RowChunk* chunks, unsigned long long cap) {
+    ROWS_GATE(c);
     __shared__ int32_t s_form[kPlanRules], s_B[kPlanRules];
     __shared__ const int32_t* s_ptr[kPlanRules];
     __shared__ int32_t s_wsum[5][32];
@@ -1320,6 +1332,7 @@ constexpr int kCompactB = 4;
 template <int MODE>
 __global__ void __launch_bounds__(256) rows_compact_kernel(DenseParams p, RowsCtx c, const RowChunk* __restrict__ tasks,
                                                            int counter) {
+    ROWS_GATE(c);
     const int lane = threadIdx.x & 31;
     const int64_t nv4 = ((p.n + 31) / 32 + 3) / 4;
     const unsigned long long m = min(c.rc[counter], c.chunk_cap);
@@ -1388,6 +1401,7 @@ __global__ void __launch_bounds__(256) rows_compact_kernel(DenseParams p, RowsCt
 
 // L entries {leader rule, i, r}: every rule A -> B C_g of the group, j in CSR_C_g(r).
 __global__ void __launch_bounds__(256) rows_lmerge_kernel(DenseParams p, RowsCtx c, const int32_t* __restrict__ rule_out) {
+    ROWS_GATE(c);
     const unsigned long long m = min(c.rc[5], c.ecap);
     unsigned long long my_new = 0;
     for (unsigned long long e = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; e < m;
@@ -1413,6 +1427,7 @@ __global__ void __launch_bounds__(256) rows_lmerge_kernel(DenseParams p, RowsCtx
 
 // R entries {rule, r, word, bits}: OR bits into word `word` of every row i in CSC_B(r).
 __global__ void __launch_bounds__(256) rows_rmerge_kernel(DenseParams p, RowsCtx c, const int32_t* __restrict__ rule_out) {
+    ROWS_GATE(c);
     const unsigned long long m = min(c.rc[6], c.ecap);
     unsigned long long my_new = 0;
     for (unsigned long long e = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; e < m;
@@ -1438,6 +1453,7 @@ __global__ void __launch_bounds__(256) rows_rmerge_kernel(DenseParams p, RowsCtx
 // Latency-bound chains (CSR pointers -> index -> pre-check -> atomic): many warps resident.
 __global__ void __launch_bounds__(256, 4) rows_scatter_kernel(DenseParams p, RowsCtx c, const int32_t* __restrict__ rule_out,
                                                               const RowChunk* __restrict__ tasks) {
+    ROWS_GATE(c);
     __shared__ int32_t wlist[8][kChunkL];   // per warp: the chunk's selected set bits
     const int lane = threadIdx.x & 31;
     const int64_t wn = (p.n + 31) / 32;
@@ -1758,6 +1774,11 @@ struct DenseEngine {
     uint4* elist = nullptr;                    // bit-row compact mode: L / R entry lists [2 * ecap]
     unsigned long long ecap = 0;
     cudaStream_t side = nullptr;               // compact mode: the R pipeline runs beside the L one
+    bool pipe = false;                         // pipelined iterations (rows_pipe_*)
+    int* d_stop = nullptr;                     // pipelined iterations: device stop flag
+    unsigned long long* h_map = nullptr;       // mapped pinned [2 slots][16]: outcome + counters
+    unsigned long long* d_map = nullptr;       // its device alias
+    bool pipe_enqueue = false;                 // inside rows_pipe_iteration
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     int32_t launch_mode = 0;                   // cfpq_options.dense_launch
     int32_t rgather_variant = 0;               // diagnostics (diag_flags bits 4-6): R-form kernel shape
@@ -1780,6 +1801,8 @@ struct DenseEngine {
         if (ev_fork) cudaEventDestroy(ev_fork);
         if (ev_join) cudaEventDestroy(ev_join);
         if (side) cudaStreamDestroy(side);
+        cudaFree(d_stop);
+        if (h_map) cudaFreeHost(h_map);
         cudaFree(rc);
         cudaFree(T8); cudaFree(T8T); cudaFree(occ); cudaFree(mapA_row); cudaFree(mapB_row); cudaFree(out_nt);
         cudaFree(rule_ptr); cudaFree(rules); cudaFree(Tptr); cudaFree(Tnptr); cudaFree(new_cells);
@@ -1913,6 +1936,9 @@ DenseEngine* dense_create(int32_t n, int32_t n_nt, int64_t Wp, const std::vector
     e->grid = std::max(1, std::min(sms, total));
     e->launch_mode = launch_mode;
     e->dlist_cap = dlist_cap > 0 ? (unsigned long long)dlist_cap : (1ull << 20);   // bit-row Δ_k word list
+    // compact-mode entry lists start at 2^21 entries each, or at the caller's (small) list
+    // capacity, so that the tests exercise their overflow-and-redo path
+    e->ecap = dlist_cap > 0 && dlist_cap < (1 << 21) ? std::max<unsigned long long>(64, dlist_cap) : (1ull << 21);
     return e;
 }
 
@@ -2118,7 +2144,8 @@ cudaError_t rows_begin(DenseEngine* e, const NTInfo* nt, const int32_t* adj_idx,
     e->rows_adj = adj_idx;
     e->rows_first = first;
     DenseParams p = rows_params(e);
-    RowsCtx rc{nt, adj_idx, e->rcnt, (uint4*)e->dlist, e->dlist_cap, e->rc, first ? 1 : 0, n_rules, 0, e->n, e->l_next, e->chunk_cap};
+    RowsCtx rc{nt, adj_idx, e->rcnt, (uint4*)e->dlist, e->dlist_cap, e->rc, first ? 1 : 0, n_rules, 0, e->n, e->l_next,
+               e->chunk_cap, 0, 0, nullptr, 0, e->pipe ? e->d_stop : nullptr};
     const int sms = device_sms();
     // T_k buffer := T_{k-1}
     if (first) {
@@ -2132,7 +2159,7 @@ cudaError_t rows_begin(DenseEngine* e, const NTInfo* nt, const int32_t* adj_idx,
     }
     if (launches) *launches += 1;
     // Δ_k list and chunk counters restart
-    rows_reset_kernel<<<1, 32, 0, s>>>(e->rc, 1);
+    rows_reset_kernel<<<1, 32, 0, s>>>(e->rc, 1, e->pipe ? e->d_stop : nullptr);
     return cudaGetLastError();
 }
 
@@ -2151,7 +2178,6 @@ cudaError_t rows_shard(DenseEngine* e, int64_t row_lo, int64_t row_hi, cudaStrea
     // operand rows streamed into entry lists, entries merged by one thread each (variant 0)
     const bool compact = push && !e->has_v && e->rgather_variant == 0;
     if (compact && !e->elist) {
-        e->ecap = 1ull << 21;
         if ((c = cudaMalloc(&e->elist, 2 * e->ecap * sizeof(uint4))) != cudaSuccess) return c;
     }
     if (compact && !e->side) {
@@ -2161,15 +2187,17 @@ cudaError_t rows_shard(DenseEngine* e, int64_t row_lo, int64_t row_hi, cudaStrea
     }
     RowsCtx rc{e->rows_nt, e->rows_adj, e->rcnt, (uint4*)e->dlist, e->dlist_cap, e->rc, e->rows_first ? 1 : 0,
                n_rules, (int32_t)row_lo, (int32_t)row_hi, e->l_next, e->chunk_cap, push ? 1 : 0,
-               compact ? 1 : 0, e->elist, compact ? e->ecap : 0};
+               compact ? 1 : 0, e->elist, compact ? e->ecap : 0, e->pipe ? e->d_stop : nullptr};
     const int sms = device_sms();
     // plan and products back to back, no host round trip: the products clamp every list to
     // its capacity and the counters are copied to pinned host memory behind them; the host
     // checks them after the iteration's synchronisation (rows_shard_check) and re-runs the
     // shard if a list overflowed (products are idempotent ORs; Δ_k records only new flips)
-    rows_reset_kernel<<<1, 32, 0, s>>>(e->rc, 0);   // chunk lists of this shard, compact entry slots
+    if (!e->pipe_enqueue)   // (a pipelined iteration's rows_begin has just reset them)
+        rows_reset_kernel<<<1, 32, 0, s>>>(e->rc, 0, e->pipe ? e->d_stop : nullptr);   // chunk lists, entry slots
     rows_plan_kernel<<<sms * 8, 256, 0, s>>>(p, rc, (RowChunk*)e->chunks, e->chunk_cap);
     // 4 CTAs x 8 warps per SM (measured: 6 or 8 CTAs with fewer registers are not faster)
+    if (!compact)   // (compact mode lists P rules with the L rows)
     rows_scatter_kernel<<<resident_grid(rows_scatter_kernel, 256, sms), 256, 0, s>>>(p, rc, e->rule_out,
                                                                                  (const RowChunk*)e->chunks + 2 * e->chunk_cap);
     const int64_t nv4 = ((e->n + 31) / 32 + 3) / 4;
@@ -2226,7 +2254,9 @@ cudaError_t rows_shard(DenseEngine* e, int64_t row_lo, int64_t row_hi, cudaStrea
         }
     }
     if (launches) *launches += 2 + (e->has_v ? 1 : 0) + (e->has_r ? 1 : 0);
-    if ((c = cudaMemcpyAsync(e->h_rc, e->rc, 7 * 8, cudaMemcpyDeviceToHost, s)) != cudaSuccess) return c;
+    // (pipelined iterations: rows_end_kernel writes the counters into mapped host memory)
+    if (!e->pipe_enqueue && (c = cudaMemcpyAsync(e->h_rc, e->rc, 7 * 8, cudaMemcpyDeviceToHost, s)) != cudaSuccess)
+        return c;
     return cudaGetLastError();
 }
 
@@ -2340,6 +2370,137 @@ cudaError_t rows_apply_all(DenseEngine* e, unsigned long long total, cudaStream_
     rows_apply_kernel<<<device_sms() * 8, 256, 0, s>>>(p, rc, 0ull, total);
     if (launches) *launches += 1;
     return cudaGetLastError();
+}
+
+// ---- pipelined bit-row iterations (unsharded compact mode) ----
+// Iteration k+1 is enqueued before the host reads iteration k's outcome, so the host round
+// trip of iteration k overlaps the products of k+1.  rows_end_kernel closes each iteration on
+// the device: it records the new-cell count, and sets the stop flag at the fixpoint (no new
+// cell), at the iteration cap, or when a chunk / entry list ran out (the host then redoes
+// that iteration with grown lists, exactly as the unpipelined loop does); the speculative next
+// iteration then does nothing.
+__global__ void rows_end_kernel(RowsCtx c, unsigned long long* new_cells, int n_nt, unsigned long long chunk_cap,
+                                unsigned long long ecap, int* stop, unsigned long long* out, long long k,
+                                long long cap_iter, const uint32_t** Tptr, uint32_t** Tnptr, const int32_t* out_nt,
+                                int n_out) {
+    if (threadIdx.x != 0) return;
+    if (*(volatile int*)stop) {
+        out[0] = ~0ull;   // this iteration did not run
+        out[1] = (unsigned long long)*(volatile int*)stop;
+        return;
+    }
+    const unsigned long long nw = new_cells[n_nt];
+    out[0] = nw;
+    out[2] = c.rc[1];   // Δ_k words (the host grows the list when it ran out)
+    for (int q = 0; q < 7; ++q) out[4 + q] = c.rc[q];
+    int st = 0;
+    if (c.rc[0] > chunk_cap || c.rc[3] > chunk_cap || c.rc[4] > chunk_cap || (ecap && (c.rc[5] > ecap || c.rc[6] > ecap)))
+        st = 2;
+    else if (nw == 0)
+        st = 1;
+    else if (k >= cap_iter)
+        st = 3;
+    out[1] = (unsigned long long)st;
+    __threadfence_system();
+    if (st) *stop = st;
+    if (st == 2) return;   // the host redoes iteration k: keep its tables and its count
+    // iteration k+1 reads T_k: swap the pointer tables of the outputs, restart the count
+    for (int o = 0; o < n_out; ++o) {
+        const int A = out_nt[o];
+        uint32_t* t = const_cast<uint32_t*>(Tptr[A]);
+        Tptr[A] = Tnptr[A];
+        Tnptr[A] = t;
+    }
+    for (int t = 0; t < n_nt + 2; ++t) new_cells[t] = 0ull;
+}
+
+cudaError_t rows_pipe_begin(DenseEngine* e, uint32_t* const* T, uint32_t* const* Tn, cudaStream_t s) {
+    cudaError_t c;
+    if (!e->d_stop) {
+        if ((c = cudaMalloc(&e->d_stop, sizeof(int))) != cudaSuccess) return c;
+        if ((c = cudaHostAlloc(&e->h_map, 32 * sizeof(unsigned long long), cudaHostAllocMapped)) != cudaSuccess) return c;
+        if ((c = cudaHostGetDevicePointer(&e->d_map, e->h_map, 0)) != cudaSuccess) return c;
+    }
+    if ((c = cudaMemsetAsync(e->d_stop, 0, sizeof(int), s)) != cudaSuccess) return c;
+    if ((c = dense_set_tables(e, T, Tn, s)) != cudaSuccess) return c;
+    if ((c = cudaMemsetAsync(e->new_cells, 0, (e->n_nt + 2) * 8, s)) != cudaSuccess) return c;
+    e->pipe = true;
+    return cudaSuccess;
+}
+
+void rows_pipe_end(DenseEngine* e) { e->pipe = false; }
+
+void rows_set_first(DenseEngine* e, bool first) { e->rows_first = first; }
+
+cudaError_t rows_pipe_clear_stop(DenseEngine* e, cudaStream_t s) {
+    return cudaMemsetAsync(e->d_stop, 0, sizeof(int), s);
+}
+
+// Upload the T / T_k pointer tables of an iteration (no counter reset).
+cudaError_t dense_set_tables(DenseEngine* e, uint32_t* const* T, uint32_t* const* Tn, cudaStream_t s) {
+    cudaError_t c;
+    if ((c = cudaMemcpyAsync((void*)e->Tptr, T, e->n_nt * sizeof(void*), cudaMemcpyHostToDevice, s)) != cudaSuccess)
+        return c;
+    return cudaMemcpyAsync((void*)e->Tnptr, Tn, e->n_nt * sizeof(void*), cudaMemcpyHostToDevice, s);
+}
+
+// One iteration, enqueued (gated by the stop flag): rows_begin, rows_shard and the closing
+// kernel, which writes the outcome into mapped slot `slot`, swaps the device pointer tables
+// and restarts the new-cell count; `done` is recorded behind it.  No host copy per iteration.
+cudaError_t rows_pipe_iteration(DenseEngine* e, const NTInfo* nt, const int32_t* adj_idx, const uint64_t* log,
+                                unsigned long long n_seeds, bool first, long long k, long long cap_iter, int slot,
+                                cudaEvent_t done, cudaStream_t s, int* launches) {
+    cudaError_t c;
+    e->pipe_enqueue = true;
+    c = rows_begin(e, nt, adj_idx, log, n_seeds, first, s, launches);
+    if (c == cudaSuccess) c = rows_shard(e, 0, e->n, s, launches);
+    e->pipe_enqueue = false;
+    if (c != cudaSuccess) return c;
+    RowsCtx rc{e->rows_nt, e->rows_adj, e->rcnt, (uint4*)e->dlist, e->dlist_cap, e->rc, 0, 0, 0, e->n, e->l_next,
+               e->chunk_cap, 0, 0, e->elist, e->ecap, e->d_stop};
+    rows_end_kernel<<<1, 32, 0, s>>>(rc, e->new_cells, e->n_nt, e->chunk_cap, e->elist ? e->ecap : 0, e->d_stop,
+                                     e->d_map + 16 * slot, k, cap_iter, e->Tptr, e->Tnptr, e->out_nt, e->n_out);
+    if (launches) *launches += 1;
+    return cudaEventRecord(done, s);
+}
+
+// The outcome of the iteration in `slot` (after its event completed): new cells (~0 = did not
+// run), stop reason (0 running, 1 fixpoint, 2 a list ran out, 3 cap), Δ_k words; the chunk
+// counters go to h_rc for rows_shard_check.
+void rows_pipe_result(DenseEngine* e, int slot, unsigned long long* nw, int* stop, unsigned long long* list_words) {
+    volatile unsigned long long* m = e->h_map + 16 * slot;
+    *nw = m[0];
+    *stop = (int)m[1];
+    *list_words = m[2];
+    if (*nw != ~0ull)
+        for (int q = 0; q < 7; ++q) e->h_rc[q] = m[4 + q];
+}
+
+unsigned long long dense_list_capacity(const DenseEngine* e) { return e->dlist_cap; }
+
+bool rows_pipe_eligible(DenseEngine* e) {
+    if (e->n_out == 0) return false;
+    if (!e->forms_known) {
+        for (size_t q = 0; q < e->h_rules.size(); ++q) {
+            const bool bc = e->is_const[e->h_rules[q].B], cc = e->is_const[e->h_rules[q].C];
+            e->has_r |= bc && !cc;
+            e->has_v |= !bc && !cc;
+        }
+        e->forms_known = true;
+    }
+    return !e->has_v && e->rgather_variant == 0;
+}
+
+// The Δ list ran out during a pipelined run (after a drain): grow it; the next iteration
+// rebuilds its T_k buffer by a whole copy.
+cudaError_t rows_grow_list(DenseEngine* e, unsigned long long words) {
+    if (words <= e->dlist_cap) return cudaSuccess;
+    cudaFree(e->dlist);
+    e->dlist = nullptr;
+    e->dlist_cap = std::max<unsigned long long>(e->dlist_cap * 4, words + words / 4);
+    cudaError_t c = cudaMalloc(&e->dlist, e->dlist_cap * sizeof(uint4));
+    e->list_complete = false;
+    return c;
 }
 
 cudaError_t dense_finish(DenseEngine* e, cudaStream_t s, unsigned long long* new_total) {

@@ -159,3 +159,27 @@ def test_rows_nccl_single_rank():
     ores = assert_parity(w, r)
     nc, _ = r.iteration_stats()
     assert nc.tolist() == ores.stats()["new_bits"].tolist()
+
+
+def test_rows_pipelined_iterations_match_unpipelined():
+    """Pipelined bit-row iterations (the next one enqueued before the host reads this one's
+    outcome; a device stop flag gates the speculative one) give the same per-iteration states
+    as the host-synchronised loop (diag_flags bit 11), at the fixpoint and under a cap, with
+    the entry lists overflowing and redone (rows_list_capacity = 8)."""
+    import numpy as np
+    from paper_1707_01007_b200 import cfpq as C
+    for w in (I.config4_workload(n=1500, seed=2), I.ontology_workload("q2", 700, depth=6, seed=3)):
+        for extra in (dict(), dict(rows_list_capacity=8)):
+            ra, _, _ = gpu_closure(w, path_policy=3, **extra)
+            rb, _, _ = gpu_closure(w, path_policy=3, flags=1 << 11, **extra)
+            assert ra.iterations == rb.iterations
+            assert ra.iteration_stats()[0].tolist() == rb.iteration_stats()[0].tolist()
+            for A in range(w.n_nt):
+                assert np.array_equal(ra.pairs(A), rb.pairs(A)), (w.name, extra, A)
+        g, d = C.Grammar.from_workload(w), C.Graph(w.n_nodes, w.edges)
+        ca = C.closure(g, d, path_policy=3, max_iterations=3)
+        cb = C.closure(g, d, path_policy=3, max_iterations=3, flags=1 << 11)
+        assert ca.status == cb.status == C.CFPQ_E_NOT_CONVERGED
+        assert ca.iterations == cb.iterations == 3
+        for A in range(w.n_nt):
+            assert np.array_equal(ca.pairs(A), cb.pairs(A))
