@@ -1049,7 +1049,10 @@ __global__ void rows_plan_kernel(DenseParams p, RowsCtx c, RowChunk* chunks, uns
     __shared__ int32_t s_wsum[5][32];
     __shared__ unsigned long long s_base[5];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    __shared__ int32_t s_active[kPlanRules];   // rules with work this iteration (cached plans)
+    __shared__ int32_t s_nact;
     const bool cached = c.n_rules <= kPlanRules;
+    int n_task_rules = c.n_rules;
     if (cached) {
         for (int q = threadIdx.x; q < c.n_rules; q += blockDim.x) {
             const DenseRule r = p.rules[q];
@@ -1058,8 +1061,18 @@ __global__ void rows_plan_kernel(DenseParams p, RowsCtx c, RowChunk* chunks, uns
             s_ptr[q] = c.nt[r.B].csr_ptr;
         }
         __syncthreads();
+        if (threadIdx.x == 0) {
+            // skip rules without tasks: no form this iteration (both operands preterminal after
+            // iteration 1) and L rules that follow their group's leader
+            int na = 0;
+            for (int q = 0; q < c.n_rules; ++q)
+                if (s_form[q] != RF_NONE && !(s_form[q] == RF_L && c.l_next[q] < -1)) s_active[na++] = q;
+            s_nact = na;
+        }
+        __syncthreads();
+        n_task_rules = s_nact;
     }
-    const int64_t tasks = (int64_t)c.n_rules * (c.row_hi - c.row_lo);   // this shard's rows only
+    const int64_t tasks = (int64_t)n_task_rules * (c.row_hi - c.row_lo);   // this shard's rows only
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t t0 = blockIdx.x * (int64_t)blockDim.x; t0 < tasks; t0 += stride) {
         const int64_t t = t0 + threadIdx.x;
@@ -1068,12 +1081,13 @@ __global__ void rows_plan_kernel(DenseParams p, RowsCtx c, RowChunk* chunks, uns
             // row-major: the rules of one row are adjacent in every list, so a bit row read
             // for two rules (e.g. S5 -> S P_sc and S6 -> S P_t) is re-read from L2
             if (tasks < (1ll << 31)) {
-                i = (int)((uint32_t)t / (uint32_t)c.n_rules);
-                q = (int)((uint32_t)t - (uint32_t)i * (uint32_t)c.n_rules);
+                i = (int)((uint32_t)t / (uint32_t)n_task_rules);
+                q = (int)((uint32_t)t - (uint32_t)i * (uint32_t)n_task_rules);
             } else {
-                i = (int)(t / c.n_rules);
-                q = (int)(t - (int64_t)i * c.n_rules);
+                i = (int)(t / n_task_rules);
+                q = (int)(t - (int64_t)i * n_task_rules);
             }
+            if (cached) q = s_active[q];
             i += c.row_lo;
             DenseRule r;
             int f;
