@@ -405,7 +405,7 @@ def rows_alg_bytes(w, r_sparse):
     return total
 
 
-def supplementary_rows(C, w, g, d, r_sparse, stream, steps=2):
+def supplementary_rows(C, w, g, d, r_sparse, stream, steps=3):
     """Config 4 in the paper-faithful full-operand mode (path_policy 3, bit-row CUDA-core
     products of Alg. 1 line 9 over whole matrices), with its HBM roofline on SURVEY §8(d)'s
     algorithmic bytes (rows_alg_bytes)."""
@@ -425,8 +425,9 @@ def supplementary_rows(C, w, g, d, r_sparse, stream, steps=2):
             "same_result_as_sparse": ok,
             "roofline": {"bound": "hbm", "achieved": alg / loop_s / 1e9, "peak": peak, "unit": "GB/s",
                          "frac": alg / loop_s / 1e9 / peak, "traffic": ncu_traffic("config4_rows"),
-                         "kernel": "cfpq::rows_scatter_kernel + rows_rgather_kernel (+ plan, delta, seed): every launch "
-                                   "of the loop; alg_bytes and traffic per closure", "alg_bytes": alg, "peak_source": src,
+                         "kernel": "cfpq::rows_compact_kernel<0/1> + rows_lmerge/rows_rmerge_kernel (+ plan, delta, "
+                                   "reset, end): every launch of the loop; alg_bytes and traffic per closure",
+                         "alg_bytes": alg, "peak_source": src,
                          "note": "model of the implemented full-operand forms (DESIGN 3.3, bench.rows_alg_bytes): "
                                  "each distinct bit row / CSR entry read once per rule and iteration, 8 B per "
                                  "output word touched, 32 B per Delta word"}}
