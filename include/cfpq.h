@@ -165,7 +165,8 @@ typedef struct {
                                 map Δ chunks to warps CTA-major instead of interleaved, bit 9
                                 seed with separate kernels instead of inside the closure
                                 kernel, bit 11 bit-row iterations without pipelining (the host
-                                reads each iteration's outcome before enqueueing the next)   */
+                                reads each iteration's outcome before enqueueing the next),
+                                bit 13 no single-cell chains in the one-warp iterations      */
     int32_t grid_rows;       /* tensor engine, world_size (or reserved_emulate) > 1: 2-D
                                 process grid grid_rows x grid_cols (SUMMA-style blocks
                                 (I_a, J_b) of every T_A); 0 = 1-D row blocks.

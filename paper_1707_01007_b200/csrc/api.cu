@@ -270,6 +270,7 @@ struct cfpq_result {
         p.self_clear = self_clear_ok() ? 1 : 0;
         p.warp_flush = (opts.diag_flags & 8) ? 1 : 0;
         p.cta_major = (opts.diag_flags & 256) ? 1 : 0;
+        p.no_chain = (opts.diag_flags & (1 << 13)) ? 1 : 0;
         p.row_lo = 0;
         p.row_hi = (uint32_t)n;
         p.clr_n = clr_active ? clr_n : 0;

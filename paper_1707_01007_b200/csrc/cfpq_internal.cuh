@@ -176,6 +176,7 @@ struct EngineParams {
     unsigned long long switch_cells;  // |Δ_k| above which the loop stops for the dense engine (0 = never)
     int32_t precheck;              // read a candidate's word before its atomicOr (hot cells)
     int32_t cta_major;             // diagnostics (diag_flags bit 8): chunk c -> warp c (CTA-major)
+    int32_t no_chain;              // diagnostics (diag_flags bit 13): no single-cell chains in warp-solo
     int32_t warp_flush;            // diagnostics (diag_flags bit 3): each warp appends its own cells
                                    // (one log atomic per warp) instead of the CTA-level flush
     int32_t self_clear;            // relational runs: at the fixpoint the kernel resets the words

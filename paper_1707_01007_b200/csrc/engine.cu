@@ -1338,7 +1338,121 @@ struct WarpSoloShared {
     unsigned long long ring[kMaxStages + 1]; // Gauss-Seidel: shared copy of EngineState::gs_ring
     int cnt;
     int ov, lov;
+    LoopState cs;                            // single-cell chain: the state it hands back
+    int cm;                                  //   cells it leaves in nxt for the warp (0: stopped)
+    int stuck;                               //   1: nxt[0] is a cell the chain cannot expand
 };
+
+// Single-cell chains (the a^n b^n worst case: one new cell per iteration for 2pq+1 iterations).
+// While Δ is one cell whose rule occurrences are all ELL walks of preterminal operands, lane 0
+// runs the iterations alone in registers: the candidates' bits are set by atomics issued
+// together, and the ELL heads of every candidate's own occurrences are loaded before those
+// atomics return, so the next iteration starts without waiting for its heads — one dependent
+// L2 round trip per iteration instead of two, and no warp barrier or shared staging.  A cell
+// it cannot expand, several new cells, or a log that might run out hand the step back to the
+// warp path (w.cm cells in w.nxt), with identical per-iteration states.
+__device__ void solo_chain(const EngineParams& p, const NTInfo* nt, const Expansion* exps, WarpSoloShared& w,
+                           LoopState& s, long long& k, uint64_t cell, long long& iters, unsigned long long& dcand,
+                           unsigned long long& dexp) {
+    int4 pre[2] = {make_int4(0, 0, -1, -1), make_int4(0, 0, -1, -1)};
+    unsigned pv = 0;
+    for (;;) {
+        const uint32_t X = cell_nt(cell), ci = cell_i(cell), cj = cell_j(cell);
+        const int eb = nt[X].exp_begin, ne = nt[X].exp_end - eb;
+        bool ok = ne <= 2 && s.hi + 4 <= p.log_cap;
+        int4 h[2];
+        uint32_t hA[2] = {0, 0}, hf[2] = {0, 0};
+#pragma unroll
+        for (int x = 0; x < 2; ++x) {
+            h[x] = make_int4(0, 0, -1, -1);
+            if (ok && x < ne) {
+                const Expansion ex = exps[eb + x];
+                if (ex.kind != EXP_L_CONST && ex.kind != EXP_R_CONST) {
+                    ok = false;
+                } else if ((pv >> x) & 1u) {
+                    h[x] = pre[x];
+                    hA[x] = (uint32_t)ex.A;
+                    hf[x] = ex.kind == EXP_L_CONST ? ci : (cj | 0x80000000u);
+                } else {
+                    h[x] = load_head(nt, ex, ci, cj, hA[x], hf[x]);
+                }
+            }
+        }
+        if (ok)
+#pragma unroll
+            for (int x = 0; x < 2; ++x) ok = ok && h[x].y <= 2;
+        if (!ok) {   // the warp path expands this cell
+            w.nxt[0] = cell;
+            w.cm = 1;
+            w.stuck = 1;
+            return;
+        }
+        uint32_t cA[4], ca[4], cb[4];
+        bool has[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int x = q >> 1, m = q & 1;
+            cand_coords(hf[x], m ? h[x].w : h[x].z, ca[q], cb[q]);
+            cA[q] = hA[x];
+            has[q] = x < ne && h[x].y > m && ca[q] >= p.row_lo && ca[q] < p.row_hi;
+        }
+        // the candidates' own heads (they are the next Δ if new), before the atomics return
+        int4 sp[4][2];
+        unsigned spv[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            spv[q] = 0;
+            sp[q][0] = sp[q][1] = make_int4(0, 0, -1, -1);
+            if (!has[q]) continue;
+            const int qb = nt[cA[q]].exp_begin, qn = nt[cA[q]].exp_end - qb;
+#pragma unroll
+            for (int x = 0; x < 2; ++x)
+                if (x < qn) {
+                    const Expansion ex = exps[qb + x];
+                    if (ex.kind == EXP_L_CONST) {
+                        sp[q][x] = __ldg(nt[ex.other].csr_ell + cb[q]);
+                        spv[q] |= 1u << x;
+                    } else if (ex.kind == EXP_R_CONST) {
+                        sp[q][x] = __ldg(nt[ex.other].csc_ell + ca[q]);
+                        spv[q] |= 1u << x;
+                    }
+                }
+        }
+        uint32_t old[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            old[q] = ~0u;
+            if (has[q]) {
+                CFPQ_DASSERT(cA[q] < (uint32_t)p.n_nt && ca[q] < (uint32_t)p.n && cb[q] < (uint32_t)p.n);
+                old[q] = atomicOr(nt[cA[q]].T + (size_t)ca[q] * (size_t)p.Wp + (cb[q] >> 5), 1u << (cb[q] & 31));
+            }
+        }
+        dexp += (unsigned long long)ne;
+        dcand += (unsigned long long)(h[0].y + (ne > 1 ? h[1].y : 0));
+        int n_new = 0, last = 0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+            if (has[q] && !(old[q] & (1u << (cb[q] & 31)))) {
+                const uint64_t c = pack_cell(cA[q], ca[q], cb[q]);
+                p.log[s.hi + (unsigned long long)n_new] = c;
+                w.nxt[n_new] = c;
+                ++n_new;
+                last = q;
+            }
+        close_iteration(p, k, s, s.hi + (unsigned long long)n_new, 0, true);
+        ++iters;
+        ++k;
+        if (s.status != ST_RUNNING || n_new != 1) {   // done, capped, or several cells: the warp path
+            w.cm = s.status == ST_RUNNING ? n_new : 0;
+            w.stuck = 0;
+            return;
+        }
+        cell = w.nxt[0];
+        pre[0] = sp[last][0];
+        pre[1] = sp[last][1];
+        pv = spv[last];
+    }
+}
 
 __device__ __forceinline__ bool ws_try(const EngineParams& p, const NTInfo* nt, uint32_t A, uint32_t i, uint32_t j,
                                        uint64_t len, long long k, int* lov, int* ovf) {
@@ -1399,7 +1513,29 @@ __device__ void warp_solo(const EngineParams& p, const NTInfo* nt, const Expansi
         ring = w.ring;
         __syncwarp();
     }
+    // single-cell chains need the plain relational Jacobi path (no keys, hashed set, stages or
+    // snapshots); cfpq diag_flags bit 13 disables them (A/B)
+    const bool chains = !p.lengths && !p.hset && !p.gs_stages && !p.has_snapshots && !p.jac && !p.no_chain;
+    bool stuck = false;
     for (;;) {
+        if (chains && m == 1 && !stuck) {
+            if (lane == 0) {
+                w.cs = s;
+                long long kk = k;
+                solo_chain(p, nt, exps, w, w.cs, kk, cell, iters, dcand, dexp);
+            }
+            __syncwarp();
+            s = w.cs;
+            k = s.iter + 1;
+            m = w.cm;
+            stuck = w.stuck != 0;
+            if (s.status != ST_RUNNING || m == 0) break;
+            if (m > p.solo_max) break;   // the CTA / grid paths take Δ from the log
+            cell = lane < m ? w.nxt[lane] : 0ull;
+            __syncwarp();
+            continue;
+        }
+        stuck = false;
         if (lane == 0) {
             w.cnt = 0;
             w.ov = 0;
