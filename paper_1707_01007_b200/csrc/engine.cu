@@ -1356,10 +1356,13 @@ __device__ void solo_chain(const EngineParams& p, const NTInfo* nt, const Expans
                            unsigned long long& dexp) {
     int4 pre[2] = {make_int4(0, 0, -1, -1), make_int4(0, 0, -1, -1)};
     unsigned pv = 0;
+    // single-path lengths: the chain's cell's length (read once, then carried: every candidate
+    // of a one-cell Δ has length l + 1 through its preterminal operand)
+    uint64_t clen = p.lengths ? cell_len(p, nt, cell_nt(cell), cell_i(cell), cell_j(cell)) : 0;
     for (;;) {
         const uint32_t X = cell_nt(cell), ci = cell_i(cell), cj = cell_j(cell);
         const int eb = nt[X].exp_begin, ne = nt[X].exp_end - eb;
-        bool ok = ne <= 2 && s.hi + 4 <= p.log_cap;
+        bool ok = ne <= 2 && s.hi + 4 <= p.log_cap && clen < 0xffffffffull;
         int4 h[2];
         uint32_t hA[2] = {0, 0}, hf[2] = {0, 0};
 #pragma unroll
@@ -1418,23 +1421,44 @@ __device__ void solo_chain(const EngineParams& p, const NTInfo* nt, const Expans
                     }
                 }
         }
-        uint32_t old[4];
+        bool fresh[4];
+        if (p.lengths) {
+            // keys (iteration << 32 | length): new iff the atomicMin leaves EMPTY (first write wins)
+            const unsigned long long kv = ((unsigned long long)k << 32) | (clen + 1ull);
+            unsigned long long old64[4];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            old[q] = ~0u;
-            if (has[q]) {
-                CFPQ_DASSERT(cA[q] < (uint32_t)p.n_nt && ca[q] < (uint32_t)p.n && cb[q] < (uint32_t)p.n);
-                old[q] = atomicOr(nt[cA[q]].T + (size_t)ca[q] * (size_t)p.Wp + (cb[q] >> 5), 1u << (cb[q] & 31));
+            for (int q = 0; q < 4; ++q) {
+                old64[q] = 0ull;
+                if (has[q]) {
+                    CFPQ_DASSERT(cA[q] < (uint32_t)p.n_nt && ca[q] < (uint32_t)p.n && cb[q] < (uint32_t)p.n);
+                    old64[q] = atomicMin((unsigned long long*)(nt[cA[q]].K + (size_t)ca[q] * (size_t)p.n + cb[q]), kv);
+                }
             }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) fresh[q] = has[q] && old64[q] == kEmptyKey;
+        } else {
+            uint32_t old[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                old[q] = ~0u;
+                if (has[q]) {
+                    CFPQ_DASSERT(cA[q] < (uint32_t)p.n_nt && ca[q] < (uint32_t)p.n && cb[q] < (uint32_t)p.n);
+                    old[q] = atomicOr(nt[cA[q]].T + (size_t)ca[q] * (size_t)p.Wp + (cb[q] >> 5), 1u << (cb[q] & 31));
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) fresh[q] = has[q] && !(old[q] & (1u << (cb[q] & 31)));
         }
         dexp += (unsigned long long)ne;
         dcand += (unsigned long long)(h[0].y + (ne > 1 ? h[1].y : 0));
         int n_new = 0, last = 0;
 #pragma unroll
         for (int q = 0; q < 4; ++q)
-            if (has[q] && !(old[q] & (1u << (cb[q] & 31)))) {
+            if (fresh[q]) {
                 const uint64_t c = pack_cell(cA[q], ca[q], cb[q]);
                 p.log[s.hi + (unsigned long long)n_new] = c;
+                if (p.lengths)   // the bit matrix mirrors the keys
+                    atomicOr(nt[cA[q]].T + (size_t)ca[q] * (size_t)p.Wp + (cb[q] >> 5), 1u << (cb[q] & 31));
                 w.nxt[n_new] = c;
                 ++n_new;
                 last = q;
@@ -1451,6 +1475,7 @@ __device__ void solo_chain(const EngineParams& p, const NTInfo* nt, const Expans
         pre[0] = sp[last][0];
         pre[1] = sp[last][1];
         pv = spv[last];
+        clen += 1ull;
     }
 }
 
@@ -1513,9 +1538,9 @@ __device__ void warp_solo(const EngineParams& p, const NTInfo* nt, const Expansi
         ring = w.ring;
         __syncwarp();
     }
-    // single-cell chains need the plain relational Jacobi path (no keys, hashed set, stages or
-    // snapshots); cfpq diag_flags bit 13 disables them (A/B)
-    const bool chains = !p.lengths && !p.hset && !p.gs_stages && !p.has_snapshots && !p.jac && !p.no_chain;
+    // single-cell chains need the plain Jacobi path (no hashed set, stages or snapshots);
+    // cfpq diag_flags bit 13 disables them (A/B)
+    const bool chains = !p.hset && !p.gs_stages && !p.has_snapshots && !p.jac && !p.no_chain;
     bool stuck = false;
     for (;;) {
         if (chains && m == 1 && !stuck) {
