@@ -1425,11 +1425,11 @@ __global__ void __launch_bounds__(256) rows_lmerge_kernel(DenseParams p, RowsCtx
         const int i = (int)en.y, rr = (int)en.z;
         CFPQ_DASSERT(i < p.n && rr < p.n);
         for (int qq = (int)en.x; qq >= 0; qq = rows_l_follow(c.l_next[qq])) {
-            const int32_t* cp = c.nt[p.rules[qq].C].csr_ptr;
-            const int e1 = __ldg(cp + rr + 1);
+            // the ELL head {beg, deg, nb0, nb1} of CSR_C(r): one load for the usual <= 2 entries
+            const int4 h = __ldg(c.nt[p.rules[qq].C].csr_ell + rr);
             const int A = rule_out[qq];
-            for (int f2 = __ldg(cp + rr); f2 < e1; ++f2) {
-                const int j = __ldg(c.adj_idx + f2);
+            for (int f2 = 0; f2 < h.y; ++f2) {
+                const int j = f2 == 0 ? h.z : (f2 == 1 ? h.w : __ldg(c.adj_idx + h.x + f2));
                 rows_merge(p, c, A, i, j >> 5, 1u << (j & 31), my_new);
             }
         }
@@ -1450,11 +1450,10 @@ __global__ void __launch_bounds__(256) rows_rmerge_kernel(DenseParams p, RowsCtx
         if (!en.w) continue;
         const int q = (int)en.x, rr = (int)en.y;
         CFPQ_DASSERT(rr < p.n && (int64_t)en.z < p.Wp);
-        const int32_t* cp = c.nt[p.rules[q].B].csc_ptr;
-        const int e1 = __ldg(cp + rr + 1);
+        const int4 h = __ldg(c.nt[p.rules[q].B].csc_ell + rr);   // CSC_B(r): ELL head first
         const int A = rule_out[q];
-        for (int f2 = __ldg(cp + rr); f2 < e1; ++f2) {
-            const int i = __ldg(c.adj_idx + f2);
+        for (int f2 = 0; f2 < h.y; ++f2) {
+            const int i = f2 == 0 ? h.z : (f2 == 1 ? h.w : __ldg(c.adj_idx + h.x + f2));
             rows_merge(p, c, A, i, (int64_t)en.z, en.w, my_new);
         }
     }
