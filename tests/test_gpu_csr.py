@@ -79,3 +79,35 @@ def test_csr_empty_relation_and_small_capacity():
     with pytest.raises(C.CfpqError) as e:
         r.csr(A, rp, cols)
     assert e.value.status == C.CFPQ_E_INVAL
+
+
+def test_csr_long_rows():
+    """S -> S S | a on a random digraph: rows of up to 288 entries."""
+    w = I.dense_stress_workload(300, 3, seed=3)
+    ores = oracle_run(w)
+    erp, ecols = _expected(w, w.start, ores)
+    assert np.diff(erp).max() > 256
+    # the sparse engine (the hashed set and row shards do not take S -> S S); device destination too
+    import torch
+    r, _, _ = gpu_closure(w, **ENGINES["sparse"])
+    rp, cols = r.csr(w.start)
+    assert np.array_equal(rp, erp) and np.array_equal(cols, ecols)
+    rp_d = torch.empty((w.n_nodes + 1,), dtype=torch.int64, device="cuda")
+    cols_d = torch.empty((len(ecols),), dtype=torch.int32, device="cuda")
+    rp, cols = r.csr(w.start, rp_d, cols_d)
+    assert np.array_equal(rp.cpu().numpy(), erp) and np.array_equal(cols.cpu().numpy(), ecols)
+
+
+def test_csr_large_n_hashed():
+    """n = 2^18 + 3 (row pointers past 2^18, 64-bit sort keys) on the hashed cell set."""
+    n = (1 << 18) + 3
+    g = I.union_grammar()
+    edges = [(0, "subClassOf_r", 5), (5, "subClassOf", n - 1), (n - 1, "subClassOf_r", 7), (7, "subClassOf", n - 2),
+             (n - 2, "type_r", 9), (9, "type", 11)]
+    w = I.bind("large_n_csr", g, n, edges, "S_Q1")
+    ores = oracle_run(w)
+    r, _, _ = gpu_closure(w, cell_set=2)
+    for A in range(w.n_nt):
+        rp, cols = r.csr(A)
+        erp, ecols = _expected(w, A, ores)
+        assert np.array_equal(rp, erp) and np.array_equal(cols, ecols), w.nt_names[A]

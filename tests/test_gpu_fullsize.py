@@ -56,6 +56,10 @@ def _check(gd, w, r, per_iteration=True, iterations=True):
         p = np.ascontiguousarray(r.pairs(A).astype("<i4"))
         assert len(p) == gd["count"][A], (w.nt_names[A], len(p), gd["count"][A])
         assert hashlib.sha256(p.tobytes()).hexdigest() == gd["sha256"][A], w.nt_names[A]
+        # the compressed-row read-back (cfpq_result_csr) expands to the same pairs
+        rp, cols = r.csr(A)
+        q = np.stack([np.repeat(np.arange(w.n_nodes, dtype=np.int32), np.diff(rp)), cols], 1).astype("<i4")
+        assert hashlib.sha256(np.ascontiguousarray(q).tobytes()).hexdigest() == gd["sha256"][A], w.nt_names[A]
 
 
 def _run(n, **kw):
