@@ -268,7 +268,7 @@ struct cfpq_result {
         // config 4: 0.611 vs 0.623 ms per step); flags bit 0 disables (diagnostics)
         p.precheck = (opts.diag_flags & 1) ? 0 : 1;
         p.self_clear = self_clear_ok() ? 1 : 0;
-        p.warp_flush = (opts.diag_flags & 8) ? 1 : 0;
+        p.warp_flush = (opts.diag_flags & 8) ? 0 : 1;   // bit 3: the CTA-level flush (round 1 default)
         p.cta_major = (opts.diag_flags & 256) ? 1 : 0;
         p.no_chain = (opts.diag_flags & (1 << 13)) ? 1 : 0;
         p.row_lo = 0;

@@ -177,7 +177,8 @@ struct EngineParams {
     int32_t precheck;              // read a candidate's word before its atomicOr (hot cells)
     int32_t cta_major;             // diagnostics (diag_flags bit 8): chunk c -> warp c (CTA-major)
     int32_t no_chain;              // diagnostics (diag_flags bit 13): no single-cell chains in warp-solo
-    int32_t warp_flush;            // diagnostics (diag_flags bit 3): each warp appends its own cells
+    int32_t warp_flush;            // each warp appends its own cells at the end of its expansion (default;
+                                   // diag_flags bit 3 = one CTA-level append instead)
                                    // (one log atomic per warp) instead of the CTA-level flush
     int32_t self_clear;            // relational runs: at the fixpoint the kernel resets the words
                                    // of all logged cells in T/S/ST (the results stay in the log)

@@ -32,7 +32,7 @@ variants = {
     "rows_R_2x1row": dict(path_policy=3, flags=2 << 4),
     "rows_R_2x4rows": dict(path_policy=3, flags=3 << 4),
     "rows_R_1x8rows": dict(path_policy=3, flags=4 << 4),
-    "warp_flush": dict(cell_set=1, flags=8),
+    "cta_flush": dict(cell_set=1, flags=8),
     "xr2_peer": dict(emulate_ranks=2, exchange=1),
     "xr8_peer": dict(emulate_ranks=8, exchange=1),
     "shard8_hostloop": dict(emulate_ranks=8),

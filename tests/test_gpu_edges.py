@@ -23,6 +23,7 @@ SIZES = [1, 31, 32, 33, 127, 128, 129, 255, 256, 257, 1025]
 ENGINES = {
     "sparse": (dict(path_policy=1, cell_set=1), True, True),
     "sparse_seed_kernels": (dict(path_policy=1, cell_set=1, flags=512), True, True),
+    "sparse_cta_flush": (dict(path_policy=1, cell_set=1, flags=8), True, True),
     "hashed": (dict(path_policy=1, cell_set=2), True, False),
     "tensor_fp4": (dict(path_policy=2, tensor_format=2), True, True),
     "tensor_int8": (dict(path_policy=2, tensor_format=1), True, True),

@@ -87,6 +87,13 @@ def test_sparse_engine_bit_matrices(n):
 
 
 @pytest.mark.parametrize("n", SIZES)
+def test_sparse_engine_cta_flush(n):
+    """diag_flags bit 3: one CTA-level log append per iteration (round 1's default)."""
+    gd, w, r = _run(n, cell_set=1, flags=8)
+    _check(gd, w, r)
+
+
+@pytest.mark.parametrize("n", SIZES)
 def test_sparse_engine_hashed_cell_set(n):
     gd, w, r = _run(n, cell_set=2)
     assert r.stats()["hashed"] == 1
